@@ -1,0 +1,364 @@
+/*
+ * orc_cfmg.c -- oracle compact FMG.  TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * Follows, step by step and in the paper's order:
+ *   Alg 3.3 cFmg            PAPER.md:766-801 (coarse solve :786, push level
+ *                           :788 with the regressive-precision widening of
+ *                           PAPER.md:493-495/757-760, N IR iterations :791-798)
+ *   Alg 3.2 fmgResidual     PAPER.md:713-748 (decode sweep :733-735, residual
+ *                           :738, truncate :739, restrict t (not r) :742-744)
+ *   Alg 3.1 cFas, nu = 1    PAPER.md:613-653 with y = 0, s = 0:
+ *                           coarse-to-fine sweep :638-643
+ *   correction              PAPER.md:798  u_l <- reg(u_l + y_l)
+ * Precisions (tab:precisions PAPER.md:820-841): sections u, r, y stored in BFP at
+ * w_u(l,L) = b_u + k_u (L-l) and w_r(l,L) = b_r + k_r (L-l); everything else FP64
+ * (reading R9).  Smoother: Chebyshev-Jacobi of degree k from a zero
+ * initial guess (a smoother of the form eq:smoother PAPER.md:521-525; DESIGN.md
+ * reading R4); coarsest level solved exactly (reading R5).
+ *
+ * Parity pins (tests/test_oracle_cfmg.py): Eq 7.3/7.4 success criteria
+ * against the FP64 discretisation solution; L2/H1 error
+ * orders p+1 / p; at width 54 the compact V(0,1) equals a standard CS V(0,1)
+ * (PAPER.md:686-690 block-system remark) to round-off; zero solution gives
+ * r_l = enc(R..R f_L); the exact discrete solution gives residual at
+ * quantisation level; bits/DoF within the paper's 4-12 / 3-6 ranges.
+ * The per-level residual norms at the bench configurations themselves are
+ * "parity unpinned" beyond these properties.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include "oracle.h"
+
+typedef struct {
+  int w;          /* current stored width */
+  int64_t* m;     /* mantissas, one per stored entry */
+  int8_t* E;      /* one exponent per 32-entry block */
+} sec_t;
+
+struct orc_ctx {
+  int d, p, levels, Lmax;
+  orc_schedule s;
+  orc_level g[ORC_MAXLEV];
+  sec_t u[ORC_MAXLEV];    /* compact solution sections ú_l */
+  sec_t r[ORC_MAXLEV];    /* residual sections r_l */
+  sec_t y[ORC_MAXLEV];    /* correction sections ý_l */
+  double* f[ORC_MAXLEV];  /* f_l (only the current FMG level is used) */
+  double* invD[ORC_MAXLEV];
+  double* ut[ORC_MAXLEV]; /* decoded standard representation temporaries u_l */
+  double* tt[ORC_MAXLEV]; /* residual temporaries t_l */
+  double* wt[ORC_MAXLEV]; /* w_l = z_l + dec ý_l */
+  double* Ainv;
+  int n0;
+  double inv_theta, cal[8], cbe[8];
+  double* norms;          /* [Lmax+1][N][Lmax+1] */
+};
+
+static int wu(const orc_ctx* c, int l, int L) { return c->s.b_u + c->s.k_u * (L - l); }
+static int wr(const orc_ctx* c, int l, int L) { return c->s.b_r + c->s.k_r * (L - l); }
+
+static int sec_alloc(sec_t* s, const orc_level* g) {
+  s->m = calloc(g->size, sizeof(int64_t));
+  s->E = malloc(g->nblk);
+  if (!s->m || !s->E) return ORC_ENOMEM;
+  memset(s->E, 0x80, g->nblk); /* -128: zero blocks */
+  s->w = 2;
+  return ORC_OK;
+}
+
+static void sec_zero(sec_t* s, const orc_level* g, int w) {
+  memset(s->m, 0, sizeof(int64_t) * g->size);
+  memset(s->E, 0x80, g->nblk);
+  s->w = w;
+}
+
+/* x = dec(section) (mantissa scaled by the block exponent) */
+static void sec_decode(const sec_t* s, const orc_level* g, double* x) {
+  for (int64_t b = 0; b < g->nblk; ++b)
+    for (int j = 0; j < 32; ++j)
+      x[32 * b + j] = orc_block_decode_one(s->m[32 * b + j], s->E[b], s->w);
+}
+
+/* section = enc_w(x): RNE per block (reading R8) */
+static int sec_encode(sec_t* s, const orc_level* g, const double* x, int w) {
+  s->w = w;
+  for (int64_t b = 0; b < g->nblk; ++b) {
+    int E;
+    int rc = orc_block_encode(x + 32 * b, w, s->m + 32 * b, &E);
+    if (rc) return rc;
+    s->E[b] = (int8_t)E;
+  }
+  return ORC_OK;
+}
+
+void orc_destroy(orc_ctx* c) {
+  if (!c) return;
+  for (int l = 0; l <= c->Lmax; ++l) {
+    free(c->u[l].m); free(c->u[l].E);
+    free(c->r[l].m); free(c->r[l].E);
+    free(c->y[l].m); free(c->y[l].E);
+    free(c->f[l]); free(c->invD[l]); free(c->ut[l]); free(c->tt[l]); free(c->wt[l]);
+  }
+  free(c->Ainv);
+  free(c->norms);
+  free(c);
+}
+
+int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out) {
+  *out = NULL;
+  if ((d != 2 && d != 3) || p < 1 || p > 3 || levels < 1 || levels > ORC_MAXLEV) return ORC_EINVAL;
+  if (s->b_u < 2 || s->b_r < 2 || s->n_ir < 1 || s->cheb_degree < 1 || s->cheb_degree > 8) return ORC_EINVAL;
+  int Lmax = levels - 1;
+  if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return ORC_EINVAL;
+  orc_ctx* c = calloc(1, sizeof(orc_ctx));
+  if (!c) return ORC_ENOMEM;
+  c->d = d; c->p = p; c->levels = levels; c->Lmax = Lmax; c->s = *s;
+  for (int l = 0; l <= Lmax; ++l) {
+    orc_level_geom(d, p, l, &c->g[l]);
+    const orc_level* g = &c->g[l];
+    if (sec_alloc(&c->u[l], g) || sec_alloc(&c->r[l], g) || sec_alloc(&c->y[l], g)) {
+      orc_destroy(c);
+      return ORC_ENOMEM;
+    }
+    c->f[l] = malloc(sizeof(double) * g->size);
+    c->invD[l] = malloc(sizeof(double) * g->size);
+    c->ut[l] = calloc(g->size, sizeof(double));
+    c->tt[l] = calloc(g->size, sizeof(double));
+    c->wt[l] = calloc(g->size, sizeof(double));
+    if (!c->f[l] || !c->invD[l] || !c->ut[l] || !c->tt[l] || !c->wt[l]) {
+      orc_destroy(c);
+      return ORC_ENOMEM;
+    }
+    orc_rhs(d, p, l, c->f[l]);
+    orc_inv_diag(d, p, l, c->invD[l]);
+  }
+  c->n0 = orc_coarse_n(d, p);
+  c->Ainv = malloc(sizeof(double) * c->n0 * c->n0);
+  if (orc_coarse_inverse(d, p, c->Ainv)) { orc_destroy(c); return ORC_EINVAL; }
+  orc_cheb_coefs(s, &c->inv_theta, c->cal, c->cbe);
+  c->norms = calloc((size_t)(Lmax + 1) * s->n_ir * (Lmax + 1), sizeof(double));
+  *out = c;
+  return ORC_OK;
+}
+
+/* y = A_0^{-1} x on level 0 (full stored layout in and out); canonical mat-vec
+ * acc = 0; acc = fma(Ainv[I][J], x_J, acc) over J in unknown order. */
+static void coarse_solve(const orc_ctx* c, const double* x, double* y) {
+  const orc_level* g = &c->g[0];
+  int m = 2 * c->p - 1, n0 = c->n0;
+  double xv[125];
+  for (int J = 0; J < n0; ++J) {
+    int jx = J % m + 1, jy = (J / m) % m + 1, jz = (c->d == 3) ? J / (m * m) + 1 : 0;
+    xv[J] = x[((int64_t)jz * g->NY + jy) * g->NX + jx];
+  }
+  memset(y, 0, sizeof(double) * g->size);
+  for (int I = 0; I < n0; ++I) {
+    double acc = 0.0;
+    for (int J = 0; J < n0; ++J) acc = fma(c->Ainv[I * n0 + J], xv[J], acc);
+    int ix = I % m + 1, iy = (I / m) % m + 1, iz = (c->d == 3) ? I / (m * m) + 1 : 0;
+    y[((int64_t)iz * g->NY + iy) * g->NX + ix] = acc;
+  }
+}
+
+/* Alg 3.2 fmgResidual at FMG level L; norms[l] = ||t_l||_2. */
+int orc_residual(orc_ctx* c, int L, double* norms) {
+  int d = c->d, p = c->p;
+  /* decode sweep PAPER.md:733-735: u_0 = ú_0; u_l = ú_l + P_l u_{l-1} */
+  sec_decode(&c->u[0], &c->g[0], c->ut[0]);
+  for (int l = 1; l <= L; ++l) {
+    const orc_level* g = &c->g[l];
+    double* pu = malloc(sizeof(double) * g->size);
+    orc_prolong(d, p, l, c->ut[l - 1], pu);
+    sec_decode(&c->u[l], g, c->ut[l]);
+    for (int64_t i = 0; i < g->size; ++i) c->ut[l][i] = c->ut[l][i] + pu[i];
+    free(pu);
+  }
+  /* residual PAPER.md:738: t_L = f_L - A_L u_L */
+  {
+    const orc_level* g = &c->g[L];
+    double* au = malloc(sizeof(double) * g->size);
+    orc_apply_A(d, p, L, c->ut[L], au);
+    for (int64_t i = 0; i < g->size; ++i) c->tt[L][i] = c->f[L][i] - au[i];
+    free(au);
+  }
+  /* truncate PAPER.md:739 */
+  int rc = sec_encode(&c->r[L], &c->g[L], c->tt[L], wr(c, L, L));
+  if (rc) return rc;
+  /* restriction sweep PAPER.md:742-744 (restricts t, not r; R11) */
+  for (int l = L - 1; l >= 0; --l) {
+    orc_restrict(d, p, l + 1, c->tt[l + 1], c->tt[l]);
+    rc = sec_encode(&c->r[l], &c->g[l], c->tt[l], wr(c, l, L));
+    if (rc) return rc;
+  }
+  if (norms)
+    for (int l = 0; l <= L; ++l) {
+      double s = 0.0;
+      for (int64_t i = 0; i < c->g[l].size; ++i) s += c->tt[l][i] * c->tt[l][i];
+      norms[l] = sqrt(s);
+    }
+  return ORC_OK;
+}
+
+/* Chebyshev-Jacobi of degree k from y = 0 on A_l y = b:
+ *   d = inv_theta (invD b); y = d;
+ *   j = 2..k: q = b - A y; d = fma(alpha_j, d, beta_j (invD q)); y = y + d. */
+static void chebyshev(const orc_ctx* c, int l, const double* b, double* y) {
+  const orc_level* g = &c->g[l];
+  const double* iD = c->invD[l];
+  double* dv = malloc(sizeof(double) * g->size);
+  double* ay = malloc(sizeof(double) * g->size);
+  for (int64_t i = 0; i < g->size; ++i) {
+    dv[i] = c->inv_theta * (iD[i] * b[i]);
+    y[i] = dv[i];
+  }
+  for (int j = 2; j <= c->s.cheb_degree; ++j) {
+    orc_apply_A(c->d, c->p, l, y, ay);
+    for (int64_t i = 0; i < g->size; ++i) {
+      double q = b[i] - ay[i];
+      dv[i] = fma(c->cal[j - 1], dv[i], c->cbe[j - 1] * (iD[i] * q));
+      y[i] = y[i] + dv[i];
+    }
+  }
+  free(dv); free(ay);
+}
+
+/* Alg 3.1 cFas (nu = 1: y = 0, s = 0) followed by the correction PAPER.md:798. */
+int orc_cfas_correct(orc_ctx* c, int L) {
+  int d = c->d, p = c->p, rc;
+  /* coarse level PAPER.md:640: y_0 = fix(M_0 r_0), M_0 = A_0^{-1} (reading R5) */
+  {
+    const orc_level* g = &c->g[0];
+    double* r0 = malloc(sizeof(double) * g->size);
+    double* y0 = malloc(sizeof(double) * g->size);
+    sec_decode(&c->r[0], g, r0);
+    coarse_solve(c, r0, y0);
+    rc = sec_encode(&c->y[0], g, y0, wr(c, 0, L));
+    free(r0); free(y0);
+    if (rc) return rc;
+    sec_decode(&c->y[0], g, c->wt[0]);   /* w_0 = z_0 + ý_0, z_0 = 0 */
+  }
+  /* coarse-to-fine sweep PAPER.md:641-643 */
+  for (int l = 1; l <= L; ++l) {
+    const orc_level* g = &c->g[l];
+    int64_t N = g->size;
+    double* z = malloc(sizeof(double) * N);
+    double* az = malloc(sizeof(double) * N);
+    double* rb = malloc(sizeof(double) * N);
+    double* yv = malloc(sizeof(double) * N);
+    orc_prolong(d, p, l, c->wt[l - 1], z);          /* z_l = P_l (ý_{l-1} + z_{l-1}) */
+    orc_apply_A(d, p, l, z, az);
+    sec_decode(&c->r[l], g, rb);
+    for (int64_t i = 0; i < N; ++i) rb[i] = rb[i] - az[i];  /* b = r_l - A_l z_l */
+    chebyshev(c, l, rb, yv);                         /* smooth from ý_l = 0 */
+    rc = sec_encode(&c->y[l], g, yv, wr(c, l, L));   /* fix: store at w_r(l,L) */
+    if (!rc) {
+      sec_decode(&c->y[l], g, yv);
+      for (int64_t i = 0; i < N; ++i) c->wt[l][i] = z[i] + yv[i];
+    }
+    free(z); free(az); free(rb); free(yv);
+    if (rc) return rc;
+  }
+  /* correction PAPER.md:798: ú_l <- reg(ú_l + ý_l) at w_u(l, L) */
+  for (int l = 0; l <= L; ++l) {
+    const orc_level* g = &c->g[l];
+    double* a = malloc(sizeof(double) * g->size);
+    double* b = malloc(sizeof(double) * g->size);
+    sec_decode(&c->u[l], g, a);
+    sec_decode(&c->y[l], g, b);
+    for (int64_t i = 0; i < g->size; ++i) a[i] = a[i] + b[i];
+    rc = sec_encode(&c->u[l], g, a, wu(c, l, L));
+    free(a); free(b);
+    if (rc) return rc;
+  }
+  return ORC_OK;
+}
+
+/* Alg 3.3, stopping after `iters_last` IR iterations of FMG level Lstop. */
+int orc_solve_upto(orc_ctx* c, int Lstop, int iters_last) {
+  int rc;
+  if (Lstop < 0 || Lstop > c->Lmax) return ORC_EINVAL;
+  for (int l = 0; l <= c->Lmax; ++l) {
+    sec_zero(&c->u[l], &c->g[l], 2);
+    sec_zero(&c->r[l], &c->g[l], 2);
+    sec_zero(&c->y[l], &c->g[l], 2);
+  }
+  memset(c->norms, 0, sizeof(double) * (c->Lmax + 1) * c->s.n_ir * (c->Lmax + 1));
+  /* coarse-grid solve PAPER.md:785-786: ú_0 = reg(A_0^{-1} f_0) */
+  {
+    const orc_level* g = &c->g[0];
+    double* y0 = malloc(sizeof(double) * g->size);
+    coarse_solve(c, c->f[0], y0);
+    rc = sec_encode(&c->u[0], g, y0, wu(c, 0, 0));
+    free(y0);
+    if (rc) return rc;
+  }
+  for (int L = 1; L <= Lstop; ++L) {
+    /* push level PAPER.md:788: ú_L = 0; the widening of ú_{0..L-1} by k_u bits is
+     * exact (m <- m 2^k_u with the same exponent), so sections keep
+     * their mantissas until the next correction re-encodes them at w_u(l, L). */
+    sec_zero(&c->u[L], &c->g[L], wu(c, L, L));
+    for (int l = 0; l < L; ++l) {
+      const orc_level* g = &c->g[l];
+      int k = c->s.k_u;
+      for (int64_t i = 0; i < g->size; ++i) c->u[l].m[i] = c->u[l].m[i] * ((int64_t)1 << k);
+      c->u[l].w += k;
+    }
+    int iters = (L == Lstop) ? iters_last : c->s.n_ir;
+    for (int it = 0; it < iters; ++it) {
+      double* nrm = c->norms + ((size_t)L * c->s.n_ir + it) * (c->Lmax + 1);
+      rc = orc_residual(c, L, nrm);
+      if (rc) return rc;
+      rc = orc_cfas_correct(c, L);
+      if (rc) return rc;
+    }
+  }
+  return ORC_OK;
+}
+
+int orc_solve(orc_ctx* c) { return orc_solve_upto(c, c->Lmax, c->s.n_ir); }
+
+const double* orc_norms(orc_ctx* c) { return c->norms; }
+int orc_lmax(orc_ctx* c) { return c->Lmax; }
+
+/* which: 0 = ú, 1 = r, 2 = ý.  Packs into the S1 layout. */
+int orc_get_section(orc_ctx* c, int which, int l, uint32_t* mant, int8_t* exps, int* width) {
+  if (l < 0 || l > c->Lmax || which < 0 || which > 2) return ORC_EINVAL;
+  sec_t* s = which == 0 ? &c->u[l] : which == 1 ? &c->r[l] : &c->y[l];
+  const orc_level* g = &c->g[l];
+  *width = s->w;
+  if (mant)
+    for (int64_t b = 0; b < g->nblk; ++b) orc_pack_block(s->m + 32 * b, s->w, mant + b * s->w);
+  if (exps) memcpy(exps, s->E, g->nblk);
+  return ORC_OK;
+}
+
+/* Test hook: section := enc_width(x). */
+int orc_set_section(orc_ctx* c, int which, int l, const double* x, int width) {
+  if (l < 0 || l > c->Lmax || which < 0 || which > 2) return ORC_EINVAL;
+  sec_t* s = which == 0 ? &c->u[l] : which == 1 ? &c->r[l] : &c->y[l];
+  return sec_encode(s, &c->g[l], x, width);
+}
+
+/* which: 0 = u_l (decoded, from the last residual), 1 = t_l, 2 = w_l. */
+int orc_get_array(orc_ctx* c, int which, int l, double* dst) {
+  if (l < 0 || l > c->Lmax) return ORC_EINVAL;
+  const double* s = which == 0 ? c->ut[l] : which == 1 ? c->tt[l] : c->wt[l];
+  memcpy(dst, s, sizeof(double) * c->g[l].size);
+  return ORC_OK;
+}
+
+/* û_L = ú_L + P_L(ú_{L-1} + ... ) (eq:compact-to-standard PAPER.md:186). */
+int orc_decode_solution(orc_ctx* c, int L, double* uhat) {
+  if (L < 0 || L > c->Lmax) return ORC_EINVAL;
+  sec_decode(&c->u[0], &c->g[0], c->ut[0]);
+  for (int l = 1; l <= L; ++l) {
+    const orc_level* g = &c->g[l];
+    double* pu = malloc(sizeof(double) * g->size);
+    orc_prolong(c->d, c->p, l, c->ut[l - 1], pu);
+    sec_decode(&c->u[l], g, c->ut[l]);
+    for (int64_t i = 0; i < g->size; ++i) c->ut[l][i] = c->ut[l][i] + pu[i];
+    free(pu);
+  }
+  memcpy(uhat, c->ut[L], sizeof(double) * c->g[L].size);
+  return ORC_OK;
+}
