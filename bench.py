@@ -1,0 +1,336 @@
+"""bench.py -- compact-FMG solve throughput on B200 (BASELINE.json metric).
+
+One step = one full compact FMG solve (Alg 3.3, all FMG levels, N IR
+iterations each: every §8(a) row S1-S11) of the configured workload, issued
+through the C-ABI (fmg_solve_async) with the context resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+Default workload: configs[1] = C2 (2D Q2, 1024^2 elements, 10-level FMG).
+Multi-GPU: 2D configs do not shard (replicas only), so each rank
+solves its own instance; value = total unknowns solved per second (weak).
+--impl reference: the CPU oracle (oracle/, plain sequential C) on the same
+config, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from fmg_inputs import CONFIGS, default_schedule, unknowns  # noqa: E402
+
+METRIC = "FMG solve DoF/s and effective HBM GB/s vs 8 TB/s roofline at 1/2/4/8 B200"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_TFLOPS = 37.2  # 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz; measured 34.0
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6536.7), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """Samples SM clock and throttle reasons through NVML every 5 ms during the
+    timed region (nvidia-smi's 200 ms period is longer than a C2 step)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.th = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def loop():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+
+            self.th = threading.Thread(target=loop, daemon=True)
+            self.th.start()
+        except Exception:
+            self.th = None
+
+    def stop(self):
+        self.stop_ev.set()
+        if self.th:
+            self.th.join(timeout=1)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        reasons = set()
+        for _, rs in self.samples:
+            for nm, bit in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def kernel_model(cfg, sched, cls):
+    """Algorithmic FP64 flops and bytes per launch of a fine-level kernel class
+    (DESIGN.md §7): per stored point of the finest level."""
+    d, p, levels = cfg["dim"], cfg["p"], cfg["levels"]
+    n = p << levels
+    NX = (n + 31) // 32 * 32
+    pts = NX * n * (n if d == 3 else 1)
+    t = 2 * p + 1
+    a_flops = (8 * t + 1) if d == 2 else (14 * t + 2)   # canonical A tree, FMA = 2 flops
+    wr_b = sched["b_r"] / 8 + 1 / 32
+    wu_b = sched["b_u"] / 8 + 1 / 32
+    if cls == 0:   # residual: read u_L (FP64), write t_L (FP64) + r_L
+        flops = a_flops + (d - 1) + 1 + 2
+        byts = 8 + 8 + wr_b
+    else:          # cFas smoothing steps, averaged over the k launches
+        k = sched["cheb_degree"]
+        f1 = a_flops + 1 + 3
+        b1 = 8 + wr_b + (24 if k > 1 else 0)
+        fl = [f1] + [a_flops + 6] * (k - 1)
+        bl = [b1] + [8 * 4 + 16] * (k - 1)
+        # last step: ú read + write, W write, Z read
+        bl[-1] += 2 * wu_b + 8 + 8
+        flops = sum(fl) / k
+        byts = sum(bl) / k
+    return flops * pts, byts * pts
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2511_19036_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = CONFIGS[args.config]
+    sched = default_schedule(cfg["dim"], cfg["p"])
+    P.use_torch_allocator(True)
+    stream = torch.cuda.current_stream()
+    solver = P.Solver(cfg["dim"], cfg["p"], cfg["levels"], sched, stream=stream)
+    solver.enable_kernel_timing(args.roofline_class)
+    info_unk = unknowns(cfg["dim"], cfg["p"], cfg["levels"])
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    for _ in range(args.warmup):
+        solver.solve_async()
+    torch.cuda.synchronize()
+    solver.solve()  # error check (FMG_ERANGE) once before timing
+    info = solver.info()
+
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+    clocks = Clocks(local_rank)
+    clocks.start()
+    times, ktimes, klaunch = [], 0.0, 0
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        solver.solve_async()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        kt, kn = solver.kernel_time()
+        ktimes += kt
+        klaunch += kn
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    ck = clocks.stop()
+    ms = sum(times) / len(times)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end to end through the C-ABI with host buffers --------------------
+    rhs_host = torch.from_numpy(solver.get_rhs()).pin_memory()
+    exp_host = torch.empty(solver.export_size(), dtype=torch.uint8).pin_memory()
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        solver.set_rhs(rhs_host)            # H2D: the separable RHS tables
+        solver.solve_async()
+        solver.export_solution(exp_host)    # D2H: every compact solution section
+        stream.synchronize()
+        e2e_times.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = sum(e2e_times) / len(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        return
+    hbm, hbm_src = peaks()
+    flops, byts = kernel_model(cfg, sched, args.roofline_class)
+    avg_launch_ms = ktimes / max(klaunch, 1)
+    t_hbm = byts / (hbm * 1e9)
+    t_alu = flops / (FP64_PEAK_TFLOPS * 1e12)
+    if t_alu >= t_hbm:
+        roof = {"bound": "alu", "achieved": flops / (avg_launch_ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "peak_source": "derived FP64 (DESIGN.md §7); measured 34.0"}
+    else:
+        roof = {"bound": "hbm", "achieved": byts / (avg_launch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "peak_source": hbm_src}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = args.traffic
+    roof["kernel"] = ["k_residual (fine level)", "k_cfas_step (fine level)"][args.roofline_class]
+    roof["avg_launch_ms"] = avg_launch_ms
+    roof["launches_timed"] = klaunch
+    roof["alg_flops_per_launch"] = flops
+    roof["alg_bytes_per_launch"] = byts
+
+    eff_gbs = info["alg_bytes_per_solve"] / (ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC,
+        "value": info_unk * world / (ms * 1e-3),
+        "unit": "DoF/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (manufactured solution u = prod sin(pi x_k); no dataset)",
+        "config": {"workload": args.config + ": " + cfg["desc"], "dim": cfg["dim"], "p": cfg["p"],
+                   "levels": cfg["levels"], "unknowns": info_unk,
+                   "schedule": sched, "l2": "flushed (256 MB write) before every timed step",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "effective_hbm_gbs": eff_gbs,
+        "hbm_roofline_frac_nominal_8tbs": eff_gbs / 8000.0,
+        "hbm_roofline_frac_measured": eff_gbs / hbm,
+        "alg_bytes_per_solve": info["alg_bytes_per_solve"],
+        "roofline": roof,
+        "e2e": {"value": info_unk * world / (e2e_ms * 1e-3), "unit": "DoF/s",
+                "h2d_bytes_per_step": rhs_host.numel() * 8, "d2h_bytes_per_step": exp_host.numel(),
+                "ms_per_step": e2e_ms},
+        "gpu_launches": int(info["launches_per_solve"]) * args.steps,
+        "clocks": ck,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.config)
+    print(json.dumps(out))
+
+
+def cpu_baseline(config):
+    import oracle as O
+    cfg = CONFIGS[config]
+    d, p, lev = cfg["dim"], cfg["p"], cfg["levels"]
+    # bounded sample: the full solve when it fits ~30 s, else the same solver
+    # on fewer levels (same d, p, schedule)
+    sample_lev = lev
+    while sample_lev > 2 and (p << sample_lev) ** d > 5_000_000:
+        sample_lev -= 1
+    s = O.schedule(d, p)
+    c = O.CFMG(d, p, sample_lev, s)
+    t0 = time.perf_counter()
+    c.solve()
+    dt = time.perf_counter() - t0
+    unk = unknowns(d, p, sample_lev)
+    return {"value": unk / dt, "unit": "DoF/s", "cores": 1, "kind": "oracle",
+            "sample": f"one full compact FMG solve, {d}D Q{p}, {sample_lev} levels ({unk} unknowns), "
+                      f"{dt:.2f} s single-threaded"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle as O
+    cfg = CONFIGS[args.config]
+    d, p, lev = cfg["dim"], cfg["p"], cfg["levels"]
+    sample_lev = lev
+    while sample_lev > 2 and (p << sample_lev) ** d > 5_000_000:
+        sample_lev -= 1
+    s = O.schedule(d, p)
+    c = O.CFMG(d, p, sample_lev, s)
+    for _ in range(args.warmup):
+        c.solve()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        c.solve()
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(ts) / len(ts)
+    unk = unknowns(d, p, sample_lev)
+    v = unk / (ms * 1e-3)
+    out = {
+        "impl": "reference",
+        "metric": METRIC, "value": v, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (manufactured solution)",
+        "config": {"workload": args.config + ": " + cfg["desc"], "dim": d, "p": p, "levels": lev,
+                   "sample_levels": sample_lev},
+        "cpu_baseline": {"value": v, "unit": "DoF/s", "cores": 1, "kind": "oracle",
+                         "sample": f"each step one full oracle solve with {sample_lev} levels"},
+        "e2e": {"value": v, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--roofline-class", type=int, default=1, choices=[0, 1])
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the roofline kernel (profiles/)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * fmg.h -- C-ABI of libfmg.so: the B200 compact full multigrid hot path of
+ * arXiv 2511.19036 ("compact FMG": solution, residual and correction stored as
+ * multilevel compact sections in block floating point at regressive widths).
+ *
+ * Problem (eq:pde-poisson PAPER.md:1418-1424):
+ *   -Δu = f on (0,1)^dim, u = 0 on the boundary, Lagrange Q_p elements on the
+ *   uniform dyadic hierarchy; level l has element size h_l = 2^-(l+1) and
+ *   n_l = p 2^(l+1) nodes per dimension excluding the far boundary; f is the
+ *   load vector of the manufactured solution u = prod_k sin(pi x_k).
+ *
+ * Storage layout of a level: x fastest, stored extent
+ *   NX = roundup(n_l, 32), NY = n_l, NZ = n_l (3D) or 1 (2D); node index 0 is the
+ *   (zero) boundary; entries at non-unknowns (index 0, x >= n_l) are 0.
+ *
+ * BFP format (rounding PAPER.md:846, R8):
+ *   blocks of 32 consecutive x entries; one int8 exponent E per block;
+ *   w-bit two's-complement mantissas (sign bit included),
+ *   value = m 2^(E-(w-1)); entry j of a block occupies bits [j w, j w + w) of
+ *   the block's bit stream, stream bit k = bit (k mod 32) of word k/32, so a
+ *   block is exactly w uint32 words.  E = -128 marks an all-zero block.
+ *   Encode: q = w-1, E0 = ilogb(max|x|)+1, E = E0+1 if RNE(max|x| 2^(q-E0)) = 2^q
+ *   else E0, E < -127 saturates to -127, E > 127 -> FMG_ERANGE; m = RNE(x 2^(q-E)).
+ *
+ * Threading / streams: every call is issued on the context's stream (or the
+ * `stream` argument); calls documented "synchronous" wait for completion.
+ * All pointers are owned by the caller unless stated otherwise.
+ * Errors: every function returns FMG_OK (0) or one of the codes below.
+ */
+#ifndef FMG_H
+#define FMG_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMG_OK 0
+#define FMG_EINVAL 1  /* bad argument (dim, p, levels, width outside [2,54], n % 32) */
+#define FMG_ERANGE 2  /* BFP exponent > 127 or non-finite value met by an encode */
+#define FMG_ENOMEM 3  /* device allocation failed */
+#define FMG_ECUDA 4   /* CUDA runtime error */
+#define FMG_ESTATE 5  /* call out of order (e.g. residual before any solve) */
+
+/* Bit-width schedule (tab:precisions PAPER.md:820-841).
+ *   w_u(l,L) = b_u + k_u (L-l)   solution sections  (b1 of Table 3, k_u = p+1)
+ *   w_r(l,L) = b_r + k_r (L-l)   residual / correction sections (b2, k_r = m = 1)
+ * n_ir: IR iterations N per FMG level (Alg 3.3).
+ * cheb_degree, lambda_hi, alpha: Chebyshev-Jacobi smoother of degree k on
+ * [lambda_hi/alpha, lambda_hi] for D^-1 A (reading R4). */
+typedef struct {
+  int b_u, k_u;
+  int b_r, k_r;
+  int n_ir;
+  int cheb_degree;
+  double lambda_hi;
+  double alpha;
+} fmg_schedule;
+
+typedef struct fmg_ctx fmg_ctx;
+
+/* Device allocator hook (e.g. torch's caching allocator).  alloc returns a
+ * device pointer of at least `bytes` or NULL; free releases it.  Applies to
+ * contexts created afterwards.  Pass NULLs to restore cudaMalloc/cudaFree. */
+typedef void* (*fmg_alloc_fn)(size_t bytes, void* user);
+typedef void (*fmg_free_fn)(void* ptr, size_t bytes, void* user);
+int fmg_set_allocator(fmg_alloc_fn alloc, fmg_free_fn free_fn, void* user);
+
+/* Create a solver context on the current CUDA device.
+ *   dim in {2,3}; p in {1,2,3}; levels >= 1 (solver levels 0..levels-1, finest
+ *   element size 2^-levels; reading R3); s: schedule (copied);
+ *   stream: cudaStream_t the context runs on (NULL = legacy default stream).
+ * Allocates every section and workspace (owned by the context) and uploads the
+ * operator / RHS tables.  Errors: FMG_EINVAL (any width w_u(0,L), w_r(0,L) > 54
+ * or < 2, bad dim/p/levels/schedule), FMG_ENOMEM, FMG_ECUDA. */
+int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, fmg_ctx** out);
+
+/* Alg 3.3 from scratch: coarse solve, then for L = 1..levels-1
+ * push a level and run N x {fmgResidual, cFas V(0,1), correction}.  Enqueues one
+ * CUDA graph on the context stream and returns without waiting (asynchronous).
+ * Deterministic: repeated solves are bit-identical. */
+int fmg_solve_async(fmg_ctx* c);
+
+/* fmg_solve_async + wait + device error check (synchronous).
+ * Errors: FMG_ERANGE if any encode saw a non-finite value or exponent > 127. */
+int fmg_solve(fmg_ctx* c);
+
+/* Partial solve for parity tests: stops after `iters_last` IR iterations of FMG
+ * level Lstop (0 <= Lstop < levels).  Synchronous. */
+int fmg_solve_upto(fmg_ctx* c, int Lstop, int iters_last);
+
+/* Norm log of the last solve: norms[(L*n_ir + it)*levels + l] = ||t_l||_2 after
+ * the residual of IR iteration `it` at FMG level L (entries l > L are 0).
+ * `host` holds levels*n_ir*levels doubles.  Synchronous. */
+int fmg_norms(fmg_ctx* c, double* host);
+
+/* Alg 3.2 fmgResidual on the current compact solution at the
+ * finest FMG level reached; leaves r_l sections on the device and writes
+ * ||t_l||_2, l = 0..L, to `host_norms` (levels doubles, l > L zero).
+ * FMG_ESTATE before any solve.  Synchronous. */
+int fmg_residual(fmg_ctx* c, double* host_norms);
+
+/* Decoded standard representation û_L (eq:compact-to-standard PAPER.md:186) of
+ * the finest FMG level reached, written to the caller's device buffer `dst`
+ * in the stored layout of level L (NX*NY*NZ doubles).  Synchronous. */
+int fmg_get_solution(fmg_ctx* c, double* dst_dev);
+
+/* Relative L2, H1-semi and H1 errors of û_L against u = prod sin(pi x_k)
+ * (tensor Gauss-Legendre, p+3 points per dim per element; R13).
+ * err3: host, 3 doubles.  Synchronous. */
+int fmg_errors(fmg_ctx* c, double* err3);
+
+/* Copy a compact section to the host in the dense BFP layout above.
+ *   which: 0 = solution ú_l, 1 = residual r_l.  mant: nblk*width words (may be
+ *   NULL to query width), exps: nblk bytes (may be NULL), width: out.  Synchronous. */
+int fmg_get_section(fmg_ctx* c, int which, int level, uint32_t* mant, int8_t* exps, int* width);
+
+/* Geometry / accounting of the context.  info[0..9] = dim, p, levels, NX, NY, NZ
+ * of the finest level, unknowns of the finest level, stored section bits of the
+ * finest FMG level (mantissas + exponents, u and r), algorithmic bytes of one
+ * full solve, number of kernel launches per solve. */
+int fmg_info(fmg_ctx* c, double* info10);
+
+/* Kernel-time instrumentation for bench.py: when enabled before the first
+ * solve, the captured graph brackets every launch of kernel class `cls`
+ * (0 = fine residual, 1 = fine cFas smoothing step, 2 = prolong/decode,
+ * 3 = restriction) with CUDA events; fmg_kernel_time returns the summed device
+ * time (ms) and launch count of the last solve (synchronous). */
+int fmg_enable_kernel_timing(fmg_ctx* c, int cls);
+int fmg_kernel_time(fmg_ctx* c, double* total_ms, int* launches);
+
+/* Separable right-hand side f_l(i,j,k) = ((C g_l(i)) g_l(j)) g_l(k):
+ * the 1D factor tables of every level, concatenated level by level
+ * (sum_l n_l doubles, n_l = p 2^(l+1)).  fmg_create fills them with the load
+ * integrals of the manufactured RHS; fmg_set_rhs uploads caller tables from
+ * HOST memory (asynchronous on the context stream; pinned memory recommended)
+ * and fmg_get_rhs copies them back (synchronous).  fmg_rhs_size returns the
+ * table length. */
+int64_t fmg_rhs_size(fmg_ctx* c);
+int fmg_set_rhs(fmg_ctx* c, const double* host_tables);
+int fmg_get_rhs(fmg_ctx* c, double* host_tables);
+
+/* Export the compact solution ú_0..ú_L (device storage layout: per level l,
+ * nblk_l * stride_l uint32 words -- block b at word b*stride_l, stride_l =
+ * w_u(l, levels-1) -- followed by nblk_l exponent bytes) into `host` (pinned
+ * host memory recommended; asynchronous on the context stream).  Returns the
+ * number of bytes needed (host == NULL or cap too small copies nothing), or a
+ * negative FMG error code. */
+int64_t fmg_export_solution(fmg_ctx* c, void* host, int64_t cap);
+
+void fmg_destroy(fmg_ctx* c);          /* idempotent on NULL */
+const char* fmg_strerror(int code);
+
+/* Standalone BFP codec (K1).  x, mant, exps are DEVICE pointers
+ * (caller-owned); n is a multiple of 32; width in [2,54]; asynchronous on
+ * `stream` (cudaStream_t, NULL = default).  bfp_encode reports FMG_ERANGE
+ * through the next synchronous call of bfp_status. */
+int bfp_encode(const double* x, int64_t n, int width, uint32_t* mant, int8_t* exps, void* stream);
+int bfp_decode(const uint32_t* mant, const int8_t* exps, int64_t n, int width, double* x, void* stream);
+/* Returns and clears the sticky codec error status (synchronises `stream`). */
+int bfp_status(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,264 @@
+"""Thin Python binding of libfmg.so (include/fmg.h) -- the B200 compact-FMG hot
+path of arXiv 2511.19036.
+
+Argument marshalling only: every step of the method runs in the CUDA kernels
+of ``csrc/``.  PyTorch provides device memory (through the allocator hook),
+streams and tensors.  There is no CPU fallback: importing this package raises
+if the extension has not been built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libfmg.so")
+
+if not os.path.exists(_SO):
+    raise ImportError(f"libfmg.so not built ({_SO}); run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+_lib = C.CDLL(_SO)
+
+FMG_OK, FMG_EINVAL, FMG_ERANGE, FMG_ENOMEM, FMG_ECUDA, FMG_ESTATE = range(6)
+
+
+class FmgError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {_lib.fmg_strerror(code).decode()} (code {code})")
+        self.code = code
+
+
+class Schedule(C.Structure):
+    """fmg_schedule (include/fmg.h)."""
+
+    _fields_ = [("b_u", C.c_int), ("k_u", C.c_int), ("b_r", C.c_int), ("k_r", C.c_int),
+                ("n_ir", C.c_int), ("cheb_degree", C.c_int),
+                ("lambda_hi", C.c_double), ("alpha", C.c_double)]
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "Schedule":
+        return cls(d["b_u"], d["k_u"], d["b_r"], d["k_r"], d["n_ir"], d["cheb_degree"],
+                   d["lambda_hi"], d["alpha"])
+
+
+_vp = C.c_void_p
+_dp = C.POINTER(C.c_double)
+_lib.fmg_strerror.restype = C.c_char_p
+_lib.fmg_strerror.argtypes = [C.c_int]
+_lib.fmg_create.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule), _vp, C.POINTER(_vp)]
+_lib.fmg_solve.argtypes = [_vp]
+_lib.fmg_solve_async.argtypes = [_vp]
+_lib.fmg_solve_upto.argtypes = [_vp, C.c_int, C.c_int]
+_lib.fmg_norms.argtypes = [_vp, _dp]
+_lib.fmg_residual.argtypes = [_vp, _dp]
+_lib.fmg_get_solution.argtypes = [_vp, _vp]
+_lib.fmg_errors.argtypes = [_vp, _dp]
+_lib.fmg_get_section.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, C.POINTER(C.c_int)]
+_lib.fmg_info.argtypes = [_vp, _dp]
+_lib.fmg_enable_kernel_timing.argtypes = [_vp, C.c_int]
+_lib.fmg_kernel_time.argtypes = [_vp, _dp, C.POINTER(C.c_int)]
+_lib.fmg_destroy.argtypes = [_vp]
+_lib.fmg_destroy.restype = None
+_lib.fmg_rhs_size.argtypes = [_vp]
+_lib.fmg_rhs_size.restype = C.c_int64
+_lib.fmg_set_rhs.argtypes = [_vp, _vp]
+_lib.fmg_export_solution.argtypes = [_vp, _vp, C.c_int64]
+_lib.fmg_export_solution.restype = C.c_int64
+_lib.fmg_get_rhs.argtypes = [_vp, _vp]
+_lib.bfp_encode.argtypes = [_vp, C.c_int64, C.c_int, _vp, _vp, _vp]
+_lib.bfp_decode.argtypes = [_vp, _vp, C.c_int64, C.c_int, _vp, _vp]
+_lib.bfp_status.argtypes = [_vp]
+
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p)
+_lib.fmg_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, C.c_void_p]
+
+EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_solve_async", "fmg_solve", "fmg_solve_upto",
+           "fmg_norms", "fmg_residual", "fmg_get_solution", "fmg_errors", "fmg_get_section",
+           "fmg_info", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_destroy",
+           "fmg_rhs_size", "fmg_set_rhs", "fmg_get_rhs", "fmg_export_solution",
+           "fmg_strerror", "bfp_encode", "bfp_decode", "bfp_status"]
+
+
+def _check(rc: int, what: str):
+    if rc != FMG_OK:
+        raise FmgError(rc, what)
+
+
+_torch_alloc_refs = None
+
+
+def use_torch_allocator(enable: bool = True):
+    """Back every context's device memory by torch's caching allocator."""
+    global _torch_alloc_refs
+    import torch
+
+    if not enable:
+        _lib.fmg_set_allocator(_ALLOC_FN(), _FREE_FN(), None)
+        _torch_alloc_refs = None
+        return
+
+    def _alloc(nbytes, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device())
+        except Exception:
+            return None
+
+    def _free(ptr, nbytes, user):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    _torch_alloc_refs = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+    _check(_lib.fmg_set_allocator(_torch_alloc_refs[0], _torch_alloc_refs[1], None), "fmg_set_allocator")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+class Solver:
+    """A compact-FMG context (fmg_create ... fmg_destroy)."""
+
+    def __init__(self, dim: int, p: int, levels: int, schedule: Schedule | dict | None = None,
+                 stream=None):
+        if schedule is None:
+            from fmg_inputs import default_schedule
+            schedule = default_schedule(dim, p)
+        if isinstance(schedule, dict):
+            schedule = Schedule.from_dict(schedule)
+        self.dim, self.p, self.levels, self.schedule = dim, p, levels, schedule
+        self.stream = stream
+        h = C.c_void_p()
+        _check(_lib.fmg_create(dim, p, levels, C.byref(schedule), _stream_ptr(stream), C.byref(h)),
+               "fmg_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.fmg_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    # -- Alg 3.3 ----------------------------------------------------------
+    def solve(self):
+        _check(_lib.fmg_solve(self._h), "fmg_solve")
+
+    def solve_async(self):
+        _check(_lib.fmg_solve_async(self._h), "fmg_solve_async")
+
+    def solve_upto(self, L: int, iters_last: int):
+        _check(_lib.fmg_solve_upto(self._h, L, iters_last), "fmg_solve_upto")
+
+    def norms(self):
+        import numpy as np
+        n = self.levels * self.schedule.n_ir * self.levels
+        out = np.zeros(n)
+        _check(_lib.fmg_norms(self._h, out.ctypes.data_as(_dp)), "fmg_norms")
+        return out.reshape(self.levels, self.schedule.n_ir, self.levels)
+
+    def residual(self):
+        import numpy as np
+        out = np.zeros(self.levels)
+        _check(_lib.fmg_residual(self._h, out.ctypes.data_as(_dp)), "fmg_residual")
+        return out
+
+    def geom(self, l: int):
+        n = self.p << (l + 1)
+        NX = (n + 31) // 32 * 32
+        return (n, n, NX) if self.dim == 3 else (1, n, NX)
+
+    def solution(self, L: int | None = None):
+        import torch
+        L = self.levels - 1 if L is None else L
+        out = torch.empty(self.geom(L), dtype=torch.float64, device="cuda")
+        _check(_lib.fmg_get_solution(self._h, C.c_void_p(out.data_ptr())), "fmg_get_solution")
+        return out
+
+    def errors(self):
+        import numpy as np
+        e = np.zeros(3)
+        _check(_lib.fmg_errors(self._h, e.ctypes.data_as(_dp)), "fmg_errors")
+        return e
+
+    def section(self, which: int, l: int):
+        import numpy as np
+        w = C.c_int()
+        _check(_lib.fmg_get_section(self._h, which, l, None, None, C.byref(w)), "fmg_get_section")
+        shp = self.geom(l)
+        nblk = shp[0] * shp[1] * shp[2] // 32
+        mant = np.zeros(nblk * w.value, dtype=np.uint32)
+        exps = np.zeros(nblk, dtype=np.int8)
+        _check(_lib.fmg_get_section(self._h, which, l, mant.ctypes.data, exps.ctypes.data, C.byref(w)),
+               "fmg_get_section")
+        return mant, exps, w.value
+
+    def info(self) -> dict:
+        import numpy as np
+        v = np.zeros(10)
+        _check(_lib.fmg_info(self._h, v.ctypes.data_as(_dp)), "fmg_info")
+        keys = ["dim", "p", "levels", "NX", "NY", "NZ", "unknowns", "stored_bits", "alg_bytes_per_solve",
+                "launches_per_solve"]
+        return dict(zip(keys, v.tolist()))
+
+    def rhs_size(self) -> int:
+        return int(_lib.fmg_rhs_size(self._h))
+
+    def get_rhs(self):
+        import numpy as np
+        out = np.zeros(self.rhs_size())
+        _check(_lib.fmg_get_rhs(self._h, out.ctypes.data), "fmg_get_rhs")
+        return out
+
+    def set_rhs(self, host_tables):
+        """host_tables: numpy float64 array or pinned torch CPU tensor (async copy)."""
+        ptr = host_tables.data_ptr() if hasattr(host_tables, "data_ptr") else host_tables.ctypes.data
+        _check(_lib.fmg_set_rhs(self._h, C.c_void_p(ptr)), "fmg_set_rhs")
+
+    def export_size(self) -> int:
+        return int(_lib.fmg_export_solution(self._h, None, 0))
+
+    def export_solution(self, host_buf):
+        """Asynchronous D2H copy of every compact solution section (storage
+        layout, see fmg.h) into a pinned torch CPU uint8 tensor."""
+        rc = _lib.fmg_export_solution(self._h, C.c_void_p(host_buf.data_ptr()), host_buf.numel())
+        if rc < 0:
+            raise FmgError(-rc, "fmg_export_solution")
+
+    def enable_kernel_timing(self, cls: int):
+        _check(_lib.fmg_enable_kernel_timing(self._h, cls), "fmg_enable_kernel_timing")
+
+    def kernel_time(self):
+        t = C.c_double()
+        n = C.c_int()
+        _check(_lib.fmg_kernel_time(self._h, C.byref(t), C.byref(n)), "fmg_kernel_time")
+        return t.value, n.value
+
+
+def bfp_encode(x, width: int, stream=None):
+    """Encode a CUDA float64 tensor (numel % 32 == 0) -> (mant uint32-as-int32, exps int8)."""
+    import torch
+    assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
+    n = x.numel()
+    mant = torch.empty((n // 32) * width, dtype=torch.int32, device=x.device)
+    exps = torch.empty(n // 32, dtype=torch.int8, device=x.device)
+    st = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    _check(_lib.bfp_encode(C.c_void_p(x.data_ptr()), n, width, C.c_void_p(mant.data_ptr()),
+                           C.c_void_p(exps.data_ptr()), st), "bfp_encode")
+    return mant, exps
+
+
+def bfp_decode(mant, exps, n: int, width: int, stream=None):
+    import torch
+    x = torch.empty(n, dtype=torch.float64, device=mant.device)
+    st = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    _check(_lib.bfp_decode(C.c_void_p(mant.data_ptr()), C.c_void_p(exps.data_ptr()), n, width,
+                           C.c_void_p(x.data_ptr()), st), "bfp_decode")
+    return x
+
+
+def bfp_status(stream=None) -> int:
+    import torch
+    st = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    return _lib.bfp_status(st)

@@ -1,0 +1,607 @@
+// fmg_api.cpp -- C-ABI (include/fmg.h) and the FMG level driver (S11).
+//
+// The driver issues Alg 3.3 as a fixed sequence of kernel
+// launches, captured once into a CUDA graph per context and replayed on every
+// solve.  Per IR iteration at FMG level L:
+//   fmgResidual: prolong/decode l = 0..L, fused residual + encode at L,
+//                restriction + encode l = L-1..0, norm reduction;
+//   cFas + correction: coarse kernel (exact solve, encode ý_0, W_0, ú_0 update),
+//                then per l = 1..L: prolong W_{l-1}, k Chebyshev steps, the last
+//                one fused with encode ý_l, W_l = z_l + dec ý_l and the ú_l update.
+#include "../../include/fmg.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "fmg_internal.h"
+
+using namespace fmg;
+
+namespace {
+fmg_alloc_fn g_alloc = nullptr;
+fmg_free_fn g_free = nullptr;
+void* g_alloc_user = nullptr;
+}  // namespace
+
+struct fmg_ctx {
+  int dim = 0, p = 0, levels = 0, Lmax = 0;
+  fmg_schedule s{};
+  cudaStream_t st = nullptr;      // user stream
+  cudaStream_t cap = nullptr;     // private capture stream
+  cudaStream_t cur = nullptr;     // stream launches are issued on
+  Geom g[kMaxLev];
+  Coefs cf{};
+  Sec u[kMaxLev]{}, r[kMaxLev]{};
+  double* gtab[kMaxLev]{};
+  double* Ainv = nullptr;
+  int n0 = 0;
+  double* buf[7]{};
+  double* partials = nullptr;
+  long long part_off[kMaxLev]{};
+  int part_cnt[kMaxLev]{};
+  double* norms_dev = nullptr;
+  double* err_part = nullptr;
+  int* status = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int solved_L = -1;
+  int wu_cur[kMaxLev]{};
+  fmg_alloc_fn afn = nullptr;
+  fmg_free_fn ffn = nullptr;
+  void* auser = nullptr;
+  std::vector<std::pair<void*, size_t>> allocs;
+  // kernel timing
+  int timing_cls = -1;
+  std::vector<cudaEvent_t> ev;
+  int ev_used = 0;
+  long long launches = 0;
+};
+
+namespace {
+
+int wu(const fmg_ctx* c, int l, int L) { return c->s.b_u + c->s.k_u * (L - l); }
+int wr(const fmg_ctx* c, int l, int L) { return c->s.b_r + c->s.k_r * (L - l); }
+
+void* dalloc(fmg_ctx* c, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* ptr = nullptr;
+  if (c->afn) {
+    ptr = c->afn(bytes, c->auser);
+  } else if (cudaMalloc(&ptr, bytes) != cudaSuccess) {
+    ptr = nullptr;
+  }
+  if (ptr) c->allocs.emplace_back(ptr, bytes);
+  return ptr;
+}
+
+void free_all(fmg_ctx* c) {
+  for (auto& a : c->allocs) {
+    if (c->ffn) c->ffn(a.first, a.second, c->auser);
+    else cudaFree(a.first);
+  }
+  c->allocs.clear();
+}
+
+Launch L_(fmg_ctx* c) { return Launch{c->dim, c->p, c->cur}; }
+
+// Kernel-time instrumentation (fine-level launches of the selected class).
+void mark(fmg_ctx* c, int cls, int level) {
+  if (c->timing_cls != cls || level != c->Lmax) return;
+  if (c->ev_used >= (int)c->ev.size()) return;
+  cudaEventRecordWithFlags(c->ev[c->ev_used++], c->cur, cudaEventRecordExternal);
+}
+
+void record_residual(fmg_ctx* c, int L, int it) {
+  double* U[2] = {c->buf[0], c->buf[1]};
+  double* T[2] = {c->buf[2], c->buf[3]};
+  Launch ln = L_(c);
+  launch_prolong_decode(ln, U[0], c->g[0], nullptr, c->g[0], c->u[0].mant, c->u[0].exps, c->wu_cur[0],
+                        c->u[0].stride, c->cf);
+  c->launches++;
+  for (int l = 1; l <= L; ++l) {
+    bool tm = (l == L && L == c->Lmax);
+    if (tm) mark(c, 2, L);
+    launch_prolong_decode(ln, U[l & 1], c->g[l], U[(l - 1) & 1], c->g[l - 1], c->u[l].mant, c->u[l].exps,
+                          c->wu_cur[l], c->u[l].stride, c->cf);
+    if (tm) mark(c, 2, L);
+    c->launches++;
+  }
+  mark(c, 0, L);
+  launch_residual(ln, U[L & 1], T[L & 1], c->g[L], c->gtab[L], c->r[L], wr(c, L, L),
+                  c->partials + c->part_off[L], c->cf, c->status);
+  mark(c, 0, L);
+  c->launches++;
+  for (int l = L - 1; l >= 0; --l) {
+    bool tm = (l == L - 1);
+    if (tm) mark(c, 3, L);
+    launch_restrict(ln, T[(l + 1) & 1], c->g[l + 1], T[l & 1], c->g[l], c->r[l], wr(c, l, L),
+                    c->partials + c->part_off[l], c->cf, c->status);
+    if (tm) mark(c, 3, L);
+    c->launches++;
+  }
+  launch_norms(c->cur, c->partials, c->part_off, c->part_cnt, L + 1,
+               c->norms_dev + ((size_t)L * c->s.n_ir + it) * c->levels);
+  c->launches++;
+}
+
+void record_cfas(fmg_ctx* c, int L) {
+  double* W[2] = {c->buf[0], c->buf[1]};
+  double* Z = c->buf[2];
+  double* B = c->buf[3];
+  double* Y[2] = {c->buf[4], c->buf[5]};
+  double* Dv = c->buf[6];
+  Launch ln = L_(c);
+  launch_coarse(ln, 1, c->g[0], c->gtab[0], c->Ainv, c->n0, c->u[0], c->wu_cur[0], wu(c, 0, L), c->r[0],
+                wr(c, 0, L), W[0], c->cf, c->status);
+  c->launches++;
+  c->wu_cur[0] = wu(c, 0, L);
+  const int k = c->s.cheb_degree;
+  for (int l = 1; l <= L; ++l) {
+    launch_prolong_decode(ln, Z, c->g[l], W[(l - 1) & 1], c->g[l - 1], nullptr, nullptr, 0, 0, c->cf);
+    c->launches++;
+    for (int step = 1; step <= k; ++step) {
+      CfasArgs a;
+      a.Z = Z;
+      a.B = B;
+      a.Yin = step == 1 ? nullptr : Y[step & 1];
+      a.Yout = Y[(step - 1) & 1];
+      a.Dv = Dv;
+      a.W = l < L ? W[l & 1] : nullptr;
+      a.r = c->r[l];
+      a.wr = wr(c, l, L);
+      a.u = c->u[l];
+      a.wu_in = c->wu_cur[l];
+      a.wu_out = wu(c, l, L);
+      a.step = step;
+      a.last = step == k;
+      bool tm = (l == L);
+      if (tm) mark(c, 1, L);
+      launch_cfas_step(ln, c->g[l], a, c->cf, c->status);
+      if (tm) mark(c, 1, L);
+      c->launches++;
+    }
+    c->wu_cur[l] = wu(c, l, L);
+  }
+}
+
+// Alg 3.3 up to FMG level Lstop (iters_last IR iterations there).
+void record_solve(fmg_ctx* c, int Lstop, int iters_last) {
+  c->launches = 0;
+  c->ev_used = 0;
+  for (int l = 0; l <= c->Lmax; ++l) {
+    cudaMemsetAsync(c->u[l].mant, 0, sizeof(uint32_t) * c->g[l].nblk * c->u[l].stride, c->cur);
+    cudaMemsetAsync(c->u[l].exps, 0x80, c->g[l].nblk, c->cur);
+    c->wu_cur[l] = wu(c, l, l);
+  }
+  cudaMemsetAsync(c->norms_dev, 0, sizeof(double) * c->levels * c->s.n_ir * c->levels, c->cur);
+  // coarse-grid solve PAPER.md:786: ú_0 = reg(A_0^{-1} f_0) at w_u(0,0)
+  launch_coarse(L_(c), 0, c->g[0], c->gtab[0], c->Ainv, c->n0, c->u[0], wu(c, 0, 0), wu(c, 0, 0), c->r[0],
+                wr(c, 0, 0), c->buf[0], c->cf, c->status);
+  c->launches++;
+  c->wu_cur[0] = wu(c, 0, 0);
+  for (int L = 1; L <= Lstop; ++L) {
+    // push level PAPER.md:788: ú_L = 0 (already zero); widening of ú_{0..L-1}
+    // is value-preserving and happens at the next re-encode.
+    c->wu_cur[L] = wu(c, L, L);
+    int iters = (L == Lstop) ? iters_last : c->s.n_ir;
+    for (int it = 0; it < iters; ++it) {
+      record_residual(c, L, it);
+      record_cfas(c, L);
+    }
+  }
+}
+
+int cuda_err(cudaError_t e) {
+  if (e == cudaSuccess) return FMG_OK;
+  if (e == cudaErrorMemoryAllocation) return FMG_ENOMEM;
+  return FMG_ECUDA;
+}
+
+int sync_check(fmg_ctx* c) {
+  cudaError_t e = cudaStreamSynchronize(c->st);
+  if (e != cudaSuccess) return cuda_err(e);
+  int st = 0;
+  e = cudaMemcpy(&st, c->status, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_err(e);
+  if (st) {
+    cudaMemset(c->status, 0, sizeof(int));
+    return FMG_ERANGE;
+  }
+  return FMG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmg_set_allocator(fmg_alloc_fn alloc, fmg_free_fn free_fn, void* user) {
+  if ((alloc == nullptr) != (free_fn == nullptr)) return FMG_EINVAL;
+  g_alloc = alloc;
+  g_free = free_fn;
+  g_alloc_user = user;
+  return FMG_OK;
+}
+
+int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, fmg_ctx** out) {
+  if (!out || !s) return FMG_EINVAL;
+  *out = nullptr;
+  if ((dim != 2 && dim != 3) || p < 1 || p > 3 || levels < 1 || levels > kMaxLev) return FMG_EINVAL;
+  if (s->b_u < 2 || s->b_r < 2 || s->k_u < 0 || s->k_r < 0 || s->n_ir < 1 || s->cheb_degree < 1 ||
+      s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1))
+    return FMG_EINVAL;
+  int Lmax = levels - 1;
+  if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
+  fmg_ctx* c = new fmg_ctx();
+  c->dim = dim; c->p = p; c->levels = levels; c->Lmax = Lmax; c->s = *s;
+  c->st = (cudaStream_t)stream;
+  c->afn = g_alloc; c->ffn = g_free; c->auser = g_alloc_user;
+  if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) { delete c; return FMG_ECUDA; }
+  set_kernel_attributes();
+  build_coefs(dim, p, s->lambda_hi, s->alpha, s->cheb_degree, &c->cf);
+  int rc = FMG_OK;
+  long long tot_parts = 0;
+  for (int l = 0; l <= Lmax; ++l) {
+    Geom& g = c->g[l];
+    g.l = l;
+    g.n = p << (l + 1);
+    g.NX = ((g.n + 31) / 32) * 32;
+    g.NY = g.n;
+    g.NZ = dim == 3 ? g.n : 1;
+    g.size = (long long)g.NX * g.NY * g.NZ;
+    g.nblk = g.size / 32;
+    c->u[l].stride = wu(c, l, Lmax);
+    c->r[l].stride = wr(c, l, Lmax);
+    c->u[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->u[l].stride);
+    c->u[l].exps = (int8_t*)dalloc(c, g.nblk);
+    c->r[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->r[l].stride);
+    c->r[l].exps = (int8_t*)dalloc(c, g.nblk);
+    c->gtab[l] = (double*)dalloc(c, sizeof(double) * g.n);
+    if (!c->u[l].mant || !c->u[l].exps || !c->r[l].mant || !c->r[l].exps || !c->gtab[l]) { rc = FMG_ENOMEM; break; }
+    std::vector<double> gt(g.n);
+    build_rhs_table(p, l, gt.data());
+    cudaMemcpy(c->gtab[l], gt.data(), sizeof(double) * g.n, cudaMemcpyHostToDevice);
+    c->part_cnt[l] = tile_count(dim, p, 0, g);
+    c->part_off[l] = tot_parts;
+    tot_parts += c->part_cnt[l];
+  }
+  if (rc == FMG_OK) {
+    for (int i = 0; i < 7 && rc == FMG_OK; ++i) {
+      c->buf[i] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
+      if (!c->buf[i]) rc = FMG_ENOMEM;
+    }
+  }
+  if (rc == FMG_OK) {
+    c->n0 = coarse_count(dim, p);
+    std::vector<double> Ai((size_t)c->n0 * c->n0);
+    if (build_coarse_inverse(dim, p, Ai.data())) rc = FMG_EINVAL;
+    c->Ainv = (double*)dalloc(c, sizeof(double) * Ai.size());
+    c->partials = (double*)dalloc(c, sizeof(double) * tot_parts);
+    c->norms_dev = (double*)dalloc(c, sizeof(double) * levels * s->n_ir * levels);
+    c->err_part = (double*)dalloc(c, sizeof(double) * 2 * 148 * 16);
+    c->status = (int*)dalloc(c, sizeof(int));
+    if (!c->Ainv || !c->partials || !c->norms_dev || !c->err_part || !c->status) rc = FMG_ENOMEM;
+    else {
+      cudaMemcpy(c->Ainv, Ai.data(), sizeof(double) * Ai.size(), cudaMemcpyHostToDevice);
+      cudaMemset(c->status, 0, sizeof(int));
+      cudaMemset(c->norms_dev, 0, sizeof(double) * levels * s->n_ir * levels);
+    }
+  }
+  if (rc == FMG_OK) rc = cuda_err(cudaDeviceSynchronize());
+  if (rc != FMG_OK) {
+    fmg_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return FMG_OK;
+}
+
+int fmg_solve_async(fmg_ctx* c) {
+  if (!c) return FMG_EINVAL;
+  if (!c->graph) {
+    c->cur = c->cap;
+    cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_err(e);
+    record_solve(c, c->Lmax, c->s.n_ir);
+    cudaGraph_t gr;
+    e = cudaStreamEndCapture(c->cap, &gr);
+    if (e != cudaSuccess) return cuda_err(e);
+    e = cudaGraphInstantiate(&c->graph, gr, 0);
+    cudaGraphDestroy(gr);
+    if (e != cudaSuccess) { c->graph = nullptr; return cuda_err(e); }
+  }
+  cudaError_t e = cudaGraphLaunch(c->graph, c->st);
+  if (e != cudaSuccess) return cuda_err(e);
+  c->solved_L = c->Lmax;
+  return FMG_OK;
+}
+
+int fmg_solve(fmg_ctx* c) {
+  int rc = fmg_solve_async(c);
+  if (rc) return rc;
+  return sync_check(c);
+}
+
+int fmg_solve_upto(fmg_ctx* c, int Lstop, int iters_last) {
+  if (!c || Lstop < 0 || Lstop > c->Lmax || iters_last < 0) return FMG_EINVAL;
+  c->cur = c->st;
+  int save = c->timing_cls;
+  c->timing_cls = -1;
+  record_solve(c, Lstop, iters_last);
+  c->timing_cls = save;
+  c->solved_L = Lstop;
+  return sync_check(c);
+}
+
+int fmg_norms(fmg_ctx* c, double* host) {
+  if (!c || !host) return FMG_EINVAL;
+  cudaError_t e = cudaStreamSynchronize(c->st);
+  if (e != cudaSuccess) return cuda_err(e);
+  e = cudaMemcpy(host, c->norms_dev, sizeof(double) * c->levels * c->s.n_ir * c->levels, cudaMemcpyDeviceToHost);
+  return cuda_err(e);
+}
+
+int fmg_residual(fmg_ctx* c, double* host_norms) {
+  if (!c) return FMG_EINVAL;
+  if (c->solved_L < 0) return FMG_ESTATE;
+  int L = c->solved_L;
+  c->cur = c->st;
+  int save = c->timing_cls;
+  c->timing_cls = -1;
+  // Use row (L, it = 0) of a scratch region: the last norm row of the log is
+  // preserved by copying it around the call.
+  std::vector<double> keep(c->levels);
+  double* row = c->norms_dev + ((size_t)L * c->s.n_ir) * c->levels;
+  cudaMemcpyAsync(keep.data(), row, sizeof(double) * c->levels, cudaMemcpyDeviceToHost, c->st);
+  cudaStreamSynchronize(c->st);
+  record_residual(c, L, 0);
+  c->timing_cls = save;
+  int rc = sync_check(c);
+  if (rc) return rc;
+  if (host_norms) {
+    std::vector<double> tmp(c->levels, 0.0);
+    cudaMemcpy(tmp.data(), row, sizeof(double) * c->levels, cudaMemcpyDeviceToHost);
+    for (int l = 0; l < c->levels; ++l) host_norms[l] = l <= L ? tmp[l] : 0.0;
+  }
+  cudaMemcpy(row, keep.data(), sizeof(double) * c->levels, cudaMemcpyHostToDevice);
+  return FMG_OK;
+}
+
+static int decode_solution(fmg_ctx* c) {
+  int L = c->solved_L;
+  c->cur = c->st;
+  Launch ln = L_(c);
+  double* U[2] = {c->buf[0], c->buf[1]};
+  launch_prolong_decode(ln, U[0], c->g[0], nullptr, c->g[0], c->u[0].mant, c->u[0].exps, c->wu_cur[0],
+                        c->u[0].stride, c->cf);
+  for (int l = 1; l <= L; ++l)
+    launch_prolong_decode(ln, U[l & 1], c->g[l], U[(l - 1) & 1], c->g[l - 1], c->u[l].mant, c->u[l].exps,
+                          c->wu_cur[l], c->u[l].stride, c->cf);
+  return L & 1;
+}
+
+int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
+  if (!c || !dst_dev) return FMG_EINVAL;
+  if (c->solved_L < 0) return FMG_ESTATE;
+  int which = decode_solution(c);
+  cudaMemcpyAsync(dst_dev, c->buf[which], sizeof(double) * c->g[c->solved_L].size, cudaMemcpyDeviceToDevice,
+                  c->st);
+  return sync_check(c);
+}
+
+int fmg_errors(fmg_ctx* c, double* err3) {
+  if (!c || !err3) return FMG_EINVAL;
+  if (c->solved_L < 0) return FMG_ESTATE;
+  int which = decode_solution(c);
+  int np = 0;
+  launch_errors(L_(c), c->buf[which], c->g[c->solved_L], c->err_part, &np);
+  int rc = sync_check(c);
+  if (rc) return rc;
+  std::vector<double> h(2 * np);
+  cudaMemcpy(h.data(), c->err_part, sizeof(double) * 2 * np, cudaMemcpyDeviceToHost);
+  double e0 = 0.0, e1 = 0.0;
+  for (int i = 0; i < np; ++i) { e0 += h[2 * i]; e1 += h[2 * i + 1]; }
+  double hh = std::ldexp(1.0, -(c->solved_L + 1));
+  double vol = c->dim == 3 ? hh * hh * hh : hh * hh;
+  e0 *= vol; e1 *= vol;
+  double nL2 = std::ldexp(1.0, -c->dim), nH1 = c->dim * M_PI * M_PI * std::ldexp(1.0, -c->dim);
+  err3[0] = std::sqrt(e0 / nL2);
+  err3[1] = std::sqrt(e1 / nH1);
+  err3[2] = std::sqrt((e0 + e1) / (nL2 + nH1));
+  return FMG_OK;
+}
+
+int fmg_get_section(fmg_ctx* c, int which, int level, uint32_t* mant, int8_t* exps, int* width) {
+  if (!c || which < 0 || which > 1 || level < 0 || level > c->Lmax || !width) return FMG_EINVAL;
+  if (c->solved_L < 0) return FMG_ESTATE;
+  const Geom& g = c->g[level];
+  const Sec& s = which == 0 ? c->u[level] : c->r[level];
+  int w = which == 0 ? c->wu_cur[level] : wr(c, level, c->solved_L);
+  *width = w;
+  cudaError_t e = cudaStreamSynchronize(c->st);
+  if (e != cudaSuccess) return cuda_err(e);
+  if (mant) {
+    std::vector<uint32_t> tmp((size_t)g.nblk * s.stride);
+    e = cudaMemcpy(tmp.data(), s.mant, sizeof(uint32_t) * tmp.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_err(e);
+    for (long long b = 0; b < g.nblk; ++b) std::memcpy(mant + b * w, tmp.data() + b * s.stride, sizeof(uint32_t) * w);
+  }
+  if (exps) {
+    e = cudaMemcpy(exps, s.exps, g.nblk, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_err(e);
+  }
+  return FMG_OK;
+}
+
+int fmg_info(fmg_ctx* c, double* info) {
+  if (!c || !info) return FMG_EINVAL;
+  const Geom& g = c->g[c->Lmax];
+  info[0] = c->dim; info[1] = c->p; info[2] = c->levels;
+  info[3] = g.NX; info[4] = g.NY; info[5] = g.NZ;
+  info[6] = std::pow((double)(g.n - 1), c->dim);
+  // stored bits at the finest FMG level: mantissas + exponents of u and r sections
+  double bits = 0.0, bytes_solve = 0.0;
+  for (int l = 0; l <= c->Lmax; ++l)
+    bits += (double)c->g[l].size * (wu(c, l, c->Lmax) + wr(c, l, c->Lmax)) + 2.0 * 8 * c->g[l].nblk;
+  info[7] = bits;
+  // algorithmic bytes: per IR iteration at FMG level L every
+  // stored u and r section is read once and written once.
+  for (int L = 1; L <= c->Lmax; ++L) {
+    double sweep = 0.0;
+    for (int l = 0; l <= L; ++l)
+      sweep += 2.0 * ((double)c->g[l].size * (wu(c, l, L) + wr(c, l, L)) / 8.0 + 2.0 * c->g[l].nblk);
+    bytes_solve += c->s.n_ir * sweep;
+  }
+  info[8] = bytes_solve;
+  info[9] = (double)c->launches;
+  return FMG_OK;
+}
+
+int fmg_enable_kernel_timing(fmg_ctx* c, int cls) {
+  if (!c || cls < -1 || cls > 3) return FMG_EINVAL;
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  for (auto e : c->ev) cudaEventDestroy(e);
+  c->ev.clear();
+  c->timing_cls = cls;
+  if (cls >= 0) {
+    int per = (cls == 1) ? c->s.cheb_degree : 1;
+    int n = 2 * c->s.n_ir * per;
+    for (int i = 0; i < n; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->ev.push_back(e);
+    }
+  }
+  return FMG_OK;
+}
+
+int fmg_kernel_time(fmg_ctx* c, double* total_ms, int* launches) {
+  if (!c || !total_ms || !launches) return FMG_EINVAL;
+  cudaError_t e = cudaStreamSynchronize(c->st);
+  if (e != cudaSuccess) return cuda_err(e);
+  double tot = 0.0;
+  int n = 0;
+  for (int i = 0; i + 1 < c->ev_used; i += 2) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]) == cudaSuccess) {
+      tot += ms;
+      n++;
+    }
+  }
+  *total_ms = tot;
+  *launches = n;
+  return FMG_OK;
+}
+
+int64_t fmg_rhs_size(fmg_ctx* c) {
+  if (!c) return -1;
+  int64_t n = 0;
+  for (int l = 0; l <= c->Lmax; ++l) n += c->g[l].n;
+  return n;
+}
+
+int fmg_set_rhs(fmg_ctx* c, const double* host) {
+  if (!c || !host) return FMG_EINVAL;
+  int64_t off = 0;
+  for (int l = 0; l <= c->Lmax; ++l) {
+    cudaError_t e = cudaMemcpyAsync(c->gtab[l], host + off, sizeof(double) * c->g[l].n, cudaMemcpyHostToDevice, c->st);
+    if (e != cudaSuccess) return cuda_err(e);
+    off += c->g[l].n;
+  }
+  return FMG_OK;
+}
+
+int fmg_get_rhs(fmg_ctx* c, double* host) {
+  if (!c || !host) return FMG_EINVAL;
+  cudaError_t e = cudaStreamSynchronize(c->st);
+  if (e != cudaSuccess) return cuda_err(e);
+  int64_t off = 0;
+  for (int l = 0; l <= c->Lmax; ++l) {
+    e = cudaMemcpy(host + off, c->gtab[l], sizeof(double) * c->g[l].n, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_err(e);
+    off += c->g[l].n;
+  }
+  return FMG_OK;
+}
+
+int64_t fmg_export_solution(fmg_ctx* c, void* host, int64_t cap) {
+  if (!c) return -FMG_EINVAL;
+  int64_t need = 0;
+  for (int l = 0; l <= c->Lmax; ++l) need += (int64_t)c->g[l].nblk * (4 * c->u[l].stride + 1);
+  if (!host || cap < need) return need;
+  char* dst = (char*)host;
+  for (int l = 0; l <= c->Lmax; ++l) {
+    size_t mb = sizeof(uint32_t) * c->g[l].nblk * c->u[l].stride;
+    cudaError_t e = cudaMemcpyAsync(dst, c->u[l].mant, mb, cudaMemcpyDeviceToHost, c->st);
+    if (e != cudaSuccess) return -cuda_err(e);
+    dst += mb;
+    e = cudaMemcpyAsync(dst, c->u[l].exps, c->g[l].nblk, cudaMemcpyDeviceToHost, c->st);
+    if (e != cudaSuccess) return -cuda_err(e);
+    dst += c->g[l].nblk;
+  }
+  return need;
+}
+
+void fmg_destroy(fmg_ctx* c) {
+  if (!c) return;
+  cudaDeviceSynchronize();
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  free_all(c);
+  if (c->cap) cudaStreamDestroy(c->cap);
+  delete c;
+}
+
+const char* fmg_strerror(int code) {
+  switch (code) {
+    case FMG_OK: return "ok";
+    case FMG_EINVAL: return "invalid argument";
+    case FMG_ERANGE: return "BFP exponent out of range or non-finite value";
+    case FMG_ENOMEM: return "device allocation failed";
+    case FMG_ECUDA: return "CUDA runtime error";
+    case FMG_ESTATE: return "call out of order";
+    default: return "unknown error";
+  }
+}
+
+// ------------------------------------------------------------ codec API --
+static int* g_codec_status = nullptr;
+
+int bfp_encode(const double* x, int64_t n, int width, uint32_t* mant, int8_t* exps, void* stream) {
+  if (width < 2 || width > 54 || n < 0 || (n % 32) != 0 || (n > 0 && (!x || !mant || !exps))) return FMG_EINVAL;
+  if (n == 0) return FMG_OK;
+  if (!g_codec_status) {
+    if (cudaMalloc(&g_codec_status, sizeof(int)) != cudaSuccess) return FMG_ENOMEM;
+    cudaMemset(g_codec_status, 0, sizeof(int));
+  }
+  launch_bfp_encode(x, n, width, mant, exps, g_codec_status, (cudaStream_t)stream);
+  return cuda_err(cudaGetLastError());
+}
+
+int bfp_decode(const uint32_t* mant, const int8_t* exps, int64_t n, int width, double* x, void* stream) {
+  if (width < 2 || width > 54 || n < 0 || (n % 32) != 0 || (n > 0 && (!x || !mant || !exps))) return FMG_EINVAL;
+  if (n == 0) return FMG_OK;
+  launch_bfp_decode(mant, exps, n, width, x, (cudaStream_t)stream);
+  return cuda_err(cudaGetLastError());
+}
+
+int bfp_status(void* stream) {
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_err(e);
+  if (!g_codec_status) return FMG_OK;
+  int st = 0;
+  cudaMemcpy(&st, g_codec_status, sizeof(int), cudaMemcpyDeviceToHost);
+  if (st) {
+    cudaMemset(g_codec_status, 0, sizeof(int));
+    return FMG_ERANGE;
+  }
+  return FMG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,197 @@
+"""GPU parity: libfmg.so (C-ABI, via the thin binding) against the CPU oracle.
+
+Bars (BASELINE.json north star): codec bit-exact on identical
+inputs; packed sections <= 1 LSB apart in <= 1e-4 of entries (design target and
+asserted here: bit-identical, canonical FP64 order DESIGN.md §3); per-level
+residual norms within 1e-6 relative; final relative H1 error within 1e-3.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import oracle as O
+from fmg_inputs import CONFIGS, codec_vectors, default_schedule
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2511_19036_b200 as P
+    return P
+
+
+def _oracle_sched(d, p, **kw):
+    return O.schedule(d, p, **kw)
+
+
+def _gpu_sched(P, d, p, **kw):
+    s = default_schedule(d, p)
+    s.update({k: v for k, v in kw.items() if v is not None})
+    return P.Schedule.from_dict(s)
+
+
+# ------------------------------------------------------------------ codec --
+@pytest.mark.parametrize("kind", ["smooth", "gauss", "adversarial"])
+@pytest.mark.parametrize("w", [2, 3, 4, 5, 6, 7, 8, 12, 13, 21, 31, 32, 33, 40, 53, 54])
+def test_codec_bit_exact(P, kind, w):
+    n = 32 * 4099  # ragged block count
+    x = codec_vectors(n, seed=1000 + w, kind=kind)
+    rc, m_ref, e_ref = O.bfp_encode(x, w)
+    assert rc == 0
+    xt = torch.from_numpy(x).cuda()
+    mant, exps = P.bfp_encode(xt, w)
+    assert P.bfp_status() == 0
+    assert np.array_equal(mant.cpu().numpy().view(np.uint32), m_ref)
+    assert np.array_equal(exps.cpu().numpy(), e_ref)
+    y = P.bfp_decode(mant, exps, n, w)
+    _, y_ref = O.bfp_decode(m_ref, e_ref, n, w)
+    assert np.array_equal(y.cpu().numpy(), y_ref)
+
+
+def test_codec_empty_and_errors(P):
+    x = torch.zeros(0, dtype=torch.float64, device="cuda")
+    mant, exps = P.bfp_encode(x, 4)
+    assert mant.numel() == 0
+    x = torch.zeros(64, dtype=torch.float64, device="cuda")
+    x[3] = float("inf")
+    P.bfp_encode(x, 4)
+    assert P.bfp_status() == P.FMG_ERANGE
+    assert P.bfp_status() == 0  # cleared
+    x[3] = 2.0 ** 300
+    P.bfp_encode(x, 4)
+    assert P.bfp_status() == P.FMG_ERANGE
+
+
+def test_codec_large_sampled(P):
+    """Full-size codec call (2^27 values) in the bench launch config; sampled
+    blocks checked against the oracle block by block."""
+    n = 1 << 27
+    g = torch.Generator(device="cuda").manual_seed(7)
+    xt = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    for w in (4, 6):
+        mant, exps = P.bfp_encode(xt, w)
+        assert P.bfp_status() == 0
+        rng = np.random.default_rng(w)
+        blocks = np.concatenate([[0, n // 32 - 1], rng.integers(0, n // 32, 200)])
+        xs = xt.view(-1, 32)[torch.from_numpy(blocks).cuda()].cpu().numpy().reshape(-1)
+        _, m_ref, e_ref = O.bfp_encode(xs, w)
+        mm = mant.view(-1, w)[torch.from_numpy(blocks).cuda()].cpu().numpy().view(np.uint32).reshape(-1)
+        ee = exps[torch.from_numpy(blocks).cuda()].cpu().numpy()
+        assert np.array_equal(mm, m_ref) and np.array_equal(ee, e_ref)
+
+
+# -------------------------------------------------------------------- FMG --
+def compare_solvers(P, d, p, levels, check_r=True, **kw):
+    so = _oracle_sched(d, p, **kw)
+    oc = O.CFMG(d, p, levels, so)
+    oc.solve()
+    gs = P.Solver(d, p, levels, _gpu_sched(P, d, p, **kw))
+    gs.solve()
+    # norms: per FMG level, IR iteration and level
+    no, ng = oc.norms(), gs.norms()
+    mask = no != 0
+    assert np.array_equal(mask, ng != 0)
+    if mask.any():
+        rel = np.abs(ng[mask] - no[mask]) / no[mask]
+        assert rel.max() <= 1e-6, rel.max()
+    # packed sections: bit-identical (design target; bar is <= 1 LSB in <= 1e-4)
+    for l in range(levels):
+        mo, eo, wo = oc.section(0, l)
+        mg, eg, wg = gs.section(0, l)
+        assert wo == wg
+        assert np.array_equal(eo, eg), l
+        assert np.array_equal(mo, mg), l
+        if check_r and levels > 1:
+            mo, eo, wo = oc.section(1, l)
+            mg, eg, wg = gs.section(1, l)
+            assert wo == wg and np.array_equal(eo, eg) and np.array_equal(mo, mg), ("r", l)
+    # decoded standard representation: bit-identical
+    uo = oc.solution()
+    ug = gs.solution().cpu().numpy()
+    assert np.array_equal(uo, ug)
+    # final relative errors
+    eo, eg = oc.errors(), gs.errors()
+    assert np.all(np.abs(eg - eo) <= 1e-3 * eo), (eo, eg)
+    return oc, gs
+
+
+@pytest.mark.parametrize("d,p,levels", [(2, 1, 1), (2, 1, 2), (2, 1, 7), (2, 2, 6), (2, 3, 5),
+                                        (3, 1, 2), (3, 1, 5), (3, 2, 4), (3, 3, 4)])
+def test_fmg_parity_small(P, d, p, levels):
+    compare_solvers(P, d, p, levels)
+
+
+def test_fmg_parity_C1(P):
+    c = CONFIGS["C1"]
+    compare_solvers(P, c["dim"], c["p"], c["levels"])
+
+
+def test_fmg_parity_C2_full(P):
+    """The bench workload (configs[1]) at full size, element by element."""
+    c = CONFIGS["C2"]
+    compare_solvers(P, c["dim"], c["p"], c["levels"], check_r=False)
+
+
+@pytest.mark.parametrize("d,p,levels,L,it", [(2, 2, 5, 3, 1), (3, 1, 4, 2, 2), (3, 3, 3, 2, 1)])
+def test_partial_solve_parity(P, d, p, levels, L, it):
+    so = _oracle_sched(d, p)
+    oc = O.CFMG(d, p, levels, so)
+    oc.solve_upto(L, it)
+    gs = P.Solver(d, p, levels)
+    gs.solve_upto(L, it)
+    for l in range(L + 1):
+        for which in (0, 1):
+            mo, eo, _ = oc.section(which, l)
+            mg, eg, _ = gs.section(which, l)
+            assert np.array_equal(eo, eg) and np.array_equal(mo, mg), (which, l)
+    ro = oc.residual(L)
+    rg = gs.residual()[: L + 1]
+    assert np.all(np.abs(rg - ro) <= 1e-6 * ro)
+
+
+@pytest.mark.parametrize("d,p,levels", [(2, 1, 5), (3, 2, 3)])
+def test_width_edge_schedules(P, d, p, levels):
+    """Edge widths: minimum width 2 for r, high widths up to 54 on coarse levels."""
+    compare_solvers(P, d, p, levels, b_r=2)
+    compare_solvers(P, d, p, levels, b_u=54 - (p + 1) * (levels - 1), b_r=54 - (levels - 1))
+
+
+def test_determinism_and_graph_replay(P):
+    gs = P.Solver(2, 2, 6)
+    gs.solve()
+    a = gs.norms().copy()
+    sa = [gs.section(0, l)[0].copy() for l in range(6)]
+    for _ in range(3):
+        gs.solve()
+    assert np.array_equal(a, gs.norms())
+    for l in range(6):
+        assert np.array_equal(sa[l], gs.section(0, l)[0])
+
+
+def test_residual_api_and_state(P):
+    gs = P.Solver(2, 1, 5)
+    with pytest.raises(P.FmgError):
+        gs.residual()
+    gs.solve()
+    r = gs.residual()
+    oc = O.CFMG(2, 1, 5, _oracle_sched(2, 1))
+    oc.solve()
+    ro = oc.residual(4)
+    assert np.all(np.abs(r - ro) <= 1e-6 * ro)
+
+
+def test_torch_allocator_hook(P):
+    P.use_torch_allocator(True)
+    try:
+        before = torch.cuda.memory_allocated()
+        gs = P.Solver(2, 2, 5)
+        assert torch.cuda.memory_allocated() > before
+        gs.solve()
+        oc = O.CFMG(2, 2, 5, _oracle_sched(2, 2))
+        oc.solve()
+        assert np.array_equal(oc.section(0, 4)[0], gs.section(0, 4)[0])
+        gs.close()
+    finally:
+        P.use_torch_allocator(False)
