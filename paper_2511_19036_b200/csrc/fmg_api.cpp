@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "fmg_internal.h"
@@ -38,18 +39,22 @@ struct fmg_ctx {
   Coefs cf{};
   Sec u[kMaxLev]{}, r[kMaxLev]{};
   double* gtab[kMaxLev]{};
+  int tiles[kMaxLev][3]{};
   double* Ainv = nullptr;
   int n0 = 0;
   double* buf[7]{};
   double* partials = nullptr;
   long long part_off[kMaxLev]{};
-  int part_cnt[kMaxLev]{};
   double* norms_dev = nullptr;
   double* err_part = nullptr;
   int* status = nullptr;
+  void* devctx = nullptr;         // DevCtx in device memory
+  void* prog[2] = {nullptr, nullptr};  // op programs: [0] graph, [1] direct
+  size_t prog_cap[2] = {0, 0};
   cudaGraphExec_t graph = nullptr;
   int solved_L = -1;
   int wu_cur[kMaxLev]{};
+  int seq_max_level = -1;         // levels <= this run inside the sequencer kernel
   fmg_alloc_fn afn = nullptr;
   fmg_free_fn ffn = nullptr;
   void* auser = nullptr;
@@ -88,111 +93,161 @@ void free_all(fmg_ctx* c) {
 
 Launch L_(fmg_ctx* c) { return Launch{c->dim, c->p, c->cur}; }
 
-// Kernel-time instrumentation (fine-level launches of the selected class).
-void mark(fmg_ctx* c, int cls, int level) {
-  if (c->timing_cls != cls || level != c->Lmax) return;
-  if (c->ev_used >= (int)c->ev.size()) return;
-  cudaEventRecordWithFlags(c->ev[c->ev_used++], c->cur, cudaEventRecordExternal);
+// ---------------------------------------------------------------- schedule --
+// A solve is a list of items: a grid launch of one op over all tiles of its
+// level, or a sequencer launch of consecutive small-level ops.
+struct Item {
+  bool seq;
+  OpDesc op;          // grid item
+  int first, count;   // seq item: range in the op program
+  int timed_cls;      // kernel-timing class of a grid item (-1: none)
+};
+
+struct Builder {
+  fmg_ctx* c;
+  std::vector<Item> items;
+  std::vector<OpDesc> prog;
+  bool small(int l) const { return l <= c->seq_max_level; }
+  void add(const OpDesc& op, bool in_seq, int cls = -1) {
+    if (in_seq) {
+      if (!items.empty() && items.back().seq && items.back().first + items.back().count == (int)prog.size()) {
+        items.back().count++;
+      } else {
+        Item it{};
+        it.seq = true;
+        it.first = (int)prog.size();
+        it.count = 1;
+        it.timed_cls = -1;
+        items.push_back(it);
+      }
+      prog.push_back(op);
+    } else {
+      Item it{};
+      it.seq = false;
+      it.op = op;
+      it.timed_cls = cls;
+      items.push_back(it);
+    }
+  }
+};
+
+OpDesc mkop(int type, int l, int L) {
+  OpDesc o{};
+  o.type = type;
+  o.l = l;
+  o.L = L;
+  return o;
 }
 
-void record_residual(fmg_ctx* c, int L, int it) {
-  double* U[2] = {c->buf[0], c->buf[1]};
-  double* T[2] = {c->buf[2], c->buf[3]};
-  Launch ln = L_(c);
-  launch_prolong_decode(ln, U[0], c->g[0], nullptr, c->g[0], c->u[0].mant, c->u[0].exps, c->wu_cur[0],
-                        c->u[0].stride, c->cf);
-  c->launches++;
-  for (int l = 1; l <= L; ++l) {
-    bool tm = (l == L && L == c->Lmax);
-    if (tm) mark(c, 2, L);
-    launch_prolong_decode(ln, U[l & 1], c->g[l], U[(l - 1) & 1], c->g[l - 1], c->u[l].mant, c->u[l].exps,
-                          c->wu_cur[l], c->u[l].stride, c->cf);
-    if (tm) mark(c, 2, L);
-    c->launches++;
+// fmgResidual (Alg 3.2) at FMG level L, norm row `row`.
+void build_residual(Builder& b, int L, int row) {
+  fmg_ctx* c = b.c;
+  for (int l = 0; l < L; ++l) {  // decode sweep u_0..u_{L-1} (u_L fused into the residual)
+    OpDesc o = mkop(OP_DECODE, l, L);
+    o.wu_in = c->wu_cur[l];
+    b.add(o, b.small(l), l == L - 1 && L == c->Lmax ? 2 : -1);
   }
-  mark(c, 0, L);
-  launch_residual(ln, U[L & 1], T[L & 1], c->g[L], c->gtab[L], c->r[L], wr(c, L, L),
-                  c->partials + c->part_off[L], c->cf, c->status);
-  mark(c, 0, L);
-  c->launches++;
+  OpDesc o = mkop(OP_RESIDUAL, L, L);
+  o.wu_in = c->wu_cur[L];
+  o.wr = wr(c, L, L);
+  b.add(o, b.small(L), L == c->Lmax ? 0 : -1);
   for (int l = L - 1; l >= 0; --l) {
-    bool tm = (l == L - 1);
-    if (tm) mark(c, 3, L);
-    launch_restrict(ln, T[(l + 1) & 1], c->g[l + 1], T[l & 1], c->g[l], c->r[l], wr(c, l, L),
-                    c->partials + c->part_off[l], c->cf, c->status);
-    if (tm) mark(c, 3, L);
-    c->launches++;
+    OpDesc q = mkop(OP_RESTRICT, l, L);
+    q.wr = wr(c, l, L);
+    b.add(q, b.small(l), l == L - 1 && L == c->Lmax ? 3 : -1);
   }
-  launch_norms(c->cur, c->partials, c->part_off, c->part_cnt, L + 1,
-               c->norms_dev + ((size_t)L * c->s.n_ir + it) * c->levels);
-  c->launches++;
+  OpDesc n = mkop(OP_NORMS, 0, L);
+  n.row = row;
+  b.add(n, true);
 }
 
-void record_cfas(fmg_ctx* c, int L) {
-  double* W[2] = {c->buf[0], c->buf[1]};
-  double* Z = c->buf[2];
-  double* B = c->buf[3];
-  double* Y[2] = {c->buf[4], c->buf[5]};
-  double* Dv = c->buf[6];
-  Launch ln = L_(c);
-  launch_coarse(ln, 1, c->g[0], c->gtab[0], c->Ainv, c->n0, c->u[0], c->wu_cur[0], wu(c, 0, L), c->r[0],
-                wr(c, 0, L), W[0], c->cf, c->status);
-  c->launches++;
+// cFas V(0,1) (Alg 3.1, nu = 1) + correction at FMG level L.
+void build_cfas(Builder& b, int L) {
+  fmg_ctx* c = b.c;
+  OpDesc o = mkop(OP_COARSE_CFAS, 0, L);
+  o.wr = wr(c, 0, L);
+  o.wu_in = c->wu_cur[0];
+  o.wu_out = wu(c, 0, L);
+  b.add(o, true);
   c->wu_cur[0] = wu(c, 0, L);
   const int k = c->s.cheb_degree;
   for (int l = 1; l <= L; ++l) {
-    launch_prolong_decode(ln, Z, c->g[l], W[(l - 1) & 1], c->g[l - 1], nullptr, nullptr, 0, 0, c->cf);
-    c->launches++;
     for (int step = 1; step <= k; ++step) {
-      CfasArgs a;
-      a.Z = Z;
-      a.B = B;
-      a.Yin = step == 1 ? nullptr : Y[step & 1];
-      a.Yout = Y[(step - 1) & 1];
-      a.Dv = Dv;
-      a.W = l < L ? W[l & 1] : nullptr;
-      a.r = c->r[l];
-      a.wr = wr(c, l, L);
-      a.u = c->u[l];
-      a.wu_in = c->wu_cur[l];
-      a.wu_out = wu(c, l, L);
-      a.step = step;
-      a.last = step == k;
-      bool tm = (l == L);
-      if (tm) mark(c, 1, L);
-      launch_cfas_step(ln, c->g[l], a, c->cf, c->status);
-      if (tm) mark(c, 1, L);
-      c->launches++;
+      OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
+      q.step = step;
+      q.last = step == k;
+      q.wr = wr(c, l, L);
+      q.wu_in = c->wu_cur[l];
+      q.wu_out = wu(c, l, L);
+      b.add(q, b.small(l), (l == L && L == c->Lmax) ? 1 : -1);
     }
     c->wu_cur[l] = wu(c, l, L);
   }
 }
 
 // Alg 3.3 up to FMG level Lstop (iters_last IR iterations there).
-void record_solve(fmg_ctx* c, int Lstop, int iters_last) {
-  c->launches = 0;
-  c->ev_used = 0;
-  for (int l = 0; l <= c->Lmax; ++l) {
-    cudaMemsetAsync(c->u[l].mant, 0, sizeof(uint32_t) * c->g[l].nblk * c->u[l].stride, c->cur);
-    cudaMemsetAsync(c->u[l].exps, 0x80, c->g[l].nblk, c->cur);
-    c->wu_cur[l] = wu(c, l, l);
-  }
-  cudaMemsetAsync(c->norms_dev, 0, sizeof(double) * c->levels * c->s.n_ir * c->levels, c->cur);
-  // coarse-grid solve PAPER.md:786: ú_0 = reg(A_0^{-1} f_0) at w_u(0,0)
-  launch_coarse(L_(c), 0, c->g[0], c->gtab[0], c->Ainv, c->n0, c->u[0], wu(c, 0, 0), wu(c, 0, 0), c->r[0],
-                wr(c, 0, 0), c->buf[0], c->cf, c->status);
-  c->launches++;
+void build_solve(Builder& b, int Lstop, int iters_last) {
+  fmg_ctx* c = b.c;
+  for (int l = 0; l <= c->Lmax; ++l) c->wu_cur[l] = wu(c, l, l);
+  OpDesc o = mkop(OP_COARSE_INIT, 0, 0);
+  o.wu_out = wu(c, 0, 0);
+  b.add(o, true);  // coarse-grid solve PAPER.md:786
   c->wu_cur[0] = wu(c, 0, 0);
   for (int L = 1; L <= Lstop; ++L) {
-    // push level PAPER.md:788: ú_L = 0 (already zero); widening of ú_{0..L-1}
-    // is value-preserving and happens at the next re-encode.
+    // push level PAPER.md:788: ú_L = 0 (zeroed at solve start); the widening of
+    // ú_{0..L-1} is value-preserving and happens at the next encode.
     c->wu_cur[L] = wu(c, L, L);
     int iters = (L == Lstop) ? iters_last : c->s.n_ir;
     for (int it = 0; it < iters; ++it) {
-      record_residual(c, L, it);
-      record_cfas(c, L);
+      build_residual(b, L, L * c->s.n_ir + it);
+      build_cfas(b, L);
     }
   }
+}
+
+void mark(fmg_ctx* c, int cls) {
+  if (c->timing_cls != cls || cls < 0) return;
+  if (c->ev_used >= (int)c->ev.size()) return;
+  cudaEventRecordWithFlags(c->ev[c->ev_used++], c->cur, cudaEventRecordExternal);
+}
+
+int op_tiles(const fmg_ctx* c, const OpDesc& o) {
+  if (o.type == OP_NORMS || o.type == OP_COARSE_INIT || o.type == OP_COARSE_CFAS) return 1;
+  return c->tiles[o.l][0] * c->tiles[o.l][1] * c->tiles[o.l][2];
+}
+
+// Upload the op program into prog[slot] and issue every item on c->cur.
+int issue(fmg_ctx* c, Builder& b, int slot) {
+  size_t osz = op_size();
+  size_t need = std::max<size_t>(1, b.prog.size()) * osz;
+  if (c->prog_cap[slot] < need) {
+    c->prog[slot] = dalloc(c, need);
+    if (!c->prog[slot]) return FMG_ENOMEM;
+    c->prog_cap[slot] = need;
+  }
+  std::vector<char> host(need);
+  for (size_t i = 0; i < b.prog.size(); ++i) pack_op(host.data() + i * osz, b.prog[i]);
+  cudaError_t e = cudaMemcpy(c->prog[slot], host.data(), need, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return FMG_ECUDA;
+  for (const Item& it : b.items) {
+    if (it.seq) {
+      launch_seq(c->dim, c->p, c->cur, c->devctx, (const char*)c->prog[slot] + it.first * osz, it.count);
+    } else {
+      mark(c, it.timed_cls);
+      launch_op(c->dim, c->p, c->cur, c->devctx, it.op, op_tiles(c, it.op));
+      mark(c, it.timed_cls);
+    }
+    c->launches++;
+  }
+  return FMG_OK;
+}
+
+void zero_sections(fmg_ctx* c) {
+  for (int l = 0; l <= c->Lmax; ++l) {
+    cudaMemsetAsync(c->u[l].mant, 0, sizeof(uint32_t) * c->g[l].nblk * c->u[l].stride, c->cur);
+    cudaMemsetAsync(c->u[l].exps, 0x80, c->g[l].nblk, c->cur);
+  }
+  cudaMemsetAsync(c->norms_dev, 0, sizeof(double) * c->levels * c->s.n_ir * c->levels, c->cur);
 }
 
 int cuda_err(cudaError_t e) {
@@ -204,6 +259,8 @@ int cuda_err(cudaError_t e) {
 int sync_check(fmg_ctx* c) {
   cudaError_t e = cudaStreamSynchronize(c->st);
   if (e != cudaSuccess) return cuda_err(e);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_err(e);
   int st = 0;
   e = cudaMemcpy(&st, c->status, sizeof(int), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_err(e);
@@ -212,6 +269,20 @@ int sync_check(fmg_ctx* c) {
     return FMG_ERANGE;
   }
   return FMG_OK;
+}
+
+// Run a freshly built program directly on the user stream (no graph).
+int run_direct(fmg_ctx* c, Builder& b) {
+  c->cur = c->st;
+  int save = c->timing_cls;
+  long long save_l = c->launches;
+  c->timing_cls = -1;
+  cudaStreamSynchronize(c->st);  // prog[1] may still be read by earlier work
+  int rc = issue(c, b, 1);
+  c->timing_cls = save;
+  c->launches = save_l;
+  if (rc) return rc;
+  return sync_check(c);
 }
 
 }  // namespace
@@ -242,8 +313,14 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) { delete c; return FMG_ECUDA; }
   set_kernel_attributes();
   build_coefs(dim, p, s->lambda_hi, s->alpha, s->cheb_degree, &c->cf);
+  int TY, TZ;
+  tile_shape(dim, p, &TY, &TZ);
+  // sequencer threshold: levels with at most `seq_tiles` tiles (env FMG_SEQ_TILES)
+  int seq_tiles = 2;
+  if (const char* e = getenv("FMG_SEQ_TILES")) seq_tiles = atoi(e);
   int rc = FMG_OK;
   long long tot_parts = 0;
+  DevCtxDesc dd{};
   for (int l = 0; l <= Lmax; ++l) {
     Geom& g = c->g[l];
     g.l = l;
@@ -253,6 +330,11 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     g.NZ = dim == 3 ? g.n : 1;
     g.size = (long long)g.NX * g.NY * g.NZ;
     g.nblk = g.size / 32;
+    c->tiles[l][0] = g.NX / 32;
+    c->tiles[l][1] = (g.NY + TY - 1) / TY;
+    c->tiles[l][2] = (g.NZ + TZ - 1) / TZ;
+    int nt = c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2];
+    if (nt <= seq_tiles) c->seq_max_level = l;
     c->u[l].stride = wu(c, l, Lmax);
     c->r[l].stride = wr(c, l, Lmax);
     c->u[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->u[l].stride);
@@ -264,12 +346,13 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     std::vector<double> gt(g.n);
     build_rhs_table(p, l, gt.data());
     cudaMemcpy(c->gtab[l], gt.data(), sizeof(double) * g.n, cudaMemcpyHostToDevice);
-    c->part_cnt[l] = tile_count(dim, p, 0, g);
     c->part_off[l] = tot_parts;
-    tot_parts += c->part_cnt[l];
+    tot_parts += nt;
   }
+  // FP64 workspace (finest size): U/W ping-pong, T ping-pong / Z, B; Y ping-pong + D (k >= 3)
+  int nbuf = s->cheb_degree >= 3 ? 7 : 4;
   if (rc == FMG_OK) {
-    for (int i = 0; i < 7 && rc == FMG_OK; ++i) {
+    for (int i = 0; i < nbuf && rc == FMG_OK; ++i) {
       c->buf[i] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
       if (!c->buf[i]) rc = FMG_ENOMEM;
     }
@@ -283,11 +366,37 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     c->norms_dev = (double*)dalloc(c, sizeof(double) * levels * s->n_ir * levels);
     c->err_part = (double*)dalloc(c, sizeof(double) * 2 * 148 * 16);
     c->status = (int*)dalloc(c, sizeof(int));
-    if (!c->Ainv || !c->partials || !c->norms_dev || !c->err_part || !c->status) rc = FMG_ENOMEM;
+    c->devctx = dalloc(c, devctx_size());
+    if (!c->Ainv || !c->partials || !c->norms_dev || !c->err_part || !c->status || !c->devctx) rc = FMG_ENOMEM;
     else {
       cudaMemcpy(c->Ainv, Ai.data(), sizeof(double) * Ai.size(), cudaMemcpyHostToDevice);
       cudaMemset(c->status, 0, sizeof(int));
       cudaMemset(c->norms_dev, 0, sizeof(double) * levels * s->n_ir * levels);
+      dd.levels = levels;
+      dd.n_ir = s->n_ir;
+      dd.n0 = c->n0;
+      for (int l = 0; l <= Lmax; ++l) {
+        dd.g[l] = c->g[l];
+        dd.u[l] = c->u[l];
+        dd.r[l] = c->r[l];
+        dd.gtab[l] = c->gtab[l];
+        for (int k = 0; k < 3; ++k) dd.tiles[l][k] = c->tiles[l][k];
+        dd.part[l] = c->partials + c->part_off[l];
+      }
+      dd.U[0] = dd.W[0] = c->buf[0];
+      dd.U[1] = dd.W[1] = c->buf[1];
+      dd.T[0] = dd.Z = c->buf[2];
+      dd.T[1] = dd.B = c->buf[3];
+      dd.Y[0] = c->buf[4];
+      dd.Y[1] = c->buf[5];
+      dd.Dv = c->buf[6];
+      dd.Ainv = c->Ainv;
+      dd.norms = c->norms_dev;
+      dd.status = c->status;
+      dd.cf = c->cf;
+      std::vector<char> host(devctx_size());
+      fill_devctx(host.data(), dd);
+      cudaMemcpy(c->devctx, host.data(), host.size(), cudaMemcpyHostToDevice);
     }
   }
   if (rc == FMG_OK) rc = cuda_err(cudaDeviceSynchronize());
@@ -302,10 +411,35 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
 int fmg_solve_async(fmg_ctx* c) {
   if (!c) return FMG_EINVAL;
   if (!c->graph) {
+    Builder b{c, {}, {}};
+    c->launches = 0;
+    c->ev_used = 0;
+    build_solve(b, c->Lmax, c->s.n_ir);
     c->cur = c->cap;
+    // upload the op program first (outside the capture)
+    size_t osz = op_size();
+    size_t need = std::max<size_t>(1, b.prog.size()) * osz;
+    if (c->prog_cap[0] < need) {
+      c->prog[0] = dalloc(c, need);
+      if (!c->prog[0]) return FMG_ENOMEM;
+      c->prog_cap[0] = need;
+    }
+    std::vector<char> host(need);
+    for (size_t i = 0; i < b.prog.size(); ++i) pack_op(host.data() + i * osz, b.prog[i]);
+    if (cudaMemcpy(c->prog[0], host.data(), need, cudaMemcpyHostToDevice) != cudaSuccess) return FMG_ECUDA;
     cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return cuda_err(e);
-    record_solve(c, c->Lmax, c->s.n_ir);
+    zero_sections(c);
+    for (const Item& it : b.items) {
+      if (it.seq) {
+        launch_seq(c->dim, c->p, c->cur, c->devctx, (const char*)c->prog[0] + it.first * osz, it.count);
+      } else {
+        mark(c, it.timed_cls);
+        launch_op(c->dim, c->p, c->cur, c->devctx, it.op, op_tiles(c, it.op));
+        mark(c, it.timed_cls);
+      }
+      c->launches++;
+    }
     cudaGraph_t gr;
     e = cudaStreamEndCapture(c->cap, &gr);
     if (e != cudaSuccess) return cuda_err(e);
@@ -316,6 +450,7 @@ int fmg_solve_async(fmg_ctx* c) {
   cudaError_t e = cudaGraphLaunch(c->graph, c->st);
   if (e != cudaSuccess) return cuda_err(e);
   c->solved_L = c->Lmax;
+  // wu_cur reflects the end of a full solve (build_solve left it there)
   return FMG_OK;
 }
 
@@ -327,13 +462,13 @@ int fmg_solve(fmg_ctx* c) {
 
 int fmg_solve_upto(fmg_ctx* c, int Lstop, int iters_last) {
   if (!c || Lstop < 0 || Lstop > c->Lmax || iters_last < 0) return FMG_EINVAL;
+  Builder b{c, {}, {}};
   c->cur = c->st;
-  int save = c->timing_cls;
-  c->timing_cls = -1;
-  record_solve(c, Lstop, iters_last);
-  c->timing_cls = save;
+  cudaStreamSynchronize(c->st);
+  zero_sections(c);
+  build_solve(b, Lstop, iters_last);
   c->solved_L = Lstop;
-  return sync_check(c);
+  return run_direct(c, b);
 }
 
 int fmg_norms(fmg_ctx* c, double* host) {
@@ -348,18 +483,15 @@ int fmg_residual(fmg_ctx* c, double* host_norms) {
   if (!c) return FMG_EINVAL;
   if (c->solved_L < 0) return FMG_ESTATE;
   int L = c->solved_L;
-  c->cur = c->st;
-  int save = c->timing_cls;
-  c->timing_cls = -1;
-  // Use row (L, it = 0) of a scratch region: the last norm row of the log is
-  // preserved by copying it around the call.
+  if (L < 1) return FMG_ESTATE;
+  // Runs into norm row (L*n_ir) and restores the log afterwards.
   std::vector<double> keep(c->levels);
   double* row = c->norms_dev + ((size_t)L * c->s.n_ir) * c->levels;
-  cudaMemcpyAsync(keep.data(), row, sizeof(double) * c->levels, cudaMemcpyDeviceToHost, c->st);
   cudaStreamSynchronize(c->st);
-  record_residual(c, L, 0);
-  c->timing_cls = save;
-  int rc = sync_check(c);
+  cudaMemcpy(keep.data(), row, sizeof(double) * c->levels, cudaMemcpyDeviceToHost);
+  Builder b{c, {}, {}};
+  build_residual(b, L, L * c->s.n_ir);
+  int rc = run_direct(c, b);
   if (rc) return rc;
   if (host_norms) {
     std::vector<double> tmp(c->levels, 0.0);
@@ -370,23 +502,25 @@ int fmg_residual(fmg_ctx* c, double* host_norms) {
   return FMG_OK;
 }
 
-static int decode_solution(fmg_ctx* c) {
+// û_L into U[L & 1] (decode ops for l = 0..L, materialised).
+static int decode_solution(fmg_ctx* c, int* which) {
   int L = c->solved_L;
-  c->cur = c->st;
-  Launch ln = L_(c);
-  double* U[2] = {c->buf[0], c->buf[1]};
-  launch_prolong_decode(ln, U[0], c->g[0], nullptr, c->g[0], c->u[0].mant, c->u[0].exps, c->wu_cur[0],
-                        c->u[0].stride, c->cf);
-  for (int l = 1; l <= L; ++l)
-    launch_prolong_decode(ln, U[l & 1], c->g[l], U[(l - 1) & 1], c->g[l - 1], c->u[l].mant, c->u[l].exps,
-                          c->wu_cur[l], c->u[l].stride, c->cf);
-  return L & 1;
+  Builder b{c, {}, {}};
+  for (int l = 0; l <= L; ++l) {
+    OpDesc o = mkop(OP_DECODE, l, L);
+    o.wu_in = c->wu_cur[l];
+    b.add(o, b.small(l));
+  }
+  *which = L & 1;
+  return run_direct(c, b);
 }
 
 int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
   if (!c || !dst_dev) return FMG_EINVAL;
   if (c->solved_L < 0) return FMG_ESTATE;
-  int which = decode_solution(c);
+  int which = 0;
+  int rc = decode_solution(c, &which);
+  if (rc) return rc;
   cudaMemcpyAsync(dst_dev, c->buf[which], sizeof(double) * c->g[c->solved_L].size, cudaMemcpyDeviceToDevice,
                   c->st);
   return sync_check(c);
@@ -395,10 +529,13 @@ int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
 int fmg_errors(fmg_ctx* c, double* err3) {
   if (!c || !err3) return FMG_EINVAL;
   if (c->solved_L < 0) return FMG_ESTATE;
-  int which = decode_solution(c);
+  int which = 0;
+  int rc = decode_solution(c, &which);
+  if (rc) return rc;
   int np = 0;
+  c->cur = c->st;
   launch_errors(L_(c), c->buf[which], c->g[c->solved_L], c->err_part, &np);
-  int rc = sync_check(c);
+  rc = sync_check(c);
   if (rc) return rc;
   std::vector<double> h(2 * np);
   cudaMemcpy(h.data(), c->err_part, sizeof(double) * 2 * np, cudaMemcpyDeviceToHost);

@@ -3,6 +3,7 @@
 // shared with oracle/.
 #pragma once
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 namespace fmg {
@@ -18,7 +19,7 @@ struct Geom {
   int l;            // level index
 };
 
-// Operator tables (passed by value to kernels -> constant bank).
+// Operator tables (correctly rounded doubles of exact rationals).
 struct Coefs {
   double Kc[3][7];    // assembled 1D stiffness rows (reference, h-free) by node type, offsets -p..p
   double Mc[3][7];    // assembled 1D mass rows
@@ -34,7 +35,7 @@ struct Coefs {
 struct Sec {
   uint32_t* mant;
   int8_t* exps;
-  int stride;         // words per block slot (max width over the solve)
+  int stride;
 };
 
 // Host-side table builders (fmg_tables.cpp).
@@ -43,37 +44,46 @@ void build_rhs_table(int p, int l, double* g);       // g[0..n-1]
 int coarse_count(int dim, int p);
 int build_coarse_inverse(int dim, int p, double* Ainv);  // 0 on success
 
-// Kernel launchers (fmg_kernels.cu).  All asynchronous on `st`.
+// Operation descriptors (mirrors the device Op).
+enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_COARSE_INIT, OP_COARSE_CFAS, OP_CFAS1, OP_CHEB };
+struct OpDesc {
+  int type, l, L, step, last;
+  int wr, wu_in, wu_out;
+  int row;
+};
+
+// Everything the device context needs.
+struct DevCtxDesc {
+  int levels, n_ir, n0;
+  Geom g[kMaxLev];
+  Sec u[kMaxLev], r[kMaxLev];
+  const double* gtab[kMaxLev];
+  int tiles[kMaxLev][3];
+  double* part[kMaxLev];
+  double *U[2], *T[2], *W[2], *Y[2];
+  double *Z, *B, *Dv;
+  const double* Ainv;
+  double* norms;
+  int* status;
+  Coefs cf;
+};
+
 struct Launch {
   int dim, p;
   cudaStream_t st;
 };
-void launch_prolong_decode(const Launch& L, double* out, const Geom& gf, const double* coarse,
-                           const Geom& gc, const uint32_t* mant, const int8_t* exps, int w,
-                           int stride, const Coefs& cf);
-void launch_residual(const Launch& L, const double* U, double* T, const Geom& g, const double* gtab,
-                     Sec r, int wr, double* partials, const Coefs& cf, int* status);
-void launch_restrict(const Launch& L, const double* Tf, const Geom& gf, double* Tc, const Geom& gc,
-                     Sec r, int wr, double* partials, const Coefs& cf, int* status);
-void launch_coarse(const Launch& L, int mode, const Geom& g0, const double* gtab0, const double* Ainv,
-                   int n0, Sec u, int wu_in, int wu_out, Sec r, int wr, double* W0, const Coefs& cf,
-                   int* status);
-// cFas level kernels.  step = 1: b = dec r - A Z, first Chebyshev step.
-// step >= 2: q = B - A Yin.  finalize (last step): encode ý, W = Z + dec ý,
-// ú <- enc(dec ú + dec ý).
-struct CfasArgs {
-  const double* Z; double* B; const double* Yin; double* Yout; double* Dv;
-  double* W;  // may be null (finest level)
-  Sec r; int wr;
-  Sec u; int wu_in, wu_out;
-  int step, last;
-};
-void launch_cfas_step(const Launch& L, const Geom& g, const CfasArgs& a, const Coefs& cf, int* status);
-void launch_norms(cudaStream_t st, const double* partials, const long long* offs, const int* counts,
-                  int nlev, double* out);
-int tile_count(int dim, int p, int kind, const Geom& g);  // CTAs of residual (0) / restrict (1)
-void launch_errors(const Launch& L, const double* U, const Geom& g, double* partials, int* nparts);
+
+// Kernel side (fmg_kernels.cu).
 void set_kernel_attributes();
+int smem_bytes(int dim, int p);
+void tile_shape(int dim, int p, int* TY, int* TZ);
+size_t devctx_size();
+size_t op_size();
+void fill_devctx(void* host_buf, const DevCtxDesc& d);
+void pack_op(void* dst, const OpDesc& od);
+void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int ntiles);
+void launch_seq(int dim, int p, cudaStream_t st, const void* devctx, const void* prog_dev, int count);
+void launch_errors(const Launch& L, const double* U, const Geom& g, double* partials, int* nparts);
 void launch_bfp_encode(const double* x, long long n, int w, uint32_t* mant, int8_t* exps, int* status,
                        cudaStream_t st);
 void launch_bfp_decode(const uint32_t* mant, const int8_t* exps, long long n, int w, double* x,

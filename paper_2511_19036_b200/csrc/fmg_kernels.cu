@@ -1,36 +1,49 @@
 // fmg_kernels.cu -- sm_100a kernels of the compact-FMG hot path.
 //
-// Every floating-point expression follows the canonical evaluation order of
-// DESIGN.md §3 with explicit fma(); the file is compiled with -fmad=false so no
-// other contraction happens.  Tensor-product operators are applied factor by
-// factor (sum factorisation) on shared-memory tiles: x pass, then y, then z.
+// Structure: every step of the method is a *tile operation* (a __device__
+// function that produces one output tile of one level: 32 x TY (x TZ) points,
+// 256 threads, one warp per 32-entry x row = one BFP block).  A step is
+// executed either by a grid kernel (one CTA per tile, `k_op`) or, for the
+// small levels, inside a single-CTA sequencer kernel (`k_seq`) that runs a
+// list of operations back to back with __syncthreads between them (no launch
+// gaps).  All kernels use programmatic dependent launch (griddepcontrol).
 //
-// Paper passages: BFP codec PAPER.md:1240-1274 with RNE; decode
-// sweep / residual / truncate / restriction of fmgResidual (Alg 3.2,
-// PAPER.md:713-748); cFas coarse-to-fine sweep (Alg 3.1, nu = 1
-// so s = 0) fused with the correction (Alg 3.3).
+// Every floating-point expression follows the canonical evaluation order of
+// DESIGN.md §3 with explicit fma(); compiled with -fmad=false.  Tensor-product
+// operators are applied factor by factor in shared memory: x pass, y, z.
+//
+// Paper: BFP codec PAPER.md:1240-1274 with RNE; decode sweep /
+// residual / truncate / restriction = fmgResidual (Alg 3.2);
+// coarse-to-fine sweep of cFas (Alg 3.1, nu = 1 so s = 0,
+// PAPER.md:809-812) fused with the correction (Alg 3.3).
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 
 #include "fmg_internal.h"
 
 namespace fmg {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int NWARP = 8;  // warps per CTA of every tiled kernel
+constexpr int NWARP = 8;
+constexpr int NT = 32 * NWARP;
 
-// Exact 2^k for k in [-1022, 1023].
-__device__ __forceinline__ double pow2(int k) {
+__device__ __forceinline__ double pow2(int k) {  // exact 2^k, k in [-1022, 1023]
   return __longlong_as_double((long long)(k + 1023) << 52);
 }
+__device__ __forceinline__ bool unk1(int i, int n) { return i >= 1 && i <= n - 1; }
+__device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ----------------------------------------------------------------- codec --
-// Warp-cooperative decode: lane j returns entry j of the block whose `w` words
-// start at `words`.  Must be called by all 32 lanes.
-__device__ __forceinline__ double warp_decode(const uint32_t* __restrict__ words, int E, int w, int lane) {
-  uint32_t my0 = lane < w ? __ldg(words + lane) : 0u;
+// Warp-cooperative decode: lane j returns entry j of the block whose w words
+// start at `words`.  All 32 lanes must call.
+__device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int w, int lane) {
+  uint32_t my0 = lane < w ? words[lane] : 0u;
   uint32_t my1 = 0u;
-  if (w > 32) my1 = lane + 32 < w ? __ldg(words + lane + 32) : 0u;
+  if (w > 32) my1 = lane + 32 < w ? words[lane + 32] : 0u;
   int o = lane * w, j0 = o >> 5, s = o & 31;
   uint32_t w0, w1, w2;
   if (w <= 32) {
@@ -48,16 +61,27 @@ __device__ __forceinline__ double warp_decode(const uint32_t* __restrict__ words
   unsigned long long lo = (unsigned long long)w0 | ((unsigned long long)w1 << 32);
   unsigned long long field = lo >> s;
   if (s + w > 64) field |= (unsigned long long)w2 << (64 - s);
-  long long m = (long long)(field << (64 - w)) >> (64 - w);  // sign-extend w bits
+  long long m = (long long)(field << (64 - w)) >> (64 - w);
   return (double)m * pow2(E - (w - 1));
 }
 
-// Warp-cooperative encode of one 32-entry block (R8); lane j holds
-// entry j.  Writes the w words and the exponent (if `words` is non-null) and
-// returns the quantised value m 2^(E-q) of this lane's entry.  Non-finite input
-// or E > 127 sets *status (FMG_ERANGE) and stores a zero block.
-__device__ __forceinline__ double warp_encode(double v, int w, uint32_t* __restrict__ words,
-                                              int8_t* __restrict__ eptr, int lane, int* status) {
+// Single-entry decode (entry j of a block), for halo points.
+__device__ __forceinline__ double point_decode(const uint32_t* words, int E, int w, int j) {
+  int o = j * w, j0 = o >> 5, s = o & 31;
+  int jl = (o + w - 1) >> 5;
+  unsigned long long lo = words[j0];
+  if (jl > j0) lo |= (unsigned long long)words[j0 + 1] << 32;
+  unsigned long long field = lo >> s;
+  if (jl > j0 + 1) field |= (unsigned long long)words[j0 + 2] << (64 - s);
+  long long m = (long long)(field << (64 - w)) >> (64 - w);
+  return (double)m * pow2(E - (w - 1));
+}
+
+// Warp-cooperative encode of one block; lane j holds entry j.
+// Writes the w words and the exponent when `words` is non-null; returns the
+// quantised value m 2^(E-q).  Non-finite input or E > 127 sets *status.
+__device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, int8_t* eptr, int lane,
+                                              int* status) {
   unsigned long long bits = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
   bool bad = bits >= 0x7ff0000000000000ULL;
   unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
@@ -107,302 +131,471 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* __restr
   return E == -128 ? 0.0 : (double)m * pow2(E - q);
 }
 
-// --------------------------------------------------------------- tiles ----
+// ------------------------------------------------------------ tile plans --
 template <int D, int P> struct TileCfg;
 template <int P> struct TileCfg<2, P> { static constexpr int TY = 16, TZ = 1; };
 template <> struct TileCfg<3, 1> { static constexpr int TY = 8, TZ = 4; };
 template <> struct TileCfg<3, 2> { static constexpr int TY = 4, TZ = 4; };
 template <> struct TileCfg<3, 3> { static constexpr int TY = 4, TZ = 4; };
 
-// Shared-memory plan of the A-apply tile (output 32 x TY x TZ).
-template <int D, int P> struct ATile {
+template <int D, int P> struct Plan {
   static constexpr int TY = TileCfg<D, P>::TY, TZ = TileCfg<D, P>::TZ;
+  static constexpr int T = 2 * P + 1;  // A taps
+  // A tile: input box (output + P halo), x-pass out, y-pass out (3D)
   static constexpr int BX = 32 + 2 * P, BY = TY + 2 * P, BZ = (D == 3) ? TZ + 2 * P : 1;
-  static constexpr int NU = BX * BY * BZ;          // input box
-  static constexpr int NAB = 32 * BY * BZ;         // x-pass outputs a = Mx u, b = Kx u
-  static constexpr int NCS = (D == 3) ? 32 * TY * BZ : 0;  // y-pass outputs c, s
-  static constexpr int SMEM = (NU + 2 * NAB + 2 * NCS) * 8;
-};
-
-// Shared-memory plan of the restriction tile (coarse output 32 x TY x TZ).
-template <int D, int P> struct RTile {
-  static constexpr int TY = TileCfg<D, P>::TY, TZ = TileCfg<D, P>::TZ;
+  static constexpr int NU = BX * BY * BZ;
+  static constexpr int NAB = 32 * BY * BZ;
+  static constexpr int NCS = (D == 3) ? 32 * TY * BZ : 0;
+  // coarse box feeding a prolongation onto the input box
+  static constexpr int CBX = P * ((BX - 1) / (2 * P) + 2) + 1;
+  static constexpr int CBY = P * ((BY - 1) / (2 * P) + 2) + 1;
+  static constexpr int CBZ = (D == 3) ? P * ((BZ - 1) / (2 * P) + 2) + 1 : 1;
+  static constexpr int NCB = CBX * CBY * CBZ;
+  static constexpr int NV1 = BX * CBY * CBZ;              // P x-pass out
+  static constexpr int NV2 = (D == 3) ? BX * BY * CBZ : 0; // P y-pass out (3D)
+  static constexpr int PRO_REGION = NCB + NV1 + NV2;
+  static constexpr int A_REGION = 2 * NAB + 2 * NCS;
+  static constexpr int A_SMEM = (NU + (PRO_REGION > A_REGION ? PRO_REGION : A_REGION)) * 8;
+  // decode/prolong tile (output only, no halo)
+  static constexpr int DBX = 32, DBY = TY, DBZ = (D == 3) ? TZ : 1;
+  static constexpr int DCBX = P * ((DBX - 1) / (2 * P) + 2) + 1;
+  static constexpr int DCBY = P * ((DBY - 1) / (2 * P) + 2) + 1;
+  static constexpr int DCBZ = (D == 3) ? P * ((DBZ - 1) / (2 * P) + 2) + 1 : 1;
+  static constexpr int D_SMEM = (DCBX * DCBY * DCBZ + DBX * DCBY * DCBZ + ((D == 3) ? DBX * DBY * DCBZ : 0)) * 8;
+  // restriction tile (coarse output 32 x TY x TZ); x pass gathered from global
   static constexpr int FBY = 2 * TY + 4 * P - 3, FBZ = (D == 3) ? 2 * TZ + 4 * P - 3 : 1;
-  static constexpr int NX = 32 * FBY * FBZ;         // x-pass outputs
-  static constexpr int NYR = (D == 3) ? 32 * TY * FBZ : 0;  // y-pass outputs
-  static constexpr int SMEM = (NX + NYR) * 8;
+  static constexpr int NXR = 32 * FBY * FBZ;
+  static constexpr int NYR = (D == 3) ? 32 * TY * FBZ : 0;
+  static constexpr int R_SMEM = (NXR + NYR) * 8;
+  static constexpr int C_SMEM = 2 * ((D == 3) ? 4 * P * P : 2 * P) * 32 * 8;  // coarse solve
+  static constexpr int mx2(int a, int b) { return a > b ? a : b; }
+  static constexpr int SMEM = mx2(mx2(A_SMEM, D_SMEM), mx2(R_SMEM, C_SMEM));
 };
 
-__device__ __forceinline__ bool unk1(int i, int n) { return i >= 1 && i <= n - 1; }
+// ------------------------------------------------------------- contexts --
+// Device-side context (lives in global memory, built by fmg_api.cpp).
+struct LevelDev {
+  Geom g;
+  uint32_t* umant;
+  int8_t* uexp;
+  int ustride;
+  uint32_t* rmant;
+  int8_t* rexp;
+  int rstride;
+  const double* gtab;
+  int tx, ty, tz;  // tile grid of this level
+  double* part;    // norm partials, one per tile
+};
 
-// Stages of A applied to the box around output tile (x0,y0,z0) of `src`
-// (DESIGN.md §3.2): load u, x pass (a = Mx u, b = Kx u), y pass (3D: c = My a,
-// s = Ky a + My b).  The last pass is done per output point by atile_final.
-template <int D, int P>
-__device__ void atile_stages(const double* __restrict__ src, const Geom& g, int x0, int y0, int z0,
-                             const Coefs& cf, double* sm) {
-  using T = ATile<D, P>;
-  double* U = sm;
-  double* A = U + T::NU;
-  double* B = A + T::NAB;
-  double* C = B + T::NAB;
-  double* S = C + T::NCS;
-  const int tid = threadIdx.y * 32 + threadIdx.x, nt = 32 * NWARP;
-  for (int i = tid; i < T::NU; i += nt) {
-    int bx = i % T::BX, r = i / T::BX, by = r % T::BY, bz = r / T::BY;
-    int gx = x0 - P + bx, gy = y0 - P + by, gz = (D == 3) ? z0 - P + bz : 0;
-    double v = 0.0;
-    if (gx >= 0 && gx < g.NX && gy >= 0 && gy < g.NY && gz >= 0 && gz < g.NZ)
-      v = src[((long long)gz * g.NY + gy) * g.NX + gx];
-    U[i] = v;
+struct DevCtx {
+  LevelDev lv[kMaxLev];
+  double* U[2];  // decoded u_l (ping-pong by level parity)
+  double* T[2];  // residual temporaries t_l
+  double* W[2];  // w_l = z_l + dec ý_l
+  double* Z;     // z_l (only for l < L)
+  double* B;     // b_l = dec r_l - A z_l
+  double* Y[2];  // Chebyshev iterates (k >= 3)
+  double* Dv;    // Chebyshev direction (k >= 3)
+  const double* Ainv;
+  int n0;
+  double* norms;
+  int levels, n_ir;
+  int* status;
+  Coefs cf;
+};
+
+using Op = OpDesc;  // one step of the method on one level (fmg_internal.h)
+
+__device__ __forceinline__ int op_tiles(const DevCtx& c, const Op& op) {
+  const LevelDev& lv = c.lv[op.l];
+  if (op.type == OP_NORMS || op.type == OP_COARSE_INIT || op.type == OP_COARSE_CFAS) return 1;
+  return lv.tx * lv.ty * lv.tz;
+}
+
+// ------------------------------------------------ prolongation onto a box --
+// out[bz][by][bx] = (P_lf coarse)(fx0+bx, fy0+by, fz0+bz) over a box of
+// NBX x NBY x NBZ fine points, canonical x, y, z passes; 0 at
+// fine non-unknowns.  Scratch: cb (coarse box), v1, v2.  Lanes own x columns
+// (weights in registers), warps own rows (row-uniform weights).
+template <int D, int P, int NBX, int NBY, int NBZ, int NCX, int NCY, int NCZ>
+__device__ void box_prolong(const double* __restrict__ coarse, const Geom& gc, int nf, int fx0, int fy0, int fz0,
+                            const Coefs& cf, double* cb, double* v1, double* v2, double* out) {
+  static_assert(NCX <= 32, "coarse box wider than a warp");
+  const int lane = threadIdx.x, wid = threadIdx.y;
+  const int nc = gc.n;
+  const int cx0 = P * floordiv(fx0, 2 * P), cy0 = P * floordiv(fy0, 2 * P);
+  const int cz0 = (D == 3) ? P * floordiv(fz0, 2 * P) : 0;
+  {
+    const int gx = cx0 + lane;
+    const bool okx = lane < NCX && gx >= 0 && gx < nc;
+    for (int r = wid; r < NCY * NCZ; r += NWARP) {
+      int gy = cy0 + r % NCY, gz = cz0 + r / NCY;
+      bool ok = okx && gy >= 0 && gy < nc && (D == 2 || (gz >= 0 && gz < nc));
+      double v = ok ? coarse[((long long)gz * gc.NY + gy) * gc.NX + gx] : 0.0;
+      if (lane < NCX) cb[r * NCX + lane] = v;
+    }
   }
   __syncthreads();
-  for (int i = tid; i < T::NAB; i += nt) {
-    int lx = i & 31, r = i >> 5;
-    int gx = x0 + lx;
-    double a = 0.0, b = 0.0;
-    if (unk1(gx, g.n)) {
-      int tau = gx % P;
-      const double* u = U + r * T::BX + lx;
+  // x pass: v1[cz][cy][bx]; columns bx = lane and lane + 32
+  {
+    constexpr int NCOL = (NBX + 31) / 32;
+    double w[NCOL][P + 1];
+    int base[NCOL];
+    bool ok[NCOL];
 #pragma unroll
-      for (int o = 0; o <= 2 * P; ++o) {
-        a = fma(cf.Mc[tau][o], u[o], a);
-        b = fma(cf.Kc[tau][o], u[o], b);
+    for (int k = 0; k < NCOL; ++k) {
+      int bx = lane + 32 * k;
+      int x = fx0 + bx;
+      ok[k] = bx < NBX && unk1(x, nf);
+      int rx = ok[k] ? x % (2 * P) : 0;
+      base[k] = ok[k] ? P * (x / (2 * P)) - cx0 : 0;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) w[k][t] = cf.Pw[rx][t];
+    }
+    for (int r = wid; r < NCY * NCZ; r += NWARP) {
+      const double* src = cb + r * NCX;
+#pragma unroll
+      for (int k = 0; k < NCOL; ++k) {
+        int bx = lane + 32 * k;
+        if (bx >= NBX) break;
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t <= P; ++t) acc = fma(w[k][t], src[base[k] + t], acc);
+        v1[r * NBX + bx] = ok[k] ? acc : 0.0;
       }
     }
-    A[i] = a;
-    B[i] = b;
+  }
+  __syncthreads();
+  // y pass (rows (cz, by), weights row-uniform)
+  double* yout = (D == 3) ? v2 : out;
+  for (int r = wid; r < NBY * NCZ; r += NWARP) {
+    int by = r % NBY, cz = r / NBY;
+    int y = fy0 + by;
+    bool ok = unk1(y, nf);
+    int ry = ok ? y % (2 * P) : 0, base = ok ? P * (y / (2 * P)) - cy0 : 0;
+    double w[P + 1];
+#pragma unroll
+    for (int t = 0; t <= P; ++t) w[t] = cf.Pw[ry][t];
+    const double* src = v1 + (cz * NCY + base) * NBX;
+    for (int bx = lane; bx < NBX; bx += 32) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) acc = fma(w[t], src[t * NBX + bx], acc);
+      yout[r * NBX + bx] = ok ? acc : 0.0;
+    }
+  }
+  if constexpr (D == 3) {
+    __syncthreads();
+    for (int r = wid; r < NBY * NBZ; r += NWARP) {
+      int by = r % NBY, bz = r / NBY;
+      int z = fz0 + bz;
+      bool ok = unk1(z, nf);
+      int rz = ok ? z % (2 * P) : 0, base = ok ? P * (z / (2 * P)) - cz0 : 0;
+      double w[P + 1];
+#pragma unroll
+      for (int t = 0; t <= P; ++t) w[t] = cf.Pw[rz][t];
+      const double* src = v2 + (base * NBY + by) * NBX;
+      for (int bx = lane; bx < NBX; bx += 32) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t <= P; ++t) acc = fma(w[t], src[t * NBY * NBX + bx], acc);
+        out[r * NBX + bx] = ok ? acc : 0.0;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Adds dec(section) to the box rows (in place): box covers fine x in
+// [bx0, bx0+NBX) = [x0-H, x0+32+H) and rows (y, z); 0 outside the stored level.
+template <int D, int NBX, int NBY, int NBZ, int H>
+__device__ void box_add_decode(const LevelDev& lv, int w, int x0, int y0b, int z0b, double* box) {
+  const int lane = threadIdx.x;
+  const Geom& g = lv.g;
+  const int nxb = g.NX >> 5, xb = x0 >> 5;
+  for (int r = threadIdx.y; r < NBY * NBZ; r += NWARP) {
+    int by = r % NBY, bz = r / NBY;
+    int gy = y0b + by, gz = (D == 3) ? z0b + bz : 0;
+    if (gy < 0 || gy >= g.NY || gz < 0 || gz >= g.NZ) continue;  // warp-uniform
+    long long rowblk = ((long long)gz * g.NY + gy) * nxb;
+    long long blk = rowblk + xb;
+    double dv = warp_decode(lv.umant + blk * lv.ustride, lv.uexp[blk], w, lane);
+    double* brow = box + r * NBX;
+    brow[H + lane] = dv + brow[H + lane];
+    if (H > 0 && lane < 2 * H) {
+      int xl = lane < H ? x0 - H + lane : x0 + 32 + (lane - H);
+      if (xl >= 0 && xl < g.NX) {
+        long long b2 = rowblk + (xl >> 5);
+        double d2 = point_decode(lv.umant + b2 * lv.ustride, lv.uexp[b2], w, xl & 31);
+        int bx = lane < H ? lane : 32 + lane;
+        brow[bx] = d2 + brow[bx];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ A on a tile --
+// Given the input box U (output tile + P halo) in smem, computes the x pass
+// (a = Mx u, b = Kx u) and, in 3D, the y pass (c = My a, s = Ky a + My b)
+// (DESIGN.md §3.2).  The last pass is done per output point by a_final.
+template <int D, int P>
+__device__ void a_stages(const Geom& g, int x0, int y0, const Coefs& cf, const double* U, double* AB, double* CS) {
+  using PL = Plan<D, P>;
+  const int lane = threadIdx.x, wid = threadIdx.y;
+  double* A = AB;
+  double* B = AB + PL::NAB;
+  // x pass: lane = output x column (node type fixed per thread -> registers)
+  {
+    const int gx = x0 + lane;
+    const bool ok = unk1(gx, g.n);
+    const int tau = ok ? gx % P : 0;
+    double km[PL::T], kk[PL::T];
+#pragma unroll
+    for (int o = 0; o < PL::T; ++o) {
+      km[o] = cf.Mc[tau][o];
+      kk[o] = cf.Kc[tau][o];
+    }
+    for (int r = wid; r < PL::BY * PL::BZ; r += NWARP) {
+      const double* u = U + r * PL::BX + lane;
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int o = 0; o < PL::T; ++o) {
+        a = fma(km[o], u[o], a);
+        b = fma(kk[o], u[o], b);
+      }
+      A[r * 32 + lane] = ok ? a : 0.0;
+      B[r * 32 + lane] = ok ? b : 0.0;
+    }
   }
   __syncthreads();
   if constexpr (D == 3) {
-    for (int i = tid; i < T::NCS; i += nt) {
-      int lx = i & 31, r = i >> 5, ty = r % T::TY, bz = r / T::TY;
+    double* C = CS;
+    double* S = CS + PL::NCS;
+    for (int r = wid; r < PL::TY * PL::BZ; r += NWARP) {
+      int ty = r % PL::TY, bz = r / PL::TY;
       int gy = y0 + ty;
-      double c = 0.0, s = 0.0;
-      if (unk1(gy, g.n)) {
-        int tau = gy % P;
-        const double* a = A + (bz * T::BY + ty) * 32 + lx;
-        const double* b = B + (bz * T::BY + ty) * 32 + lx;
-        double dd = 0.0, e = 0.0;
+      bool ok = unk1(gy, g.n);
+      int tau = ok ? gy % P : 0;
+      const double* a = A + (bz * PL::BY + ty) * 32 + lane;
+      const double* b = B + (bz * PL::BY + ty) * 32 + lane;
+      double c = 0.0, dd = 0.0, e = 0.0;
 #pragma unroll
-        for (int o = 0; o <= 2 * P; ++o) {
-          c = fma(cf.Mc[tau][o], a[o * 32], c);
-          dd = fma(cf.Kc[tau][o], a[o * 32], dd);
-          e = fma(cf.Mc[tau][o], b[o * 32], e);
-        }
-        s = dd + e;
+      for (int o = 0; o < PL::T; ++o) {
+        c = fma(cf.Mc[tau][o], a[o * 32], c);
+        dd = fma(cf.Kc[tau][o], a[o * 32], dd);
+        e = fma(cf.Mc[tau][o], b[o * 32], e);
       }
-      C[i] = c;
-      S[i] = s;
+      C[r * 32 + lane] = ok ? c : 0.0;
+      S[r * 32 + lane] = ok ? dd + e : 0.0;
     }
     __syncthreads();
   }
 }
 
-// Last pass of A at output (x0+lx, y0+ty, z0+tz): 2D  s = Ky a + My b;
-// 3D  h * (Kz c + Mz s) as one fma chain.  0 at non-unknowns.
+// Last pass of A at output (x0+lane, y0+ty, z0+tz); 0 at non-unknowns.
 template <int D, int P>
-__device__ __forceinline__ double atile_final(const double* sm, const Geom& g, int x0, int y0, int z0,
-                                              int lx, int ty, int tz, const Coefs& cf) {
-  using T = ATile<D, P>;
-  const double* A = sm + T::NU;
-  const double* B = A + T::NAB;
-  const double* C = B + T::NAB;
-  const double* S = C + T::NCS;
-  int gx = x0 + lx, gy = y0 + ty, gz = z0 + tz;
+__device__ __forceinline__ double a_final(const Geom& g, int x0, int y0, int z0, int ty, int tz, const Coefs& cf,
+                                          const double* AB, const double* CS) {
+  using PL = Plan<D, P>;
+  const int lane = threadIdx.x;
+  int gx = x0 + lane, gy = y0 + ty, gz = z0 + tz;
   if (!unk1(gx, g.n) || !unk1(gy, g.n) || (D == 3 && !unk1(gz, g.n))) return 0.0;
   if constexpr (D == 2) {
+    const double* A = AB;
+    const double* B = AB + PL::NAB;
     int tau = gy % P;
     double d = 0.0, e = 0.0;
 #pragma unroll
-    for (int o = 0; o <= 2 * P; ++o) {
-      d = fma(cf.Kc[tau][o], A[(ty + o) * 32 + lx], d);
-      e = fma(cf.Mc[tau][o], B[(ty + o) * 32 + lx], e);
+    for (int o = 0; o < PL::T; ++o) {
+      d = fma(cf.Kc[tau][o], A[(ty + o) * 32 + lane], d);
+      e = fma(cf.Mc[tau][o], B[(ty + o) * 32 + lane], e);
     }
     return d + e;
   } else {
+    const double* C = CS;
+    const double* S = CS + PL::NCS;
     int tau = gz % P;
     double acc = 0.0;
 #pragma unroll
-    for (int o = 0; o <= 2 * P; ++o) acc = fma(cf.Kc[tau][o], C[((tz + o) * T::TY + ty) * 32 + lx], acc);
+    for (int o = 0; o < PL::T; ++o) acc = fma(cf.Kc[tau][o], C[((tz + o) * PL::TY + ty) * 32 + lane], acc);
 #pragma unroll
-    for (int o = 0; o <= 2 * P; ++o) acc = fma(cf.Mc[tau][o], S[((tz + o) * T::TY + ty) * 32 + lx], acc);
+    for (int o = 0; o < PL::T; ++o) acc = fma(cf.Mc[tau][o], S[((tz + o) * PL::TY + ty) * 32 + lane], acc);
     return acc * pow2(-(g.l + 1));
   }
 }
 
-// Deterministic CTA sum of one double per thread -> partials[cta].
-__device__ __forceinline__ void cta_sum(double v, double* out) {
-  __shared__ double red[NWARP];
+// Load a plain FP64 array onto the input box (0 outside the stored level).
+template <int D, int P>
+__device__ void box_load(const double* __restrict__ src, const Geom& g, int x0, int y0, int z0, double* U) {
+  using PL = Plan<D, P>;
+  const int lane = threadIdx.x;
+  for (int r = threadIdx.y; r < PL::BY * PL::BZ; r += NWARP) {
+    int gy = y0 - P + r % PL::BY, gz = (D == 3) ? z0 - P + r / PL::BY : 0;
+    bool rowok = gy >= 0 && gy < g.NY && gz >= 0 && gz < g.NZ;
+    const double* row = src + ((long long)gz * g.NY + gy) * g.NX;
+    for (int bx = lane; bx < PL::BX; bx += 32) {
+      int gx = x0 - P + bx;
+      U[r * PL::BX + bx] = (rowok && gx >= 0 && gx < g.NX) ? row[gx] : 0.0;
+    }
+  }
+  __syncthreads();
+}
+
+// Deterministic CTA sum; result valid in thread 0.
+__device__ __forceinline__ double cta_sum(double v, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   if (threadIdx.x == 0) red[threadIdx.y] = v;
   __syncthreads();
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    double s = 0.0;
+  double s = 0.0;
+  if (threadIdx.x == 0 && threadIdx.y == 0)
     for (int i = 0; i < NWARP; ++i) s += red[i];
-    *out = s;
-  }
+  __syncthreads();
+  return s;
 }
 
-__device__ __forceinline__ long long cta_linear() {
-  return ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+__device__ __forceinline__ void tile_coords(const LevelDev& lv, int tile, int TY, int TZ, int& x0, int& y0, int& z0) {
+  int bx = tile % lv.tx, r = tile / lv.tx, by = r % lv.ty, bz = r / lv.ty;
+  x0 = bx * 32;
+  y0 = by * TY;
+  z0 = bz * TZ;
 }
 
-// ------------------------------------------------------- prolong/decode ----
-// out_l = dec(section) + P_l coarse  (decode sweep PAPER.md:733-735 when both
-// are given; z_l = P_l w_{l-1} with no section).  One warp per
-// 32-entry x block; P evaluated per fine point in the canonical x, y, z order.
+// ============================================================ tile ops =====
+// S2: u_l = dec ú_l + P_l u_{l-1} (decode sweep PAPER.md:733-735), materialised.
 template <int D, int P>
-__global__ void __launch_bounds__(256) k_prolong_decode(double* __restrict__ out, Geom gf,
-                                                        const double* __restrict__ coarse, Geom gc,
-                                                        const uint32_t* __restrict__ mant,
-                                                        const int8_t* __restrict__ exps, int w, int stride,
-                                                        Coefs cf) {
-  const int lane = threadIdx.x;
-  const int nxb = gf.NX >> 5;
-  long long row = (long long)blockIdx.x * NWARP + threadIdx.y;
-  if (row >= (long long)gf.NY * gf.NZ * nxb) return;
-  int xb = (int)(row % nxb);
-  long long yz = row / nxb;
-  int y = (int)(yz % gf.NY), z = (int)(yz / gf.NY);
-  int x = xb * 32 + lane;
-  long long idx = ((long long)z * gf.NY + y) * gf.NX + x;
-  double val = 0.0;
-  bool unk = unk1(x, gf.n) && unk1(y, gf.n) && (D == 2 || unk1(z, gf.n));
-  if (coarse != nullptr && unk) {
-    const int nc = gc.n;
-    int rx = x % (2 * P), bx = P * (x / (2 * P));
-    int ry = y % (2 * P), by = P * (y / (2 * P));
-    auto xpass = [&](int cy, int cz) -> double {  // v1 = Px v at (x, cy, cz)
-      const double* row_ = coarse + ((long long)cz * gc.NY + cy) * gc.NX;
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) {
-        int cx = bx + t;
-        double v = unk1(cx, nc) ? __ldg(row_ + cx) : 0.0;
-        acc = fma(cf.Pw[rx][t], v, acc);
-      }
-      return acc;
-    };
-    auto ypass = [&](int cz) -> double {  // v2 = Py v1 at (x, y, cz)
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) {
-        int cy = by + t;
-        double v = unk1(cy, nc) ? xpass(cy, cz) : 0.0;
-        acc = fma(cf.Pw[ry][t], v, acc);
-      }
-      return acc;
-    };
-    if constexpr (D == 2) {
-      val = ypass(0);
-    } else {
-      int rz = z % (2 * P), bz = P * (z / (2 * P));
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) {
-        int cz = bz + t;
-        double v = unk1(cz, nc) ? ypass(cz) : 0.0;
-        acc = fma(cf.Pw[rz][t], v, acc);
-      }
-      val = acc;
-    }
+__device__ void tile_decode(const DevCtx& c, const Op& op, int tile, double* sm) {
+  using PL = Plan<D, P>;
+  const LevelDev& lv = c.lv[op.l];
+  const Geom& g = lv.g;
+  int x0, y0, z0;
+  tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
+  double* out = c.U[op.l & 1];
+  double* box = sm;  // DBX x DBY x DBZ
+  if (op.l > 0) {
+    double* cb = box + PL::DBX * PL::DBY * PL::DBZ;
+    double* v1 = cb + PL::DCBX * PL::DCBY * PL::DCBZ;
+    double* v2 = v1 + PL::DBX * PL::DCBY * PL::DCBZ;
+    box_prolong<D, P, PL::DBX, PL::DBY, PL::DBZ, PL::DCBX, PL::DCBY, PL::DCBZ>(
+        c.U[(op.l - 1) & 1], c.lv[op.l - 1].g, g.n, x0, y0, z0, c.cf, cb, v1, v2, box);
+  } else {
+    for (int i = threadIdx.y * 32 + threadIdx.x; i < PL::DBX * PL::DBY * PL::DBZ; i += NT) box[i] = 0.0;
+    __syncthreads();
   }
-  if (mant != nullptr) {
-    long long blk = idx >> 5;
-    double dv = warp_decode(mant + blk * stride, exps[blk], w, lane);
-    val = dv + val;
+  box_add_decode<D, PL::DBX, PL::DBY, PL::DBZ, 0>(lv, op.wu_in, x0, y0, z0, box);
+  for (int r = threadIdx.y; r < PL::DBY * PL::DBZ; r += NWARP) {
+    int gy = y0 + r % PL::DBY, gz = z0 + r / PL::DBY;
+    if (gy >= g.NY || gz >= g.NZ) continue;
+    out[((long long)gz * g.NY + gy) * g.NX + x0 + threadIdx.x] = box[r * 32 + threadIdx.x];
   }
-  out[idx] = val;
 }
 
-// ---------------------------------------------------------- residual -------
-// t_L = f_L - A_L u_L, r_L = enc(t_L), ||t_L||^2.
+// S2+S3+S4: t_L = f_L - A_L (dec ú_L + P u_{L-1}) on the tile, r_L = enc(t_L),
+// ||t_L||^2 partial.  u_L is never materialised.
 template <int D, int P>
-__global__ void __launch_bounds__(256) k_residual(const double* __restrict__ U, double* __restrict__ T, Geom g,
-                                                  const double* __restrict__ gtab, Sec r, int wr,
-                                                  double* __restrict__ partials, Coefs cf, int* status) {
-  extern __shared__ double sm[];
-  using TT = ATile<D, P>;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * TT::TY, z0 = blockIdx.z * TT::TZ;
-  atile_stages<D, P>(U, g, x0, y0, z0, cf, sm);
+__device__ void tile_residual(const DevCtx& c, const Op& op, int tile, double* sm) {
+  using PL = Plan<D, P>;
+  const LevelDev& lv = c.lv[op.L];
+  const Geom& g = lv.g;
+  int x0, y0, z0;
+  tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
+  double* U = sm;
+  double* R1 = sm + PL::NU;
+  {
+    double* cb = R1;
+    double* v1 = cb + PL::NCB;
+    double* v2 = v1 + PL::NV1;
+    box_prolong<D, P, PL::BX, PL::BY, PL::BZ, PL::CBX, PL::CBY, PL::CBZ>(
+        c.U[(op.L - 1) & 1], c.lv[op.L - 1].g, g.n, x0 - P, y0 - P, z0 - P, c.cf, cb, v1, v2, U);
+  }
+  box_add_decode<D, PL::BX, PL::BY, PL::BZ, P>(lv, op.wu_in, x0, y0 - P, (D == 3) ? z0 - P : 0, U);
+  double* AB = R1;
+  double* CS = R1 + 2 * PL::NAB;
+  a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
   const int lane = threadIdx.x;
+  double* T = c.T[op.L & 1];
   double ss = 0.0;
-  for (int row = threadIdx.y; row < TT::TY * TT::TZ; row += NWARP) {
-    int ty = row % TT::TY, tz = row / TT::TY;
-    int y = y0 + ty, z = z0 + tz;
+  for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
+    int ty = row % PL::TY, tz = row / PL::TY;
+    int y = y0 + ty, z = z0 + tz, x = x0 + lane;
     if (y >= g.NY || z >= g.NZ) continue;
-    double au = atile_final<D, P>(sm, g, x0, y0, z0, lane, ty, tz, cf);
-    int x = x0 + lane;
+    double au = a_final<D, P>(g, x0, y0, z0, ty, tz, c.cf, AB, CS);
     bool unk = unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(z, g.n));
     double t = 0.0;
     if (unk) {
-      double f = cf.rhs_c * __ldg(gtab + x);
-      f = f * __ldg(gtab + y);
-      if (D == 3) f = f * __ldg(gtab + z);
+      double f = c.cf.rhs_c * lv.gtab[x];
+      f = f * lv.gtab[y];
+      if (D == 3) f = f * lv.gtab[z];
       t = f - au;
     }
     long long idx = ((long long)z * g.NY + y) * g.NX + x;
     T[idx] = t;
     ss = fma(t, t, ss);
     long long blk = idx >> 5;
-    warp_encode(t, wr, r.mant + blk * r.stride, r.exps + blk, lane, status);
+    warp_encode(t, op.wr, lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
   }
-  cta_sum(ss, partials + cta_linear());
+  __shared__ double red[NWARP];
+  double s = cta_sum(ss, red);
+  if (threadIdx.x == 0 && threadIdx.y == 0) lv.part[tile] = s;
 }
 
-// -------------------------------------------------------- restriction ------
-// t_l = R_{l+1} t_{l+1} (restricts t, not r), r_l = enc(t_l).
+// S5: t_l = R_{l+1} t_{l+1} (restricts t, not r), r_l = enc.
 template <int D, int P>
-__global__ void __launch_bounds__(256) k_restrict(const double* __restrict__ Tf, Geom gf, double* __restrict__ Tc,
-                                                  Geom gc, Sec r, int wr, double* __restrict__ partials,
-                                                  Coefs cf, int* status) {
-  extern __shared__ double sm[];
-  using RT = RTile<D, P>;
+__device__ void tile_restrict(const DevCtx& c, const Op& op, int tile, double* sm) {
+  using PL = Plan<D, P>;
+  const LevelDev& lc = c.lv[op.l];
+  const Geom& gc = lc.g;
+  const Geom& gf = c.lv[op.l + 1].g;
+  const double* __restrict__ Tf = c.T[(op.l + 1) & 1];
+  double* Tc = c.T[op.l & 1];
+  int x0, y0, z0;
+  tile_coords(lc, tile, PL::TY, PL::TZ, x0, y0, z0);
   double* XR = sm;
-  double* YR = sm + RT::NX;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * RT::TY, z0 = blockIdx.z * RT::TZ;
-  const int tid = threadIdx.y * 32 + threadIdx.x, nt = 32 * NWARP;
-  const int nf = gf.n, nc = gc.n;
-  for (int i = tid; i < RT::NX; i += nt) {
-    int lx = i & 31, rr = i >> 5, by = rr % RT::FBY, bz = rr / RT::FBY;
-    int fy = 2 * y0 - (2 * P - 1) + by;
-    int fz = (D == 3) ? 2 * z0 - (2 * P - 1) + bz : 0;
-    int cx = x0 + lx;
-    double v = 0.0;
-    if (unk1(cx, nc) && fy >= 0 && fy < gf.NY && fz >= 0 && fz < gf.NZ) {
-      int tau = cx % P, fx0 = 2 * cx - (2 * P - 1);
-      const double* rowp = Tf + ((long long)fz * gf.NY + fy) * gf.NX;
+  double* YR = sm + PL::NXR;
+  const int lane = threadIdx.x, nf = gf.n, nc = gc.n;
+  {
+    const int cx = x0 + lane;
+    const bool ok = unk1(cx, nc);
+    const int tau = ok ? cx % P : 0, fx0 = 2 * cx - (2 * P - 1);
+    double rw[4 * P - 1];
 #pragma unroll
-      for (int s = 0; s <= 4 * P - 2; ++s) {
-        int fx = fx0 + s;
-        double t = unk1(fx, nf) ? __ldg(rowp + fx) : 0.0;
-        v = fma(cf.Rw[tau][s], t, v);
+    for (int s = 0; s < 4 * P - 1; ++s) rw[s] = c.cf.Rw[tau][s];
+    for (int rr = threadIdx.y; rr < PL::FBY * PL::FBZ; rr += NWARP) {
+      int by = rr % PL::FBY, bz = rr / PL::FBY;
+      int fy = 2 * y0 - (2 * P - 1) + by;
+      int fz = (D == 3) ? 2 * z0 - (2 * P - 1) + bz : 0;
+      double v = 0.0;
+      if (ok && fy >= 0 && fy < gf.NY && fz >= 0 && fz < gf.NZ) {
+        const double* rowp = Tf + ((long long)fz * gf.NY + fy) * gf.NX;
+#pragma unroll
+        for (int s = 0; s < 4 * P - 1; ++s) {
+          int fx = fx0 + s;
+          double t = unk1(fx, nf) ? rowp[fx] : 0.0;
+          v = fma(rw[s], t, v);
+        }
       }
+      XR[rr * 32 + lane] = v;
     }
-    XR[i] = v;
   }
   __syncthreads();
   if constexpr (D == 3) {
-    for (int i = tid; i < RT::NYR; i += nt) {
-      int lx = i & 31, rr = i >> 5, ty = rr % RT::TY, bz = rr / RT::TY;
+    for (int rr = threadIdx.y; rr < PL::TY * PL::FBZ; rr += NWARP) {
+      int ty = rr % PL::TY, bz = rr / PL::TY;
       int cy = y0 + ty;
+      bool ok = unk1(cy, nc);
+      int tau = ok ? cy % P : 0;
+      const double* xr = XR + (bz * PL::FBY + 2 * ty) * 32 + lane;
       double v = 0.0;
-      if (unk1(cy, nc)) {
-        int tau = cy % P;
-        const double* xr = XR + (bz * RT::FBY + 2 * ty) * 32 + lx;
 #pragma unroll
-        for (int s = 0; s <= 4 * P - 2; ++s) v = fma(cf.Rw[tau][s], xr[s * 32], v);
-      }
-      YR[i] = v;
+      for (int s = 0; s < 4 * P - 1; ++s) v = fma(c.cf.Rw[tau][s], xr[s * 32], v);
+      YR[rr * 32 + lane] = ok ? v : 0.0;
     }
     __syncthreads();
   }
-  const int lane = threadIdx.x;
   double ss = 0.0;
-  for (int row = threadIdx.y; row < RT::TY * RT::TZ; row += NWARP) {
-    int ty = row % RT::TY, tz = row / RT::TY;
+  for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
+    int ty = row % PL::TY, tz = row / PL::TY;
     int y = y0 + ty, z = z0 + tz, x = x0 + lane;
     if (y >= gc.NY || z >= gc.NZ) continue;
     double t = 0.0;
@@ -410,59 +603,77 @@ __global__ void __launch_bounds__(256) k_restrict(const double* __restrict__ Tf,
       if constexpr (D == 2) {
         int tau = y % P;
 #pragma unroll
-        for (int s = 0; s <= 4 * P - 2; ++s) t = fma(cf.Rw[tau][s], XR[(2 * ty + s) * 32 + lane], t);
+        for (int s = 0; s < 4 * P - 1; ++s) t = fma(c.cf.Rw[tau][s], XR[(2 * ty + s) * 32 + lane], t);
       } else {
         int tau = z % P;
 #pragma unroll
-        for (int s = 0; s <= 4 * P - 2; ++s) t = fma(cf.Rw[tau][s], YR[((2 * tz + s) * RT::TY + ty) * 32 + lane], t);
+        for (int s = 0; s < 4 * P - 1; ++s) t = fma(c.cf.Rw[tau][s], YR[((2 * tz + s) * PL::TY + ty) * 32 + lane], t);
       }
     }
     long long idx = ((long long)z * gc.NY + y) * gc.NX + x;
     Tc[idx] = t;
     ss = fma(t, t, ss);
     long long blk = idx >> 5;
-    warp_encode(t, wr, r.mant + blk * r.stride, r.exps + blk, lane, status);
+    warp_encode(t, op.wr, lc.rmant + blk * lc.rstride, lc.rexp + blk, lane, c.status);
   }
-  cta_sum(ss, partials + cta_linear());
+  __shared__ double red[NWARP];
+  double s = cta_sum(ss, red);
+  if (threadIdx.x == 0 && threadIdx.y == 0) lc.part[tile] = s;
 }
 
-// --------------------------------------------------------- coarse level ----
-// mode 0: ú_0 = enc_{wu_out}(A_0^{-1} f_0)
-// mode 1: ý_0 = enc_{wr}(A_0^{-1} dec r_0), W_0 = dec ý_0,
-//         ú_0 <- enc_{wu_out}(dec_{wu_in} ú_0 + dec ý_0)
-// Canonical mat-vec: acc = 0; acc = fma(Ainv[I][J], x_J, acc), J in unknown order.
+// Norms of t_0..t_L from the per-tile partials (fixed order).
+__device__ void op_norms(const DevCtx& c, const Op& op, double* sm) {
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int l = 0; l <= op.L; ++l) {
+    const LevelDev& lv = c.lv[l];
+    int n = lv.tx * lv.ty * lv.tz;
+    double s = 0.0;
+    for (int i = tid; i < n; i += NT) s += lv.part[i];
+    sm[tid] = s;
+    __syncthreads();
+    for (int o = NT / 2; o > 0; o >>= 1) {
+      if (tid < o) sm[tid] += sm[tid + o];
+      __syncthreads();
+    }
+    if (tid == 0) c.norms[(long long)op.row * c.levels + l] = sqrt(sm[0]);
+    __syncthreads();
+  }
+}
+
+// S6 / S10 on level 0 (dense A_0^{-1}, canonical mat-vec DESIGN.md §3.7).
+// INIT:  ú_0 = enc_{wu_out}(A_0^{-1} f_0)
+// CFAS:  ý_0 = enc_{wr}(A_0^{-1} dec r_0); W_0 = dec ý_0; ú_0 = enc(dec ú_0 + dec ý_0)
 template <int D, int P>
-__global__ void __launch_bounds__(256) k_coarse(int mode, Geom g, const double* __restrict__ gtab,
-                                                const double* __restrict__ Ainv, int n0, Sec u, int wu_in,
-                                                int wu_out, Sec r, int wr, double* __restrict__ W0,
-                                                Coefs cf, int* status) {
+__device__ void op_coarse(const DevCtx& c, const Op& op, double* sm) {
   constexpr int n = 2 * P, m = 2 * P - 1;
   constexpr int ROWS = (D == 3) ? n * n : n;
-  __shared__ double X[ROWS * 32], Y[ROWS * 32];
+  const LevelDev& lv = c.lv[0];
+  double* X = sm;
+  double* Y = sm + ROWS * 32;
   const int lane = threadIdx.x, tid = threadIdx.y * 32 + threadIdx.x;
   for (int row = threadIdx.y; row < ROWS; row += NWARP) {
     int y = row % n, z = row / n;
     double v;
-    if (mode == 0) {
+    if (op.type == OP_COARSE_INIT) {
       bool unk = unk1(lane, n) && unk1(y, n) && (D == 2 || unk1(z, n));
       v = 0.0;
       if (unk) {
-        v = cf.rhs_c * gtab[lane];
-        v = v * gtab[y];
-        if (D == 3) v = v * gtab[z];
+        v = c.cf.rhs_c * lv.gtab[lane];
+        v = v * lv.gtab[y];
+        if (D == 3) v = v * lv.gtab[z];
       }
     } else {
-      v = warp_decode(r.mant + (long long)row * r.stride, r.exps[row], wr, lane);
+      v = warp_decode(lv.rmant + (long long)row * lv.rstride, lv.rexp[row], op.wr, lane);
     }
     X[row * 32 + lane] = v;
     Y[row * 32 + lane] = 0.0;
   }
   __syncthreads();
-  for (int I = tid; I < n0; I += 32 * NWARP) {
+  for (int I = tid; I < c.n0; I += NT) {
     double acc = 0.0;
-    for (int J = 0; J < n0; ++J) {
+    for (int J = 0; J < c.n0; ++J) {
       int jx = J % m + 1, jy = (J / m) % m + 1, jz = (D == 3) ? J / (m * m) + 1 : 0;
-      acc = fma(Ainv[(long long)I * n0 + J], X[(jz * n + jy) * 32 + jx], acc);
+      acc = fma(c.Ainv[(long long)I * c.n0 + J], X[(jz * n + jy) * 32 + jx], acc);
     }
     int ix = I % m + 1, iy = (I / m) % m + 1, iz = (D == 3) ? I / (m * m) + 1 : 0;
     Y[(iz * n + iy) * 32 + ix] = acc;
@@ -470,92 +681,197 @@ __global__ void __launch_bounds__(256) k_coarse(int mode, Geom g, const double* 
   __syncthreads();
   for (int row = threadIdx.y; row < ROWS; row += NWARP) {
     double y = Y[row * 32 + lane];
-    uint32_t* uw = u.mant + (long long)row * u.stride;
-    if (mode == 0) {
-      warp_encode(y, wu_out, uw, u.exps + row, lane, status);
+    uint32_t* uw = lv.umant + (long long)row * lv.ustride;
+    if (op.type == OP_COARSE_INIT) {
+      warp_encode(y, op.wu_out, uw, lv.uexp + row, lane, c.status);
     } else {
-      double yq = warp_encode(y, wr, nullptr, nullptr, lane, status);
-      W0[row * 32 + lane] = yq;
-      double uo = warp_decode(uw, u.exps[row], wu_in, lane);
-      warp_encode(uo + yq, wu_out, uw, u.exps + row, lane, status);
+      double yq = warp_encode(y, op.wr, nullptr, nullptr, lane, c.status);
+      c.W[0][row * 32 + lane] = yq;
+      double uo = warp_decode(uw, lv.uexp[row], op.wu_in, lane);
+      warp_encode(uo + yq, op.wu_out, uw, lv.uexp + row, lane, c.status);
     }
   }
+  __syncthreads();
 }
 
-// ------------------------------------------------------------ cFas level --
-// Level l of the coarse-to-fine sweep with Chebyshev-Jacobi
-// (DESIGN.md §3.5).  step 1: b = dec r_l - A_l z_l, d = inv_theta (invD b), y = d.
-// step j >= 2: q = b - A y, d = fma(alpha_j, d, beta_j (invD q)), y = y + d.
-// last step: ý = enc_{wr}(y); W_l = z_l + dec ý; ú_l <- enc_{wu_out}(dec ú_l + dec ý).
-template <int D, int P>
-__global__ void __launch_bounds__(256) k_cfas_step(Geom g, CfasArgs a, Coefs cf, int* status) {
-  extern __shared__ double sm[];
-  using TT = ATile<D, P>;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * TT::TY, z0 = blockIdx.z * TT::TZ;
-  atile_stages<D, P>(a.step == 1 ? a.Z : a.Yin, g, x0, y0, z0, cf, sm);
+// Finalise a cFas level at one output row:
+// ý = enc_wr(y); W_l = z_l + dec ý (l < L); ú_l = enc_{wu_out}(dec_{wu_in} ú_l + dec ý).
+__device__ __forceinline__ void cfas_finalize(const DevCtx& c, const Op& op, const LevelDev& lv, long long idx,
+                                              double y) {
   const int lane = threadIdx.x;
-  const double dsc = pow2((g.l + 1) * (D - 2));
-  for (int row = threadIdx.y; row < TT::TY * TT::TZ; row += NWARP) {
-    int ty = row % TT::TY, tz = row / TT::TY;
+  double yq = warp_encode(y, op.wr, nullptr, nullptr, lane, c.status);
+  if (op.l < op.L) c.W[op.l & 1][idx] = c.Z[idx] + yq;
+  long long blk = idx >> 5;
+  uint32_t* uw = lv.umant + blk * lv.ustride;
+  double uo = warp_decode(uw, lv.uexp[blk], op.wu_in, lane);
+  warp_encode(uo + yq, op.wu_out, uw, lv.uexp + blk, lane, c.status);
+}
+
+__device__ __forceinline__ double inv_diag(const Coefs& cf, int D, int P, int l, int x, int y, int z) {
+  return cf.invd[((D == 3 ? z % P : 0) * P + y % P) * P + x % P] * pow2((l + 1) * (D - 2));
+}
+
+// S7 + S8 step 1: z = P w_{l-1} on the box, b = dec r_l - A z;
+// d = inv_theta (invD b), y = d.  Writes B (and Z for l < L);
+// with k == 1 finalises directly.
+template <int D, int P>
+__device__ void tile_cfas1(const DevCtx& c, const Op& op, int tile, double* sm) {
+  using PL = Plan<D, P>;
+  const LevelDev& lv = c.lv[op.l];
+  const Geom& g = lv.g;
+  int x0, y0, z0;
+  tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
+  double* U = sm;
+  double* R1 = sm + PL::NU;
+  {
+    double* cb = R1;
+    double* v1 = cb + PL::NCB;
+    double* v2 = v1 + PL::NV1;
+    box_prolong<D, P, PL::BX, PL::BY, PL::BZ, PL::CBX, PL::CBY, PL::CBZ>(
+        c.W[(op.l - 1) & 1], c.lv[op.l - 1].g, g.n, x0 - P, y0 - P, z0 - P, c.cf, cb, v1, v2, U);
+  }
+  double* AB = R1;
+  double* CS = R1 + 2 * PL::NAB;
+  a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
+  const int lane = threadIdx.x;
+  for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
+    int ty = row % PL::TY, tz = row / PL::TY;
     int y = y0 + ty, z = z0 + tz, x = x0 + lane;
     if (y >= g.NY || z >= g.NZ) continue;
-    double au = atile_final<D, P>(sm, g, x0, y0, z0, lane, ty, tz, cf);
+    double az = a_final<D, P>(g, x0, y0, z0, ty, tz, c.cf, AB, CS);
     bool unk = unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(z, g.n));
     long long idx = ((long long)z * g.NY + y) * g.NX + x;
     long long blk = idx >> 5;
-    double invD = 0.0;
-    if (unk) invD = cf.invd[((D == 3 ? z % P : 0) * P + y % P) * P + x % P] * dsc;
-    double d, yv, b = 0.0;
-    if (a.step == 1) {
-      double rv = warp_decode(a.r.mant + blk * a.r.stride, a.r.exps[blk], a.wr, lane);
-      b = rv - au;
-      d = cf.inv_theta * (invD * b);
-      yv = d;
+    double rv = warp_decode(lv.rmant + blk * lv.rstride, lv.rexp[blk], op.wr, lane);
+    double b = rv - az;
+    double zc = U[((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane];
+    if (op.last) {
+      double invD = unk ? inv_diag(c.cf, D, P, op.l, x, y, z) : 0.0;
+      double d = c.cf.inv_theta * (invD * b);
+      if (op.l < op.L) c.Z[idx] = zc;
+      cfas_finalize(c, op, lv, idx, d);
     } else {
-      b = a.B[idx];
-      double q = b - au;
-      d = fma(cf.cal[a.step - 1], a.Dv[idx], cf.cbe[a.step - 1] * (invD * q));
-      yv = a.Yin[idx] + d;
-    }
-    if (!a.last) {
-      if (a.step == 1) a.B[idx] = b;
-      a.Yout[idx] = yv;
-      a.Dv[idx] = d;
-    } else {
-      double yq = warp_encode(yv, a.wr, nullptr, nullptr, lane, status);
-      if (a.W) a.W[idx] = a.Z[idx] + yq;
-      uint32_t* uw = a.u.mant + blk * a.u.stride;
-      double uo = warp_decode(uw, a.u.exps[blk], a.wu_in, lane);
-      warp_encode(uo + yq, a.wu_out, uw, a.u.exps + blk, lane, status);
+      c.B[idx] = b;
+      if (op.l < op.L) c.Z[idx] = zc;
     }
   }
 }
 
-// --------------------------------------------------------------- norms ----
-struct NormArgs {
-  long long offs[kMaxLev];
-  int counts[kMaxLev];
-  int nlev;
-};
-__global__ void k_norms(const double* __restrict__ partials, NormArgs na, double* __restrict__ out) {
-  __shared__ double red[256];
-  for (int l = 0; l < na.nlev; ++l) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < na.counts[l]; i += 256) s += partials[na.offs[l] + i];
-    red[threadIdx.x] = s;
+// S8 step j >= 2: q = b - A y, d = fma(alpha_j, d, beta_j (invD q)), y = y + d.
+// Step 2 reconstructs y_1 = d_1 = inv_theta (invD b) from B on the box (no Y/D
+// arrays for k = 2); later steps read Y/Dv.  Last step finalises (S9, S10).
+template <int D, int P>
+__device__ void tile_cheb(const DevCtx& c, const Op& op, int tile, double* sm) {
+  using PL = Plan<D, P>;
+  const LevelDev& lv = c.lv[op.l];
+  const Geom& g = lv.g;
+  int x0, y0, z0;
+  tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
+  double* U = sm;
+  double* R1 = sm + PL::NU;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  if (op.step == 2) {
+    const double sc = pow2((op.l + 1) * (D - 2));
+    for (int r = threadIdx.y; r < PL::BY * PL::BZ; r += NWARP) {
+      int gy = y0 - P + r % PL::BY, gz = (D == 3) ? z0 - P + r / PL::BY : 0;
+      bool rowok = unk1(gy, g.n) && (D == 2 || unk1(gz, g.n));
+      int rowt = rowok ? ((D == 3 ? gz % P : 0) * P + gy % P) * P : 0;
+      const double* row = c.B + ((long long)gz * g.NY + gy) * g.NX;
+      for (int bx = threadIdx.x; bx < PL::BX; bx += 32) {
+        int gx = x0 - P + bx;
+        bool ok = rowok && unk1(gx, g.n);
+        double v = 0.0;
+        if (ok) v = c.cf.inv_theta * ((c.cf.invd[rowt + gx % P] * sc) * row[gx]);
+        U[r * PL::BX + bx] = v;
+      }
+    }
     __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+  } else {
+    box_load<D, P>(c.Y[op.step & 1], g, x0, y0, z0, U);
+  }
+  double* AB = R1;
+  double* CS = R1 + 2 * PL::NAB;
+  a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
+  const int lane = threadIdx.x;
+  for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
+    int ty = row % PL::TY, tz = row / PL::TY;
+    int y = y0 + ty, z = z0 + tz, x = x0 + lane;
+    if (y >= g.NY || z >= g.NZ) continue;
+    double ay = a_final<D, P>(g, x0, y0, z0, ty, tz, c.cf, AB, CS);
+    bool unk = unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(z, g.n));
+    long long idx = ((long long)z * g.NY + y) * g.NX + x;
+    double invD = unk ? inv_diag(c.cf, D, P, op.l, x, y, z) : 0.0;
+    double b = c.B[idx];
+    double q = b - ay;
+    double yprev = U[((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane];
+    double dprev = (op.step == 2) ? yprev : c.Dv[idx];
+    double d = fma(c.cf.cal[op.step - 1], dprev, c.cf.cbe[op.step - 1] * (invD * q));
+    double yv = yprev + d;
+    if (op.last) {
+      cfas_finalize(c, op, lv, idx, yv);
+    } else {
+      c.Y[(op.step + 1) & 1][idx] = yv;
+      c.Dv[idx] = d;
+    }
+  }
+}
+
+template <int D, int P>
+__device__ __forceinline__ void run_op(const DevCtx& c, const Op& op, int tile, double* sm) {
+  switch (op.type) {
+    case OP_DECODE: tile_decode<D, P>(c, op, tile, sm); break;
+    case OP_RESIDUAL: tile_residual<D, P>(c, op, tile, sm); break;
+    case OP_RESTRICT: tile_restrict<D, P>(c, op, tile, sm); break;
+    case OP_NORMS: op_norms(c, op, sm); break;
+    case OP_COARSE_INIT:
+    case OP_COARSE_CFAS: op_coarse<D, P>(c, op, sm); break;
+    case OP_CFAS1: tile_cfas1<D, P>(c, op, tile, sm); break;
+    case OP_CHEB: tile_cheb<D, P>(c, op, tile, sm); break;
+  }
+}
+
+// Copies the device context (pointers, geometry, coefficient tables) into
+// shared memory once per CTA: every later access is an LDS (broadcast for
+// uniform indices) instead of a global load.
+__device__ __forceinline__ void load_ctx(const DevCtx* __restrict__ cp, DevCtx* sc) {
+  static_assert(sizeof(DevCtx) % 8 == 0, "DevCtx size");
+  const unsigned long long* src = (const unsigned long long*)cp;
+  unsigned long long* dst = (unsigned long long*)sc;
+  for (int i = threadIdx.y * 32 + threadIdx.x; i < (int)(sizeof(DevCtx) / 8); i += NT) dst[i] = src[i];
+  __syncthreads();
+}
+
+// Grid kernel: one CTA per tile of one operation.
+template <int D, int P>
+__global__ void __launch_bounds__(NT) k_op(const DevCtx* __restrict__ cp, Op op) {
+  extern __shared__ double sm[];
+  __shared__ DevCtx sc;
+  pdl_wait();
+  pdl_trigger();
+  load_ctx(cp, &sc);
+  run_op<D, P>(sc, op, blockIdx.x, sm);
+}
+
+// Sequencer kernel: one CTA runs ops [first, first+count) of `prog` over all
+// their tiles (small levels), with __syncthreads between tiles/ops.
+template <int D, int P>
+__global__ void __launch_bounds__(NT) k_seq(const DevCtx* __restrict__ cp, const Op* __restrict__ prog, int count) {
+  extern __shared__ double sm[];
+  __shared__ DevCtx sc;
+  pdl_wait();
+  pdl_trigger();
+  load_ctx(cp, &sc);
+  for (int i = 0; i < count; ++i) {
+    Op op = prog[i];
+    int nt = op_tiles(sc, op);
+    for (int t = 0; t < nt; ++t) {
+      run_op<D, P>(sc, op, t, sm);
       __syncthreads();
     }
-    if (threadIdx.x == 0) out[l] = sqrt(red[0]);
-    __syncthreads();
   }
 }
 
 // ------------------------------------------------------- error norms -------
-// Per element: tensor Gauss-Legendre (p+3)^d points; partial sums of
-// (u_h - u)^2 and |grad(u_h - u)|^2 (R13).  Validation only.
 struct ErrTab {
   double qx[6], qw[6];
   double phi[6][4], dphi[6][4];
@@ -650,14 +966,14 @@ __global__ void __launch_bounds__(256) k_bfp_decode(const uint32_t* __restrict__
 }
 
 // ============================================================ launchers ===
-#define FMG_DISPATCH(dim, p, F)                     \
-  do {                                              \
-    if (dim == 2 && p == 1) { F(2, 1); }            \
-    else if (dim == 2 && p == 2) { F(2, 2); }       \
-    else if (dim == 2 && p == 3) { F(2, 3); }       \
-    else if (dim == 3 && p == 1) { F(3, 1); }       \
-    else if (dim == 3 && p == 2) { F(3, 2); }       \
-    else { F(3, 3); }                               \
+#define FMG_DISPATCH(dim, p, F)               \
+  do {                                        \
+    if (dim == 2 && p == 1) { F(2, 1); }      \
+    else if (dim == 2 && p == 2) { F(2, 2); } \
+    else if (dim == 2 && p == 3) { F(2, 3); } \
+    else if (dim == 3 && p == 1) { F(3, 1); } \
+    else if (dim == 3 && p == 2) { F(3, 2); } \
+    else { F(3, 3); }                         \
   } while (0)
 
 static int g_num_sms = 0;
@@ -671,83 +987,100 @@ static int num_sms() {
   return g_num_sms;
 }
 
+int smem_bytes(int dim, int p) {
+  int s = 0;
+#define F(D, P) s = Plan<D, P>::SMEM
+  FMG_DISPATCH(dim, p, F);
+#undef F
+  return s;
+}
+
 void set_kernel_attributes() {
-#define SETA(D, P)                                                                                    \
-  cudaFuncSetAttribute(k_residual<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ATile<D, P>::SMEM); \
-  cudaFuncSetAttribute(k_cfas_step<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ATile<D, P>::SMEM); \
-  cudaFuncSetAttribute(k_restrict<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, RTile<D, P>::SMEM);
+#define SETA(D, P)                                                                                        \
+  cudaFuncSetAttribute(k_op<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM);  \
+  cudaFuncSetAttribute(k_seq<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM);
   SETA(2, 1) SETA(2, 2) SETA(2, 3) SETA(3, 1) SETA(3, 2) SETA(3, 3)
 #undef SETA
 }
 
-static dim3 tile_grid(int dim, int p, const Geom& g) {
-  int TY = 16, TZ = 1;
-  if (dim == 3) {
-    TY = (p == 1) ? 8 : 4;
-    TZ = 4;
+void tile_shape(int dim, int p, int* TY, int* TZ) {
+#define F(D, P) do { *TY = TileCfg<D, P>::TY; *TZ = TileCfg<D, P>::TZ; } while (0)
+  FMG_DISPATCH(dim, p, F);
+#undef F
+}
+
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K kernel, dim3 grid, int smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(32, NWARP);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& op, int ntiles) {
+  const DevCtx* c = (const DevCtx*)devctx;
+#define F(D, P) launch_pdl(k_op<D, P>, dim3(ntiles), Plan<D, P>::SMEM, st, c, op)
+  FMG_DISPATCH(dim, p, F);
+#undef F
+}
+
+void launch_seq(int dim, int p, cudaStream_t st, const void* devctx, const void* prog_dev, int count) {
+  const DevCtx* c = (const DevCtx*)devctx;
+  const Op* pr = (const Op*)prog_dev;
+#define F(D, P) launch_pdl(k_seq<D, P>, dim3(1), Plan<D, P>::SMEM, st, c, pr, count)
+  FMG_DISPATCH(dim, p, F);
+#undef F
+}
+
+size_t devctx_size() { return sizeof(DevCtx); }
+size_t op_size() { return sizeof(Op); }
+
+void fill_devctx(void* host_buf, const DevCtxDesc& d) {
+  DevCtx* c = (DevCtx*)host_buf;
+  memset(c, 0, sizeof(DevCtx));
+  for (int l = 0; l < d.levels; ++l) {
+    LevelDev& lv = c->lv[l];
+    lv.g = d.g[l];
+    lv.umant = d.u[l].mant;
+    lv.uexp = d.u[l].exps;
+    lv.ustride = d.u[l].stride;
+    lv.rmant = d.r[l].mant;
+    lv.rexp = d.r[l].exps;
+    lv.rstride = d.r[l].stride;
+    lv.gtab = d.gtab[l];
+    lv.tx = d.tiles[l][0];
+    lv.ty = d.tiles[l][1];
+    lv.tz = d.tiles[l][2];
+    lv.part = d.part[l];
   }
-  return dim3(g.NX / 32, (g.NY + TY - 1) / TY, (g.NZ + TZ - 1) / TZ);
-}
-
-int tile_count(int dim, int p, int kind, const Geom& g) {
-  (void)kind;
-  dim3 gr = tile_grid(dim, p, g);
-  return gr.x * gr.y * gr.z;
-}
-
-void launch_prolong_decode(const Launch& L, double* out, const Geom& gf, const double* coarse, const Geom& gc,
-                           const uint32_t* mant, const int8_t* exps, int w, int stride, const Coefs& cf) {
-  long long rows = (long long)gf.NY * gf.NZ * (gf.NX / 32);
-  dim3 grid((unsigned)((rows + NWARP - 1) / NWARP)), block(32, NWARP);
-#define F(D, P) k_prolong_decode<D, P><<<grid, block, 0, L.st>>>(out, gf, coarse, gc, mant, exps, w, stride, cf)
-  FMG_DISPATCH(L.dim, L.p, F);
-#undef F
-}
-
-void launch_residual(const Launch& L, const double* U, double* T, const Geom& g, const double* gtab, Sec r,
-                     int wr, double* partials, const Coefs& cf, int* status) {
-  dim3 grid = tile_grid(L.dim, L.p, g), block(32, NWARP);
-#define F(D, P) k_residual<D, P><<<grid, block, ATile<D, P>::SMEM, L.st>>>(U, T, g, gtab, r, wr, partials, cf, status)
-  FMG_DISPATCH(L.dim, L.p, F);
-#undef F
-}
-
-void launch_restrict(const Launch& L, const double* Tf, const Geom& gf, double* Tc, const Geom& gc, Sec r,
-                     int wr, double* partials, const Coefs& cf, int* status) {
-  dim3 grid = tile_grid(L.dim, L.p, gc), block(32, NWARP);
-#define F(D, P) k_restrict<D, P><<<grid, block, RTile<D, P>::SMEM, L.st>>>(Tf, gf, Tc, gc, r, wr, partials, cf, status)
-  FMG_DISPATCH(L.dim, L.p, F);
-#undef F
-}
-
-void launch_coarse(const Launch& L, int mode, const Geom& g0, const double* gtab0, const double* Ainv, int n0,
-                   Sec u, int wu_in, int wu_out, Sec r, int wr, double* W0, const Coefs& cf, int* status) {
-  dim3 block(32, NWARP);
-#define F(D, P) k_coarse<D, P><<<1, block, 0, L.st>>>(mode, g0, gtab0, Ainv, n0, u, wu_in, wu_out, r, wr, W0, cf, status)
-  FMG_DISPATCH(L.dim, L.p, F);
-#undef F
-}
-
-void launch_cfas_step(const Launch& L, const Geom& g, const CfasArgs& a, const Coefs& cf, int* status) {
-  dim3 grid = tile_grid(L.dim, L.p, g), block(32, NWARP);
-#define F(D, P) k_cfas_step<D, P><<<grid, block, ATile<D, P>::SMEM, L.st>>>(g, a, cf, status)
-  FMG_DISPATCH(L.dim, L.p, F);
-#undef F
-}
-
-void launch_norms(cudaStream_t st, const double* partials, const long long* offs, const int* counts, int nlev,
-                  double* out) {
-  NormArgs na;
-  for (int l = 0; l < kMaxLev; ++l) {
-    na.offs[l] = l < nlev ? offs[l] : 0;
-    na.counts[l] = l < nlev ? counts[l] : 0;
+  for (int i = 0; i < 2; ++i) {
+    c->U[i] = d.U[i];
+    c->T[i] = d.T[i];
+    c->W[i] = d.W[i];
+    c->Y[i] = d.Y[i];
   }
-  na.nlev = nlev;
-  k_norms<<<1, 256, 0, st>>>(partials, na, out);
+  c->Z = d.Z;
+  c->B = d.B;
+  c->Dv = d.Dv;
+  c->Ainv = d.Ainv;
+  c->n0 = d.n0;
+  c->norms = d.norms;
+  c->levels = d.levels;
+  c->n_ir = d.n_ir;
+  c->status = d.status;
+  c->cf = d.cf;
 }
+
+void pack_op(void* dst, const OpDesc& od) { memcpy(dst, &od, sizeof(Op)); }
 
 void launch_errors(const Launch& L, const double* U, const Geom& g, double* partials, int* nparts) {
-  // Gauss-Legendre nodes/weights on [0,1] (Newton on P_n) and Lagrange values.
   ErrTab et;
   int nq = L.p + 3;
   for (int i = 0; i < nq; ++i) {
