@@ -125,10 +125,14 @@ int fmg_info(fmg_ctx* c, double* info10);
 /* Kernel-time instrumentation for bench.py: when enabled before the first
  * solve, the captured graph brackets every launch of kernel class `cls`
  * (0 = fine residual, 1 = fine cFas smoothing step, 2 = prolong/decode,
- * 3 = restriction) with CUDA events; fmg_kernel_time returns the summed device
+ * 3 = restriction, 4 = every launch) with CUDA events; fmg_kernel_time returns the summed device
  * time (ms) and launch count of the last solve (synchronous). */
 int fmg_enable_kernel_timing(fmg_ctx* c, int cls);
 int fmg_kernel_time(fmg_ctx* c, double* total_ms, int* launches);
+/* Class 4 brackets every launch; fmg_kernel_times returns the per-launch
+ * device times (ms, launch order) of the last solve into ms[cap]; returns the
+ * count (synchronous). */
+int fmg_kernel_times(fmg_ctx* c, float* ms, int cap);
 
 /* Separable right-hand side f_l(i,j,k) = ((C g_l(i)) g_l(j)) g_l(k):
  * the 1D factor tables of every level, concatenated level by level

@@ -57,6 +57,7 @@ _lib.fmg_get_section.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, C.POINTER(C.c_
 _lib.fmg_info.argtypes = [_vp, _dp]
 _lib.fmg_enable_kernel_timing.argtypes = [_vp, C.c_int]
 _lib.fmg_kernel_time.argtypes = [_vp, _dp, C.POINTER(C.c_int)]
+_lib.fmg_kernel_times.argtypes = [_vp, _vp, C.c_int]
 _lib.fmg_destroy.argtypes = [_vp]
 _lib.fmg_destroy.restype = None
 _lib.fmg_rhs_size.argtypes = [_vp]
@@ -75,7 +76,7 @@ _lib.fmg_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, C.c_void_p]
 
 EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_solve_async", "fmg_solve", "fmg_solve_upto",
            "fmg_norms", "fmg_residual", "fmg_get_solution", "fmg_errors", "fmg_get_section",
-           "fmg_info", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_destroy",
+           "fmg_info", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_kernel_times", "fmg_destroy",
            "fmg_rhs_size", "fmg_set_rhs", "fmg_get_rhs", "fmg_export_solution",
            "fmg_strerror", "bfp_encode", "bfp_decode", "bfp_status"]
 
@@ -228,6 +229,12 @@ class Solver:
 
     def enable_kernel_timing(self, cls: int):
         _check(_lib.fmg_enable_kernel_timing(self._h, cls), "fmg_enable_kernel_timing")
+
+    def kernel_times(self):
+        import numpy as np
+        buf = np.zeros(20000, dtype=np.float32)
+        n = _lib.fmg_kernel_times(self._h, buf.ctypes.data, buf.size)
+        return buf[:max(n, 0)].copy()
 
     def kernel_time(self):
         t = C.c_double()

@@ -42,19 +42,19 @@ struct fmg_ctx {
   int tiles[kMaxLev][3]{};
   double* Ainv = nullptr;
   int n0 = 0;
-  double* buf[7]{};
+  double* buf[9]{};
   double* partials = nullptr;
   long long part_off[kMaxLev]{};
   double* norms_dev = nullptr;
   double* err_part = nullptr;
   int* status = nullptr;
   void* devctx = nullptr;         // DevCtx in device memory
-  void* prog[2] = {nullptr, nullptr};  // op programs: [0] graph, [1] direct
-  size_t prog_cap[2] = {0, 0};
   cudaGraphExec_t graph = nullptr;
   int solved_L = -1;
   int wu_cur[kMaxLev]{};
-  int seq_max_level = -1;         // levels <= this run inside the sequencer kernel
+  int lc = 0;                     // levels 0..lc run inside K4 (shared memory)
+  int k4_smem = 0;
+  double* usm = nullptr;
   fmg_alloc_fn afn = nullptr;
   fmg_free_fn ffn = nullptr;
   void* auser = nullptr;
@@ -94,40 +94,32 @@ void free_all(fmg_ctx* c) {
 Launch L_(fmg_ctx* c) { return Launch{c->dim, c->p, c->cur}; }
 
 // ---------------------------------------------------------------- schedule --
-// A solve is a list of items: a grid launch of one op over all tiles of its
-// level, or a sequencer launch of consecutive small-level ops.
+// A solve is a list of items: a grid launch of one tile op over all tiles of its
+// level, or one launch of the shared-memory coarse-hierarchy kernel K4
+// (levels 0..lc).  DESIGN.md §4.
 struct Item {
-  bool seq;
-  OpDesc op;          // grid item
-  int first, count;   // seq item: range in the op program
-  int timed_cls;      // kernel-timing class of a grid item (-1: none)
+  int kind;          // 0 grid op, 1 K4
+  OpDesc op;         // grid item
+  K4Desc k4;         // K4 item
+  int timed_cls;     // kernel-timing class of a grid item (-1: none)
 };
 
 struct Builder {
   fmg_ctx* c;
   std::vector<Item> items;
-  std::vector<OpDesc> prog;
-  bool small(int l) const { return l <= c->seq_max_level; }
-  void add(const OpDesc& op, bool in_seq, int cls = -1) {
-    if (in_seq) {
-      if (!items.empty() && items.back().seq && items.back().first + items.back().count == (int)prog.size()) {
-        items.back().count++;
-      } else {
-        Item it{};
-        it.seq = true;
-        it.first = (int)prog.size();
-        it.count = 1;
-        it.timed_cls = -1;
-        items.push_back(it);
-      }
-      prog.push_back(op);
-    } else {
-      Item it{};
-      it.seq = false;
-      it.op = op;
-      it.timed_cls = cls;
-      items.push_back(it);
-    }
+  void grid(const OpDesc& op, int cls = -1) {
+    Item it{};
+    it.kind = 0;
+    it.op = op;
+    it.timed_cls = cls;
+    items.push_back(it);
+  }
+  void k4(const K4Desc& d) {
+    Item it{};
+    it.kind = 1;
+    it.k4 = d;
+    it.timed_cls = -1;
+    items.push_back(it);
   }
 };
 
@@ -139,39 +131,58 @@ OpDesc mkop(int type, int l, int L) {
   return o;
 }
 
-// fmgResidual (Alg 3.2) at FMG level L, norm row `row`.
-void build_residual(Builder& b, int L, int row) {
+// Grid-only fmgResidual (API paths): decode sweep, residual, restriction, norms.
+void build_residual_grid(Builder& b, int L, int row) {
   fmg_ctx* c = b.c;
-  for (int l = 0; l < L; ++l) {  // decode sweep u_0..u_{L-1} (u_L fused into the residual)
+  for (int l = 0; l <= L; ++l) {
     OpDesc o = mkop(OP_DECODE, l, L);
     o.wu_in = c->wu_cur[l];
-    b.add(o, b.small(l), l == L - 1 && L == c->Lmax ? 2 : -1);
+    b.grid(o);
   }
   OpDesc o = mkop(OP_RESIDUAL, L, L);
-  o.wu_in = c->wu_cur[L];
   o.wr = wr(c, L, L);
-  b.add(o, b.small(L), L == c->Lmax ? 0 : -1);
+  b.grid(o);
   for (int l = L - 1; l >= 0; --l) {
     OpDesc q = mkop(OP_RESTRICT, l, L);
     q.wr = wr(c, l, L);
-    b.add(q, b.small(l), l == L - 1 && L == c->Lmax ? 3 : -1);
+    b.grid(q);
   }
   OpDesc n = mkop(OP_NORMS, 0, L);
   n.row = row;
-  b.add(n, true);
+  b.grid(n);
 }
 
-// cFas V(0,1) (Alg 3.1, nu = 1) + correction at FMG level L.
-void build_cfas(Builder& b, int L) {
+// One IR iteration at FMG level L: fmgResidual (Alg 3.2),
+// cFas V(0,1) (Alg 3.1, nu = 1), correction.  Levels <= lc run inside K4.
+void build_iteration(Builder& b, int L, int it) {
   fmg_ctx* c = b.c;
-  OpDesc o = mkop(OP_COARSE_CFAS, 0, L);
-  o.wr = wr(c, 0, L);
-  o.wu_in = c->wu_cur[0];
-  o.wu_out = wu(c, 0, L);
-  b.add(o, true);
-  c->wu_cur[0] = wu(c, 0, L);
+  const int lc = c->lc;
+  const bool fine = L == c->Lmax;
+  if (L > lc) {
+    OpDesc o = mkop(OP_RESIDUAL, L, L);
+    o.wr = wr(c, L, L);
+    b.grid(o, fine ? 0 : -1);
+    for (int l = L - 1; l > lc; --l) {
+      OpDesc q = mkop(OP_RESTRICT, l, L);
+      q.wr = wr(c, l, L);
+      b.grid(q, (fine && l == L - 1) ? 3 : -1);
+    }
+  }
+  K4Desc d{};
+  d.mode = 1;
+  d.L = L;
+  d.first = it == 0;
+  d.row = L * c->s.n_ir + it;
+  int top = L < lc ? L : lc;
+  for (int l = 0; l <= top; ++l) {
+    d.wr[l] = wr(c, l, L);
+    d.wu_in[l] = c->wu_cur[l];
+    d.wu_out[l] = wu(c, l, L);
+    c->wu_cur[l] = wu(c, l, L);
+  }
+  b.k4(d);
   const int k = c->s.cheb_degree;
-  for (int l = 1; l <= L; ++l) {
+  for (int l = lc + 1; l <= L; ++l) {
     for (int step = 1; step <= k; ++step) {
       OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
       q.step = step;
@@ -179,7 +190,7 @@ void build_cfas(Builder& b, int L) {
       q.wr = wr(c, l, L);
       q.wu_in = c->wu_cur[l];
       q.wu_out = wu(c, l, L);
-      b.add(q, b.small(l), (l == L && L == c->Lmax) ? 1 : -1);
+      b.grid(q, (fine && l == L) ? 1 : -1);
     }
     c->wu_cur[l] = wu(c, l, L);
   }
@@ -189,49 +200,44 @@ void build_cfas(Builder& b, int L) {
 void build_solve(Builder& b, int Lstop, int iters_last) {
   fmg_ctx* c = b.c;
   for (int l = 0; l <= c->Lmax; ++l) c->wu_cur[l] = wu(c, l, l);
-  OpDesc o = mkop(OP_COARSE_INIT, 0, 0);
-  o.wu_out = wu(c, 0, 0);
-  b.add(o, true);  // coarse-grid solve PAPER.md:786
+  K4Desc d{};
+  d.mode = 0;
+  d.wu_out[0] = wu(c, 0, 0);
+  b.k4(d);  // coarse-grid solve PAPER.md:786
   c->wu_cur[0] = wu(c, 0, 0);
   for (int L = 1; L <= Lstop; ++L) {
     // push level PAPER.md:788: ú_L = 0 (zeroed at solve start); the widening of
     // ú_{0..L-1} is value-preserving and happens at the next encode.
     c->wu_cur[L] = wu(c, L, L);
-    int iters = (L == Lstop) ? iters_last : c->s.n_ir;
-    for (int it = 0; it < iters; ++it) {
-      build_residual(b, L, L * c->s.n_ir + it);
-      build_cfas(b, L);
+    if (L > c->lc) {  // u_L = dec ú_L + P u_{L-1} = P u_{L-1} for the first residual
+      OpDesc o = mkop(OP_DECODE, L, L);
+      o.wu_in = c->wu_cur[L];
+      b.grid(o, (L == c->Lmax) ? 2 : -1);
     }
+    int iters = (L == Lstop) ? iters_last : c->s.n_ir;
+    for (int it = 0; it < iters; ++it) build_iteration(b, L, it);
   }
 }
 
 void mark(fmg_ctx* c, int cls) {
+  if (c->timing_cls == 4) cls = 4;  // class 4: every launch
   if (c->timing_cls != cls || cls < 0) return;
   if (c->ev_used >= (int)c->ev.size()) return;
   cudaEventRecordWithFlags(c->ev[c->ev_used++], c->cur, cudaEventRecordExternal);
 }
 
 int op_tiles(const fmg_ctx* c, const OpDesc& o) {
-  if (o.type == OP_NORMS || o.type == OP_COARSE_INIT || o.type == OP_COARSE_CFAS) return 1;
+  if (o.type == OP_NORMS) return 1;
   return c->tiles[o.l][0] * c->tiles[o.l][1] * c->tiles[o.l][2];
 }
 
-// Upload the op program into prog[slot] and issue every item on c->cur.
-int issue(fmg_ctx* c, Builder& b, int slot) {
-  size_t osz = op_size();
-  size_t need = std::max<size_t>(1, b.prog.size()) * osz;
-  if (c->prog_cap[slot] < need) {
-    c->prog[slot] = dalloc(c, need);
-    if (!c->prog[slot]) return FMG_ENOMEM;
-    c->prog_cap[slot] = need;
-  }
-  std::vector<char> host(need);
-  for (size_t i = 0; i < b.prog.size(); ++i) pack_op(host.data() + i * osz, b.prog[i]);
-  cudaError_t e = cudaMemcpy(c->prog[slot], host.data(), need, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return FMG_ECUDA;
+// Issue every item on c->cur (inside a capture or directly).
+void issue(fmg_ctx* c, const Builder& b) {
   for (const Item& it : b.items) {
-    if (it.seq) {
-      launch_seq(c->dim, c->p, c->cur, c->devctx, (const char*)c->prog[slot] + it.first * osz, it.count);
+    if (it.kind == 1) {
+      mark(c, -2);
+      launch_k4(c->dim, c->p, c->cur, c->devctx, it.k4, c->k4_smem);
+      mark(c, -2);
     } else {
       mark(c, it.timed_cls);
       launch_op(c->dim, c->p, c->cur, c->devctx, it.op, op_tiles(c, it.op));
@@ -239,7 +245,6 @@ int issue(fmg_ctx* c, Builder& b, int slot) {
     }
     c->launches++;
   }
-  return FMG_OK;
 }
 
 void zero_sections(fmg_ctx* c) {
@@ -271,17 +276,15 @@ int sync_check(fmg_ctx* c) {
   return FMG_OK;
 }
 
-// Run a freshly built program directly on the user stream (no graph).
+// Run a freshly built item list directly on the user stream (no graph).
 int run_direct(fmg_ctx* c, Builder& b) {
   c->cur = c->st;
   int save = c->timing_cls;
   long long save_l = c->launches;
   c->timing_cls = -1;
-  cudaStreamSynchronize(c->st);  // prog[1] may still be read by earlier work
-  int rc = issue(c, b, 1);
+  issue(c, b);
   c->timing_cls = save;
   c->launches = save_l;
-  if (rc) return rc;
   return sync_check(c);
 }
 
@@ -315,9 +318,14 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   build_coefs(dim, p, s->lambda_hi, s->alpha, s->cheb_degree, &c->cf);
   int TY, TZ;
   tile_shape(dim, p, &TY, &TZ);
-  // sequencer threshold: levels with at most `seq_tiles` tiles (env FMG_SEQ_TILES)
-  int seq_tiles = 2;
-  if (const char* e = getenv("FMG_SEQ_TILES")) seq_tiles = atoi(e);
+  // K4 owns the largest prefix of levels that fits its shared-memory budget
+  // (env FMG_LC caps it).
+  int lc_cap = Lmax;
+  if (const char* e = getenv("FMG_LC")) lc_cap = std::min(lc_cap, atoi(e));
+  c->lc = 0;
+  for (int l = 0; l <= lc_cap; ++l)
+    if (k4_smem_bytes(dim, p, l) <= 200 * 1024) c->lc = l;
+  c->k4_smem = k4_smem_bytes(dim, p, c->lc);
   int rc = FMG_OK;
   long long tot_parts = 0;
   DevCtxDesc dd{};
@@ -334,7 +342,6 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     c->tiles[l][1] = (g.NY + TY - 1) / TY;
     c->tiles[l][2] = (g.NZ + TZ - 1) / TZ;
     int nt = c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2];
-    if (nt <= seq_tiles) c->seq_max_level = l;
     c->u[l].stride = wu(c, l, Lmax);
     c->r[l].stride = wr(c, l, Lmax);
     c->u[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->u[l].stride);
@@ -349,8 +356,9 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     c->part_off[l] = tot_parts;
     tot_parts += nt;
   }
-  // FP64 workspace (finest size): U/W ping-pong, T ping-pong / Z, B; Y ping-pong + D (k >= 3)
-  int nbuf = s->cheb_degree >= 3 ? 7 : 4;
+  // FP64 workspace (finest size): U ping-pong, W ping-pong, T ping-pong / Z, B;
+  // Y ping-pong + D (k >= 3)
+  int nbuf = s->cheb_degree >= 3 ? 9 : 6;
   if (rc == FMG_OK) {
     for (int i = 0; i < nbuf && rc == FMG_OK; ++i) {
       c->buf[i] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
@@ -367,7 +375,14 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     c->err_part = (double*)dalloc(c, sizeof(double) * 2 * 148 * 16);
     c->status = (int*)dalloc(c, sizeof(int));
     c->devctx = dalloc(c, devctx_size());
-    if (!c->Ainv || !c->partials || !c->norms_dev || !c->err_part || !c->status || !c->devctx) rc = FMG_ENOMEM;
+    long long usm_n = 0;
+    for (int l = 0; l <= c->lc; ++l) {
+      dd.usm_off[l] = usm_n;
+      usm_n += (long long)std::pow((double)(p << (l + 1)), dim);
+    }
+    c->usm = (double*)dalloc(c, sizeof(double) * usm_n);
+    if (!c->Ainv || !c->partials || !c->norms_dev || !c->err_part || !c->status || !c->devctx || !c->usm)
+      rc = FMG_ENOMEM;
     else {
       cudaMemcpy(c->Ainv, Ai.data(), sizeof(double) * Ai.size(), cudaMemcpyHostToDevice);
       cudaMemset(c->status, 0, sizeof(int));
@@ -383,13 +398,18 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
         for (int k = 0; k < 3; ++k) dd.tiles[l][k] = c->tiles[l][k];
         dd.part[l] = c->partials + c->part_off[l];
       }
-      dd.U[0] = dd.W[0] = c->buf[0];
-      dd.U[1] = dd.W[1] = c->buf[1];
-      dd.T[0] = dd.Z = c->buf[2];
-      dd.T[1] = dd.B = c->buf[3];
-      dd.Y[0] = c->buf[4];
-      dd.Y[1] = c->buf[5];
-      dd.Dv = c->buf[6];
+      dd.U[0] = c->buf[0];
+      dd.U[1] = c->buf[1];
+      dd.W[0] = c->buf[2];
+      dd.W[1] = c->buf[3];
+      dd.T[0] = dd.Z = c->buf[4];
+      dd.T[1] = dd.B = c->buf[5];
+      dd.Y[0] = c->buf[6];
+      dd.Y[1] = c->buf[7];
+      dd.Dv = c->buf[8];
+      dd.usm = c->usm;
+      dd.lc = c->lc;
+      dd.n_cheb = s->cheb_degree;
       dd.Ainv = c->Ainv;
       dd.norms = c->norms_dev;
       dd.status = c->status;
@@ -411,35 +431,15 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
 int fmg_solve_async(fmg_ctx* c) {
   if (!c) return FMG_EINVAL;
   if (!c->graph) {
-    Builder b{c, {}, {}};
+    Builder b{c, {}};
     c->launches = 0;
     c->ev_used = 0;
     build_solve(b, c->Lmax, c->s.n_ir);
     c->cur = c->cap;
-    // upload the op program first (outside the capture)
-    size_t osz = op_size();
-    size_t need = std::max<size_t>(1, b.prog.size()) * osz;
-    if (c->prog_cap[0] < need) {
-      c->prog[0] = dalloc(c, need);
-      if (!c->prog[0]) return FMG_ENOMEM;
-      c->prog_cap[0] = need;
-    }
-    std::vector<char> host(need);
-    for (size_t i = 0; i < b.prog.size(); ++i) pack_op(host.data() + i * osz, b.prog[i]);
-    if (cudaMemcpy(c->prog[0], host.data(), need, cudaMemcpyHostToDevice) != cudaSuccess) return FMG_ECUDA;
     cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return cuda_err(e);
     zero_sections(c);
-    for (const Item& it : b.items) {
-      if (it.seq) {
-        launch_seq(c->dim, c->p, c->cur, c->devctx, (const char*)c->prog[0] + it.first * osz, it.count);
-      } else {
-        mark(c, it.timed_cls);
-        launch_op(c->dim, c->p, c->cur, c->devctx, it.op, op_tiles(c, it.op));
-        mark(c, it.timed_cls);
-      }
-      c->launches++;
-    }
+    issue(c, b);
     cudaGraph_t gr;
     e = cudaStreamEndCapture(c->cap, &gr);
     if (e != cudaSuccess) return cuda_err(e);
@@ -450,7 +450,6 @@ int fmg_solve_async(fmg_ctx* c) {
   cudaError_t e = cudaGraphLaunch(c->graph, c->st);
   if (e != cudaSuccess) return cuda_err(e);
   c->solved_L = c->Lmax;
-  // wu_cur reflects the end of a full solve (build_solve left it there)
   return FMG_OK;
 }
 
@@ -462,7 +461,7 @@ int fmg_solve(fmg_ctx* c) {
 
 int fmg_solve_upto(fmg_ctx* c, int Lstop, int iters_last) {
   if (!c || Lstop < 0 || Lstop > c->Lmax || iters_last < 0) return FMG_EINVAL;
-  Builder b{c, {}, {}};
+  Builder b{c, {}};
   c->cur = c->st;
   cudaStreamSynchronize(c->st);
   zero_sections(c);
@@ -489,8 +488,8 @@ int fmg_residual(fmg_ctx* c, double* host_norms) {
   double* row = c->norms_dev + ((size_t)L * c->s.n_ir) * c->levels;
   cudaStreamSynchronize(c->st);
   cudaMemcpy(keep.data(), row, sizeof(double) * c->levels, cudaMemcpyDeviceToHost);
-  Builder b{c, {}, {}};
-  build_residual(b, L, L * c->s.n_ir);
+  Builder b{c, {}};
+  build_residual_grid(b, L, L * c->s.n_ir);
   int rc = run_direct(c, b);
   if (rc) return rc;
   if (host_norms) {
@@ -505,11 +504,11 @@ int fmg_residual(fmg_ctx* c, double* host_norms) {
 // û_L into U[L & 1] (decode ops for l = 0..L, materialised).
 static int decode_solution(fmg_ctx* c, int* which) {
   int L = c->solved_L;
-  Builder b{c, {}, {}};
+  Builder b{c, {}};
   for (int l = 0; l <= L; ++l) {
     OpDesc o = mkop(OP_DECODE, l, L);
     o.wu_in = c->wu_cur[l];
-    b.add(o, b.small(l));
+    b.grid(o);
   }
   *which = L & 1;
   return run_direct(c, b);
@@ -598,7 +597,7 @@ int fmg_info(fmg_ctx* c, double* info) {
 }
 
 int fmg_enable_kernel_timing(fmg_ctx* c, int cls) {
-  if (!c || cls < -1 || cls > 3) return FMG_EINVAL;
+  if (!c || cls < -1 || cls > 4) return FMG_EINVAL;
   if (c->graph) {
     cudaGraphExecDestroy(c->graph);
     c->graph = nullptr;
@@ -609,6 +608,7 @@ int fmg_enable_kernel_timing(fmg_ctx* c, int cls) {
   if (cls >= 0) {
     int per = (cls == 1) ? c->s.cheb_degree : 1;
     int n = 2 * c->s.n_ir * per;
+    if (cls == 4) n = 2 * 20000;
     for (int i = 0; i < n; ++i) {
       cudaEvent_t e;
       cudaEventCreate(&e);
@@ -616,6 +616,19 @@ int fmg_enable_kernel_timing(fmg_ctx* c, int cls) {
     }
   }
   return FMG_OK;
+}
+
+int fmg_kernel_times(fmg_ctx* c, float* ms, int cap) {
+  if (!c || !ms) return -FMG_EINVAL;
+  cudaError_t e = cudaStreamSynchronize(c->st);
+  if (e != cudaSuccess) return -cuda_err(e);
+  int n = 0;
+  for (int i = 0; i + 1 < c->ev_used && n < cap; i += 2) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, c->ev[i], c->ev[i + 1]);
+    ms[n++] = t;
+  }
+  return n;
 }
 
 int fmg_kernel_time(fmg_ctx* c, double* total_ms, int* launches) {

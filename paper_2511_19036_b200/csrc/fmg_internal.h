@@ -45,11 +45,20 @@ int coarse_count(int dim, int p);
 int build_coarse_inverse(int dim, int p, double* Ainv);  // 0 on success
 
 // Operation descriptors (mirrors the device Op).
-enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_COARSE_INIT, OP_COARSE_CFAS, OP_CFAS1, OP_CHEB };
+enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_CFAS1 = 6, OP_CHEB };
 struct OpDesc {
   int type, l, L, step, last;
   int wr, wu_in, wu_out;
   int row;
+};
+
+// K4 (shared-memory coarse hierarchy kernel) launch descriptor.
+struct K4Desc {
+  int mode;   // 0: coarse-grid solve; 1: one IR iteration at FMG level L
+  int L;      // FMG level
+  int first;  // first IR iteration of FMG level L
+  int row;    // norm row
+  int wr[kMaxLev], wu_in[kMaxLev], wu_out[kMaxLev];
 };
 
 // Everything the device context needs.
@@ -65,6 +74,9 @@ struct DevCtxDesc {
   const double* Ainv;
   double* norms;
   int* status;
+  double* usm;
+  long long usm_off[kMaxLev];
+  int lc, n_cheb;
   Coefs cf;
 };
 
@@ -82,7 +94,8 @@ size_t op_size();
 void fill_devctx(void* host_buf, const DevCtxDesc& d);
 void pack_op(void* dst, const OpDesc& od);
 void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int ntiles);
-void launch_seq(int dim, int p, cudaStream_t st, const void* devctx, const void* prog_dev, int count);
+int k4_smem_bytes(int dim, int p, int lc);
+void launch_k4(int dim, int p, cudaStream_t st, const void* devctx, const K4Desc& a, int smem);
 void launch_errors(const Launch& L, const double* U, const Geom& g, double* partials, int* nparts);
 void launch_bfp_encode(const double* x, long long n, int w, uint32_t* mant, int8_t* exps, int* status,
                        cudaStream_t st);

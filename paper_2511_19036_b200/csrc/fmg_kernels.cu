@@ -3,10 +3,10 @@
 // Structure: every step of the method is a *tile operation* (a __device__
 // function that produces one output tile of one level: 32 x TY (x TZ) points,
 // 256 threads, one warp per 32-entry x row = one BFP block).  A step is
-// executed either by a grid kernel (one CTA per tile, `k_op`) or, for the
-// small levels, inside a single-CTA sequencer kernel (`k_seq`) that runs a
-// list of operations back to back with __syncthreads between them (no launch
-// gaps).  All kernels use programmatic dependent launch (griddepcontrol).
+// executed by a grid kernel (one CTA per tile, `k_op`).  The small levels
+// 0..lc live in shared memory of one CTA (`k4_kernel`), which runs their part
+// of every IR iteration back to back (no launch gaps, no global round trips).
+// All kernels use programmatic dependent launch (griddepcontrol).
 //
 // Every floating-point expression follows the canonical evaluation order of
 // DESIGN.md §3 with explicit fma(); compiled with -fmad=false.  Tensor-product
@@ -111,17 +111,36 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
   }
   if (words) {
     unsigned long long field = (unsigned long long)m & ((1ULL << w) - 1ULL);
-    int o = lane * w;
     uint32_t mine0 = 0u, mine1 = 0u;
-    for (int j = 0; j < w; ++j) {
-      int s = o - 32 * j;
-      uint32_t c = 0u;
-      if (s > -w && s < 32) c = s >= 0 ? (uint32_t)(field << s) : (uint32_t)(field >> (-s));
-      uint32_t word = __reduce_or_sync(FULL, c);
-      if (j < 32) {
+    if (w <= 8) {
+      // narrow: one redux.or per output word
+      int o = lane * w;
+      for (int j = 0; j < w; ++j) {
+        int s = o - 32 * j;
+        uint32_t c = 0u;
+        if (s > -w && s < 32) c = s >= 0 ? (uint32_t)(field << s) : (uint32_t)(field >> (-s));
+        uint32_t word = __reduce_or_sync(FULL, c);
         if (lane == j) mine0 = word;
-      } else if (lane == j - 32) {
-        mine1 = word;
+      }
+    } else {
+      // wide: word j gathers its <= ceil(32/w)+1 entries by shuffles
+      const int K = (32 + w - 1) / w + 1;
+      uint32_t flo = (uint32_t)field, fhi = (uint32_t)(field >> 32);
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        int j = lane + 32 * half;
+        if (half == 1 && w <= 32) break;
+        int e0 = (32 * j) / w;
+        uint32_t acc = 0u;
+        for (int k = 0; k < K; ++k) {
+          int e = e0 + k;
+          int src = e < 32 ? e : 31;
+          uint32_t lo_ = __shfl_sync(FULL, flo, src), hi_ = __shfl_sync(FULL, fhi, src);
+          unsigned long long f = ((unsigned long long)hi_ << 32) | lo_;
+          int s = e * w - 32 * j;
+          if (e < 32 && s < 32 && s > -w) acc |= s >= 0 ? (uint32_t)(f << s) : (uint32_t)(f >> (-s));
+        }
+        if (half == 0) mine0 = acc; else mine1 = acc;
       }
     }
     if (lane < w) words[lane] = mine0;
@@ -155,13 +174,15 @@ template <int D, int P> struct Plan {
   static constexpr int NV2 = (D == 3) ? BX * BY * CBZ : 0; // P y-pass out (3D)
   static constexpr int PRO_REGION = NCB + NV1 + NV2;
   static constexpr int A_REGION = 2 * NAB + 2 * NCS;
-  static constexpr int A_SMEM = (NU + (PRO_REGION > A_REGION ? PRO_REGION : A_REGION)) * 8;
+  static constexpr int A_SMEM = (NU + (PRO_REGION > A_REGION ? PRO_REGION : A_REGION)) * 8 + 32 * TY * TZ * 8;
   // decode/prolong tile (output only, no halo)
   static constexpr int DBX = 32, DBY = TY, DBZ = (D == 3) ? TZ : 1;
   static constexpr int DCBX = P * ((DBX - 1) / (2 * P) + 2) + 1;
   static constexpr int DCBY = P * ((DBY - 1) / (2 * P) + 2) + 1;
   static constexpr int DCBZ = (D == 3) ? P * ((DBZ - 1) / (2 * P) + 2) + 1 : 1;
-  static constexpr int D_SMEM = (DCBX * DCBY * DCBZ + DBX * DCBY * DCBZ + ((D == 3) ? DBX * DBY * DCBZ : 0)) * 8;
+  static constexpr int D_SCR = DCBX * DCBY * DCBZ + DBX * DCBY * DCBZ + ((D == 3) ? DBX * DBY * DCBZ : 0);
+  static constexpr int D_SMEM = (D_SCR + DBX * DBY * DBZ) * 8;
+  static constexpr int NPU = DBX * DBY * DBZ;  // emitted-u prolongation tile
   // restriction tile (coarse output 32 x TY x TZ); x pass gathered from global
   static constexpr int FBY = 2 * TY + 4 * P - 3, FBZ = (D == 3) ? 2 * TZ + 4 * P - 3 : 1;
   static constexpr int NXR = 32 * FBY * FBZ;
@@ -189,9 +210,13 @@ struct LevelDev {
 
 struct DevCtx {
   LevelDev lv[kMaxLev];
-  double* U[2];  // decoded u_l (ping-pong by level parity)
+  double* U[2];  // decoded u_l (ping-pong by level parity), emitted by the cFas finalize
   double* T[2];  // residual temporaries t_l
   double* W[2];  // w_l = z_l + dec ý_l
+  double* usm;   // K4: dense u_l of the smem levels, persisted between launches
+  long long usm_off[kMaxLev];
+  int lc;        // K4 handles levels 0..lc in shared memory
+  int n_cheb;    // Chebyshev degree k
   double* Z;     // z_l (only for l < L)
   double* B;     // b_l = dec r_l - A z_l
   double* Y[2];  // Chebyshev iterates (k >= 3)
@@ -208,7 +233,7 @@ using Op = OpDesc;  // one step of the method on one level (fmg_internal.h)
 
 __device__ __forceinline__ int op_tiles(const DevCtx& c, const Op& op) {
   const LevelDev& lv = c.lv[op.l];
-  if (op.type == OP_NORMS || op.type == OP_COARSE_INIT || op.type == OP_COARSE_CFAS) return 1;
+  if (op.type == OP_NORMS) return 1;
   return lv.tx * lv.ty * lv.tz;
 }
 
@@ -491,8 +516,9 @@ __device__ void tile_decode(const DevCtx& c, const Op& op, int tile, double* sm)
   }
 }
 
-// S2+S3+S4: t_L = f_L - A_L (dec ú_L + P u_{L-1}) on the tile, r_L = enc(t_L),
-// ||t_L||^2 partial.  u_L is never materialised.
+// S3+S4: t_L = f_L - A_L u_L on the tile, r_L = enc(t_L), ||t_L||^2 partial
+// (PAPER.md:738-739).  u_L = dec ú_L + P u_{L-1} (S2) was emitted by the previous
+// sweep's finalize (or by the decode op at the start of the FMG level).
 template <int D, int P>
 __device__ void tile_residual(const DevCtx& c, const Op& op, int tile, double* sm) {
   using PL = Plan<D, P>;
@@ -502,14 +528,7 @@ __device__ void tile_residual(const DevCtx& c, const Op& op, int tile, double* s
   tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
   double* U = sm;
   double* R1 = sm + PL::NU;
-  {
-    double* cb = R1;
-    double* v1 = cb + PL::NCB;
-    double* v2 = v1 + PL::NV1;
-    box_prolong<D, P, PL::BX, PL::BY, PL::BZ, PL::CBX, PL::CBY, PL::CBZ>(
-        c.U[(op.L - 1) & 1], c.lv[op.L - 1].g, g.n, x0 - P, y0 - P, z0 - P, c.cf, cb, v1, v2, U);
-  }
-  box_add_decode<D, PL::BX, PL::BY, PL::BZ, P>(lv, op.wu_in, x0, y0 - P, (D == 3) ? z0 - P : 0, U);
+  box_load<D, P>(c.U[op.L & 1], g, x0, y0, z0, U);
   double* AB = R1;
   double* CS = R1 + 2 * PL::NAB;
   a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
@@ -640,71 +659,30 @@ __device__ void op_norms(const DevCtx& c, const Op& op, double* sm) {
   }
 }
 
-// S6 / S10 on level 0 (dense A_0^{-1}, canonical mat-vec DESIGN.md §3.7).
-// INIT:  ú_0 = enc_{wu_out}(A_0^{-1} f_0)
-// CFAS:  ý_0 = enc_{wr}(A_0^{-1} dec r_0); W_0 = dec ý_0; ú_0 = enc(dec ú_0 + dec ý_0)
-template <int D, int P>
-__device__ void op_coarse(const DevCtx& c, const Op& op, double* sm) {
-  constexpr int n = 2 * P, m = 2 * P - 1;
-  constexpr int ROWS = (D == 3) ? n * n : n;
-  const LevelDev& lv = c.lv[0];
-  double* X = sm;
-  double* Y = sm + ROWS * 32;
-  const int lane = threadIdx.x, tid = threadIdx.y * 32 + threadIdx.x;
-  for (int row = threadIdx.y; row < ROWS; row += NWARP) {
-    int y = row % n, z = row / n;
-    double v;
-    if (op.type == OP_COARSE_INIT) {
-      bool unk = unk1(lane, n) && unk1(y, n) && (D == 2 || unk1(z, n));
-      v = 0.0;
-      if (unk) {
-        v = c.cf.rhs_c * lv.gtab[lane];
-        v = v * lv.gtab[y];
-        if (D == 3) v = v * lv.gtab[z];
-      }
-    } else {
-      v = warp_decode(lv.rmant + (long long)row * lv.rstride, lv.rexp[row], op.wr, lane);
-    }
-    X[row * 32 + lane] = v;
-    Y[row * 32 + lane] = 0.0;
-  }
-  __syncthreads();
-  for (int I = tid; I < c.n0; I += NT) {
-    double acc = 0.0;
-    for (int J = 0; J < c.n0; ++J) {
-      int jx = J % m + 1, jy = (J / m) % m + 1, jz = (D == 3) ? J / (m * m) + 1 : 0;
-      acc = fma(c.Ainv[(long long)I * c.n0 + J], X[(jz * n + jy) * 32 + jx], acc);
-    }
-    int ix = I % m + 1, iy = (I / m) % m + 1, iz = (D == 3) ? I / (m * m) + 1 : 0;
-    Y[(iz * n + iy) * 32 + ix] = acc;
-  }
-  __syncthreads();
-  for (int row = threadIdx.y; row < ROWS; row += NWARP) {
-    double y = Y[row * 32 + lane];
-    uint32_t* uw = lv.umant + (long long)row * lv.ustride;
-    if (op.type == OP_COARSE_INIT) {
-      warp_encode(y, op.wu_out, uw, lv.uexp + row, lane, c.status);
-    } else {
-      double yq = warp_encode(y, op.wr, nullptr, nullptr, lane, c.status);
-      c.W[0][row * 32 + lane] = yq;
-      double uo = warp_decode(uw, lv.uexp[row], op.wu_in, lane);
-      warp_encode(uo + yq, op.wu_out, uw, lv.uexp + row, lane, c.status);
-    }
-  }
-  __syncthreads();
-}
-
 // Finalise a cFas level at one output row:
-// ý = enc_wr(y); W_l = z_l + dec ý (l < L); ú_l = enc_{wu_out}(dec_{wu_in} ú_l + dec ý).
+// ý = enc_wr(y); W_l = z_l + dec ý (l < L); ú_l = enc_{wu_out}(dec_{wu_in} ú_l + dec ý);
+// and the next sweep's decoded u_l = dec ú_l + P_l u_{l-1} (S2).
 __device__ __forceinline__ void cfas_finalize(const DevCtx& c, const Op& op, const LevelDev& lv, long long idx,
-                                              double y) {
+                                              double y, double pu) {
   const int lane = threadIdx.x;
   double yq = warp_encode(y, op.wr, nullptr, nullptr, lane, c.status);
   if (op.l < op.L) c.W[op.l & 1][idx] = c.Z[idx] + yq;
   long long blk = idx >> 5;
   uint32_t* uw = lv.umant + blk * lv.ustride;
   double uo = warp_decode(uw, lv.uexp[blk], op.wu_in, lane);
-  warp_encode(uo + yq, op.wu_out, uw, lv.uexp + blk, lane, c.status);
+  double uq = warp_encode(uo + yq, op.wu_out, uw, lv.uexp + blk, lane, c.status);
+  c.U[op.l & 1][idx] = uq + pu;
+}
+
+// P_l u_{l-1} on the output tile (for the emitted u_l), into `pu` (32 x TY x TZ).
+template <int D, int P>
+__device__ void tile_pu(const DevCtx& c, int l, int x0, int y0, int z0, double* scratch, double* pu) {
+  using PL = Plan<D, P>;
+  double* cb = scratch;
+  double* v1 = cb + PL::DCBX * PL::DCBY * PL::DCBZ;
+  double* v2 = v1 + PL::DBX * PL::DCBY * PL::DCBZ;
+  box_prolong<D, P, PL::DBX, PL::DBY, PL::DBZ, PL::DCBX, PL::DCBY, PL::DCBZ>(
+      c.U[(l - 1) & 1], c.lv[l - 1].g, c.lv[l].g.n, x0, y0, z0, c.cf, cb, v1, v2, pu);
 }
 
 __device__ __forceinline__ double inv_diag(const Coefs& cf, int D, int P, int l, int x, int y, int z) {
@@ -732,8 +710,37 @@ __device__ void tile_cfas1(const DevCtx& c, const Op& op, int tile, double* sm) 
   }
   double* AB = R1;
   double* CS = R1 + 2 * PL::NAB;
+  double* PU = R1 + (PL::PRO_REGION > PL::A_REGION ? PL::PRO_REGION : PL::A_REGION);
   a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
   const int lane = threadIdx.x;
+  double zsave[(PL::TY * PL::TZ + NWARP - 1) / NWARP], bsave[(PL::TY * PL::TZ + NWARP - 1) / NWARP];
+  if (op.last) {  // k == 1: keep b and z, then prolong u_{l-1} for the emitted u_l
+    int k = 0;
+    for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP, ++k) {
+      int ty = row % PL::TY, tz = row / PL::TY;
+      double az = a_final<D, P>(g, x0, y0, z0, ty, tz, c.cf, AB, CS);
+      zsave[k] = U[((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane];
+      bsave[k] = az;
+    }
+    __syncthreads();
+    tile_pu<D, P>(c, op.l, x0, y0, z0, R1, PU);
+    k = 0;
+    for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP, ++k) {
+      int ty = row % PL::TY, tz = row / PL::TY;
+      int y = y0 + ty, z = z0 + tz, x = x0 + lane;
+      if (y >= g.NY || z >= g.NZ) continue;
+      bool unk = unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(z, g.n));
+      long long idx = ((long long)z * g.NY + y) * g.NX + x;
+      long long blk = idx >> 5;
+      double rv = warp_decode(lv.rmant + blk * lv.rstride, lv.rexp[blk], op.wr, lane);
+      double b = rv - bsave[k];
+      double invD = unk ? inv_diag(c.cf, D, P, op.l, x, y, z) : 0.0;
+      double d = c.cf.inv_theta * (invD * b);
+      if (op.l < op.L) c.Z[idx] = zsave[k];
+      cfas_finalize(c, op, lv, idx, d, PU[row * 32 + lane]);
+    }
+    return;
+  }
   for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
     int ty = row % PL::TY, tz = row / PL::TY;
     int y = y0 + ty, z = z0 + tz, x = x0 + lane;
@@ -745,15 +752,9 @@ __device__ void tile_cfas1(const DevCtx& c, const Op& op, int tile, double* sm) 
     double rv = warp_decode(lv.rmant + blk * lv.rstride, lv.rexp[blk], op.wr, lane);
     double b = rv - az;
     double zc = U[((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane];
-    if (op.last) {
-      double invD = unk ? inv_diag(c.cf, D, P, op.l, x, y, z) : 0.0;
-      double d = c.cf.inv_theta * (invD * b);
-      if (op.l < op.L) c.Z[idx] = zc;
-      cfas_finalize(c, op, lv, idx, d);
-    } else {
-      c.B[idx] = b;
-      if (op.l < op.L) c.Z[idx] = zc;
-    }
+    c.B[idx] = b;
+    if (op.l < op.L) c.Z[idx] = zc;
+    (void)unk;
   }
 }
 
@@ -791,6 +792,8 @@ __device__ void tile_cheb(const DevCtx& c, const Op& op, int tile, double* sm) {
   }
   double* AB = R1;
   double* CS = R1 + 2 * PL::NAB;
+  double* PU = R1 + (PL::PRO_REGION > PL::A_REGION ? PL::PRO_REGION : PL::A_REGION);
+  if (op.last) tile_pu<D, P>(c, op.l, x0, y0, z0, R1, PU);
   a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
   const int lane = threadIdx.x;
   for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
@@ -808,7 +811,7 @@ __device__ void tile_cheb(const DevCtx& c, const Op& op, int tile, double* sm) {
     double d = fma(c.cf.cal[op.step - 1], dprev, c.cf.cbe[op.step - 1] * (invD * q));
     double yv = yprev + d;
     if (op.last) {
-      cfas_finalize(c, op, lv, idx, yv);
+      cfas_finalize(c, op, lv, idx, yv, PU[row * 32 + lane]);
     } else {
       c.Y[(op.step + 1) & 1][idx] = yv;
       c.Dv[idx] = d;
@@ -823,8 +826,6 @@ __device__ __forceinline__ void run_op(const DevCtx& c, const Op& op, int tile, 
     case OP_RESIDUAL: tile_residual<D, P>(c, op, tile, sm); break;
     case OP_RESTRICT: tile_restrict<D, P>(c, op, tile, sm); break;
     case OP_NORMS: op_norms(c, op, sm); break;
-    case OP_COARSE_INIT:
-    case OP_COARSE_CFAS: op_coarse<D, P>(c, op, sm); break;
     case OP_CFAS1: tile_cfas1<D, P>(c, op, tile, sm); break;
     case OP_CHEB: tile_cheb<D, P>(c, op, tile, sm); break;
   }
@@ -852,22 +853,487 @@ __global__ void __launch_bounds__(NT) k_op(const DevCtx* __restrict__ cp, Op op)
   run_op<D, P>(sc, op, blockIdx.x, sm);
 }
 
-// Sequencer kernel: one CTA runs ops [first, first+count) of `prog` over all
-// their tiles (small levels), with __syncthreads between tiles/ops.
+// =============================================== K4: coarse hierarchy ======
+// One 512-thread CTA owns levels 0..lc, stored densely (n_l^d doubles, x
+// fastest, no padding) in shared memory: the restriction tail, the norms, the
+// exact coarse solve, the cFas sweep with the corrections and the emitted u_l
+// of those levels run back to back with only __syncthreads between phases (no
+// launch gaps, no global round trips).  Same canonical expression trees as the
+// tile ops.  For FMG levels L <= lc the whole IR iteration
+// (residual included) runs here.
+constexpr int NW4 = 16, NT4 = 32 * NW4;
+constexpr int K4_MAX_SMEM = 200 * 1024;  // dynamic smem budget of the K4 CTA
+
+using K4Args = K4Desc;
+
+__host__ __device__ inline int ipow(int n, int d) { return d == 3 ? n * n * n : n * n; }
+
+// smem offsets (doubles): per level U, T, RQ, W blocks, then 6 scratch arrays of the top level
+__host__ __device__ inline int k4_level_off(int D, int P, int l) {
+  int o = 0;
+  for (int k = 0; k < l; ++k) o += 4 * ipow(P << (k + 1), D);
+  return o;
+}
+__host__ __device__ inline int k4_smem_doubles(int D, int P, int lc) {
+  return k4_level_off(D, P, lc + 1) + 6 * ipow(P << (lc + 1), D);
+}
+
+struct K4Lvl {
+  int n, len;
+  double *U, *T, *RQ, *W;
+};
+
+__device__ __forceinline__ K4Lvl k4_lvl(int D, int P, int l, double* sm) {
+  K4Lvl v;
+  v.n = P << (l + 1);
+  v.len = ipow(v.n, D);
+  // offset of level l: 4 * sum_{k<l} (P 2^(k+1))^D  (geometric sum)
+  const int r = D == 3 ? 8 : 4;                         // ratio between consecutive levels
+  const int first = ipow(2 * P, D);
+  double* b = sm + 4 * first * ((l == 0) ? 0 : ((1 << (D * l)) - 1) / (r - 1));
+  v.U = b;
+  v.T = b + v.len;
+  v.RQ = b + 2 * v.len;
+  v.W = b + 3 * v.len;
+  return v;
+}
+
+__device__ __forceinline__ double rd(const double* a, int j, int n) { return (j >= 0 && j < n) ? a[j] : 0.0; }
+
+// out = A_l in (dense level arrays); scratch: 4 * len.
 template <int D, int P>
-__global__ void __launch_bounds__(NT) k_seq(const DevCtx* __restrict__ cp, const Op* __restrict__ prog, int count) {
+__device__ void k4_A(const Coefs& cf, int l, int n, const double* in, double* out, double* s) {
+  const int lane = threadIdx.x, w = threadIdx.y, len = ipow(n, D), rows = len / n;
+  double* a = s;
+  double* b = s + len;
+  for (int r = w; r < rows; r += NW4)
+    for (int x = lane; x < n; x += 32) {
+      const double* u = in + r * n;
+      bool ok = unk1(x, n);
+      int tau = ok ? x % P : 0;
+      double aa = 0.0, bb = 0.0;
+#pragma unroll
+      for (int o = 0; o <= 2 * P; ++o) {
+        double v = rd(u, x - P + o, n);
+        aa = fma(cf.Mc[tau][o], v, aa);
+        bb = fma(cf.Kc[tau][o], v, bb);
+      }
+      a[r * n + x] = ok ? aa : 0.0;
+      b[r * n + x] = ok ? bb : 0.0;
+    }
+  __syncthreads();
+  if constexpr (D == 2) {
+    for (int y = w; y < n; y += NW4) {
+      bool oky = unk1(y, n);
+      int tau = oky ? y % P : 0;
+      for (int x = lane; x < n; x += 32) {
+        double d = 0.0, e = 0.0;
+#pragma unroll
+        for (int o = 0; o <= 2 * P; ++o) {
+          int j = y - P + o;
+          bool in_ = j >= 0 && j < n;
+          d = fma(cf.Kc[tau][o], in_ ? a[j * n + x] : 0.0, d);
+          e = fma(cf.Mc[tau][o], in_ ? b[j * n + x] : 0.0, e);
+        }
+        out[y * n + x] = (oky && unk1(x, n)) ? d + e : 0.0;
+      }
+    }
+  } else {
+    double* c = s + 2 * len;
+    double* sv = s + 3 * len;
+    for (int r = w; r < n * n; r += NW4) {  // rows (z, y)
+      int y = r % n, z = r / n;
+      bool oky = unk1(y, n);
+      int tau = oky ? y % P : 0;
+      for (int x = lane; x < n; x += 32) {
+        double cc = 0.0, dd = 0.0, e = 0.0;
+#pragma unroll
+        for (int o = 0; o <= 2 * P; ++o) {
+          int j = y - P + o;
+          bool in_ = j >= 0 && j < n;
+          double av = in_ ? a[(z * n + j) * n + x] : 0.0, bv = in_ ? b[(z * n + j) * n + x] : 0.0;
+          cc = fma(cf.Mc[tau][o], av, cc);
+          dd = fma(cf.Kc[tau][o], av, dd);
+          e = fma(cf.Mc[tau][o], bv, e);
+        }
+        c[r * n + x] = oky ? cc : 0.0;
+        sv[r * n + x] = oky ? dd + e : 0.0;
+      }
+    }
+    __syncthreads();
+    const double h = pow2(-(l + 1));
+    for (int r = w; r < n * n; r += NW4) {
+      int y = r % n, z = r / n;
+      bool okz = unk1(z, n) && unk1(y, n);
+      int tau = unk1(z, n) ? z % P : 0;
+      for (int x = lane; x < n; x += 32) {
+        double acc = 0.0;
+#pragma unroll
+        for (int o = 0; o <= 2 * P; ++o) {
+          int j = z - P + o;
+          acc = fma(cf.Kc[tau][o], (j >= 0 && j < n) ? c[(j * n + y) * n + x] : 0.0, acc);
+        }
+#pragma unroll
+        for (int o = 0; o <= 2 * P; ++o) {
+          int j = z - P + o;
+          acc = fma(cf.Mc[tau][o], (j >= 0 && j < n) ? sv[(j * n + y) * n + x] : 0.0, acc);
+        }
+        out[r * n + x] = (okz && unk1(x, n)) ? acc * h : 0.0;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// fine = P_lf coarse (dense); scratch: len_f (x-pass) + len_f/2 (y-pass, 3D).
+template <int D, int P>
+__device__ void k4_P(const Coefs& cf, int nf, const double* coarse, double* fine, double* s) {
+  const int lane = threadIdx.x, w = threadIdx.y, nc = nf / 2;
+  double* t1 = s;  // [cz][cy][xf]
+  const int rows1 = (D == 3) ? nc * nc : nc;
+  for (int r = w; r < rows1; r += NW4)
+    for (int x = lane; x < nf; x += 32) {
+      bool ok = unk1(x, nf);
+      int rx = ok ? x % (2 * P) : 0, base = ok ? P * (x / (2 * P)) : 0;
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) acc = fma(cf.Pw[rx][t], rd(coarse + r * nc, base + t, nc), acc);
+      t1[r * nf + x] = ok ? acc : 0.0;
+    }
+  __syncthreads();
+  double* t2 = (D == 3) ? s + nc * nc * nf : fine;  // [cz][yf][xf]
+  const int rows2 = (D == 3) ? nc * nf : nf;
+  for (int r = w; r < rows2; r += NW4) {
+    int y = r % nf, cz = r / nf;
+    bool ok = unk1(y, nf);
+    int ry = ok ? y % (2 * P) : 0, base = ok ? P * (y / (2 * P)) : 0;
+    for (int x = lane; x < nf; x += 32) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t <= P; ++t) {
+        int j = base + t;
+        acc = fma(cf.Pw[ry][t], (j < nc) ? t1[(cz * nc + j) * nf + x] : 0.0, acc);
+      }
+      t2[r * nf + x] = ok ? acc : 0.0;
+    }
+  }
+  __syncthreads();
+  if constexpr (D == 3) {
+    for (int r = w; r < nf * nf; r += NW4) {
+      int y = r % nf, z = r / nf;
+      bool ok = unk1(z, nf);
+      int rz = ok ? z % (2 * P) : 0, base = ok ? P * (z / (2 * P)) : 0;
+      for (int x = lane; x < nf; x += 32) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t <= P; ++t) {
+          int j = base + t;
+          acc = fma(cf.Pw[rz][t], (j < nc) ? t2[(j * nf + y) * nf + x] : 0.0, acc);
+        }
+        fine[r * nf + x] = ok ? acc : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// coarse = R fine; fine given by (ptr, row stride sy, plane stride sz) with x < nf
+// valid (global padded or dense smem).  scratch: nc*nf^(d-1) + nc^2*nf (3D).
+template <int D, int P>
+__device__ void k4_R(const Coefs& cf, int nf, const double* fine, long long sy, long long sz, double* coarse,
+                     double* s) {
+  const int lane = threadIdx.x, w = threadIdx.y, nc = nf / 2;
+  double* t1 = s;  // [zf][yf][xc]
+  const int rows1 = (D == 3) ? nf * nf : nf;
+  for (int r = w; r < rows1; r += NW4) {
+    int yf = r % nf, zf = r / nf;
+    const double* row = fine + (long long)zf * sz + (long long)yf * sy;
+    for (int x = lane; x < nc; x += 32) {
+      bool ok = unk1(x, nc);
+      int tau = ok ? x % P : 0;
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t <= 4 * P - 2; ++t) {
+        int j = 2 * x - (2 * P - 1) + t;
+        acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? row[j] : 0.0, acc);
+      }
+      t1[r * nc + x] = ok ? acc : 0.0;
+    }
+  }
+  __syncthreads();
+  double* t2 = (D == 3) ? s + nf * nf * nc : coarse;  // [zf][yc][xc]
+  const int rows2 = (D == 3) ? nf * nc : nc;
+  for (int r = w; r < rows2; r += NW4) {
+    int yc = r % nc, zf = r / nc;
+    bool ok = unk1(yc, nc);
+    int tau = ok ? yc % P : 0;
+    for (int x = lane; x < nc; x += 32) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t <= 4 * P - 2; ++t) {
+        int j = 2 * yc - (2 * P - 1) + t;
+        acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t1[(zf * nf + j) * nc + x] : 0.0, acc);
+      }
+      t2[r * nc + x] = ok ? acc : 0.0;
+    }
+  }
+  __syncthreads();
+  if constexpr (D == 3) {
+    for (int r = w; r < nc * nc; r += NW4) {
+      int yc = r % nc, zc = r / nc;
+      bool ok = unk1(zc, nc);
+      int tau = ok ? zc % P : 0;
+      for (int x = lane; x < nc; x += 32) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t <= 4 * P - 2; ++t) {
+          int j = 2 * zc - (2 * P - 1) + t;
+          acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t2[(j * nc + yc) * nc + x] : 0.0, acc);
+        }
+        coarse[r * nc + x] = ok ? acc : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Encode the dense level array `v` into section (mant, exps, stride) at width w
+// (global padded rows), storing the quantised values into `q` (may alias v).
+__device__ void k4_encode(const LevelDev& lv, int D, int n, const double* v, uint32_t* mant, int8_t* exps,
+                          int stride, int w, double* q, int* status) {
+  const int lane = threadIdx.x, nxb = lv.g.NX >> 5, rows = (D == 3) ? n * n : n;
+  for (int rb = threadIdx.y; rb < rows * nxb; rb += NW4) {
+    int r = rb / nxb, xb = rb % nxb;
+    int x = xb * 32 + lane;
+    double val = x < n ? v[r * n + x] : 0.0;
+    long long blk = (long long)r * nxb + xb;
+    double qq = warp_encode(val, w, mant ? mant + blk * stride : nullptr, exps ? exps + blk : nullptr, lane, status);
+    if (q && x < n) q[r * n + x] = qq;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double k4_invd(const Coefs& cf, int D, int P, int l, int n, int e) {
+  int x = e % n, y = (e / n) % n, z = (D == 3) ? e / (n * n) : 0;
+  if (!unk1(x, n) || !unk1(y, n) || (D == 3 && !unk1(z, n))) return 0.0;
+  return cf.invd[((D == 3 ? z % P : 0) * P + y % P) * P + x % P] * pow2((l + 1) * (D - 2));
+}
+
+// Copy a dense level into a padded global array (zeros in the padding).
+__device__ void k4_to_global(int D, int n, const double* v, double* g, const Geom& gg) {
+  const int rows = (D == 3) ? n * n : n;
+  for (int r = threadIdx.y; r < rows; r += NW4)
+    for (int x = threadIdx.x; x < gg.NX; x += 32) g[(long long)r * gg.NX + x] = x < n ? v[r * n + x] : 0.0;
+}
+
+template <int D, int P>
+__global__ void __launch_bounds__(NT4) k4_kernel(const DevCtx* __restrict__ cp, K4Args a) {
   extern __shared__ double sm[];
   __shared__ DevCtx sc;
+  __shared__ double red[NT4];
   pdl_wait();
   pdl_trigger();
-  load_ctx(cp, &sc);
-  for (int i = 0; i < count; ++i) {
-    Op op = prog[i];
-    int nt = op_tiles(sc, op);
-    for (int t = 0; t < nt; ++t) {
-      run_op<D, P>(sc, op, t, sm);
+  {
+    const unsigned long long* src = (const unsigned long long*)cp;
+    unsigned long long* dst = (unsigned long long*)&sc;
+    for (int i = threadIdx.y * 32 + threadIdx.x; i < (int)(sizeof(DevCtx) / 8); i += NT4) dst[i] = src[i];
+    __syncthreads();
+  }
+  const DevCtx& c = sc;
+  const Coefs& cf = c.cf;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int lc = c.lc;
+  const int L = a.L, lce = L < lc ? L : lc;
+  double* scr = sm + k4_level_off(D, P, lc + 1);
+  const int lenc = ipow(P << (lc + 1), D);
+  double* S0 = scr;              // A / P / R scratch (4 arrays)
+  double* SZ = scr + 4 * lenc;   // z_l
+  double* SB = scr + 5 * lenc;   // b_l / p u_{l-1}
+
+  if (a.mode == 0) {
+    // ú_0 = reg(A_0^{-1} f_0); u_0 = dec ú_0
+    K4Lvl v0 = k4_lvl(D, P, 0, sm);
+    const int n = v0.n, m = 2 * P - 1;
+    const LevelDev& lv = c.lv[0];
+    for (int e = tid; e < v0.len; e += NT4) {
+      int x = e % n, y = (e / n) % n, z = (D == 3) ? e / (n * n) : 0;
+      double f = 0.0;
+      if (unk1(x, n) && unk1(y, n) && (D == 2 || unk1(z, n))) {
+        f = cf.rhs_c * lv.gtab[x];
+        f = f * lv.gtab[y];
+        if (D == 3) f = f * lv.gtab[z];
+      }
+      v0.T[e] = f;
+      v0.W[e] = 0.0;
+    }
+    __syncthreads();
+    for (int I = tid; I < c.n0; I += NT4) {
+      double acc = 0.0;
+      for (int J = 0; J < c.n0; ++J) {
+        int jx = J % m + 1, jy = (J / m) % m + 1, jz = (D == 3) ? J / (m * m) + 1 : 0;
+        acc = fma(c.Ainv[(long long)I * c.n0 + J], v0.T[(jz * n + jy) * n + jx], acc);
+      }
+      int ix = I % m + 1, iy = (I / m) % m + 1, iz = (D == 3) ? I / (m * m) + 1 : 0;
+      v0.W[(iz * n + iy) * n + ix] = acc;
+    }
+    __syncthreads();
+    k4_encode(lv, D, n, v0.W, lv.umant, lv.uexp, lv.ustride, a.wu_out[0], v0.U, c.status);
+    for (int e = tid; e < v0.len; e += NT4) c.usm[c.usm_off[0] + e] = v0.U[e];
+    if (lc == 0) k4_to_global(D, n, v0.U, c.U[0], lv.g);
+    return;
+  }
+
+  // ---- load the persisted u_l the residual needs (L <= lc) --------------------
+  if (L <= lc) {
+    K4Lvl vL = k4_lvl(D, P, L, sm);
+    if (a.first) {
+      K4Lvl vp = k4_lvl(D, P, L - 1, sm);
+      for (int e = tid; e < vp.len; e += NT4) vp.U[e] = c.usm[c.usm_off[L - 1] + e];
+      __syncthreads();
+      k4_P<D, P>(cf, vL.n, vp.U, vL.U, S0);  // u_L = dec(0) + P u_{L-1}
+    } else {
+      for (int e = tid; e < vL.len; e += NT4) vL.U[e] = c.usm[c.usm_off[L] + e];
       __syncthreads();
     }
+    // residual t_L = f_L - A_L u_L, r_L = enc(t_L)
+    const LevelDev& lv = c.lv[L];
+    const int n = vL.n;
+    k4_A<D, P>(cf, L, n, vL.U, vL.T, S0);
+    for (int e = tid; e < vL.len; e += NT4) {
+      int x = e % n, y = (e / n) % n, z = (D == 3) ? e / (n * n) : 0;
+      double t = 0.0;
+      if (unk1(x, n) && unk1(y, n) && (D == 2 || unk1(z, n))) {
+        double f = cf.rhs_c * lv.gtab[x];
+        f = f * lv.gtab[y];
+        if (D == 3) f = f * lv.gtab[z];
+        t = f - vL.T[e];
+      }
+      vL.T[e] = t;
+    }
+    __syncthreads();
+    k4_encode(lv, D, n, vL.T, lv.rmant, lv.rexp, lv.rstride, a.wr[L], vL.RQ, c.status);
+  } else {
+    // restriction from the grid level lc+1 (global t_{lc+1})
+    K4Lvl vc = k4_lvl(D, P, lc, sm);
+    const Geom& gf = c.lv[lc + 1].g;
+    k4_R<D, P>(cf, gf.n, c.T[(lc + 1) & 1], gf.NX, (long long)gf.NX * gf.NY, vc.T, S0);
+    k4_encode(c.lv[lc], D, vc.n, vc.T, c.lv[lc].rmant, c.lv[lc].rexp, c.lv[lc].rstride, a.wr[lc], vc.RQ, c.status);
+  }
+  // restriction sweep inside smem
+  for (int l = lce - 1; l >= 0; --l) {
+    K4Lvl vf = k4_lvl(D, P, l + 1, sm), vc = k4_lvl(D, P, l, sm);
+    k4_R<D, P>(cf, vf.n, vf.T, vf.n, (long long)vf.n * vf.n, vc.T, S0);
+    k4_encode(c.lv[l], D, vc.n, vc.T, c.lv[l].rmant, c.lv[l].rexp, c.lv[l].rstride, a.wr[l], vc.RQ, c.status);
+  }
+  // norms ||t_l||_2, l = 0..L (grid levels from their tile partials): per-warp
+  // sums for every level, then one thread per level adds the 16 warp sums.
+  for (int l = 0; l <= L; ++l) {
+    double sacc = 0.0;
+    if (l <= lce) {
+      K4Lvl v = k4_lvl(D, P, l, sm);
+      for (int e = tid; e < v.len; e += NT4) sacc = fma(v.T[e], v.T[e], sacc);
+    } else {
+      const LevelDev& lv = c.lv[l];
+      int nt = lv.tx * lv.ty * lv.tz;
+      for (int i = tid; i < nt; i += NT4) sacc += lv.part[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(FULL, sacc, o);
+    if (threadIdx.x == 0) red[l * NW4 + threadIdx.y] = sacc;
+  }
+  __syncthreads();
+  if (tid <= L) {
+    double sacc = 0.0;
+    for (int i = 0; i < NW4; ++i) sacc += red[tid * NW4 + i];
+    c.norms[(long long)a.row * c.levels + tid] = sqrt(sacc);
+  }
+  // coarse level (reading R5): ý_0 = enc(A_0^{-1} dec r_0); w_0 = dec ý_0;
+  // ú_0 = enc(dec ú_0 + dec ý_0); u_0 = dec ú_0
+  {
+    K4Lvl v0 = k4_lvl(D, P, 0, sm);
+    const int n = v0.n, m = 2 * P - 1;
+    for (int e = tid; e < v0.len; e += NT4) SB[e] = 0.0;
+    __syncthreads();
+    for (int I = tid; I < c.n0; I += NT4) {
+      double acc = 0.0;
+      for (int J = 0; J < c.n0; ++J) {
+        int jx = J % m + 1, jy = (J / m) % m + 1, jz = (D == 3) ? J / (m * m) + 1 : 0;
+        acc = fma(c.Ainv[(long long)I * c.n0 + J], v0.RQ[(jz * n + jy) * n + jx], acc);
+      }
+      int ix = I % m + 1, iy = (I / m) % m + 1, iz = (D == 3) ? I / (m * m) + 1 : 0;
+      SB[(iz * n + iy) * n + ix] = acc;
+    }
+    __syncthreads();
+    const LevelDev& lv = c.lv[0];
+    const int lane = threadIdx.x, nxb = lv.g.NX >> 5, rows = (D == 3) ? n * n : n;
+    for (int rb = threadIdx.y; rb < rows * nxb; rb += NW4) {
+      int r = rb / nxb, xb = rb % nxb, x = xb * 32 + lane;
+      long long blk = (long long)r * nxb + xb;
+      double y = x < n ? SB[r * n + x] : 0.0;
+      double yq = warp_encode(y, a.wr[0], nullptr, nullptr, lane, c.status);
+      uint32_t* uw = lv.umant + blk * lv.ustride;
+      double uo = warp_decode(uw, lv.uexp[blk], a.wu_in[0], lane);
+      double uq = warp_encode(uo + yq, a.wu_out[0], uw, lv.uexp + blk, lane, c.status);
+      if (x < n) {
+        v0.W[r * n + x] = yq;
+        v0.U[r * n + x] = uq;
+      }
+    }
+    __syncthreads();
+  }
+  // coarse-to-fine sweep with Chebyshev-Jacobi
+  for (int l = 1; l <= lce; ++l) {
+    K4Lvl vp = k4_lvl(D, P, l - 1, sm), v = k4_lvl(D, P, l, sm);
+    const int n = v.n, len = v.len;
+    double* Y = v.T;   // t_l is dead now: reuse for the Chebyshev iterate
+    k4_P<D, P>(cf, n, vp.W, SZ, S0);                 // z_l = P w_{l-1}
+    k4_A<D, P>(cf, l, n, SZ, SB, S0);                // A z
+    for (int e = tid; e < len; e += NT4) {
+      double b = v.RQ[e] - SB[e];                    // b = dec r_l - A z
+      double d = cf.inv_theta * (k4_invd(cf, D, P, l, n, e) * b);
+      v.RQ[e] = b;                                   // RQ now holds b
+      SB[e] = d;                                     // SB holds d
+      Y[e] = d;                                      // y_1 = d_1
+    }
+    __syncthreads();
+    for (int j = 2; j <= c.n_cheb; ++j) {
+      k4_A<D, P>(cf, l, n, Y, v.U, S0);              // A y (u_l slot is free until the finalize)
+      for (int e = tid; e < len; e += NT4) {
+        double q = v.RQ[e] - v.U[e];
+        double d = fma(cf.cal[j - 1], SB[e], cf.cbe[j - 1] * (k4_invd(cf, D, P, l, n, e) * q));
+        SB[e] = d;
+        Y[e] = Y[e] + d;
+      }
+      __syncthreads();
+    }
+    k4_P<D, P>(cf, n, vp.U, v.U, S0);                // P u_{l-1} (new) for the emitted u_l
+    // finalise: ý_l = enc_wr(y); w_l = z_l + dec ý; ú_l = enc(dec ú_l + dec ý); u_l = dec ú_l + P u_{l-1}
+    const LevelDev& lv = c.lv[l];
+    const int lane = threadIdx.x, nxb = lv.g.NX >> 5, rows = (D == 3) ? n * n : n;
+    for (int rb = threadIdx.y; rb < rows * nxb; rb += NW4) {
+      int r = rb / nxb, xb = rb % nxb, x = xb * 32 + lane;
+      long long blk = (long long)r * nxb + xb;
+      double y = x < n ? Y[r * n + x] : 0.0;
+      double yq = warp_encode(y, a.wr[l], nullptr, nullptr, lane, c.status);
+      uint32_t* uw = lv.umant + blk * lv.ustride;
+      double uo = warp_decode(uw, lv.uexp[blk], a.wu_in[l], lane);
+      double uq = warp_encode(uo + yq, a.wu_out[l], uw, lv.uexp + blk, lane, c.status);
+      if (x < n) {
+        v.W[r * n + x] = SZ[r * n + x] + yq;
+        v.U[r * n + x] = uq + v.U[r * n + x];
+      }
+    }
+    __syncthreads();
+  }
+  // persist u_l; hand w_lc, u_lc to the grid levels above
+  for (int l = 0; l <= lce; ++l) {
+    K4Lvl v = k4_lvl(D, P, l, sm);
+    for (int e = tid; e < v.len; e += NT4) c.usm[c.usm_off[l] + e] = v.U[e];
+  }
+  if (lce == lc) {  // the grid levels above (this or the next FMG level) read u_lc, w_lc
+    K4Lvl v = k4_lvl(D, P, lc, sm);
+    k4_to_global(D, v.n, v.U, c.U[lc & 1], c.lv[lc].g);
+    k4_to_global(D, v.n, v.W, c.W[lc & 1], c.lv[lc].g);
   }
 }
 
@@ -996,9 +1462,9 @@ int smem_bytes(int dim, int p) {
 }
 
 void set_kernel_attributes() {
-#define SETA(D, P)                                                                                        \
-  cudaFuncSetAttribute(k_op<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM);  \
-  cudaFuncSetAttribute(k_seq<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM);
+#define SETA(D, P)                                                                                       \
+  cudaFuncSetAttribute(k_op<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM); \
+  cudaFuncSetAttribute(k4_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4_MAX_SMEM);
   SETA(2, 1) SETA(2, 2) SETA(2, 3) SETA(3, 1) SETA(3, 2) SETA(3, 3)
 #undef SETA
 }
@@ -1031,10 +1497,21 @@ void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc
 #undef F
 }
 
-void launch_seq(int dim, int p, cudaStream_t st, const void* devctx, const void* prog_dev, int count) {
+int k4_smem_bytes(int dim, int p, int lc) { return k4_smem_doubles(dim, p, lc) * 8; }
+
+void launch_k4(int dim, int p, cudaStream_t st, const void* devctx, const K4Desc& a, int smem) {
   const DevCtx* c = (const DevCtx*)devctx;
-  const Op* pr = (const Op*)prog_dev;
-#define F(D, P) launch_pdl(k_seq<D, P>, dim3(1), Plan<D, P>::SMEM, st, c, pr, count)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32, NW4);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+#define F(D, P) cudaLaunchKernelEx(&cfg, k4_kernel<D, P>, c, a)
   FMG_DISPATCH(dim, p, F);
 #undef F
 }
@@ -1066,6 +1543,10 @@ void fill_devctx(void* host_buf, const DevCtxDesc& d) {
     c->W[i] = d.W[i];
     c->Y[i] = d.Y[i];
   }
+  c->usm = d.usm;
+  for (int l = 0; l < kMaxLev; ++l) c->usm_off[l] = d.usm_off[l];
+  c->lc = d.lc;
+  c->n_cheb = d.n_cheb;
   c->Z = d.Z;
   c->B = d.B;
   c->Dv = d.Dv;
