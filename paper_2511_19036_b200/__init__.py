@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libfmg.so")
+_SO = os.environ.get("FMG_LIB") or os.path.join(_HERE, "libfmg.so")
 
 if not os.path.exists(_SO):
     raise ImportError(f"libfmg.so not built ({_SO}); run `python -c 'import __graft_entry__ as g; g.build()'`")

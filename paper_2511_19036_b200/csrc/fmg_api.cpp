@@ -46,6 +46,11 @@ struct fmg_ctx {
   double* partials = nullptr;
   long long part_off[kMaxLev]{};
   double* norms_dev = nullptr;
+  double* pbase = nullptr;         // deferred norm partials
+  long long pbase_cap = 0;
+  NormEntry* nent[2] = {nullptr, nullptr};  // deferred norm entries: [0] graph, [1] direct runs
+  int nent_cap[2] = {0, 0};
+  int nent_slot = 0;
   double* err_part = nullptr;
   int* status = nullptr;
   void* devctx = nullptr;         // DevCtx in device memory
@@ -107,6 +112,17 @@ struct Item {
 struct Builder {
   fmg_ctx* c;
   std::vector<Item> items;
+  std::vector<NormEntry> norms;
+  long long ptot = 0;
+  // reserve partial slots for (row, level l) and record the deferred norm
+  long long slot(int row, int l) {
+    int nt = c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2];
+    long long off = ptot;
+    ptot += nt;
+    NormEntry e{off, row, l, nt, 0};
+    norms.push_back(e);
+    return off;
+  }
   void grid(const OpDesc& op, int cls = -1) {
     Item it{};
     it.kind = 0;
@@ -128,6 +144,7 @@ OpDesc mkop(int type, int l, int L) {
   o.type = type;
   o.l = l;
   o.L = L;
+  o.poff = -1;
   return o;
 }
 
@@ -141,15 +158,16 @@ void build_residual_grid(Builder& b, int L, int row) {
   }
   OpDesc o = mkop(OP_RESIDUAL, L, L);
   o.wr = wr(c, L, L);
+  o.row = row;
+  o.poff = b.slot(row, L);
   b.grid(o);
   for (int l = L - 1; l >= 0; --l) {
     OpDesc q = mkop(OP_RESTRICT, l, L);
     q.wr = wr(c, l, L);
+    q.row = row;
+    q.poff = b.slot(row, l);
     b.grid(q);
   }
-  OpDesc n = mkop(OP_NORMS, 0, L);
-  n.row = row;
-  b.grid(n);
 }
 
 // One IR iteration at FMG level L: fmgResidual (Alg 3.2),
@@ -158,13 +176,18 @@ void build_iteration(Builder& b, int L, int it) {
   fmg_ctx* c = b.c;
   const int lc = c->lc;
   const bool fine = L == c->Lmax;
+  const int row = L * c->s.n_ir + it;
   if (L > lc) {
     OpDesc o = mkop(OP_RESIDUAL, L, L);
     o.wr = wr(c, L, L);
+    o.row = row;
+    o.poff = b.slot(row, L);
     b.grid(o, fine ? 0 : -1);
     for (int l = L - 1; l > lc; --l) {
       OpDesc q = mkop(OP_RESTRICT, l, L);
       q.wr = wr(c, l, L);
+      q.row = row;
+      q.poff = b.slot(row, l);
       b.grid(q, (fine && l == L - 1) ? 3 : -1);
     }
   }
@@ -226,12 +249,35 @@ void mark(fmg_ctx* c, int cls) {
   cudaEventRecordWithFlags(c->ev[c->ev_used++], c->cur, cudaEventRecordExternal);
 }
 
-int op_tiles(const fmg_ctx* c, const OpDesc& o) {
-  if (o.type == OP_NORMS) return 1;
-  return c->tiles[o.l][0] * c->tiles[o.l][1] * c->tiles[o.l][2];
+
+// Size the partial / norm-entry buffers for a built item list (before capture).
+int prepare(fmg_ctx* c, const Builder& b, int slot) {
+  c->nent_slot = slot;
+  bool dirty = false;
+  if (b.ptot > c->pbase_cap) {
+    c->pbase = (double*)dalloc(c, sizeof(double) * b.ptot);
+    if (!c->pbase) return FMG_ENOMEM;
+    c->pbase_cap = b.ptot;
+    dirty = true;
+  }
+  if ((int)b.norms.size() > c->nent_cap[slot]) {
+    c->nent[slot] = (NormEntry*)dalloc(c, sizeof(NormEntry) * b.norms.size());
+    if (!c->nent[slot]) return FMG_ENOMEM;
+    c->nent_cap[slot] = (int)b.norms.size();
+  }
+  if (!b.norms.empty())
+    cudaMemcpy(c->nent[slot], b.norms.data(), sizeof(NormEntry) * b.norms.size(), cudaMemcpyHostToDevice);
+  if (dirty) {
+    // the device context carries pbase
+    std::vector<char> host(devctx_size());
+    cudaMemcpy(host.data(), c->devctx, host.size(), cudaMemcpyDeviceToHost);
+    set_devctx_pbase(host.data(), c->pbase);
+    cudaMemcpy(c->devctx, host.data(), host.size(), cudaMemcpyHostToDevice);
+  }
+  return FMG_OK;
 }
 
-// Issue every item on c->cur (inside a capture or directly).
+// Issue every item on c->cur (inside a capture or directly), then the deferred norms.
 void issue(fmg_ctx* c, const Builder& b) {
   for (const Item& it : b.items) {
     if (it.kind == 1) {
@@ -240,11 +286,19 @@ void issue(fmg_ctx* c, const Builder& b) {
       mark(c, -2);
     } else {
       mark(c, it.timed_cls);
-      launch_op(c->dim, c->p, c->cur, c->devctx, it.op, op_tiles(c, it.op));
+      int tx = 1, ty = 1, tz = 1;
+      if (it.op.type != OP_NORMS) {
+        tx = c->tiles[it.op.l][0];
+        ty = c->tiles[it.op.l][1];
+        tz = c->tiles[it.op.l][2];
+      }
+      launch_op(c->dim, c->p, c->cur, c->devctx, it.op, tx, ty, tz);
       mark(c, it.timed_cls);
     }
     c->launches++;
   }
+  launch_norms_all(c->cur, c->devctx, c->nent[c->nent_slot], (int)b.norms.size());
+  c->launches++;
 }
 
 void zero_sections(fmg_ctx* c) {
@@ -282,6 +336,9 @@ int run_direct(fmg_ctx* c, Builder& b) {
   int save = c->timing_cls;
   long long save_l = c->launches;
   c->timing_cls = -1;
+  cudaStreamSynchronize(c->st);
+  int prc = prepare(c, b, 1);
+  if (prc) return prc;
   issue(c, b);
   c->timing_cls = save;
   c->launches = save_l;
@@ -290,7 +347,19 @@ int run_direct(fmg_ctx* c, Builder& b) {
 
 }  // namespace
 
+namespace fmg {
+void k4_debug(int on);
+void k4_stamps(unsigned long long* out);
+}
+
 extern "C" {
+
+/* debug: K4 phase timestamps (ns) of the last K4 launch */
+int fmg_debug_k4(int on, unsigned long long* stamps64) {
+  if (stamps64) { cudaDeviceSynchronize(); fmg::k4_stamps(stamps64); }
+  else fmg::k4_debug(on);
+  return 0;
+}
 
 int fmg_set_allocator(fmg_alloc_fn alloc, fmg_free_fn free_fn, void* user) {
   if ((alloc == nullptr) != (free_fn == nullptr)) return FMG_EINVAL;
@@ -374,6 +443,9 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     c->norms_dev = (double*)dalloc(c, sizeof(double) * levels * s->n_ir * levels);
     c->err_part = (double*)dalloc(c, sizeof(double) * 2 * 148 * 16);
     c->status = (int*)dalloc(c, sizeof(int));
+    int* counters = (int*)dalloc(c, sizeof(int) * kMaxLev);
+    if (counters) cudaMemset(counters, 0, sizeof(int) * kMaxLev);
+    dd.count = counters;
     c->devctx = dalloc(c, devctx_size());
     long long usm_n = 0;
     for (int l = 0; l <= c->lc; ++l) {
@@ -435,6 +507,8 @@ int fmg_solve_async(fmg_ctx* c) {
     c->launches = 0;
     c->ev_used = 0;
     build_solve(b, c->Lmax, c->s.n_ir);
+    int prc = prepare(c, b, 0);
+    if (prc) return prc;
     c->cur = c->cap;
     cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return cuda_err(e);

@@ -50,6 +50,13 @@ struct OpDesc {
   int type, l, L, step, last;
   int wr, wu_in, wu_out;
   int row;
+  long long poff;  // norm partials of this (FMG level, iteration, level): pbase + poff
+};
+
+// One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.
+struct NormEntry {
+  long long poff;
+  int row, l, count, pad;
 };
 
 // K4 (shared-memory coarse hierarchy kernel) launch descriptor.
@@ -69,6 +76,8 @@ struct DevCtxDesc {
   const double* gtab[kMaxLev];
   int tiles[kMaxLev][3];
   double* part[kMaxLev];
+  int* count;  // kMaxLev arrival counters (zeroed)
+  double* pbase;
   double *U[2], *T[2], *W[2], *Y[2];
   double *Z, *B, *Dv;
   const double* Ainv;
@@ -90,12 +99,14 @@ void set_kernel_attributes();
 int smem_bytes(int dim, int p);
 void tile_shape(int dim, int p, int* TY, int* TZ);
 size_t devctx_size();
+void set_devctx_pbase(void* host_buf, double* pbase);
 size_t op_size();
 void fill_devctx(void* host_buf, const DevCtxDesc& d);
 void pack_op(void* dst, const OpDesc& od);
-void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int ntiles);
+void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int tx, int ty, int tz);
 int k4_smem_bytes(int dim, int p, int lc);
 void launch_k4(int dim, int p, cudaStream_t st, const void* devctx, const K4Desc& a, int smem);
+void launch_norms_all(cudaStream_t st, const void* devctx, const NormEntry* entries_dev, int n);
 void launch_errors(const Launch& L, const double* U, const Geom& g, double* partials, int* nparts);
 void launch_bfp_encode(const double* x, long long n, int w, uint32_t* mant, int8_t* exps, int* status,
                        cudaStream_t st);

@@ -38,6 +38,19 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ----------------------------------------------------------------- codec --
+// Exact int -> double for |m| < 2^31 by the 1.5*2^52 magic constant (an FP64
+// add instead of an I2F conversion); wider mantissas use the conversion.
+__device__ __forceinline__ double i2d(long long m, int w) {
+  if (w <= 32) return __longlong_as_double(0x4338000000000000LL + m) - 6755399441055744.0;
+  return (double)m;
+}
+// RNE of x to an integer for |x| < 2^31 (x + 1.5*2^52 rounds to nearest even at
+// integer granularity; the low word is the two's-complement result).
+__device__ __forceinline__ long long rne_int(double x, int w) {
+  if (w <= 32) return (long long)(int)__double2loint(x + 6755399441055744.0);
+  return (long long)rint(x);
+}
+
 // Warp-cooperative decode: lane j returns entry j of the block whose w words
 // start at `words`.  All 32 lanes must call.
 __device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int w, int lane) {
@@ -62,7 +75,7 @@ __device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int 
   unsigned long long field = lo >> s;
   if (s + w > 64) field |= (unsigned long long)w2 << (64 - s);
   long long m = (long long)(field << (64 - w)) >> (64 - w);
-  return (double)m * pow2(E - (w - 1));
+  return i2d(m, w) * pow2(E - (w - 1));
 }
 
 // Single-entry decode (entry j of a block), for halo points.
@@ -74,7 +87,7 @@ __device__ __forceinline__ double point_decode(const uint32_t* words, int E, int
   unsigned long long field = lo >> s;
   if (jl > j0 + 1) field |= (unsigned long long)words[j0 + 2] << (64 - s);
   long long m = (long long)(field << (64 - w)) >> (64 - w);
-  return (double)m * pow2(E - (w - 1));
+  return i2d(m, w) * pow2(E - (w - 1));
 }
 
 // Warp-cooperative encode of one block; lane j holds entry j.
@@ -91,7 +104,8 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
   double mx = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
   int q = w - 1, E = -128;
   if (!err && mx != 0.0) {
-    int E0 = ilogb(mx) + 1;
+    int ebits = (int)((mh >> 20) & 0x7FFu);
+    int E0 = ebits == 0 ? -1100 : ebits - 1022;  // ilogb(mx) + 1; subnormal max -> saturates below
     if (E0 > 127) {
       err = true;
     } else if (E0 < -127) {
@@ -107,7 +121,7 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
     E = -128;
     if (lane == 0 && status) atomicOr(status, 1);
   } else if (E != -128) {
-    m = (long long)rint(v * pow2(q - E));
+    m = rne_int(v * pow2(q - E), w);
   }
   if (words) {
     unsigned long long field = (unsigned long long)m & ((1ULL << w) - 1ULL);
@@ -147,12 +161,15 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
     if (lane + 32 < w) words[lane + 32] = mine1;
     if (lane == 0) *eptr = (int8_t)E;
   }
-  return E == -128 ? 0.0 : (double)m * pow2(E - q);
+  return E == -128 ? 0.0 : i2d(m, w) * pow2(E - q);
 }
 
 // ------------------------------------------------------------ tile plans --
 template <int D, int P> struct TileCfg;
-template <int P> struct TileCfg<2, P> { static constexpr int TY = 16, TZ = 1; };
+#ifndef FMG_TY2D
+#define FMG_TY2D 16
+#endif
+template <int P> struct TileCfg<2, P> { static constexpr int TY = FMG_TY2D, TZ = 1; };
 template <> struct TileCfg<3, 1> { static constexpr int TY = 8, TZ = 4; };
 template <> struct TileCfg<3, 2> { static constexpr int TY = 4, TZ = 4; };
 template <> struct TileCfg<3, 3> { static constexpr int TY = 4, TZ = 4; };
@@ -206,6 +223,7 @@ struct LevelDev {
   const double* gtab;
   int tx, ty, tz;  // tile grid of this level
   double* part;    // norm partials, one per tile
+  int* count;      // arrival counter for the last-CTA norm reduction
 };
 
 struct DevCtx {
@@ -213,6 +231,7 @@ struct DevCtx {
   double* U[2];  // decoded u_l (ping-pong by level parity), emitted by the cFas finalize
   double* T[2];  // residual temporaries t_l
   double* W[2];  // w_l = z_l + dec ý_l
+  double* pbase; // norm partials of the grid levels (one slot per FMG level, iteration, level)
   double* usm;   // K4: dense u_l of the smem levels, persisted between launches
   long long usm_off[kMaxLev];
   int lc;        // K4 handles levels 0..lc in shared memory
@@ -451,18 +470,17 @@ __device__ __forceinline__ double a_final(const Geom& g, int x0, int y0, int z0,
 }
 
 // Load a plain FP64 array onto the input box (0 outside the stored level).
+// Flat element mapping (constant divisors): no half-empty column iterations.
 template <int D, int P>
 __device__ void box_load(const double* __restrict__ src, const Geom& g, int x0, int y0, int z0, double* U) {
   using PL = Plan<D, P>;
-  const int lane = threadIdx.x;
-  for (int r = threadIdx.y; r < PL::BY * PL::BZ; r += NWARP) {
-    int gy = y0 - P + r % PL::BY, gz = (D == 3) ? z0 - P + r / PL::BY : 0;
-    bool rowok = gy >= 0 && gy < g.NY && gz >= 0 && gz < g.NZ;
-    const double* row = src + ((long long)gz * g.NY + gy) * g.NX;
-    for (int bx = lane; bx < PL::BX; bx += 32) {
-      int gx = x0 - P + bx;
-      U[r * PL::BX + bx] = (rowok && gx >= 0 && gx < g.NX) ? row[gx] : 0.0;
-    }
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+#pragma unroll 4
+  for (int i = tid; i < PL::NU; i += NT) {
+    int bx = i % PL::BX, r = i / PL::BX;
+    int gy = y0 - P + r % PL::BY, gz = (D == 3) ? z0 - P + r / PL::BY : 0, gx = x0 - P + bx;
+    bool ok = gx >= 0 && gx < g.NX && gy >= 0 && gy < g.NY && gz >= 0 && gz < g.NZ;
+    U[i] = ok ? src[((long long)gz * g.NY + gy) * g.NX + gx] : 0.0;
   }
   __syncthreads();
 }
@@ -480,22 +498,67 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
   return s;
 }
 
-__device__ __forceinline__ void tile_coords(const LevelDev& lv, int tile, int TY, int TZ, int& x0, int& y0, int& z0) {
-  int bx = tile % lv.tx, r = tile / lv.tx, by = r % lv.ty, bz = r / lv.ty;
-  x0 = bx * 32;
-  y0 = by * TY;
-  z0 = bz * TZ;
+// Per-tile partial of ||t_l||^2 -> part[tile]; the last CTA of the level to
+// arrive sums all partials in fixed order and writes ||t_l||_2 to the norm row
+// (deterministic: the order does not depend on which CTA is last).
+__device__ void level_norm(const DevCtx& c, const LevelDev& lv, int l, int row, int tile, double ss, bool reduce,
+                           long long poff) {
+  __shared__ double red[NT];
+  __shared__ int last;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+  if (threadIdx.x == 0) red[threadIdx.y] = ss;
+  __syncthreads();
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  if (tid == 0) {
+    double s = 0.0;
+    for (int i = 0; i < NWARP; ++i) s += red[i];
+    if (poff >= 0) c.pbase[poff + tile] = s;
+    lv.part[tile] = s;
+    last = 0;
+    if (reduce) {
+      __threadfence();
+      int nt = lv.tx * lv.ty * lv.tz;
+      last = atomicAdd(lv.count, 1) == nt - 1;
+    }
+  }
+  __syncthreads();
+  if (!last || row < 0) return;
+  __threadfence();
+  const int nt = lv.tx * lv.ty * lv.tz;
+  double s = 0.0;
+  for (int i = tid; i < nt; i += NT) s += ((volatile double*)lv.part)[i];
+  red[tid] = s;
+  __syncthreads();
+  for (int o = NT / 2; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    c.norms[(long long)row * c.levels + l] = sqrt(red[0]);
+    *lv.count = 0;
+  }
+}
+
+// Tile of a grid op: 3D block index (no runtime division) and its linear index.
+struct TileIdx {
+  int bx, by, bz, lin;
+};
+__device__ __forceinline__ void tile_coords(const TileIdx& t, int TY, int TZ, int& x0, int& y0, int& z0) {
+  x0 = t.bx * 32;
+  y0 = t.by * TY;
+  z0 = t.bz * TZ;
 }
 
 // ============================================================ tile ops =====
 // S2: u_l = dec ú_l + P_l u_{l-1} (decode sweep PAPER.md:733-735), materialised.
 template <int D, int P>
-__device__ void tile_decode(const DevCtx& c, const Op& op, int tile, double* sm) {
+__device__ void tile_decode(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
   using PL = Plan<D, P>;
   const LevelDev& lv = c.lv[op.l];
   const Geom& g = lv.g;
   int x0, y0, z0;
-  tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
+  tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
   double* out = c.U[op.l & 1];
   double* box = sm;  // DBX x DBY x DBZ
   if (op.l > 0) {
@@ -520,12 +583,12 @@ __device__ void tile_decode(const DevCtx& c, const Op& op, int tile, double* sm)
 // (PAPER.md:738-739).  u_L = dec ú_L + P u_{L-1} (S2) was emitted by the previous
 // sweep's finalize (or by the decode op at the start of the FMG level).
 template <int D, int P>
-__device__ void tile_residual(const DevCtx& c, const Op& op, int tile, double* sm) {
+__device__ void tile_residual(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
   using PL = Plan<D, P>;
   const LevelDev& lv = c.lv[op.L];
   const Geom& g = lv.g;
   int x0, y0, z0;
-  tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
+  tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
   double* U = sm;
   double* R1 = sm + PL::NU;
   box_load<D, P>(c.U[op.L & 1], g, x0, y0, z0, U);
@@ -554,14 +617,12 @@ __device__ void tile_residual(const DevCtx& c, const Op& op, int tile, double* s
     long long blk = idx >> 5;
     warp_encode(t, op.wr, lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
   }
-  __shared__ double red[NWARP];
-  double s = cta_sum(ss, red);
-  if (threadIdx.x == 0 && threadIdx.y == 0) lv.part[tile] = s;
+  level_norm(c, lv, op.L, op.row, tile.lin, ss, op.step == 9, op.poff);
 }
 
 // S5: t_l = R_{l+1} t_{l+1} (restricts t, not r), r_l = enc.
 template <int D, int P>
-__device__ void tile_restrict(const DevCtx& c, const Op& op, int tile, double* sm) {
+__device__ void tile_restrict(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
   using PL = Plan<D, P>;
   const LevelDev& lc = c.lv[op.l];
   const Geom& gc = lc.g;
@@ -569,7 +630,7 @@ __device__ void tile_restrict(const DevCtx& c, const Op& op, int tile, double* s
   const double* __restrict__ Tf = c.T[(op.l + 1) & 1];
   double* Tc = c.T[op.l & 1];
   int x0, y0, z0;
-  tile_coords(lc, tile, PL::TY, PL::TZ, x0, y0, z0);
+  tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
   double* XR = sm;
   double* YR = sm + PL::NXR;
   const int lane = threadIdx.x, nf = gf.n, nc = gc.n;
@@ -635,9 +696,7 @@ __device__ void tile_restrict(const DevCtx& c, const Op& op, int tile, double* s
     long long blk = idx >> 5;
     warp_encode(t, op.wr, lc.rmant + blk * lc.rstride, lc.rexp + blk, lane, c.status);
   }
-  __shared__ double red[NWARP];
-  double s = cta_sum(ss, red);
-  if (threadIdx.x == 0 && threadIdx.y == 0) lc.part[tile] = s;
+  level_norm(c, lc, op.l, op.row, tile.lin, ss, op.step == 9, op.poff);
 }
 
 // Norms of t_0..t_L from the per-tile partials (fixed order).
@@ -693,12 +752,12 @@ __device__ __forceinline__ double inv_diag(const Coefs& cf, int D, int P, int l,
 // d = inv_theta (invD b), y = d.  Writes B (and Z for l < L);
 // with k == 1 finalises directly.
 template <int D, int P>
-__device__ void tile_cfas1(const DevCtx& c, const Op& op, int tile, double* sm) {
+__device__ void tile_cfas1(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
   using PL = Plan<D, P>;
   const LevelDev& lv = c.lv[op.l];
   const Geom& g = lv.g;
   int x0, y0, z0;
-  tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
+  tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
   double* U = sm;
   double* R1 = sm + PL::NU;
   {
@@ -762,12 +821,12 @@ __device__ void tile_cfas1(const DevCtx& c, const Op& op, int tile, double* sm) 
 // Step 2 reconstructs y_1 = d_1 = inv_theta (invD b) from B on the box (no Y/D
 // arrays for k = 2); later steps read Y/Dv.  Last step finalises (S9, S10).
 template <int D, int P>
-__device__ void tile_cheb(const DevCtx& c, const Op& op, int tile, double* sm) {
+__device__ void tile_cheb(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
   using PL = Plan<D, P>;
   const LevelDev& lv = c.lv[op.l];
   const Geom& g = lv.g;
   int x0, y0, z0;
-  tile_coords(lv, tile, PL::TY, PL::TZ, x0, y0, z0);
+  tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
   double* U = sm;
   double* R1 = sm + PL::NU;
   const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -820,7 +879,7 @@ __device__ void tile_cheb(const DevCtx& c, const Op& op, int tile, double* sm) {
 }
 
 template <int D, int P>
-__device__ __forceinline__ void run_op(const DevCtx& c, const Op& op, int tile, double* sm) {
+__device__ __forceinline__ void run_op(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
   switch (op.type) {
     case OP_DECODE: tile_decode<D, P>(c, op, tile, sm); break;
     case OP_RESIDUAL: tile_residual<D, P>(c, op, tile, sm); break;
@@ -831,26 +890,17 @@ __device__ __forceinline__ void run_op(const DevCtx& c, const Op& op, int tile, 
   }
 }
 
-// Copies the device context (pointers, geometry, coefficient tables) into
-// shared memory once per CTA: every later access is an LDS (broadcast for
-// uniform indices) instead of a global load.
-__device__ __forceinline__ void load_ctx(const DevCtx* __restrict__ cp, DevCtx* sc) {
-  static_assert(sizeof(DevCtx) % 8 == 0, "DevCtx size");
-  const unsigned long long* src = (const unsigned long long*)cp;
-  unsigned long long* dst = (unsigned long long*)sc;
-  for (int i = threadIdx.y * 32 + threadIdx.x; i < (int)(sizeof(DevCtx) / 8); i += NT) dst[i] = src[i];
-  __syncthreads();
-}
-
-// Grid kernel: one CTA per tile of one operation.
+// Grid kernel: one CTA per tile of one operation.  The device context lives in
+// global memory and is read through the read-only path (uniform, L1-cached).
 template <int D, int P>
 __global__ void __launch_bounds__(NT) k_op(const DevCtx* __restrict__ cp, Op op) {
   extern __shared__ double sm[];
-  __shared__ DevCtx sc;
   pdl_wait();
   pdl_trigger();
-  load_ctx(cp, &sc);
-  run_op<D, P>(sc, op, blockIdx.x, sm);
+  const DevCtx& c = *cp;
+  TileIdx t{(int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z,
+            (int)((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x)};
+  run_op<D, P>(c, op, t, sm);
 }
 
 // =============================================== K4: coarse hierarchy ======
@@ -900,9 +950,17 @@ __device__ __forceinline__ K4Lvl k4_lvl(int D, int P, int l, double* sm) {
 
 __device__ __forceinline__ double rd(const double* a, int j, int n) { return (j >= 0 && j < n) ? a[j] : 0.0; }
 
-// out = A_l in (dense level arrays); scratch: 4 * len.
-template <int D, int P>
-__device__ void k4_A(const Coefs& cf, int l, int n, const double* in, double* out, double* s) {
+// Final-pass iteration helper: warps walk (row, 32-entry block) pairs of a
+// dense level so that each warp holds one BFP block (x = xb*32 + lane, values
+// beyond n are 0) -- epilogues may then encode/decode with warp collectives.
+#define K4_BLOCKS(n, rows)                                                        \
+  for (int rb = threadIdx.y, nxb_ = ((n) + 31) >> 5; rb < (rows) * nxb_; rb += NW4) \
+    for (int r = rb / nxb_, x = (rb % nxb_) * 32 + (int)threadIdx.x, once_ = 1; once_; once_ = 0)
+
+// A_l in (dense), canonical passes; the last pass calls
+// epi(r, x, Av) per point (Av = 0 at non-unknowns and beyond n), warp-aligned.
+template <int D, int P, class Epi>
+__device__ void k4_A(const Coefs& cf, int l, int n, const double* in, double* s, Epi epi) {
   const int lane = threadIdx.x, w = threadIdx.y, len = ipow(n, D), rows = len / n;
   double* a = s;
   double* b = s + len;
@@ -923,20 +981,19 @@ __device__ void k4_A(const Coefs& cf, int l, int n, const double* in, double* ou
     }
   __syncthreads();
   if constexpr (D == 2) {
-    for (int y = w; y < n; y += NW4) {
-      bool oky = unk1(y, n);
-      int tau = oky ? y % P : 0;
-      for (int x = lane; x < n; x += 32) {
-        double d = 0.0, e = 0.0;
+    K4_BLOCKS(n, n) {
+      const int y = r;
+      bool ok = unk1(y, n) && unk1(x, n);
+      int tau = unk1(y, n) ? y % P : 0, xs = x < n ? x : 0;
+      double d = 0.0, e = 0.0;
 #pragma unroll
-        for (int o = 0; o <= 2 * P; ++o) {
-          int j = y - P + o;
-          bool in_ = j >= 0 && j < n;
-          d = fma(cf.Kc[tau][o], in_ ? a[j * n + x] : 0.0, d);
-          e = fma(cf.Mc[tau][o], in_ ? b[j * n + x] : 0.0, e);
-        }
-        out[y * n + x] = (oky && unk1(x, n)) ? d + e : 0.0;
+      for (int o = 0; o <= 2 * P; ++o) {
+        int j = y - P + o;
+        bool in_ = j >= 0 && j < n;
+        d = fma(cf.Kc[tau][o], in_ ? a[j * n + xs] : 0.0, d);
+        e = fma(cf.Mc[tau][o], in_ ? b[j * n + xs] : 0.0, e);
       }
+      epi(r, x, ok ? d + e : 0.0);
     }
   } else {
     double* c = s + 2 * len;
@@ -962,49 +1019,56 @@ __device__ void k4_A(const Coefs& cf, int l, int n, const double* in, double* ou
     }
     __syncthreads();
     const double h = pow2(-(l + 1));
-    for (int r = w; r < n * n; r += NW4) {
-      int y = r % n, z = r / n;
-      bool okz = unk1(z, n) && unk1(y, n);
+    K4_BLOCKS(n, n * n) {
+      int y = r % n, z = r / n, xs = x < n ? x : 0;
+      bool ok = unk1(z, n) && unk1(y, n) && unk1(x, n);
       int tau = unk1(z, n) ? z % P : 0;
-      for (int x = lane; x < n; x += 32) {
-        double acc = 0.0;
+      double acc = 0.0;
 #pragma unroll
-        for (int o = 0; o <= 2 * P; ++o) {
-          int j = z - P + o;
-          acc = fma(cf.Kc[tau][o], (j >= 0 && j < n) ? c[(j * n + y) * n + x] : 0.0, acc);
-        }
-#pragma unroll
-        for (int o = 0; o <= 2 * P; ++o) {
-          int j = z - P + o;
-          acc = fma(cf.Mc[tau][o], (j >= 0 && j < n) ? sv[(j * n + y) * n + x] : 0.0, acc);
-        }
-        out[r * n + x] = (okz && unk1(x, n)) ? acc * h : 0.0;
+      for (int o = 0; o <= 2 * P; ++o) {
+        int j = z - P + o;
+        acc = fma(cf.Kc[tau][o], (j >= 0 && j < n) ? c[(j * n + y) * n + xs] : 0.0, acc);
       }
+#pragma unroll
+      for (int o = 0; o <= 2 * P; ++o) {
+        int j = z - P + o;
+        acc = fma(cf.Mc[tau][o], (j >= 0 && j < n) ? sv[(j * n + y) * n + xs] : 0.0, acc);
+      }
+      epi(r, x, ok ? acc * h : 0.0);
     }
   }
   __syncthreads();
 }
 
-// fine = P_lf coarse (dense); scratch: len_f (x-pass) + len_f/2 (y-pass, 3D).
+// f1 = P c1 and (if c2) f2 = P c2 on the fine level nf, one set of passes
+// (DESIGN.md §3.3).  scratch: 2 * (len_f/2^(d-1) + len_f/2).
 template <int D, int P>
-__device__ void k4_P(const Coefs& cf, int nf, const double* coarse, double* fine, double* s) {
+__device__ void k4_P2(const Coefs& cf, int nf, const double* c1, double* f1, const double* c2, double* f2, double* s) {
   const int lane = threadIdx.x, w = threadIdx.y, nc = nf / 2;
-  double* t1 = s;  // [cz][cy][xf]
+  const int nv = c2 ? 2 : 1;
+  const int n1 = (D == 3) ? nc * nc * nf : nc * nf;  // x-pass size
+  const int n2 = (D == 3) ? nc * nf * nf : 0;        // y-pass size (3D)
   const int rows1 = (D == 3) ? nc * nc : nc;
-  for (int r = w; r < rows1; r += NW4)
+  for (int r = w; r < nv * rows1; r += NW4) {
+    int k = r / rows1, rr = r % rows1;
+    const double* cs = (k == 0 ? c1 : c2) + rr * nc;
+    double* t1 = s + k * n1;
     for (int x = lane; x < nf; x += 32) {
       bool ok = unk1(x, nf);
       int rx = ok ? x % (2 * P) : 0, base = ok ? P * (x / (2 * P)) : 0;
       double acc = 0.0;
 #pragma unroll
-      for (int t = 0; t <= P; ++t) acc = fma(cf.Pw[rx][t], rd(coarse + r * nc, base + t, nc), acc);
-      t1[r * nf + x] = ok ? acc : 0.0;
+      for (int t = 0; t <= P; ++t) acc = fma(cf.Pw[rx][t], rd(cs, base + t, nc), acc);
+      t1[rr * nf + x] = ok ? acc : 0.0;
     }
+  }
   __syncthreads();
-  double* t2 = (D == 3) ? s + nc * nc * nf : fine;  // [cz][yf][xf]
   const int rows2 = (D == 3) ? nc * nf : nf;
-  for (int r = w; r < rows2; r += NW4) {
-    int y = r % nf, cz = r / nf;
+  for (int r = w; r < nv * rows2; r += NW4) {
+    int k = r / rows2, rr = r % rows2;
+    const double* t1 = s + k * n1;
+    double* t2 = (D == 3) ? s + 2 * n1 + k * n2 : (k == 0 ? f1 : f2);
+    int y = rr % nf, cz = rr / nf;
     bool ok = unk1(y, nf);
     int ry = ok ? y % (2 * P) : 0, base = ok ? P * (y / (2 * P)) : 0;
     for (int x = lane; x < nf; x += 32) {
@@ -1014,13 +1078,16 @@ __device__ void k4_P(const Coefs& cf, int nf, const double* coarse, double* fine
         int j = base + t;
         acc = fma(cf.Pw[ry][t], (j < nc) ? t1[(cz * nc + j) * nf + x] : 0.0, acc);
       }
-      t2[r * nf + x] = ok ? acc : 0.0;
+      t2[rr * nf + x] = ok ? acc : 0.0;
     }
   }
   __syncthreads();
   if constexpr (D == 3) {
-    for (int r = w; r < nf * nf; r += NW4) {
-      int y = r % nf, z = r / nf;
+    for (int r = w; r < nv * nf * nf; r += NW4) {
+      int k = r / (nf * nf), rr = r % (nf * nf);
+      const double* t2 = s + 2 * n1 + k * n2;
+      double* fo = k == 0 ? f1 : f2;
+      int y = rr % nf, z = rr / nf;
       bool ok = unk1(z, nf);
       int rz = ok ? z % (2 * P) : 0, base = ok ? P * (z / (2 * P)) : 0;
       for (int x = lane; x < nf; x += 32) {
@@ -1030,18 +1097,18 @@ __device__ void k4_P(const Coefs& cf, int nf, const double* coarse, double* fine
           int j = base + t;
           acc = fma(cf.Pw[rz][t], (j < nc) ? t2[(j * nf + y) * nf + x] : 0.0, acc);
         }
-        fine[r * nf + x] = ok ? acc : 0.0;
+        fo[rr * nf + x] = ok ? acc : 0.0;
       }
     }
     __syncthreads();
   }
 }
 
-// coarse = R fine; fine given by (ptr, row stride sy, plane stride sz) with x < nf
-// valid (global padded or dense smem).  scratch: nc*nf^(d-1) + nc^2*nf (3D).
-template <int D, int P>
-__device__ void k4_R(const Coefs& cf, int nf, const double* fine, long long sy, long long sz, double* coarse,
-                     double* s) {
+// coarse = R fine; fine given by (ptr, row stride sy, plane
+// stride sz), x < nf valid.  The last pass calls epi(r, x, t) warp-aligned.
+// scratch: nc*nf^(d-1) + nc^2*nf (3D).
+template <int D, int P, class Epi>
+__device__ void k4_R(const Coefs& cf, int nf, const double* fine, long long sy, long long sz, double* s, Epi epi) {
   const int lane = threadIdx.x, w = threadIdx.y, nc = nf / 2;
   double* t1 = s;  // [zf][yf][xc]
   const int rows1 = (D == 3) ? nf * nf : nf;
@@ -1061,62 +1128,55 @@ __device__ void k4_R(const Coefs& cf, int nf, const double* fine, long long sy, 
     }
   }
   __syncthreads();
-  double* t2 = (D == 3) ? s + nf * nf * nc : coarse;  // [zf][yc][xc]
-  const int rows2 = (D == 3) ? nf * nc : nc;
-  for (int r = w; r < rows2; r += NW4) {
-    int yc = r % nc, zf = r / nc;
-    bool ok = unk1(yc, nc);
-    int tau = ok ? yc % P : 0;
-    for (int x = lane; x < nc; x += 32) {
+  if constexpr (D == 2) {
+    K4_BLOCKS(nc, nc) {
+      const int yc = r, xs = x < nc ? x : 0;
+      bool ok = unk1(yc, nc) && unk1(x, nc);
+      int tau = unk1(yc, nc) ? yc % P : 0;
       double acc = 0.0;
 #pragma unroll
       for (int t = 0; t <= 4 * P - 2; ++t) {
         int j = 2 * yc - (2 * P - 1) + t;
-        acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t1[(zf * nf + j) * nc + x] : 0.0, acc);
+        acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t1[j * nc + xs] : 0.0, acc);
       }
-      t2[r * nc + x] = ok ? acc : 0.0;
+      epi(r, x, ok ? acc : 0.0);
     }
-  }
-  __syncthreads();
-  if constexpr (D == 3) {
-    for (int r = w; r < nc * nc; r += NW4) {
-      int yc = r % nc, zc = r / nc;
-      bool ok = unk1(zc, nc);
-      int tau = ok ? zc % P : 0;
+  } else {
+    double* t2 = s + nf * nf * nc;  // [zf][yc][xc]
+    for (int r = w; r < nf * nc; r += NW4) {
+      int yc = r % nc, zf = r / nc;
+      bool ok = unk1(yc, nc);
+      int tau = ok ? yc % P : 0;
       for (int x = lane; x < nc; x += 32) {
         double acc = 0.0;
 #pragma unroll
         for (int t = 0; t <= 4 * P - 2; ++t) {
-          int j = 2 * zc - (2 * P - 1) + t;
-          acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t2[(j * nc + yc) * nc + x] : 0.0, acc);
+          int j = 2 * yc - (2 * P - 1) + t;
+          acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t1[(zf * nf + j) * nc + x] : 0.0, acc);
         }
-        coarse[r * nc + x] = ok ? acc : 0.0;
+        t2[r * nc + x] = ok ? acc : 0.0;
       }
     }
     __syncthreads();
-  }
-}
-
-// Encode the dense level array `v` into section (mant, exps, stride) at width w
-// (global padded rows), storing the quantised values into `q` (may alias v).
-__device__ void k4_encode(const LevelDev& lv, int D, int n, const double* v, uint32_t* mant, int8_t* exps,
-                          int stride, int w, double* q, int* status) {
-  const int lane = threadIdx.x, nxb = lv.g.NX >> 5, rows = (D == 3) ? n * n : n;
-  for (int rb = threadIdx.y; rb < rows * nxb; rb += NW4) {
-    int r = rb / nxb, xb = rb % nxb;
-    int x = xb * 32 + lane;
-    double val = x < n ? v[r * n + x] : 0.0;
-    long long blk = (long long)r * nxb + xb;
-    double qq = warp_encode(val, w, mant ? mant + blk * stride : nullptr, exps ? exps + blk : nullptr, lane, status);
-    if (q && x < n) q[r * n + x] = qq;
+    K4_BLOCKS(nc, nc * nc) {
+      int yc = r % nc, zc = r / nc, xs = x < nc ? x : 0;
+      bool ok = unk1(zc, nc) && unk1(yc, nc) && unk1(x, nc);
+      int tau = unk1(zc, nc) ? zc % P : 0;
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t <= 4 * P - 2; ++t) {
+        int j = 2 * zc - (2 * P - 1) + t;
+        acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t2[(j * nc + yc) * nc + xs] : 0.0, acc);
+      }
+      epi(r, x, ok ? acc : 0.0);
+    }
   }
   __syncthreads();
 }
 
-__device__ __forceinline__ double k4_invd(const Coefs& cf, int D, int P, int l, int n, int e) {
-  int x = e % n, y = (e / n) % n, z = (D == 3) ? e / (n * n) : 0;
-  if (!unk1(x, n) || !unk1(y, n) || (D == 3 && !unk1(z, n))) return 0.0;
-  return cf.invd[((D == 3 ? z % P : 0) * P + y % P) * P + x % P] * pow2((l + 1) * (D - 2));
+// BFP block of dense level row r, block x/32 (global padded layout).
+__device__ __forceinline__ long long k4_blk(const LevelDev& lv, int r, int x) {
+  return (long long)r * (lv.g.NX >> 5) + (x >> 5);
 }
 
 // Copy a dense level into a padded global array (zeros in the padding).
@@ -1126,30 +1186,41 @@ __device__ void k4_to_global(int D, int n, const double* v, double* g, const Geo
     for (int x = threadIdx.x; x < gg.NX; x += 32) g[(long long)r * gg.NX + x] = x < n ? v[r * n + x] : 0.0;
 }
 
+__device__ __forceinline__ double k4_invd_at(const Coefs& cf, int D, int P, int l, int n, int r, int x) {
+  int y = r % n, z = (D == 3) ? r / n : 0;
+  if (!unk1(x, n) || !unk1(y, n) || (D == 3 && !unk1(z, n))) return 0.0;
+  return cf.invd[((D == 3 ? z % P : 0) * P + y % P) * P + x % P] * pow2((l + 1) * (D - 2));
+}
+
+// Optional phase timestamps (debug): thread 0 records globaltimer after phases.
+__device__ unsigned long long g_k4_stamps[64];
+__device__ int g_k4_debug = 0;
+__device__ __forceinline__ void k4_stamp(int i) {
+  if (g_k4_debug && threadIdx.x == 0 && threadIdx.y == 0 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k4_stamps[i] = t;
+  }
+}
+
 template <int D, int P>
-__global__ void __launch_bounds__(NT4) k4_kernel(const DevCtx* __restrict__ cp, K4Args a) {
+__global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ cp, K4Args a) {
   extern __shared__ double sm[];
-  __shared__ DevCtx sc;
-  __shared__ double red[NT4];
+  __shared__ double red[kMaxLev * NW4];
   pdl_wait();
   pdl_trigger();
-  {
-    const unsigned long long* src = (const unsigned long long*)cp;
-    unsigned long long* dst = (unsigned long long*)&sc;
-    for (int i = threadIdx.y * 32 + threadIdx.x; i < (int)(sizeof(DevCtx) / 8); i += NT4) dst[i] = src[i];
-    __syncthreads();
-  }
-  const DevCtx& c = sc;
+  const DevCtx& c = *cp;
   const Coefs& cf = c.cf;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int tid = threadIdx.y * 32 + threadIdx.x, lane = threadIdx.x;
   const int lc = c.lc;
+  int stamp = 0;
+  k4_stamp(stamp++);
   const int L = a.L, lce = L < lc ? L : lc;
   double* scr = sm + k4_level_off(D, P, lc + 1);
   const int lenc = ipow(P << (lc + 1), D);
-  double* S0 = scr;              // A / P / R scratch (4 arrays)
+  double* S0 = scr;              // pass scratch (4 arrays)
   double* SZ = scr + 4 * lenc;   // z_l
-  double* SB = scr + 5 * lenc;   // b_l / p u_{l-1}
-
+  double* SB = scr + 5 * lenc;   // Chebyshev direction d
   if (a.mode == 0) {
     // ú_0 = reg(A_0^{-1} f_0); u_0 = dec ú_0
     K4Lvl v0 = k4_lvl(D, P, 0, sm);
@@ -1177,83 +1248,101 @@ __global__ void __launch_bounds__(NT4) k4_kernel(const DevCtx* __restrict__ cp, 
       v0.W[(iz * n + iy) * n + ix] = acc;
     }
     __syncthreads();
-    k4_encode(lv, D, n, v0.W, lv.umant, lv.uexp, lv.ustride, a.wu_out[0], v0.U, c.status);
+    K4_BLOCKS(n, v0.len / n) {
+      long long blk = k4_blk(lv, r, x);
+      double val = x < n ? v0.W[r * n + x] : 0.0;
+      double q = warp_encode(val, a.wu_out[0], lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
+      if (x < n) v0.U[r * n + x] = q;
+    }
+    __syncthreads();
     for (int e = tid; e < v0.len; e += NT4) c.usm[c.usm_off[0] + e] = v0.U[e];
     if (lc == 0) k4_to_global(D, n, v0.U, c.U[0], lv.g);
     return;
   }
 
-  // ---- load the persisted u_l the residual needs (L <= lc) --------------------
   if (L <= lc) {
+    // ---- residual inside K4: u_L (persisted or P u_{L-1}), t_L = f_L - A_L u_L,
+    //      r_L = enc(t_L)
     K4Lvl vL = k4_lvl(D, P, L, sm);
     if (a.first) {
       K4Lvl vp = k4_lvl(D, P, L - 1, sm);
       for (int e = tid; e < vp.len; e += NT4) vp.U[e] = c.usm[c.usm_off[L - 1] + e];
       __syncthreads();
-      k4_P<D, P>(cf, vL.n, vp.U, vL.U, S0);  // u_L = dec(0) + P u_{L-1}
+      k4_P2<D, P>(cf, vL.n, vp.U, vL.U, nullptr, nullptr, S0);
     } else {
       for (int e = tid; e < vL.len; e += NT4) vL.U[e] = c.usm[c.usm_off[L] + e];
       __syncthreads();
     }
-    // residual t_L = f_L - A_L u_L, r_L = enc(t_L)
     const LevelDev& lv = c.lv[L];
     const int n = vL.n;
-    k4_A<D, P>(cf, L, n, vL.U, vL.T, S0);
-    for (int e = tid; e < vL.len; e += NT4) {
-      int x = e % n, y = (e / n) % n, z = (D == 3) ? e / (n * n) : 0;
+    k4_A<D, P>(cf, L, n, vL.U, S0, [&](int r, int x, double au) {
+      int y = r % n, z = (D == 3) ? r / n : 0;
       double t = 0.0;
-      if (unk1(x, n) && unk1(y, n) && (D == 2 || unk1(z, n))) {
+      if (x < n && unk1(x, n) && unk1(y, n) && (D == 2 || unk1(z, n))) {
         double f = cf.rhs_c * lv.gtab[x];
         f = f * lv.gtab[y];
         if (D == 3) f = f * lv.gtab[z];
-        t = f - vL.T[e];
+        t = f - au;
       }
-      vL.T[e] = t;
-    }
-    __syncthreads();
-    k4_encode(lv, D, n, vL.T, lv.rmant, lv.rexp, lv.rstride, a.wr[L], vL.RQ, c.status);
+      long long blk = k4_blk(lv, r, x);
+      double q = warp_encode(t, a.wr[L], lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
+      if (x < n) {
+        vL.T[r * n + x] = t;
+        vL.RQ[r * n + x] = q;
+      }
+    });
   } else {
-    // restriction from the grid level lc+1 (global t_{lc+1})
+    // ---- restriction from the grid level lc+1 (global t_{lc+1})
     K4Lvl vc = k4_lvl(D, P, lc, sm);
     const Geom& gf = c.lv[lc + 1].g;
-    k4_R<D, P>(cf, gf.n, c.T[(lc + 1) & 1], gf.NX, (long long)gf.NX * gf.NY, vc.T, S0);
-    k4_encode(c.lv[lc], D, vc.n, vc.T, c.lv[lc].rmant, c.lv[lc].rexp, c.lv[lc].rstride, a.wr[lc], vc.RQ, c.status);
+    const LevelDev& lv = c.lv[lc];
+    const int n = vc.n;
+    k4_R<D, P>(cf, gf.n, c.T[(lc + 1) & 1], gf.NX, (long long)gf.NX * gf.NY, S0, [&](int r, int x, double t) {
+      long long blk = k4_blk(lv, r, x);
+      double q = warp_encode(t, a.wr[lc], lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
+      if (x < n) {
+        vc.T[r * n + x] = t;
+        vc.RQ[r * n + x] = q;
+      }
+    });
   }
-  // restriction sweep inside smem
+  k4_stamp(stamp++);
+  // ---- restriction sweep inside smem, r_l = enc(t_l)
   for (int l = lce - 1; l >= 0; --l) {
     K4Lvl vf = k4_lvl(D, P, l + 1, sm), vc = k4_lvl(D, P, l, sm);
-    k4_R<D, P>(cf, vf.n, vf.T, vf.n, (long long)vf.n * vf.n, vc.T, S0);
-    k4_encode(c.lv[l], D, vc.n, vc.T, c.lv[l].rmant, c.lv[l].rexp, c.lv[l].rstride, a.wr[l], vc.RQ, c.status);
+    const LevelDev& lv = c.lv[l];
+    const int n = vc.n;
+    k4_R<D, P>(cf, vf.n, vf.T, vf.n, (long long)vf.n * vf.n, S0, [&](int r, int x, double t) {
+      long long blk = k4_blk(lv, r, x);
+      double q = warp_encode(t, a.wr[l], lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
+      if (x < n) {
+        vc.T[r * n + x] = t;
+        vc.RQ[r * n + x] = q;
+      }
+    });
   }
-  // norms ||t_l||_2, l = 0..L (grid levels from their tile partials): per-warp
-  // sums for every level, then one thread per level adds the 16 warp sums.
-  for (int l = 0; l <= L; ++l) {
+  k4_stamp(stamp++);
+  // ---- norms ||t_l||_2 of the smem levels (grid levels: deferred, k_norms_all)
+  for (int l = 0; l <= lce; ++l) {
+    K4Lvl v = k4_lvl(D, P, l, sm);
     double sacc = 0.0;
-    if (l <= lce) {
-      K4Lvl v = k4_lvl(D, P, l, sm);
-      for (int e = tid; e < v.len; e += NT4) sacc = fma(v.T[e], v.T[e], sacc);
-    } else {
-      const LevelDev& lv = c.lv[l];
-      int nt = lv.tx * lv.ty * lv.tz;
-      for (int i = tid; i < nt; i += NT4) sacc += lv.part[i];
-    }
+    for (int e = tid; e < v.len; e += NT4) sacc = fma(v.T[e], v.T[e], sacc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(FULL, sacc, o);
-    if (threadIdx.x == 0) red[l * NW4 + threadIdx.y] = sacc;
+    if (lane == 0) red[l * NW4 + threadIdx.y] = sacc;
   }
-  __syncthreads();
-  if (tid <= L) {
-    double sacc = 0.0;
-    for (int i = 0; i < NW4; ++i) sacc += red[tid * NW4 + i];
-    c.norms[(long long)a.row * c.levels + tid] = sqrt(sacc);
-  }
-  // coarse level (reading R5): ý_0 = enc(A_0^{-1} dec r_0); w_0 = dec ý_0;
-  // ú_0 = enc(dec ú_0 + dec ý_0); u_0 = dec ú_0
+  // ---- coarse level (reading R5): ý_0 = enc(A_0^{-1} dec r_0);
+  //      w_0 = dec ý_0; ú_0 = enc(dec ú_0 + dec ý_0); u_0 = dec ú_0
   {
     K4Lvl v0 = k4_lvl(D, P, 0, sm);
     const int n = v0.n, m = 2 * P - 1;
     for (int e = tid; e < v0.len; e += NT4) SB[e] = 0.0;
     __syncthreads();
+    if (tid <= lce) {
+      double sacc = 0.0;
+      for (int i = 0; i < NW4; ++i) sacc += red[tid * NW4 + i];
+      c.norms[(long long)a.row * c.levels + tid] = sqrt(sacc);
+    }
     for (int I = tid; I < c.n0; I += NT4) {
       double acc = 0.0;
       for (int J = 0; J < c.n0; ++J) {
@@ -1265,10 +1354,8 @@ __global__ void __launch_bounds__(NT4) k4_kernel(const DevCtx* __restrict__ cp, 
     }
     __syncthreads();
     const LevelDev& lv = c.lv[0];
-    const int lane = threadIdx.x, nxb = lv.g.NX >> 5, rows = (D == 3) ? n * n : n;
-    for (int rb = threadIdx.y; rb < rows * nxb; rb += NW4) {
-      int r = rb / nxb, xb = rb % nxb, x = xb * 32 + lane;
-      long long blk = (long long)r * nxb + xb;
+    K4_BLOCKS(n, v0.len / n) {
+      long long blk = k4_blk(lv, r, x);
       double y = x < n ? SB[r * n + x] : 0.0;
       double yq = warp_encode(y, a.wr[0], nullptr, nullptr, lane, c.status);
       uint32_t* uw = lv.umant + blk * lv.ustride;
@@ -1281,60 +1368,96 @@ __global__ void __launch_bounds__(NT4) k4_kernel(const DevCtx* __restrict__ cp, 
     }
     __syncthreads();
   }
-  // coarse-to-fine sweep with Chebyshev-Jacobi
+  k4_stamp(stamp++);
+  // ---- coarse-to-fine sweep, Chebyshev-Jacobi,
+  //      correction and the next sweep's u_l, fused per level
+  const int k = c.n_cheb;
   for (int l = 1; l <= lce; ++l) {
     K4Lvl vp = k4_lvl(D, P, l - 1, sm), v = k4_lvl(D, P, l, sm);
-    const int n = v.n, len = v.len;
-    double* Y = v.T;   // t_l is dead now: reuse for the Chebyshev iterate
-    k4_P<D, P>(cf, n, vp.W, SZ, S0);                 // z_l = P w_{l-1}
-    k4_A<D, P>(cf, l, n, SZ, SB, S0);                // A z
-    for (int e = tid; e < len; e += NT4) {
-      double b = v.RQ[e] - SB[e];                    // b = dec r_l - A z
-      double d = cf.inv_theta * (k4_invd(cf, D, P, l, n, e) * b);
-      v.RQ[e] = b;                                   // RQ now holds b
-      SB[e] = d;                                     // SB holds d
-      Y[e] = d;                                      // y_1 = d_1
-    }
-    __syncthreads();
-    for (int j = 2; j <= c.n_cheb; ++j) {
-      k4_A<D, P>(cf, l, n, Y, v.U, S0);              // A y (u_l slot is free until the finalize)
-      for (int e = tid; e < len; e += NT4) {
-        double q = v.RQ[e] - v.U[e];
-        double d = fma(cf.cal[j - 1], SB[e], cf.cbe[j - 1] * (k4_invd(cf, D, P, l, n, e) * q));
-        SB[e] = d;
-        Y[e] = Y[e] + d;
-      }
-      __syncthreads();
-    }
-    k4_P<D, P>(cf, n, vp.U, v.U, S0);                // P u_{l-1} (new) for the emitted u_l
-    // finalise: ý_l = enc_wr(y); w_l = z_l + dec ý; ú_l = enc(dec ú_l + dec ý); u_l = dec ú_l + P u_{l-1}
+    const int n = v.n;
     const LevelDev& lv = c.lv[l];
-    const int lane = threadIdx.x, nxb = lv.g.NX >> 5, rows = (D == 3) ? n * n : n;
-    for (int rb = threadIdx.y; rb < rows * nxb; rb += NW4) {
-      int r = rb / nxb, xb = rb % nxb, x = xb * 32 + lane;
-      long long blk = (long long)r * nxb + xb;
-      double y = x < n ? Y[r * n + x] : 0.0;
+    double* Y = v.T;    // t_l is dead: Chebyshev iterate
+    double* PU = v.U;   // P u_{l-1} (new), then the emitted u_l
+    k4_P2<D, P>(cf, n, vp.W, SZ, vp.U, PU, S0);  // z_l = P w_{l-1}; P u_{l-1}
+    k4_stamp(stamp++);
+    auto finalize = [&](int r, int x, double y) {
+      // ý_l = enc_wr(y); w_l = z_l + dec ý; ú_l = enc(dec ú_l + dec ý); u_l = dec ú_l + P u_{l-1}
+      long long blk = k4_blk(lv, r, x);
       double yq = warp_encode(y, a.wr[l], nullptr, nullptr, lane, c.status);
       uint32_t* uw = lv.umant + blk * lv.ustride;
       double uo = warp_decode(uw, lv.uexp[blk], a.wu_in[l], lane);
       double uq = warp_encode(uo + yq, a.wu_out[l], uw, lv.uexp + blk, lane, c.status);
       if (x < n) {
         v.W[r * n + x] = SZ[r * n + x] + yq;
-        v.U[r * n + x] = uq + v.U[r * n + x];
+        PU[r * n + x] = uq + PU[r * n + x];
       }
+    };
+    // b = dec r_l - A z_l; d_1 = inv_theta (invD b); y_1 = d_1
+    k4_A<D, P>(cf, l, n, SZ, S0, [&](int r, int x, double az) {
+      double b = 0.0, d = 0.0;
+      if (x < n) {
+        b = v.RQ[r * n + x] - az;
+        d = cf.inv_theta * (k4_invd_at(cf, D, P, l, n, r, x) * b);
+      }
+      if (k == 1) {
+        finalize(r, x, d);
+      } else if (x < n) {
+        v.RQ[r * n + x] = b;
+        SB[r * n + x] = d;
+        Y[r * n + x] = d;
+      }
+    });
+    k4_stamp(stamp++);
+    for (int j = 2; j <= k; ++j) {
+      // q = b - A y; d_j = fma(alpha_j, d_{j-1}, beta_j (invD q)); y_j = y_{j-1} + d_j
+      k4_A<D, P>(cf, l, n, Y, S0, [&](int r, int x, double ay) {
+        double y = 0.0;
+        if (x < n) {
+          double q = v.RQ[r * n + x] - ay;
+          double d = fma(cf.cal[j - 1], SB[r * n + x], cf.cbe[j - 1] * (k4_invd_at(cf, D, P, l, n, r, x) * q));
+          y = Y[r * n + x] + d;
+          if (j < k) {
+            SB[r * n + x] = d;
+            Y[r * n + x] = y;
+          }
+        }
+        if (j == k) finalize(r, x, y);
+      });
+      k4_stamp(stamp++);
     }
-    __syncthreads();
   }
-  // persist u_l; hand w_lc, u_lc to the grid levels above
+  // ---- persist u_l; hand u_lc, w_lc to the grid levels above
   for (int l = 0; l <= lce; ++l) {
     K4Lvl v = k4_lvl(D, P, l, sm);
     for (int e = tid; e < v.len; e += NT4) c.usm[c.usm_off[l] + e] = v.U[e];
   }
-  if (lce == lc) {  // the grid levels above (this or the next FMG level) read u_lc, w_lc
+  if (lce == lc) {
     K4Lvl v = k4_lvl(D, P, lc, sm);
     k4_to_global(D, v.n, v.U, c.U[lc & 1], c.lv[lc].g);
     k4_to_global(D, v.n, v.W, c.W[lc & 1], c.lv[lc].g);
   }
+  __syncthreads();
+  k4_stamp(stamp++);
+}
+
+void k4_debug(int on) { cudaMemcpyToSymbol(g_k4_debug, &on, sizeof(int)); }
+void k4_stamps(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_k4_stamps, sizeof(unsigned long long) * 64); }
+
+// Deferred norms of the grid levels (end of the solve, off the critical path):
+// one CTA per entry, fixed-order reduction.
+__global__ void __launch_bounds__(256) k_norms_all(const DevCtx* __restrict__ cp, const NormEntry* __restrict__ en) {
+  __shared__ double red[256];
+  const DevCtx& c = *cp;
+  NormEntry e = en[blockIdx.x];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < e.count; i += 256) s += c.pbase[e.poff + i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) c.norms[(long long)e.row * c.levels + e.l] = sqrt(red[0]);
 }
 
 // ------------------------------------------------------- error norms -------
@@ -1490,9 +1613,9 @@ static cudaError_t launch_pdl(K kernel, dim3 grid, int smem, cudaStream_t st, Ar
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
-void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& op, int ntiles) {
+void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& op, int tx, int ty, int tz) {
   const DevCtx* c = (const DevCtx*)devctx;
-#define F(D, P) launch_pdl(k_op<D, P>, dim3(ntiles), Plan<D, P>::SMEM, st, c, op)
+#define F(D, P) launch_pdl(k_op<D, P>, dim3(tx, ty, tz), Plan<D, P>::SMEM, st, c, op)
   FMG_DISPATCH(dim, p, F);
 #undef F
 }
@@ -1517,6 +1640,7 @@ void launch_k4(int dim, int p, cudaStream_t st, const void* devctx, const K4Desc
 }
 
 size_t devctx_size() { return sizeof(DevCtx); }
+void set_devctx_pbase(void* host_buf, double* pbase) { ((DevCtx*)host_buf)->pbase = pbase; }
 size_t op_size() { return sizeof(Op); }
 
 void fill_devctx(void* host_buf, const DevCtxDesc& d) {
@@ -1536,6 +1660,7 @@ void fill_devctx(void* host_buf, const DevCtxDesc& d) {
     lv.ty = d.tiles[l][1];
     lv.tz = d.tiles[l][2];
     lv.part = d.part[l];
+    lv.count = d.count ? d.count + l : nullptr;
   }
   for (int i = 0; i < 2; ++i) {
     c->U[i] = d.U[i];
@@ -1544,6 +1669,7 @@ void fill_devctx(void* host_buf, const DevCtxDesc& d) {
     c->Y[i] = d.Y[i];
   }
   c->usm = d.usm;
+  c->pbase = d.pbase;
   for (int l = 0; l < kMaxLev; ++l) c->usm_off[l] = d.usm_off[l];
   c->lc = d.lc;
   c->n_cheb = d.n_cheb;
@@ -1560,6 +1686,10 @@ void fill_devctx(void* host_buf, const DevCtxDesc& d) {
 }
 
 void pack_op(void* dst, const OpDesc& od) { memcpy(dst, &od, sizeof(Op)); }
+
+void launch_norms_all(cudaStream_t st, const void* devctx, const NormEntry* entries_dev, int n) {
+  if (n > 0) k_norms_all<<<n, 256, 0, st>>>((const DevCtx*)devctx, entries_dev);
+}
 
 void launch_errors(const Launch& L, const double* U, const Geom& g, double* partials, int* nparts) {
   ErrTab et;
