@@ -391,10 +391,23 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   // (env FMG_LC caps it).
   int lc_cap = Lmax;
   if (const char* e = getenv("FMG_LC")) lc_cap = std::min(lc_cap, atoi(e));
+  // bytes K4 needs for levels 0..lc: dense level arrays + scratch + staged sections + A_0^{-1}
+  auto k4_bytes = [&](int lc) {
+    long long b = k4_smem_bytes(dim, p, lc);
+    for (int l = 0; l <= lc; ++l) {
+      int n = p << (l + 1), NX = ((n + 31) / 32) * 32;
+      long long nblk = (long long)NX * n * (dim == 3 ? n : 1) / 32;
+      b += nblk * 4 * (wu(c, l, Lmax) + wr(c, l, Lmax)) + 2 * nblk;
+    }
+    b = (b + 15) / 16 * 16;
+    int n0 = coarse_count(dim, p);
+    if (k4_ainv_staged(n0)) b += 8LL * n0 * n0;
+    return b;
+  };
   c->lc = 0;
   for (int l = 0; l <= lc_cap; ++l)
-    if (k4_smem_bytes(dim, p, l) <= 200 * 1024) c->lc = l;
-  c->k4_smem = k4_smem_bytes(dim, p, c->lc);
+    if (k4_bytes(l) <= 210 * 1024) c->lc = l;
+  c->k4_smem = (int)k4_bytes(c->lc);
   int rc = FMG_OK;
   long long tot_parts = 0;
   DevCtxDesc dd{};

@@ -105,6 +105,7 @@ void fill_devctx(void* host_buf, const DevCtxDesc& d);
 void pack_op(void* dst, const OpDesc& od);
 void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int tx, int ty, int tz);
 int k4_smem_bytes(int dim, int p, int lc);
+int k4_ainv_staged(int n0);
 void launch_k4(int dim, int p, cudaStream_t st, const void* devctx, const K4Desc& a, int smem);
 void launch_norms_all(cudaStream_t st, const void* devctx, const NormEntry* entries_dev, int n);
 void launch_errors(const Launch& L, const double* U, const Geom& g, double* partials, int* nparts);

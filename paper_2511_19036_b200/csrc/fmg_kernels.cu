@@ -912,7 +912,8 @@ __global__ void __launch_bounds__(NT) k_op(const DevCtx* __restrict__ cp, Op op)
 // tile ops.  For FMG levels L <= lc the whole IR iteration
 // (residual included) runs here.
 constexpr int NW4 = 16, NT4 = 32 * NW4;
-constexpr int K4_MAX_SMEM = 200 * 1024;  // dynamic smem budget of the K4 CTA
+constexpr int K4_MAX_SMEM = 210 * 1024;  // dynamic smem budget of the K4 CTA
+constexpr int K4_AINV_MAX = 4096;         // A_0^{-1} entries staged in smem
 
 using K4Args = K4Desc;
 
@@ -1221,6 +1222,33 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
   double* S0 = scr;              // pass scratch (4 arrays)
   double* SZ = scr + 4 * lenc;   // z_l
   double* SB = scr + 5 * lenc;   // Chebyshev direction d
+  // Shared-memory staging of the sections of levels 0..lc (read once in the
+  // prologue, written back once in the epilogue) and of A_0^{-1}.
+  __shared__ uint32_t* s_uw[kMaxLev];
+  __shared__ uint32_t* s_rw[kMaxLev];
+  __shared__ int8_t* s_ue[kMaxLev];
+  __shared__ int8_t* s_re[kMaxLev];
+  __shared__ const double* s_ainv;
+  if (tid == 0) {
+    char* p = (char*)(scr + 6 * lenc);
+    for (int l = 0; l <= lc; ++l) {
+      const LevelDev& lv = c.lv[l];
+      s_uw[l] = (uint32_t*)p;
+      p += 4 * lv.g.nblk * lv.ustride;
+      s_rw[l] = (uint32_t*)p;
+      p += 4 * lv.g.nblk * lv.rstride;
+    }
+    for (int l = 0; l <= lc; ++l) {
+      const LevelDev& lv = c.lv[l];
+      s_ue[l] = (int8_t*)p;
+      p += lv.g.nblk;
+      s_re[l] = (int8_t*)p;
+      p += lv.g.nblk;
+    }
+    p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    s_ainv = (c.n0 * c.n0 <= K4_AINV_MAX) ? (const double*)p : c.Ainv;
+  }
+  __syncthreads();
   if (a.mode == 0) {
     // ú_0 = reg(A_0^{-1} f_0); u_0 = dec ú_0
     K4Lvl v0 = k4_lvl(D, P, 0, sm);
@@ -1260,6 +1288,26 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
     return;
   }
 
+  // ---- prologue: one round of coalesced loads (ú sections, A_0^{-1}, and in 2D
+  //      the fine-level t_{lc+1} feeding the first restriction)
+  for (int l = 0; l <= lce; ++l) {
+    const LevelDev& lv = c.lv[l];
+    const int nw = (int)(lv.g.nblk * lv.ustride);
+    for (int i = tid; i < nw; i += NT4) s_uw[l][i] = lv.umant[i];
+    for (int i = tid; i < (int)lv.g.nblk; i += NT4) s_ue[l][i] = lv.uexp[i];
+  }
+  if (s_ainv != c.Ainv)
+    for (int i = tid; i < c.n0 * c.n0; i += NT4) ((double*)s_ainv)[i] = c.Ainv[i];
+  const bool stage_fine = D == 2 && L > lc &&
+                          (long long)c.lv[lc + 1].g.NX * c.lv[lc + 1].g.NY <= 4LL * lenc;
+  if (stage_fine) {
+    const Geom& gf = c.lv[lc + 1].g;
+    const double* src = c.T[(lc + 1) & 1];
+    const int nt = gf.NX * gf.NY;
+    for (int i = tid; i < nt; i += NT4) S0[i] = src[i];
+  }
+  __syncthreads();
+
   if (L <= lc) {
     // ---- residual inside K4: u_L (persisted or P u_{L-1}), t_L = f_L - A_L u_L,
     //      r_L = enc(t_L)
@@ -1285,7 +1333,7 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
         t = f - au;
       }
       long long blk = k4_blk(lv, r, x);
-      double q = warp_encode(t, a.wr[L], lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
+      double q = warp_encode(t, a.wr[L], s_rw[L] + blk * lv.rstride, s_re[L] + blk, lane, c.status);
       if (x < n) {
         vL.T[r * n + x] = t;
         vL.RQ[r * n + x] = q;
@@ -1297,9 +1345,11 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
     const Geom& gf = c.lv[lc + 1].g;
     const LevelDev& lv = c.lv[lc];
     const int n = vc.n;
-    k4_R<D, P>(cf, gf.n, c.T[(lc + 1) & 1], gf.NX, (long long)gf.NX * gf.NY, S0, [&](int r, int x, double t) {
+    const double* fine = stage_fine ? S0 : c.T[(lc + 1) & 1];
+    double* rscr = stage_fine ? S0 + 4 * lenc : S0;  // 2D: t1 (2 lenc) after the staged fine level
+    k4_R<D, P>(cf, gf.n, fine, gf.NX, (long long)gf.NX * gf.NY, rscr, [&](int r, int x, double t) {
       long long blk = k4_blk(lv, r, x);
-      double q = warp_encode(t, a.wr[lc], lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
+      double q = warp_encode(t, a.wr[lc], s_rw[lc] + blk * lv.rstride, s_re[lc] + blk, lane, c.status);
       if (x < n) {
         vc.T[r * n + x] = t;
         vc.RQ[r * n + x] = q;
@@ -1314,7 +1364,7 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
     const int n = vc.n;
     k4_R<D, P>(cf, vf.n, vf.T, vf.n, (long long)vf.n * vf.n, S0, [&](int r, int x, double t) {
       long long blk = k4_blk(lv, r, x);
-      double q = warp_encode(t, a.wr[l], lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
+      double q = warp_encode(t, a.wr[l], s_rw[l] + blk * lv.rstride, s_re[l] + blk, lane, c.status);
       if (x < n) {
         vc.T[r * n + x] = t;
         vc.RQ[r * n + x] = q;
@@ -1347,7 +1397,7 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
       double acc = 0.0;
       for (int J = 0; J < c.n0; ++J) {
         int jx = J % m + 1, jy = (J / m) % m + 1, jz = (D == 3) ? J / (m * m) + 1 : 0;
-        acc = fma(c.Ainv[(long long)I * c.n0 + J], v0.RQ[(jz * n + jy) * n + jx], acc);
+        acc = fma(s_ainv[(long long)I * c.n0 + J], v0.RQ[(jz * n + jy) * n + jx], acc);
       }
       int ix = I % m + 1, iy = (I / m) % m + 1, iz = (D == 3) ? I / (m * m) + 1 : 0;
       SB[(iz * n + iy) * n + ix] = acc;
@@ -1358,9 +1408,9 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
       long long blk = k4_blk(lv, r, x);
       double y = x < n ? SB[r * n + x] : 0.0;
       double yq = warp_encode(y, a.wr[0], nullptr, nullptr, lane, c.status);
-      uint32_t* uw = lv.umant + blk * lv.ustride;
-      double uo = warp_decode(uw, lv.uexp[blk], a.wu_in[0], lane);
-      double uq = warp_encode(uo + yq, a.wu_out[0], uw, lv.uexp + blk, lane, c.status);
+      uint32_t* uw = s_uw[0] + blk * lv.ustride;
+      double uo = warp_decode(uw, s_ue[0][blk], a.wu_in[0], lane);
+      double uq = warp_encode(uo + yq, a.wu_out[0], uw, s_ue[0] + blk, lane, c.status);
       if (x < n) {
         v0.W[r * n + x] = yq;
         v0.U[r * n + x] = uq;
@@ -1384,9 +1434,9 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
       // ý_l = enc_wr(y); w_l = z_l + dec ý; ú_l = enc(dec ú_l + dec ý); u_l = dec ú_l + P u_{l-1}
       long long blk = k4_blk(lv, r, x);
       double yq = warp_encode(y, a.wr[l], nullptr, nullptr, lane, c.status);
-      uint32_t* uw = lv.umant + blk * lv.ustride;
-      double uo = warp_decode(uw, lv.uexp[blk], a.wu_in[l], lane);
-      double uq = warp_encode(uo + yq, a.wu_out[l], uw, lv.uexp + blk, lane, c.status);
+      uint32_t* uw = s_uw[l] + blk * lv.ustride;
+      double uo = warp_decode(uw, s_ue[l][blk], a.wu_in[l], lane);
+      double uq = warp_encode(uo + yq, a.wu_out[l], uw, s_ue[l] + blk, lane, c.status);
       if (x < n) {
         v.W[r * n + x] = SZ[r * n + x] + yq;
         PU[r * n + x] = uq + PU[r * n + x];
@@ -1424,6 +1474,17 @@ __global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ c
         if (j == k) finalize(r, x, y);
       });
       k4_stamp(stamp++);
+    }
+  }
+  // ---- epilogue: sections back to global (one round of coalesced stores)
+  for (int l = 0; l <= lce; ++l) {
+    const LevelDev& lv = c.lv[l];
+    const int nu = (int)(lv.g.nblk * lv.ustride), nr = (int)(lv.g.nblk * lv.rstride);
+    for (int i = tid; i < nu; i += NT4) lv.umant[i] = s_uw[l][i];
+    for (int i = tid; i < nr; i += NT4) lv.rmant[i] = s_rw[l][i];
+    for (int i = tid; i < (int)lv.g.nblk; i += NT4) {
+      lv.uexp[i] = s_ue[l][i];
+      lv.rexp[i] = s_re[l][i];
     }
   }
   // ---- persist u_l; hand u_lc, w_lc to the grid levels above
@@ -1621,6 +1682,7 @@ void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc
 }
 
 int k4_smem_bytes(int dim, int p, int lc) { return k4_smem_doubles(dim, p, lc) * 8; }
+int k4_ainv_staged(int n0) { return n0 * n0 <= K4_AINV_MAX; }
 
 void launch_k4(int dim, int p, cudaStream_t st, const void* devctx, const K4Desc& a, int smem) {
   const DevCtx* c = (const DevCtx*)devctx;
