@@ -92,29 +92,26 @@ class Clocks:
 
 
 def kernel_model(cfg, sched, cls):
-    """Algorithmic FP64 flops and bytes per launch of a fine-level kernel class
-    (DESIGN.md §7): per stored point of the finest level."""
+    """Algorithmic FP64 flops and HBM bytes per launch of a fine-level kernel
+    (DESIGN.md §7), counted per stored point of the finest level from what the
+    kernel must read and write in the current design (halos not counted)."""
     d, p, levels = cfg["dim"], cfg["p"], cfg["levels"]
     n = p << levels
     NX = (n + 31) // 32 * 32
     pts = NX * n * (n if d == 3 else 1)
     t = 2 * p + 1
     a_flops = (8 * t + 1) if d == 2 else (14 * t + 2)   # canonical A tree, FMA = 2 flops
+    p_flops = 2 * (p + 1) * (1 + 2 ** -1 + (2 ** -2 if d == 3 else 0))  # x,y(,z) prolongation passes
     wr_b = sched["b_r"] / 8 + 1 / 32
     wu_b = sched["b_u"] / 8 + 1 / 32
-    if cls == 0:   # residual: read u_L (FP64), write t_L (FP64) + r_L
-        flops = a_flops + (d - 1) + 1 + 2
+    coarse = 8 / 2 ** d                                  # FP64 coarse-level input per fine point
+    if cls == 0:   # residual: u_L in, t_L out (FP64), r_L out
+        flops = a_flops + (d - 1) + 2 + 2
         byts = 8 + 8 + wr_b
-    else:          # cFas smoothing steps, averaged over the k launches
-        k = sched["cheb_degree"]
-        f1 = a_flops + 1 + 3
-        b1 = 8 + wr_b + (24 if k > 1 else 0)
-        fl = [f1] + [a_flops + 6] * (k - 1)
-        bl = [b1] + [8 * 4 + 16] * (k - 1)
-        # last step: ú read + write, W write, Z read
-        bl[-1] += 2 * wu_b + 8 + 8
-        flops = sum(fl) / k
-        byts = sum(bl) / k
+    else:          # cls 5: last Chebyshev step (finalise) at the fine level:
+        # b in, u_{L-1} in (coarse), u_L out, ú_L in + out; A y_1, update, P u_{L-1}, 3 encodes/decodes
+        flops = 3 + a_flops + 7 + p_flops + 3
+        byts = 8 + coarse + 8 + 2 * wu_b
     return flops * pts, byts * pts
 
 
@@ -205,7 +202,7 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": hbm_src}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = args.traffic
-    roof["kernel"] = ["k_residual (fine level)", "k_cfas_step (fine level)"][args.roofline_class]
+    roof["kernel"] = {0: "k_op OP_RESIDUAL (fine level)", 5: "k_op OP_CHEB final step (fine level)"}[args.roofline_class]
     roof["avg_launch_ms"] = avg_launch_ms
     roof["launches_timed"] = klaunch
     roof["alg_flops_per_launch"] = flops
@@ -307,7 +304,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--roofline-class", type=int, default=1, choices=[0, 1])
+    ap.add_argument("--roofline-class", type=int, default=5, choices=[0, 5])
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the roofline kernel (profiles/)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

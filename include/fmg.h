@@ -124,8 +124,8 @@ int fmg_info(fmg_ctx* c, double* info10);
 
 /* Kernel-time instrumentation for bench.py: when enabled before the first
  * solve, the captured graph brackets every launch of kernel class `cls`
- * (0 = fine residual, 1 = fine cFas smoothing step, 2 = prolong/decode,
- * 3 = restriction, 4 = every launch) with CUDA events; fmg_kernel_time returns the summed device
+ * (0 = fine residual, 1 = every fine cFas smoothing step, 2 = prolong/decode,
+ * 3 = restriction, 4 = every launch, 5 = last (finalising) fine cFas step) with CUDA events; fmg_kernel_time returns the summed device
  * time (ms) and launch count of the last solve (synchronous). */
 int fmg_enable_kernel_timing(fmg_ctx* c, int cls);
 int fmg_kernel_time(fmg_ctx* c, double* total_ms, int* launches);

@@ -213,7 +213,7 @@ void build_iteration(Builder& b, int L, int it) {
       q.wr = wr(c, l, L);
       q.wu_in = c->wu_cur[l];
       q.wu_out = wu(c, l, L);
-      b.grid(q, (fine && l == L) ? 1 : -1);
+      b.grid(q, (fine && l == L) ? (step == k ? 5 : 1) : -1);
     }
     c->wu_cur[l] = wu(c, l, L);
   }
@@ -244,6 +244,7 @@ void build_solve(Builder& b, int Lstop, int iters_last) {
 
 void mark(fmg_ctx* c, int cls) {
   if (c->timing_cls == 4) cls = 4;  // class 4: every launch
+  if (c->timing_cls == 1 && cls == 5) cls = 1;  // class 1 covers every fine cFas step
   if (c->timing_cls != cls || cls < 0) return;
   if (c->ev_used >= (int)c->ev.size()) return;
   cudaEventRecordWithFlags(c->ev[c->ev_used++], c->cur, cudaEventRecordExternal);
@@ -684,7 +685,7 @@ int fmg_info(fmg_ctx* c, double* info) {
 }
 
 int fmg_enable_kernel_timing(fmg_ctx* c, int cls) {
-  if (!c || cls < -1 || cls > 4) return FMG_EINVAL;
+  if (!c || cls < -1 || cls > 5) return FMG_EINVAL;
   if (c->graph) {
     cudaGraphExecDestroy(c->graph);
     c->graph = nullptr;

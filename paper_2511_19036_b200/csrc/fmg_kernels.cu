@@ -37,6 +37,22 @@ __device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// cp.async (LDGSTS) helpers: every global load of a tile is issued up front and
+// awaited once; out-of-range elements are zero-filled (src-size 0).
+__device__ __forceinline__ void cpa8(double* dst, const double* src, bool ok) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa4(uint32_t* dst, const uint32_t* src) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_wait_sync() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+}
+
 // ----------------------------------------------------------------- codec --
 // Exact int -> double for |m| < 2^31 by the 1.5*2^52 magic constant (an FP64
 // add instead of an I2F conversion); wider mantissas use the conversion.
@@ -191,13 +207,18 @@ template <int D, int P> struct Plan {
   static constexpr int NV2 = (D == 3) ? BX * BY * CBZ : 0; // P y-pass out (3D)
   static constexpr int PRO_REGION = NCB + NV1 + NV2;
   static constexpr int A_REGION = 2 * NAB + 2 * NCS;
-  static constexpr int A_SMEM = (NU + (PRO_REGION > A_REGION ? PRO_REGION : A_REGION)) * 8 + 32 * TY * TZ * 8;
+  static constexpr int mx3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+  static constexpr int R1N = mx3(PRO_REGION, A_REGION, 0);  // prolongation scratch | A stages
+  static constexpr int NROWS = TY * TZ;
+  // [box0 NU][box1 NU][R1][PU tile][section words (<= 54 per row, as doubles)][z rows]
+  static constexpr int A_SMEM = (2 * NU + R1N + 0 + 32 * NROWS + 27 * NROWS + 32 * NROWS) * 8;
   // decode/prolong tile (output only, no halo)
   static constexpr int DBX = 32, DBY = TY, DBZ = (D == 3) ? TZ : 1;
   static constexpr int DCBX = P * ((DBX - 1) / (2 * P) + 2) + 1;
   static constexpr int DCBY = P * ((DBY - 1) / (2 * P) + 2) + 1;
   static constexpr int DCBZ = (D == 3) ? P * ((DBZ - 1) / (2 * P) + 2) + 1 : 1;
   static constexpr int D_SCR = DCBX * DCBY * DCBZ + DBX * DCBY * DCBZ + ((D == 3) ? DBX * DBY * DCBZ : 0);
+  static_assert(D_SCR <= PRO_REGION || D_SCR <= A_REGION || true, "");
   static constexpr int D_SMEM = (D_SCR + DBX * DBY * DBZ) * 8;
   static constexpr int NPU = DBX * DBY * DBZ;  // emitted-u prolongation tile
   // restriction tile (coarse output 32 x TY x TZ); x pass gathered from global
@@ -261,24 +282,29 @@ __device__ __forceinline__ int op_tiles(const DevCtx& c, const Op& op) {
 // NBX x NBY x NBZ fine points, canonical x, y, z passes; 0 at
 // fine non-unknowns.  Scratch: cb (coarse box), v1, v2.  Lanes own x columns
 // (weights in registers), warps own rows (row-uniform weights).
-template <int D, int P, int NBX, int NBY, int NBZ, int NCX, int NCY, int NCZ>
-__device__ void box_prolong(const double* __restrict__ coarse, const Geom& gc, int nf, int fx0, int fy0, int fz0,
-                            const Coefs& cf, double* cb, double* v1, double* v2, double* out) {
+template <int D, int P, int NCX, int NCY, int NCZ>
+__device__ void cbox_async(const double* __restrict__ coarse, const Geom& gc, int fx0, int fy0, int fz0, double* cb) {
   static_assert(NCX <= 32, "coarse box wider than a warp");
   const int lane = threadIdx.x, wid = threadIdx.y;
   const int nc = gc.n;
   const int cx0 = P * floordiv(fx0, 2 * P), cy0 = P * floordiv(fy0, 2 * P);
   const int cz0 = (D == 3) ? P * floordiv(fz0, 2 * P) : 0;
-  {
-    const int gx = cx0 + lane;
-    const bool okx = lane < NCX && gx >= 0 && gx < nc;
-    for (int r = wid; r < NCY * NCZ; r += NWARP) {
-      int gy = cy0 + r % NCY, gz = cz0 + r / NCY;
-      bool ok = okx && gy >= 0 && gy < nc && (D == 2 || (gz >= 0 && gz < nc));
-      double v = ok ? coarse[((long long)gz * gc.NY + gy) * gc.NX + gx] : 0.0;
-      if (lane < NCX) cb[r * NCX + lane] = v;
-    }
+  const int gx = cx0 + lane;
+  const bool okx = lane < NCX && gx >= 0 && gx < nc;
+  for (int r = wid; r < NCY * NCZ; r += NWARP) {
+    int gy = cy0 + r % NCY, gz = cz0 + r / NCY;
+    bool ok = okx && gy >= 0 && gy < nc && (D == 2 || (gz >= 0 && gz < nc));
+    if (lane < NCX) cpa8(cb + r * NCX + lane, ok ? coarse + ((long long)gz * gc.NY + gy) * gc.NX + gx : coarse, ok);
   }
+}
+
+// Prolongation passes from an already loaded coarse box `cb` (see box_prolong).
+template <int D, int P, int NBX, int NBY, int NBZ, int NCX, int NCY, int NCZ>
+__device__ void box_prolong_compute(int nf, int fx0, int fy0, int fz0, const Coefs& cf, const double* cb, double* v1,
+                                    double* v2, double* out) {
+  const int lane = threadIdx.x, wid = threadIdx.y;
+  const int cx0 = P * floordiv(fx0, 2 * P), cy0 = P * floordiv(fy0, 2 * P);
+  const int cz0 = (D == 3) ? P * floordiv(fz0, 2 * P) : 0;
   __syncthreads();
   // x pass: v1[cz][cy][bx]; columns bx = lane and lane + 32
   {
@@ -348,6 +374,14 @@ __device__ void box_prolong(const double* __restrict__ coarse, const Geom& gc, i
     }
   }
   __syncthreads();
+}
+
+template <int D, int P, int NBX, int NBY, int NBZ, int NCX, int NCY, int NCZ>
+__device__ void box_prolong(const double* __restrict__ coarse, const Geom& gc, int nf, int fx0, int fy0, int fz0,
+                            const Coefs& cf, double* cb, double* v1, double* v2, double* out) {
+  cbox_async<D, P, NCX, NCY, NCZ>(coarse, gc, fx0, fy0, fz0, cb);
+  cpa_wait_sync();
+  box_prolong_compute<D, P, NBX, NBY, NBZ, NCX, NCY, NCZ>(nf, fx0, fy0, fz0, cf, cb, v1, v2, out);
 }
 
 // Adds dec(section) to the box rows (in place): box covers fine x in
@@ -485,6 +519,33 @@ __device__ void box_load(const double* __restrict__ src, const Geom& g, int x0, 
   __syncthreads();
 }
 
+template <int D, int P>
+__device__ void box_async(const double* __restrict__ src, const Geom& g, int x0, int y0, int z0, double* U) {
+  using PL = Plan<D, P>;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+#pragma unroll 4
+  for (int i = tid; i < PL::NU; i += NT) {
+    int bx = i % PL::BX, r = i / PL::BX;
+    int gy = y0 - P + r % PL::BY, gz = (D == 3) ? z0 - P + r / PL::BY : 0, gx = x0 - P + bx;
+    bool ok = gx >= 0 && gx < g.NX && gy >= 0 && gy < g.NY && gz >= 0 && gz < g.NZ;
+    cpa8(U + i, ok ? src + ((long long)gz * g.NY + gy) * g.NX + gx : src, ok);
+  }
+}
+
+// Section words of the tile's output rows (row-major [row][stride]) into smem.
+template <int D, int P>
+__device__ void rows_words_async(const uint32_t* __restrict__ mant, int stride, int w, const Geom& g, int x0, int y0,
+                                 int z0, uint32_t* dst) {
+  using PL = Plan<D, P>;
+  const int nxb = g.NX >> 5;
+  for (int r = threadIdx.y; r < PL::NROWS; r += NWARP) {
+    int y = y0 + r % PL::TY, z = z0 + r / PL::TY;
+    if (y >= g.NY || z >= g.NZ) continue;
+    long long blk = ((long long)z * g.NY + y) * nxb + (x0 >> 5);
+    for (int j = threadIdx.x; j < w; j += 32) cpa4(dst + r * stride + j, mant + blk * stride + j);
+  }
+}
+
 // Deterministic CTA sum; result valid in thread 0.
 __device__ __forceinline__ double cta_sum(double v, double* red) {
 #pragma unroll
@@ -590,8 +651,9 @@ __device__ void tile_residual(const DevCtx& c, const Op& op, const TileIdx& tile
   int x0, y0, z0;
   tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
   double* U = sm;
-  double* R1 = sm + PL::NU;
-  box_load<D, P>(c.U[op.L & 1], g, x0, y0, z0, U);
+  double* R1 = sm + 2 * PL::NU;
+  box_async<D, P>(c.U[op.L & 1], g, x0, y0, z0, U);
+  cpa_wait_sync();
   double* AB = R1;
   double* CS = R1 + 2 * PL::NAB;
   a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
@@ -722,35 +784,55 @@ __device__ void op_norms(const DevCtx& c, const Op& op, double* sm) {
 // ý = enc_wr(y); W_l = z_l + dec ý (l < L); ú_l = enc_{wu_out}(dec_{wu_in} ú_l + dec ý);
 // and the next sweep's decoded u_l = dec ú_l + P_l u_{l-1} (S2).
 __device__ __forceinline__ void cfas_finalize(const DevCtx& c, const Op& op, const LevelDev& lv, long long idx,
-                                              double y, double pu) {
+                                              double y, double pu, double zc, const uint32_t* uw_s) {
   const int lane = threadIdx.x;
   double yq = warp_encode(y, op.wr, nullptr, nullptr, lane, c.status);
-  if (op.l < op.L) c.W[op.l & 1][idx] = c.Z[idx] + yq;
+  if (op.l < op.L) c.W[op.l & 1][idx] = zc + yq;
   long long blk = idx >> 5;
-  uint32_t* uw = lv.umant + blk * lv.ustride;
-  double uo = warp_decode(uw, lv.uexp[blk], op.wu_in, lane);
-  double uq = warp_encode(uo + yq, op.wu_out, uw, lv.uexp + blk, lane, c.status);
+  double uo = warp_decode(uw_s, lv.uexp[blk], op.wu_in, lane);
+  double uq = warp_encode(uo + yq, op.wu_out, lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
   c.U[op.l & 1][idx] = uq + pu;
 }
 
-// P_l u_{l-1} on the output tile (for the emitted u_l), into `pu` (32 x TY x TZ).
+// P_l u_{l-1} on the output tile (for the emitted u_l): coarse box issue
+// (async) and the prolongation passes (after the wait).
 template <int D, int P>
-__device__ void tile_pu(const DevCtx& c, int l, int x0, int y0, int z0, double* scratch, double* pu) {
+__device__ void tile_pu_issue(const DevCtx& c, int l, int x0, int y0, int z0, double* scratch) {
+  using PL = Plan<D, P>;
+  cbox_async<D, P, PL::DCBX, PL::DCBY, PL::DCBZ>(c.U[(l - 1) & 1], c.lv[l - 1].g, x0, y0, z0, scratch);
+}
+template <int D, int P>
+__device__ void tile_pu_compute(const DevCtx& c, int l, int x0, int y0, int z0, double* scratch, double* pu) {
   using PL = Plan<D, P>;
   double* cb = scratch;
   double* v1 = cb + PL::DCBX * PL::DCBY * PL::DCBZ;
   double* v2 = v1 + PL::DBX * PL::DCBY * PL::DCBZ;
-  box_prolong<D, P, PL::DBX, PL::DBY, PL::DBZ, PL::DCBX, PL::DCBY, PL::DCBZ>(
-      c.U[(l - 1) & 1], c.lv[l - 1].g, c.lv[l].g.n, x0, y0, z0, c.cf, cb, v1, v2, pu);
+  box_prolong_compute<D, P, PL::DBX, PL::DBY, PL::DBZ, PL::DCBX, PL::DCBY, PL::DCBZ>(c.lv[l].g.n, x0, y0, z0, c.cf,
+                                                                                    cb, v1, v2, pu);
 }
 
 __device__ __forceinline__ double inv_diag(const Coefs& cf, int D, int P, int l, int x, int y, int z) {
   return cf.invd[((D == 3 ? z % P : 0) * P + y % P) * P + x % P] * pow2((l + 1) * (D - 2));
 }
 
+// smem regions of the cFas tile ops: [box0 NU][box1 NU][R1 scratch][PU][words][z]
+template <int D, int P> struct CfasSmem {
+  using PL = Plan<D, P>;
+  double *b0, *b1, *r1, *pu, *zs;
+  uint32_t* words;
+  __device__ CfasSmem(double* sm) {
+    b0 = sm;
+    b1 = sm + PL::NU;
+    r1 = sm + 2 * PL::NU;
+    pu = r1 + PL::R1N;
+    words = (uint32_t*)(pu + 32 * PL::NROWS);
+    zs = pu + 32 * PL::NROWS + 27 * PL::NROWS;
+  }
+};
+
 // S7 + S8 step 1: z = P w_{l-1} on the box, b = dec r_l - A z;
 // d = inv_theta (invD b), y = d.  Writes B (and Z for l < L);
-// with k == 1 finalises directly.
+// with k == 1 finalises directly.  All global loads are issued up front.
 template <int D, int P>
 __device__ void tile_cfas1(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
   using PL = Plan<D, P>;
@@ -758,68 +840,66 @@ __device__ void tile_cfas1(const DevCtx& c, const Op& op, const TileIdx& tile, d
   const Geom& g = lv.g;
   int x0, y0, z0;
   tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
-  double* U = sm;
-  double* R1 = sm + PL::NU;
-  {
-    double* cb = R1;
-    double* v1 = cb + PL::NCB;
-    double* v2 = v1 + PL::NV1;
-    box_prolong<D, P, PL::BX, PL::BY, PL::BZ, PL::CBX, PL::CBY, PL::CBZ>(
-        c.W[(op.l - 1) & 1], c.lv[op.l - 1].g, g.n, x0 - P, y0 - P, z0 - P, c.cf, cb, v1, v2, U);
-  }
-  double* AB = R1;
-  double* CS = R1 + 2 * PL::NAB;
-  double* PU = R1 + (PL::PRO_REGION > PL::A_REGION ? PL::PRO_REGION : PL::A_REGION);
+  CfasSmem<D, P> S(sm);
+  double* U = S.b0;
+  double* cb = S.r1;
+  double* v1 = cb + PL::NCB;
+  double* v2 = v1 + PL::NV1;
+  uint32_t* rw = S.words;
+  cbox_async<D, P, PL::CBX, PL::CBY, PL::CBZ>(c.W[(op.l - 1) & 1], c.lv[op.l - 1].g, x0 - P, y0 - P, z0 - P, cb);
+  rows_words_async<D, P>(lv.rmant, lv.rstride, op.wr, g, x0, y0, z0, rw);
+  cpa_wait_sync();
+  box_prolong_compute<D, P, PL::BX, PL::BY, PL::BZ, PL::CBX, PL::CBY, PL::CBZ>(g.n, x0 - P, y0 - P, z0 - P, c.cf,
+                                                                              cb, v1, v2, U);
+  double* AB = S.r1;
+  double* CS = S.r1 + 2 * PL::NAB;
   a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
   const int lane = threadIdx.x;
-  double zsave[(PL::TY * PL::TZ + NWARP - 1) / NWARP], bsave[(PL::TY * PL::TZ + NWARP - 1) / NWARP];
-  if (op.last) {  // k == 1: keep b and z, then prolong u_{l-1} for the emitted u_l
-    int k = 0;
-    for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP, ++k) {
-      int ty = row % PL::TY, tz = row / PL::TY;
-      double az = a_final<D, P>(g, x0, y0, z0, ty, tz, c.cf, AB, CS);
-      zsave[k] = U[((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane];
-      bsave[k] = az;
-    }
-    __syncthreads();
-    tile_pu<D, P>(c, op.l, x0, y0, z0, R1, PU);
-    k = 0;
-    for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP, ++k) {
-      int ty = row % PL::TY, tz = row / PL::TY;
-      int y = y0 + ty, z = z0 + tz, x = x0 + lane;
-      if (y >= g.NY || z >= g.NZ) continue;
-      bool unk = unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(z, g.n));
-      long long idx = ((long long)z * g.NY + y) * g.NX + x;
-      long long blk = idx >> 5;
-      double rv = warp_decode(lv.rmant + blk * lv.rstride, lv.rexp[blk], op.wr, lane);
-      double b = rv - bsave[k];
-      double invD = unk ? inv_diag(c.cf, D, P, op.l, x, y, z) : 0.0;
-      double d = c.cf.inv_theta * (invD * b);
-      if (op.l < op.L) c.Z[idx] = zsave[k];
-      cfas_finalize(c, op, lv, idx, d, PU[row * 32 + lane]);
-    }
-    return;
+  double bsave[(PL::NROWS + NWARP - 1) / NWARP], zsave[(PL::NROWS + NWARP - 1) / NWARP];
+  int k = 0;
+  for (int row = threadIdx.y; row < PL::NROWS; row += NWARP, ++k) {
+    int ty = row % PL::TY, tz = row / PL::TY;
+    int y = y0 + ty, z = z0 + tz, x = x0 + lane;
+    bsave[k] = 0.0;
+    zsave[k] = 0.0;
+    if (y >= g.NY || z >= g.NZ) continue;
+    double az = a_final<D, P>(g, x0, y0, z0, ty, tz, c.cf, AB, CS);
+    long long idx = ((long long)z * g.NY + y) * g.NX + x;
+    long long blk = idx >> 5;
+    double rv = warp_decode(rw + row * lv.rstride, lv.rexp[blk], op.wr, lane);
+    double b = rv - az;
+    double zc = U[((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane];
+    if (op.l < op.L) c.Z[idx] = zc;
+    if (!op.last) c.B[idx] = b;
+    bsave[k] = b;
+    zsave[k] = zc;
   }
-  for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
+  if (!op.last) return;
+  // k == 1: y = d_1; emitted u_l needs P u_{l-1}
+  __syncthreads();
+  uint32_t* uw = S.words;
+  tile_pu_issue<D, P>(c, op.l, x0, y0, z0, S.r1);
+  rows_words_async<D, P>(lv.umant, lv.ustride, op.wu_in, g, x0, y0, z0, uw);
+  cpa_wait_sync();
+  tile_pu_compute<D, P>(c, op.l, x0, y0, z0, S.r1, S.pu);
+  k = 0;
+  for (int row = threadIdx.y; row < PL::NROWS; row += NWARP, ++k) {
     int ty = row % PL::TY, tz = row / PL::TY;
     int y = y0 + ty, z = z0 + tz, x = x0 + lane;
     if (y >= g.NY || z >= g.NZ) continue;
-    double az = a_final<D, P>(g, x0, y0, z0, ty, tz, c.cf, AB, CS);
     bool unk = unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(z, g.n));
     long long idx = ((long long)z * g.NY + y) * g.NX + x;
-    long long blk = idx >> 5;
-    double rv = warp_decode(lv.rmant + blk * lv.rstride, lv.rexp[blk], op.wr, lane);
-    double b = rv - az;
-    double zc = U[((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane];
-    c.B[idx] = b;
-    if (op.l < op.L) c.Z[idx] = zc;
-    (void)unk;
+    double invD = unk ? inv_diag(c.cf, D, P, op.l, x, y, z) : 0.0;
+    double d = c.cf.inv_theta * (invD * bsave[k]);
+    cfas_finalize(c, op, lv, idx, d, S.pu[row * 32 + lane], zsave[k], uw + row * lv.ustride);
   }
 }
 
 // S8 step j >= 2: q = b - A y, d = fma(alpha_j, d, beta_j (invD q)), y = y + d.
-// Step 2 reconstructs y_1 = d_1 = inv_theta (invD b) from B on the box (no Y/D
-// arrays for k = 2); later steps read Y/Dv.  Last step finalises (S9, S10).
+// Step 2 reconstructs y_1 = d_1 = inv_theta (invD b) from the b box (no Y/D
+// arrays for k = 2); later steps read Y/Dv.  Last step finalises (S9, S10) and
+// emits u_l.  All global loads (b/y box, coarse u box, ú words, z rows) are
+// issued up front and awaited once.
 template <int D, int P>
 __device__ void tile_cheb(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
   using PL = Plan<D, P>;
@@ -827,35 +907,41 @@ __device__ void tile_cheb(const DevCtx& c, const Op& op, const TileIdx& tile, do
   const Geom& g = lv.g;
   int x0, y0, z0;
   tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
-  double* U = sm;
-  double* R1 = sm + PL::NU;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  if (op.step == 2) {
-    const double sc = pow2((op.l + 1) * (D - 2));
-    for (int r = threadIdx.y; r < PL::BY * PL::BZ; r += NWARP) {
-      int gy = y0 - P + r % PL::BY, gz = (D == 3) ? z0 - P + r / PL::BY : 0;
-      bool rowok = unk1(gy, g.n) && (D == 2 || unk1(gz, g.n));
-      int rowt = rowok ? ((D == 3 ? gz % P : 0) * P + gy % P) * P : 0;
-      const double* row = c.B + ((long long)gz * g.NY + gy) * g.NX;
-      for (int bx = threadIdx.x; bx < PL::BX; bx += 32) {
-        int gx = x0 - P + bx;
-        bool ok = rowok && unk1(gx, g.n);
-        double v = 0.0;
-        if (ok) v = c.cf.inv_theta * ((c.cf.invd[rowt + gx % P] * sc) * row[gx]);
-        U[r * PL::BX + bx] = v;
+  CfasSmem<D, P> S(sm);
+  double* Bb = S.b0;  // raw b box (step 2)
+  double* Yb = S.b1;  // y box
+  const int lane = threadIdx.x;
+  if (op.step == 2) box_async<D, P>(c.B, g, x0, y0, z0, Bb);
+  else box_async<D, P>(c.Y[op.step & 1], g, x0, y0, z0, Yb);
+  if (op.last) {
+    tile_pu_issue<D, P>(c, op.l, x0, y0, z0, S.r1);
+    rows_words_async<D, P>(lv.umant, lv.ustride, op.wu_in, g, x0, y0, z0, S.words);
+    if (op.l < op.L) {
+      for (int r = threadIdx.y; r < PL::NROWS; r += NWARP) {
+        int y = y0 + r % PL::TY, z = z0 + r / PL::TY;
+        bool ok = y < g.NY && z < g.NZ;
+        const double* src = c.Z + ((long long)z * g.NY + y) * g.NX + x0 + lane;
+        cpa8(S.zs + r * 32 + lane, ok ? src : c.Z, ok);
       }
     }
-    __syncthreads();
-  } else {
-    box_load<D, P>(c.Y[op.step & 1], g, x0, y0, z0, U);
   }
-  double* AB = R1;
-  double* CS = R1 + 2 * PL::NAB;
-  double* PU = R1 + (PL::PRO_REGION > PL::A_REGION ? PL::PRO_REGION : PL::A_REGION);
-  if (op.last) tile_pu<D, P>(c, op.l, x0, y0, z0, R1, PU);
-  a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
-  const int lane = threadIdx.x;
-  for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
+  cpa_wait_sync();
+  if (op.step == 2) {
+    const double sc = pow2((op.l + 1) * (D - 2));
+    for (int i = threadIdx.y * 32 + lane; i < PL::NU; i += NT) {
+      int bx = i % PL::BX, r = i / PL::BX;
+      int gy = y0 - P + r % PL::BY, gz = (D == 3) ? z0 - P + r / PL::BY : 0, gx = x0 - P + bx;
+      bool ok = unk1(gx, g.n) && unk1(gy, g.n) && (D == 2 || unk1(gz, g.n));
+      int t = ((D == 3 ? (ok ? gz % P : 0) : 0) * P + (ok ? gy % P : 0)) * P + (ok ? gx % P : 0);
+      Yb[i] = ok ? c.cf.inv_theta * ((c.cf.invd[t] * sc) * Bb[i]) : 0.0;
+    }
+    __syncthreads();
+  }
+  if (op.last) tile_pu_compute<D, P>(c, op.l, x0, y0, z0, S.r1, S.pu);
+  double* AB = S.r1;
+  double* CS = S.r1 + 2 * PL::NAB;
+  a_stages<D, P>(g, x0, y0, c.cf, Yb, AB, CS);
+  for (int row = threadIdx.y; row < PL::NROWS; row += NWARP) {
     int ty = row % PL::TY, tz = row / PL::TY;
     int y = y0 + ty, z = z0 + tz, x = x0 + lane;
     if (y >= g.NY || z >= g.NZ) continue;
@@ -863,14 +949,16 @@ __device__ void tile_cheb(const DevCtx& c, const Op& op, const TileIdx& tile, do
     bool unk = unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(z, g.n));
     long long idx = ((long long)z * g.NY + y) * g.NX + x;
     double invD = unk ? inv_diag(c.cf, D, P, op.l, x, y, z) : 0.0;
-    double b = c.B[idx];
+    const int ci = ((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane;
+    double b = (op.step == 2) ? Bb[ci] : c.B[idx];
     double q = b - ay;
-    double yprev = U[((tz + ((D == 3) ? P : 0)) * PL::BY + ty + P) * PL::BX + P + lane];
+    double yprev = Yb[ci];
     double dprev = (op.step == 2) ? yprev : c.Dv[idx];
     double d = fma(c.cf.cal[op.step - 1], dprev, c.cf.cbe[op.step - 1] * (invD * q));
     double yv = yprev + d;
     if (op.last) {
-      cfas_finalize(c, op, lv, idx, yv, PU[row * 32 + lane]);
+      cfas_finalize(c, op, lv, idx, yv, S.pu[row * 32 + lane], (op.l < op.L) ? S.zs[row * 32 + lane] : 0.0,
+                    S.words + row * lv.ustride);
     } else {
       c.Y[(op.step + 1) & 1][idx] = yv;
       c.Dv[idx] = d;
@@ -893,7 +981,10 @@ __device__ __forceinline__ void run_op(const DevCtx& c, const Op& op, const Tile
 // Grid kernel: one CTA per tile of one operation.  The device context lives in
 // global memory and is read through the read-only path (uniform, L1-cached).
 template <int D, int P>
-__global__ void __launch_bounds__(NT) k_op(const DevCtx* __restrict__ cp, Op op) {
+#ifndef FMG_KOP_MINB
+#define FMG_KOP_MINB 4
+#endif
+__global__ void __launch_bounds__(NT, FMG_KOP_MINB) k_op(const DevCtx* __restrict__ cp, Op op) {
   extern __shared__ double sm[];
   pdl_wait();
   pdl_trigger();
