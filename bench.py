@@ -91,6 +91,24 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
+def reduce_max(value: float, device=None) -> float:
+    """Max of a per-rank scalar over all ranks (timings are max-over-ranks);
+    identity without an initialised process group."""
+    import torch
+    import torch.distributed as tdist
+    if not (tdist.is_available() and tdist.is_initialized()) or tdist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate(unknowns_per_rank: int, world: int, ms_max: float) -> float:
+    """Whole-job DoF/s: every rank solves its own replica (2D configs do not
+    shard), timed by the slowest rank."""
+    return unknowns_per_rank * world / (ms_max * 1e-3)
+
+
 def kernel_model(cfg, sched, cls):
     """Algorithmic FP64 flops and HBM bytes per launch of a fine-level kernel
     (DESIGN.md §7), counted per stored point of the finest level from what the
@@ -162,11 +180,7 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         tdist.barrier()
     ck = clocks.stop()
-    ms = sum(times) / len(times)
-    if dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = reduce_max(sum(times) / len(times), dev)
 
     # ---- end to end through the C-ABI with host buffers --------------------
     rhs_host = torch.from_numpy(solver.get_rhs()).pin_memory()
@@ -181,11 +195,7 @@ def run_ours(args, rank, world, local_rank):
         solver.export_solution(exp_host)    # D2H: every compact solution section
         stream.synchronize()
         e2e_times.append((time.perf_counter() - t0) * 1e3)
-    e2e_ms = sum(e2e_times) / len(e2e_times)
-    if dist:
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = reduce_max(sum(e2e_times) / len(e2e_times), dev)
 
     if rank != 0:
         return
@@ -211,7 +221,7 @@ def run_ours(args, rank, world, local_rank):
     eff_gbs = info["alg_bytes_per_solve"] / (ms * 1e-3) / 1e9
     out = {
         "metric": METRIC,
-        "value": info_unk * world / (ms * 1e-3),
+        "value": aggregate(info_unk, world, ms),
         "unit": "DoF/s",
         "n_gpus": world,
         "steps": args.steps,
@@ -231,7 +241,7 @@ def run_ours(args, rank, world, local_rank):
         "hbm_roofline_frac_measured": eff_gbs / hbm,
         "alg_bytes_per_solve": info["alg_bytes_per_solve"],
         "roofline": roof,
-        "e2e": {"value": info_unk * world / (e2e_ms * 1e-3), "unit": "DoF/s",
+        "e2e": {"value": aggregate(info_unk, world, e2e_ms), "unit": "DoF/s",
                 "h2d_bytes_per_step": rhs_host.numel() * 8, "d2h_bytes_per_step": exp_host.numel(),
                 "ms_per_step": e2e_ms},
         "gpu_launches": int(info["launches_per_solve"]) * args.steps,
