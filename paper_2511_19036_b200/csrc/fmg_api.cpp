@@ -280,6 +280,13 @@ int prepare(fmg_ctx* c, const Builder& b, int slot) {
 
 // Issue every item on c->cur (inside a capture or directly), then the deferred norms.
 void issue(fmg_ctx* c, const Builder& b) {
+  // FMG_SYNC_DEBUG=1 (direct runs only): synchronise after every launch and
+  // report the first failing item.
+  const bool dbg = c->cur == c->st && getenv("FMG_SYNC_DEBUG") != nullptr;
+  if (dbg) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[fmg] pending CUDA error before issue: %s\n", cudaGetErrorString(e));
+  }
   for (const Item& it : b.items) {
     if (it.kind == 1) {
       mark(c, -2);
@@ -297,6 +304,15 @@ void issue(fmg_ctx* c, const Builder& b) {
       mark(c, it.timed_cls);
     }
     c->launches++;
+    if (dbg) {
+      cudaError_t e = cudaStreamSynchronize(c->cur);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        fprintf(stderr, "[fmg] CUDA error in item kind=%d type=%d l=%d L=%d: %s\n", it.kind, it.op.type, it.op.l,
+                it.kind ? it.k4.L : it.op.L, cudaGetErrorString(e));
+        return;
+      }
+    }
   }
   launch_norms_all(c->cur, c->devctx, c->nent[c->nent_slot], (int)b.norms.size());
   c->launches++;
@@ -385,6 +401,10 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   c->afn = g_alloc; c->ffn = g_free; c->auser = g_alloc_user;
   if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) { delete c; return FMG_ECUDA; }
   set_kernel_attributes();
+  if (getenv("FMG_SYNC_DEBUG")) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[fmg] set_kernel_attributes: %s\n", cudaGetErrorString(e));
+  }
   build_coefs(dim, p, s->lambda_hi, s->alpha, s->cheb_degree, &c->cf);
   int TY, TZ;
   tile_shape(dim, p, &TY, &TZ);
@@ -406,8 +426,12 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     return b;
   };
   c->lc = 0;
-  for (int l = 0; l <= lc_cap; ++l)
-    if (k4_bytes(l) <= 210 * 1024) c->lc = l;
+  // (k4_bytes grows monotonically with lc; stop at the first level that does not fit,
+  // before any 32-bit size arithmetic can overflow)
+  for (int l = 0; l <= lc_cap; ++l) {
+    if (k4_bytes(l) > 210 * 1024) break;
+    c->lc = l;
+  }
   c->k4_smem = (int)k4_bytes(c->lc);
   int rc = FMG_OK;
   long long tot_parts = 0;
@@ -506,6 +530,10 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     }
   }
   if (rc == FMG_OK) rc = cuda_err(cudaDeviceSynchronize());
+  if (getenv("FMG_SYNC_DEBUG")) {
+    cudaError_t e = cudaGetLastError();
+    fprintf(stderr, "[fmg] create: rc=%d last=%s lc=%d k4_smem=%d\n", rc, cudaGetErrorString(e), c->lc, c->k4_smem);
+  }
   if (rc != FMG_OK) {
     fmg_destroy(c);
     return rc;
