@@ -57,9 +57,13 @@ struct fmg_ctx {
   cudaGraphExec_t graph = nullptr;
   int solved_L = -1;
   int wu_cur[kMaxLev]{};
-  int lc = 0;                     // levels 0..lc run inside K4 (shared memory)
-  int k4_smem = 0;
-  double* usm = nullptr;
+  int lc = 0;                     // levels 0..lc run inside the cluster kernel KC
+  int kc_cluster = 1;             // CTAs of the KC cluster
+  KcLayout kcl{};                 // KC shared-memory layout
+  int kc_tw = 16;                 // KC warps (cluster x warps per CTA): norm partials per level
+  double* Ul[kMaxLev]{};          // per-level u_l, t_l, w_l (padded level layout)
+  double* Tl[kMaxLev]{};
+  double* Wl[kMaxLev]{};
   fmg_alloc_fn afn = nullptr;
   fmg_free_fn ffn = nullptr;
   void* auser = nullptr;
@@ -100,12 +104,12 @@ Launch L_(fmg_ctx* c) { return Launch{c->dim, c->p, c->cur}; }
 
 // ---------------------------------------------------------------- schedule --
 // A solve is a list of items: a grid launch of one tile op over all tiles of its
-// level, or one launch of the shared-memory coarse-hierarchy kernel K4
-// (levels 0..lc).  DESIGN.md §4.
+// level, or one launch of the coarse-hierarchy cluster kernel KC (levels
+// 0..lc).  DESIGN.md §4.
 struct Item {
-  int kind;          // 0 grid op, 1 K4
+  int kind;          // 0 grid op, 1 KC
   OpDesc op;         // grid item
-  K4Desc k4;         // K4 item
+  KcDesc kc;         // KC item
   int timed_cls;     // kernel-timing class of a grid item (-1: none)
 };
 
@@ -113,7 +117,7 @@ struct Builder {
   fmg_ctx* c;
   std::vector<Item> items;
   std::vector<NormEntry> norms;
-  long long ptot = 0;
+  long long ptot = 0;  // (set past the KC partial region by make_builder)
   // reserve partial slots for (row, level l) and record the deferred norm
   long long slot(int row, int l) {
     int nt = c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2];
@@ -130,14 +134,36 @@ struct Builder {
     it.timed_cls = cls;
     items.push_back(it);
   }
-  void k4(const K4Desc& d) {
+  void kc(const KcDesc& d) {
     Item it{};
     it.kind = 1;
-    it.k4 = d;
+    it.kc = d;
     it.timed_cls = -1;
     items.push_back(it);
   }
+  // deferred norm of level l <= lc computed by KC: one partial per KC warp in
+  // the KC region at the start of the partial buffer (fmg_kc.cu norm_partial)
+  void kc_norm(int row, int l) {
+    NormEntry e{((long long)row * c->levels + l) * c->kc_tw, row, l, c->kc_tw, 0};
+    norms.push_back(e);
+  }
 };
+
+Builder make_builder(fmg_ctx* c) {
+  Builder b{c, {}, {}, 0};
+  b.ptot = (long long)c->levels * c->s.n_ir * c->levels * c->kc_tw;
+  return b;
+}
+
+KcDesc mkkc(fmg_ctx* c, int mode) {
+  KcDesc d{};
+  d.mode = mode;
+  d.b_u = c->s.b_u;
+  d.k_u = c->s.k_u;
+  d.b_r = c->s.b_r;
+  d.k_r = c->s.k_r;
+  return d;
+}
 
 OpDesc mkop(int type, int l, int L) {
   OpDesc o{};
@@ -171,7 +197,7 @@ void build_residual_grid(Builder& b, int L, int row) {
 }
 
 // One IR iteration at FMG level L: fmgResidual (Alg 3.2),
-// cFas V(0,1) (Alg 3.1, nu = 1), correction.  Levels <= lc run inside K4.
+// cFas V(0,1) (Alg 3.1, nu = 1), correction.  Levels <= lc run inside KC.
 void build_iteration(Builder& b, int L, int it) {
   fmg_ctx* c = b.c;
   const int lc = c->lc;
@@ -191,19 +217,17 @@ void build_iteration(Builder& b, int L, int it) {
       b.grid(q, (fine && l == L - 1) ? 3 : -1);
     }
   }
-  K4Desc d{};
-  d.mode = 1;
+  // levels 0..lc: KC (restriction tail, coarse solve, cFas + correction)
+  KcDesc d = mkkc(c, 1);
   d.L = L;
-  d.first = it == 0;
-  d.row = L * c->s.n_ir + it;
-  int top = L < lc ? L : lc;
-  for (int l = 0; l <= top; ++l) {
-    d.wr[l] = wr(c, l, L);
-    d.wu_in[l] = c->wu_cur[l];
-    d.wu_out[l] = wu(c, l, L);
+  d.it = it;
+  d.row0 = row;
+  d.nrows = 1;
+  b.kc(d);
+  for (int l = 0; l <= lc; ++l) {
+    b.kc_norm(row, l);
     c->wu_cur[l] = wu(c, l, L);
   }
-  b.k4(d);
   const int k = c->s.cheb_degree;
   for (int l = lc + 1; l <= L; ++l) {
     for (int step = 1; step <= k; ++step) {
@@ -219,24 +243,37 @@ void build_iteration(Builder& b, int L, int it) {
   }
 }
 
-// Alg 3.3 up to FMG level Lstop (iters_last IR iterations there).
+// Alg 3.3 up to FMG level Lstop (iters_last IR iterations there).  One KC
+// launch runs the coarse-grid solve and every FMG level L <= lc in full.
 void build_solve(Builder& b, int Lstop, int iters_last) {
   fmg_ctx* c = b.c;
+  const int lc = c->lc;
   for (int l = 0; l <= c->Lmax; ++l) c->wu_cur[l] = wu(c, l, l);
-  K4Desc d{};
-  d.mode = 0;
-  d.wu_out[0] = wu(c, 0, 0);
-  b.k4(d);  // coarse-grid solve PAPER.md:786
+  KcDesc d = mkkc(c, 0);
+  d.Llast = std::min(Lstop, lc);
+  d.iters_last = (Lstop <= lc) ? iters_last : c->s.n_ir;
+  d.row0 = c->s.n_ir;  // (L = 1, it = 0)
+  d.nrows = d.Llast >= 1 ? (d.Llast - 1) * c->s.n_ir + d.iters_last : 0;
+  b.kc(d);  // coarse-grid solve PAPER.md:786, FMG levels 1..min(Lstop, lc)
   c->wu_cur[0] = wu(c, 0, 0);
-  for (int L = 1; L <= Lstop; ++L) {
+  for (int L = 1; L <= d.Llast; ++L) {
+    c->wu_cur[L] = wu(c, L, L);
+    int iters = (L == d.Llast) ? d.iters_last : c->s.n_ir;
+    for (int it = 0; it < iters; ++it) {
+      for (int l = 0; l <= L; ++l) {
+        b.kc_norm(L * c->s.n_ir + it, l);
+        c->wu_cur[l] = wu(c, l, L);
+      }
+    }
+  }
+  for (int L = lc + 1; L <= Lstop; ++L) {
     // push level PAPER.md:788: ú_L = 0 (zeroed at solve start); the widening of
     // ú_{0..L-1} is value-preserving and happens at the next encode.
     c->wu_cur[L] = wu(c, L, L);
-    if (L > c->lc) {  // u_L = dec ú_L + P u_{L-1} = P u_{L-1} for the first residual
-      OpDesc o = mkop(OP_DECODE, L, L);
-      o.wu_in = c->wu_cur[L];
-      b.grid(o, (L == c->Lmax) ? 2 : -1);
-    }
+    // u_L = dec ú_L + P u_{L-1} = P u_{L-1} for the first residual
+    OpDesc o = mkop(OP_DECODE, L, L);
+    o.wu_in = c->wu_cur[L];
+    b.grid(o, (L == c->Lmax) ? 2 : -1);
     int iters = (L == Lstop) ? iters_last : c->s.n_ir;
     for (int it = 0; it < iters; ++it) build_iteration(b, L, it);
   }
@@ -290,7 +327,7 @@ void issue(fmg_ctx* c, const Builder& b) {
   for (const Item& it : b.items) {
     if (it.kind == 1) {
       mark(c, -2);
-      launch_k4(c->dim, c->p, c->cur, c->devctx, it.k4, c->k4_smem);
+      launch_kc(c->dim, c->p, c->cur, c->devctx, it.kc, c->kc_cluster, c->kcl.bytes);
       mark(c, -2);
     } else {
       mark(c, it.timed_cls);
@@ -309,7 +346,7 @@ void issue(fmg_ctx* c, const Builder& b) {
       if (e == cudaSuccess) e = cudaGetLastError();
       if (e != cudaSuccess) {
         fprintf(stderr, "[fmg] CUDA error in item kind=%d type=%d l=%d L=%d: %s\n", it.kind, it.op.type, it.op.l,
-                it.kind ? it.k4.L : it.op.L, cudaGetErrorString(e));
+                it.kind ? it.kc.L : it.op.L, cudaGetErrorString(e));
         return;
       }
     }
@@ -365,16 +402,20 @@ int run_direct(fmg_ctx* c, Builder& b) {
 }  // namespace
 
 namespace fmg {
-void k4_debug(int on);
-void k4_stamps(unsigned long long* out);
+void kc_debug(int on);
+int kc_stamps(unsigned long long* out);
 }
 
 extern "C" {
 
-/* debug: K4 phase timestamps (ns) of the last K4 launch */
-int fmg_debug_k4(int on, unsigned long long* stamps64) {
-  if (stamps64) { cudaDeviceSynchronize(); fmg::k4_stamps(stamps64); }
-  else fmg::k4_debug(on);
+/* debug: phase timestamps (globaltimer ns, CTA 0 after every cluster barrier)
+ * of the last KC launch; returns the stamp count when `stamps` is non-null. */
+int fmg_debug_kc(int on, unsigned long long* stamps) {
+  if (stamps) {
+    cudaDeviceSynchronize();
+    return fmg::kc_stamps(stamps);
+  }
+  fmg::kc_debug(on);
   return 0;
 }
 
@@ -408,31 +449,6 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   build_coefs(dim, p, s->lambda_hi, s->alpha, s->cheb_degree, &c->cf);
   int TY, TZ;
   tile_shape(dim, p, &TY, &TZ);
-  // K4 owns the largest prefix of levels that fits its shared-memory budget
-  // (env FMG_LC caps it).
-  int lc_cap = Lmax;
-  if (const char* e = getenv("FMG_LC")) lc_cap = std::min(lc_cap, atoi(e));
-  // bytes K4 needs for levels 0..lc: dense level arrays + scratch + staged sections + A_0^{-1}
-  auto k4_bytes = [&](int lc) {
-    long long b = k4_smem_bytes(dim, p, lc);
-    for (int l = 0; l <= lc; ++l) {
-      int n = p << (l + 1), NX = ((n + 31) / 32) * 32;
-      long long nblk = (long long)NX * n * (dim == 3 ? n : 1) / 32;
-      b += nblk * 4 * (wu(c, l, Lmax) + wr(c, l, Lmax)) + 2 * nblk;
-    }
-    b = (b + 15) / 16 * 16;
-    int n0 = coarse_count(dim, p);
-    if (k4_ainv_staged(n0)) b += 8LL * n0 * n0;
-    return b;
-  };
-  c->lc = 0;
-  // (k4_bytes grows monotonically with lc; stop at the first level that does not fit,
-  // before any 32-bit size arithmetic can overflow)
-  for (int l = 0; l <= lc_cap; ++l) {
-    if (k4_bytes(l) > 210 * 1024) break;
-    c->lc = l;
-  }
-  c->k4_smem = (int)k4_bytes(c->lc);
   int rc = FMG_OK;
   long long tot_parts = 0;
   DevCtxDesc dd{};
@@ -463,14 +479,42 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     c->part_off[l] = tot_parts;
     tot_parts += nt;
   }
-  // FP64 workspace (finest size): U ping-pong, W ping-pong, T ping-pong / Z, B;
-  // Y ping-pong + D (k >= 3)
-  int nbuf = s->cheb_degree >= 3 ? 9 : 6;
+  // KC (one thread-block cluster, fmg_kc.cu) owns levels 0..lc: the largest
+  // prefix with <= 2 BFP blocks per KC warp whose data fits the cluster's
+  // distributed shared memory (env FMG_LC caps lc, FMG_KC_CLUSTER forces NC).
   if (rc == FMG_OK) {
-    for (int i = 0; i < nbuf && rc == FMG_OK; ++i) {
-      c->buf[i] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
-      if (!c->buf[i]) rc = FMG_ENOMEM;
+    int lc_cap = Lmax;
+    if (const char* e = getenv("FMG_LC")) lc_cap = std::min(lc_cap, atoi(e));
+    int ust[kMaxLev], rst[kMaxLev];
+    for (int l = 0; l <= Lmax; ++l) {
+      ust[l] = c->u[l].stride;
+      rst[l] = c->r[l].stride;
     }
+    if (kc_plan(dim, p, Lmax, c->g, ust, rst, s->n_ir, lc_cap, &c->kcl, &c->lc, &c->kc_cluster)) rc = FMG_ECUDA;
+    c->kc_tw = c->kc_cluster * kc_warps_per_cta();
+  }
+  // FP64 workspace: per-level u_l, t_l, w_l; finest-size Z, B, Y[2], Dv, PU;
+  // KC scratch of twice the level-lc size (3D restriction staging).
+  for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
+    size_t bytes = sizeof(double) * c->g[l].size;
+    c->Ul[l] = (double*)dalloc(c, bytes);
+    c->Tl[l] = (double*)dalloc(c, bytes);
+    c->Wl[l] = (double*)dalloc(c, bytes);
+    if (!c->Ul[l] || !c->Tl[l] || !c->Wl[l]) rc = FMG_ENOMEM;
+    else {
+      cudaMemset(c->Ul[l], 0, bytes);
+      cudaMemset(c->Tl[l], 0, bytes);
+      cudaMemset(c->Wl[l], 0, bytes);
+    }
+  }
+  for (int i = 0; i < 6 && rc == FMG_OK; ++i) {
+    c->buf[i] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
+    if (!c->buf[i]) rc = FMG_ENOMEM;
+    else cudaMemset(c->buf[i], 0, sizeof(double) * c->g[Lmax].size);
+  }
+  for (int i = 6; i < 8 && rc == FMG_OK; ++i) {
+    c->buf[i] = (double*)dalloc(c, sizeof(double) * 2 * c->g[c->lc].size);
+    if (!c->buf[i]) rc = FMG_ENOMEM;
   }
   if (rc == FMG_OK) {
     c->n0 = coarse_count(dim, p);
@@ -485,13 +529,7 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     if (counters) cudaMemset(counters, 0, sizeof(int) * kMaxLev);
     dd.count = counters;
     c->devctx = dalloc(c, devctx_size());
-    long long usm_n = 0;
-    for (int l = 0; l <= c->lc; ++l) {
-      dd.usm_off[l] = usm_n;
-      usm_n += (long long)std::pow((double)(p << (l + 1)), dim);
-    }
-    c->usm = (double*)dalloc(c, sizeof(double) * usm_n);
-    if (!c->Ainv || !c->partials || !c->norms_dev || !c->err_part || !c->status || !c->devctx || !c->usm)
+    if (!c->Ainv || !c->partials || !c->norms_dev || !c->err_part || !c->status || !c->devctx)
       rc = FMG_ENOMEM;
     else {
       cudaMemcpy(c->Ainv, Ai.data(), sizeof(double) * Ai.size(), cudaMemcpyHostToDevice);
@@ -507,17 +545,19 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
         dd.gtab[l] = c->gtab[l];
         for (int k = 0; k < 3; ++k) dd.tiles[l][k] = c->tiles[l][k];
         dd.part[l] = c->partials + c->part_off[l];
+        dd.Ul[l] = c->Ul[l];
+        dd.Tl[l] = c->Tl[l];
+        dd.Wl[l] = c->Wl[l];
       }
-      dd.U[0] = c->buf[0];
-      dd.U[1] = c->buf[1];
-      dd.W[0] = c->buf[2];
-      dd.W[1] = c->buf[3];
-      dd.T[0] = dd.Z = c->buf[4];
-      dd.T[1] = dd.B = c->buf[5];
-      dd.Y[0] = c->buf[6];
-      dd.Y[1] = c->buf[7];
-      dd.Dv = c->buf[8];
-      dd.usm = c->usm;
+      dd.Z = c->buf[0];
+      dd.B = c->buf[1];
+      dd.Y[0] = c->buf[2];
+      dd.Y[1] = c->buf[3];
+      dd.Dv = c->buf[4];
+      dd.PU = c->buf[5];
+      dd.KS[0] = c->buf[6];
+      dd.KS[1] = c->buf[7];
+      dd.kc = c->kcl;
       dd.lc = c->lc;
       dd.n_cheb = s->cheb_degree;
       dd.Ainv = c->Ainv;
@@ -532,7 +572,8 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   if (rc == FMG_OK) rc = cuda_err(cudaDeviceSynchronize());
   if (getenv("FMG_SYNC_DEBUG")) {
     cudaError_t e = cudaGetLastError();
-    fprintf(stderr, "[fmg] create: rc=%d last=%s lc=%d k4_smem=%d\n", rc, cudaGetErrorString(e), c->lc, c->k4_smem);
+    fprintf(stderr, "[fmg] create: rc=%d last=%s lc=%d kc_cluster=%d\n", rc, cudaGetErrorString(e), c->lc,
+            c->kc_cluster);
   }
   if (rc != FMG_OK) {
     fmg_destroy(c);
@@ -545,7 +586,7 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
 int fmg_solve_async(fmg_ctx* c) {
   if (!c) return FMG_EINVAL;
   if (!c->graph) {
-    Builder b{c, {}};
+    Builder b = make_builder(c);
     c->launches = 0;
     c->ev_used = 0;
     build_solve(b, c->Lmax, c->s.n_ir);
@@ -577,7 +618,7 @@ int fmg_solve(fmg_ctx* c) {
 
 int fmg_solve_upto(fmg_ctx* c, int Lstop, int iters_last) {
   if (!c || Lstop < 0 || Lstop > c->Lmax || iters_last < 0) return FMG_EINVAL;
-  Builder b{c, {}};
+  Builder b = make_builder(c);
   c->cur = c->st;
   cudaStreamSynchronize(c->st);
   zero_sections(c);
@@ -604,7 +645,7 @@ int fmg_residual(fmg_ctx* c, double* host_norms) {
   double* row = c->norms_dev + ((size_t)L * c->s.n_ir) * c->levels;
   cudaStreamSynchronize(c->st);
   cudaMemcpy(keep.data(), row, sizeof(double) * c->levels, cudaMemcpyDeviceToHost);
-  Builder b{c, {}};
+  Builder b = make_builder(c);
   build_residual_grid(b, L, L * c->s.n_ir);
   int rc = run_direct(c, b);
   if (rc) return rc;
@@ -617,16 +658,16 @@ int fmg_residual(fmg_ctx* c, double* host_norms) {
   return FMG_OK;
 }
 
-// û_L into U[L & 1] (decode ops for l = 0..L, materialised).
+// û_L into the level-L u array (decode ops for l = 0..L, materialised).
 static int decode_solution(fmg_ctx* c, int* which) {
   int L = c->solved_L;
-  Builder b{c, {}};
+  Builder b = make_builder(c);
   for (int l = 0; l <= L; ++l) {
     OpDesc o = mkop(OP_DECODE, l, L);
     o.wu_in = c->wu_cur[l];
     b.grid(o);
   }
-  *which = L & 1;
+  *which = L;
   return run_direct(c, b);
 }
 
@@ -636,7 +677,7 @@ int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
   int which = 0;
   int rc = decode_solution(c, &which);
   if (rc) return rc;
-  cudaMemcpyAsync(dst_dev, c->buf[which], sizeof(double) * c->g[c->solved_L].size, cudaMemcpyDeviceToDevice,
+  cudaMemcpyAsync(dst_dev, c->Ul[which], sizeof(double) * c->g[c->solved_L].size, cudaMemcpyDeviceToDevice,
                   c->st);
   return sync_check(c);
 }
@@ -649,7 +690,7 @@ int fmg_errors(fmg_ctx* c, double* err3) {
   if (rc) return rc;
   int np = 0;
   c->cur = c->st;
-  launch_errors(L_(c), c->buf[which], c->g[c->solved_L], c->err_part, &np);
+  launch_errors(L_(c), c->Ul[which], c->g[c->solved_L], c->err_part, &np);
   rc = sync_check(c);
   if (rc) return rc;
   std::vector<double> h(2 * np);

@@ -1,0 +1,211 @@
+// fmg_device.cuh -- device-side helpers shared by the sm_100a kernels of the
+// compact-FMG hot path (fmg_kernels.cu: grid tile ops; fmg_kc.cu: the cluster
+// kernel of the coarse levels): BFP codec (RNE PAPER.md:846),
+// cp.async / PDL helpers and the device context.  Product path only.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "fmg_internal.h"
+
+namespace fmg {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NWARP = 8;
+constexpr int NT = 32 * NWARP;
+
+__device__ __forceinline__ double pow2(int k) {  // exact 2^k, k in [-1022, 1023]
+  return __longlong_as_double((long long)(k + 1023) << 52);
+}
+__device__ __forceinline__ bool unk1(int i, int n) { return i >= 1 && i <= n - 1; }
+__device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// cp.async (LDGSTS) helpers: every global load of a tile is issued up front and
+// awaited once; out-of-range elements are zero-filled (src-size 0).
+__device__ __forceinline__ void cpa8(double* dst, const double* src, bool ok) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa4(uint32_t* dst, const uint32_t* src) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_wait_sync() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+}
+
+// ----------------------------------------------------------------- codec --
+// Exact int -> double for |m| < 2^31 by the 1.5*2^52 magic constant (an FP64
+// add instead of an I2F conversion); wider mantissas use the conversion.
+__device__ __forceinline__ double i2d(long long m, int w) {
+  if (w <= 32) return __longlong_as_double(0x4338000000000000LL + m) - 6755399441055744.0;
+  return (double)m;
+}
+// RNE of x to an integer for |x| < 2^31 (x + 1.5*2^52 rounds to nearest even at
+// integer granularity; the low word is the two's-complement result).
+__device__ __forceinline__ long long rne_int(double x, int w) {
+  if (w <= 32) return (long long)(int)__double2loint(x + 6755399441055744.0);
+  return (long long)rint(x);
+}
+
+// Warp-cooperative decode: lane j returns entry j of the block whose w words
+// start at `words`.  All 32 lanes must call.
+__device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int w, int lane) {
+  uint32_t my0 = lane < w ? words[lane] : 0u;
+  uint32_t my1 = 0u;
+  if (w > 32) my1 = lane + 32 < w ? words[lane + 32] : 0u;
+  int o = lane * w, j0 = o >> 5, s = o & 31;
+  uint32_t w0, w1, w2;
+  if (w <= 32) {
+    w0 = __shfl_sync(FULL, my0, j0 & 31);
+    w1 = __shfl_sync(FULL, my0, (j0 + 1) & 31);
+    w2 = __shfl_sync(FULL, my0, (j0 + 2) & 31);
+  } else {
+    uint32_t a0 = __shfl_sync(FULL, my0, j0 & 31), b0 = __shfl_sync(FULL, my1, j0 & 31);
+    uint32_t a1 = __shfl_sync(FULL, my0, (j0 + 1) & 31), b1 = __shfl_sync(FULL, my1, (j0 + 1) & 31);
+    uint32_t a2 = __shfl_sync(FULL, my0, (j0 + 2) & 31), b2 = __shfl_sync(FULL, my1, (j0 + 2) & 31);
+    w0 = j0 < 32 ? a0 : b0;
+    w1 = j0 + 1 < 32 ? a1 : b1;
+    w2 = j0 + 2 < 32 ? a2 : b2;
+  }
+  unsigned long long lo = (unsigned long long)w0 | ((unsigned long long)w1 << 32);
+  unsigned long long field = lo >> s;
+  if (s + w > 64) field |= (unsigned long long)w2 << (64 - s);
+  long long m = (long long)(field << (64 - w)) >> (64 - w);
+  return i2d(m, w) * pow2(E - (w - 1));
+}
+
+// Single-entry decode (entry j of a block), for halo points.
+__device__ __forceinline__ double point_decode(const uint32_t* words, int E, int w, int j) {
+  int o = j * w, j0 = o >> 5, s = o & 31;
+  int jl = (o + w - 1) >> 5;
+  unsigned long long lo = words[j0];
+  if (jl > j0) lo |= (unsigned long long)words[j0 + 1] << 32;
+  unsigned long long field = lo >> s;
+  if (jl > j0 + 1) field |= (unsigned long long)words[j0 + 2] << (64 - s);
+  long long m = (long long)(field << (64 - w)) >> (64 - w);
+  return i2d(m, w) * pow2(E - (w - 1));
+}
+
+// Warp-cooperative encode of one block; lane j holds entry j.
+// Writes the w words and the exponent when `words` is non-null; returns the
+// quantised value m 2^(E-q).  Non-finite input or E > 127 sets *status.
+__device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, int8_t* eptr, int lane,
+                                              int* status) {
+  unsigned long long bits = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
+  bool bad = bits >= 0x7ff0000000000000ULL;
+  unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+  unsigned mh = __reduce_max_sync(FULL, hi);
+  unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
+  bool err = __any_sync(FULL, bad);
+  double mx = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+  int q = w - 1, E = -128;
+  if (!err && mx != 0.0) {
+    int ebits = (int)((mh >> 20) & 0x7FFu);
+    int E0 = ebits == 0 ? -1100 : ebits - 1022;  // ilogb(mx) + 1; subnormal max -> saturates below
+    if (E0 > 127) {
+      err = true;
+    } else if (E0 < -127) {
+      E = -127;
+    } else {
+      E = E0;
+      if (rint(mx * pow2(q - E0)) == pow2(q)) E = E0 + 1;
+      if (E > 127) err = true;
+    }
+  }
+  long long m = 0;
+  if (err) {
+    E = -128;
+    if (lane == 0 && status) atomicOr(status, 1);
+  } else if (E != -128) {
+    m = rne_int(v * pow2(q - E), w);
+  }
+  if (words) {
+    const unsigned long long field = (unsigned long long)m & ((1ULL << w) - 1ULL);
+    uint32_t mine0 = 0u, mine1 = 0u;
+    if (w <= 8) {
+      // narrow: entry `lane` occupies stream bits [lane w, lane w + w) = (low, high)
+      // parts of words j0, j0 + 1; one redux.or per output word
+      const int p = lane * w, j0 = p >> 5;
+      const unsigned long long cf = field << (p & 31);
+      const uint32_t c0 = (uint32_t)cf, c1 = (uint32_t)(cf >> 32);
+#pragma unroll 1
+      for (int j = 0; j < w; ++j) {
+        uint32_t word = __reduce_or_sync(FULL, j == j0 ? c0 : (j == j0 + 1 ? c1 : 0u));
+        mine0 = lane == j ? word : mine0;
+      }
+    } else {
+      // wide: word j gathers its <= ceil(32/w)+1 entries by shuffles
+      const int K = (32 + w - 1) / w + 1;
+      const uint32_t flo = (uint32_t)field, fhi = (uint32_t)(field >> 32);
+#pragma unroll 1
+      for (int half = 0; half < (w > 32 ? 2 : 1); ++half) {
+        const int j = lane + 32 * half;
+        const int e0 = (32 * j) / w;
+        uint32_t acc = 0u;
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) {
+          const int e = e0 + k;
+          const int src = e < 32 ? e : 31;
+          const uint32_t lo_ = __shfl_sync(FULL, flo, src), hi_ = __shfl_sync(FULL, fhi, src);
+          const unsigned long long f = ((unsigned long long)hi_ << 32) | lo_;
+          const int sh = e * w - 32 * j;
+          if (e < 32 && sh < 32 && sh > -w) acc |= sh >= 0 ? (uint32_t)(f << sh) : (uint32_t)(f >> (-sh));
+        }
+        if (half == 0) mine0 = acc; else mine1 = acc;
+      }
+    }
+    if (lane < w) words[lane] = mine0;
+    if (lane + 32 < w) words[lane + 32] = mine1;
+    if (lane == 0) *eptr = (int8_t)E;
+  }
+  return E == -128 ? 0.0 : i2d(m, w) * pow2(E - q);
+}
+
+// ------------------------------------------------------------- contexts --
+// Device-side context (lives in global memory, built by fmg_api.cpp).
+struct LevelDev {
+  Geom g;
+  uint32_t* umant;
+  int8_t* uexp;
+  int ustride;
+  uint32_t* rmant;
+  int8_t* rexp;
+  int rstride;
+  const double* gtab;
+  int tx, ty, tz;  // tile grid of this level
+  double* part;    // norm partials, one per tile
+  int* count;      // arrival counter for the last-CTA norm reduction
+  double* U;       // decoded u_l = dec ú_l + P_l u_{l-1} (padded level layout)
+  double* T;       // residual temporary t_l
+  double* W;       // w_l = z_l + dec ý_l
+};
+
+struct __align__(16) DevCtx {
+  LevelDev lv[kMaxLev];
+  double* pbase; // norm partials of the grid levels (one slot per FMG level, iteration, level)
+  int lc;        // the cluster kernel (fmg_kc.cu) handles levels 0..lc
+  int n_cheb;    // Chebyshev degree k
+  double* Z;     // z_l (only for l < L)
+  double* B;     // b_l = dec r_l - A z_l
+  double* Y[2];  // Chebyshev iterates (k >= 3)
+  double* Dv;    // Chebyshev direction (k >= 3)
+  double* PU;    // P_l u_{l-1} (cluster kernel)
+  double* KS[2]; // (unused)
+  KcLayout kc;   // cluster-kernel shared-memory layout
+  const double* Ainv;
+  int n0;
+  double* norms;
+  int levels, n_ir;
+  int* status;
+  Coefs cf;
+};
+
+
+}  // namespace fmg

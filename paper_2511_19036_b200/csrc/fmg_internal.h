@@ -59,13 +59,30 @@ struct NormEntry {
   int row, l, count, pad;
 };
 
-// K4 (shared-memory coarse hierarchy kernel) launch descriptor.
-struct K4Desc {
-  int mode;   // 0: coarse-grid solve; 1: one IR iteration at FMG level L
-  int L;      // FMG level
-  int first;  // first IR iteration of FMG level L
-  int row;    // norm row
-  int wr[kMaxLev], wu_in[kMaxLev], wu_out[kMaxLev];
+// KC (coarse-hierarchy cluster kernel, fmg_kc.cu) launch descriptor.
+struct KcDesc {
+  int mode;        // 0: coarse-grid solve, then FMG levels 1..Llast (<= lc) in full
+                   // 1: the levels-0..lc part of IR iteration `it` at FMG level L > lc
+  int L, it;       // mode 1
+  int Llast;       // mode 0: last FMG level run inside (0: coarse solve only)
+  int iters_last;  // mode 0: IR iterations at FMG level Llast
+  int b_u, k_u, b_r, k_r;  // width law w_u = b_u + k_u (L - l), w_r = b_r + k_r (L - l)
+  int row0, nrows;         // norm rows (L n_ir + it) written by this launch
+  int debug;               // record phase timestamps (tools/kc_phases.py)
+};
+
+// KC distributed-shared-memory layout (same offsets in every CTA of the cluster):
+// per-level slabs of u_l, t_l, w_l; scratch slabs; section storage of the owned
+// blocks; the norm-partial table.  Double offsets unless noted.
+struct KcLayout {
+  int lg;  // log2(cluster size)
+  int bytes;
+  int U[kMaxLev], T[kMaxLev], W[kMaxLev];
+  int Z, B, Y0, Y1, Dv, PU, KS0, KS1, RQ0;
+  int part;
+  int um[kMaxLev], rm[kMaxLev];  // uint32 word offsets
+  int ue[kMaxLev], re[kMaxLev];  // byte offsets
+  int lgc[kMaxLev];              // log2 of the blocks per CTA of each level
 };
 
 // Everything the device context needs.
@@ -78,13 +95,14 @@ struct DevCtxDesc {
   double* part[kMaxLev];
   int* count;  // kMaxLev arrival counters (zeroed)
   double* pbase;
-  double *U[2], *T[2], *W[2], *Y[2];
-  double *Z, *B, *Dv;
+  double *Ul[kMaxLev], *Tl[kMaxLev], *Wl[kMaxLev];  // per-level u_l, t_l, w_l
+  double *Y[2];
+  double *Z, *B, *Dv, *PU;
+  double *KS[2];   // (unused by the DSMEM KC; kept for layout compatibility)
+  KcLayout kc;
   const double* Ainv;
   double* norms;
   int* status;
-  double* usm;
-  long long usm_off[kMaxLev];
   int lc, n_cheb;
   Coefs cf;
 };
@@ -104,9 +122,10 @@ size_t op_size();
 void fill_devctx(void* host_buf, const DevCtxDesc& d);
 void pack_op(void* dst, const OpDesc& od);
 void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int tx, int ty, int tz);
-int k4_smem_bytes(int dim, int p, int lc);
-int k4_ainv_staged(int n0);
-void launch_k4(int dim, int p, cudaStream_t st, const void* devctx, const K4Desc& a, int smem);
+int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* rst, int n_ir, int lc_cap,
+            KcLayout* ly, int* lc_out, int* cs_out);
+int kc_warps_per_cta();
+void launch_kc(int dim, int p, cudaStream_t st, const void* devctx, const KcDesc& a, int cluster, int smem);
 void launch_norms_all(cudaStream_t st, const void* devctx, const NormEntry* entries_dev, int n);
 void launch_errors(const Launch& L, const double* U, const Geom& g, double* partials, int* nparts);
 void launch_bfp_encode(const double* x, long long n, int w, uint32_t* mant, int8_t* exps, int* status,

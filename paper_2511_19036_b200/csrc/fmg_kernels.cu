@@ -16,169 +16,9 @@
 // residual / truncate / restriction = fmgResidual (Alg 3.2);
 // coarse-to-fine sweep of cFas (Alg 3.1, nu = 1 so s = 0,
 // PAPER.md:809-812) fused with the correction (Alg 3.3).
-#include <cstdint>
-#include <cstdio>
-#include <cstring>
-
-#include "fmg_internal.h"
+#include "fmg_device.cuh"
 
 namespace fmg {
-
-constexpr unsigned FULL = 0xffffffffu;
-constexpr int NWARP = 8;
-constexpr int NT = 32 * NWARP;
-
-__device__ __forceinline__ double pow2(int k) {  // exact 2^k, k in [-1022, 1023]
-  return __longlong_as_double((long long)(k + 1023) << 52);
-}
-__device__ __forceinline__ bool unk1(int i, int n) { return i >= 1 && i <= n - 1; }
-__device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
-
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
-// cp.async (LDGSTS) helpers: every global load of a tile is issued up front and
-// awaited once; out-of-range elements are zero-filled (src-size 0).
-__device__ __forceinline__ void cpa8(double* dst, const double* src, bool ok) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(ok ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cpa4(uint32_t* dst, const uint32_t* src) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cpa_wait_sync() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
-}
-
-// ----------------------------------------------------------------- codec --
-// Exact int -> double for |m| < 2^31 by the 1.5*2^52 magic constant (an FP64
-// add instead of an I2F conversion); wider mantissas use the conversion.
-__device__ __forceinline__ double i2d(long long m, int w) {
-  if (w <= 32) return __longlong_as_double(0x4338000000000000LL + m) - 6755399441055744.0;
-  return (double)m;
-}
-// RNE of x to an integer for |x| < 2^31 (x + 1.5*2^52 rounds to nearest even at
-// integer granularity; the low word is the two's-complement result).
-__device__ __forceinline__ long long rne_int(double x, int w) {
-  if (w <= 32) return (long long)(int)__double2loint(x + 6755399441055744.0);
-  return (long long)rint(x);
-}
-
-// Warp-cooperative decode: lane j returns entry j of the block whose w words
-// start at `words`.  All 32 lanes must call.
-__device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int w, int lane) {
-  uint32_t my0 = lane < w ? words[lane] : 0u;
-  uint32_t my1 = 0u;
-  if (w > 32) my1 = lane + 32 < w ? words[lane + 32] : 0u;
-  int o = lane * w, j0 = o >> 5, s = o & 31;
-  uint32_t w0, w1, w2;
-  if (w <= 32) {
-    w0 = __shfl_sync(FULL, my0, j0 & 31);
-    w1 = __shfl_sync(FULL, my0, (j0 + 1) & 31);
-    w2 = __shfl_sync(FULL, my0, (j0 + 2) & 31);
-  } else {
-    uint32_t a0 = __shfl_sync(FULL, my0, j0 & 31), b0 = __shfl_sync(FULL, my1, j0 & 31);
-    uint32_t a1 = __shfl_sync(FULL, my0, (j0 + 1) & 31), b1 = __shfl_sync(FULL, my1, (j0 + 1) & 31);
-    uint32_t a2 = __shfl_sync(FULL, my0, (j0 + 2) & 31), b2 = __shfl_sync(FULL, my1, (j0 + 2) & 31);
-    w0 = j0 < 32 ? a0 : b0;
-    w1 = j0 + 1 < 32 ? a1 : b1;
-    w2 = j0 + 2 < 32 ? a2 : b2;
-  }
-  unsigned long long lo = (unsigned long long)w0 | ((unsigned long long)w1 << 32);
-  unsigned long long field = lo >> s;
-  if (s + w > 64) field |= (unsigned long long)w2 << (64 - s);
-  long long m = (long long)(field << (64 - w)) >> (64 - w);
-  return i2d(m, w) * pow2(E - (w - 1));
-}
-
-// Single-entry decode (entry j of a block), for halo points.
-__device__ __forceinline__ double point_decode(const uint32_t* words, int E, int w, int j) {
-  int o = j * w, j0 = o >> 5, s = o & 31;
-  int jl = (o + w - 1) >> 5;
-  unsigned long long lo = words[j0];
-  if (jl > j0) lo |= (unsigned long long)words[j0 + 1] << 32;
-  unsigned long long field = lo >> s;
-  if (jl > j0 + 1) field |= (unsigned long long)words[j0 + 2] << (64 - s);
-  long long m = (long long)(field << (64 - w)) >> (64 - w);
-  return i2d(m, w) * pow2(E - (w - 1));
-}
-
-// Warp-cooperative encode of one block; lane j holds entry j.
-// Writes the w words and the exponent when `words` is non-null; returns the
-// quantised value m 2^(E-q).  Non-finite input or E > 127 sets *status.
-__device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, int8_t* eptr, int lane,
-                                              int* status) {
-  unsigned long long bits = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
-  bool bad = bits >= 0x7ff0000000000000ULL;
-  unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
-  unsigned mh = __reduce_max_sync(FULL, hi);
-  unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
-  bool err = __any_sync(FULL, bad);
-  double mx = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
-  int q = w - 1, E = -128;
-  if (!err && mx != 0.0) {
-    int ebits = (int)((mh >> 20) & 0x7FFu);
-    int E0 = ebits == 0 ? -1100 : ebits - 1022;  // ilogb(mx) + 1; subnormal max -> saturates below
-    if (E0 > 127) {
-      err = true;
-    } else if (E0 < -127) {
-      E = -127;
-    } else {
-      E = E0;
-      if (rint(mx * pow2(q - E0)) == pow2(q)) E = E0 + 1;
-      if (E > 127) err = true;
-    }
-  }
-  long long m = 0;
-  if (err) {
-    E = -128;
-    if (lane == 0 && status) atomicOr(status, 1);
-  } else if (E != -128) {
-    m = rne_int(v * pow2(q - E), w);
-  }
-  if (words) {
-    unsigned long long field = (unsigned long long)m & ((1ULL << w) - 1ULL);
-    uint32_t mine0 = 0u, mine1 = 0u;
-    if (w <= 8) {
-      // narrow: one redux.or per output word
-      int o = lane * w;
-      for (int j = 0; j < w; ++j) {
-        int s = o - 32 * j;
-        uint32_t c = 0u;
-        if (s > -w && s < 32) c = s >= 0 ? (uint32_t)(field << s) : (uint32_t)(field >> (-s));
-        uint32_t word = __reduce_or_sync(FULL, c);
-        if (lane == j) mine0 = word;
-      }
-    } else {
-      // wide: word j gathers its <= ceil(32/w)+1 entries by shuffles
-      const int K = (32 + w - 1) / w + 1;
-      uint32_t flo = (uint32_t)field, fhi = (uint32_t)(field >> 32);
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        int j = lane + 32 * half;
-        if (half == 1 && w <= 32) break;
-        int e0 = (32 * j) / w;
-        uint32_t acc = 0u;
-        for (int k = 0; k < K; ++k) {
-          int e = e0 + k;
-          int src = e < 32 ? e : 31;
-          uint32_t lo_ = __shfl_sync(FULL, flo, src), hi_ = __shfl_sync(FULL, fhi, src);
-          unsigned long long f = ((unsigned long long)hi_ << 32) | lo_;
-          int s = e * w - 32 * j;
-          if (e < 32 && s < 32 && s > -w) acc |= s >= 0 ? (uint32_t)(f << s) : (uint32_t)(f >> (-s));
-        }
-        if (half == 0) mine0 = acc; else mine1 = acc;
-      }
-    }
-    if (lane < w) words[lane] = mine0;
-    if (lane + 32 < w) words[lane + 32] = mine1;
-    if (lane == 0) *eptr = (int8_t)E;
-  }
-  return E == -128 ? 0.0 : i2d(m, w) * pow2(E - q);
-}
 
 // ------------------------------------------------------------ tile plans --
 template <int D, int P> struct TileCfg;
@@ -229,44 +69,6 @@ template <int D, int P> struct Plan {
   static constexpr int C_SMEM = 2 * ((D == 3) ? 4 * P * P : 2 * P) * 32 * 8;  // coarse solve
   static constexpr int mx2(int a, int b) { return a > b ? a : b; }
   static constexpr int SMEM = mx2(mx2(A_SMEM, D_SMEM), mx2(R_SMEM, C_SMEM));
-};
-
-// ------------------------------------------------------------- contexts --
-// Device-side context (lives in global memory, built by fmg_api.cpp).
-struct LevelDev {
-  Geom g;
-  uint32_t* umant;
-  int8_t* uexp;
-  int ustride;
-  uint32_t* rmant;
-  int8_t* rexp;
-  int rstride;
-  const double* gtab;
-  int tx, ty, tz;  // tile grid of this level
-  double* part;    // norm partials, one per tile
-  int* count;      // arrival counter for the last-CTA norm reduction
-};
-
-struct DevCtx {
-  LevelDev lv[kMaxLev];
-  double* U[2];  // decoded u_l (ping-pong by level parity), emitted by the cFas finalize
-  double* T[2];  // residual temporaries t_l
-  double* W[2];  // w_l = z_l + dec ý_l
-  double* pbase; // norm partials of the grid levels (one slot per FMG level, iteration, level)
-  double* usm;   // K4: dense u_l of the smem levels, persisted between launches
-  long long usm_off[kMaxLev];
-  int lc;        // K4 handles levels 0..lc in shared memory
-  int n_cheb;    // Chebyshev degree k
-  double* Z;     // z_l (only for l < L)
-  double* B;     // b_l = dec r_l - A z_l
-  double* Y[2];  // Chebyshev iterates (k >= 3)
-  double* Dv;    // Chebyshev direction (k >= 3)
-  const double* Ainv;
-  int n0;
-  double* norms;
-  int levels, n_ir;
-  int* status;
-  Coefs cf;
 };
 
 using Op = OpDesc;  // one step of the method on one level (fmg_internal.h)
@@ -620,14 +422,14 @@ __device__ void tile_decode(const DevCtx& c, const Op& op, const TileIdx& tile, 
   const Geom& g = lv.g;
   int x0, y0, z0;
   tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
-  double* out = c.U[op.l & 1];
+  double* out = c.lv[op.l].U;
   double* box = sm;  // DBX x DBY x DBZ
   if (op.l > 0) {
     double* cb = box + PL::DBX * PL::DBY * PL::DBZ;
     double* v1 = cb + PL::DCBX * PL::DCBY * PL::DCBZ;
     double* v2 = v1 + PL::DBX * PL::DCBY * PL::DCBZ;
     box_prolong<D, P, PL::DBX, PL::DBY, PL::DBZ, PL::DCBX, PL::DCBY, PL::DCBZ>(
-        c.U[(op.l - 1) & 1], c.lv[op.l - 1].g, g.n, x0, y0, z0, c.cf, cb, v1, v2, box);
+        c.lv[op.l - 1].U, c.lv[op.l - 1].g, g.n, x0, y0, z0, c.cf, cb, v1, v2, box);
   } else {
     for (int i = threadIdx.y * 32 + threadIdx.x; i < PL::DBX * PL::DBY * PL::DBZ; i += NT) box[i] = 0.0;
     __syncthreads();
@@ -652,13 +454,13 @@ __device__ void tile_residual(const DevCtx& c, const Op& op, const TileIdx& tile
   tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
   double* U = sm;
   double* R1 = sm + 2 * PL::NU;
-  box_async<D, P>(c.U[op.L & 1], g, x0, y0, z0, U);
+  box_async<D, P>(c.lv[op.L].U, g, x0, y0, z0, U);
   cpa_wait_sync();
   double* AB = R1;
   double* CS = R1 + 2 * PL::NAB;
   a_stages<D, P>(g, x0, y0, c.cf, U, AB, CS);
   const int lane = threadIdx.x;
-  double* T = c.T[op.L & 1];
+  double* T = c.lv[op.L].T;
   double ss = 0.0;
   for (int row = threadIdx.y; row < PL::TY * PL::TZ; row += NWARP) {
     int ty = row % PL::TY, tz = row / PL::TY;
@@ -689,8 +491,8 @@ __device__ void tile_restrict(const DevCtx& c, const Op& op, const TileIdx& tile
   const LevelDev& lc = c.lv[op.l];
   const Geom& gc = lc.g;
   const Geom& gf = c.lv[op.l + 1].g;
-  const double* __restrict__ Tf = c.T[(op.l + 1) & 1];
-  double* Tc = c.T[op.l & 1];
+  const double* __restrict__ Tf = c.lv[op.l + 1].T;
+  double* Tc = c.lv[op.l].T;
   int x0, y0, z0;
   tile_coords(tile, PL::TY, PL::TZ, x0, y0, z0);
   double* XR = sm;
@@ -787,11 +589,11 @@ __device__ __forceinline__ void cfas_finalize(const DevCtx& c, const Op& op, con
                                               double y, double pu, double zc, const uint32_t* uw_s) {
   const int lane = threadIdx.x;
   double yq = warp_encode(y, op.wr, nullptr, nullptr, lane, c.status);
-  if (op.l < op.L) c.W[op.l & 1][idx] = zc + yq;
+  if (op.l < op.L) c.lv[op.l].W[idx] = zc + yq;
   long long blk = idx >> 5;
   double uo = warp_decode(uw_s, lv.uexp[blk], op.wu_in, lane);
   double uq = warp_encode(uo + yq, op.wu_out, lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
-  c.U[op.l & 1][idx] = uq + pu;
+  c.lv[op.l].U[idx] = uq + pu;
 }
 
 // P_l u_{l-1} on the output tile (for the emitted u_l): coarse box issue
@@ -799,7 +601,7 @@ __device__ __forceinline__ void cfas_finalize(const DevCtx& c, const Op& op, con
 template <int D, int P>
 __device__ void tile_pu_issue(const DevCtx& c, int l, int x0, int y0, int z0, double* scratch) {
   using PL = Plan<D, P>;
-  cbox_async<D, P, PL::DCBX, PL::DCBY, PL::DCBZ>(c.U[(l - 1) & 1], c.lv[l - 1].g, x0, y0, z0, scratch);
+  cbox_async<D, P, PL::DCBX, PL::DCBY, PL::DCBZ>(c.lv[l - 1].U, c.lv[l - 1].g, x0, y0, z0, scratch);
 }
 template <int D, int P>
 __device__ void tile_pu_compute(const DevCtx& c, int l, int x0, int y0, int z0, double* scratch, double* pu) {
@@ -846,7 +648,7 @@ __device__ void tile_cfas1(const DevCtx& c, const Op& op, const TileIdx& tile, d
   double* v1 = cb + PL::NCB;
   double* v2 = v1 + PL::NV1;
   uint32_t* rw = S.words;
-  cbox_async<D, P, PL::CBX, PL::CBY, PL::CBZ>(c.W[(op.l - 1) & 1], c.lv[op.l - 1].g, x0 - P, y0 - P, z0 - P, cb);
+  cbox_async<D, P, PL::CBX, PL::CBY, PL::CBZ>(c.lv[op.l - 1].W, c.lv[op.l - 1].g, x0 - P, y0 - P, z0 - P, cb);
   rows_words_async<D, P>(lv.rmant, lv.rstride, op.wr, g, x0, y0, z0, rw);
   cpa_wait_sync();
   box_prolong_compute<D, P, PL::BX, PL::BY, PL::BZ, PL::CBX, PL::CBY, PL::CBZ>(g.n, x0 - P, y0 - P, z0 - P, c.cf,
@@ -966,24 +768,23 @@ __device__ void tile_cheb(const DevCtx& c, const Op& op, const TileIdx& tile, do
   }
 }
 
-template <int D, int P>
+template <int D, int P, int T>
 __device__ __forceinline__ void run_op(const DevCtx& c, const Op& op, const TileIdx& tile, double* sm) {
-  switch (op.type) {
-    case OP_DECODE: tile_decode<D, P>(c, op, tile, sm); break;
-    case OP_RESIDUAL: tile_residual<D, P>(c, op, tile, sm); break;
-    case OP_RESTRICT: tile_restrict<D, P>(c, op, tile, sm); break;
-    case OP_NORMS: op_norms(c, op, sm); break;
-    case OP_CFAS1: tile_cfas1<D, P>(c, op, tile, sm); break;
-    case OP_CHEB: tile_cheb<D, P>(c, op, tile, sm); break;
-  }
+  if constexpr (T == OP_DECODE) tile_decode<D, P>(c, op, tile, sm);
+  else if constexpr (T == OP_RESIDUAL) tile_residual<D, P>(c, op, tile, sm);
+  else if constexpr (T == OP_RESTRICT) tile_restrict<D, P>(c, op, tile, sm);
+  else if constexpr (T == OP_NORMS) op_norms(c, op, sm);
+  else if constexpr (T == OP_CFAS1) tile_cfas1<D, P>(c, op, tile, sm);
+  else tile_cheb<D, P>(c, op, tile, sm);
 }
 
-// Grid kernel: one CTA per tile of one operation.  The device context lives in
-// global memory and is read through the read-only path (uniform, L1-cached).
-template <int D, int P>
+// Grid kernel: one CTA per tile of one operation; one kernel per operation
+// type T, so a launch only pulls its own code into the instruction caches.
+// The device context lives in global memory (uniform, L1-cached).
 #ifndef FMG_KOP_MINB
 #define FMG_KOP_MINB 4
 #endif
+template <int D, int P, int T>
 __global__ void __launch_bounds__(NT, FMG_KOP_MINB) k_op(const DevCtx* __restrict__ cp, Op op) {
   extern __shared__ double sm[];
   pdl_wait();
@@ -991,609 +792,8 @@ __global__ void __launch_bounds__(NT, FMG_KOP_MINB) k_op(const DevCtx* __restric
   const DevCtx& c = *cp;
   TileIdx t{(int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z,
             (int)((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x)};
-  run_op<D, P>(c, op, t, sm);
+  run_op<D, P, T>(c, op, t, sm);
 }
-
-// =============================================== K4: coarse hierarchy ======
-// One 512-thread CTA owns levels 0..lc, stored densely (n_l^d doubles, x
-// fastest, no padding) in shared memory: the restriction tail, the norms, the
-// exact coarse solve, the cFas sweep with the corrections and the emitted u_l
-// of those levels run back to back with only __syncthreads between phases (no
-// launch gaps, no global round trips).  Same canonical expression trees as the
-// tile ops.  For FMG levels L <= lc the whole IR iteration
-// (residual included) runs here.
-constexpr int NW4 = 16, NT4 = 32 * NW4;
-constexpr int K4_MAX_SMEM = 210 * 1024;  // dynamic smem budget of the K4 CTA
-constexpr int K4_AINV_MAX = 4096;         // A_0^{-1} entries staged in smem
-
-using K4Args = K4Desc;
-
-__host__ __device__ inline int ipow(int n, int d) { return d == 3 ? n * n * n : n * n; }
-
-// smem offsets (doubles): per level U, T, RQ, W blocks, then 6 scratch arrays of the top level
-__host__ __device__ inline int k4_level_off(int D, int P, int l) {
-  int o = 0;
-  for (int k = 0; k < l; ++k) o += 4 * ipow(P << (k + 1), D);
-  return o;
-}
-__host__ __device__ inline int k4_smem_doubles(int D, int P, int lc) {
-  return k4_level_off(D, P, lc + 1) + 6 * ipow(P << (lc + 1), D);
-}
-
-struct K4Lvl {
-  int n, len;
-  double *U, *T, *RQ, *W;
-};
-
-__device__ __forceinline__ K4Lvl k4_lvl(int D, int P, int l, double* sm) {
-  K4Lvl v;
-  v.n = P << (l + 1);
-  v.len = ipow(v.n, D);
-  // offset of level l: 4 * sum_{k<l} (P 2^(k+1))^D  (geometric sum)
-  const int r = D == 3 ? 8 : 4;                         // ratio between consecutive levels
-  const int first = ipow(2 * P, D);
-  double* b = sm + 4 * first * ((l == 0) ? 0 : ((1 << (D * l)) - 1) / (r - 1));
-  v.U = b;
-  v.T = b + v.len;
-  v.RQ = b + 2 * v.len;
-  v.W = b + 3 * v.len;
-  return v;
-}
-
-__device__ __forceinline__ double rd(const double* a, int j, int n) { return (j >= 0 && j < n) ? a[j] : 0.0; }
-
-// Final-pass iteration helper: warps walk (row, 32-entry block) pairs of a
-// dense level so that each warp holds one BFP block (x = xb*32 + lane, values
-// beyond n are 0) -- epilogues may then encode/decode with warp collectives.
-#define K4_BLOCKS(n, rows)                                                        \
-  for (int rb = threadIdx.y, nxb_ = ((n) + 31) >> 5; rb < (rows) * nxb_; rb += NW4) \
-    for (int r = rb / nxb_, x = (rb % nxb_) * 32 + (int)threadIdx.x, once_ = 1; once_; once_ = 0)
-
-// A_l in (dense), canonical passes; the last pass calls
-// epi(r, x, Av) per point (Av = 0 at non-unknowns and beyond n), warp-aligned.
-template <int D, int P, class Epi>
-__device__ void k4_A(const Coefs& cf, int l, int n, const double* in, double* s, Epi epi) {
-  const int lane = threadIdx.x, w = threadIdx.y, len = ipow(n, D), rows = len / n;
-  double* a = s;
-  double* b = s + len;
-  for (int r = w; r < rows; r += NW4)
-    for (int x = lane; x < n; x += 32) {
-      const double* u = in + r * n;
-      bool ok = unk1(x, n);
-      int tau = ok ? x % P : 0;
-      double aa = 0.0, bb = 0.0;
-#pragma unroll
-      for (int o = 0; o <= 2 * P; ++o) {
-        double v = rd(u, x - P + o, n);
-        aa = fma(cf.Mc[tau][o], v, aa);
-        bb = fma(cf.Kc[tau][o], v, bb);
-      }
-      a[r * n + x] = ok ? aa : 0.0;
-      b[r * n + x] = ok ? bb : 0.0;
-    }
-  __syncthreads();
-  if constexpr (D == 2) {
-    K4_BLOCKS(n, n) {
-      const int y = r;
-      bool ok = unk1(y, n) && unk1(x, n);
-      int tau = unk1(y, n) ? y % P : 0, xs = x < n ? x : 0;
-      double d = 0.0, e = 0.0;
-#pragma unroll
-      for (int o = 0; o <= 2 * P; ++o) {
-        int j = y - P + o;
-        bool in_ = j >= 0 && j < n;
-        d = fma(cf.Kc[tau][o], in_ ? a[j * n + xs] : 0.0, d);
-        e = fma(cf.Mc[tau][o], in_ ? b[j * n + xs] : 0.0, e);
-      }
-      epi(r, x, ok ? d + e : 0.0);
-    }
-  } else {
-    double* c = s + 2 * len;
-    double* sv = s + 3 * len;
-    for (int r = w; r < n * n; r += NW4) {  // rows (z, y)
-      int y = r % n, z = r / n;
-      bool oky = unk1(y, n);
-      int tau = oky ? y % P : 0;
-      for (int x = lane; x < n; x += 32) {
-        double cc = 0.0, dd = 0.0, e = 0.0;
-#pragma unroll
-        for (int o = 0; o <= 2 * P; ++o) {
-          int j = y - P + o;
-          bool in_ = j >= 0 && j < n;
-          double av = in_ ? a[(z * n + j) * n + x] : 0.0, bv = in_ ? b[(z * n + j) * n + x] : 0.0;
-          cc = fma(cf.Mc[tau][o], av, cc);
-          dd = fma(cf.Kc[tau][o], av, dd);
-          e = fma(cf.Mc[tau][o], bv, e);
-        }
-        c[r * n + x] = oky ? cc : 0.0;
-        sv[r * n + x] = oky ? dd + e : 0.0;
-      }
-    }
-    __syncthreads();
-    const double h = pow2(-(l + 1));
-    K4_BLOCKS(n, n * n) {
-      int y = r % n, z = r / n, xs = x < n ? x : 0;
-      bool ok = unk1(z, n) && unk1(y, n) && unk1(x, n);
-      int tau = unk1(z, n) ? z % P : 0;
-      double acc = 0.0;
-#pragma unroll
-      for (int o = 0; o <= 2 * P; ++o) {
-        int j = z - P + o;
-        acc = fma(cf.Kc[tau][o], (j >= 0 && j < n) ? c[(j * n + y) * n + xs] : 0.0, acc);
-      }
-#pragma unroll
-      for (int o = 0; o <= 2 * P; ++o) {
-        int j = z - P + o;
-        acc = fma(cf.Mc[tau][o], (j >= 0 && j < n) ? sv[(j * n + y) * n + xs] : 0.0, acc);
-      }
-      epi(r, x, ok ? acc * h : 0.0);
-    }
-  }
-  __syncthreads();
-}
-
-// f1 = P c1 and (if c2) f2 = P c2 on the fine level nf, one set of passes
-// (DESIGN.md §3.3).  scratch: 2 * (len_f/2^(d-1) + len_f/2).
-template <int D, int P>
-__device__ void k4_P2(const Coefs& cf, int nf, const double* c1, double* f1, const double* c2, double* f2, double* s) {
-  const int lane = threadIdx.x, w = threadIdx.y, nc = nf / 2;
-  const int nv = c2 ? 2 : 1;
-  const int n1 = (D == 3) ? nc * nc * nf : nc * nf;  // x-pass size
-  const int n2 = (D == 3) ? nc * nf * nf : 0;        // y-pass size (3D)
-  const int rows1 = (D == 3) ? nc * nc : nc;
-  for (int r = w; r < nv * rows1; r += NW4) {
-    int k = r / rows1, rr = r % rows1;
-    const double* cs = (k == 0 ? c1 : c2) + rr * nc;
-    double* t1 = s + k * n1;
-    for (int x = lane; x < nf; x += 32) {
-      bool ok = unk1(x, nf);
-      int rx = ok ? x % (2 * P) : 0, base = ok ? P * (x / (2 * P)) : 0;
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) acc = fma(cf.Pw[rx][t], rd(cs, base + t, nc), acc);
-      t1[rr * nf + x] = ok ? acc : 0.0;
-    }
-  }
-  __syncthreads();
-  const int rows2 = (D == 3) ? nc * nf : nf;
-  for (int r = w; r < nv * rows2; r += NW4) {
-    int k = r / rows2, rr = r % rows2;
-    const double* t1 = s + k * n1;
-    double* t2 = (D == 3) ? s + 2 * n1 + k * n2 : (k == 0 ? f1 : f2);
-    int y = rr % nf, cz = rr / nf;
-    bool ok = unk1(y, nf);
-    int ry = ok ? y % (2 * P) : 0, base = ok ? P * (y / (2 * P)) : 0;
-    for (int x = lane; x < nf; x += 32) {
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t <= P; ++t) {
-        int j = base + t;
-        acc = fma(cf.Pw[ry][t], (j < nc) ? t1[(cz * nc + j) * nf + x] : 0.0, acc);
-      }
-      t2[rr * nf + x] = ok ? acc : 0.0;
-    }
-  }
-  __syncthreads();
-  if constexpr (D == 3) {
-    for (int r = w; r < nv * nf * nf; r += NW4) {
-      int k = r / (nf * nf), rr = r % (nf * nf);
-      const double* t2 = s + 2 * n1 + k * n2;
-      double* fo = k == 0 ? f1 : f2;
-      int y = rr % nf, z = rr / nf;
-      bool ok = unk1(z, nf);
-      int rz = ok ? z % (2 * P) : 0, base = ok ? P * (z / (2 * P)) : 0;
-      for (int x = lane; x < nf; x += 32) {
-        double acc = 0.0;
-#pragma unroll
-        for (int t = 0; t <= P; ++t) {
-          int j = base + t;
-          acc = fma(cf.Pw[rz][t], (j < nc) ? t2[(j * nf + y) * nf + x] : 0.0, acc);
-        }
-        fo[rr * nf + x] = ok ? acc : 0.0;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// coarse = R fine; fine given by (ptr, row stride sy, plane
-// stride sz), x < nf valid.  The last pass calls epi(r, x, t) warp-aligned.
-// scratch: nc*nf^(d-1) + nc^2*nf (3D).
-template <int D, int P, class Epi>
-__device__ void k4_R(const Coefs& cf, int nf, const double* fine, long long sy, long long sz, double* s, Epi epi) {
-  const int lane = threadIdx.x, w = threadIdx.y, nc = nf / 2;
-  double* t1 = s;  // [zf][yf][xc]
-  const int rows1 = (D == 3) ? nf * nf : nf;
-  for (int r = w; r < rows1; r += NW4) {
-    int yf = r % nf, zf = r / nf;
-    const double* row = fine + (long long)zf * sz + (long long)yf * sy;
-    for (int x = lane; x < nc; x += 32) {
-      bool ok = unk1(x, nc);
-      int tau = ok ? x % P : 0;
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t <= 4 * P - 2; ++t) {
-        int j = 2 * x - (2 * P - 1) + t;
-        acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? row[j] : 0.0, acc);
-      }
-      t1[r * nc + x] = ok ? acc : 0.0;
-    }
-  }
-  __syncthreads();
-  if constexpr (D == 2) {
-    K4_BLOCKS(nc, nc) {
-      const int yc = r, xs = x < nc ? x : 0;
-      bool ok = unk1(yc, nc) && unk1(x, nc);
-      int tau = unk1(yc, nc) ? yc % P : 0;
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t <= 4 * P - 2; ++t) {
-        int j = 2 * yc - (2 * P - 1) + t;
-        acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t1[j * nc + xs] : 0.0, acc);
-      }
-      epi(r, x, ok ? acc : 0.0);
-    }
-  } else {
-    double* t2 = s + nf * nf * nc;  // [zf][yc][xc]
-    for (int r = w; r < nf * nc; r += NW4) {
-      int yc = r % nc, zf = r / nc;
-      bool ok = unk1(yc, nc);
-      int tau = ok ? yc % P : 0;
-      for (int x = lane; x < nc; x += 32) {
-        double acc = 0.0;
-#pragma unroll
-        for (int t = 0; t <= 4 * P - 2; ++t) {
-          int j = 2 * yc - (2 * P - 1) + t;
-          acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t1[(zf * nf + j) * nc + x] : 0.0, acc);
-        }
-        t2[r * nc + x] = ok ? acc : 0.0;
-      }
-    }
-    __syncthreads();
-    K4_BLOCKS(nc, nc * nc) {
-      int yc = r % nc, zc = r / nc, xs = x < nc ? x : 0;
-      bool ok = unk1(zc, nc) && unk1(yc, nc) && unk1(x, nc);
-      int tau = unk1(zc, nc) ? zc % P : 0;
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t <= 4 * P - 2; ++t) {
-        int j = 2 * zc - (2 * P - 1) + t;
-        acc = fma(cf.Rw[tau][t], (j >= 0 && j < nf) ? t2[(j * nc + yc) * nc + xs] : 0.0, acc);
-      }
-      epi(r, x, ok ? acc : 0.0);
-    }
-  }
-  __syncthreads();
-}
-
-// BFP block of dense level row r, block x/32 (global padded layout).
-__device__ __forceinline__ long long k4_blk(const LevelDev& lv, int r, int x) {
-  return (long long)r * (lv.g.NX >> 5) + (x >> 5);
-}
-
-// Copy a dense level into a padded global array (zeros in the padding).
-__device__ void k4_to_global(int D, int n, const double* v, double* g, const Geom& gg) {
-  const int rows = (D == 3) ? n * n : n;
-  for (int r = threadIdx.y; r < rows; r += NW4)
-    for (int x = threadIdx.x; x < gg.NX; x += 32) g[(long long)r * gg.NX + x] = x < n ? v[r * n + x] : 0.0;
-}
-
-__device__ __forceinline__ double k4_invd_at(const Coefs& cf, int D, int P, int l, int n, int r, int x) {
-  int y = r % n, z = (D == 3) ? r / n : 0;
-  if (!unk1(x, n) || !unk1(y, n) || (D == 3 && !unk1(z, n))) return 0.0;
-  return cf.invd[((D == 3 ? z % P : 0) * P + y % P) * P + x % P] * pow2((l + 1) * (D - 2));
-}
-
-// Optional phase timestamps (debug): thread 0 records globaltimer after phases.
-__device__ unsigned long long g_k4_stamps[64];
-__device__ int g_k4_debug = 0;
-__device__ __forceinline__ void k4_stamp(int i) {
-  if (g_k4_debug && threadIdx.x == 0 && threadIdx.y == 0 && i < 64) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_k4_stamps[i] = t;
-  }
-}
-
-template <int D, int P>
-__global__ void __launch_bounds__(NT4, 1) k4_kernel(const DevCtx* __restrict__ cp, K4Args a) {
-  extern __shared__ double sm[];
-  __shared__ double red[kMaxLev * NW4];
-  pdl_wait();
-  pdl_trigger();
-  const DevCtx& c = *cp;
-  const Coefs& cf = c.cf;
-  const int tid = threadIdx.y * 32 + threadIdx.x, lane = threadIdx.x;
-  const int lc = c.lc;
-  int stamp = 0;
-  k4_stamp(stamp++);
-  const int L = a.L, lce = L < lc ? L : lc;
-  double* scr = sm + k4_level_off(D, P, lc + 1);
-  const int lenc = ipow(P << (lc + 1), D);
-  double* S0 = scr;              // pass scratch (4 arrays)
-  double* SZ = scr + 4 * lenc;   // z_l
-  double* SB = scr + 5 * lenc;   // Chebyshev direction d
-  // Shared-memory staging of the sections of levels 0..lc (read once in the
-  // prologue, written back once in the epilogue) and of A_0^{-1}.
-  __shared__ uint32_t* s_uw[kMaxLev];
-  __shared__ uint32_t* s_rw[kMaxLev];
-  __shared__ int8_t* s_ue[kMaxLev];
-  __shared__ int8_t* s_re[kMaxLev];
-  __shared__ const double* s_ainv;
-  if (tid == 0) {
-    char* p = (char*)(scr + 6 * lenc);
-    for (int l = 0; l <= lc; ++l) {
-      const LevelDev& lv = c.lv[l];
-      s_uw[l] = (uint32_t*)p;
-      p += 4 * lv.g.nblk * lv.ustride;
-      s_rw[l] = (uint32_t*)p;
-      p += 4 * lv.g.nblk * lv.rstride;
-    }
-    for (int l = 0; l <= lc; ++l) {
-      const LevelDev& lv = c.lv[l];
-      s_ue[l] = (int8_t*)p;
-      p += lv.g.nblk;
-      s_re[l] = (int8_t*)p;
-      p += lv.g.nblk;
-    }
-    p = (char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-    s_ainv = (c.n0 * c.n0 <= K4_AINV_MAX) ? (const double*)p : c.Ainv;
-  }
-  __syncthreads();
-  if (a.mode == 0) {
-    // ú_0 = reg(A_0^{-1} f_0); u_0 = dec ú_0
-    K4Lvl v0 = k4_lvl(D, P, 0, sm);
-    const int n = v0.n, m = 2 * P - 1;
-    const LevelDev& lv = c.lv[0];
-    for (int e = tid; e < v0.len; e += NT4) {
-      int x = e % n, y = (e / n) % n, z = (D == 3) ? e / (n * n) : 0;
-      double f = 0.0;
-      if (unk1(x, n) && unk1(y, n) && (D == 2 || unk1(z, n))) {
-        f = cf.rhs_c * lv.gtab[x];
-        f = f * lv.gtab[y];
-        if (D == 3) f = f * lv.gtab[z];
-      }
-      v0.T[e] = f;
-      v0.W[e] = 0.0;
-    }
-    __syncthreads();
-    for (int I = tid; I < c.n0; I += NT4) {
-      double acc = 0.0;
-      for (int J = 0; J < c.n0; ++J) {
-        int jx = J % m + 1, jy = (J / m) % m + 1, jz = (D == 3) ? J / (m * m) + 1 : 0;
-        acc = fma(c.Ainv[(long long)I * c.n0 + J], v0.T[(jz * n + jy) * n + jx], acc);
-      }
-      int ix = I % m + 1, iy = (I / m) % m + 1, iz = (D == 3) ? I / (m * m) + 1 : 0;
-      v0.W[(iz * n + iy) * n + ix] = acc;
-    }
-    __syncthreads();
-    K4_BLOCKS(n, v0.len / n) {
-      long long blk = k4_blk(lv, r, x);
-      double val = x < n ? v0.W[r * n + x] : 0.0;
-      double q = warp_encode(val, a.wu_out[0], lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
-      if (x < n) v0.U[r * n + x] = q;
-    }
-    __syncthreads();
-    for (int e = tid; e < v0.len; e += NT4) c.usm[c.usm_off[0] + e] = v0.U[e];
-    if (lc == 0) k4_to_global(D, n, v0.U, c.U[0], lv.g);
-    return;
-  }
-
-  // ---- prologue: one round of coalesced loads (ú sections, A_0^{-1}, and in 2D
-  //      the fine-level t_{lc+1} feeding the first restriction)
-  for (int l = 0; l <= lce; ++l) {
-    const LevelDev& lv = c.lv[l];
-    const int nw = (int)(lv.g.nblk * lv.ustride);
-    for (int i = tid; i < nw; i += NT4) s_uw[l][i] = lv.umant[i];
-    for (int i = tid; i < (int)lv.g.nblk; i += NT4) s_ue[l][i] = lv.uexp[i];
-  }
-  if (s_ainv != c.Ainv)
-    for (int i = tid; i < c.n0 * c.n0; i += NT4) ((double*)s_ainv)[i] = c.Ainv[i];
-  const bool stage_fine = D == 2 && L > lc &&
-                          (long long)c.lv[lc + 1].g.NX * c.lv[lc + 1].g.NY <= 4LL * lenc;
-  if (stage_fine) {
-    const Geom& gf = c.lv[lc + 1].g;
-    const double* src = c.T[(lc + 1) & 1];
-    const int nt = gf.NX * gf.NY;
-    for (int i = tid; i < nt; i += NT4) S0[i] = src[i];
-  }
-  __syncthreads();
-
-  if (L <= lc) {
-    // ---- residual inside K4: u_L (persisted or P u_{L-1}), t_L = f_L - A_L u_L,
-    //      r_L = enc(t_L)
-    K4Lvl vL = k4_lvl(D, P, L, sm);
-    if (a.first) {
-      K4Lvl vp = k4_lvl(D, P, L - 1, sm);
-      for (int e = tid; e < vp.len; e += NT4) vp.U[e] = c.usm[c.usm_off[L - 1] + e];
-      __syncthreads();
-      k4_P2<D, P>(cf, vL.n, vp.U, vL.U, nullptr, nullptr, S0);
-    } else {
-      for (int e = tid; e < vL.len; e += NT4) vL.U[e] = c.usm[c.usm_off[L] + e];
-      __syncthreads();
-    }
-    const LevelDev& lv = c.lv[L];
-    const int n = vL.n;
-    k4_A<D, P>(cf, L, n, vL.U, S0, [&](int r, int x, double au) {
-      int y = r % n, z = (D == 3) ? r / n : 0;
-      double t = 0.0;
-      if (x < n && unk1(x, n) && unk1(y, n) && (D == 2 || unk1(z, n))) {
-        double f = cf.rhs_c * lv.gtab[x];
-        f = f * lv.gtab[y];
-        if (D == 3) f = f * lv.gtab[z];
-        t = f - au;
-      }
-      long long blk = k4_blk(lv, r, x);
-      double q = warp_encode(t, a.wr[L], s_rw[L] + blk * lv.rstride, s_re[L] + blk, lane, c.status);
-      if (x < n) {
-        vL.T[r * n + x] = t;
-        vL.RQ[r * n + x] = q;
-      }
-    });
-  } else {
-    // ---- restriction from the grid level lc+1 (global t_{lc+1})
-    K4Lvl vc = k4_lvl(D, P, lc, sm);
-    const Geom& gf = c.lv[lc + 1].g;
-    const LevelDev& lv = c.lv[lc];
-    const int n = vc.n;
-    const double* fine = stage_fine ? S0 : c.T[(lc + 1) & 1];
-    double* rscr = stage_fine ? S0 + 4 * lenc : S0;  // 2D: t1 (2 lenc) after the staged fine level
-    k4_R<D, P>(cf, gf.n, fine, gf.NX, (long long)gf.NX * gf.NY, rscr, [&](int r, int x, double t) {
-      long long blk = k4_blk(lv, r, x);
-      double q = warp_encode(t, a.wr[lc], s_rw[lc] + blk * lv.rstride, s_re[lc] + blk, lane, c.status);
-      if (x < n) {
-        vc.T[r * n + x] = t;
-        vc.RQ[r * n + x] = q;
-      }
-    });
-  }
-  k4_stamp(stamp++);
-  // ---- restriction sweep inside smem, r_l = enc(t_l)
-  for (int l = lce - 1; l >= 0; --l) {
-    K4Lvl vf = k4_lvl(D, P, l + 1, sm), vc = k4_lvl(D, P, l, sm);
-    const LevelDev& lv = c.lv[l];
-    const int n = vc.n;
-    k4_R<D, P>(cf, vf.n, vf.T, vf.n, (long long)vf.n * vf.n, S0, [&](int r, int x, double t) {
-      long long blk = k4_blk(lv, r, x);
-      double q = warp_encode(t, a.wr[l], s_rw[l] + blk * lv.rstride, s_re[l] + blk, lane, c.status);
-      if (x < n) {
-        vc.T[r * n + x] = t;
-        vc.RQ[r * n + x] = q;
-      }
-    });
-  }
-  k4_stamp(stamp++);
-  // ---- norms ||t_l||_2 of the smem levels (grid levels: deferred, k_norms_all)
-  for (int l = 0; l <= lce; ++l) {
-    K4Lvl v = k4_lvl(D, P, l, sm);
-    double sacc = 0.0;
-    for (int e = tid; e < v.len; e += NT4) sacc = fma(v.T[e], v.T[e], sacc);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(FULL, sacc, o);
-    if (lane == 0) red[l * NW4 + threadIdx.y] = sacc;
-  }
-  // ---- coarse level (reading R5): ý_0 = enc(A_0^{-1} dec r_0);
-  //      w_0 = dec ý_0; ú_0 = enc(dec ú_0 + dec ý_0); u_0 = dec ú_0
-  {
-    K4Lvl v0 = k4_lvl(D, P, 0, sm);
-    const int n = v0.n, m = 2 * P - 1;
-    for (int e = tid; e < v0.len; e += NT4) SB[e] = 0.0;
-    __syncthreads();
-    if (tid <= lce) {
-      double sacc = 0.0;
-      for (int i = 0; i < NW4; ++i) sacc += red[tid * NW4 + i];
-      c.norms[(long long)a.row * c.levels + tid] = sqrt(sacc);
-    }
-    for (int I = tid; I < c.n0; I += NT4) {
-      double acc = 0.0;
-      for (int J = 0; J < c.n0; ++J) {
-        int jx = J % m + 1, jy = (J / m) % m + 1, jz = (D == 3) ? J / (m * m) + 1 : 0;
-        acc = fma(s_ainv[(long long)I * c.n0 + J], v0.RQ[(jz * n + jy) * n + jx], acc);
-      }
-      int ix = I % m + 1, iy = (I / m) % m + 1, iz = (D == 3) ? I / (m * m) + 1 : 0;
-      SB[(iz * n + iy) * n + ix] = acc;
-    }
-    __syncthreads();
-    const LevelDev& lv = c.lv[0];
-    K4_BLOCKS(n, v0.len / n) {
-      long long blk = k4_blk(lv, r, x);
-      double y = x < n ? SB[r * n + x] : 0.0;
-      double yq = warp_encode(y, a.wr[0], nullptr, nullptr, lane, c.status);
-      uint32_t* uw = s_uw[0] + blk * lv.ustride;
-      double uo = warp_decode(uw, s_ue[0][blk], a.wu_in[0], lane);
-      double uq = warp_encode(uo + yq, a.wu_out[0], uw, s_ue[0] + blk, lane, c.status);
-      if (x < n) {
-        v0.W[r * n + x] = yq;
-        v0.U[r * n + x] = uq;
-      }
-    }
-    __syncthreads();
-  }
-  k4_stamp(stamp++);
-  // ---- coarse-to-fine sweep, Chebyshev-Jacobi,
-  //      correction and the next sweep's u_l, fused per level
-  const int k = c.n_cheb;
-  for (int l = 1; l <= lce; ++l) {
-    K4Lvl vp = k4_lvl(D, P, l - 1, sm), v = k4_lvl(D, P, l, sm);
-    const int n = v.n;
-    const LevelDev& lv = c.lv[l];
-    double* Y = v.T;    // t_l is dead: Chebyshev iterate
-    double* PU = v.U;   // P u_{l-1} (new), then the emitted u_l
-    k4_P2<D, P>(cf, n, vp.W, SZ, vp.U, PU, S0);  // z_l = P w_{l-1}; P u_{l-1}
-    k4_stamp(stamp++);
-    auto finalize = [&](int r, int x, double y) {
-      // ý_l = enc_wr(y); w_l = z_l + dec ý; ú_l = enc(dec ú_l + dec ý); u_l = dec ú_l + P u_{l-1}
-      long long blk = k4_blk(lv, r, x);
-      double yq = warp_encode(y, a.wr[l], nullptr, nullptr, lane, c.status);
-      uint32_t* uw = s_uw[l] + blk * lv.ustride;
-      double uo = warp_decode(uw, s_ue[l][blk], a.wu_in[l], lane);
-      double uq = warp_encode(uo + yq, a.wu_out[l], uw, s_ue[l] + blk, lane, c.status);
-      if (x < n) {
-        v.W[r * n + x] = SZ[r * n + x] + yq;
-        PU[r * n + x] = uq + PU[r * n + x];
-      }
-    };
-    // b = dec r_l - A z_l; d_1 = inv_theta (invD b); y_1 = d_1
-    k4_A<D, P>(cf, l, n, SZ, S0, [&](int r, int x, double az) {
-      double b = 0.0, d = 0.0;
-      if (x < n) {
-        b = v.RQ[r * n + x] - az;
-        d = cf.inv_theta * (k4_invd_at(cf, D, P, l, n, r, x) * b);
-      }
-      if (k == 1) {
-        finalize(r, x, d);
-      } else if (x < n) {
-        v.RQ[r * n + x] = b;
-        SB[r * n + x] = d;
-        Y[r * n + x] = d;
-      }
-    });
-    k4_stamp(stamp++);
-    for (int j = 2; j <= k; ++j) {
-      // q = b - A y; d_j = fma(alpha_j, d_{j-1}, beta_j (invD q)); y_j = y_{j-1} + d_j
-      k4_A<D, P>(cf, l, n, Y, S0, [&](int r, int x, double ay) {
-        double y = 0.0;
-        if (x < n) {
-          double q = v.RQ[r * n + x] - ay;
-          double d = fma(cf.cal[j - 1], SB[r * n + x], cf.cbe[j - 1] * (k4_invd_at(cf, D, P, l, n, r, x) * q));
-          y = Y[r * n + x] + d;
-          if (j < k) {
-            SB[r * n + x] = d;
-            Y[r * n + x] = y;
-          }
-        }
-        if (j == k) finalize(r, x, y);
-      });
-      k4_stamp(stamp++);
-    }
-  }
-  // ---- epilogue: sections back to global (one round of coalesced stores)
-  for (int l = 0; l <= lce; ++l) {
-    const LevelDev& lv = c.lv[l];
-    const int nu = (int)(lv.g.nblk * lv.ustride), nr = (int)(lv.g.nblk * lv.rstride);
-    for (int i = tid; i < nu; i += NT4) lv.umant[i] = s_uw[l][i];
-    for (int i = tid; i < nr; i += NT4) lv.rmant[i] = s_rw[l][i];
-    for (int i = tid; i < (int)lv.g.nblk; i += NT4) {
-      lv.uexp[i] = s_ue[l][i];
-      lv.rexp[i] = s_re[l][i];
-    }
-  }
-  // ---- persist u_l; hand u_lc, w_lc to the grid levels above
-  for (int l = 0; l <= lce; ++l) {
-    K4Lvl v = k4_lvl(D, P, l, sm);
-    for (int e = tid; e < v.len; e += NT4) c.usm[c.usm_off[l] + e] = v.U[e];
-  }
-  if (lce == lc) {
-    K4Lvl v = k4_lvl(D, P, lc, sm);
-    k4_to_global(D, v.n, v.U, c.U[lc & 1], c.lv[lc].g);
-    k4_to_global(D, v.n, v.W, c.W[lc & 1], c.lv[lc].g);
-  }
-  __syncthreads();
-  k4_stamp(stamp++);
-}
-
-void k4_debug(int on) { cudaMemcpyToSymbol(g_k4_debug, &on, sizeof(int)); }
-void k4_stamps(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_k4_stamps, sizeof(unsigned long long) * 64); }
 
 // Deferred norms of the grid levels (end of the solve, off the critical path):
 // one CTA per entry, fixed-order reduction.
@@ -1737,9 +937,12 @@ int smem_bytes(int dim, int p) {
 }
 
 void set_kernel_attributes() {
-#define SETA(D, P)                                                                                       \
-  cudaFuncSetAttribute(k_op<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM); \
-  cudaFuncSetAttribute(k4_kernel<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, K4_MAX_SMEM);
+#define SETA(D, P)                                                                                        \
+  cudaFuncSetAttribute(k_op<D, P, OP_DECODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM);   \
+  cudaFuncSetAttribute(k_op<D, P, OP_RESIDUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM); \
+  cudaFuncSetAttribute(k_op<D, P, OP_RESTRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM); \
+  cudaFuncSetAttribute(k_op<D, P, OP_CFAS1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM);    \
+  cudaFuncSetAttribute(k_op<D, P, OP_CHEB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Plan<D, P>::SMEM);
   SETA(2, 1) SETA(2, 2) SETA(2, 3) SETA(3, 1) SETA(3, 2) SETA(3, 3)
 #undef SETA
 }
@@ -1767,30 +970,22 @@ static cudaError_t launch_pdl(K kernel, dim3 grid, int smem, cudaStream_t st, Ar
 
 void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& op, int tx, int ty, int tz) {
   const DevCtx* c = (const DevCtx*)devctx;
-#define F(D, P) launch_pdl(k_op<D, P>, dim3(tx, ty, tz), Plan<D, P>::SMEM, st, c, op)
+#define LT(D, P, T) launch_pdl(k_op<D, P, T>, dim3(tx, ty, tz), Plan<D, P>::SMEM, st, c, op)
+#define F(D, P)                                            \
+  do {                                                     \
+    switch (op.type) {                                     \
+      case OP_DECODE: LT(D, P, OP_DECODE); break;          \
+      case OP_RESIDUAL: LT(D, P, OP_RESIDUAL); break;      \
+      case OP_RESTRICT: LT(D, P, OP_RESTRICT); break;      \
+      case OP_CFAS1: LT(D, P, OP_CFAS1); break;            \
+      default: LT(D, P, OP_CHEB); break;                   \
+    }                                                      \
+  } while (0)
   FMG_DISPATCH(dim, p, F);
 #undef F
+#undef LT
 }
 
-int k4_smem_bytes(int dim, int p, int lc) { return k4_smem_doubles(dim, p, lc) * 8; }
-int k4_ainv_staged(int n0) { return n0 * n0 <= K4_AINV_MAX; }
-
-void launch_k4(int dim, int p, cudaStream_t st, const void* devctx, const K4Desc& a, int smem) {
-  const DevCtx* c = (const DevCtx*)devctx;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(1);
-  cfg.blockDim = dim3(32, NW4);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-#define F(D, P) cudaLaunchKernelEx(&cfg, k4_kernel<D, P>, c, a)
-  FMG_DISPATCH(dim, p, F);
-#undef F
-}
 
 size_t devctx_size() { return sizeof(DevCtx); }
 void set_devctx_pbase(void* host_buf, double* pbase) { ((DevCtx*)host_buf)->pbase = pbase; }
@@ -1814,19 +1009,19 @@ void fill_devctx(void* host_buf, const DevCtxDesc& d) {
     lv.tz = d.tiles[l][2];
     lv.part = d.part[l];
     lv.count = d.count ? d.count + l : nullptr;
+    lv.U = d.Ul[l];
+    lv.T = d.Tl[l];
+    lv.W = d.Wl[l];
   }
-  for (int i = 0; i < 2; ++i) {
-    c->U[i] = d.U[i];
-    c->T[i] = d.T[i];
-    c->W[i] = d.W[i];
-    c->Y[i] = d.Y[i];
-  }
-  c->usm = d.usm;
+  for (int i = 0; i < 2; ++i) c->Y[i] = d.Y[i];
   c->pbase = d.pbase;
-  for (int l = 0; l < kMaxLev; ++l) c->usm_off[l] = d.usm_off[l];
   c->lc = d.lc;
   c->n_cheb = d.n_cheb;
   c->Z = d.Z;
+  c->PU = d.PU;
+  c->KS[0] = d.KS[0];
+  c->KS[1] = d.KS[1];
+  c->kc = d.kc;
   c->B = d.B;
   c->Dv = d.Dv;
   c->Ainv = d.Ainv;
