@@ -28,6 +28,7 @@
 // and, for FMG levels L <= lc, whole IR iterations.
 #include <algorithm>
 #include <cstdlib>
+#include <new>
 
 #include "fmg_device.cuh"
 
@@ -53,15 +54,18 @@ __device__ __forceinline__ T* mapa(T* p, unsigned rank) {
 __device__ unsigned long long g_kc_stamps[256];
 __device__ int g_kc_nstamp = 0;
 // Cluster-wide phase barrier (release/acquire at cluster scope).
-__device__ __forceinline__ void csync(bool dbg = false) {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  if (dbg && threadIdx.x == 0 && threadIdx.y == 0 && cl_rank() == 0) {  // debug phase stamps
+__device__ __noinline__ void kc_stamp() {  // debug phase stamps
+  if (threadIdx.x == 0 && threadIdx.y == 0 && cl_rank() == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     int i = g_kc_nstamp;
     if (i < 256) g_kc_stamps[i] = t;
     g_kc_nstamp = i + 1;
   }
+}
+__device__ __forceinline__ void csync(bool dbg = false) {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (dbg) kc_stamp();
 }
 
 // Element access.  A distributed array is a per-CTA slab at the same shared
@@ -89,6 +93,14 @@ struct DAcc {
     double* p = base + (idx & ((32 << lgc) - 1));
     return ow == me ? *p : *mapa(p, ow);
   }
+  // pointer to the first entry of 32-entry block column xb of row (y, z), or null
+  __device__ __forceinline__ const double* blk(int xb, int y, int z) const {
+    if (xb < 0 || xb >= (g.NX >> 5) || y < 0 || y >= g.NY || z < 0 || z >= g.NZ) return nullptr;
+    int idx = ((z * g.NY + y) * g.NX) + (xb << 5);
+    unsigned ow = (unsigned)(idx >> (5 + lgc));
+    double* p = base + (idx & ((32 << lgc) - 1));
+    return ow == me ? p : mapa(p, ow);
+  }
 };
 // stencil read of a global level array
 struct GAcc {
@@ -98,9 +110,27 @@ struct GAcc {
     if (x < 0 || x >= g.NX || y < 0 || y >= g.NY || z < 0 || z >= g.NZ) return 0.0;
     return p[((long long)z * g.NY + y) * g.NX + x];
   }
+  __device__ __forceinline__ const double* blk(int xb, int y, int z) const {
+    if (xb < 0 || xb >= (g.NX >> 5) || y < 0 || y >= g.NY || z < 0 || z >= g.NZ) return nullptr;
+    return p + ((long long)z * g.NY + y) * g.NX + (xb << 5);
+  }
 };
 
 constexpr int KC_ROWBUF = 96;  // per-warp staging row (doubles)
+
+#define LANE ((int)threadIdx.x)
+#define WID ((int)threadIdx.y)
+#define SROW (kc_srow[threadIdx.y])
+__shared__ double kc_srow[KC_NW][KC_ROWBUF];  // per-warp staging rows
+
+// Out-of-line codec (one copy shared by every phase: KC is bound by
+// instruction-cache misses, not by call overhead).
+__device__ __noinline__ double kc_enc(double v, int w, uint32_t* words, int8_t* eptr, int* status) {
+  return warp_encode(v, w, words, eptr, (int)threadIdx.x, status);
+}
+__device__ __noinline__ double kc_dec(const uint32_t* words, int E, int w) {
+  return warp_decode(words, E, w, (int)threadIdx.x);
+}
 
 template <int D, int P>
 struct Kc {
@@ -109,9 +139,9 @@ struct Kc {
   const KcDesc& a;
   const Coefs& cf;
   double* sd;          // this CTA's dynamic shared memory (as doubles)
-  double* sr;          // this warp's staging row
-  int NC, rank, w, lane;
+  int NC, rank;
   bool dbg;            // debug phase stamps
+  // (the object lives in shared memory; per-thread values come from threadIdx)
 
   __device__ int wu(int l, int L) const { return a.b_u + a.k_u * (L - l); }
   __device__ int wr(int l, int L) const { return a.b_r + a.k_r * (L - l); }
@@ -146,7 +176,7 @@ struct Kc {
   __device__ __forceinline__ void gather(const U& a_, int xs, int W, int y, int z, double (&v)[K]) const {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      int j = lane + 32 * k;
+      int j = LANE + 32 * k;
       v[k] = j < W ? a_(xs + j, y, z) : 0.0;
     }
   }
@@ -156,20 +186,20 @@ struct Kc {
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      int j = lane + 32 * k;
-      if (j < W) sr[j] = v[k];
+      int j = LANE + 32 * k;
+      if (j < W) SROW[j] = v[k];
     }
     __syncwarp();
   }
 
   // ---- per-point operators, warp-level (canonical trees) ----
-  // x0: first column of the warp's block; every lane returns its column's value.
+  // x0: first column of the warp's block; every LANE returns its column's value.
   // A, x and y passes at output row y, plane z: returns (2D) A u, or (3D) the
   // staged c = My Mx u and s = Ky Mx u + My Kx u (0 where x or y is not an unknown)
   template <class U>
-  __device__ void Axy(const U& u, const Geom& g, int x0, int y, int z, double& cv, double& sv) const {
+  __device__ __noinline__ void Axy(U u, const Geom g, int x0, int y, int z, double& cv, double& sv) const {
     constexpr int R = 2 * P + 1, W = 32 + 2 * P;
-    const int x = x0 + lane, tx = x % P, ty = y % P;
+    const int x = x0 + LANE, tx = x % P, ty = y % P;
     double v[R][2];
 #pragma unroll
     for (int r = 0; r < R; ++r) gather<2>(u, x0 - P, W, y - P + r, z, v[r]);
@@ -180,7 +210,7 @@ struct Kc {
       double s = 0.0, t = 0.0;
 #pragma unroll
       for (int o = 0; o < R; ++o) {
-        double val = sr[lane + o];
+        double val = SROW[LANE + o];
         s = fma(cf.Mc[tx][o], val, s);
         t = fma(cf.Kc[tx][o], val, t);
       }
@@ -198,7 +228,7 @@ struct Kc {
     sv = ok ? dd + e : 0.0;
   }
   // 3D z pass over the staged c, s (KS0, KS1), times h
-  __device__ double A3z(const Geom& g, int x, int y, int z) const {
+  __device__ __noinline__ double A3z(const Geom g, int x, int y, int z) const {
     constexpr int R = 2 * P + 1;
     const DAcc C = acc(ly.KS0, g), S = acc(ly.KS1, g);
     double cz[R], sz[R];
@@ -216,12 +246,12 @@ struct Kc {
     for (int o = 0; o < R; ++o) s = fma(cf.Mc[tz][o], sz[o], s);
     return s * pow2(-(g.l + 1));
   }
-  // (P_l coarse) at fine (x0 + lane, y, z): x, y, z passes;
+  // (P_l coarse) at fine (x0 + LANE, y, z): x, y, z passes;
   // 0 at fine non-unknowns.  The coarse rows are gathered 32 columns wide.
   template <class U>
-  __device__ double Pat(const U& cA, int nf, int x0, int y, int z) const {
+  __device__ __noinline__ double Pat(U cA, int nf, int x0, int y, int z) const {
     constexpr int NR = (D == 3) ? (P + 1) * (P + 1) : P + 1;
-    const int x = x0 + lane;
+    const int x = x0 + LANE;
     const bool okx = unk1(x, nf);
     const int cxs = P * (x0 / (2 * P));
     const int rx = okx ? x % (2 * P) : 0, bx = okx ? P * (x / (2 * P)) : cxs;
@@ -242,7 +272,7 @@ struct Kc {
         stage<1>(v[t3 * (P + 1) + t2], 32);
         double accx = 0.0;
 #pragma unroll
-        for (int t1 = 0; t1 <= P; ++t1) accx = fma(cf.Pw[rx][t1], sr[bx - cxs + t1], accx);
+        for (int t1 = 0; t1 <= P; ++t1) accx = fma(cf.Pw[rx][t1], SROW[bx - cxs + t1], accx);
         accy = fma(cf.Pw[ry][t2], accx, accy);
       }
       if (D == 3) accz = fma(cf.Pw[rz][t3], accy, accz);
@@ -250,12 +280,12 @@ struct Kc {
     if (!okx || !oky || !okz) return 0.0;
     return D == 2 ? accy : accz;
   }
-  // R at coarse (x0c + lane, yc) on fine plane fz: the x and y passes (2D: R t_f;
+  // R at coarse (x0c + LANE, yc) on fine plane fz: the x and y passes (2D: R t_f;
   // 3D: the staged y pass).  Fine rows are gathered in batches of RB.
   template <class U>
-  __device__ double Rxy(const U& tf, const Geom& gf, int nc, int x0c, int yc, int fz) const {
+  __device__ __noinline__ double Rxy(U tf, const Geom gf, int nc, int x0c, int yc, int fz) const {
     constexpr int NS = 4 * P - 1, W = 64 + NS - 1, RB = 4;
-    const int xc = x0c + lane, txc = xc % P, tyc = yc % P;
+    const int xc = x0c + LANE, txc = xc % P, tyc = yc % P;
     const int fxs = 2 * x0c - (2 * P - 1);
     double t = 0.0;
 #pragma unroll
@@ -272,7 +302,7 @@ struct Kc {
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           // (t is stored as +0 at fine non-unknowns: no mask needed)
-          xv = fma(cf.Rw[txc][s], sr[2 * lane + s], xv);
+          xv = fma(cf.Rw[txc][s], SROW[2 * LANE + s], xv);
         }
         t = fma(cf.Rw[tyc][s0 + r], xv, t);
       }
@@ -280,7 +310,7 @@ struct Kc {
     return (unk1(xc, nc) && unk1(yc, nc)) ? t : 0.0;
   }
   // 3D second half of R: z pass over the staged planes (KS0, geometry (NXc, NYc, NZf))
-  __device__ double R3z(const Geom& gc, int nzf, int xc, int yc, int zc) const {
+  __device__ __noinline__ double R3z(const Geom gc, int nzf, int xc, int yc, int zc) const {
     constexpr int NS = 4 * P - 1;
     Geom gs = gc;
     gs.NZ = nzf;
@@ -320,11 +350,11 @@ struct Kc {
     const int nb = nxb * g.NY * nz;
     const int lgc = kc_lgc(nb, ly.lg);
     const int b1 = min(nb, (rank + 1) << lgc);
-    for (int b = (rank << lgc) + w; b < b1; b += KC_NW) {
+    for (int b = (rank << lgc) + WID; b < b1; b += KC_NW) {
       int xb = b % nxb;
       int r = b / nxb;
       int y = r % g.NY, z = r / g.NY;
-      body(xb * 32, y, z, (long long)(b * 32 + lane), (long long)b, lgc);
+      body(xb * 32, y, z, (long long)(b * 32 + LANE), (long long)b, lgc);
     }
   }
   template <class F>
@@ -336,7 +366,7 @@ struct Kc {
   __device__ void norm_partial(double ss, int row, int l) const {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
-    if (lane == 0) sd[ly.part + ((row - a.row0) * (c.lc + 1) + l) * KC_NW + w] = ss;
+    if (LANE == 0) sd[ly.part + ((row - a.row0) * (c.lc + 1) + l) * KC_NW + WID] = ss;
   }
 
   // A applied at the warp's block (2D: one phase; 3D: z pass over KS0/KS1 staged by ph_A3xy)
@@ -346,23 +376,23 @@ struct Kc {
       Axy(acc(off, g), g, x0, y, 0, cv, sv);
       return cv;
     } else {
-      return A3z(g, x0 + lane, y, z);
+      return A3z(g, x0 + LANE, y, z);
     }
   }
 
   // ---- phases ------------------------------------------------------------
   // u_L = dec ú_L + P_L u_{L-1} (decode sweep S2)
-  __device__ void ph_decode(int L, int wd) const {
+  __device__ __noinline__ void ph_decode(int L, int wd) const {
     const Geom& g = c.lv[L].g;
     const DAcc up = acc(ly.U[L - 1], c.lv[L - 1].g);
     blocks(g, [&](int x0, int y, int z, long long idx, long long b, int nb) {
       double pu = Pat(up, g.n, x0, y, z);
-      double dv = warp_decode(umw(L, b), *uex(L, b), wd, lane);
+      double dv = kc_dec(umw(L, b), *uex(L, b), wd);
       own(ly.U[L], nb, idx) = dv + pu;
     });
   }
   // 3D scratch phase: KS0, KS1 = x/y passes of A on the array at `off`
-  __device__ void ph_A3xy(int off, const Geom& g) const {
+  __device__ __noinline__ void ph_A3xy(int off, const Geom& g) const {
     const DAcc u = acc(off, g);
     blocks(g, [&](int x0, int y, int z, long long idx, long long, int nb) {
       double cv, sv;
@@ -372,17 +402,17 @@ struct Kc {
     });
   }
   // t_L = f_L - A_L u_L, r_L = enc(t_L)
-  __device__ void ph_residual(int L, int row) const {
+  __device__ __noinline__ void ph_residual(int L, int row) const {
     const LevelDev& lv = c.lv[L];
     const int wrL = wr(L, L);
     double ss = 0.0;
     blocks(lv.g, [&](int x0, int y, int z, long long idx, long long b, int nb) {
-      const int x = x0 + lane;
+      const int x = x0 + LANE;
       double au = Aat(ly.U[L], lv.g, x0, y, z);
       double t = unk(lv.g, x, y, z) ? rhs(lv, x, y, z) - au : 0.0;
       own(ly.T[L], nb, idx) = t;
       ss = fma(t, t, ss);
-      double q = warp_encode(t, wrL, rmw(L, b), rex(L, b), lane, c.status);
+      double q = kc_enc(t, wrL, rmw(L, b), rex(L, b), c.status);
       if (L == 0) own(ly.RQ0, nb, idx) = q;
     });
     norm_partial(ss, row, L);
@@ -394,7 +424,7 @@ struct Kc {
     else f(acc(ly.T[l + 1], c.lv[l + 1].g));
   }
   // 3D scratch phase of R: KS0 = y pass of the x pass of t_{l+1}, per fine plane
-  __device__ void ph_R3xy(int l) const {
+  __device__ __noinline__ void ph_R3xy(int l) const {
     const Geom& gc = c.lv[l].g;
     const Geom& gf = c.lv[l + 1].g;
     with_fine(l, [&](const auto& tf) {
@@ -404,7 +434,7 @@ struct Kc {
     });
   }
   // t_l = R_{l+1} t_{l+1} (restricts t, not r: PAPER.md:742-744), r_l = enc(t_l)
-  __device__ void ph_restrict(int l, int L, int row) const {
+  __device__ __noinline__ void ph_restrict(int l, int L, int row) const {
     const Geom& gc = c.lv[l].g;
     const Geom& gf = c.lv[l + 1].g;
     const int wrl = wr(l, L);
@@ -413,10 +443,10 @@ struct Kc {
       blocks(gc, [&](int x0, int y, int z, long long idx, long long b, int nb) {
         double t;
         if constexpr (D == 2) t = Rxy(tf, gf, gc.n, x0, y, 0);
-        else t = R3z(gc, gf.NZ, x0 + lane, y, z);
+        else t = R3z(gc, gf.NZ, x0 + LANE, y, z);
         own(ly.T[l], nb, idx) = t;
         ss = fma(t, t, ss);
-        double q = warp_encode(t, wrl, rmw(l, b), rex(l, b), lane, c.status);
+        double q = kc_enc(t, wrl, rmw(l, b), rex(l, b), c.status);
         if (l == 0) own(ly.RQ0, nb, idx) = q;
       });
     });
@@ -428,11 +458,11 @@ struct Kc {
     return ((D == 3 ? z - 1 : 0) * m + (y - 1)) * m + (x - 1);
   }
   // Initial coarse solve ú_0 = enc(A_0^{-1} f_0), u_0 = dec ú_0
-  __device__ void ph_coarse_initial() const {
+  __device__ __noinline__ void ph_coarse_initial() const {
     const LevelDev& lv = c.lv[0];
     const int m = 2 * P - 1;
     blocks(lv.g, [&](int x0, int y, int z, long long idx, long long b, int nb) {
-      const int x = x0 + lane;
+      const int x = x0 + LANE;
       double s = 0.0;
       if (unk(lv.g, x, y, z)) {
         const int I = coarse_index(x, y, z);
@@ -441,38 +471,38 @@ struct Kc {
           s = fma(c.Ainv[(long long)I * c.n0 + J], rhs(lv, jx, jy, jz), s);
         }
       }
-      double q = warp_encode(s, wu(0, 0), umw(0, b), uex(0, b), lane, c.status);
+      double q = kc_enc(s, wu(0, 0), umw(0, b), uex(0, b), c.status);
       own(ly.U[0], nb, idx) = q;
     });
   }
   // ý_0 = enc(A_0^{-1} dec r_0) (reading R5); w_0 = dec ý_0;
   // ú_0 = enc(dec ú_0 + dec ý_0); u_0 = dec ú_0.
-  __device__ void ph_coarse(int L, int it, double* srq) const {
+  __device__ __noinline__ void ph_coarse(int L, int it, double* srq) const {
     const Geom& g = c.lv[0].g;
     const int m = 2 * P - 1;
     {  // every CTA gathers dec r_0 at the unknowns (one batched round of loads)
       const DAcc rq = acc(ly.RQ0, g);
-      const int J = w * 32 + lane;
+      const int J = WID * 32 + LANE;
       if (J < c.n0) srq[J] = rq(J % m + 1, (J / m) % m + 1, (D == 3) ? J / (m * m) + 1 : 0);
       __syncthreads();
     }
     blocks(g, [&](int x0, int y, int z, long long idx, long long b, int nb) {
-      const int x = x0 + lane;
+      const int x = x0 + LANE;
       double s = 0.0;
       if (unk(g, x, y, z)) {
         const double* Ai = c.Ainv + (long long)coarse_index(x, y, z) * c.n0;
 #pragma unroll 9
         for (int J = 0; J < c.n0; ++J) s = fma(Ai[J], srq[J], s);
       }
-      double yq = warp_encode(s, wr(0, L), nullptr, nullptr, lane, c.status);
-      double uo = warp_decode(umw(0, b), *uex(0, b), wu_in(0, L, it), lane);
-      double uq = warp_encode(uo + yq, wu(0, L), umw(0, b), uex(0, b), lane, c.status);
+      double yq = kc_enc(s, wr(0, L), nullptr, nullptr, c.status);
+      double uo = kc_dec(umw(0, b), *uex(0, b), wu_in(0, L, it));
+      double uq = kc_enc(uo + yq, wu(0, L), umw(0, b), uex(0, b), c.status);
       own(ly.W[0], nb, idx) = yq;
       own(ly.U[0], nb, idx) = uq;
     });
   }
   // z_l = P_l w_{l-1} and P_l u_{l-1} (for the emitted u_l)
-  __device__ void ph_prolong(int l) const {
+  __device__ __noinline__ void ph_prolong(int l) const {
     const Geom& g = c.lv[l].g;
     const DAcc wp = acc(ly.W[l - 1], c.lv[l - 1].g), up = acc(ly.U[l - 1], c.lv[l - 1].g);
     blocks(g, [&](int x0, int y, int z, long long idx, long long, int nb) {
@@ -482,21 +512,21 @@ struct Kc {
   }
   // ý_l = enc(y); w_l = z_l + dec ý_l; ú_l = enc(dec ú_l + dec ý_l); u_l = dec ú_l + P u_{l-1}
   __device__ __forceinline__ void finalize(int l, int L, int it, long long idx, long long b, int nb, double y) const {
-    double yq = warp_encode(y, wr(l, L), nullptr, nullptr, lane, c.status);
+    double yq = kc_enc(y, wr(l, L), nullptr, nullptr, c.status);
     if (l < L) own(ly.W[l], nb, idx) = own(ly.Z, nb, idx) + yq;
-    double uo = warp_decode(umw(l, b), *uex(l, b), wu_in(l, L, it), lane);
-    double uq = warp_encode(uo + yq, wu(l, L), umw(l, b), uex(l, b), lane, c.status);
+    double uo = kc_dec(umw(l, b), *uex(l, b), wu_in(l, L, it));
+    double uq = kc_enc(uo + yq, wu(l, L), umw(l, b), uex(l, b), c.status);
     own(ly.U[l], nb, idx) = uq + own(ly.PU, nb, idx);
   }
   // Chebyshev step 1: b = dec r_l - A z_l; d_1 = y_1 = inv_theta (invD b)
-  __device__ void ph_cheb1(int l, int L, int it) const {
+  __device__ __noinline__ void ph_cheb1(int l, int L, int it) const {
     const Geom& g = c.lv[l].g;
     const int wrl = wr(l, L);
     const int k = c.n_cheb;
     blocks(g, [&](int x0, int y, int z, long long idx, long long b, int nb) {
-      const int x = x0 + lane;
+      const int x = x0 + LANE;
       double az = Aat(ly.Z, g, x0, y, z);
-      double rv = warp_decode(rmw(l, b), *rex(l, b), wrl, lane);
+      double rv = kc_dec(rmw(l, b), *rex(l, b), wrl);
       double bb = rv - az;
       double d = cf.inv_theta * (invd(g, x, y, z) * bb);
       if (k == 1) {
@@ -508,12 +538,12 @@ struct Kc {
     });
   }
   // step j >= 2: q = b - A y; d_j = fma(alpha_j, d_{j-1}, beta_j (invD q)); y_j = y_{j-1} + d_j
-  __device__ void ph_chebj(int l, int L, int it, int j) const {
+  __device__ __noinline__ void ph_chebj(int l, int L, int it, int j) const {
     const Geom& g = c.lv[l].g;
     const int k = c.n_cheb;
     const int yp = (j - 1) & 1 ? ly.Y1 : ly.Y0, yn = j & 1 ? ly.Y1 : ly.Y0;
     blocks(g, [&](int x0, int y, int z, long long idx, long long b, int nb) {
-      const int x = x0 + lane;
+      const int x = x0 + LANE;
       double ay = Aat(yp, g, x0, y, z);
       double q = own(ly.B, nb, idx) - ay;
       double yprev = own(yp, nb, idx);
@@ -532,7 +562,7 @@ struct Kc {
   // One IR iteration at FMG level L restricted to levels 0..min(L, lc)
   // (PAPER.md:791-798).  For L > lc the grid ops did the residual and the
   // restriction down to lc+1 and do the cFas levels above lc afterwards.
-  __device__ void iteration(int L, int it, double* srq) const {
+  __device__ __noinline__ void iteration(int L, int it, double* srq) const {
     const int lc = c.lc;
     const int top = L < lc ? L : lc;
     const int row = L * c.n_ir + it;
@@ -579,8 +609,8 @@ struct Kc {
   }
 
   // ---- prologue / epilogue (the only global-memory traffic) ---------------
-  __device__ void load_sections(int top) const {
-    const int tid = w * 32 + lane;
+  __device__ __noinline__ void load_sections(int top) const {
+    const int tid = WID * 32 + LANE;
     for (int l = 0; l <= top; ++l) {
       const LevelDev& lv = c.lv[l];
       const int nb = (int)lv.g.nblk, nbpc = 1 << ly.lgc[l], b0 = rank * nbpc;
@@ -595,8 +625,8 @@ struct Kc {
       }
     }
   }
-  __device__ void store_back(int top, int nrows) const {
-    const int tid = w * 32 + lane;
+  __device__ __noinline__ void store_back(int top, int nrows) const {
+    const int tid = WID * 32 + LANE;
     for (int l = 0; l <= top; ++l) {
       const LevelDev& lv = c.lv[l];
       const int nb = (int)lv.g.nblk, nbpc = 1 << ly.lgc[l], b0 = rank * nbpc;
@@ -628,13 +658,16 @@ struct Kc {
   }
 };
 
+#undef LANE
+#undef WID
+#undef SROW
+
 template <int D, int P>
 __global__ void __launch_bounds__(KC_NT, 1) kc_kernel(const DevCtx* __restrict__ cp, KcDesc a) {
   extern __shared__ __align__(16) double kc_dsm[];
   // The context (level descriptors, operator coefficients, layout) is copied
   // to shared memory once: the cluster barrier's acquire invalidates L1.
   __shared__ __align__(16) unsigned char sctx[sizeof(DevCtx)];
-  __shared__ double srow[KC_NW][KC_ROWBUF];  // per-warp staging rows
   __shared__ double srq[128];                // dec r_0 at the coarse unknowns (<= 125)
   pdl_wait();
   pdl_trigger();
@@ -649,7 +682,16 @@ __global__ void __launch_bounds__(KC_NT, 1) kc_kernel(const DevCtx* __restrict__
   const int NC = 1 << ly.lg;
   const bool dbg = a.debug != 0;
   if (dbg && threadIdx.x == 0 && threadIdx.y == 0 && cl_rank() == 0) g_kc_nstamp = 0;
-  Kc<D, P> k{c, ly, a, c.cf, kc_dsm, srow[threadIdx.y], NC, (int)cl_rank(), (int)threadIdx.y, (int)threadIdx.x, dbg};
+  // The phase object lives in shared memory: its (non-inlined) phase functions
+  // read their state with shared loads, never from the stack.
+  __shared__ KcDesc sa;
+  __shared__ __align__(16) unsigned char kbuf[sizeof(Kc<D, P>)];
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    sa = a;
+    new (kbuf) Kc<D, P>{c, ly, sa, c.cf, kc_dsm, NC, (int)cl_rank(), dbg};
+  }
+  __syncthreads();
+  Kc<D, P>& k = *reinterpret_cast<Kc<D, P>*>(kbuf);
   const int top = (a.mode == 0) ? a.Llast : c.lc;
   k.load_sections(top);
   csync(dbg);  // every CTA's slabs are loaded before any remote read
