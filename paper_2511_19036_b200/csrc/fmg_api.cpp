@@ -64,6 +64,8 @@ struct fmg_ctx {
   double* Ul[kMaxLev]{};          // per-level u_l, t_l, w_l (padded level layout)
   double* Tl[kMaxLev]{};
   double* Wl[kMaxLev]{};
+  bool march = false;             // 2D grid levels run the row-march kernels (fmg_march.cu)
+  int mrc[kMaxLev]{}, mitems[kMaxLev]{};  // march rows per chunk, work items per level
   fmg_alloc_fn afn = nullptr;
   fmg_free_fn ffn = nullptr;
   void* auser = nullptr;
@@ -120,7 +122,7 @@ struct Builder {
   long long ptot = 0;  // (set past the KC partial region by make_builder)
   // reserve partial slots for (row, level l) and record the deferred norm
   long long slot(int row, int l) {
-    int nt = c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2];
+    int nt = c->march ? c->mitems[l] : c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2];
     long long off = ptot;
     ptot += nt;
     NormEntry e{off, row, l, nt, 0};
@@ -331,13 +333,32 @@ void issue(fmg_ctx* c, const Builder& b) {
       mark(c, -2);
     } else {
       mark(c, it.timed_cls);
-      int tx = 1, ty = 1, tz = 1;
-      if (it.op.type != OP_NORMS) {
-        tx = c->tiles[it.op.l][0];
-        ty = c->tiles[it.op.l][1];
-        tz = c->tiles[it.op.l][2];
+      if (c->march) {
+        const OpDesc& o = it.op;
+        MArgs m{};
+        m.type = o.type;
+        m.l = o.l;
+        m.L = o.L;
+        m.step = o.step;
+        m.last = o.last;
+        m.wr = o.wr;
+        m.wu_in = o.wu_in;
+        m.wu_out = o.wu_out;
+        m.RC = c->mrc[o.l];
+        m.nxb = c->g[o.l].NX / 32;
+        m.nitems = c->mitems[o.l];
+        m.NYo = c->g[o.l].NY;
+        m.poff = o.poff;
+        launch_march(c->p, c->cur, c->devctx, m, c->cf);
+      } else {
+        int tx = 1, ty = 1, tz = 1;
+        if (it.op.type != OP_NORMS) {
+          tx = c->tiles[it.op.l][0];
+          ty = c->tiles[it.op.l][1];
+          tz = c->tiles[it.op.l][2];
+        }
+        launch_op(c->dim, c->p, c->cur, c->devctx, it.op, tx, ty, tz);
       }
-      launch_op(c->dim, c->p, c->cur, c->devctx, it.op, tx, ty, tz);
       mark(c, it.timed_cls);
     }
     c->launches++;
@@ -442,6 +463,8 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   c->afn = g_alloc; c->ffn = g_free; c->auser = g_alloc_user;
   if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) { delete c; return FMG_ECUDA; }
   set_kernel_attributes();
+  march_set_attributes();
+  c->march = dim == 2 && !(getenv("FMG_MARCH") && atoi(getenv("FMG_MARCH")) == 0);
   if (getenv("FMG_SYNC_DEBUG")) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fprintf(stderr, "[fmg] set_kernel_attributes: %s\n", cudaGetErrorString(e));
@@ -478,6 +501,13 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     cudaMemcpy(c->gtab[l], gt.data(), sizeof(double) * g.n, cudaMemcpyHostToDevice);
     c->part_off[l] = tot_parts;
     tot_parts += nt;
+    // 2D row march: ~3600 warps of work (148 SMs x 24 warps) per full level
+    int nxb = g.NX / 32;
+    long long want = 148LL * 24;
+    int rc = (int)(((long long)g.NY * nxb + want - 1) / want);
+    rc = std::max(1, std::min(rc, g.NY));
+    c->mrc[l] = rc;
+    c->mitems[l] = nxb * ((g.NY + rc - 1) / rc);
   }
   // KC (one thread-block cluster, fmg_kc.cu) owns levels 0..lc: the largest
   // prefix with <= 2 BFP blocks per KC warp whose data fits the cluster's

@@ -135,10 +135,12 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
       const int p = lane * w, j0 = p >> 5;
       const unsigned long long cf = field << (p & 31);
       const uint32_t c0 = (uint32_t)cf, c1 = (uint32_t)(cf >> 32);
-#pragma unroll 1
-      for (int j = 0; j < w; ++j) {
-        uint32_t word = __reduce_or_sync(FULL, j == j0 ? c0 : (j == j0 + 1 ? c1 : 0u));
-        mine0 = lane == j ? word : mine0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // independent reductions (w is warp-uniform)
+        if (j < w) {
+          uint32_t word = __reduce_or_sync(FULL, j == j0 ? c0 : (j == j0 + 1 ? c1 : 0u));
+          mine0 = lane == j ? word : mine0;
+        }
       }
     } else {
       // wide: word j gathers its <= ceil(32/w)+1 entries by shuffles
@@ -149,8 +151,9 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
         const int j = lane + 32 * half;
         const int e0 = (32 * j) / w;
         uint32_t acc = 0u;
-#pragma unroll 1
-        for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {  // K <= 5 for w >= 9
+          if (k >= K) break;
           const int e = e0 + k;
           const int src = e < 32 ? e : 31;
           const uint32_t lo_ = __shfl_sync(FULL, flo, src), hi_ = __shfl_sync(FULL, fhi, src);

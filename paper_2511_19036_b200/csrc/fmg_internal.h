@@ -53,6 +53,14 @@ struct OpDesc {
   long long poff;  // norm partials of this (FMG level, iteration, level): pbase + poff
 };
 
+// 2D row-march launch (fmg_march.cu): one warp per (32-column block, chunk of RC output rows).
+struct MArgs {
+  int type, l, L, step, last;
+  int wr, wu_in, wu_out;
+  int RC, nxb, nitems, NYo;  // rows per chunk, block columns, work items, output rows
+  long long poff;            // norm partials (one per item) at pbase + poff, or -1
+};
+
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.
 struct NormEntry {
   long long poff;
@@ -122,6 +130,8 @@ size_t op_size();
 void fill_devctx(void* host_buf, const DevCtxDesc& d);
 void pack_op(void* dst, const OpDesc& od);
 void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int tx, int ty, int tz);
+void march_set_attributes();
+void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);
 int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* rst, int n_ir, int lc_cap,
             KcLayout* ly, int* lc_out, int* cs_out);
 int kc_warps_per_cta();

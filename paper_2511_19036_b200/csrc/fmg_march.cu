@@ -1,0 +1,529 @@
+// fmg_march.cu -- 2D grid-level kernels of the compact-FMG hot path as
+// row-marching warps.
+//
+// A warp owns one 32-entry block column (= one BFP block per row) and marches
+// down a chunk of rows.  Input rows (the block plus its x halo) are staged in a
+// per-warp shared ring by cp.async PF rows ahead; the x pass of the
+// tensor-product operator reads the staged row, the y pass runs on a register
+// ring of the last 2p+1 x-pass results, and the epilogue (residual, Chebyshev
+// update, BFP encode / decode, correction) works on whole 32-entry rows with
+// warp collectives.  Warps are independent (no __syncthreads): a CTA is just
+// 8 warps of work items (block column, row chunk).
+//
+// Every expression follows the canonical evaluation order of DESIGN.md §3
+// with explicit fma() (-fmad=false): results are bit-identical to the tile
+// ops, the cluster kernel and the oracle.
+//
+// Paper: residual t_L = f_L - A_L u_L and r_L = enc(t_L) (Alg 3.2),
+// restriction t_l = R t_{l+1}, r_l = enc(t_l), decode sweep
+// u_l = dec ú_l + P u_{l-1}, cFas level step z_l = P w_{l-1},
+// smoothing, ý encode, correction (Alg 3.1, Alg 3.3).
+#include "fmg_device.cuh"
+
+namespace fmg {
+
+constexpr int MW = 8;        // warps per CTA
+constexpr int MNB = 8;       // staged rows per warp (ring; >= MPF + p + 1)
+constexpr int MPF = 4;       // rows staged ahead
+constexpr int MSLOT = 80;    // doubles per staged row (>= 64 + 4p - 2 + 1)
+
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+struct MItem {
+  int x0, ys, ye, item;
+};
+// work item of this warp: (block column, row chunk), or false if none
+__device__ __forceinline__ bool m_item(const MArgs& a, MItem& it) {
+  const int item = blockIdx.x * MW + threadIdx.y;
+  if (item >= a.nitems) return false;
+  const int xb = item % a.nxb, ch = item / a.nxb;
+  it.x0 = xb * 32;
+  it.ys = ch * a.RC;
+  it.ye = min(a.NYo, it.ys + a.RC);
+  it.item = item;
+  return true;
+}
+
+// Stage row y of `src` (geometry g) into `dst`: dst[H + j] = src(x0 + j, y),
+// dst[j] = src(x0 - H + j, y) and dst[H + 32 + j] = src(x0 + 32 + j, y) for
+// j < H; zero outside the stored level.  cp.async (zero-filled when out of range).
+__device__ __forceinline__ void stage_row(const double* __restrict__ src, const Geom& g, int x0, int y, int H,
+                                          double* dst, int lane) {
+  const bool rowok = y >= 0 && y < g.NY;
+  const double* rp = src + (long long)(rowok ? y : 0) * g.NX;
+  const int x = x0 + lane;
+  const bool ok = rowok && x < g.NX;
+  cpa8(dst + H + lane, ok ? rp + x : src, ok);
+  if (lane < 2 * H) {
+    const int xh = lane < H ? x0 - H + lane : x0 + 32 + (lane - H);
+    const bool okh = rowok && xh >= 0 && xh < g.NX;
+    cpa8(dst + (lane < H ? lane : 32 + lane), okh ? rp + xh : src, okh);
+  }
+}
+
+// P_l c at fine (x, y) from the coarse array (x, y passes); 0 at fine
+// non-unknowns.  Direct (L1-cached) loads.
+template <int P>
+__device__ __forceinline__ double prolong_at(const Coefs& cf, const double* __restrict__ cA, const Geom& gc, int nf,
+                                             int x, int y) {
+  if (!unk1(x, nf) || !unk1(y, nf)) return 0.0;
+  const int rx = x % (2 * P), bx = P * (x / (2 * P));
+  const int ry = y % (2 * P), by = P * (y / (2 * P));
+  double v[P + 1][P + 1];
+#pragma unroll
+  for (int t2 = 0; t2 <= P; ++t2)
+#pragma unroll
+    for (int t1 = 0; t1 <= P; ++t1) {
+      const int cx = bx + t1, cy = by + t2;
+      v[t2][t1] = (cx < gc.NX && cy < gc.NY) ? cA[(long long)cy * gc.NX + cx] : 0.0;
+    }
+  double accy = 0.0;
+#pragma unroll
+  for (int t2 = 0; t2 <= P; ++t2) {
+    double accx = 0.0;
+#pragma unroll
+    for (int t1 = 0; t1 <= P; ++t1) accx = fma(cf.Pw[rx][t1], v[t2][t1], accx);
+    accy = fma(cf.Pw[ry][t2], accx, accy);
+  }
+  return accy;
+}
+
+// warp_decode with the block's words already in registers (lane j holds word j
+// and, for w > 32, word j + 32 in w1)
+__device__ __forceinline__ double warp_decode_r(uint32_t my0, int E, int w, int lane, uint32_t my1 = 0u) {
+  const int o = lane * w, j0 = o >> 5, s = o & 31;
+  uint32_t w0, w1, w2;
+  if (w <= 32) {
+    w0 = __shfl_sync(FULL, my0, j0 & 31);
+    w1 = __shfl_sync(FULL, my0, (j0 + 1) & 31);
+    w2 = __shfl_sync(FULL, my0, (j0 + 2) & 31);
+  } else {
+    uint32_t a0 = __shfl_sync(FULL, my0, j0 & 31), b0 = __shfl_sync(FULL, my1, j0 & 31);
+    uint32_t a1 = __shfl_sync(FULL, my0, (j0 + 1) & 31), b1 = __shfl_sync(FULL, my1, (j0 + 1) & 31);
+    uint32_t a2 = __shfl_sync(FULL, my0, (j0 + 2) & 31), b2 = __shfl_sync(FULL, my1, (j0 + 2) & 31);
+    w0 = j0 < 32 ? a0 : b0;
+    w1 = j0 + 1 < 32 ? a1 : b1;
+    w2 = j0 + 2 < 32 ? a2 : b2;
+  }
+  unsigned long long lo = (unsigned long long)w0 | ((unsigned long long)w1 << 32);
+  unsigned long long field = lo >> s;
+  if (s + w > 64) field |= (unsigned long long)w2 << (64 - s);
+  long long m = (long long)(field << (64 - w)) >> (64 - w);
+  return i2d(m, w) * pow2(E - (w - 1));
+}
+
+__device__ __forceinline__ double invd2(const Coefs& cf, int P, int n, int x, int y) {
+  return (unk1(x, n) && unk1(y, n)) ? cf.invd[(y % P) * P + x % P] : 0.0;
+}
+
+// The A march: input rows y' = ys-P .. ye+P-1 are staged
+// (stage(y', slot), async or not), optionally transformed in place
+// (xform(y', slot)), x-passed (a = Mx u, b = Kx u) into the register ring;
+// out(y, Au, slot_of_row_y) runs for every output row y in [ys, ye).
+template <int P, class Stage, class Xform, class Pre, class Out>
+__device__ __forceinline__ void march_A(const Coefs& cf, int ys, int ye, int x, double* ring, Stage stage, Xform xform,
+                                        Pre pre, Out out) {
+  constexpr int R = 2 * P + 1;
+  const int lane = threadIdx.x;
+  const int tx = x % P;
+  double km[R], kk[R], ra[R], rb[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) {
+    km[o] = cf.Mc[tx][o];
+    kk[o] = cf.Kc[tx][o];
+    ra[o] = 0.0;
+    rb[o] = 0.0;
+  }
+  const int nin = (ye - ys) + 2 * P, y0 = ys - P;
+  using AuxT = decltype(pre(0));
+  AuxT cur{}, nxt{};
+#pragma unroll
+  for (int i = 0; i < MPF; ++i) {
+    if (i < nin) stage(y0 + i, ring + (i % MNB) * MSLOT);
+    cp_commit();
+  }
+  for (int i = 0; i < nin; ++i) {
+    if (i + MPF < nin) stage(y0 + i + MPF, ring + ((i + MPF) % MNB) * MSLOT);
+    cp_commit();
+    // register prefetch of the per-row operands of the next output row
+    if (i >= 2 * P - 1 && i + 1 < nin) nxt = pre(y0 + i + 1 - P);
+    cp_wait<MPF>();
+    __syncwarp();
+    double* row = ring + (i % MNB) * MSLOT;
+    xform(y0 + i, row);
+    double s = 0.0, t = 0.0;
+#pragma unroll
+    for (int o = 0; o < R; ++o) {
+      const double v = row[lane + o];
+      s = fma(km[o], v, s);
+      t = fma(kk[o], v, t);
+    }
+#pragma unroll
+    for (int o = 0; o < R - 1; ++o) {
+      ra[o] = ra[o + 1];
+      rb[o] = rb[o + 1];
+    }
+    ra[R - 1] = s;
+    rb[R - 1] = t;
+    if (i >= 2 * P) {
+      const int y = y0 + i - P;
+      const int ty = y % P;
+      double d = 0.0, e = 0.0;
+#pragma unroll
+      for (int o = 0; o < R; ++o) {
+        d = fma(cf.Kc[ty][o], ra[o], d);
+        e = fma(cf.Mc[ty][o], rb[o], e);
+      }
+      out(y, d + e, ring + ((i - P) % MNB) * MSLOT, cur);
+    }
+    cur = nxt;
+    __syncwarp();
+  }
+}
+
+struct NoAux {};
+struct RAux {  // r_l block words / exponent
+  uint32_t w0, w1;
+  int e;
+};
+struct CAux {  // Chebyshev operands of one output row
+  double b, dv, z, pu;
+  uint32_t w0, w1;
+  int e;
+};
+
+// ------------------------------------------------------------ kernels --
+// u_l = dec ú_l + P_l u_{l-1} (decode sweep S2)
+template <int P>
+__global__ void __launch_bounds__(32 * MW, 3) k_m_decode(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  const DevCtx& c = *cp;
+  const LevelDev& lv = c.lv[a.l];
+  const LevelDev& lp = c.lv[a.l - 1 >= 0 ? a.l - 1 : 0];
+  const int lane = threadIdx.x, x = it.x0 + lane, nxb = lv.g.NX >> 5;
+  for (int y = it.ys; y < it.ye; ++y) {
+    const long long blk = (long long)y * nxb + (it.x0 >> 5);
+    const double pu = a.l > 0 ? prolong_at<P>(cf, lp.U, lp.g, lv.g.n, x, y) : 0.0;
+    const double dv = warp_decode(lv.umant + blk * lv.ustride, lv.uexp[blk], a.wu_in, lane);
+    lv.U[(long long)y * lv.g.NX + x] = dv + pu;
+  }
+}
+
+// t_L = f_L - A_L u_L, r_L = enc(t_L), ||t_L||^2 partial
+template <int P>
+__global__ void __launch_bounds__(32 * MW, 3) k_m_residual(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
+  extern __shared__ double msm[];
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  const DevCtx& c = *cp;
+  const LevelDev& lv = c.lv[a.l];
+  const Geom g = lv.g;
+  const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
+  double* ring = msm + threadIdx.y * (MNB * MSLOT);
+  const double* __restrict__ U = lv.U;
+  const double* __restrict__ gt = lv.gtab;
+  const double gx = unk1(x, g.n) ? cf.rhs_c * gt[x] : 0.0;
+  double ss = 0.0;
+  march_A<P>(
+      cf, it.ys, it.ye, x, ring,
+      [&](int yy, double* slot) {
+        stage_row(U, g, it.x0, yy, P, slot, lane);
+        if (lane == 0) {
+          const bool ok = yy >= 0 && yy < g.n;
+          cpa8(slot + 32 + 2 * P, ok ? gt + yy : gt, ok);  // g_l(y') for the RHS
+        }
+      },
+      [&](int, double*) {}, [&](int) { return NoAux{}; },
+      [&](int y, double au, const double* slot, const NoAux&) {
+        const bool unk = unk1(x, g.n) && unk1(y, g.n);
+        const double f = gx * slot[32 + 2 * P];  // ((C g(x)) g(y))
+        const double t = unk ? f - au : 0.0;
+        lv.T[(long long)y * g.NX + x] = t;
+        ss = fma(t, t, ss);
+        const long long blk = (long long)y * nxb + (it.x0 >> 5);
+        warp_encode(t, a.wr, lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
+      });
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+  if (lane == 0 && a.poff >= 0) c.pbase[a.poff + it.item] = ss;
+}
+
+// t_l = R_{l+1} t_{l+1} (restricts t, not r: PAPER.md:742-744), r_l = enc(t_l).
+// The warp owns 32 coarse columns; every coarse row consumes two fine rows.
+template <int P>
+__global__ void __launch_bounds__(32 * MW, 3) k_m_restrict(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
+  extern __shared__ double msm[];
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  constexpr int NS = 4 * P - 1, H = 2 * P - 1;
+  const DevCtx& c = *cp;
+  const LevelDev& lc_ = c.lv[a.l];
+  const LevelDev& lf = c.lv[a.l + 1];
+  const Geom gc = lc_.g, gf = lf.g;
+  const int lane = threadIdx.x, xc = it.x0 + lane, nxb = gc.NX >> 5;
+  const int txc = xc % P;
+  const int fxs = 2 * it.x0 - H;  // first staged fine column
+  double* ring = msm + threadIdx.y * (MNB * MSLOT);
+  const double* __restrict__ Tf = lf.T;
+  double rw[NS], rv[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    rw[s] = cf.Rw[txc][s];
+    rv[s] = 0.0;
+  }
+  // fine row f staged as columns fxs .. fxs + 64 + 2H - 1
+  auto stage = [&](int fy, double* slot) {
+    const bool rowok = fy >= 0 && fy < gf.NY;
+    const double* rp = Tf + (long long)(rowok ? fy : 0) * gf.NX;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int j = lane + 32 * k;
+      if (j < 64 + 2 * H) {
+        const int fx = fxs + j;
+        const bool ok = rowok && fx >= 0 && fx < gf.NX;
+        cpa8(slot + j, ok ? rp + fx : Tf, ok);
+      }
+    }
+  };
+  const int fy0 = 2 * it.ys - H, nin = 2 * (it.ye - it.ys) + 2 * H;
+  double ss = 0.0;
+#pragma unroll
+  for (int i = 0; i < MPF; ++i) {
+    if (i < nin) stage(fy0 + i, ring + (i % MNB) * MSLOT);
+    cp_commit();
+  }
+  for (int i = 0; i < nin; ++i) {
+    if (i + MPF < nin) stage(fy0 + i + MPF, ring + ((i + MPF) % MNB) * MSLOT);
+    cp_commit();
+    cp_wait<MPF>();
+    __syncwarp();
+    const double* row = ring + (i % MNB) * MSLOT;
+    double v = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) v = fma(rw[s], row[2 * lane + s], v);  // (t = +0 at fine non-unknowns)
+#pragma unroll
+    for (int s = 0; s < NS - 1; ++s) rv[s] = rv[s + 1];
+    rv[NS - 1] = v;
+    if (i >= NS - 1 && ((i - (NS - 1)) & 1) == 0) {
+      const int yc = it.ys + (i - (NS - 1)) / 2;
+      const int tyc = yc % P;
+      double t = 0.0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) t = fma(cf.Rw[tyc][s], rv[s], t);
+      t = (unk1(xc, gc.n) && unk1(yc, gc.n)) ? t : 0.0;
+      lc_.T[(long long)yc * gc.NX + xc] = t;
+      ss = fma(t, t, ss);
+      const long long blk = (long long)yc * nxb + (it.x0 >> 5);
+      warp_encode(t, a.wr, lc_.rmant + blk * lc_.rstride, lc_.rexp + blk, lane, c.status);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+  if (lane == 0 && a.poff >= 0) c.pbase[a.poff + it.item] = ss;
+}
+
+// ý_l = enc(y); w_l = z_l + dec ý_l (l < L); ú_l = enc(dec ú_l + dec ý_l);
+// u_l = dec ú_l + P u_{l-1}
+__device__ __forceinline__ void m_finalize(const DevCtx& c, const MArgs& a, const LevelDev& lv, long long idx,
+                                           long long blk, double y, double zc, double pu, int lane) {
+  const double yq = warp_encode(y, a.wr, nullptr, nullptr, lane, c.status);
+  if (a.l < a.L) lv.W[idx] = zc + yq;
+  uint32_t* uw = lv.umant + blk * lv.ustride;
+  const double uo = warp_decode(uw, lv.uexp[blk], a.wu_in, lane);
+  const double uq = warp_encode(uo + yq, a.wu_out, uw, lv.uexp + blk, lane, c.status);
+  lv.U[idx] = uq + pu;
+}
+
+// m_finalize with the ú words / exponent and z, P u prefetched into registers
+__device__ __forceinline__ void m_finalize_r(const DevCtx& c, const MArgs& a, const LevelDev& lv, long long idx,
+                                             long long blk, double y, double zc, double pu, uint32_t w0, uint32_t w1,
+                                             int e, int lane) {
+  const double yq = warp_encode(y, a.wr, nullptr, nullptr, lane, c.status);
+  if (a.l < a.L) lv.W[idx] = zc + yq;
+  const double uo = warp_decode_r(w0, e, a.wu_in, lane, w1);
+  const double uq = warp_encode(uo + yq, a.wu_out, lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
+  lv.U[idx] = uq + pu;
+}
+
+// Chebyshev step 1 with the prolongation fused:
+// z_l = P w_{l-1} computed on the staged rows, b = dec r_l - A z_l;
+// stores Z (l < L), PU = P u_{l-1}, B; k == 1 finalises directly.
+template <int P>
+__global__ void __launch_bounds__(32 * MW, 3) k_m_cfas1(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
+  extern __shared__ double msm[];
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  const DevCtx& c = *cp;
+  const LevelDev& lv = c.lv[a.l];
+  const LevelDev& lp = c.lv[a.l - 1];
+  const Geom g = lv.g, gp = lp.g;
+  const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
+  double* ring = msm + threadIdx.y * (MNB * MSLOT);
+  const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);  // halo column of lanes < 2P
+  march_A<P>(
+      cf, it.ys, it.ye, x, ring,
+      [&](int yy, double* slot) {
+        // z row yy on the block columns and the x halo (0 outside the level)
+        const double zm = (yy >= 0 && yy < g.NY) ? prolong_at<P>(cf, lp.W, gp, g.n, x, yy) : 0.0;
+        slot[P + lane] = zm;
+        if (lane < 2 * P) {
+          const double zh = (yy >= 0 && yy < g.NY && xh >= 0 && xh < g.NX) ? prolong_at<P>(cf, lp.W, gp, g.n, xh, yy)
+                                                                            : 0.0;
+          slot[lane < P ? lane : 32 + lane] = zh;
+        }
+        if (yy >= it.ys && yy < it.ye) {
+          const long long idx = (long long)yy * g.NX + x;
+          if (a.l < a.L) c.Z[idx] = zm;
+          c.PU[idx] = prolong_at<P>(cf, lp.U, gp, g.n, x, yy);
+        }
+      },
+      [&](int, double*) {},
+      [&](int yn) {
+        const long long blk = (long long)yn * nxb + (it.x0 >> 5);
+        RAux r;
+        r.w0 = lane < a.wr ? lv.rmant[blk * lv.rstride + lane] : 0u;
+        r.w1 = lane + 32 < a.wr ? lv.rmant[blk * lv.rstride + lane + 32] : 0u;
+        r.e = lv.rexp[blk];
+        return r;
+      },
+      [&](int y, double az, const double* slot, const RAux& r) {
+        const long long idx = (long long)y * g.NX + x, blk = (long long)y * nxb + (it.x0 >> 5);
+        const double rv = warp_decode_r(r.w0, r.e, a.wr, lane, r.w1);
+        const double b = rv - az;
+        if (a.last) {  // k == 1: y = d_1 = inv_theta (invD b)
+          const double d = cf.inv_theta * (invd2(cf, P, g.n, x, y) * b);
+          m_finalize(c, a, lv, idx, blk, d, slot[P + lane], c.PU[idx], lane);
+        } else {
+          c.B[idx] = b;
+        }
+      });
+}
+
+// Chebyshev step j >= 2: q = b - A y; d_j = fma(alpha_j, d_{j-1}, beta_j (invD q));
+// y_j = y_{j-1} + d_j.  Step 2 stages b and forms
+// y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
+template <int P>
+__global__ void __launch_bounds__(32 * MW, 3) k_m_cheb(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
+  extern __shared__ double msm[];
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  const DevCtx& c = *cp;
+  const LevelDev& lv = c.lv[a.l];
+  const Geom g = lv.g;
+  const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
+  const int j = a.step;
+  double* ring = msm + threadIdx.y * (MNB * MSLOT);
+  const double* __restrict__ src = (j == 2) ? c.B : c.Y[(j - 1) & 1];
+  const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);
+  const double al = cf.cal[j - 1], be = cf.cbe[j - 1];
+  march_A<P>(
+      cf, it.ys, it.ye, x, ring, [&](int yy, double* slot) { stage_row(src, g, it.x0, yy, P, slot, lane); },
+      [&](int yy, double* slot) {
+        if (j != 2) return;
+        // y_1 = inv_theta (invD b) on the lane's own staged entries
+        slot[P + lane] = cf.inv_theta * (invd2(cf, P, g.n, x, yy) * slot[P + lane]);
+        if (lane < 2 * P) {
+          double& v = slot[lane < P ? lane : 32 + lane];
+          v = cf.inv_theta * (invd2(cf, P, g.n, xh, yy) * v);
+        }
+        __syncwarp();
+      },
+      [&](int yn) {
+        const long long idx = (long long)yn * g.NX + x, blk = (long long)yn * nxb + (it.x0 >> 5);
+        CAux q{};
+        q.b = c.B[idx];
+        if (j > 2) q.dv = c.Dv[idx];
+        if (a.last) {
+          q.z = a.l < a.L ? c.Z[idx] : 0.0;
+          q.pu = c.PU[idx];
+          q.w0 = lane < a.wu_in ? lv.umant[blk * lv.ustride + lane] : 0u;
+          q.w1 = lane + 32 < a.wu_in ? lv.umant[blk * lv.ustride + lane + 32] : 0u;
+          q.e = lv.uexp[blk];
+        }
+        return q;
+      },
+      [&](int y, double ay, const double* slot, const CAux& p) {
+        const long long idx = (long long)y * g.NX + x, blk = (long long)y * nxb + (it.x0 >> 5);
+        const double q = p.b - ay;
+        const double yprev = slot[P + lane];
+        const double dprev = (j == 2) ? yprev : p.dv;
+        const double d = fma(al, dprev, be * (invd2(cf, P, g.n, x, y) * q));
+        const double yv = yprev + d;
+        if (a.last) {
+          m_finalize_r(c, a, lv, idx, blk, yv, p.z, p.pu, p.w0, p.w1, p.e, lane);
+        } else {
+          c.Y[j & 1][idx] = yv;
+          c.Dv[idx] = d;
+        }
+      });
+}
+
+// ------------------------------------------------------------------ host --
+int march_smem() { return MW * MNB * MSLOT * 8; }
+int march_warps() { return MW; }
+
+#define M_DISPATCH(p, F)   \
+  do {                     \
+    if (p == 1) { F(1); }  \
+    else if (p == 2) { F(2); } \
+    else { F(3); }         \
+  } while (0)
+
+void march_set_attributes() {
+#define F(P)                                                                                            \
+  cudaFuncSetAttribute(k_m_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());     \
+  cudaFuncSetAttribute(k_m_restrict<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());     \
+  cudaFuncSetAttribute(k_m_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());        \
+  cudaFuncSetAttribute(k_m_cheb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());
+  F(1) F(2) F(3)
+#undef F
+}
+
+template <typename K>
+static void m_launch(K kernel, int nitems, int smem, cudaStream_t st, const DevCtx* c, const MArgs& a,
+                     const Coefs& cf) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((nitems + MW - 1) / MW);
+  cfg.blockDim = dim3(32, MW);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, c, a, cf);
+}
+
+void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf) {
+  const DevCtx* c = (const DevCtx*)devctx;
+  const int sm = march_smem();
+#define F(P)                                                                            \
+  switch (a.type) {                                                                     \
+    case OP_DECODE: m_launch(k_m_decode<P>, a.nitems, 0, st, c, a, cf); break;          \
+    case OP_RESIDUAL: m_launch(k_m_residual<P>, a.nitems, sm, st, c, a, cf); break;     \
+    case OP_RESTRICT: m_launch(k_m_restrict<P>, a.nitems, sm, st, c, a, cf); break;     \
+    case OP_CFAS1: m_launch(k_m_cfas1<P>, a.nitems, sm, st, c, a, cf); break;           \
+    default: m_launch(k_m_cheb<P>, a.nitems, sm, st, c, a, cf); break;                  \
+  }
+  M_DISPATCH(p, F);
+#undef F
+}
+
+}  // namespace fmg
