@@ -64,8 +64,9 @@ struct fmg_ctx {
   double* Ul[kMaxLev]{};          // per-level u_l, t_l, w_l (padded level layout)
   double* Tl[kMaxLev]{};
   double* Wl[kMaxLev]{};
-  bool march = false;             // 2D grid levels run the row-march kernels (fmg_march.cu)
-  int mrc[kMaxLev]{}, mitems[kMaxLev]{};  // march rows per chunk, work items per level
+  bool march = false;             // grid levels run the march kernels (fmg_march.cu 2D, fmg_march3.cu 3D)
+  int mrc[kMaxLev]{}, mitems[kMaxLev]{};  // march rows / planes per chunk, work items (3D: CTAs) per level
+  int mnyb[kMaxLev]{};
   fmg_alloc_fn afn = nullptr;
   fmg_free_fn ffn = nullptr;
   void* auser = nullptr;
@@ -122,7 +123,8 @@ struct Builder {
   long long ptot = 0;  // (set past the KC partial region by make_builder)
   // reserve partial slots for (row, level l) and record the deferred norm
   long long slot(int row, int l) {
-    int nt = c->march ? c->mitems[l] : c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2];
+    int nt = !c->march ? c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2]
+                       : (c->dim == 2 ? c->mitems[l] : c->mitems[l] * march3_rows());
     long long off = ptot;
     ptot += nt;
     NormEntry e{off, row, l, nt, 0};
@@ -232,6 +234,10 @@ void build_iteration(Builder& b, int L, int it) {
   }
   const int k = c->s.cheb_degree;
   for (int l = lc + 1; l <= L; ++l) {
+    if (c->march && c->dim == 3) {  // z_l = P w_{l-1}, P u_{l-1} (fmg_march3.cu k_m3_prolong)
+      OpDesc q = mkop(OP_PROLONG, l, L);
+      b.grid(q);
+    }
     for (int step = 1; step <= k; ++step) {
       OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
       q.step = step;
@@ -348,8 +354,11 @@ void issue(fmg_ctx* c, const Builder& b) {
         m.nxb = c->g[o.l].NX / 32;
         m.nitems = c->mitems[o.l];
         m.NYo = c->g[o.l].NY;
+        m.nyb = c->mnyb[o.l];
+        m.NZo = c->g[o.l].NZ;
         m.poff = o.poff;
-        launch_march(c->p, c->cur, c->devctx, m, c->cf);
+        if (c->dim == 2) launch_march(c->p, c->cur, c->devctx, m, c->cf);
+        else launch_march3(c->p, c->cur, c->devctx, m, c->cf);
       } else {
         int tx = 1, ty = 1, tz = 1;
         if (it.op.type != OP_NORMS) {
@@ -464,7 +473,8 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) { delete c; return FMG_ECUDA; }
   set_kernel_attributes();
   march_set_attributes();
-  c->march = dim == 2 && !(getenv("FMG_MARCH") && atoi(getenv("FMG_MARCH")) == 0);
+  march3_set_attributes();
+  c->march = !(getenv("FMG_MARCH") && atoi(getenv("FMG_MARCH")) == 0);
   if (getenv("FMG_SYNC_DEBUG")) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fprintf(stderr, "[fmg] set_kernel_attributes: %s\n", cudaGetErrorString(e));
@@ -501,13 +511,25 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     cudaMemcpy(c->gtab[l], gt.data(), sizeof(double) * g.n, cudaMemcpyHostToDevice);
     c->part_off[l] = tot_parts;
     tot_parts += nt;
-    // 2D row march: ~3600 warps of work (148 SMs x 24 warps) per full level
     int nxb = g.NX / 32;
-    long long want = 148LL * 24;
-    int rc = (int)(((long long)g.NY * nxb + want - 1) / want);
-    rc = std::max(1, std::min(rc, g.NY));
-    c->mrc[l] = rc;
-    c->mitems[l] = nxb * ((g.NY + rc - 1) / rc);
+    if (dim == 2) {
+      // 2D row march: ~3600 warps of work (148 SMs x 24 warps) per full level
+      long long want = 148LL * 24;
+      int rc = (int)(((long long)g.NY * nxb + want - 1) / want);
+      rc = std::max(1, std::min(rc, g.NY));
+      c->mrc[l] = rc;
+      c->mitems[l] = nxb * ((g.NY + rc - 1) / rc);
+    } else {
+      // 3D plane march: CTAs of 32 x 8 columns, ~4 waves of 2 CTAs per SM
+      int nyb = (g.NY + march3_rows() - 1) / march3_rows();
+      int tiles = nxb * nyb;
+      int nch = std::max(1, std::min(g.NZ, (148 * 2 * 4 + tiles - 1) / tiles));
+      int rc = (g.NZ + nch - 1) / nch;
+      nch = (g.NZ + rc - 1) / rc;
+      c->mnyb[l] = nyb;
+      c->mrc[l] = rc;
+      c->mitems[l] = tiles * nch;
+    }
   }
   // KC (one thread-block cluster, fmg_kc.cu) owns levels 0..lc: the largest
   // prefix with <= 2 BFP blocks per KC warp whose data fits the cluster's

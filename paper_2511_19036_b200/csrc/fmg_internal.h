@@ -45,7 +45,7 @@ int coarse_count(int dim, int p);
 int build_coarse_inverse(int dim, int p, double* Ainv);  // 0 on success
 
 // Operation descriptors (mirrors the device Op).
-enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_CFAS1 = 6, OP_CHEB };
+enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_CFAS1 = 6, OP_CHEB, OP_PROLONG };
 struct OpDesc {
   int type, l, L, step, last;
   int wr, wu_in, wu_out;
@@ -57,7 +57,8 @@ struct OpDesc {
 struct MArgs {
   int type, l, L, step, last;
   int wr, wu_in, wu_out;
-  int RC, nxb, nitems, NYo;  // rows per chunk, block columns, work items, output rows
+  int RC, nxb, nitems, NYo;  // rows (2D) / planes (3D) per chunk, block columns, work items (3D: CTAs), output rows
+  int nyb, NZo;              // 3D: tile rows (of 8), output planes
   long long poff;            // norm partials (one per item) at pbase + poff, or -1
 };
 
@@ -132,6 +133,9 @@ void pack_op(void* dst, const OpDesc& od);
 void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int tx, int ty, int tz);
 void march_set_attributes();
 void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);
+void march3_set_attributes();
+int march3_rows();
+void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);
 int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* rst, int n_ir, int lc_cap,
             KcLayout* ly, int* lc_out, int* cs_out);
 int kc_warps_per_cta();
