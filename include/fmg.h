@@ -76,6 +76,20 @@ int fmg_set_allocator(fmg_alloc_fn alloc, fmg_free_fn free_fn, void* user);
  * or < 2, bad dim/p/levels/schedule), FMG_ENOMEM, FMG_ECUDA. */
 int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, fmg_ctx** out);
 
+/* z-slab decomposition emulated on ONE device: a
+ * group of `nslabs` sub-contexts (3D only), each computing the planes
+ * [r NZ_l/G, (r+1) NZ_l/G) of every grid level l > lc, with the ghost planes
+ * each stencil consumer needs copied from the owning sub-context (device to
+ * device, on the group stream) and t_{lc+1} gathered before the replicated
+ * coarse-hierarchy kernel.  The same exchange plan a multi-GPU run performs
+ * over NVLink; its results are bit-identical to fmg_create (decomposition
+ * invariance).  Supports fmg_solve / fmg_solve_async / fmg_solve_upto /
+ * fmg_norms / fmg_get_section / fmg_info / fmg_destroy (others: FMG_EINVAL).
+ * Errors: FMG_EINVAL (dim != 3, a slab level with NZ_l % nslabs != 0), as
+ * fmg_create otherwise. */
+int fmg_create_slabs(int dim, int p, int levels, const fmg_schedule* s, int nslabs, void* stream,
+                     fmg_ctx** out);
+
 /* Alg 3.3 from scratch: coarse solve, then for L = 1..levels-1
  * push a level and run N x {fmgResidual, cFas V(0,1), correction}.  Enqueues one
  * CUDA graph on the context stream and returns without waiting (asynchronous).

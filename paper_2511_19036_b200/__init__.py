@@ -46,6 +46,7 @@ _dp = C.POINTER(C.c_double)
 _lib.fmg_strerror.restype = C.c_char_p
 _lib.fmg_strerror.argtypes = [C.c_int]
 _lib.fmg_create.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule), _vp, C.POINTER(_vp)]
+_lib.fmg_create_slabs.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule), C.c_int, _vp, C.POINTER(_vp)]
 _lib.fmg_solve.argtypes = [_vp]
 _lib.fmg_solve_async.argtypes = [_vp]
 _lib.fmg_solve_upto.argtypes = [_vp, C.c_int, C.c_int]
@@ -74,7 +75,7 @@ _ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
 _FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p)
 _lib.fmg_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, C.c_void_p]
 
-EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_solve_async", "fmg_solve", "fmg_solve_upto",
+EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_create_slabs", "fmg_solve_async", "fmg_solve", "fmg_solve_upto",
            "fmg_norms", "fmg_residual", "fmg_get_solution", "fmg_errors", "fmg_get_section",
            "fmg_info", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_kernel_times", "fmg_destroy",
            "fmg_rhs_size", "fmg_set_rhs", "fmg_get_rhs", "fmg_export_solution",
@@ -122,7 +123,7 @@ class Solver:
     """A compact-FMG context (fmg_create ... fmg_destroy)."""
 
     def __init__(self, dim: int, p: int, levels: int, schedule: Schedule | dict | None = None,
-                 stream=None):
+                 stream=None, slabs: int = 1):
         if schedule is None:
             from fmg_inputs import default_schedule
             schedule = default_schedule(dim, p)
@@ -131,8 +132,12 @@ class Solver:
         self.dim, self.p, self.levels, self.schedule = dim, p, levels, schedule
         self.stream = stream
         h = C.c_void_p()
-        _check(_lib.fmg_create(dim, p, levels, C.byref(schedule), _stream_ptr(stream), C.byref(h)),
-               "fmg_create")
+        if slabs > 1:  # virtual z slabs on one device (fmg_create_slabs)
+            _check(_lib.fmg_create_slabs(dim, p, levels, C.byref(schedule), slabs, _stream_ptr(stream),
+                                         C.byref(h)), "fmg_create_slabs")
+        else:
+            _check(_lib.fmg_create(dim, p, levels, C.byref(schedule), _stream_ptr(stream), C.byref(h)),
+                   "fmg_create")
         self._h = h
 
     def close(self):

@@ -67,6 +67,12 @@ struct fmg_ctx {
   bool march = false;             // grid levels run the march kernels (fmg_march.cu 2D, fmg_march3.cu 3D)
   int mrc[kMaxLev]{}, mitems[kMaxLev]{};  // march rows / planes per chunk, work items (3D: CTAs) per level
   int mnyb[kMaxLev]{};
+  // z-slab decomposition (3D): this context computes planes
+  // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
+  // exchanged before each stencil consumer, t_{lc+1} is gathered before KC)
+  int G = 1, rank = 0;
+  int zlo[kMaxLev]{}, zhi[kMaxLev]{};
+  std::vector<fmg_ctx*> sub;      // virtual slabs: G sub-contexts driven in lockstep (group handle)
   fmg_alloc_fn afn = nullptr;
   fmg_free_fn ffn = nullptr;
   void* auser = nullptr;
@@ -110,11 +116,13 @@ Launch L_(fmg_ctx* c) { return Launch{c->dim, c->p, c->cur}; }
 // level, or one launch of the coarse-hierarchy cluster kernel KC (levels
 // 0..lc).  DESIGN.md §4.
 struct Item {
-  int kind;          // 0 grid op, 1 KC
+  int kind;          // 0 grid op, 1 KC, 2 ghost-plane exchange / gather (z slabs)
   OpDesc op;         // grid item
   KcDesc kc;         // KC item
   int timed_cls;     // kernel-timing class of a grid item (-1: none)
+  int xarr, xl, xdepth, xgather;  // exchange item: array, level, ghost depth, gather-all
 };
+enum { XA_U = 0, XA_T, XA_W, XA_Z, XA_B, XA_Y0, XA_Y1 };
 
 struct Builder {
   fmg_ctx* c;
@@ -136,6 +144,18 @@ struct Builder {
     it.kind = 0;
     it.op = op;
     it.timed_cls = cls;
+    items.push_back(it);
+  }
+  // ghost planes of array `arr` at slab level l (l > lc) before a stencil consumer
+  void xchg(int arr, int l, int depth, int gather = 0) {
+    if (c->G <= 1 || l <= c->lc) return;
+    Item it{};
+    it.kind = 2;
+    it.xarr = arr;
+    it.xl = l;
+    it.xdepth = depth;
+    it.xgather = gather;
+    it.timed_cls = -1;
     items.push_back(it);
   }
   void kc(const KcDesc& d) {
@@ -207,13 +227,16 @@ void build_iteration(Builder& b, int L, int it) {
   const int lc = c->lc;
   const bool fine = L == c->Lmax;
   const int row = L * c->s.n_ir + it;
+  const int P = c->p;
   if (L > lc) {
+    b.xchg(XA_U, L, P);
     OpDesc o = mkop(OP_RESIDUAL, L, L);
     o.wr = wr(c, L, L);
     o.row = row;
     o.poff = b.slot(row, L);
     b.grid(o, fine ? 0 : -1);
     for (int l = L - 1; l > lc; --l) {
+      b.xchg(XA_T, l + 1, 2 * P - 1);
       OpDesc q = mkop(OP_RESTRICT, l, L);
       q.wr = wr(c, l, L);
       q.row = row;
@@ -221,7 +244,9 @@ void build_iteration(Builder& b, int L, int it) {
       b.grid(q, (fine && l == L - 1) ? 3 : -1);
     }
   }
-  // levels 0..lc: KC (restriction tail, coarse solve, cFas + correction)
+  // levels 0..lc: KC (restriction tail, coarse solve, cFas + correction);
+  // with z slabs every rank runs it on the gathered t_{lc+1} (replicated)
+  if (L > lc) b.xchg(XA_T, lc + 1, 0, 1);
   KcDesc d = mkkc(c, 1);
   d.L = L;
   d.it = it;
@@ -235,10 +260,14 @@ void build_iteration(Builder& b, int L, int it) {
   const int k = c->s.cheb_degree;
   for (int l = lc + 1; l <= L; ++l) {
     if (c->march && c->dim == 3) {  // z_l = P w_{l-1}, P u_{l-1} (fmg_march3.cu k_m3_prolong)
+      b.xchg(XA_W, l - 1, P);
+      b.xchg(XA_U, l - 1, P);
       OpDesc q = mkop(OP_PROLONG, l, L);
       b.grid(q);
+      b.xchg(XA_Z, l, P);
     }
     for (int step = 1; step <= k; ++step) {
+      if (step >= 2) b.xchg(step == 2 ? XA_B : ((step - 1) & 1 ? XA_Y1 : XA_Y0), l, P);
       OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
       q.step = step;
       q.last = step == k;
@@ -279,6 +308,7 @@ void build_solve(Builder& b, int Lstop, int iters_last) {
     // ú_{0..L-1} is value-preserving and happens at the next encode.
     c->wu_cur[L] = wu(c, L, L);
     // u_L = dec ú_L + P u_{L-1} = P u_{L-1} for the first residual
+    b.xchg(XA_U, L - 1, c->p);
     OpDesc o = mkop(OP_DECODE, L, L);
     o.wu_in = c->wu_cur[L];
     b.grid(o, (L == c->Lmax) ? 2 : -1);
@@ -323,6 +353,92 @@ int prepare(fmg_ctx* c, const Builder& b, int slot) {
   return FMG_OK;
 }
 
+// Launch one op / KC item of the list on c->cur.
+void issue_item(fmg_ctx* c, const Item& it) {
+  if (it.kind == 1) {
+    mark(c, -2);
+    launch_kc(c->dim, c->p, c->cur, c->devctx, it.kc, c->kc_cluster, c->kcl.bytes);
+    mark(c, -2);
+  } else {
+    mark(c, it.timed_cls);
+    if (c->march) {
+      const OpDesc& o = it.op;
+      MArgs m{};
+      m.type = o.type;
+      m.l = o.l;
+      m.L = o.L;
+      m.step = o.step;
+      m.last = o.last;
+      m.wr = o.wr;
+      m.wu_in = o.wu_in;
+      m.wu_out = o.wu_out;
+      m.RC = c->mrc[o.l];
+      m.nxb = c->g[o.l].NX / 32;
+      m.nitems = c->mitems[o.l];
+      m.NYo = c->g[o.l].NY;
+      m.nyb = c->mnyb[o.l];
+      m.NZo = c->g[o.l].NZ;
+      m.zlo = c->zlo[o.l];
+      m.zhi = c->zhi[o.l];
+      m.poff = o.poff;
+      if (c->dim == 2) launch_march(c->p, c->cur, c->devctx, m, c->cf);
+      else launch_march3(c->p, c->cur, c->devctx, m, c->cf);
+    } else {
+      int tx = 1, ty = 1, tz = 1;
+      if (it.op.type != OP_NORMS) {
+        tx = c->tiles[it.op.l][0];
+        ty = c->tiles[it.op.l][1];
+        tz = c->tiles[it.op.l][2];
+      }
+      launch_op(c->dim, c->p, c->cur, c->devctx, it.op, tx, ty, tz);
+    }
+    mark(c, it.timed_cls);
+  }
+  c->launches++;
+}
+
+// FP64 level array of an exchange item
+double* xarray(fmg_ctx* c, int arr, int l) {
+  switch (arr) {
+    case XA_U: return c->Ul[l];
+    case XA_T: return c->Tl[l];
+    case XA_W: return c->Wl[l];
+    case XA_Z: return c->buf[0];
+    case XA_B: return c->buf[1];
+    case XA_Y0: return c->buf[2];
+    default: return c->buf[3];
+  }
+}
+
+// Virtual z slabs: fill the ghost planes (or, for a gather, every foreign plane)
+// of each sub-context from the sub-context that owns them (D2D copies on the
+// group's stream; the owners computed those planes in the previous item).
+void group_exchange(fmg_ctx* grp, const Item& it) {
+  const int G = (int)grp->sub.size(), l = it.xl;
+  fmg_ctx* s0 = grp->sub[0];
+  const Geom& g = s0->g[l];
+  const size_t plane = (size_t)g.NX * g.NY;
+  const int slab = g.NZ / G;
+  for (int r = 0; r < G; ++r) {
+    fmg_ctx* dst = grp->sub[r];
+    const int zlo = dst->zlo[l], zhi = dst->zhi[l];
+    int ranges[2][2] = {{std::max(0, zlo - it.xdepth), zlo}, {zhi, std::min(g.NZ, zhi + it.xdepth)}};
+    if (it.xgather) {
+      ranges[0][0] = 0;
+      ranges[1][1] = g.NZ;
+    }
+    for (int k = 0; k < 2; ++k) {
+      for (int z = ranges[k][0]; z < ranges[k][1];) {
+        const int owner = z / slab, zend = std::min(ranges[k][1], (owner + 1) * slab);
+        double* d = xarray(dst, it.xarr, l) + (size_t)z * plane;
+        const double* s = xarray(grp->sub[owner], it.xarr, l) + (size_t)z * plane;
+        cudaMemcpyAsync(d, s, sizeof(double) * plane * (zend - z), cudaMemcpyDeviceToDevice, dst->cur);
+        z = zend;
+      }
+    }
+  }
+}
+
 // Issue every item on c->cur (inside a capture or directly), then the deferred norms.
 void issue(fmg_ctx* c, const Builder& b) {
   // FMG_SYNC_DEBUG=1 (direct runs only): synchronise after every launch and
@@ -333,44 +449,8 @@ void issue(fmg_ctx* c, const Builder& b) {
     if (e != cudaSuccess) fprintf(stderr, "[fmg] pending CUDA error before issue: %s\n", cudaGetErrorString(e));
   }
   for (const Item& it : b.items) {
-    if (it.kind == 1) {
-      mark(c, -2);
-      launch_kc(c->dim, c->p, c->cur, c->devctx, it.kc, c->kc_cluster, c->kcl.bytes);
-      mark(c, -2);
-    } else {
-      mark(c, it.timed_cls);
-      if (c->march) {
-        const OpDesc& o = it.op;
-        MArgs m{};
-        m.type = o.type;
-        m.l = o.l;
-        m.L = o.L;
-        m.step = o.step;
-        m.last = o.last;
-        m.wr = o.wr;
-        m.wu_in = o.wu_in;
-        m.wu_out = o.wu_out;
-        m.RC = c->mrc[o.l];
-        m.nxb = c->g[o.l].NX / 32;
-        m.nitems = c->mitems[o.l];
-        m.NYo = c->g[o.l].NY;
-        m.nyb = c->mnyb[o.l];
-        m.NZo = c->g[o.l].NZ;
-        m.poff = o.poff;
-        if (c->dim == 2) launch_march(c->p, c->cur, c->devctx, m, c->cf);
-        else launch_march3(c->p, c->cur, c->devctx, m, c->cf);
-      } else {
-        int tx = 1, ty = 1, tz = 1;
-        if (it.op.type != OP_NORMS) {
-          tx = c->tiles[it.op.l][0];
-          ty = c->tiles[it.op.l][1];
-          tz = c->tiles[it.op.l][2];
-        }
-        launch_op(c->dim, c->p, c->cur, c->devctx, it.op, tx, ty, tz);
-      }
-      mark(c, it.timed_cls);
-    }
-    c->launches++;
+    if (it.kind == 2) continue;  // (single context: no slabs)
+    issue_item(c, it);
     if (dbg) {
       cudaError_t e = cudaStreamSynchronize(c->cur);
       if (e == cudaSuccess) e = cudaGetLastError();
@@ -383,6 +463,22 @@ void issue(fmg_ctx* c, const Builder& b) {
   }
   launch_norms_all(c->cur, c->devctx, c->nent[c->nent_slot], (int)b.norms.size());
   c->launches++;
+}
+
+// Group (virtual slabs): every item on every sub-context in rank order, the
+// exchanges in between, all on one stream (no cross-launch waiting).
+void issue_group(fmg_ctx* grp, const Builder& b) {
+  for (const Item& it : b.items) {
+    if (it.kind == 2) {
+      group_exchange(grp, it);
+      continue;
+    }
+    for (fmg_ctx* s : grp->sub) issue_item(s, it);
+  }
+  for (fmg_ctx* s : grp->sub) {
+    launch_norms_all(s->cur, s->devctx, s->nent[s->nent_slot], (int)b.norms.size());
+    s->launches++;
+  }
 }
 
 void zero_sections(fmg_ctx* c) {
@@ -457,7 +553,8 @@ int fmg_set_allocator(fmg_alloc_fn alloc, fmg_free_fn free_fn, void* user) {
   return FMG_OK;
 }
 
-int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, fmg_ctx** out) {
+static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* stream, int G, int rank,
+                       fmg_ctx** out) {
   if (!out || !s) return FMG_EINVAL;
   *out = nullptr;
   if ((dim != 2 && dim != 3) || p < 1 || p > 3 || levels < 1 || levels > kMaxLev) return FMG_EINVAL;
@@ -468,6 +565,8 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
   fmg_ctx* c = new fmg_ctx();
   c->dim = dim; c->p = p; c->levels = levels; c->Lmax = Lmax; c->s = *s;
+  c->G = G;
+  c->rank = rank;
   c->st = (cudaStream_t)stream;
   c->afn = g_alloc; c->ffn = g_free; c->auser = g_alloc_user;
   if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) { delete c; return FMG_ECUDA; }
@@ -519,17 +618,7 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
       rc = std::max(1, std::min(rc, g.NY));
       c->mrc[l] = rc;
       c->mitems[l] = nxb * ((g.NY + rc - 1) / rc);
-    } else {
-      // 3D plane march: CTAs of 32 x 8 columns, ~4 waves of 2 CTAs per SM
-      int nyb = (g.NY + march3_rows() - 1) / march3_rows();
-      int tiles = nxb * nyb;
-      int nch = std::max(1, std::min(g.NZ, (148 * 2 * 4 + tiles - 1) / tiles));
-      int rc = (g.NZ + nch - 1) / nch;
-      nch = (g.NZ + rc - 1) / rc;
-      c->mnyb[l] = nyb;
-      c->mrc[l] = rc;
-      c->mitems[l] = tiles * nch;
-    }
+    }  // (3D march geometry: after the KC plan, per z slab)
   }
   // KC (one thread-block cluster, fmg_kc.cu) owns levels 0..lc: the largest
   // prefix with <= 2 BFP blocks per KC warp whose data fits the cluster's
@@ -544,6 +633,30 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
     }
     if (kc_plan(dim, p, Lmax, c->g, ust, rst, s->n_ir, lc_cap, &c->kcl, &c->lc, &c->kc_cluster)) rc = FMG_ECUDA;
     c->kc_tw = c->kc_cluster * kc_warps_per_cta();
+  }
+  // z slabs: rank r owns planes [r NZ/G, (r+1) NZ/G) of every grid level l > lc
+  for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
+    const Geom& g = c->g[l];
+    if (G > 1 && l > c->lc) {
+      if (dim != 3 || g.NZ % G != 0) rc = FMG_EINVAL;
+      c->zlo[l] = rank * (g.NZ / G);
+      c->zhi[l] = (rank + 1) * (g.NZ / G);
+    } else {
+      c->zlo[l] = 0;
+      c->zhi[l] = g.NZ;
+    }
+    if (dim == 3) {
+      // 3D plane march: CTAs of 32 x 8 columns over this rank's planes, ~4 waves of 2 CTAs per SM
+      const int nxb = g.NX / 32, nz = c->zhi[l] - c->zlo[l];
+      int nyb = (g.NY + march3_rows() - 1) / march3_rows();
+      int tiles = nxb * nyb;
+      int nch = std::max(1, std::min(nz, (148 * 2 * 4 + tiles - 1) / tiles));
+      int rcz = (nz + nch - 1) / nch;
+      nch = (nz + rcz - 1) / rcz;
+      c->mnyb[l] = nyb;
+      c->mrc[l] = rcz;
+      c->mitems[l] = tiles * nch;
+    }
   }
   // FP64 workspace: per-level u_l, t_l, w_l; finest-size Z, B, Y[2], Dv, PU;
   // KC scratch of twice the level-lc size (3D restriction staging).
@@ -635,8 +748,83 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   return FMG_OK;
 }
 
+int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, fmg_ctx** out) {
+  return create_impl(dim, p, levels, s, stream, 1, 0, out);
+}
+
+int fmg_create_slabs(int dim, int p, int levels, const fmg_schedule* s, int nslabs, void* stream, fmg_ctx** out) {
+  if (!out || !s || dim != 3 || nslabs < 1 || nslabs > 64) return FMG_EINVAL;
+  *out = nullptr;
+  fmg_ctx* grp = new fmg_ctx();
+  grp->dim = dim; grp->p = p; grp->levels = levels; grp->Lmax = levels - 1; grp->s = *s;
+  grp->st = (cudaStream_t)stream;
+  grp->G = nslabs;
+  if (cudaStreamCreateWithFlags(&grp->cap, cudaStreamNonBlocking) != cudaSuccess) { delete grp; return FMG_ECUDA; }
+  for (int r = 0; r < nslabs; ++r) {
+    fmg_ctx* sc = nullptr;
+    int rc = create_impl(dim, p, levels, s, stream, nslabs, r, &sc);
+    if (rc != FMG_OK) {
+      fmg_destroy(grp);
+      return rc;
+    }
+    grp->sub.push_back(sc);
+  }
+  grp->lc = grp->sub[0]->lc;
+  *out = grp;
+  return FMG_OK;
+}
+
+// Group (virtual slabs) solve: the item list is built once (identical for all
+// ranks: equal slabs) and issued to every sub-context in lockstep.
+static int group_solve(fmg_ctx* grp, int Lstop, int iters_last, bool graph) {
+  fmg_ctx* s0 = grp->sub[0];
+  Builder b = make_builder(s0);
+  build_solve(b, Lstop, iters_last);
+  for (fmg_ctx* s : grp->sub) {
+    std::memcpy(s->wu_cur, s0->wu_cur, sizeof(s->wu_cur));
+    s->solved_L = Lstop;
+    s->launches = 0;
+    int prc = prepare(s, b, graph ? 0 : 1);
+    if (prc) return prc;
+  }
+  grp->solved_L = Lstop;
+  if (graph) {
+    if (!grp->graph) {
+      for (fmg_ctx* s : grp->sub) s->cur = grp->cap;
+      cudaError_t e = cudaStreamBeginCapture(grp->cap, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return cuda_err(e);
+      for (fmg_ctx* s : grp->sub) zero_sections(s);
+      issue_group(grp, b);
+      cudaGraph_t gr;
+      e = cudaStreamEndCapture(grp->cap, &gr);
+      if (e != cudaSuccess) return cuda_err(e);
+      e = cudaGraphInstantiate(&grp->graph, gr, 0);
+      cudaGraphDestroy(gr);
+      if (e != cudaSuccess) { grp->graph = nullptr; return cuda_err(e); }
+    }
+    cudaError_t e = cudaGraphLaunch(grp->graph, grp->st);
+    return cuda_err(e);
+  }
+  cudaStreamSynchronize(grp->st);
+  for (fmg_ctx* s : grp->sub) {
+    s->cur = grp->st;
+    zero_sections(s);
+  }
+  issue_group(grp, b);
+  return FMG_OK;
+}
+
+static int group_check(fmg_ctx* grp) {
+  for (fmg_ctx* s : grp->sub) {
+    int rc = sync_check(s);
+    if (rc) return rc;
+  }
+  return FMG_OK;
+}
+
 int fmg_solve_async(fmg_ctx* c) {
   if (!c) return FMG_EINVAL;
+  if (!c->sub.empty()) return group_solve(c, c->Lmax, c->s.n_ir, true);
   if (!c->graph) {
     Builder b = make_builder(c);
     c->launches = 0;
@@ -665,11 +853,17 @@ int fmg_solve_async(fmg_ctx* c) {
 int fmg_solve(fmg_ctx* c) {
   int rc = fmg_solve_async(c);
   if (rc) return rc;
+  if (!c->sub.empty()) return group_check(c);
   return sync_check(c);
 }
 
 int fmg_solve_upto(fmg_ctx* c, int Lstop, int iters_last) {
   if (!c || Lstop < 0 || Lstop > c->Lmax || iters_last < 0) return FMG_EINVAL;
+  if (!c->sub.empty()) {
+    int rc = group_solve(c, Lstop, iters_last, false);
+    if (rc) return rc;
+    return group_check(c);
+  }
   Builder b = make_builder(c);
   c->cur = c->st;
   cudaStreamSynchronize(c->st);
@@ -679,16 +873,38 @@ int fmg_solve_upto(fmg_ctx* c, int Lstop, int iters_last) {
   return run_direct(c, b);
 }
 
+// Squared norms ||t_l||^2 of the log (device holds sums of squares; z-slab
+// levels l > lc of a group are summed over the slabs, KC levels are replicated).
+static int norms_sq(fmg_ctx* c, double* host) {
+  const size_t n = (size_t)c->levels * c->s.n_ir * c->levels;
+  if (c->sub.empty()) {
+    cudaError_t e = cudaStreamSynchronize(c->st);
+    if (e != cudaSuccess) return cuda_err(e);
+    return cuda_err(cudaMemcpy(host, c->norms_dev, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  }
+  std::vector<double> tmp(n);
+  for (size_t i = 0; i < n; ++i) host[i] = 0.0;
+  for (size_t r = 0; r < c->sub.size(); ++r) {
+    int rc = norms_sq(c->sub[r], tmp.data());
+    if (rc) return rc;
+    for (size_t i = 0; i < n; ++i) {
+      const int l = (int)(i % c->levels);
+      if (l > c->lc || r == 0) host[i] += tmp[i];
+    }
+  }
+  return FMG_OK;
+}
+
 int fmg_norms(fmg_ctx* c, double* host) {
   if (!c || !host) return FMG_EINVAL;
-  cudaError_t e = cudaStreamSynchronize(c->st);
-  if (e != cudaSuccess) return cuda_err(e);
-  e = cudaMemcpy(host, c->norms_dev, sizeof(double) * c->levels * c->s.n_ir * c->levels, cudaMemcpyDeviceToHost);
-  return cuda_err(e);
+  int rc = norms_sq(c, host);
+  if (rc) return rc;
+  for (size_t i = 0; i < (size_t)c->levels * c->s.n_ir * c->levels; ++i) host[i] = std::sqrt(host[i]);
+  return FMG_OK;
 }
 
 int fmg_residual(fmg_ctx* c, double* host_norms) {
-  if (!c) return FMG_EINVAL;
+  if (!c || !c->sub.empty()) return FMG_EINVAL;  // (virtual-slab groups: solve / norms / sections only)
   if (c->solved_L < 0) return FMG_ESTATE;
   int L = c->solved_L;
   if (L < 1) return FMG_ESTATE;
@@ -704,7 +920,7 @@ int fmg_residual(fmg_ctx* c, double* host_norms) {
   if (host_norms) {
     std::vector<double> tmp(c->levels, 0.0);
     cudaMemcpy(tmp.data(), row, sizeof(double) * c->levels, cudaMemcpyDeviceToHost);
-    for (int l = 0; l < c->levels; ++l) host_norms[l] = l <= L ? tmp[l] : 0.0;
+    for (int l = 0; l < c->levels; ++l) host_norms[l] = l <= L ? std::sqrt(tmp[l]) : 0.0;
   }
   cudaMemcpy(row, keep.data(), sizeof(double) * c->levels, cudaMemcpyHostToDevice);
   return FMG_OK;
@@ -725,6 +941,7 @@ static int decode_solution(fmg_ctx* c, int* which) {
 
 int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
   if (!c || !dst_dev) return FMG_EINVAL;
+  if (!c->sub.empty()) return FMG_EINVAL;
   if (c->solved_L < 0) return FMG_ESTATE;
   int which = 0;
   int rc = decode_solution(c, &which);
@@ -736,6 +953,7 @@ int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
 
 int fmg_errors(fmg_ctx* c, double* err3) {
   if (!c || !err3) return FMG_EINVAL;
+  if (!c->sub.empty()) return FMG_EINVAL;
   if (c->solved_L < 0) return FMG_ESTATE;
   int which = 0;
   int rc = decode_solution(c, &which);
@@ -762,6 +980,26 @@ int fmg_errors(fmg_ctx* c, double* err3) {
 int fmg_get_section(fmg_ctx* c, int which, int level, uint32_t* mant, int8_t* exps, int* width) {
   if (!c || which < 0 || which > 1 || level < 0 || level > c->Lmax || !width) return FMG_EINVAL;
   if (c->solved_L < 0) return FMG_ESTATE;
+  if (!c->sub.empty()) {
+    // assemble: every slab's planes [zlo, zhi) from its owner (KC levels from rank 0)
+    fmg_ctx* s0 = c->sub[0];
+    int rc = fmg_get_section(s0, which, level, mant, exps, width);
+    if (rc || level <= c->lc) return rc;
+    const Geom& g = s0->g[level];
+    const long long bpp = (long long)(g.NX / 32) * g.NY;  // blocks per plane
+    const int w = *width;
+    std::vector<uint32_t> m2(mant ? (size_t)g.nblk * w : 0);
+    std::vector<int8_t> e2(exps ? (size_t)g.nblk : 0);
+    for (size_t r = 1; r < c->sub.size(); ++r) {
+      fmg_ctx* sr = c->sub[r];
+      rc = fmg_get_section(sr, which, level, mant ? m2.data() : nullptr, exps ? e2.data() : nullptr, width);
+      if (rc) return rc;
+      const long long b0 = sr->zlo[level] * bpp, b1 = sr->zhi[level] * bpp;
+      if (mant) std::memcpy(mant + b0 * w, m2.data() + b0 * w, sizeof(uint32_t) * (b1 - b0) * w);
+      if (exps) std::memcpy(exps + b0, e2.data() + b0, (size_t)(b1 - b0));
+    }
+    return FMG_OK;
+  }
   const Geom& g = c->g[level];
   const Sec& s = which == 0 ? c->u[level] : c->r[level];
   int w = which == 0 ? c->wu_cur[level] : wr(c, level, c->solved_L);
@@ -783,6 +1021,13 @@ int fmg_get_section(fmg_ctx* c, int which, int level, uint32_t* mant, int8_t* ex
 
 int fmg_info(fmg_ctx* c, double* info) {
   if (!c || !info) return FMG_EINVAL;
+  if (!c->sub.empty()) {
+    int rc = fmg_info(c->sub[0], info);
+    double launches = 0.0;
+    for (fmg_ctx* s : c->sub) launches += (double)s->launches;
+    info[9] = launches;
+    return rc;
+  }
   const Geom& g = c->g[c->Lmax];
   info[0] = c->dim; info[1] = c->p; info[2] = c->levels;
   info[3] = g.NX; info[4] = g.NY; info[5] = g.NZ;
@@ -910,6 +1155,8 @@ int64_t fmg_export_solution(fmg_ctx* c, void* host, int64_t cap) {
 void fmg_destroy(fmg_ctx* c) {
   if (!c) return;
   cudaDeviceSynchronize();
+  for (fmg_ctx* s : c->sub) fmg_destroy(s);
+  c->sub.clear();
   if (c->graph) cudaGraphExecDestroy(c->graph);
   for (auto e : c->ev) cudaEventDestroy(e);
   free_all(c);

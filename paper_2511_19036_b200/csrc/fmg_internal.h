@@ -59,6 +59,7 @@ struct MArgs {
   int wr, wu_in, wu_out;
   int RC, nxb, nitems, NYo;  // rows (2D) / planes (3D) per chunk, block columns, work items (3D: CTAs), output rows
   int nyb, NZo;              // 3D: tile rows (of 8), output planes
+  int zlo, zhi;              // 3D: the planes of this rank (z slab), [zlo, zhi)
   long long poff;            // norm partials (one per item) at pbase + poff, or -1
 };
 

@@ -809,7 +809,8 @@ __global__ void __launch_bounds__(256) k_norms_all(const DevCtx* __restrict__ cp
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) c.norms[(long long)e.row * c.levels + e.l] = sqrt(red[0]);
+  // squared norm: the host takes the root (after summing the z-slab partials of all ranks)
+  if (threadIdx.x == 0) c.norms[(long long)e.row * c.levels + e.l] = red[0];
 }
 
 // ------------------------------------------------------- error norms -------

@@ -39,8 +39,8 @@ __device__ __forceinline__ void m3_item(const MArgs& a, M3Item& it) {
   const int t = cta % tiles, ch = cta / tiles;
   it.x0 = (t % a.nxb) * 32;
   it.y0 = (t / a.nxb) * TW3;
-  it.zs = ch * a.RC;
-  it.ze = min(a.NZo, it.zs + a.RC);
+  it.zs = a.zlo + ch * a.RC;  // (z-slab of this rank: planes [zlo, zhi))
+  it.ze = min(a.zhi, it.zs + a.RC);
   it.cta = cta;
 }
 

@@ -195,3 +195,68 @@ def test_torch_allocator_hook(P):
         gs.close()
     finally:
         P.use_torch_allocator(False)
+
+
+# ------------------------------------------------------- z slabs (§8e) --
+def _sections(s, levels):
+    return [(s.section(0, l), s.section(1, l)) for l in range(levels)]
+
+
+@pytest.mark.parametrize("d,p,levels,G", [(3, 1, 6, 2), (3, 1, 6, 4), (3, 1, 6, 8), (3, 2, 5, 2), (3, 2, 5, 4),
+                                          (3, 3, 4, 2), (3, 3, 4, 4), (3, 3, 4, 8)])
+def test_slab_decomposition_invariance(P, d, p, levels, G):
+    """Virtual z slabs (ghost-plane exchange + gather before the coarse kernel,
+    DESIGN.md §8): every section bit-identical to the undecomposed GPU solve
+    and to the oracle; norms within 1e-12 (slab partial sums reassociate)."""
+    s1 = P.Solver(d, p, levels)
+    s1.solve()
+    sg = P.Solver(d, p, levels, slabs=G)
+    sg.solve()
+    n1, ng = s1.norms(), sg.norms()
+    m = n1 != 0
+    assert np.array_equal(m, ng != 0)
+    assert np.all(np.abs(ng[m] - n1[m]) <= 1e-12 * n1[m])
+    for l in range(levels):
+        for which in (0, 1):
+            a, b = s1.section(which, l), sg.section(which, l)
+            assert a[2] == b[2] and np.array_equal(a[1], b[1]) and np.array_equal(a[0], b[0]), (which, l)
+    oc = O.CFMG(d, p, levels, O.schedule(d, p))
+    oc.solve()
+    for l in range(levels):
+        mo, eo, _ = oc.section(0, l)
+        mg, eg, _ = sg.section(0, l)
+        assert np.array_equal(eo, eg) and np.array_equal(mo, mg), l
+
+
+def test_slab_partial_solve(P):
+    sg = P.Solver(3, 2, 5, slabs=4)
+    sg.solve_upto(3, 2)
+    oc = O.CFMG(3, 2, 5, O.schedule(3, 2))
+    oc.solve_upto(3, 2)
+    for l in range(4):
+        for which in (0, 1):
+            mo, eo, _ = oc.section(which, l)
+            mg, eg, _ = sg.section(which, l)
+            assert np.array_equal(eo, eg) and np.array_equal(mo, mg), (which, l)
+
+
+def test_slab_C3_full(P):
+    """C3 (3D Q1, 512^3, 9 levels) at full size split into 2 and 4 z slabs:
+    bit-identical to the single-slab solve (decomposition invariance at the
+    configuration BASELINE.json shards over 1/2/4/8 GPUs)."""
+    c = CONFIGS["C3"]
+    s1 = P.Solver(c["dim"], c["p"], c["levels"])
+    s1.solve()
+    ref = [s1.section(0, l) for l in range(c["levels"])]
+    n1 = s1.norms()
+    s1.close()
+    for G in (2, 4):
+        sg = P.Solver(c["dim"], c["p"], c["levels"], slabs=G)
+        sg.solve()
+        for l in range(c["levels"]):
+            a = sg.section(0, l)
+            assert np.array_equal(ref[l][1], a[1]) and np.array_equal(ref[l][0], a[0]), (G, l)
+        ng = sg.norms()
+        m = n1 != 0
+        assert np.all(np.abs(ng[m] - n1[m]) <= 1e-12 * n1[m])
+        sg.close()
