@@ -42,6 +42,7 @@ extern "C" {
 #define FMG_ENOMEM 3  /* device allocation failed */
 #define FMG_ECUDA 4   /* CUDA runtime error */
 #define FMG_ESTATE 5  /* call out of order (e.g. residual before any solve) */
+#define FMG_ENCCL 6   /* NCCL not loadable or an NCCL call failed (multi-GPU slabs) */
 
 /* Bit-width schedule (tab:precisions PAPER.md:820-841).
  *   w_u(l,L) = b_u + k_u (L-l)   solution sections  (b1 of Table 3, k_u = p+1)
@@ -89,6 +90,27 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
  * fmg_create otherwise. */
 int fmg_create_slabs(int dim, int p, int levels, const fmg_schedule* s, int nslabs, void* stream,
                      fmg_ctx** out);
+
+/* Multi-GPU z slabs: one process per GPU, rank `rank` of `nranks` (3D only).
+ * Same decomposition and exchange plan as fmg_create_slabs; ghost planes move
+ * by grouped ncclSend/ncclRecv over NVLink and t_{lc+1} by an in-place
+ * ncclAllGather, all on the context stream inside the solve graph.  `id` is a
+ * 128-byte ncclUniqueId from fmg_nccl_unique_id on rank 0, broadcast by the
+ * caller (e.g. torch.distributed); collective over the ranks.  NCCL is
+ * resolved at run time (libnccl.so.2 already loaded, or FMG_NCCL_LIB).  After
+ * a solve each rank's sections hold its own planes of the grid levels;
+ * fmg_norms all-reduces the slab partials.  Errors: FMG_ENCCL, as
+ * fmg_create_slabs otherwise. */
+int fmg_nccl_unique_id(void* id);
+int fmg_create_dist(int dim, int p, int levels, const fmg_schedule* s, int nranks, int rank, const void* id,
+                    void* stream, fmg_ctx** out);
+
+/* Host-only helper (no device work): the ghost-plane exchange plan of rank
+ * `rank` of `nslabs` equal slabs of `nz` planes for halo depth `depth` (or a
+ * gather of every foreign plane): up to `cap` pieces of 4 ints {peer, z0, z1,
+ * send} (planes [z0, z1) sent to / received from peer) into `out`; returns
+ * the piece count, or -FMG_EINVAL. */
+int fmg_slab_plan(int nz, int nslabs, int rank, int depth, int gather, int* out, int cap);
 
 /* Alg 3.3 from scratch: coarse solve, then for L = 1..levels-1
  * push a level and run N x {fmgResidual, cFas V(0,1), correction}.  Enqueues one

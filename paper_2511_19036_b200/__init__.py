@@ -19,7 +19,7 @@ if not os.path.exists(_SO):
 
 _lib = C.CDLL(_SO)
 
-FMG_OK, FMG_EINVAL, FMG_ERANGE, FMG_ENOMEM, FMG_ECUDA, FMG_ESTATE = range(6)
+FMG_OK, FMG_EINVAL, FMG_ERANGE, FMG_ENOMEM, FMG_ECUDA, FMG_ESTATE, FMG_ENCCL = range(7)
 
 
 class FmgError(RuntimeError):
@@ -47,6 +47,10 @@ _lib.fmg_strerror.restype = C.c_char_p
 _lib.fmg_strerror.argtypes = [C.c_int]
 _lib.fmg_create.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule), _vp, C.POINTER(_vp)]
 _lib.fmg_create_slabs.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule), C.c_int, _vp, C.POINTER(_vp)]
+_lib.fmg_create_dist.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule), C.c_int, C.c_int, _vp, _vp,
+                                 C.POINTER(_vp)]
+_lib.fmg_nccl_unique_id.argtypes = [_vp]
+_lib.fmg_slab_plan.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int]
 _lib.fmg_solve.argtypes = [_vp]
 _lib.fmg_solve_async.argtypes = [_vp]
 _lib.fmg_solve_upto.argtypes = [_vp, C.c_int, C.c_int]
@@ -75,7 +79,8 @@ _ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
 _FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p)
 _lib.fmg_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, C.c_void_p]
 
-EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_create_slabs", "fmg_solve_async", "fmg_solve", "fmg_solve_upto",
+EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_create_slabs", "fmg_create_dist", "fmg_nccl_unique_id",
+           "fmg_slab_plan", "fmg_solve_async", "fmg_solve", "fmg_solve_upto",
            "fmg_norms", "fmg_residual", "fmg_get_solution", "fmg_errors", "fmg_get_section",
            "fmg_info", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_kernel_times", "fmg_destroy",
            "fmg_rhs_size", "fmg_set_rhs", "fmg_get_rhs", "fmg_export_solution",
@@ -113,6 +118,24 @@ def use_torch_allocator(enable: bool = True):
     _check(_lib.fmg_set_allocator(_torch_alloc_refs[0], _torch_alloc_refs[1], None), "fmg_set_allocator")
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for fmg_create_dist (call on rank 0, broadcast)."""
+    buf = C.create_string_buffer(128)
+    _check(_lib.fmg_nccl_unique_id(buf), "fmg_nccl_unique_id")
+    return buf.raw
+
+
+def slab_plan(nz: int, nslabs: int, rank: int, depth: int, gather: bool = False):
+    """Host-only ghost-plane exchange plan of one z slab (fmg_slab_plan):
+    list of (peer, z0, z1, send)."""
+    n = _lib.fmg_slab_plan(nz, nslabs, rank, depth, int(gather), None, 0)
+    if n < 0:
+        raise FmgError(-n, "fmg_slab_plan")
+    out = (C.c_int * (4 * max(n, 1)))()
+    _lib.fmg_slab_plan(nz, nslabs, rank, depth, int(gather), out, n)
+    return [tuple(out[4 * i:4 * i + 4]) for i in range(n)]
+
+
 def _stream_ptr(stream):
     if stream is None:
         return None
@@ -123,7 +146,10 @@ class Solver:
     """A compact-FMG context (fmg_create ... fmg_destroy)."""
 
     def __init__(self, dim: int, p: int, levels: int, schedule: Schedule | dict | None = None,
-                 stream=None, slabs: int = 1):
+                 stream=None, slabs: int = 1, dist: tuple | None = None):
+        """slabs > 1: virtual z slabs on this device (fmg_create_slabs).
+        dist = (rank, nranks, uid): this process is z-slab `rank` of `nranks`
+        GPUs (fmg_create_dist); uid from nccl_unique_id() on rank 0."""
         if schedule is None:
             from fmg_inputs import default_schedule
             schedule = default_schedule(dim, p)
@@ -132,7 +158,12 @@ class Solver:
         self.dim, self.p, self.levels, self.schedule = dim, p, levels, schedule
         self.stream = stream
         h = C.c_void_p()
-        if slabs > 1:  # virtual z slabs on one device (fmg_create_slabs)
+        if dist is not None:
+            rank, nranks, uid = dist
+            ub = C.create_string_buffer(bytes(uid), 128)
+            _check(_lib.fmg_create_dist(dim, p, levels, C.byref(schedule), nranks, rank, ub, _stream_ptr(stream),
+                                        C.byref(h)), "fmg_create_dist")
+        elif slabs > 1:  # virtual z slabs on one device (fmg_create_slabs)
             _check(_lib.fmg_create_slabs(dim, p, levels, C.byref(schedule), slabs, _stream_ptr(stream),
                                          C.byref(h)), "fmg_create_slabs")
         else:

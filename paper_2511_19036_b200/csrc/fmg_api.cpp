@@ -19,6 +19,9 @@
 #include <algorithm>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "fmg_internal.h"
 
 using namespace fmg;
@@ -73,6 +76,7 @@ struct fmg_ctx {
   int G = 1, rank = 0;
   int zlo[kMaxLev]{}, zhi[kMaxLev]{};
   std::vector<fmg_ctx*> sub;      // virtual slabs: G sub-contexts driven in lockstep (group handle)
+  void* comm = nullptr;           // multi-GPU slabs: ncclComm_t (one rank per process)
   fmg_alloc_fn afn = nullptr;
   fmg_free_fn ffn = nullptr;
   void* auser = nullptr;
@@ -410,31 +414,129 @@ double* xarray(fmg_ctx* c, int arr, int l) {
   }
 }
 
+// ---- exchange plan (shared by virtual slabs and NCCL ranks) ----------------
+// Rank r of G equal slabs of NZ planes: the plane runs it receives (ghost
+// planes [zlo-h, zlo) and [zhi, zhi+h), or every foreign plane for a gather)
+// from their owners, and the runs of its own planes the other ranks receive
+// from it.  Both sides list a pair's runs in increasing z, so NCCL
+// send/recv pairs match.
+struct XPiece {
+  int peer, z0, z1, send;
+};
+std::vector<XPiece> slab_plan(int NZ, int G, int r, int h, int gather) {
+  std::vector<XPiece> out;
+  const int slab = NZ / G;
+  auto ghost = [&](int s, int k, int& a, int& b) {  // k = 0 low, 1 high ghost run of rank s
+    const int zlo = s * slab, zhi = (s + 1) * slab;
+    if (gather) {
+      a = k == 0 ? 0 : zhi;
+      b = k == 0 ? zlo : NZ;
+    } else {
+      a = k == 0 ? std::max(0, zlo - h) : zhi;
+      b = k == 0 ? zlo : std::min(NZ, zhi + h);
+    }
+  };
+  for (int s = 0; s < G; ++s) {
+    if (s == r) continue;
+    // receive from owner s: my ghost runs within s's planes
+    for (int k = 0; k < 2; ++k) {
+      int a, b;
+      ghost(r, k, a, b);
+      a = std::max(a, s * slab);
+      b = std::min(b, (s + 1) * slab);
+      if (a < b) out.push_back({s, a, b, 0});
+    }
+    // send to s: s's ghost runs within my planes
+    for (int k = 0; k < 2; ++k) {
+      int a, b;
+      ghost(s, k, a, b);
+      a = std::max(a, r * slab);
+      b = std::min(b, (r + 1) * slab);
+      if (a < b) out.push_back({s, a, b, 1});
+    }
+  }
+  return out;
+}
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+};
+
+// NCCL is resolved at run time (the torch-bundled libnccl.so.2 is normally
+// already loaded; FMG_NCCL_LIB names another copy), so libfmg.so carries no
+// link-time NCCL dependency.
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h && getenv("FMG_NCCL_LIB")) h = dlopen(getenv("FMG_NCCL_LIB"), RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+  api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+  api.send = (decltype(api.send))dlsym(h, "ncclSend");
+  api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+  api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+  api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+  api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+  api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+  api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.send && api.recv && api.allGather &&
+           api.allReduce && api.groupStart && api.groupEnd;
+  return api;
+}
+
+// Multi-GPU slabs: the same plan as grouped NCCL point-to-point transfers over
+// NVLink (a gather is an in-place all-gather), on the context stream (captured
+// into the solve graph).
+void nccl_exchange(fmg_ctx* c, const Item& it) {
+  NcclApi& N = nccl();
+  const int l = it.xl;
+  const Geom& g = c->g[l];
+  const size_t plane = (size_t)g.NX * g.NY;
+  double* arr = xarray(c, it.xarr, l);
+  ncclComm_t comm = (ncclComm_t)c->comm;
+  if (it.xgather) {
+    const size_t cnt = plane * (size_t)(g.NZ / c->G);
+    N.allGather(arr + (size_t)c->zlo[l] * plane, arr, cnt, ncclDouble, comm, c->cur);
+    return;
+  }
+  N.groupStart();
+  for (const XPiece& q : slab_plan(g.NZ, c->G, c->rank, it.xdepth, 0)) {
+    double* p = arr + (size_t)q.z0 * plane;
+    const size_t cnt = plane * (size_t)(q.z1 - q.z0);
+    if (q.send) N.send(p, cnt, ncclDouble, q.peer, comm, c->cur);
+    else N.recv(p, cnt, ncclDouble, q.peer, comm, c->cur);
+  }
+  N.groupEnd();
+}
+
 // Virtual z slabs: fill the ghost planes (or, for a gather, every foreign plane)
 // of each sub-context from the sub-context that owns them (D2D copies on the
 // group's stream; the owners computed those planes in the previous item).
 void group_exchange(fmg_ctx* grp, const Item& it) {
   const int G = (int)grp->sub.size(), l = it.xl;
-  fmg_ctx* s0 = grp->sub[0];
-  const Geom& g = s0->g[l];
+  const Geom& g = grp->sub[0]->g[l];
   const size_t plane = (size_t)g.NX * g.NY;
-  const int slab = g.NZ / G;
   for (int r = 0; r < G; ++r) {
     fmg_ctx* dst = grp->sub[r];
-    const int zlo = dst->zlo[l], zhi = dst->zhi[l];
-    int ranges[2][2] = {{std::max(0, zlo - it.xdepth), zlo}, {zhi, std::min(g.NZ, zhi + it.xdepth)}};
-    if (it.xgather) {
-      ranges[0][0] = 0;
-      ranges[1][1] = g.NZ;
-    }
-    for (int k = 0; k < 2; ++k) {
-      for (int z = ranges[k][0]; z < ranges[k][1];) {
-        const int owner = z / slab, zend = std::min(ranges[k][1], (owner + 1) * slab);
-        double* d = xarray(dst, it.xarr, l) + (size_t)z * plane;
-        const double* s = xarray(grp->sub[owner], it.xarr, l) + (size_t)z * plane;
-        cudaMemcpyAsync(d, s, sizeof(double) * plane * (zend - z), cudaMemcpyDeviceToDevice, dst->cur);
-        z = zend;
-      }
+    for (const XPiece& q : slab_plan(g.NZ, G, r, it.xdepth, it.xgather)) {
+      if (q.send) continue;  // (the receiving side performs each copy)
+      double* d = xarray(dst, it.xarr, l) + (size_t)q.z0 * plane;
+      const double* s = xarray(grp->sub[q.peer], it.xarr, l) + (size_t)q.z0 * plane;
+      cudaMemcpyAsync(d, s, sizeof(double) * plane * (q.z1 - q.z0), cudaMemcpyDeviceToDevice, dst->cur);
     }
   }
 }
@@ -449,7 +551,10 @@ void issue(fmg_ctx* c, const Builder& b) {
     if (e != cudaSuccess) fprintf(stderr, "[fmg] pending CUDA error before issue: %s\n", cudaGetErrorString(e));
   }
   for (const Item& it : b.items) {
-    if (it.kind == 2) continue;  // (single context: no slabs)
+    if (it.kind == 2) {  // ghost planes: NCCL ranks (single-rank contexts have none)
+      if (c->comm) nccl_exchange(c, it);
+      continue;
+    }
     issue_item(c, it);
     if (dbg) {
       cudaError_t e = cudaStreamSynchronize(c->cur);
@@ -752,6 +857,48 @@ int fmg_create(int dim, int p, int levels, const fmg_schedule* s, void* stream, 
   return create_impl(dim, p, levels, s, stream, 1, 0, out);
 }
 
+int fmg_nccl_unique_id(void* id) {
+  if (!id) return FMG_EINVAL;
+  NcclApi& N = nccl();
+  if (!N.ok) return FMG_ENCCL;
+  ncclUniqueId u;
+  if (N.getUniqueId(&u) != ncclSuccess) return FMG_ENCCL;
+  std::memcpy(id, &u, sizeof(u));
+  return FMG_OK;
+}
+
+int fmg_create_dist(int dim, int p, int levels, const fmg_schedule* s, int nranks, int rank, const void* id,
+                    void* stream, fmg_ctx** out) {
+  if (!out || !id || dim != 3 || nranks < 1 || rank < 0 || rank >= nranks) return FMG_EINVAL;
+  NcclApi& N = nccl();
+  if (!N.ok) return FMG_ENCCL;
+  int rc = create_impl(dim, p, levels, s, stream, nranks, rank, out);
+  if (rc) return rc;
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  ncclComm_t comm = nullptr;
+  if (N.commInitRank(&comm, nranks, u, rank) != ncclSuccess) {
+    fmg_destroy(*out);
+    *out = nullptr;
+    return FMG_ENCCL;
+  }
+  (*out)->comm = comm;
+  return FMG_OK;
+}
+
+int fmg_slab_plan(int nz, int nslabs, int rank, int depth, int gather, int* out, int cap) {
+  if (nz < 1 || nslabs < 1 || nz % nslabs != 0 || rank < 0 || rank >= nslabs || depth < 0) return -FMG_EINVAL;
+  std::vector<XPiece> v = slab_plan(nz, nslabs, rank, depth, gather);
+  if (out)
+    for (int i = 0; i < (int)v.size() && i < cap; ++i) {
+      out[4 * i] = v[i].peer;
+      out[4 * i + 1] = v[i].z0;
+      out[4 * i + 2] = v[i].z1;
+      out[4 * i + 3] = v[i].send;
+    }
+  return (int)v.size();
+}
+
 int fmg_create_slabs(int dim, int p, int levels, const fmg_schedule* s, int nslabs, void* stream, fmg_ctx** out) {
   if (!out || !s || dim != 3 || nslabs < 1 || nslabs > 64) return FMG_EINVAL;
   *out = nullptr;
@@ -880,7 +1027,17 @@ static int norms_sq(fmg_ctx* c, double* host) {
   if (c->sub.empty()) {
     cudaError_t e = cudaStreamSynchronize(c->st);
     if (e != cudaSuccess) return cuda_err(e);
-    return cuda_err(cudaMemcpy(host, c->norms_dev, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    e = cudaMemcpy(host, c->norms_dev, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess || !c->comm) return cuda_err(e);
+    // NCCL ranks: sum the slab partials of levels > lc (KC levels from rank 0)
+    for (size_t i = 0; i < n; ++i)
+      if ((int)(i % c->levels) <= c->lc && c->rank != 0) host[i] = 0.0;
+    cudaMemcpy(c->err_part, host, sizeof(double) * n, cudaMemcpyHostToDevice);
+    if (nccl().allReduce(c->err_part, c->err_part, n, ncclDouble, ncclSum, (ncclComm_t)c->comm, c->st) != ncclSuccess)
+      return FMG_ENCCL;
+    e = cudaStreamSynchronize(c->st);
+    if (e != cudaSuccess) return cuda_err(e);
+    return cuda_err(cudaMemcpy(host, c->err_part, sizeof(double) * n, cudaMemcpyDeviceToHost));
   }
   std::vector<double> tmp(n);
   for (size_t i = 0; i < n; ++i) host[i] = 0.0;
@@ -904,7 +1061,7 @@ int fmg_norms(fmg_ctx* c, double* host) {
 }
 
 int fmg_residual(fmg_ctx* c, double* host_norms) {
-  if (!c || !c->sub.empty()) return FMG_EINVAL;  // (virtual-slab groups: solve / norms / sections only)
+  if (!c || !c->sub.empty() || c->comm) return FMG_EINVAL;  // (virtual-slab groups: solve / norms / sections only)
   if (c->solved_L < 0) return FMG_ESTATE;
   int L = c->solved_L;
   if (L < 1) return FMG_ESTATE;
@@ -1157,6 +1314,7 @@ void fmg_destroy(fmg_ctx* c) {
   cudaDeviceSynchronize();
   for (fmg_ctx* s : c->sub) fmg_destroy(s);
   c->sub.clear();
+  if (c->comm) nccl().commDestroy((ncclComm_t)c->comm);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   for (auto e : c->ev) cudaEventDestroy(e);
   free_all(c);
@@ -1172,6 +1330,7 @@ const char* fmg_strerror(int code) {
     case FMG_ENOMEM: return "device allocation failed";
     case FMG_ECUDA: return "CUDA runtime error";
     case FMG_ESTATE: return "call out of order";
+    case FMG_ENCCL: return "NCCL unavailable or failed";
     default: return "unknown error";
   }
 }

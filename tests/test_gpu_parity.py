@@ -260,3 +260,16 @@ def test_slab_C3_full(P):
         m = n1 != 0
         assert np.all(np.abs(ng[m] - n1[m]) <= 1e-12 * n1[m])
         sg.close()
+
+
+def test_nccl_dist_single_rank(P):
+    """fmg_create_dist with one rank: NCCL resolved at run time, communicator
+    created, norms all-reduced; results identical to fmg_create."""
+    s1 = P.Solver(3, 2, 4)
+    s1.solve()
+    uid = P.nccl_unique_id()
+    sd = P.Solver(3, 2, 4, dist=(0, 1, uid))
+    sd.solve()
+    assert np.array_equal(s1.norms(), sd.norms())
+    for l in range(4):
+        assert np.array_equal(s1.section(0, l)[0], sd.section(0, l)[0])
