@@ -36,7 +36,7 @@ namespace fmg {
 
 constexpr int KC_NW = 16;
 constexpr int KC_NT = 32 * KC_NW;
-constexpr int KC_SMEM_MAX = 200 * 1024;  // dynamic shared memory budget per CTA
+constexpr int KC_SMEM_MAX = 176 * 1024;  // dynamic shared memory budget per CTA (static: ~46 KB)
 
 __device__ __forceinline__ unsigned cl_rank() {
   unsigned r;
@@ -116,11 +116,12 @@ struct GAcc {
   }
 };
 
-constexpr int KC_ROWBUF = 96;  // per-warp staging row (doubles)
+constexpr int KC_ROWBUF = 320;  // per-warp staging tile (doubles): 7 rows x 40 (A) / 4 rows x 80 (R)
 
 #define LANE ((int)threadIdx.x)
 #define WID ((int)threadIdx.y)
 #define SROW (kc_srow[threadIdx.y])
+#define SROWR(r, j) (kc_srow[threadIdx.y][(r) * RSTR + (j)])
 __shared__ double kc_srow[KC_NW][KC_ROWBUF];  // per-warp staging rows
 
 // Out-of-line codec (one copy shared by every phase: KC is bound by
@@ -191,6 +192,15 @@ struct Kc {
     }
     __syncwarp();
   }
+  // store a gathered row as row r (stride RSTR) of the warp's staging tile (no sync)
+  template <int K, int RSTR>
+  __device__ __forceinline__ void put(const double (&v)[K], int W, int r) const {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int j = LANE + 32 * k;
+      if (j < W) SROWR(r, j) = v[k];
+    }
+  }
 
   // ---- per-point operators, warp-level (canonical trees) ----
   // x0: first column of the warp's block; every LANE returns its column's value.
@@ -200,20 +210,33 @@ struct Kc {
   __device__ __noinline__ void Axy(U u, const Geom g, int x0, int y, int z, double& cv, double& sv) const {
     constexpr int R = 2 * P + 1, W = 32 + 2 * P;
     const int x = x0 + LANE, tx = x % P, ty = y % P;
+    constexpr int RSTR = 40;
     double v[R][2];
 #pragma unroll
     for (int r = 0; r < R; ++r) gather<2>(u, x0 - P, W, y - P + r, z, v[r]);
-    double cc = 0.0, dd = 0.0, e = 0.0;
+    // all rows staged at once; the R x passes are independent chains (ILP)
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) put<2, RSTR>(v[r], W, r);
+    __syncwarp();
+    double xs[R], xt[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      stage<2>(v[r], W);
       double s = 0.0, t = 0.0;
 #pragma unroll
       for (int o = 0; o < R; ++o) {
-        double val = SROW[LANE + o];
+        double val = SROWR(r, LANE + o);
         s = fma(cf.Mc[tx][o], val, s);
         t = fma(cf.Kc[tx][o], val, t);
       }
+      xs[r] = s;
+      xt[r] = t;
+    }
+    __syncwarp();
+    double cc = 0.0, dd = 0.0, e = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double s = xs[r], t = xt[r];
       if constexpr (D == 2) {
         dd = fma(cf.Kc[ty][r], s, dd);
         e = fma(cf.Mc[ty][r], t, e);
@@ -284,7 +307,7 @@ struct Kc {
   // 3D: the staged y pass).  Fine rows are gathered in batches of RB.
   template <class U>
   __device__ __noinline__ double Rxy(U tf, const Geom gf, int nc, int x0c, int yc, int fz) const {
-    constexpr int NS = 4 * P - 1, W = 64 + NS - 1, RB = 4;
+    constexpr int NS = 4 * P - 1, W = 64 + NS - 1, RB = 4, RSTR = 80;
     const int xc = x0c + LANE, txc = xc % P, tyc = yc % P;
     const int fxs = 2 * x0c - (2 * P - 1);
     double t = 0.0;
@@ -294,18 +317,25 @@ struct Kc {
 #pragma unroll
       for (int r = 0; r < RB; ++r)
         if (s0 + r < NS) gather<3>(tf, fxs, W, 2 * yc - (2 * P - 1) + s0 + r, fz, v[r]);
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+        if (s0 + r < NS) put<3, 80>(v[r], W, r);
+      __syncwarp();
+      double xv[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        if (s0 + r >= NS) break;
-        stage<3>(v[r], W);
-        double xv = 0.0;
+        xv[r] = 0.0;
+        if (s0 + r >= NS) continue;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           // (t is stored as +0 at fine non-unknowns: no mask needed)
-          xv = fma(cf.Rw[txc][s], SROW[2 * LANE + s], xv);
+          xv[r] = fma(cf.Rw[txc][s], SROWR(r, 2 * LANE + s), xv[r]);
         }
-        t = fma(cf.Rw[tyc][s0 + r], xv, t);
       }
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+        if (s0 + r < NS) t = fma(cf.Rw[tyc][s0 + r], xv[r], t);
     }
     return (unk1(xc, nc) && unk1(yc, nc)) ? t : 0.0;
   }
@@ -661,6 +691,7 @@ struct Kc {
 #undef LANE
 #undef WID
 #undef SROW
+#undef SROWR
 
 template <int D, int P>
 __global__ void __launch_bounds__(KC_NT, 1) kc_kernel(const DevCtx* __restrict__ cp, KcDesc a) {
