@@ -112,24 +112,24 @@ def aggregate(unknowns_per_rank: int, world: int, ms_max: float) -> float:
 def kernel_model(cfg, sched, cls):
     """Algorithmic FP64 flops and HBM bytes per launch of a fine-level kernel
     (DESIGN.md §7), counted per stored point of the finest level from what the
-    kernel must read and write in the current design (halos not counted)."""
+    march kernels (fmg_march*.cu) must read and write (halos, the second L2
+    touch of the staged operand and the encode's integer work not counted)."""
     d, p, levels = cfg["dim"], cfg["p"], cfg["levels"]
     n = p << levels
     NX = (n + 31) // 32 * 32
     pts = NX * n * (n if d == 3 else 1)
     t = 2 * p + 1
     a_flops = (8 * t + 1) if d == 2 else (14 * t + 2)   # canonical A tree, FMA = 2 flops
-    p_flops = 2 * (p + 1) * (1 + 2 ** -1 + (2 ** -2 if d == 3 else 0))  # x,y(,z) prolongation passes
     wr_b = sched["b_r"] / 8 + 1 / 32
     wu_b = sched["b_u"] / 8 + 1 / 32
-    coarse = 8 / 2 ** d                                  # FP64 coarse-level input per fine point
-    if cls == 0:   # residual: u_L in, t_L out (FP64), r_L out
-        flops = a_flops + (d - 1) + 2 + 2
+    if cls == 0:   # residual: u_L in, t_L out (FP64), r_L out; f = ((C g) g) g
+        flops = a_flops + (d - 1) + 2
         byts = 8 + 8 + wr_b
-    else:          # cls 5: last Chebyshev step (finalise) at the fine level:
-        # b in, u_{L-1} in (coarse), u_L out, ú_L in + out; A y_1, update, P u_{L-1}, 3 encodes/decodes
-        flops = 3 + a_flops + 7 + p_flops + 3
-        byts = 8 + coarse + 8 + 2 * wu_b
+    else:          # cls 5: last Chebyshev step (finalise) at the finest level (l = L: no w_L, z_L):
+        # b in (staged, transformed to y_1 = inv_theta invD b), P u_{L-1} in, u_L out, ú_L in + out;
+        # y_1 (2), A y_1, q, d, y (5), w-free correction (2 adds)
+        flops = 2 + a_flops + 5 + 2
+        byts = 8 + 8 + 8 + 2 * wu_b
     return flops * pts, byts * pts
 
 
