@@ -93,6 +93,21 @@ __device__ __forceinline__ double point_decode(const uint32_t* words, int E, int
   return i2d(m, w) * pow2(E - (w - 1));
 }
 
+// Packed words of a narrow block (w = W <= 8): lane j returns word j (j < W).
+template <int W>
+__device__ __forceinline__ uint32_t pack_narrow(unsigned long long field, int lane) {
+  const int p = lane * W, j0 = p >> 5;
+  const unsigned long long cf = field << (p & 31);
+  const uint32_t c0 = (uint32_t)cf, c1 = (uint32_t)(cf >> 32);
+  uint32_t mine = 0u;
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    const uint32_t word = __reduce_or_sync(FULL, j == j0 ? c0 : (j == j0 + 1 ? c1 : 0u));
+    mine = lane == j ? word : mine;
+  }
+  return mine;
+}
+
 // Warp-cooperative encode of one block; lane j holds entry j.
 // Writes the w words and the exponent when `words` is non-null; returns the
 // quantised value m 2^(E-q).  Non-finite input or E > 127 sets *status.
@@ -131,16 +146,15 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
     uint32_t mine0 = 0u, mine1 = 0u;
     if (w <= 8) {
       // narrow: entry `lane` occupies stream bits [lane w, lane w + w) = (low, high)
-      // parts of words j0, j0 + 1; one redux.or per output word
-      const int p = lane * w, j0 = p >> 5;
-      const unsigned long long cf = field << (p & 31);
-      const uint32_t c0 = (uint32_t)cf, c1 = (uint32_t)(cf >> 32);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {  // independent reductions (w is warp-uniform)
-        if (j < w) {
-          uint32_t word = __reduce_or_sync(FULL, j == j0 ? c0 : (j == j0 + 1 ? c1 : 0u));
-          mine0 = lane == j ? word : mine0;
-        }
+      // parts of words j0, j0 + 1; one redux.or per output word (width-specialised)
+      switch (w) {
+        case 2: mine0 = pack_narrow<2>(field, lane); break;
+        case 3: mine0 = pack_narrow<3>(field, lane); break;
+        case 4: mine0 = pack_narrow<4>(field, lane); break;
+        case 5: mine0 = pack_narrow<5>(field, lane); break;
+        case 6: mine0 = pack_narrow<6>(field, lane); break;
+        case 7: mine0 = pack_narrow<7>(field, lane); break;
+        default: mine0 = pack_narrow<8>(field, lane); break;
       }
     } else {
       // wide: word j gathers its <= ceil(32/w)+1 entries by shuffles

@@ -829,13 +829,15 @@ int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* 
             KcLayout* ly, int* lc_out, int* cs_out) {
   int forced = 0;
   if (const char* e = getenv("FMG_KC_CLUSTER")) forced = atoi(e);
+  int bpw = 1;  // BFP blocks per KC warp at level lc (env FMG_KC_BPW; 2 measured slower on C2)
+  if (const char* e = getenv("FMG_KC_BPW")) bpw = std::max(1, atoi(e));
   for (int lg = 4; lg >= 0; --lg) {
     const int cs = 1 << lg;
     if (forced && cs != forced) continue;
     // largest lc with at most one BFP block per KC warp whose layout fits
     int lc = 0;
     for (int l = 1; l <= std::min(Lmax, lc_cap); ++l) {
-      if (g[l].nblk > (long long)cs * KC_NW) break;
+      if (g[l].nblk > (long long)cs * KC_NW * bpw) break;
       KcLayout t;
       if (kc_layout(lg, l, g, ust, rst, n_ir, &t) > KC_SMEM_MAX) break;
       lc = l;
