@@ -357,6 +357,50 @@ int prepare(fmg_ctx* c, const Builder& b, int slot) {
   return FMG_OK;
 }
 
+// Host copy of the device view of level l (mirrors fill_devctx).
+LevelDev level_dev(const fmg_ctx* c, int l) {
+  LevelDev v{};
+  v.g = c->g[l];
+  v.umant = c->u[l].mant;
+  v.uexp = c->u[l].exps;
+  v.ustride = c->u[l].stride;
+  v.rmant = c->r[l].mant;
+  v.rexp = c->r[l].exps;
+  v.rstride = c->r[l].stride;
+  v.gtab = c->gtab[l];
+  v.U = c->Ul[l];
+  v.T = c->Tl[l];
+  v.W = c->Wl[l];
+  return v;
+}
+
+// March-kernel arguments of a grid op.
+MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
+  MArgs m{};
+  m.type = o.type;
+  m.l = o.l;
+  m.L = o.L;
+  m.step = o.step;
+  m.last = o.last;
+  m.wr = o.wr;
+  m.wu_in = o.wu_in;
+  m.wu_out = o.wu_out;
+  m.RC = c->mrc[o.l];
+  m.nxb = c->g[o.l].NX / 32;
+  m.nitems = c->mitems[o.l];
+  m.NYo = c->g[o.l].NY;
+  m.nyb = c->mnyb[o.l];
+  m.NZo = c->g[o.l].NZ;
+  m.zlo = c->zlo[o.l];
+  m.zhi = c->zhi[o.l];
+  m.poff = o.poff;
+  m.lv = level_dev(c, o.l);
+  const int lo = o.type == OP_RESTRICT ? o.l + 1 : o.l - 1;
+  if (lo >= 0 && lo <= c->Lmax) m.lo = level_dev(c, lo);
+  m.p = MPtrs{c->buf[0], c->buf[1], {c->buf[2], c->buf[3]}, c->buf[4], c->buf[5], c->pbase, c->status};
+  return m;
+}
+
 // Launch one op / KC item of the list on c->cur.
 void issue_item(fmg_ctx* c, const Item& it) {
   if (it.kind == 1) {
@@ -366,25 +410,7 @@ void issue_item(fmg_ctx* c, const Item& it) {
   } else {
     mark(c, it.timed_cls);
     if (c->march) {
-      const OpDesc& o = it.op;
-      MArgs m{};
-      m.type = o.type;
-      m.l = o.l;
-      m.L = o.L;
-      m.step = o.step;
-      m.last = o.last;
-      m.wr = o.wr;
-      m.wu_in = o.wu_in;
-      m.wu_out = o.wu_out;
-      m.RC = c->mrc[o.l];
-      m.nxb = c->g[o.l].NX / 32;
-      m.nitems = c->mitems[o.l];
-      m.NYo = c->g[o.l].NY;
-      m.nyb = c->mnyb[o.l];
-      m.NZo = c->g[o.l].NZ;
-      m.zlo = c->zlo[o.l];
-      m.zhi = c->zhi[o.l];
-      m.poff = o.poff;
+      const MArgs m = march_args(c, it.op);
       if (c->dim == 2) launch_march(c->p, c->cur, c->devctx, m, c->cf);
       else launch_march3(c->p, c->cur, c->devctx, m, c->cf);
     } else {
@@ -550,7 +576,8 @@ void issue(fmg_ctx* c, const Builder& b) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fprintf(stderr, "[fmg] pending CUDA error before issue: %s\n", cudaGetErrorString(e));
   }
-  for (const Item& it : b.items) {
+  for (size_t ii = 0; ii < b.items.size(); ++ii) {
+    const Item& it = b.items[ii];
     if (it.kind == 2) {  // ghost planes: NCCL ranks (single-rank contexts have none)
       if (c->comm) nccl_exchange(c, it);
       continue;

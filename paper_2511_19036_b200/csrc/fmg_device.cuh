@@ -187,22 +187,7 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
 
 // ------------------------------------------------------------- contexts --
 // Device-side context (lives in global memory, built by fmg_api.cpp).
-struct LevelDev {
-  Geom g;
-  uint32_t* umant;
-  int8_t* uexp;
-  int ustride;
-  uint32_t* rmant;
-  int8_t* rexp;
-  int rstride;
-  const double* gtab;
-  int tx, ty, tz;  // tile grid of this level
-  double* part;    // norm partials, one per tile
-  int* count;      // arrival counter for the last-CTA norm reduction
-  double* U;       // decoded u_l = dec ú_l + P_l u_{l-1} (padded level layout)
-  double* T;       // residual temporary t_l
-  double* W;       // w_l = z_l + dec ý_l
-};
+// (LevelDev: fmg_internal.h)
 
 struct __align__(16) DevCtx {
   LevelDev lv[kMaxLev];

@@ -53,6 +53,31 @@ struct OpDesc {
   long long poff;  // norm partials of this (FMG level, iteration, level): pbase + poff
 };
 
+// Device view of one level (also a member of the device context).
+struct LevelDev {
+  Geom g;
+  uint32_t* umant;
+  int8_t* uexp;
+  int ustride;
+  uint32_t* rmant;
+  int8_t* rexp;
+  int rstride;
+  const double* gtab;
+  int tx, ty, tz;  // tile grid of this level
+  double* part;    // norm partials, one per tile
+  int* count;      // arrival counter for the last-CTA norm reduction
+  double* U;       // decoded u_l = dec ú_l + P_l u_{l-1} (padded level layout)
+  double* T;       // residual temporary t_l
+  double* W;       // w_l = z_l + dec ý_l
+};
+
+// Scratch and bookkeeping pointers of the march kernels.
+struct MPtrs {
+  double *Z, *B, *Y[2], *Dv, *PU;
+  double* pbase;
+  int* status;
+};
+
 // 2D row-march launch (fmg_march.cu): one warp per (32-column block, chunk of RC output rows).
 struct MArgs {
   int type, l, L, step, last;
@@ -60,6 +85,10 @@ struct MArgs {
   int RC, nxb, nitems, NYo;  // rows (2D) / planes (3D) per chunk, block columns, work items (3D: CTAs), output rows
   int nyb, NZo;              // 3D: tile rows (of 8), output planes
   int zlo, zhi;              // 3D: the planes of this rank (z slab), [zlo, zhi)
+  // operands in the parameter space (no dependent global loads at kernel start)
+  LevelDev lv;               // the output level l
+  LevelDev lo;               // the other level: l-1 (decode, prolongation, cFas) or l+1 (restriction)
+  MPtrs p;
   long long poff;            // norm partials (one per item) at pbase + poff, or -1
 };
 

@@ -22,6 +22,9 @@
 
 namespace fmg {
 
+#ifndef FMG_MARCH_MINB
+#define FMG_MARCH_MINB 3     // CTAs per SM the register budget is sized for
+#endif
 constexpr int MW = 8;        // warps per CTA
 constexpr int MNB = 8;       // staged rows per warp (ring; >= MPF + p + 1)
 constexpr int MPF = 4;       // rows staged ahead
@@ -36,15 +39,19 @@ __device__ __forceinline__ void cp_wait() {
 struct MItem {
   int x0, ys, ye, item;
 };
-// work item of this warp: (block column, row chunk), or false if none
-__device__ __forceinline__ bool m_item(const MArgs& a, MItem& it) {
-  const int item = blockIdx.x * MW + threadIdx.y;
-  if (item >= a.nitems) return false;
+// work item `item`: (block column, row chunk)
+__device__ __forceinline__ void m_item_at(const MArgs& a, int item, MItem& it) {
   const int xb = item % a.nxb, ch = item / a.nxb;
   it.x0 = xb * 32;
   it.ys = ch * a.RC;
   it.ye = min(a.NYo, it.ys + a.RC);
   it.item = item;
+}
+// work item of this warp in a one-op launch, or false if none
+__device__ __forceinline__ bool m_item(const MArgs& a, MItem& it) {
+  const int item = blockIdx.x * MW + threadIdx.y;
+  if (item >= a.nitems) return false;
+  m_item_at(a, item, it);
   return true;
 }
 
@@ -199,14 +206,10 @@ struct CAux {  // Chebyshev operands of one output row
 // ------------------------------------------------------------ kernels --
 // u_l = dec ú_l + P_l u_{l-1} (decode sweep S2)
 template <int P>
-__global__ void __launch_bounds__(32 * MW, 3) k_m_decode(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
-  pdl_wait();
-  pdl_trigger();
-  MItem it;
-  if (!m_item(a, it)) return;
-  const DevCtx& c = *cp;
-  const LevelDev& lv = c.lv[a.l];
-  const LevelDev& lp = c.lv[a.l - 1 >= 0 ? a.l - 1 : 0];
+__device__ __forceinline__ void m_decode_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
+  const LevelDev& lp = a.lo;
   const int lane = threadIdx.x, x = it.x0 + lane, nxb = lv.g.NX >> 5;
   for (int y = it.ys; y < it.ye; ++y) {
     const long long blk = (long long)y * nxb + (it.x0 >> 5);
@@ -215,17 +218,22 @@ __global__ void __launch_bounds__(32 * MW, 3) k_m_decode(const DevCtx* __restric
     lv.U[(long long)y * lv.g.NX + x] = dv + pu;
   }
 }
-
-// t_L = f_L - A_L u_L, r_L = enc(t_L), ||t_L||^2 partial (PAPER.md:738-739)
 template <int P>
-__global__ void __launch_bounds__(32 * MW, 3) k_m_residual(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
+__global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_decode(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+    const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  const DevCtx& c = *cp;
-  const LevelDev& lv = c.lv[a.l];
+  m_decode_item<P>(a, cf, it, msm);
+}
+
+// t_L = f_L - A_L u_L, r_L = enc(t_L), ||t_L||^2 partial (PAPER.md:738-739)
+template <int P>
+__device__ __forceinline__ void m_residual_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
   const Geom g = lv.g;
   const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
   double* ring = msm + threadIdx.y * (MNB * MSLOT);
@@ -256,20 +264,25 @@ __global__ void __launch_bounds__(32 * MW, 3) k_m_residual(const DevCtx* __restr
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
   if (lane == 0 && a.poff >= 0) c.pbase[a.poff + it.item] = ss;
 }
-
-// t_l = R_{l+1} t_{l+1} (restricts t, not r: PAPER.md:742-744), r_l = enc(t_l).
-// The warp owns 32 coarse columns; every coarse row consumes two fine rows.
 template <int P>
-__global__ void __launch_bounds__(32 * MW, 3) k_m_restrict(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
+__global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_residual(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+    const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
+  m_residual_item<P>(a, cf, it, msm);
+}
+
+// t_l = R_{l+1} t_{l+1} (restricts t, not r: PAPER.md:742-744), r_l = enc(t_l).
+// The warp owns 32 coarse columns; every coarse row consumes two fine rows.
+template <int P>
+__device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
   constexpr int NS = 4 * P - 1, H = 2 * P - 1;
-  const DevCtx& c = *cp;
-  const LevelDev& lc_ = c.lv[a.l];
-  const LevelDev& lf = c.lv[a.l + 1];
+  const MPtrs& c = a.p;
+  const LevelDev& lc_ = a.lv;
+  const LevelDev& lf = a.lo;
   const Geom gc = lc_.g, gf = lf.g;
   const int lane = threadIdx.x, xc = it.x0 + lane, nxb = gc.NX >> 5;
   const int txc = xc % P;
@@ -333,10 +346,20 @@ __global__ void __launch_bounds__(32 * MW, 3) k_m_restrict(const DevCtx* __restr
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
   if (lane == 0 && a.poff >= 0) c.pbase[a.poff + it.item] = ss;
 }
+template <int P>
+__global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_restrict(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+    const __grid_constant__ Coefs cf) {
+  extern __shared__ double msm[];
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  m_restrict_item<P>(a, cf, it, msm);
+}
 
 // ý_l = enc(y); w_l = z_l + dec ý_l (l < L); ú_l = enc(dec ú_l + dec ý_l);
 // u_l = dec ú_l + P u_{l-1}
-__device__ __forceinline__ void m_finalize(const DevCtx& c, const MArgs& a, const LevelDev& lv, long long idx,
+__device__ __forceinline__ void m_finalize(const MPtrs& c, const MArgs& a, const LevelDev& lv, long long idx,
                                            long long blk, double y, double zc, double pu, int lane) {
   const double yq = warp_encode(y, a.wr, nullptr, nullptr, lane, c.status);
   if (a.l < a.L) lv.W[idx] = zc + yq;
@@ -347,7 +370,7 @@ __device__ __forceinline__ void m_finalize(const DevCtx& c, const MArgs& a, cons
 }
 
 // m_finalize with the ú words / exponent and z, P u prefetched into registers
-__device__ __forceinline__ void m_finalize_r(const DevCtx& c, const MArgs& a, const LevelDev& lv, long long idx,
+__device__ __forceinline__ void m_finalize_r(const MPtrs& c, const MArgs& a, const LevelDev& lv, long long idx,
                                              long long blk, double y, double zc, double pu, uint32_t w0, uint32_t w1,
                                              int e, int lane) {
   const double yq = warp_encode(y, a.wr, nullptr, nullptr, lane, c.status);
@@ -361,15 +384,10 @@ __device__ __forceinline__ void m_finalize_r(const DevCtx& c, const MArgs& a, co
 // z_l = P w_{l-1} computed on the staged rows, b = dec r_l - A z_l;
 // stores Z (l < L), PU = P u_{l-1}, B; k == 1 finalises directly.
 template <int P>
-__global__ void __launch_bounds__(32 * MW, 3) k_m_cfas1(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
-  pdl_wait();
-  pdl_trigger();
-  MItem it;
-  if (!m_item(a, it)) return;
-  const DevCtx& c = *cp;
-  const LevelDev& lv = c.lv[a.l];
-  const LevelDev& lp = c.lv[a.l - 1];
+__device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
+  const LevelDev& lp = a.lo;
   const Geom g = lv.g, gp = lp.g;
   const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
   double* ring = msm + threadIdx.y * (MNB * MSLOT);
@@ -412,19 +430,24 @@ __global__ void __launch_bounds__(32 * MW, 3) k_m_cfas1(const DevCtx* __restrict
         }
       });
 }
-
-// Chebyshev step j >= 2: q = b - A y; d_j = fma(alpha_j, d_{j-1}, beta_j (invD q));
-// y_j = y_{j-1} + d_j (DESIGN.md §3.5).  Step 2 stages b and forms
-// y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
 template <int P>
-__global__ void __launch_bounds__(32 * MW, 3) k_m_cheb(const DevCtx* __restrict__ cp, MArgs a, const __grid_constant__ Coefs cf) {
+__global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+    const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  const DevCtx& c = *cp;
-  const LevelDev& lv = c.lv[a.l];
+  m_cfas1_item<P>(a, cf, it, msm);
+}
+
+// Chebyshev step j >= 2: q = b - A y; d_j = fma(alpha_j, d_{j-1}, beta_j (invD q));
+// y_j = y_{j-1} + d_j (DESIGN.md §3.5).  Step 2 stages b and forms
+// y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
+template <int P>
+__device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
   const Geom g = lv.g;
   const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
   const int j = a.step;
@@ -472,6 +495,16 @@ __global__ void __launch_bounds__(32 * MW, 3) k_m_cheb(const DevCtx* __restrict_
           c.Dv[idx] = d;
         }
       });
+}
+template <int P>
+__global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+    const __grid_constant__ Coefs cf) {
+  extern __shared__ double msm[];
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  m_cheb_item<P>(a, cf, it, msm);
 }
 
 // ------------------------------------------------------------------ host --

@@ -193,15 +193,15 @@ __device__ __forceinline__ size_t m3_ring_doubles() {
 // ------------------------------------------------------------ kernels --
 // t_L = f_L - A_L u_L, r_L = enc(t_L), ||t_L||^2 partial
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_residual(const DevCtx* __restrict__ cp, MArgs a,
+__global__ void __launch_bounds__(32 * TW3, 2) k_m3_residual(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                             const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
   pdl_trigger();
   M3Item it;
   m3_item(a, it);
-  const DevCtx& c = *cp;
-  const LevelDev& lv = c.lv[a.l];
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
   const Geom g = lv.g;
   const int lane = threadIdx.x, x = it.x0 + lane, y = it.y0 + threadIdx.y;
   const bool rowok = y < g.NY;
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(32 * TW3, 2) k_m3_residual(const DevCtx* __res
 
 // Chebyshev step 1: b = dec r_l - A z_l (z_l = P w_{l-1} staged
 // by k_m3_prolong); stores B; k == 1 finalises.
-__device__ __forceinline__ void m3_finalize(const DevCtx& c, const MArgs& a, const LevelDev& lv, long long idx,
+__device__ __forceinline__ void m3_finalize(const MPtrs& c, const MArgs& a, const LevelDev& lv, long long idx,
                                             long long blk, double y, double zc, double pu, uint32_t w0, uint32_t w1,
                                             int e, int lane) {
   const double yq = warp_encode(y, a.wr, nullptr, nullptr, lane, c.status);
@@ -249,15 +249,15 @@ __device__ __forceinline__ void m3_finalize(const DevCtx& c, const MArgs& a, con
 }
 
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_cfas1(const DevCtx* __restrict__ cp, MArgs a,
+__global__ void __launch_bounds__(32 * TW3, 2) k_m3_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                          const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
   pdl_trigger();
   M3Item it;
   m3_item(a, it);
-  const DevCtx& c = *cp;
-  const LevelDev& lv = c.lv[a.l];
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
   const Geom g = lv.g;
   const int lane = threadIdx.x, x = it.x0 + lane, y = it.y0 + threadIdx.y;
   const bool rowok = y < g.NY;
@@ -307,15 +307,15 @@ __global__ void __launch_bounds__(32 * TW3, 2) k_m3_cfas1(const DevCtx* __restri
 // Chebyshev step j >= 2; step 2 stages b and forms
 // y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_cheb(const DevCtx* __restrict__ cp, MArgs a,
+__global__ void __launch_bounds__(32 * TW3, 2) k_m3_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                         const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
   pdl_trigger();
   M3Item it;
   m3_item(a, it);
-  const DevCtx& c = *cp;
-  const LevelDev& lv = c.lv[a.l];
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
   const Geom g = lv.g;
   const int lane = threadIdx.x, w = threadIdx.y, x = it.x0 + lane, y = it.y0 + w;
   const bool rowok = y < g.NY;
@@ -407,15 +407,15 @@ __device__ __forceinline__ double pxy(const Coefs& cf, const double* __restrict_
 }
 
 template <int P>
-__global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restrict__ cp, MArgs a,
+__global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                         const __grid_constant__ Coefs cf) {
   pdl_wait();
   pdl_trigger();
   M3Item it;
   m3_item(a, it);
-  const DevCtx& c = *cp;
-  const LevelDev& lv = c.lv[a.l];
-  const LevelDev& lp = c.lv[a.l > 0 ? a.l - 1 : 0];
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
+  const LevelDev& lp = a.lo;
   const Geom g = lv.g, gp = lp.g;
   const int lane = threadIdx.x, x = it.x0 + lane, y = it.y0 + threadIdx.y;
   if (y >= g.NY) return;  // (no collectives across warps here)
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restric
 // last 4p-1 fine planes (two new planes per coarse output plane).
 constexpr int RPF3 = 2, RNB3 = 3, RRS3 = 80;
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_restrict(const DevCtx* __restrict__ cp, MArgs a,
+__global__ void __launch_bounds__(32 * TW3, 2) k_m3_restrict(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                             const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
@@ -476,9 +476,9 @@ __global__ void __launch_bounds__(32 * TW3, 2) k_m3_restrict(const DevCtx* __res
   M3Item it;
   m3_item(a, it);
   constexpr int NS = 4 * P - 1, H = 2 * P - 1, FR = 2 * TW3 + 2 * H, FW = 64 + 2 * H;
-  const DevCtx& c = *cp;
-  const LevelDev& lc_ = c.lv[a.l];
-  const LevelDev& lf = c.lv[a.l + 1];
+  const MPtrs& c = a.p;
+  const LevelDev& lc_ = a.lv;
+  const LevelDev& lf = a.lo;
   const Geom gc = lc_.g, gf = lf.g;
   const int lane = threadIdx.x, w = threadIdx.y, xc = it.x0 + lane, yc = it.y0 + w;
   const bool rowok = yc < gc.NY;
