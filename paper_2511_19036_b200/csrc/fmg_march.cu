@@ -26,7 +26,7 @@ namespace fmg {
 #define FMG_MARCH_MINB 3     // CTAs per SM the register budget is sized for
 #endif
 constexpr int MW = 8;        // warps per CTA
-constexpr int MNB = 8;       // staged rows per warp (ring; >= MPF + p + 1)
+constexpr int MNB = 8;       // staged rows per warp (ring; >= MPF + p + 1, >= 2p + 1)
 constexpr int MPF = 4;       // rows staged ahead
 constexpr int MSLOT = 80;    // doubles per staged row (>= 64 + 4p - 2 + 1)
 
@@ -147,6 +147,40 @@ __device__ __forceinline__ void march_A(const Coefs& cf, int ys, int ye, int x, 
   }
   const int nin = (ye - ys) + 2 * P, y0 = ys - P;
   using AuxT = decltype(pre(0));
+  if (ye - ys == 1) {
+    // single output row: all 2P+1 input rows in flight at once, independent x passes
+#pragma unroll
+    for (int i = 0; i < R; ++i) stage(y0 + i, ring + i * MSLOT);
+    cp_commit();
+    const AuxT a1 = pre(ys);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < R; ++i) xform(y0 + i, ring + i * MSLOT);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double* row = ring + i * MSLOT;
+      double s = 0.0, t = 0.0;
+#pragma unroll
+      for (int o = 0; o < R; ++o) {
+        const double v = row[lane + o];
+        s = fma(km[o], v, s);
+        t = fma(kk[o], v, t);
+      }
+      ra[i] = s;
+      rb[i] = t;
+    }
+    const int ty = ys % P;
+    double d = 0.0, e = 0.0;
+#pragma unroll
+    for (int o = 0; o < R; ++o) {
+      d = fma(cf.Kc[ty][o], ra[o], d);
+      e = fma(cf.Mc[ty][o], rb[o], e);
+    }
+    out(ys, d + e, ring + P * MSLOT, a1);
+    __syncwarp();
+    return;
+  }
   AuxT cur{}, nxt{};
 #pragma unroll
   for (int i = 0; i < MPF; ++i) {
