@@ -82,11 +82,14 @@ class Schedule(C.Structure):
 
     _fields_ = [("b_u", C.c_int), ("k_u", C.c_int), ("b_r", C.c_int), ("k_r", C.c_int),
                 ("n_ir", C.c_int), ("cheb_degree", C.c_int),
-                ("lambda_hi", C.c_double), ("alpha", C.c_double)]
+                ("lambda_hi", C.c_double), ("alpha", C.c_double), ("smoother", C.c_int)]
+
+
+SMOOTHERS = {"chebyshev": 0, "mcgs": 1, "lexgs": 2}
 
 
 def schedule(d: int, p: int, b_u=None, b_r=None, n_ir=None, k_u=None, k_r=1,
-             cheb_degree=None, lambda_hi=None, alpha=None) -> Schedule:
+             cheb_degree=None, lambda_hi=None, alpha=None, smoother="chebyshev") -> Schedule:
     """Default schedule of DESIGN.md §5 (same numbers the product path uses)."""
     from fmg_inputs import default_schedule
     s = default_schedule(d, p)
@@ -96,7 +99,7 @@ def schedule(d: int, p: int, b_u=None, b_r=None, n_ir=None, k_u=None, k_r=1,
         if v is not None:
             s[k] = v
     return Schedule(s["b_u"], s["k_u"], s["b_r"], s["k_r"], s["n_ir"], s["cheb_degree"],
-                    s["lambda_hi"], s["alpha"])
+                    s["lambda_hi"], s["alpha"], SMOOTHERS[smoother] if isinstance(smoother, str) else smoother)
 
 
 @dataclass
@@ -269,6 +272,14 @@ class CFMG:
         rc = lib().orc_residual(self.h, L, _dp(nr))
         assert rc == 0
         return nr
+
+    def smooth(self, l: int, b: np.ndarray) -> np.ndarray:
+        """The schedule's cFas smoother on level l from y = 0 (orc_smooth)."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        y = np.zeros_like(b)
+        rc = lib().orc_smooth(self.h, l, _dp(b), _dp(y))
+        assert rc == 0
+        return y
 
     def cfas_correct(self, L):
         rc = lib().orc_cfas_correct(self.h, L)

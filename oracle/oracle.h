@@ -36,6 +36,9 @@ typedef struct {
   int cheb_degree;   /* k: Chebyshev-Jacobi degree (reading R4) */
   double lambda_hi;  /* upper eigenvalue bound of D^-1 A used by Chebyshev */
   double alpha;      /* lower bound = lambda_hi / alpha */
+  int smoother;      /* 0 Chebyshev-Jacobi (R4), 1 multicolor Gauss-Seidel with
+                        (p+1)^d colours, 2 lexicographic Gauss-Seidel (PAPER.md:689-690,
+                        1624; oracle only) -- SURVEY §8f N1 */
 } orc_schedule;
 
 /* ---- grid geometry of level l ---- */
@@ -80,6 +83,7 @@ typedef struct orc_ctx orc_ctx;
 int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out);
 void orc_destroy(orc_ctx* c);
 int orc_solve(orc_ctx* c);                         /* Alg 3.3 from scratch */
+int orc_smooth(orc_ctx* c, int l, const double* b, double* y); /* cFas smoother from y = 0 */
 int orc_solve_upto(orc_ctx* c, int Lstop, int iters_last); /* partial solve, for tests */
 int orc_residual(orc_ctx* c, int L, double* norms);/* Alg 3.2 at FMG level L */
 int orc_cfas_correct(orc_ctx* c, int L);           /* Alg 3.1 + correction */

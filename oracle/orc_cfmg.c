@@ -108,6 +108,7 @@ int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out) {
   *out = NULL;
   if ((d != 2 && d != 3) || p < 1 || p > 3 || levels < 1 || levels > ORC_MAXLEV) return ORC_EINVAL;
   if (s->b_u < 2 || s->b_r < 2 || s->n_ir < 1 || s->cheb_degree < 1 || s->cheb_degree > 8) return ORC_EINVAL;
+  if (s->smoother < 0 || s->smoother > 2) return ORC_EINVAL;
   int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return ORC_EINVAL;
   orc_ctx* c = calloc(1, sizeof(orc_ctx));
@@ -222,6 +223,83 @@ static void chebyshev(const orc_ctx* c, int l, const double* b, double* y) {
   free(dv); free(ay);
 }
 
+/* Colour of node (x, y, z) in the multicolour ordering: nodes of one colour
+ * differ by a multiple of p+1 in every index, so (stencil reach p) no two of
+ * them are coupled and a colour's updates are independent. */
+static int gs_colour(int p, int x, int y, int z) {
+  return ((z % (p + 1)) * (p + 1) + (y % (p + 1))) * (p + 1) + (x % (p + 1));
+}
+
+/* One Gauss-Seidel sweep from y = 0 on A_l y = b (the smoother y <- y + M(b - A y)
+ * of eq:smoother PAPER.md:521-525 with M the forward Gauss-Seidel sweep, as in
+ * the paper's experiments PAPER.md:689-690, 1624), multicolour
+ * order: for each colour c = 0 .. (p+1)^d - 1, every node i of colour c:
+ *   y_i = y_i + invD_i (b_i - (A y)_i)          (mul, then add; A canonical)  */
+static void mc_gauss_seidel(const orc_ctx* c, int l, const double* b, double* y) {
+  const orc_level* g = &c->g[l];
+  const double* iD = c->invD[l];
+  const int p = c->p, nc = c->d == 3 ? (p + 1) * (p + 1) * (p + 1) : (p + 1) * (p + 1);
+  double* ay = malloc(sizeof(double) * g->size);
+  for (int64_t i = 0; i < g->size; ++i) y[i] = 0.0;
+  for (int col = 0; col < nc; ++col) {
+    orc_apply_A(c->d, p, l, y, ay);
+    for (int z = 0; z < g->NZ; ++z)
+      for (int yy = 0; yy < g->NY; ++yy)
+        for (int x = 0; x < g->NX; ++x) {
+          if (gs_colour(p, x, yy, z) != col) continue;
+          int64_t i = ((int64_t)z * g->NY + yy) * g->NX + x;
+          y[i] = y[i] + iD[i] * (b[i] - ay[i]);
+        }
+  }
+  free(ay);
+}
+
+/* One lexicographic (x fastest) Gauss-Seidel sweep from y = 0 -- the paper's
+ * ordering assumption -- with (A y)_i taken pointwise from the
+ * assembled tensor-product stencil (oracle only; no GPU counterpart). */
+static void lex_gauss_seidel(const orc_ctx* c, int l, const double* b, double* y) {
+  const orc_level* g = &c->g[l];
+  const double* iD = c->invD[l];
+  const int d = c->d, p = c->p, n = g->n, R = 2 * p + 1;
+  double Kc[3 * 7], Mc[3 * 7];
+  orc_coef_A(p, Kc, Mc);
+  const double hs = d == 3 ? ldexp(1.0, -(l + 1)) : 1.0;
+  for (int64_t i = 0; i < g->size; ++i) y[i] = 0.0;
+  for (int z = (d == 3 ? 1 : 0); z <= (d == 3 ? n - 1 : 0); ++z)
+    for (int yy = 1; yy <= n - 1; ++yy)
+      for (int x = 1; x <= n - 1; ++x) {
+        const int tx = x % p, ty = yy % p, tz = z % p;
+        double s = 0.0;
+        for (int oz = (d == 3 ? -p : 0); oz <= (d == 3 ? p : 0); ++oz)
+          for (int oy = -p; oy <= p; ++oy)
+            for (int ox = -p; ox <= p; ++ox) {
+              const int xx = x + ox, y2 = yy + oy, z2 = z + oz;
+              if (xx < 1 || xx > n - 1 || y2 < 1 || y2 > n - 1 || (d == 3 && (z2 < 1 || z2 > n - 1))) continue;
+              const double mx = Mc[tx * R + ox + p], kx = Kc[tx * R + ox + p];
+              const double my = Mc[ty * R + oy + p], ky = Kc[ty * R + oy + p];
+              double cf;
+              if (d == 2) {
+                cf = kx * my + mx * ky;
+              } else {
+                const double mz = Mc[tz * R + oz + p], kz = Kc[tz * R + oz + p];
+                cf = (kx * my * mz + mx * ky * mz + mx * my * kz) * hs;
+              }
+              s += cf * y[((int64_t)(d == 3 ? z2 : 0) * g->NY + y2) * g->NX + xx];
+            }
+        const int64_t i = ((int64_t)(d == 3 ? z : 0) * g->NY + yy) * g->NX + x;
+        y[i] = y[i] + iD[i] * (b[i] - s);
+      }
+}
+
+/* The cFas smoother of the schedule on level l from y = 0 (test access). */
+int orc_smooth(orc_ctx* c, int l, const double* b, double* y) {
+  if (l < 1 || l > c->Lmax) return ORC_EINVAL;
+  if (c->s.smoother == 1) mc_gauss_seidel(c, l, b, y);
+  else if (c->s.smoother == 2) lex_gauss_seidel(c, l, b, y);
+  else chebyshev(c, l, b, y);
+  return ORC_OK;
+}
+
 /* Alg 3.1 cFas (nu = 1: y = 0, s = 0) followed by the correction PAPER.md:798. */
 int orc_cfas_correct(orc_ctx* c, int L) {
   int d = c->d, p = c->p, rc;
@@ -249,7 +327,9 @@ int orc_cfas_correct(orc_ctx* c, int L) {
     orc_apply_A(d, p, l, z, az);
     sec_decode(&c->r[l], g, rb);
     for (int64_t i = 0; i < N; ++i) rb[i] = rb[i] - az[i];  /* b = r_l - A_l z_l */
-    chebyshev(c, l, rb, yv);                         /* smooth from ý_l = 0 */
+    if (c->s.smoother == 1) mc_gauss_seidel(c, l, rb, yv);      /* smooth from ý_l = 0 */
+    else if (c->s.smoother == 2) lex_gauss_seidel(c, l, rb, yv);
+    else chebyshev(c, l, rb, yv);
     rc = sec_encode(&c->y[l], g, yv, wr(c, l, L));   /* fix: store at w_r(l,L) */
     if (!rc) {
       sec_decode(&c->y[l], g, yv);
