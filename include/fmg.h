@@ -57,6 +57,9 @@ typedef struct {
   int cheb_degree;
   double lambda_hi;
   double alpha;
+  int smoother; /* 0: Chebyshev-Jacobi of degree cheb_degree (R4);
+                   1: one multicolour Gauss-Seidel sweep, (p+1)^d colours
+                   (the paper's smoother family PAPER.md:1624) */
 } fmg_schedule;
 
 typedef struct fmg_ctx fmg_ctx;

@@ -224,6 +224,11 @@ void build_residual_grid(Builder& b, int L, int row) {
   }
 }
 
+int ncolours(const fmg_ctx* c) {
+  const int q = c->p + 1;
+  return c->dim == 3 ? q * q * q : q * q;
+}
+
 // One IR iteration at FMG level L: fmgResidual (Alg 3.2),
 // cFas V(0,1) (Alg 3.1, nu = 1), correction.  Levels <= lc run inside KC.
 void build_iteration(Builder& b, int L, int it) {
@@ -270,11 +275,13 @@ void build_iteration(Builder& b, int L, int it) {
       b.grid(q);
       b.xchg(XA_Z, l, P);
     }
-    for (int step = 1; step <= k; ++step) {
-      if (step >= 2) b.xchg(step == 2 ? XA_B : ((step - 1) & 1 ? XA_Y1 : XA_Y0), l, P);
-      OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
-      q.step = step;
-      q.last = step == k;
+    const bool gs = c->s.smoother == 1;
+    const int nsteps = gs ? ncolours(c) : k;  // GS: colour 0 in cFas1, then colours 1 .. (p+1)^d - 1
+    for (int step = 1; step <= nsteps; ++step) {
+      if (step >= 2) b.xchg(gs ? XA_Y1 : (step == 2 ? XA_B : ((step - 1) & 1 ? XA_Y1 : XA_Y0)), l, P);
+      OpDesc q = mkop(step == 1 ? OP_CFAS1 : (gs ? OP_GS : OP_CHEB), l, L);
+      q.step = gs ? step - 1 : step;
+      q.last = step == nsteps;
       q.wr = wr(c, l, L);
       q.wu_in = c->wu_cur[l];
       q.wu_out = wu(c, l, L);
@@ -393,6 +400,7 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
   m.NZo = c->g[o.l].NZ;
   m.zlo = c->zlo[o.l];
   m.zhi = c->zhi[o.l];
+  m.gs = c->s.smoother;
   m.poff = o.poff;
   m.lv = level_dev(c, o.l);
   const int lo = o.type == OP_RESTRICT ? o.l + 1 : o.l - 1;
@@ -691,7 +699,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   *out = nullptr;
   if ((dim != 2 && dim != 3) || p < 1 || p > 3 || levels < 1 || levels > kMaxLev) return FMG_EINVAL;
   if (s->b_u < 2 || s->b_r < 2 || s->k_u < 0 || s->k_r < 0 || s->n_ir < 1 || s->cheb_degree < 1 ||
-      s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1))
+      s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1) || s->smoother < 0 || s->smoother > 1)
     return FMG_EINVAL;
   int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
@@ -706,6 +714,10 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   march_set_attributes();
   march3_set_attributes();
   c->march = !(getenv("FMG_MARCH") && atoi(getenv("FMG_MARCH")) == 0);
+  if (s->smoother == 1 && !c->march) {  // (the tile-box kernels implement Chebyshev only)
+    fmg_destroy(c);
+    return FMG_EINVAL;
+  }
   if (getenv("FMG_SYNC_DEBUG")) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fprintf(stderr, "[fmg] set_kernel_attributes: %s\n", cudaGetErrorString(e));
@@ -857,6 +869,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       dd.kc = c->kcl;
       dd.lc = c->lc;
       dd.n_cheb = s->cheb_degree;
+      dd.smoother = s->smoother;
       dd.Ainv = c->Ainv;
       dd.norms = c->norms_dev;
       dd.status = c->status;

@@ -194,6 +194,7 @@ struct __align__(16) DevCtx {
   double* pbase; // norm partials of the grid levels (one slot per FMG level, iteration, level)
   int lc;        // the cluster kernel (fmg_kc.cu) handles levels 0..lc
   int n_cheb;    // Chebyshev degree k
+  int smoother;  // 0 Chebyshev, 1 multicolour Gauss-Seidel
   double* Z;     // z_l (only for l < L)
   double* B;     // b_l = dec r_l - A z_l
   double* Y[2];  // Chebyshev iterates (k >= 3)

@@ -45,7 +45,7 @@ int coarse_count(int dim, int p);
 int build_coarse_inverse(int dim, int p, double* Ainv);  // 0 on success
 
 // Operation descriptors (mirrors the device Op).
-enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_CFAS1 = 6, OP_CHEB, OP_PROLONG };
+enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_CFAS1 = 6, OP_CHEB, OP_PROLONG, OP_GS };
 struct OpDesc {
   int type, l, L, step, last;
   int wr, wu_in, wu_out;
@@ -85,6 +85,7 @@ struct MArgs {
   int RC, nxb, nitems, NYo;  // rows (2D) / planes (3D) per chunk, block columns, work items (3D: CTAs), output rows
   int nyb, NZo;              // 3D: tile rows (of 8), output planes
   int zlo, zhi;              // 3D: the planes of this rank (z slab), [zlo, zhi)
+  int gs;                    // smoother: multicolour Gauss-Seidel (cFas1 forms colour 0; OP_GS: colour `step`)
   // operands in the parameter space (no dependent global loads at kernel start)
   LevelDev lv;               // the output level l
   LevelDev lo;               // the other level: l-1 (decode, prolongation, cFas) or l+1 (restriction)
@@ -143,6 +144,7 @@ struct DevCtxDesc {
   double* norms;
   int* status;
   int lc, n_cheb;
+  int smoother;  // 0 Chebyshev, 1 multicolour Gauss-Seidel
   Coefs cf;
 };
 

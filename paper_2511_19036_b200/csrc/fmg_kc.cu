@@ -559,7 +559,11 @@ struct Kc {
       double rv = kc_dec(rmw(l, b), *rex(l, b), wrl);
       double bb = rv - az;
       double d = cf.inv_theta * (invd(g, x, y, z) * bb);
-      if (k == 1) {
+      if (c.smoother == 1) {  // multicolour GS from y = 0: colour 0 gets y = 0 + invD (b - 0)
+        own(ly.B, nb, idx) = bb;
+        const bool c0 = x % (P + 1) == 0 && y % (P + 1) == 0 && (D == 2 || z % (P + 1) == 0);
+        own(ly.Y1, nb, idx) = c0 ? 0.0 + invd(g, x, y, z) * (bb - 0.0) : 0.0;
+      } else if (k == 1) {
         finalize(l, L, it, idx, b, nb, d);
       } else {
         own(ly.B, nb, idx) = bb;
@@ -586,6 +590,22 @@ struct Kc {
         own(yn, nb, idx) = yv;
         own(ly.Dv, nb, idx) = d;
       }
+    });
+  }
+
+  // Multicolour Gauss-Seidel colour col >= 1 on Y1 in place (nodes of one colour
+  // are uncoupled); the last colour finalises (oracle mc_gauss_seidel).
+  __device__ __noinline__ void ph_gs(int l, int L, int it, int col, int ncol) const {
+    const Geom& g = c.lv[l].g;
+    const int cx = col % (P + 1), cy = (col / (P + 1)) % (P + 1), cz = col / ((P + 1) * (P + 1));
+    blocks(g, [&](int x0, int y, int z, long long idx, long long b, int nb) {
+      const int x = x0 + LANE;
+      const double ay = Aat(ly.Y1, g, x0, y, z);
+      const bool mine = x % (P + 1) == cx && y % (P + 1) == cy && (D == 2 || z % (P + 1) == cz);
+      const double yo = own(ly.Y1, nb, idx);
+      const double yv = mine ? yo + invd(g, x, y, z) * (own(ly.B, nb, idx) - ay) : yo;
+      if (col == ncol - 1) finalize(l, L, it, idx, b, nb, yv);
+      else if (mine) own(ly.Y1, nb, idx) = yv;
     });
   }
 
@@ -627,6 +647,18 @@ struct Kc {
       }
       ph_cheb1(l, L, it);
       csync(dbg);
+      if (c.smoother == 1) {
+        const int ncol = D == 3 ? (P + 1) * (P + 1) * (P + 1) : (P + 1) * (P + 1);
+        for (int col = 1; col < ncol; ++col) {
+          if constexpr (D == 3) {
+            ph_A3xy(ly.Y1, c.lv[l].g);
+            csync(dbg);
+          }
+          ph_gs(l, L, it, col, ncol);
+          csync(dbg);
+        }
+        continue;
+      }
       for (int j = 2; j <= c.n_cheb; ++j) {
         if constexpr (D == 3) {
           ph_A3xy((j - 1) & 1 ? ly.Y1 : ly.Y0, c.lv[l].g);

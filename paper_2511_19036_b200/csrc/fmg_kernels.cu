@@ -1018,6 +1018,7 @@ void fill_devctx(void* host_buf, const DevCtxDesc& d) {
   c->pbase = d.pbase;
   c->lc = d.lc;
   c->n_cheb = d.n_cheb;
+  c->smoother = d.smoother;
   c->Z = d.Z;
   c->PU = d.PU;
   c->KS[0] = d.KS[0];

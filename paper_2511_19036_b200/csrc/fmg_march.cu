@@ -456,12 +456,56 @@ __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, co
         const long long idx = (long long)y * g.NX + x, blk = (long long)y * nxb + (it.x0 >> 5);
         const double rv = warp_decode_r(r.w0, r.e, a.wr, lane, r.w1);
         const double b = rv - az;
-        if (a.last) {  // k == 1: y = d_1 = inv_theta (invD b)
+        if (a.gs) {  // multicolour GS from y = 0: colour 0 gets y = 0 + invD (b - 0), others 0
+          c.B[idx] = b;
+          const bool c0 = x % (P + 1) == 0 && y % (P + 1) == 0;
+          c.Y[1][idx] = c0 ? 0.0 + invd2(cf, P, g.n, x, y) * (b - 0.0) : 0.0;
+        } else if (a.last) {  // k == 1: y = d_1 = inv_theta (invD b)
           const double d = cf.inv_theta * (invd2(cf, P, g.n, x, y) * b);
           m_finalize(c, a, lv, idx, blk, d, slot[P + lane], c.PU[idx], lane);
         } else {
           c.B[idx] = b;
         }
+      });
+}
+
+// Multicolour Gauss-Seidel colour `a.step` (>= 1) in place on Y[1]: at the
+// nodes of that colour y = y + invD (b - A y) (A on the current iterate; nodes
+// of one colour are uncoupled, so in-place is exact); the last colour
+// finalises every node of the row (oracle mc_gauss_seidel).
+template <int P>
+__device__ __forceinline__ void m_gs_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
+  const Geom g = lv.g;
+  const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
+  double* ring = msm + threadIdx.y * (MNB * MSLOT);
+  double* __restrict__ Yv = c.Y[1];
+  const int cx = a.step % (P + 1), cy = a.step / (P + 1);
+  const bool colx = x % (P + 1) == cx;
+  march_A<P>(
+      cf, it.ys, it.ye, x, ring, [&](int yy, double* slot) { stage_row(Yv, g, it.x0, yy, P, slot, lane); },
+      [&](int, double*) {},
+      [&](int yn) {
+        const long long idx = (long long)yn * g.NX + x, blk = (long long)yn * nxb + (it.x0 >> 5);
+        CAux q{};
+        q.b = c.B[idx];
+        if (a.last) {
+          q.z = a.l < a.L ? c.Z[idx] : 0.0;
+          q.pu = c.PU[idx];
+          q.w0 = lane < a.wu_in ? lv.umant[blk * lv.ustride + lane] : 0u;
+          q.w1 = lane + 32 < a.wu_in ? lv.umant[blk * lv.ustride + lane + 32] : 0u;
+          q.e = lv.uexp[blk];
+        }
+        return q;
+      },
+      [&](int y, double ay, const double* slot, const CAux& p) {
+        const long long idx = (long long)y * g.NX + x, blk = (long long)y * nxb + (it.x0 >> 5);
+        const bool mine = colx && y % (P + 1) == cy;
+        const double yo = slot[P + lane];
+        const double yv = mine ? yo + invd2(cf, P, g.n, x, y) * (p.b - ay) : yo;
+        if (a.last) m_finalize_r(c, a, lv, idx, blk, yv, p.z, p.pu, p.w0, p.w1, p.e, lane);
+        else if (mine) Yv[idx] = yv;
       });
 }
 template <int P>
@@ -541,6 +585,17 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx
   m_cheb_item<P>(a, cf, it, msm);
 }
 
+template <int P>
+__global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+    const __grid_constant__ Coefs cf) {
+  extern __shared__ double msm[];
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  m_gs_item<P>(a, cf, it, msm);
+}
+
 // ------------------------------------------------------------------ host --
 int march_smem() { return MW * MNB * MSLOT * 8; }
 int march_warps() { return MW; }
@@ -557,7 +612,8 @@ void march_set_attributes() {
   cudaFuncSetAttribute(k_m_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());     \
   cudaFuncSetAttribute(k_m_restrict<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());     \
   cudaFuncSetAttribute(k_m_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());        \
-  cudaFuncSetAttribute(k_m_cheb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());
+  cudaFuncSetAttribute(k_m_cheb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());      \
+  cudaFuncSetAttribute(k_m_gs<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());
   F(1) F(2) F(3)
 #undef F
 }
@@ -587,6 +643,7 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
     case OP_RESIDUAL: m_launch(k_m_residual<P>, a.nitems, sm, st, c, a, cf); break;     \
     case OP_RESTRICT: m_launch(k_m_restrict<P>, a.nitems, sm, st, c, a, cf); break;     \
     case OP_CFAS1: m_launch(k_m_cfas1<P>, a.nitems, sm, st, c, a, cf); break;           \
+    case OP_GS: m_launch(k_m_gs<P>, a.nitems, sm, st, c, a, cf); break;                 \
     default: m_launch(k_m_cheb<P>, a.nitems, sm, st, c, a, cf); break;                  \
   }
   M_DISPATCH(p, F);

@@ -292,7 +292,11 @@ __global__ void __launch_bounds__(32 * TW3, 2) k_m3_cfas1(const DevCtx* __restri
         const long long blk = ((long long)z * g.NY + y) * nxb + (it.x0 >> 5);
         const double rv = warp_decode_r3(q.w0, q.e, a.wr, lane, q.w1);
         const double b = rv - az;
-        if (a.last) {  // k == 1: y = d_1 = inv_theta (invD b)
+        if (a.gs) {  // multicolour GS from y = 0: colour 0 gets y = 0 + invD (b - 0), others 0
+          c.B[idx] = b;
+          const bool c0 = x % (P + 1) == 0 && y % (P + 1) == 0 && z % (P + 1) == 0;
+          c.Y[1][idx] = c0 ? 0.0 + invd3(cf, P, g.n, a.l, x, y, z) * (b - 0.0) : 0.0;
+        } else if (a.last) {  // k == 1: y = d_1 = inv_theta (invD b)
           const double d = cf.inv_theta * (invd3(cf, P, g.n, a.l, x, y, z) * b);
           const double zc = slot[(threadIdx.y + P) * RS3 + P + lane];
           uint32_t* uw = lv.umant + blk * lv.ustride;
@@ -376,6 +380,60 @@ __global__ void __launch_bounds__(32 * TW3, 2) k_m3_cheb(const DevCtx* __restric
           c.Y[j & 1][idx] = yv;
           c.Dv[idx] = d;
         }
+      });
+}
+
+// Multicolour Gauss-Seidel colour `a.step` (>= 1) in place on Y[1]
+// (oracle mc_gauss_seidel): y = y + invD (b - A y) at the nodes
+// of the colour, the last colour finalises every node.
+template <int P>
+__global__ void __launch_bounds__(32 * TW3, 2) k_m3_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+                                                      const __grid_constant__ Coefs cf) {
+  extern __shared__ double msm[];
+  pdl_wait();
+  pdl_trigger();
+  M3Item it;
+  m3_item(a, it);
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
+  const Geom g = lv.g;
+  const int lane = threadIdx.x, w = threadIdx.y, x = it.x0 + lane, y = it.y0 + w;
+  const bool rowok = y < g.NY;
+  double* ring = msm;
+  double* XA = ring + m3_ring_doubles<P>();
+  double* XB = XA + (TW3 + 2 * P) * 32;
+  const int nxb = g.NX >> 5;
+  double* __restrict__ Yv = c.Y[1];
+  const int cx = a.step % (P + 1), cy = (a.step / (P + 1)) % (P + 1), cz = a.step / ((P + 1) * (P + 1));
+  const bool colxy = x % (P + 1) == cx && y % (P + 1) == cy;
+  march3_A<P>(
+      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) { stage_box(Yv, g, it.x0, it.y0, zz, P, slot); },
+      [&](int, double*) {},
+      [&](int zn) {
+        CAux3 q{};
+        if (rowok) {
+          const long long idx = ((long long)zn * g.NY + y) * g.NX + x;
+          const long long blk = ((long long)zn * g.NY + y) * nxb + (it.x0 >> 5);
+          q.b = c.B[idx];
+          if (a.last) {
+            q.z = a.l < a.L ? c.Z[idx] : 0.0;
+            q.pu = c.PU[idx];
+            q.w0 = lane < a.wu_in ? lv.umant[blk * lv.ustride + lane] : 0u;
+            q.w1 = lane + 32 < a.wu_in ? lv.umant[blk * lv.ustride + lane + 32] : 0u;
+            q.e = lv.uexp[blk];
+          }
+        }
+        return q;
+      },
+      [&](int z, double ay, const double* slot, const CAux3& q) {
+        if (!rowok) return;
+        const long long idx = ((long long)z * g.NY + y) * g.NX + x;
+        const long long blk = ((long long)z * g.NY + y) * nxb + (it.x0 >> 5);
+        const bool mine = colxy && z % (P + 1) == cz;
+        const double yo = slot[(w + P) * RS3 + P + lane];
+        const double yv = mine ? yo + invd3(cf, P, g.n, a.l, x, y, z) * (q.b - ay) : yo;
+        if (a.last) m3_finalize(c, a, lv, idx, blk, yv, q.z, q.pu, q.w0, q.w1, q.e, lane);
+        else if (mine) Yv[idx] = yv;
       });
 }
 
@@ -569,6 +627,7 @@ void march3_set_attributes() {
   cudaFuncSetAttribute(k_m3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));     \
   cudaFuncSetAttribute(k_m3_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));        \
   cudaFuncSetAttribute(k_m3_cheb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));         \
+  cudaFuncSetAttribute(k_m3_gs<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));           \
   cudaFuncSetAttribute(k_m3_restrict<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_R(P));
   F(1) F(2) F(3)
 #undef F
@@ -600,6 +659,7 @@ void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, c
     case OP_RESIDUAL: m3_launch(k_m3_residual<P>, n, m3_smem_A(P), st, c, a, cf); break;      \
     case OP_RESTRICT: m3_launch(k_m3_restrict<P>, n, m3_smem_R(P), st, c, a, cf); break;      \
     case OP_CFAS1: m3_launch(k_m3_cfas1<P>, n, m3_smem_A(P), st, c, a, cf); break;            \
+    case OP_GS: m3_launch(k_m3_gs<P>, n, m3_smem_A(P), st, c, a, cf); break;                  \
     default: m3_launch(k_m3_cheb<P>, n, m3_smem_A(P), st, c, a, cf); break;                   \
   }
   if (p == 1) { F(1) } else if (p == 2) { F(2) } else { F(3) }

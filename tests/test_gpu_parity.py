@@ -273,3 +273,50 @@ def test_nccl_dist_single_rank(P):
     assert np.array_equal(s1.norms(), sd.norms())
     for l in range(4):
         assert np.array_equal(s1.section(0, l)[0], sd.section(0, l)[0])
+
+
+# ------------------------------------------ Gauss-Seidel smoother (§8f N1) --
+@pytest.mark.parametrize("d,p,levels", [(2, 1, 6), (2, 2, 5), (2, 3, 4), (3, 1, 5), (3, 2, 4), (3, 3, 3)])
+def test_fmg_parity_multicolour_gs(P, d, p, levels):
+    """Multicolour Gauss-Seidel smoother ((p+1)^d colours): GPU (KC + march
+    colour kernels) bit-identical to the oracle's mc_gauss_seidel."""
+    so = O.schedule(d, p, smoother="mcgs")
+    oc = O.CFMG(d, p, levels, so)
+    oc.solve()
+    gs = P.Solver(d, p, levels, _gpu_sched(P, d, p, smoother=1))
+    gs.solve()
+    no, ng = oc.norms(), gs.norms()
+    m = no != 0
+    assert np.all(np.abs(ng[m] - no[m]) <= 1e-6 * no[m])
+    for l in range(levels):
+        for which in (0, 1):
+            mo, eo, _ = oc.section(which, l)
+            mg, eg, _ = gs.section(which, l)
+            assert np.array_equal(eo, eg) and np.array_equal(mo, mg), (which, l)
+    eo, eg = oc.errors(), gs.errors()
+    assert np.all(np.abs(eg - eo) <= 1e-3 * eo)
+
+
+def test_fmg_parity_multicolour_gs_C2_full(P):
+    c = CONFIGS["C2"]
+    d, p, levels = c["dim"], c["p"], c["levels"]
+    oc = O.CFMG(d, p, levels, O.schedule(d, p, smoother="mcgs"))
+    oc.solve()
+    gs = P.Solver(d, p, levels, _gpu_sched(P, d, p, smoother=1))
+    gs.solve()
+    for l in range(levels):
+        mo, eo, _ = oc.section(0, l)
+        mg, eg, _ = gs.section(0, l)
+        assert np.array_equal(eo, eg) and np.array_equal(mo, mg), l
+    no, ng = oc.norms(), gs.norms()
+    m = no != 0
+    assert np.all(np.abs(ng[m] - no[m]) <= 1e-6 * no[m])
+
+
+def test_slab_decomposition_gs(P):
+    s1 = P.Solver(3, 1, 6, _gpu_sched(P, 3, 1, smoother=1))
+    s1.solve()
+    sg = P.Solver(3, 1, 6, _gpu_sched(P, 3, 1, smoother=1), slabs=4)
+    sg.solve()
+    for l in range(6):
+        assert np.array_equal(s1.section(0, l)[0], sg.section(0, l)[0]), l
