@@ -64,7 +64,11 @@ __device__ __noinline__ void kc_stamp() {  // debug phase stamps
   }
 }
 __device__ __forceinline__ void csync(bool dbg = false) {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (gridDim.x == 1) {  // one-CTA "cluster": all level data is local shared memory
+    __syncthreads();
+  } else {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   if (dbg) kc_stamp();
 }
 

@@ -22,6 +22,9 @@
 
 namespace fmg {
 
+#ifndef FMG_MARCH3_MINB
+#define FMG_MARCH3_MINB 2    // CTAs per SM the register budget is sized for
+#endif
 constexpr int TW3 = 8;       // warps per CTA = tile rows
 constexpr int PF3 = 3;       // planes staged ahead
 constexpr int NB3 = 8;       // staged plane ring (>= PF3 + p + 2)
@@ -193,7 +196,7 @@ __device__ __forceinline__ size_t m3_ring_doubles() {
 // ------------------------------------------------------------ kernels --
 // t_L = f_L - A_L u_L, r_L = enc(t_L), ||t_L||^2 partial
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_residual(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+__global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_residual(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                             const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
@@ -249,7 +252,7 @@ __device__ __forceinline__ void m3_finalize(const MPtrs& c, const MArgs& a, cons
 }
 
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+__global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                          const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(32 * TW3, 2) k_m3_cfas1(const DevCtx* __restri
 // Chebyshev step j >= 2; step 2 stages b and forms
 // y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+__global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                         const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(32 * TW3, 2) k_m3_cheb(const DevCtx* __restric
 // (oracle mc_gauss_seidel): y = y + invD (b - A y) at the nodes
 // of the colour, the last colour finalises every node.
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+__global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                       const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
@@ -526,7 +529,7 @@ __global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restric
 // last 4p-1 fine planes (two new planes per coarse output plane).
 constexpr int RPF3 = 2, RNB3 = 3, RRS3 = 80;
 template <int P>
-__global__ void __launch_bounds__(32 * TW3, 2) k_m3_restrict(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+__global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                             const __grid_constant__ Coefs cf) {
   extern __shared__ double msm[];
   pdl_wait();
