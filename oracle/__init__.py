@@ -38,6 +38,8 @@ def lib():
         dp = C.POINTER(C.c_double)
         L.orc_bfp_encode.argtypes = [dp, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_bfp_decode.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, dp]
+        L.orc_stream_encode.argtypes = [dp, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_stream_decode.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int, dp]
         L.orc_apply_A.argtypes = [C.c_int, C.c_int, C.c_int, dp, dp]
         L.orc_prolong.argtypes = [C.c_int, C.c_int, C.c_int, dp, dp]
         L.orc_restrict.argtypes = [C.c_int, C.c_int, C.c_int, dp, dp]
@@ -139,6 +141,29 @@ def bfp_encode(x: np.ndarray, width: int):
 def bfp_decode(mant: np.ndarray, exps: np.ndarray, n: int, width: int):
     x = np.zeros(n, dtype=np.float64)
     rc = lib().orc_bfp_decode(mant.ctypes.data, exps.ctypes.data, n, width, _dp(x))
+    return rc, x
+
+
+def stream_encode(x: np.ndarray, width: int):
+    """Streaming-exponent BFP -> (rc, mant, xexp[:K], xstart[:K])."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    n = x.size
+    mant = np.zeros((n // 32) * width, dtype=np.uint32)
+    xexp = np.zeros(width, dtype=np.int32)
+    xstart = np.zeros(width, dtype=np.int64)
+    nb = np.zeros(1, dtype=np.int32)
+    rc = lib().orc_stream_encode(_dp(x), n, width, mant.ctypes.data, xexp.ctypes.data, xstart.ctypes.data,
+                                 nb.ctypes.data)
+    k = int(nb[0])
+    return rc, mant, xexp[:k].copy(), xstart[:k].copy()
+
+
+def stream_decode(mant: np.ndarray, xexp: np.ndarray, xstart: np.ndarray, n: int, width: int):
+    x = np.zeros(n, dtype=np.float64)
+    xexp = np.ascontiguousarray(xexp, dtype=np.int32)
+    xstart = np.ascontiguousarray(xstart, dtype=np.int64)
+    rc = lib().orc_stream_decode(np.ascontiguousarray(mant, dtype=np.uint32).ctypes.data, xexp.ctypes.data,
+                                 xstart.ctypes.data, len(xexp), n, width, _dp(x))
     return rc, x
 
 

@@ -59,6 +59,12 @@ void orc_pack_block(const int64_t* m, int w, uint32_t* words);
 void orc_unpack_block(const uint32_t* words, int w, int64_t* m);
 int orc_bfp_encode(const double* x, int64_t n, int width, uint32_t* mant, int8_t* exps);
 int orc_bfp_decode(const uint32_t* mant, const int8_t* exps, int64_t n, int width, double* x);
+/* streaming-exponent BFP (readings R19-R21): xexp/xstart
+ * have room for `width` kept blocks; *nblocks <= width. */
+int orc_stream_encode(const double* x, int64_t n, int width, uint32_t* mant, int32_t* xexp,
+                      int64_t* xstart, int32_t* nblocks);
+int orc_stream_decode(const uint32_t* mant, const int32_t* xexp, const int64_t* xstart, int32_t nblocks,
+                      int64_t n, int width, double* x);
 
 /* ---- discretisation (orc_fem.c) ---- */
 void orc_ref_matrices(int p, int64_t* Knum, int64_t* Kden, int64_t* Mnum, int64_t* Mden);

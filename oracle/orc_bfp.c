@@ -12,6 +12,7 @@
  * fractions, RNE tie cases, powers of two, round-trip bound 2^(E-q-1).
  */
 #include <math.h>
+#include <stdlib.h>
 #include <stdint.h>
 #include <string.h>
 #include "oracle.h"
@@ -93,6 +94,107 @@ int orc_bfp_decode(const uint32_t* mant, const int8_t* exps, int64_t n, int widt
   for (int64_t b = 0; b < n / 32; ++b) {
     orc_unpack_block(mant + b * width, width, m);
     for (int j = 0; j < 32; ++j) x[32 * b + j] = orc_block_decode_one(m[j], exps[b], width);
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------
+ * Streaming-exponent BFP (§8(f) row N3): "As the entries
+ * of the vector are computed, we keep track of the currently largest known
+ * exponent and normalize the current mantissa to that exponent. This exponent
+ * and associated mantissas constitute one block of the BFP vector. The next
+ * block starts when a larger exponent is encountered. [...] storing only the b
+ * largest exponents suffices [...] The other exponents are smaller by at least
+ * b compared to the largest exponent. Therefore, those entries would be
+ * truncated to zero in single-exponent BFP precision."
+ *
+ * Readings (R19-R21):
+ *   R19 the exponent an entry needs is the block codec's rule applied to that
+ *       entry alone: E_i = ilogb|x_i| + 1, plus 1 when RNE(|x_i| 2^(q-E_i))
+ *       reaches 2^q; zero entries need no exponent and never start a block;
+ *   R20 b = w (the paper's "number of bits in each mantissa", sign included):
+ *       an entry whose block exponent is <= X_max - w has |x| < 2^(X_max - w),
+ *       i.e. below half a unit of the single-exponent mantissa, so it is stored
+ *       as 0;
+ *   R21 exponents are int32 in [-1073, 1024] (no int8 saturation); E_i > 1024
+ *       (a decode would overflow) and non-finite inputs are ORC_ERANGE.
+ * Output: the packed mantissa stream (same packing as the block codec: entry i
+ * at stream bits [i w, i w + w)), the kept blocks' exponents X_k and first
+ * indices s_k in increasing order, and their count K' <= w.
+ * ------------------------------------------------------------------------ */
+#define ORC_NOEXP (-0x40000000)
+
+/* R19: the exponent entry x needs on its own (ORC_NOEXP for zero). */
+static int entry_exponent(double x, int q) {
+  double a = fabs(x);
+  if (a == 0.0) return ORC_NOEXP;
+  int e = ilogb(a) + 1;
+  if (rint(ldexp(a, q - e)) == ldexp(1.0, q)) e = e + 1;
+  return e;
+}
+
+int orc_stream_encode(const double* x, int64_t n, int width, uint32_t* mant, int32_t* xexp,
+                      int64_t* xstart, int32_t* nblocks) {
+  if (width < 2 || width > 54 || n < 0 || (n % 32) != 0) return ORC_EINVAL;
+  int q = width - 1;
+  /* pass 1 (the paper's stream): running maximum exponent, a block per increase */
+  int* M = (int*)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+  int64_t cap = 2200, K = 0;
+  int32_t* bx = (int32_t*)malloc(sizeof(int32_t) * cap);
+  int64_t* bs = (int64_t*)malloc(sizeof(int64_t) * cap);
+  if (!M || !bx || !bs) { free(M); free(bx); free(bs); return ORC_ENOMEM; }
+  int cur = ORC_NOEXP;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!isfinite(x[i])) { free(M); free(bx); free(bs); return ORC_ERANGE; }
+    int e = entry_exponent(x[i], q);
+    if (e > 1024) { free(M); free(bx); free(bs); return ORC_ERANGE; }
+    if (e > cur) {       /* "the next block starts when a larger exponent is encountered" */
+      cur = e;
+      bx[K] = e;         /* K <= 2098 distinct increasing exponents < cap */
+      bs[K] = i;
+      K = K + 1;
+    }
+    M[i] = cur;
+  }
+  /* keep the b = w largest exponents: the last b blocks (exponents increase) */
+  int64_t k0 = K > width ? K - width : 0;
+  int32_t T = K > 0 ? bx[k0] : ORC_NOEXP;
+  for (int64_t k = k0; k < K; ++k) {
+    xexp[k - k0] = bx[k];
+    xstart[k - k0] = bs[k];
+  }
+  *nblocks = (int32_t)(K - k0);
+  /* pass 2: mantissas normalised to their block's exponent; dropped blocks -> 0 */
+  int64_t m[32];
+  for (int64_t g = 0; g < n / 32; ++g) {
+    for (int j = 0; j < 32; ++j) {
+      int64_t i = 32 * g + j;
+      if (K > 0 && M[i] >= T && M[i] != ORC_NOEXP)
+        m[j] = (int64_t)rint(ldexp(x[i], q - M[i]));
+      else
+        m[j] = 0;
+    }
+    orc_pack_block(m, width, mant + g * width);
+  }
+  free(M); free(bx); free(bs);
+  return ORC_OK;
+}
+
+/* x_i = m_i 2^(X_k - q) for the kept block k containing i (s_k <= i < s_{k+1});
+ * entries before s_0 are 0. */
+int orc_stream_decode(const uint32_t* mant, const int32_t* xexp, const int64_t* xstart, int32_t nblocks,
+                      int64_t n, int width, double* x) {
+  if (width < 2 || width > 54 || n < 0 || (n % 32) != 0 || nblocks < 0 || nblocks > width) return ORC_EINVAL;
+  int q = width - 1;
+  int64_t m[32];
+  int k = -1;
+  for (int64_t g = 0; g < n / 32; ++g) {
+    orc_unpack_block(mant + g * width, width, m);
+    for (int j = 0; j < 32; ++j) {
+      int64_t i = 32 * g + j;
+      while (k + 1 < nblocks && xstart[k + 1] <= i) k = k + 1;
+      x[i] = k < 0 ? 0.0 : ldexp((double)m[j], xexp[k] - q);
+    }
   }
   return ORC_OK;
 }
