@@ -117,7 +117,10 @@ int orc_bfp_decode(const uint32_t* mant, const int8_t* exps, int64_t n, int widt
  *       i.e. below half a unit of the single-exponent mantissa, so it is stored
  *       as 0;
  *   R21 exponents are int32 in [-1073, 1024] (no int8 saturation); E_i > 1024
- *       (a decode would overflow) and non-finite inputs are ORC_ERANGE.
+ *       (a decode would overflow) and non-finite inputs are ORC_ERANGE;
+ *   R22 every mantissa is written once, normalised to the running maximum at
+ *       its position; dropping a block discards only its exponent record, and
+ *       decoding reads the entries before the first kept block as 0.
  * Output: the packed mantissa stream (same packing as the block codec: entry i
  * at stream bits [i w, i w + w)), the kept blocks' exponents X_k and first
  * indices s_k in increasing order, and their count K' <= w.
@@ -158,21 +161,20 @@ int orc_stream_encode(const double* x, int64_t n, int width, uint32_t* mant, int
   }
   /* keep the b = w largest exponents: the last b blocks (exponents increase) */
   int64_t k0 = K > width ? K - width : 0;
-  int32_t T = K > 0 ? bx[k0] : ORC_NOEXP;
   for (int64_t k = k0; k < K; ++k) {
     xexp[k - k0] = bx[k];
     xstart[k - k0] = bs[k];
   }
   *nblocks = (int32_t)(K - k0);
-  /* pass 2: mantissas normalised to their block's exponent; dropped blocks -> 0 */
+  /* mantissas: each normalised once, to the running maximum at its position
+   * ("normalize the current mantissa to that exponent"); those of dropped
+   * blocks are not rewritten (R22: no re-normalisation) --
+   * the decoder reads every entry before the first kept block as 0 */
   int64_t m[32];
   for (int64_t g = 0; g < n / 32; ++g) {
     for (int j = 0; j < 32; ++j) {
       int64_t i = 32 * g + j;
-      if (K > 0 && M[i] >= T && M[i] != ORC_NOEXP)
-        m[j] = (int64_t)rint(ldexp(x[i], q - M[i]));
-      else
-        m[j] = 0;
+      m[j] = M[i] == ORC_NOEXP ? 0 : (int64_t)rint(ldexp(x[i], q - M[i]));
     }
     orc_pack_block(m, width, mant + g * width);
   }

@@ -3,7 +3,7 @@ orc_stream_encode / orc_stream_decode; §8(f) row N3).
 
 Scheme: PAPER.md:1252-1266 -- running-maximum exponent while streaming, a new
 block at each increase, only the b largest exponents stored, the rest of the
-entries "truncated to zero in single-exponent BFP precision".  Readings R19-R21
+entries "truncated to zero in single-exponent BFP precision".  Readings R19-R22
 (DESIGN.md).  The pins below do not re-state the oracle's loop.  They check it
 against:
 
@@ -77,6 +77,9 @@ def test_worked_example_drops_small_blocks():
     rc, mant, xe, xs = O.stream_encode(x, 3)
     assert rc == 0
     assert xe.tolist() == [3, 4, 5] and xs.tolist() == [2, 3, 4]
+    # R22: the dropped entries' mantissas stay as written (1 2^(2-1) = 2 and
+    # 2 2^(2-2) = 2 at q = 2); only their exponent records are gone
+    assert unpack(mant, 32, 3)[:5] == [2, 2, 2, 2, 2]
     rc, y = O.stream_decode(mant, xe, xs, 32, 3)
     assert y[:5].tolist() == [0, 0, 4, 8, 16]
     se = single_exponent_bfp(x, 3)
