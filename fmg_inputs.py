@@ -73,4 +73,19 @@ def codec_vectors(n: int, seed: int, kind: str = "smooth") -> np.ndarray:
                 v = rng.standard_normal(16) * 2.0 ** e
                 blocks[b] = np.concatenate([v, -v])
         return blocks.reshape(-1)
+    if kind == "staircase":
+        # streaming-exponent inputs (N3): magnitudes trending up from the
+        # subnormal range to 2^1000 over the vector, so the running maximum
+        # rises ~2000 times at positions spread over every CTA chunk; 5 % zeros,
+        # some exponent-bump values (2 - 2^-5) 2^e
+        e_lo, e_hi = -1070.0, 1000.0
+        t = (i / max(n, 1)) ** 1.5
+        e = np.floor(e_lo + (e_hi - e_lo) * t + rng.integers(-40, 3, n)).astype(np.int64)
+        e = np.clip(e, -1074, 1000)
+        x = rng.uniform(0.5, 1.0, n) * rng.choice([-1.0, 1.0], n)
+        bump = rng.random(n) < 0.02
+        x[bump] = np.sign(x[bump]) * (1.0 - 2.0 ** -6)
+        x = np.ldexp(x, e)
+        x[rng.random(n) < 0.05] = 0.0
+        return x
     raise ValueError(kind)

@@ -204,6 +204,29 @@ int bfp_decode(const uint32_t* mant, const int8_t* exps, int64_t n, int width, d
 /* Returns and clears the sticky codec error status (synchronises `stream`). */
 int bfp_status(void* stream);
 
+/* Streaming-exponent BFP (§8(f) row N3, readings R19-R21,
+ * DESIGN.md §N3).  The running maximum of the entry exponents is the exponent
+ * each mantissa is normalised to; a block starts at each increase; only the
+ * `width` largest block exponents are kept and entries before the first kept
+ * block are stored as 0 (they are below half a unit of single-exponent BFP).
+ * All pointers are DEVICE pointers, caller-owned:
+ *   x       n doubles (n % 32 == 0; width in [2,54])
+ *   mant    n*width/32 words; entry i at stream bits [i w, i w + w), two's
+ *           complement (the block codec's packing)
+ *   xexp    int32[width]: kept block exponents X_k, increasing
+ *   xstart  int64[width]: index of the first entry of block k, increasing
+ *   nblocks one int32: number of kept blocks (<= width; 0 for an all-zero x)
+ *   work    scratch of bfp_stream_work_bytes(n) bytes, unused between calls
+ * Asynchronous on `stream`.  Non-finite input or an exponent above 1024 is
+ * reported as FMG_ERANGE by the next bfp_status call.
+ * x_i decodes to m_i 2^(X_k - q), q = width - 1, for the block k with
+ * xstart[k] <= i < xstart[k+1]; 0 before xstart[0]. */
+int64_t bfp_stream_work_bytes(int64_t n);  /* negative FMG error code on bad n */
+int bfp_stream_encode(const double* x, int64_t n, int width, uint32_t* mant, int32_t* xexp, int64_t* xstart,
+                      int32_t* nblocks, void* work, void* stream);
+int bfp_stream_decode(const uint32_t* mant, const int32_t* xexp, const int64_t* xstart, const int32_t* nblocks,
+                      int64_t n, int width, double* x, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

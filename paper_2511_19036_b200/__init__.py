@@ -76,6 +76,10 @@ _lib.fmg_get_rhs.argtypes = [_vp, _vp]
 _lib.bfp_encode.argtypes = [_vp, C.c_int64, C.c_int, _vp, _vp, _vp]
 _lib.bfp_decode.argtypes = [_vp, _vp, C.c_int64, C.c_int, _vp, _vp]
 _lib.bfp_status.argtypes = [_vp]
+_lib.bfp_stream_work_bytes.argtypes = [C.c_int64]
+_lib.bfp_stream_work_bytes.restype = C.c_int64
+_lib.bfp_stream_encode.argtypes = [_vp, C.c_int64, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.bfp_stream_decode.argtypes = [_vp, _vp, _vp, _vp, C.c_int64, C.c_int, _vp, _vp]
 
 _ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
 _FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -86,7 +90,8 @@ EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_create_slabs", "fmg_create_di
            "fmg_norms", "fmg_residual", "fmg_get_solution", "fmg_errors", "fmg_get_section",
            "fmg_info", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_kernel_times", "fmg_destroy",
            "fmg_rhs_size", "fmg_set_rhs", "fmg_get_rhs", "fmg_export_solution",
-           "fmg_strerror", "bfp_encode", "bfp_decode", "bfp_status"]
+           "fmg_strerror", "bfp_encode", "bfp_decode", "bfp_status",
+           "bfp_stream_work_bytes", "bfp_stream_encode", "bfp_stream_decode"]
 
 
 def _check(rc: int, what: str):
@@ -300,6 +305,41 @@ def bfp_decode(mant, exps, n: int, width: int, stream=None):
     st = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
     _check(_lib.bfp_decode(C.c_void_p(mant.data_ptr()), C.c_void_p(exps.data_ptr()), n, width,
                            C.c_void_p(x.data_ptr()), st), "bfp_decode")
+    return x
+
+
+def bfp_stream_encode(x, width: int, stream=None):
+    """Streaming-exponent BFP of a CUDA float64 tensor
+    (numel % 32 == 0) -> (mant int32[n w / 32], xexp int32[width],
+    xstart int64[width], nblocks int32[1]); the first nblocks table entries are
+    valid.  All outputs stay on the device."""
+    import torch
+    assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
+    n = x.numel()
+    dev = x.device
+    mant = torch.empty((n // 32) * width, dtype=torch.int32, device=dev)
+    xexp = torch.zeros(width, dtype=torch.int32, device=dev)
+    xstart = torch.zeros(width, dtype=torch.int64, device=dev)
+    nb = torch.zeros(1, dtype=torch.int32, device=dev)
+    wb = _lib.bfp_stream_work_bytes(n)
+    if wb < 0:
+        raise FmgError(-wb, "bfp_stream_work_bytes")
+    work = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    st = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    _check(_lib.bfp_stream_encode(C.c_void_p(x.data_ptr()), n, width, C.c_void_p(mant.data_ptr()),
+                                  C.c_void_p(xexp.data_ptr()), C.c_void_p(xstart.data_ptr()),
+                                  C.c_void_p(nb.data_ptr()), C.c_void_p(work.data_ptr()), st),
+           "bfp_stream_encode")
+    return mant, xexp, xstart, nb
+
+
+def bfp_stream_decode(mant, xexp, xstart, nblocks, n: int, width: int, stream=None):
+    import torch
+    x = torch.empty(n, dtype=torch.float64, device=mant.device)
+    st = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
+    _check(_lib.bfp_stream_decode(C.c_void_p(mant.data_ptr()), C.c_void_p(xexp.data_ptr()),
+                                  C.c_void_p(xstart.data_ptr()), C.c_void_p(nblocks.data_ptr()), n, width,
+                                  C.c_void_p(x.data_ptr()), st), "bfp_stream_decode")
     return x
 
 

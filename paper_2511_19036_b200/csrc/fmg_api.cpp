@@ -1396,6 +1396,33 @@ int bfp_decode(const uint32_t* mant, const int8_t* exps, int64_t n, int width, d
   return cuda_err(cudaGetLastError());
 }
 
+int64_t bfp_stream_work_bytes(int64_t n) {
+  if (n < 0 || (n % 32) != 0) return -FMG_EINVAL;
+  return (int64_t)stream_work_bytes(n);
+}
+
+int bfp_stream_encode(const double* x, int64_t n, int width, uint32_t* mant, int32_t* xexp, int64_t* xstart,
+                      int32_t* nblocks, void* work, void* stream) {
+  if (width < 2 || width > 54 || n < 0 || (n % 32) != 0 || !nblocks) return FMG_EINVAL;
+  if (n > 0 && (!x || !mant || !xexp || !xstart || !work)) return FMG_EINVAL;
+  if (n == 0) return cuda_err(cudaMemsetAsync(nblocks, 0, sizeof(int32_t), (cudaStream_t)stream));
+  if (!g_codec_status) {
+    if (cudaMalloc(&g_codec_status, sizeof(int)) != cudaSuccess) return FMG_ENOMEM;
+    cudaMemset(g_codec_status, 0, sizeof(int));
+  }
+  launch_stream_encode(x, n, width, mant, xexp, xstart, nblocks, work, g_codec_status, (cudaStream_t)stream);
+  return cuda_err(cudaGetLastError());
+}
+
+int bfp_stream_decode(const uint32_t* mant, const int32_t* xexp, const int64_t* xstart, const int32_t* nblocks,
+                      int64_t n, int width, double* x, void* stream) {
+  if (width < 2 || width > 54 || n < 0 || (n % 32) != 0) return FMG_EINVAL;
+  if (n == 0) return FMG_OK;
+  if (!mant || !xexp || !xstart || !nblocks || !x) return FMG_EINVAL;
+  launch_stream_decode(mant, xexp, xstart, nblocks, n, width, x, (cudaStream_t)stream);
+  return cuda_err(cudaGetLastError());
+}
+
 int bfp_status(void* stream) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_err(e);

@@ -54,9 +54,10 @@ __device__ __forceinline__ long long rne_int(double x, int w) {
   return (long long)rint(x);
 }
 
-// Warp-cooperative decode: lane j returns entry j of the block whose w words
-// start at `words` (DESIGN.md §2, §3.8).  All 32 lanes must call.
-__device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int w, int lane) {
+// Warp-cooperative unpack: lane j returns the w-bit two's-complement mantissa
+// of entry j of the 32-entry group whose w words start at `words` (DESIGN.md
+// §2).  All 32 lanes must call.
+__device__ __forceinline__ long long warp_unpack(const uint32_t* words, int w, int lane) {
   uint32_t my0 = lane < w ? words[lane] : 0u;
   uint32_t my1 = 0u;
   if (w > 32) my1 = lane + 32 < w ? words[lane + 32] : 0u;
@@ -77,8 +78,13 @@ __device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int 
   unsigned long long lo = (unsigned long long)w0 | ((unsigned long long)w1 << 32);
   unsigned long long field = lo >> s;
   if (s + w > 64) field |= (unsigned long long)w2 << (64 - s);
-  long long m = (long long)(field << (64 - w)) >> (64 - w);
-  return i2d(m, w) * pow2(E - (w - 1));
+  return (long long)(field << (64 - w)) >> (64 - w);
+}
+
+// Warp-cooperative decode: lane j returns entry j of the block whose w words
+// start at `words` (DESIGN.md §2, §3.8).  All 32 lanes must call.
+__device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int w, int lane) {
+  return i2d(warp_unpack(words, w, lane), w) * pow2(E - (w - 1));
 }
 
 // Single-entry decode (entry j of a block), for halo points.
@@ -106,6 +112,48 @@ __device__ __forceinline__ uint32_t pack_narrow(unsigned long long field, int la
     mine = lane == j ? word : mine;
   }
   return mine;
+}
+
+// Warp-cooperative pack: lane j holds the masked w-bit field of entry j; the
+// group's w words are written to `words`.  All lanes must call.
+__device__ __forceinline__ void warp_pack(unsigned long long field, int w, uint32_t* words, int lane) {
+  uint32_t mine0 = 0u, mine1 = 0u;
+  if (w <= 8) {
+    // narrow: entry `lane` occupies stream bits [lane w, lane w + w) = (low, high)
+    // parts of words j0, j0 + 1; one redux.or per output word (width-specialised)
+    switch (w) {
+      case 2: mine0 = pack_narrow<2>(field, lane); break;
+      case 3: mine0 = pack_narrow<3>(field, lane); break;
+      case 4: mine0 = pack_narrow<4>(field, lane); break;
+      case 5: mine0 = pack_narrow<5>(field, lane); break;
+      case 6: mine0 = pack_narrow<6>(field, lane); break;
+      case 7: mine0 = pack_narrow<7>(field, lane); break;
+      default: mine0 = pack_narrow<8>(field, lane); break;
+    }
+  } else {
+    // wide: word j gathers its <= ceil(32/w)+1 entries by shuffles
+    const int K = (32 + w - 1) / w + 1;
+    const uint32_t flo = (uint32_t)field, fhi = (uint32_t)(field >> 32);
+#pragma unroll 1
+    for (int half = 0; half < (w > 32 ? 2 : 1); ++half) {
+      const int j = lane + 32 * half;
+      const int e0 = (32 * j) / w;
+      uint32_t acc = 0u;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {  // K <= 5 for w >= 9
+        if (k >= K) break;
+        const int e = e0 + k;
+        const int src = e < 32 ? e : 31;
+        const uint32_t lo_ = __shfl_sync(FULL, flo, src), hi_ = __shfl_sync(FULL, fhi, src);
+        const unsigned long long f = ((unsigned long long)hi_ << 32) | lo_;
+        const int sh = e * w - 32 * j;
+        if (e < 32 && sh < 32 && sh > -w) acc |= sh >= 0 ? (uint32_t)(f << sh) : (uint32_t)(f >> (-sh));
+      }
+      if (half == 0) mine0 = acc; else mine1 = acc;
+    }
+  }
+  if (lane < w) words[lane] = mine0;
+  if (lane + 32 < w) words[lane + 32] = mine1;
 }
 
 // Warp-cooperative encode of one block; lane j holds entry j.
@@ -142,47 +190,84 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
     m = rne_int(v * pow2(q - E), w);
   }
   if (words) {
-    const unsigned long long field = (unsigned long long)m & ((1ULL << w) - 1ULL);
-    uint32_t mine0 = 0u, mine1 = 0u;
-    if (w <= 8) {
-      // narrow: entry `lane` occupies stream bits [lane w, lane w + w) = (low, high)
-      // parts of words j0, j0 + 1; one redux.or per output word (width-specialised)
-      switch (w) {
-        case 2: mine0 = pack_narrow<2>(field, lane); break;
-        case 3: mine0 = pack_narrow<3>(field, lane); break;
-        case 4: mine0 = pack_narrow<4>(field, lane); break;
-        case 5: mine0 = pack_narrow<5>(field, lane); break;
-        case 6: mine0 = pack_narrow<6>(field, lane); break;
-        case 7: mine0 = pack_narrow<7>(field, lane); break;
-        default: mine0 = pack_narrow<8>(field, lane); break;
-      }
-    } else {
-      // wide: word j gathers its <= ceil(32/w)+1 entries by shuffles
-      const int K = (32 + w - 1) / w + 1;
-      const uint32_t flo = (uint32_t)field, fhi = (uint32_t)(field >> 32);
-#pragma unroll 1
-      for (int half = 0; half < (w > 32 ? 2 : 1); ++half) {
-        const int j = lane + 32 * half;
-        const int e0 = (32 * j) / w;
-        uint32_t acc = 0u;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {  // K <= 5 for w >= 9
-          if (k >= K) break;
-          const int e = e0 + k;
-          const int src = e < 32 ? e : 31;
-          const uint32_t lo_ = __shfl_sync(FULL, flo, src), hi_ = __shfl_sync(FULL, fhi, src);
-          const unsigned long long f = ((unsigned long long)hi_ << 32) | lo_;
-          const int sh = e * w - 32 * j;
-          if (e < 32 && sh < 32 && sh > -w) acc |= sh >= 0 ? (uint32_t)(f << sh) : (uint32_t)(f >> (-sh));
-        }
-        if (half == 0) mine0 = acc; else mine1 = acc;
-      }
-    }
-    if (lane < w) words[lane] = mine0;
-    if (lane + 32 < w) words[lane + 32] = mine1;
+    warp_pack((unsigned long long)m & ((1ULL << w) - 1ULL), w, words, lane);
     if (lane == 0) *eptr = (int8_t)E;
   }
   return E == -128 ? 0.0 : i2d(m, w) * pow2(E - q);
+}
+
+// ------------------------------------------------- thread-per-block codec --
+// One THREAD encodes / decodes one whole 32-entry block held in shared memory
+// (a warp handles 32 blocks per instruction stream), so the exponent search
+// is a serial max and the packing a running 64-bit bit accumulator: about 13
+// warp instructions per block against ~100 for the warp-cooperative codec
+// above.  Same format and arithmetic (R8, §3.8); w <= 32 only.
+// `row`: the block's 32 doubles in shared memory (callers pad the row stride
+// to an odd number of doubles so the 32 lanes' rows fall in distinct banks);
+// `wrow`: its w packed words (callers pad the row stride to w + 1 words).
+
+// Exponent of one block (R8): E = -128 for an all-zero block; *bad on a
+// non-finite entry or E > 127.
+__device__ __forceinline__ int tpb_exponent(const double* row, int w, bool& bad) {
+  unsigned long long mx = 0ULL;
+#pragma unroll 8
+  for (int e = 0; e < 32; ++e) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(row[e]) & 0x7fffffffffffffffULL;
+    mx = b > mx ? b : mx;
+  }
+  if (mx >= 0x7ff0000000000000ULL) { bad = true; return -128; }
+  if (mx == 0ULL) return -128;
+  const int q = w - 1;
+  const int ebits = (int)(mx >> 52);
+  const int E0 = ebits == 0 ? -1100 : ebits - 1022;
+  if (E0 > 127) { bad = true; return -128; }
+  if (E0 < -127) return -127;
+  int E = E0;
+  if (rint(__longlong_as_double((long long)mx) * pow2(q - E0)) == pow2(q)) E = E0 + 1;
+  if (E > 127) { bad = true; return -128; }
+  return E;
+}
+
+// Quantise and pack one block with exponent E (E = -128: zeros).  When
+// `qrow` is non-null the decoded value m 2^(E-q) of entry e is stored to
+// qrow[e] (qrow may alias row).
+__device__ __forceinline__ void tpb_pack(const double* row, int E, int w, uint32_t* wrow, double* qrow) {
+  const int q = w - 1;
+  const double s = E == -128 ? 0.0 : pow2(q - E);
+  const double sb = E == -128 ? 0.0 : pow2(E - q);
+  const unsigned long long mask = (1ULL << w) - 1ULL;
+  unsigned long long acc = 0ULL;
+  int nb = 0, k = 0;
+#pragma unroll 4
+  for (int e = 0; e < 32; ++e) {
+    const long long m = rne_int(row[e] * s, w);
+    if (qrow) qrow[e] = i2d(m, w) * sb;
+    acc |= ((unsigned long long)m & mask) << nb;
+    nb += w;
+    if (nb >= 32) {
+      wrow[k++] = (uint32_t)acc;
+      acc >>= 32;
+      nb -= 32;
+    }
+  }
+}
+
+// Unpack and scale one block into row[0..32).
+__device__ __forceinline__ void tpb_unpack(const uint32_t* wrow, int E, int w, double* row) {
+  const double sb = E == -128 ? 0.0 : pow2(E - (w - 1));
+  unsigned long long acc = 0ULL;
+  int nb = 0, k = 0;
+#pragma unroll 4
+  for (int e = 0; e < 32; ++e) {
+    if (nb < w) {
+      acc |= (unsigned long long)wrow[k++] << nb;
+      nb += 32;
+    }
+    const long long m = (long long)(acc << (64 - w)) >> (64 - w);
+    acc >>= w;
+    nb -= w;
+    row[e] = i2d(m, w) * sb;
+  }
 }
 
 // ------------------------------------------------------------- contexts --

@@ -178,5 +178,10 @@ void launch_bfp_encode(const double* x, long long n, int w, uint32_t* mant, int8
                        cudaStream_t st);
 void launch_bfp_decode(const uint32_t* mant, const int8_t* exps, long long n, int w, double* x,
                        cudaStream_t st);
+long long stream_work_bytes(long long n);
+void launch_stream_encode(const double* x, long long n, int w, uint32_t* mant, int32_t* xexp, int64_t* xstart,
+                          int32_t* nblocks, void* work, int* status, cudaStream_t st);
+void launch_stream_decode(const uint32_t* mant, const int32_t* xexp, const int64_t* xstart, const int32_t* nblocks,
+                          long long n, int w, double* x, cudaStream_t st);
 
 }  // namespace fmg

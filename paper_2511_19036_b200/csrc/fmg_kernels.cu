@@ -907,6 +907,81 @@ __global__ void __launch_bounds__(256) k_bfp_decode(const uint32_t* __restrict__
   }
 }
 
+// Thread-per-block codec kernels (w <= 32): a warp stages 32 blocks (8 KB) in
+// shared memory with cp.async, one lane per block encodes / decodes, and the
+// packed words leave through a coalesced copy.
+constexpr int TPB_RS = 33;        // row stride (doubles)
+constexpr int TPB_WS = 33;        // packed row stride (words), >= w + 1
+constexpr int TPB_WARPS = 4;
+constexpr int TPB_SMEM = TPB_WARPS * (32 * TPB_RS * 8 + 32 * TPB_WS * 4);
+
+__global__ void __launch_bounds__(TPB_WARPS * 32) k_bfp_encode_tpb(const double* __restrict__ x, long long nblk,
+                                                                   int w, uint32_t* __restrict__ mant,
+                                                                   int8_t* __restrict__ exps, int* status) {
+  extern __shared__ __align__(16) unsigned char tpb_smem[];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  double* tile = (double*)tpb_smem + wp * 32 * TPB_RS;
+  uint32_t* wt = (uint32_t*)((double*)tpb_smem + TPB_WARPS * 32 * TPB_RS) + wp * 32 * TPB_WS;
+  const unsigned magic = (unsigned)((0x100000000ULL + w - 1) / w);  // t / w for t < 2^16
+  const long long ntile = (nblk + 31) / 32;
+  const long long wg = (long long)blockIdx.x * TPB_WARPS + wp, nw = (long long)gridDim.x * TPB_WARPS;
+  bool bad = false;
+  for (long long t = wg; t < ntile; t += nw) {
+    const long long b0 = t * 32;
+    const int nb = (int)(nblk - b0 < 32 ? nblk - b0 : 32);
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) cpa8(tile + r * TPB_RS + lane, x + (b0 + r) * 32 + lane, r < nb);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+    const double* row = tile + lane * TPB_RS;
+    const int E = tpb_exponent(row, w, bad);
+    tpb_pack(row, E, w, wt + lane * TPB_WS, nullptr);
+    if (lane < nb) exps[b0 + lane] = (int8_t)E;
+    __syncwarp();
+    const int nwords = nb * w;
+    uint32_t* dst = mant + b0 * w;
+    for (int o = lane; o < nwords; o += 32) {
+      const int j = (int)__umulhi((unsigned)o, magic);
+      dst[o] = wt[j * TPB_WS + (o - j * w)];
+    }
+    __syncwarp();
+  }
+  if (__any_sync(FULL, bad) && lane == 0) atomicOr(status, 1);
+}
+
+__global__ void __launch_bounds__(TPB_WARPS * 32) k_bfp_decode_tpb(const uint32_t* __restrict__ mant,
+                                                                   const int8_t* __restrict__ exps, long long nblk,
+                                                                   int w, double* __restrict__ x) {
+  extern __shared__ __align__(16) unsigned char tpb_smem[];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  double* tile = (double*)tpb_smem + wp * 32 * TPB_RS;
+  uint32_t* wt = (uint32_t*)((double*)tpb_smem + TPB_WARPS * 32 * TPB_RS) + wp * 32 * TPB_WS;
+  const unsigned magic = (unsigned)((0x100000000ULL + w - 1) / w);
+  const long long ntile = (nblk + 31) / 32;
+  const long long wg = (long long)blockIdx.x * TPB_WARPS + wp, nw = (long long)gridDim.x * TPB_WARPS;
+  for (long long t = wg; t < ntile; t += nw) {
+    const long long b0 = t * 32;
+    const int nb = (int)(nblk - b0 < 32 ? nblk - b0 : 32);
+    const int nwords = nb * w;
+    const uint32_t* src = mant + b0 * w;
+    for (int o = lane; o < nwords; o += 32) {  // all copies in flight (LDGSTS)
+      const int j = (int)__umulhi((unsigned)o, magic);
+      cpa4(wt + j * TPB_WS + (o - j * w), src + o);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const int E = lane < nb ? (int)exps[b0 + lane] : -128;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+    tpb_unpack(wt + lane * TPB_WS, E, w, tile + lane * TPB_RS);
+    __syncwarp();
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r)
+      if (r < nb) __stcs(x + (b0 + r) * 32 + lane, tile[r * TPB_RS + lane]);
+    __syncwarp();
+  }
+}
+
 // ============================================================ launchers ===
 #define FMG_DISPATCH(dim, p, F)               \
   do {                                        \
@@ -1082,6 +1157,18 @@ void launch_errors(const Launch& L, const double* U, const Geom& g, double* part
 void launch_bfp_encode(const double* x, long long n, int w, uint32_t* mant, int8_t* exps, int* status,
                        cudaStream_t st) {
   long long nblk = n / 32;
+  if (w <= 32) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_bfp_encode_tpb, cudaFuncAttributeMaxDynamicSharedMemorySize, TPB_SMEM);
+      cudaFuncSetAttribute(k_bfp_decode_tpb, cudaFuncAttributeMaxDynamicSharedMemorySize, TPB_SMEM);
+      attr = true;
+    }
+    long long want = (nblk + 32 * TPB_WARPS - 1) / (32 * TPB_WARPS);
+    int grid = (int)(want < (long long)num_sms() * 3 ? (want > 0 ? want : 1) : num_sms() * 3);
+    k_bfp_encode_tpb<<<grid, TPB_WARPS * 32, TPB_SMEM, st>>>(x, nblk, w, mant, exps, status);
+    return;
+  }
   long long want = (nblk + 7) / 8;
   int grid = (int)(want < (long long)num_sms() * 16 ? (want > 0 ? want : 1) : num_sms() * 16);
   k_bfp_encode<<<grid, 256, 0, st>>>(x, nblk, w, mant, exps, status);
@@ -1089,6 +1176,18 @@ void launch_bfp_encode(const double* x, long long n, int w, uint32_t* mant, int8
 
 void launch_bfp_decode(const uint32_t* mant, const int8_t* exps, long long n, int w, double* x, cudaStream_t st) {
   long long nblk = n / 32;
+  if (w <= 32) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_bfp_encode_tpb, cudaFuncAttributeMaxDynamicSharedMemorySize, TPB_SMEM);
+      cudaFuncSetAttribute(k_bfp_decode_tpb, cudaFuncAttributeMaxDynamicSharedMemorySize, TPB_SMEM);
+      attr = true;
+    }
+    long long want = (nblk + 32 * TPB_WARPS - 1) / (32 * TPB_WARPS);
+    int grid = (int)(want < (long long)num_sms() * 3 ? (want > 0 ? want : 1) : num_sms() * 3);
+    k_bfp_decode_tpb<<<grid, TPB_WARPS * 32, TPB_SMEM, st>>>(mant, exps, nblk, w, x);
+    return;
+  }
   long long want = (nblk + 7) / 8;
   int grid = (int)(want < (long long)num_sms() * 16 ? (want > 0 ? want : 1) : num_sms() * 16);
   k_bfp_decode<<<grid, 256, 0, st>>>(mant, exps, nblk, w, x);
