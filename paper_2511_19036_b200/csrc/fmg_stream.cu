@@ -43,10 +43,23 @@ static int sx_num_sms() {
   return n;
 }
 
+#ifdef SX_PROBE
+__device__ unsigned long long* sx_probe_buf;  // per chunk: land, lookback done, end, rounds
+__device__ __forceinline__ unsigned long long sx_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SX_STAMP(c, k, v) \
+  if (sx_probe_buf && threadIdx.x == 0) sx_probe_buf[(c) * 4 + (k)] = (v)
+#else
+#define SX_STAMP(c, k, v)
+#endif
+
 constexpr int SX_OFF = 1100;          // table index = X + SX_OFF, X in [-1073, 1024]
 constexpr int SX_N = 2176;            // > 1024 + SX_OFF
 constexpr int SX_NOEXP = -0x40000000;  // zero entries: no exponent (R19)
-constexpr int SX_WARPS = 4;
+constexpr int SX_WARPS = 2;
 constexpr int SX_GPC = 32 * SX_WARPS;  // groups per CTA chunk (one 32-group tile per warp)
 constexpr int SX_RS = 33;              // staged row stride (doubles): lanes' rows in distinct banks
 constexpr int SX_WS = 57;              // packed row stride (words) >= w + 1, odd
@@ -109,33 +122,80 @@ __device__ __forceinline__ int sx_exp_bits(unsigned long long bits, int q) {
   return ebits - 1022 + bump;
 }
 
+// Decoupled look-back (warp 0): the running maximum before chunk c, given
+// its own maximum agg; publishes agg, then the running maximum through c.
+__device__ __forceinline__ int sx_lookback(unsigned long long* tiles, long long c, int agg, int lane) {
+  int pre = SX_NOEXP;
+  if (c == 0) {
+    if (lane == 0) sx_publish(tiles, sx_word(SX_INC, agg));
+    return pre;
+  }
+  if (lane == 0) sx_publish(tiles + c, sx_word(SX_AGG, agg));
+  // window of 32 predecessors per poll (wider windows contend on the hot
+  // status lines and measured slower)
+  long long j = c - 1;
+  while (true) {
+    const long long idx = j - lane;
+    unsigned long long sw = idx >= 0 ? sx_peek(tiles + idx) : sx_word(SX_INC, SX_NOEXP);
+    while (__any_sync(FULL, (sw >> 62) == 0)) {
+      if ((sw >> 62) == 0) {
+        __nanosleep(20);
+        sw = sx_peek(tiles + idx);
+      }
+    }
+    const unsigned incm = __ballot_sync(FULL, (sw >> 62) == 2);
+    const int v = (int)(unsigned)sw;
+    if (incm) {
+      const int first = __ffs(incm) - 1;  // nearest predecessor holding its running maximum
+      pre = max(pre, __reduce_max_sync(FULL, lane <= first ? v : SX_NOEXP));
+      break;
+    }
+    pre = max(pre, __reduce_max_sync(FULL, v));
+    j -= 32;
+  }
+  SX_STAMP(c, 3, (unsigned long long)(c - 1 - j));
+  if (lane == 0) sx_publish(tiles + c, sx_word(SX_INC, max(pre, agg)));
+  return pre;
+}
+
 // Thread-per-group layout: a warp stages its 32 groups (8 KB) in shared memory
 // with cp.async; lane j owns group g0 + j for the exponent search and the
 // packing (serial, a running bit accumulator), and the packed words leave
-// through a coalesced copy.
-__global__ void __launch_bounds__(SX_WARPS * 32) k_sx_encode(const double* __restrict__ x, long long ng, int w,
+// through a coalesced copy.  One small CTA (2 warps, ~19 KB of shared memory)
+// per chunk, so that ~11 CTAs per SM hide each other's look-back latency; a
+// CTA publishes its chunk maximum as soon as its data lands.
+__device__ __forceinline__ void sx_stage(double* tile, const double* x, long long g0, int ngw, int lane) {
+#pragma unroll 8
+  for (int r = 0; r < 32; ++r) cpa8(tile + r * SX_RS + lane, x + (g0 + r) * 32 + lane, r < ngw);
+}
+
+__global__ void __launch_bounds__(SX_WARPS * 32) k_sx_encode(const double* __restrict__ x, long long ng,
+                                                             long long nc, int w, int ws,
                                                              uint32_t* __restrict__ mant, int* __restrict__ present,
                                                              long long* __restrict__ start,
                                                              unsigned long long* __restrict__ tiles, int* ticket,
                                                              int* status) {
   extern __shared__ __align__(16) unsigned char sx_smem[];
-  __shared__ int s_chunk, s_pre;
+  __shared__ long long s_chunk;
+  __shared__ int s_pre;
   __shared__ int wsum[SX_WARPS];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, q = w - 1;
   double* tile = (double*)sx_smem + wp * 32 * SX_RS;
-  uint32_t* wt = (uint32_t*)((double*)sx_smem + SX_WARPS * 32 * SX_RS) + wp * 32 * SX_WS;
+  uint32_t* wt = (uint32_t*)((double*)sx_smem + SX_WARPS * 32 * SX_RS) + wp * 32 * ws;
+  const unsigned magic = (unsigned)((0x100000000ULL + w - 1) / w);
+  const unsigned long long mask = (1ULL << w) - 1ULL;
+  // chunks in ticket order: every lower ticket belongs to a CTA already running
   if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1);
   __syncthreads();
   const long long c = s_chunk;
   const long long g0 = c * SX_GPC + wp * 32;
   const int ngw = (int)(ng - g0 < 0 ? 0 : (ng - g0 < 32 ? ng - g0 : 32));
-  // 1. stage the warp's groups (row r = group g0 + r; missing rows zero-filled)
-#pragma unroll 8
-  for (int r = 0; r < 32; ++r) cpa8(tile + r * SX_RS + lane, x + (g0 + r) * 32 + lane, r < ngw);
+  sx_stage(tile, x, g0, ngw, lane);
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncwarp();
-  // 2. group maximum exponent (monotone in |x|: the exponent of the max bits)
+  SX_STAMP(c, 0, sx_now());
+  // group maximum exponent (monotone in |x|: the exponent of the max bits)
   const double* row = tile + lane * SX_RS;
   unsigned long long mx = 0ULL;
 #pragma unroll 8
@@ -153,105 +213,81 @@ __global__ void __launch_bounds__(SX_WARPS * 32) k_sx_encode(const double* __res
   const int inc = warp_incl_max(gm, lane);
   if (lane == 31) wsum[wp] = inc;
   __syncthreads();
-  int agg = wsum[0];
+  if (wp == 0) {  // publish the chunk maximum at once, then look back
+    int agg = wsum[0];
 #pragma unroll
-  for (int i = 1; i < SX_WARPS; ++i) agg = max(agg, wsum[i]);
-  // 3. decoupled look-back for the running maximum before the chunk
-  if (wp == 0) {
-    int pre = SX_NOEXP;
-    if (c == 0) {
-      if (lane == 0) sx_publish(tiles, sx_word(SX_INC, agg));
-    } else {
-      if (lane == 0) sx_publish(tiles + c, sx_word(SX_AGG, agg));
-      // window of 256 predecessors per round: lane l reads distances 8l .. 8l+7
-      long long j = c - 1;
-      while (true) {
-        unsigned long long sw[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const long long idx = j - lane * 8 - t;
-          sw[t] = idx >= 0 ? sx_peek(tiles + idx) : sx_word(SX_INC, SX_NOEXP);
-        }
-        while (true) {
-          bool pending = false;
-#pragma unroll
-          for (int t = 0; t < 8; ++t) pending |= (sw[t] >> 62) == 0;
-          if (!__any_sync(FULL, pending)) break;
-          __nanosleep(20);
-#pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if ((sw[t] >> 62) == 0) sw[t] = sx_peek(tiles + (j - lane * 8 - t));
-        }
-        int tfirst = 8;  // nearest predecessor (in this lane's 8) holding its running maximum
-#pragma unroll
-        for (int t = 7; t >= 0; --t)
-          if ((sw[t] >> 62) == 2) tfirst = t;
-        const unsigned incm = __ballot_sync(FULL, tfirst < 8);
-        const int first = incm ? __ffs(incm) - 1 : 32;
-        const int tlim = lane < first ? 7 : (lane == first ? tfirst : -1);
-        int v = SX_NOEXP;
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (t <= tlim) v = max(v, (int)(unsigned)sw[t]);
-        pre = max(pre, __reduce_max_sync(FULL, v));
-        if (incm) break;
-        j -= 256;
-      }
-      if (lane == 0) sx_publish(tiles + c, sx_word(SX_INC, max(pre, agg)));
-    }
+    for (int i = 1; i < SX_WARPS; ++i) agg = max(agg, wsum[i]);
+    const int pre = sx_lookback(tiles, c, agg, lane);
     if (lane == 0) s_pre = pre;
+    SX_STAMP(c, 1, sx_now());
   }
   __syncthreads();
   int excl = __shfl_up_sync(FULL, inc, 1);
   if (lane == 0) excl = SX_NOEXP;
   int M = max(s_pre, excl);  // running maximum before group g0 + lane
   for (int i = 0; i < wp; ++i) M = max(M, wsum[i]);
-  // 4. normalise each entry to the running maximum at its position (R22) and
-  //    pack; a group whose maximum exceeds M raises it entry by entry and
-  //    records the block starts ("a larger exponent is encountered")
+  // normalise each entry to the running maximum at its position (R22) and
+  // pack; a group whose maximum exceeds M raises it entry by entry and
+  // records the block starts ("a larger exponent is encountered")
   const bool raise = gm > M;
-  const unsigned long long mask = (1ULL << w) - 1ULL;
-  int k = q - M;
-  bool fast = k >= -1022 && k <= 1023;
-  double sc = fast ? pow2(k) : 0.0;
-  unsigned long long acc = 0ULL;
-  int nb = 0, o = 0;
-  uint32_t* wrow = wt + lane * SX_WS;
-  for (int e = 0; e < 32; ++e) {
-    const double v = row[e];
-    if (raise) {
-      const unsigned long long b = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
-      const int Ee = b ? sx_exp_bits(b, q) : SX_NOEXP;
-      if (Ee > M) {
-        M = Ee;
-        present[M + SX_OFF] = 1;
-        start[M + SX_OFF] = (g0 + lane) * 32 + e;
-        k = q - M;
-        fast = k >= -1022 && k <= 1023;
-        sc = fast ? pow2(k) : 0.0;
+  uint32_t* wrow = wt + lane * ws;
+  if (!raise && w <= 32 && M != SX_NOEXP && q - M >= -1022 && q - M <= 1023) {
+    // common case: one exponent for the whole group, at most one word per entry
+    const double sc = pow2(q - M);
+    unsigned long long acc = 0ULL;
+    int nb = 0, o = 0;
+#pragma unroll 4
+    for (int e = 0; e < 32; ++e) {
+      const long long m = rne_int(row[e] * sc, w);
+      acc |= ((unsigned long long)m & mask) << nb;
+      nb += w;
+      if (nb >= 32) {
+        wrow[o++] = (uint32_t)acc;
+        acc >>= 32;
+        nb -= 32;
       }
     }
-    long long m = 0;
-    if (M != SX_NOEXP) m = rne_int(fast ? v * sc : ldexp(v, k), w);
-    const unsigned long long f = (unsigned long long)m & mask;
-    acc |= f << nb;
-    unsigned long long hi = nb ? f >> (64 - nb) : 0ULL;  // bits past 64 (w > 32 only)
-    nb += w;
-    while (nb >= 32) {
-      wrow[o++] = (uint32_t)acc;
-      acc = (acc >> 32) | (hi << 32);
-      hi >>= 32;
-      nb -= 32;
+  } else {
+    int k = q - M;
+    bool fast = k >= -1022 && k <= 1023;
+    double sc = fast ? pow2(k) : 0.0;
+    unsigned long long acc = 0ULL;
+    int nb = 0, o = 0;
+    for (int e = 0; e < 32; ++e) {
+      const double v = row[e];
+      if (raise) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
+        const int Ee = b ? sx_exp_bits(b, q) : SX_NOEXP;
+        if (Ee > M) {
+          M = Ee;
+          present[M + SX_OFF] = 1;
+          start[M + SX_OFF] = (g0 + lane) * 32 + e;
+          k = q - M;
+          fast = k >= -1022 && k <= 1023;
+          sc = fast ? pow2(k) : 0.0;
+        }
+      }
+      long long m = 0;
+      if (M != SX_NOEXP) m = rne_int(fast ? v * sc : ldexp(v, k), w);
+      const unsigned long long f = (unsigned long long)m & mask;
+      acc |= f << nb;
+      unsigned long long hi = nb ? f >> (64 - nb) : 0ULL;  // bits past 64 (w > 32 only)
+      nb += w;
+      while (nb >= 32) {
+        wrow[o++] = (uint32_t)acc;
+        acc = (acc >> 32) | (hi << 32);
+        hi >>= 32;
+        nb -= 32;
+      }
     }
   }
   __syncwarp();
-  // 5. coalesced copy-out of the warp's ngw * w words
-  const unsigned magic = (unsigned)((0x100000000ULL + w - 1) / w);
   uint32_t* dst = mant + g0 * w;
   for (int t = lane; t < ngw * w; t += 32) {
     const int j = (int)__umulhi((unsigned)t, magic);
-    dst[t] = wt[j * SX_WS + (t - j * w)];
+    dst[t] = wt[j * ws + (t - j * w)];
   }
+  SX_STAMP(c, 2, sx_now());
 }
 
 // Keep the w largest block exponents (ascending in xexp/xstart), *nblocks =
@@ -316,7 +352,7 @@ __global__ void __launch_bounds__(SX_WARPS * 32) k_sx_decode(const uint32_t* __r
                                                              const int32_t* __restrict__ xexp,
                                                              const int64_t* __restrict__ xstart,
                                                              const int32_t* __restrict__ nblocks, long long ng,
-                                                             int w, double* __restrict__ x) {
+                                                             int w, int ws, double* __restrict__ x) {
   extern __shared__ __align__(16) unsigned char sx_smem[];
   __shared__ long long s_start[64];
   __shared__ int s_exp[64];
@@ -328,7 +364,7 @@ __global__ void __launch_bounds__(SX_WARPS * 32) k_sx_decode(const uint32_t* __r
   __syncthreads();
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, q = w - 1;
   double* tile = (double*)sx_smem + wp * 32 * SX_RS;
-  uint32_t* wt = (uint32_t*)((double*)sx_smem + SX_WARPS * 32 * SX_RS) + wp * 32 * SX_WS;
+  uint32_t* wt = (uint32_t*)((double*)sx_smem + SX_WARPS * 32 * SX_RS) + wp * 32 * ws;
   const unsigned magic = (unsigned)((0x100000000ULL + w - 1) / w);
   const long long ntile = (ng + 31) / 32;
   const long long wg = (long long)blockIdx.x * SX_WARPS + wp, nw = (long long)gridDim.x * SX_WARPS;
@@ -338,7 +374,7 @@ __global__ void __launch_bounds__(SX_WARPS * 32) k_sx_decode(const uint32_t* __r
     const uint32_t* src = mant + g0 * w;
     for (int o = lane; o < ngw * w; o += 32) {
       const int j = (int)__umulhi((unsigned)o, magic);
-      cpa4(wt + j * SX_WS + (o - j * w), src + o);
+      cpa4(wt + j * ws + (o - j * w), src + o);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -352,7 +388,7 @@ __global__ void __launch_bounds__(SX_WARPS * 32) k_sx_decode(const uint32_t* __r
     int kb = lo;
     long long nxt = kb < nbk ? s_start[kb] : 0x7fffffffffffffffLL;
     int ks = kb > 0 ? s_exp[kb - 1] - q : 0;
-    const uint32_t* wrow = wt + lane * SX_WS;
+    const uint32_t* wrow = wt + lane * ws;
     double* row = tile + lane * SX_RS;
     for (int e = 0; e < 32; ++e) {
       if (i0 + e >= nxt) {
@@ -393,14 +429,16 @@ void launch_stream_encode(const double* x, long long n, int w, uint32_t* mant, i
   int* present = (int*)(p + 256);
   unsigned long long* tiles = (unsigned long long*)(p + 256 + SX_N * 4);
   long long* start = (long long*)(p + (sx_zeroed_bytes(nc) + 255) / 256 * 256);
+  const int ws = (w + 1) | 1;  // odd packed-row stride >= w + 1
+  const int smem = SX_WARPS * 32 * SX_RS * 8 + SX_WARPS * 32 * ws * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sx_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, SX_SMEM);
-    cudaFuncSetAttribute(k_sx_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, SX_SMEM);
     attr = true;
   }
   cudaMemsetAsync(p, 0, sx_zeroed_bytes(nc), st);
-  k_sx_encode<<<(unsigned)nc, SX_WARPS * 32, SX_SMEM, st>>>(x, ng, w, mant, present, start, tiles, ticket, status);
+  k_sx_encode<<<(unsigned)nc, SX_WARPS * 32, smem, st>>>(x, ng, nc, w, ws, mant, present, start, tiles, ticket,
+                                                         status);
   k_sx_select<<<1, 1024, 0, st>>>(present, start, w, xexp, xstart, nblocks);
 }
 
@@ -412,10 +450,15 @@ void launch_stream_decode(const uint32_t* mant, const int32_t* xexp, const int64
     cudaFuncSetAttribute(k_sx_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, SX_SMEM);
     attr = true;
   }
+  const int ws = (w + 1) | 1;
+  const int smem = SX_WARPS * 32 * SX_RS * 8 + SX_WARPS * 32 * ws * 4;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sx_decode, SX_WARPS * 32, smem);
+  if (per_sm < 1) per_sm = 1;
   long long want = (ng + 32 * SX_WARPS - 1) / (32 * SX_WARPS);
-  const long long cap = (long long)sx_num_sms() * 3;
+  const long long cap = (long long)sx_num_sms() * per_sm;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
-  k_sx_decode<<<grid, SX_WARPS * 32, SX_SMEM, st>>>(mant, xexp, xstart, nblocks, ng, w, x);
+  k_sx_decode<<<grid, SX_WARPS * 32, smem, st>>>(mant, xexp, xstart, nblocks, ng, w, ws, x);
 }
 
 }  // namespace fmg
