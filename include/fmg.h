@@ -161,6 +161,29 @@ int fmg_get_section(fmg_ctx* c, int which, int level, uint32_t* mant, int8_t* ex
  * full solve, number of kernel launches per solve. */
 int fmg_info(fmg_ctx* c, double* info10);
 
+/* Storage accounting (§8(f) row N3; Eq 6.1-6.3,
+ * DESIGN.md §2).  Host only, no device work.  For a solve whose finest FMG
+ * level is L = levels - 1, writes FMG_MEM_COUNT doubles into out (cap >=
+ * FMG_MEM_COUNT; n_l = unknowns of level l, reading R2):
+ *   0  n_L
+ *   1  mantissa bits of u_0..u_L as stored (padded x rows, w_u(l,L) bits)
+ *   2  mantissa bits of r_0..r_L as stored
+ *   3  Eq 6.1 sum for u: sum_l (k_u (L-l) + b_u) n_l
+ *   4  Eq 6.1 bound for u: (2^d/(2^d-1) b_u + 2^d/(2^d-1)^2 k_u) n_L
+ *   5  Eq 6.1 sum for r      6  Eq 6.1 bound for r
+ *   7  exponent bits with fixed 32-entry blocks (u and r, as stored)
+ *   8  exponent bits with streaming exponents (N3): <= w (32 + 64) per section
+ *   9  Eq 6.2 model: u and t as streaming windows of delta(A_l) entries at a_L bits
+ *  10  Eq 6.3 model: z as progressive-precision streaming windows
+ *  11  bytes of FP64 temporaries this implementation allocates (full arrays:
+ *      u_l, t_l, w_l per level plus six finest-size arrays; KC scratch excluded)
+ *  12  bytes of section storage this implementation allocates
+ * Errors: FMG_EINVAL (as fmg_create, or cap too small). */
+#define FMG_MEM_COUNT 13
+int fmg_memory_model(int dim, int p, int levels, const fmg_schedule* s, double* out, int cap);
+/* Device bytes a context (and its slabs) holds; negative FMG error code on NULL. */
+int64_t fmg_device_bytes(fmg_ctx* c);
+
 /* Kernel-time instrumentation for bench.py: when enabled before the first
  * solve, the captured graph brackets every launch of kernel class `cls`
  * (0 = fine residual, 1 = every fine cFas smoothing step, 2 = prolong/decode,

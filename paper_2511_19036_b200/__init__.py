@@ -62,6 +62,9 @@ _lib.fmg_get_solution.argtypes = [_vp, _vp]
 _lib.fmg_errors.argtypes = [_vp, _dp]
 _lib.fmg_get_section.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, C.POINTER(C.c_int)]
 _lib.fmg_info.argtypes = [_vp, _dp]
+_lib.fmg_memory_model.argtypes = [C.c_int, C.c_int, C.c_int, _vp, _dp, C.c_int]
+_lib.fmg_device_bytes.argtypes = [_vp]
+_lib.fmg_device_bytes.restype = C.c_int64
 _lib.fmg_enable_kernel_timing.argtypes = [_vp, C.c_int]
 _lib.fmg_kernel_time.argtypes = [_vp, _dp, C.POINTER(C.c_int)]
 _lib.fmg_kernel_times.argtypes = [_vp, _vp, C.c_int]
@@ -88,7 +91,7 @@ _lib.fmg_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, C.c_void_p]
 EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_create_slabs", "fmg_create_dist", "fmg_nccl_unique_id",
            "fmg_slab_plan", "fmg_solve_async", "fmg_solve", "fmg_solve_upto",
            "fmg_norms", "fmg_residual", "fmg_get_solution", "fmg_errors", "fmg_get_section",
-           "fmg_info", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_kernel_times", "fmg_destroy",
+           "fmg_info", "fmg_memory_model", "fmg_device_bytes", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_kernel_times", "fmg_destroy",
            "fmg_rhs_size", "fmg_set_rhs", "fmg_get_rhs", "fmg_export_solution",
            "fmg_strerror", "bfp_encode", "bfp_decode", "bfp_status",
            "bfp_stream_work_bytes", "bfp_stream_encode", "bfp_stream_decode"]
@@ -246,6 +249,10 @@ class Solver:
                 "launches_per_solve"]
         return dict(zip(keys, v.tolist()))
 
+    def device_bytes(self) -> int:
+        """Device memory this context holds (all slabs)."""
+        return int(_lib.fmg_device_bytes(self._h))
+
     def rhs_size(self) -> int:
         return int(_lib.fmg_rhs_size(self._h))
 
@@ -306,6 +313,26 @@ def bfp_decode(mant, exps, n: int, width: int, stream=None):
     _check(_lib.bfp_decode(C.c_void_p(mant.data_ptr()), C.c_void_p(exps.data_ptr()), n, width,
                            C.c_void_p(x.data_ptr()), st), "bfp_decode")
     return x
+
+
+MEMORY_KEYS = ["unknowns", "u_mantissa_bits", "r_mantissa_bits", "eq61_u", "eq61_u_bound", "eq61_r",
+               "eq61_r_bound", "exponent_bits_fixed", "exponent_bits_streaming", "eq62_ut_bits",
+               "eq63_z_bits", "fp64_temporary_bytes", "section_bytes"]
+
+
+def memory_model(dim: int, p: int, levels: int, schedule=None) -> dict:
+    """Storage accounting of a solve (Eq 6.1-6.3; host only,
+    no device work): see fmg_memory_model in include/fmg.h."""
+    import numpy as np
+    if schedule is None:
+        from fmg_inputs import default_schedule
+        schedule = default_schedule(dim, p)
+    if isinstance(schedule, dict):
+        schedule = Schedule.from_dict(schedule)
+    v = np.zeros(len(MEMORY_KEYS))
+    _check(_lib.fmg_memory_model(dim, p, levels, C.byref(schedule), v.ctypes.data_as(_dp), len(MEMORY_KEYS)),
+           "fmg_memory_model")
+    return dict(zip(MEMORY_KEYS, v.tolist()))
 
 
 def bfp_stream_encode(x, width: int, stream=None):

@@ -693,16 +693,22 @@ int fmg_set_allocator(fmg_alloc_fn alloc, fmg_free_fn free_fn, void* user) {
   return FMG_OK;
 }
 
-static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* stream, int G, int rank,
-                       fmg_ctx** out) {
-  if (!out || !s) return FMG_EINVAL;
-  *out = nullptr;
+static int check_args(int dim, int p, int levels, const fmg_schedule* s) {
   if ((dim != 2 && dim != 3) || p < 1 || p > 3 || levels < 1 || levels > kMaxLev) return FMG_EINVAL;
   if (s->b_u < 2 || s->b_r < 2 || s->k_u < 0 || s->k_r < 0 || s->n_ir < 1 || s->cheb_degree < 1 ||
       s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1) || s->smoother < 0 || s->smoother > 1)
     return FMG_EINVAL;
-  int Lmax = levels - 1;
+  const int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
+  return FMG_OK;
+}
+
+static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* stream, int G, int rank,
+                       fmg_ctx** out) {
+  if (!out || !s) return FMG_EINVAL;
+  *out = nullptr;
+  if (check_args(dim, p, levels, s)) return FMG_EINVAL;
+  int Lmax = levels - 1;
   fmg_ctx* c = new fmg_ctx();
   c->dim = dim; c->p = p; c->levels = levels; c->Lmax = Lmax; c->s = *s;
   c->G = G;
@@ -1245,6 +1251,55 @@ int fmg_info(fmg_ctx* c, double* info) {
   info[8] = bytes_solve;
   info[9] = (double)c->launches;
   return FMG_OK;
+}
+
+// Storage accounting (§8(f) row N3).  Host only.
+int fmg_memory_model(int dim, int p, int levels, const fmg_schedule* s, double* out, int cap) {
+  if (!s || !out || cap < FMG_MEM_COUNT) return FMG_EINVAL;
+  if (check_args(dim, p, levels, s)) return FMG_EINVAL;
+  const int L = levels - 1;
+  const double two_d = std::pow(2.0, dim), cst = two_d / (two_d - 1.0);
+  double nL = 0.0, um = 0.0, rm = 0.0, ue = 0.0, re = 0.0, ub = 0.0, rb = 0.0, ef = 0.0, es = 0.0;
+  double tmp62 = 0.0, tmp63 = 0.0, fp64 = 0.0, sec = 0.0;
+  for (int l = 0; l <= L; ++l) {
+    const int n = p << (l + 1);                       // nodes per side incl. the two boundary nodes - 1
+    const double N = std::pow((double)(n - 1), dim);  // unknowns (interior nodes), reading R2
+    const long long NX = ((n + 31) / 32) * 32;
+    const double stored = (double)NX * n * (dim == 3 ? n : 1);  // padded x rows
+    const int wul = s->b_u + s->k_u * (L - l), wrl = s->b_r + s->k_r * (L - l);
+    um += stored * wul;
+    rm += stored * wrl;
+    ue += N * wul;  // Eq 6.1 summand over unknowns
+    re += N * wrl;
+    ef += 2.0 * 8.0 * stored / 32.0;             // one int8 exponent per 32-entry block, u and r
+    es += (double)(wul + wrl) * (32.0 + 64.0);   // <= w (exponent, block start) pairs per section
+    // Eq 6.2 / 6.3: only delta(M_l) ~ (w(M_l) - 1) n_l^((d-1)/d) entries of a
+    // temporary live at once when streaming lexicographically;
+    // w(A) = 2p + 1 nodes per direction for Q_p, a_L = k L + b bits
+    const double delta = 2.0 * p * std::pow((double)(n - 1), dim - 1);
+    const int aL = s->b_u + s->k_u * L;
+    tmp62 += 2.0 * aL * delta;                  // u and t at a_L bits (Eq 6.2)
+    tmp63 += (double)(s->k_u * l + s->b_u) * delta;  // z, progressive (Eq 6.3)
+    fp64 += 3.0 * 8.0 * stored;                 // this implementation: full FP64 u_l, t_l, w_l
+    sec += 4.0 * (double)(NX * n * (dim == 3 ? n : 1) / 32) * (wul + wrl) + 2.0 * stored / 32.0;
+    if (l == L) {
+      nL = N;
+      fp64 += 6.0 * 8.0 * stored;               // finest-size Z, B, Y[2], Dv, PU
+    }
+  }
+  ub = (cst * s->b_u + cst / (two_d - 1.0) * s->k_u) * nL;
+  rb = (cst * s->b_r + cst / (two_d - 1.0) * s->k_r) * nL;
+  const double v[FMG_MEM_COUNT] = {nL, um, rm, ue, ub, re, rb, ef, es, tmp62, tmp63, fp64, sec};
+  for (int i = 0; i < FMG_MEM_COUNT; ++i) out[i] = v[i];
+  return FMG_OK;
+}
+
+int64_t fmg_device_bytes(fmg_ctx* c) {
+  if (!c) return -FMG_EINVAL;
+  int64_t b = 0;
+  for (auto& a : c->allocs) b += (int64_t)a.second;
+  for (fmg_ctx* sub : c->sub) b += fmg_device_bytes(sub);
+  return b;
 }
 
 int fmg_enable_kernel_timing(fmg_ctx* c, int cls) {
