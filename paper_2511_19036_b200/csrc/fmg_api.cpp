@@ -11,6 +11,7 @@
 #include "../../include/fmg.h"
 
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
 #include <cstdio>
@@ -70,6 +71,11 @@ struct fmg_ctx {
   bool march = false;             // grid levels run the march kernels (fmg_march.cu 2D, fmg_march3.cu 3D)
   int mrc[kMaxLev]{}, mitems[kMaxLev]{};  // march rows / planes per chunk, work items (3D: CTAs) per level
   int mnyb[kMaxLev]{};
+  // TMA maps of the staged arrays (march kernels): u_l rows /
+  // boxes, fine t_{l} rows for the 2D restriction, and the Z, B, Y0, Y1
+  // buffers with each level's geometry
+  bool tma = false;
+  CUtensorMap tmU[kMaxLev]{}, tmT[kMaxLev]{}, tmB[4][kMaxLev]{};
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
   // exchanged before each stencil consumer, t_{lc+1} is gathered before KC)
@@ -89,6 +95,37 @@ struct fmg_ctx {
 };
 
 namespace {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// FP64 tiled map over a [nz][ny][nx] array (rank 2 when nz == 0), box
+// bx x by x 1, out-of-range elements zero-filled.
+bool make_tmap(CUtensorMap* m, const double* base, long long nx, long long ny, long long nz, int bx, int by) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tma_encoder();
+  if (!enc || !base) return false;
+  const cuuint32_t rank = nz > 0 ? 3 : 2;
+  cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)(nz > 0 ? nz : 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
+  cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, (void*)base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 
 int wu(const fmg_ctx* c, int l, int L) { return c->s.b_u + c->s.k_u * (L - l); }
 int wr(const fmg_ctx* c, int l, int L) { return c->s.b_r + c->s.k_r * (L - l); }
@@ -406,6 +443,19 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
   const int lo = o.type == OP_RESTRICT ? o.l + 1 : o.l - 1;
   if (lo >= 0 && lo <= c->Lmax) m.lo = level_dev(c, lo);
   m.p = MPtrs{c->buf[0], c->buf[1], {c->buf[2], c->buf[3]}, c->buf[4], c->buf[5], c->pbase, c->status};
+  if (c->tma) {
+    const int l = o.l;
+    switch (o.type) {
+      case OP_RESIDUAL: m.tm = c->tmU[l]; break;
+      case OP_RESTRICT: if (c->dim == 2) m.tm = c->tmT[l + 1]; break;
+      case OP_CFAS1: if (c->dim == 3) m.tm = c->tmB[0][l]; break;
+      case OP_GS: m.tm = c->tmB[3][l]; break;
+      case OP_CHEB: m.tm = o.step == 2 ? c->tmB[1][l] : c->tmB[2 + ((o.step - 1) & 1)][l]; break;
+      default: break;
+    }
+    m.tma = (o.type == OP_RESIDUAL || o.type == OP_GS || o.type == OP_CHEB || (o.type == OP_RESTRICT && c->dim == 2) ||
+             (o.type == OP_CFAS1 && c->dim == 3)) ? 1 : 0;
+  }
   return m;
 }
 
@@ -830,6 +880,23 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   for (int i = 6; i < 8 && rc == FMG_OK; ++i) {
     c->buf[i] = (double*)dalloc(c, sizeof(double) * 2 * c->g[c->lc].size);
     if (!c->buf[i]) rc = FMG_ENOMEM;
+  }
+  // TMA maps of the staged arrays (grid levels; env FMG_TMA=0 keeps cp.async staging)
+  c->tma = c->march && !(getenv("FMG_TMA") && atoi(getenv("FMG_TMA")) == 0);
+  for (int l = 0; l <= Lmax && rc == FMG_OK && c->tma; ++l) {
+    const Geom& g = c->g[l];
+    bool ok = true;
+    if (dim == 2) {
+      // boxes start on 16-byte boundaries: halo rounded up to even (fmg_march.cu)
+      const int pe = p + (p & 1);
+      ok &= make_tmap(&c->tmU[l], c->Ul[l], g.NX, g.NY, 0, 32 + 2 * pe, 1);
+      ok &= make_tmap(&c->tmT[l], c->Tl[l], g.NX, g.NY, 0, 64 + 4 * p, 1);
+      for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, 0, 32 + 2 * pe, 1);
+    } else {
+      ok &= make_tmap(&c->tmU[l], c->Ul[l], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
+      for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
+    }
+    if (!ok) rc = FMG_ECUDA;
   }
   if (rc == FMG_OK) {
     c->n0 = coarse_count(dim, p);

@@ -40,6 +40,57 @@ __device__ __forceinline__ void cpa_wait_sync() {
   __syncthreads();
 }
 
+// ------------------------------------------------------------------ TMA --
+// Tensor-map (cp.async.bulk.tensor) staging with mbarrier completion: one
+// elected thread arms the slot's barrier with the box bytes and issues the
+// copy; out-of-range box elements are zero-filled by the hardware (the march
+// kernels' "zero outside the stored level").  The map is a __grid_constant__
+// kernel parameter (MArgs::tm).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// order this thread's generic-proxy shared accesses before a following TMA write
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y, unsigned long long* bar,
+                                            unsigned bytes) {
+  unsigned long long st;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(st)
+               : "r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"((unsigned long long)tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z,
+                                            unsigned long long* bar, unsigned bytes) {
+  unsigned long long st;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(st)
+               : "r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"((unsigned long long)tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ----------------------------------------------------------------- codec --
 // Exact int -> double for |m| < 2^31 by the 1.5*2^52 magic constant (an FP64
 // add instead of an I2F conversion); wider mantissas use the conversion.
@@ -167,9 +218,8 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
   unsigned mh = __reduce_max_sync(FULL, hi);
   unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
   bool err = __any_sync(FULL, bad);
-  double mx = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
   int q = w - 1, E = -128;
-  if (!err && mx != 0.0) {
+  if (!err && (mh | ml) != 0u) {
     int ebits = (int)((mh >> 20) & 0x7FFu);
     int E0 = ebits == 0 ? -1100 : ebits - 1022;  // ilogb(mx) + 1; subnormal max -> saturates below
     if (E0 > 127) {
@@ -177,8 +227,9 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
     } else if (E0 < -127) {
       E = -127;
     } else {
-      E = E0;
-      if (rint(mx * pow2(q - E0)) == pow2(q)) E = E0 + 1;
+      // RNE(mx 2^(q-E0)) == 2^q  <=>  frac(mx) >= 2^52 - 2^(52-q) (mx normal; never for q = 53)
+      const unsigned long long frac = (((unsigned long long)(mh & 0xFFFFFu)) << 32) | ml;
+      E = E0 + (q <= 52 && frac >= (1ULL << 52) - (1ULL << (52 - q)) ? 1 : 0);
       if (E > 127) err = true;
     }
   }

@@ -2,6 +2,7 @@
 // and the CUDA kernels (fmg_kernels.cu).  Product path only; nothing here is
 // shared with oracle/.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -91,6 +92,10 @@ struct MArgs {
   LevelDev lo;               // the other level: l-1 (decode, prolongation, cFas) or l+1 (restriction)
   MPtrs p;
   long long poff;            // norm partials (one per item) at pbase + poff, or -1
+  // TMA map of the array this launch stages (2D rows / 3D plane boxes), or
+  // zero when the kernel stages nothing from global memory
+  int tma;                   // 1: tm is valid and the kernel stages through it
+  alignas(64) CUtensorMap tm;
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.

@@ -29,6 +29,7 @@ constexpr int MW = 8;        // warps per CTA
 constexpr int MNB = 8;       // staged rows per warp (ring; >= MPF + p + 1, >= 2p + 1)
 constexpr int MPF = 4;       // rows staged ahead
 constexpr int MSLOT = 80;    // doubles per staged row (>= 64 + 4p - 2 + 1)
+constexpr int MGT = 72;      // residual: g_l(y') staged at row offset MGT (clear of the row box)
 
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -70,6 +71,33 @@ __device__ __forceinline__ void stage_row(const double* __restrict__ src, const 
     const bool okh = rowok && xh >= 0 && xh < g.NX;
     cpa8(dst + (lane < H ? lane : 32 + lane), okh ? rp + xh : src, okh);
   }
+}
+
+// TMA variant of stage_row: one box of 32 + 2H doubles from (x0 - H, y), zero
+// outside the level (the map's out-of-bounds fill); lane 0 issues it on the
+// slot's barrier.
+// The box starts at x0 - He, He = H rounded up to even (a TMA box must start
+// on a 16-byte boundary), so the consumers read the slot shifted by H & 1.
+__device__ __forceinline__ void stage_row_tma(const CUtensorMap* tm, int x0, int y, int H, double* slot,
+                                              unsigned long long* bar, int lane) {
+  if (lane == 0) {
+    const int He = H + (H & 1);
+    fence_async_smem();
+    tma_load_2d(slot, tm, x0 - He, y, bar, (unsigned)(32 + 2 * He) * 8u);
+  }
+}
+// The warp's MNB staging barriers (after the rings in dynamic shared memory),
+// initialised; nullptr when the launch does not stage through TMA.
+__device__ __forceinline__ unsigned long long* m_bars(const MArgs& a, double* msm) {
+  if (!a.tma) return nullptr;
+  unsigned long long* b = (unsigned long long*)(msm + MW * MNB * MSLOT) + threadIdx.y * MNB;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < MNB; ++k) mbar_init(b + k, 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  return b;
 }
 
 // P_l c at fine (x, y) from the coarse array (x, y passes); 0 at fine
@@ -133,7 +161,7 @@ __device__ __forceinline__ double invd2(const Coefs& cf, int P, int n, int x, in
 // out(y, Au, slot_of_row_y) runs for every output row y in [ys, ye).
 template <int P, class Stage, class Xform, class Pre, class Out>
 __device__ __forceinline__ void march_A(const Coefs& cf, int ys, int ye, int x, double* ring, Stage stage, Xform xform,
-                                        Pre pre, Out out) {
+                                        Pre pre, Out out, unsigned long long* bars = nullptr) {
   constexpr int R = 2 * P + 1;
   const int lane = threadIdx.x;
   const int tx = x % P;
@@ -146,6 +174,7 @@ __device__ __forceinline__ void march_A(const Coefs& cf, int ys, int ye, int x, 
     rb[o] = 0.0;
   }
   const int nin = (ye - ys) + 2 * P, y0 = ys - P;
+  const int SH = bars ? (P & 1) : 0;  // TMA slots start one column early for odd P
   using AuxT = decltype(pre(0));
   if (ye - ys == 1) {
     // single output row: all 2P+1 input rows in flight at once, independent x passes
@@ -154,12 +183,16 @@ __device__ __forceinline__ void march_A(const Coefs& cf, int ys, int ye, int x, 
     cp_commit();
     const AuxT a1 = pre(ys);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (bars) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) mbar_wait(bars + i, 0);
+    }
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < R; ++i) xform(y0 + i, ring + i * MSLOT);
+    for (int i = 0; i < R; ++i) xform(y0 + i, ring + i * MSLOT + SH);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const double* row = ring + i * MSLOT;
+      const double* row = ring + i * MSLOT + SH;
       double s = 0.0, t = 0.0;
 #pragma unroll
       for (int o = 0; o < R; ++o) {
@@ -177,7 +210,7 @@ __device__ __forceinline__ void march_A(const Coefs& cf, int ys, int ye, int x, 
       d = fma(cf.Kc[ty][o], ra[o], d);
       e = fma(cf.Mc[ty][o], rb[o], e);
     }
-    out(ys, d + e, ring + P * MSLOT, a1);
+    out(ys, d + e, ring + P * MSLOT + SH, a1);
     __syncwarp();
     return;
   }
@@ -193,8 +226,9 @@ __device__ __forceinline__ void march_A(const Coefs& cf, int ys, int ye, int x, 
     // register prefetch of the per-row operands of the next output row
     if (i >= 2 * P - 1 && i + 1 < nin) nxt = pre(y0 + i + 1 - P);
     cp_wait<MPF>();
+    if (bars) mbar_wait(bars + i % MNB, (unsigned)(i / MNB) & 1u);
     __syncwarp();
-    double* row = ring + (i % MNB) * MSLOT;
+    double* row = ring + (i % MNB) * MSLOT + SH;
     xform(y0 + i, row);
     double s = 0.0, t = 0.0;
 #pragma unroll
@@ -219,7 +253,7 @@ __device__ __forceinline__ void march_A(const Coefs& cf, int ys, int ye, int x, 
         d = fma(cf.Kc[ty][o], ra[o], d);
         e = fma(cf.Mc[ty][o], rb[o], e);
       }
-      out(y, d + e, ring + ((i - P) % MNB) * MSLOT, cur);
+      out(y, d + e, ring + ((i - P) % MNB) * MSLOT + SH, cur);
     }
     cur = nxt;
     __syncwarp();
@@ -255,7 +289,7 @@ __device__ __forceinline__ void m_decode_item(const MArgs& a, const Coefs& cf, c
 template <int P>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_decode(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
@@ -275,25 +309,28 @@ __device__ __forceinline__ void m_residual_item(const MArgs& a, const Coefs& cf,
   const double* __restrict__ gt = lv.gtab;
   const double gx = unk1(x, g.n) ? cf.rhs_c * gt[x] : 0.0;
   double ss = 0.0;
+  unsigned long long* bars = m_bars(a, msm);
   march_A<P>(
       cf, it.ys, it.ye, x, ring,
       [&](int yy, double* slot) {
-        stage_row(U, g, it.x0, yy, P, slot, lane);
+        if (bars) stage_row_tma(&a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
+        else stage_row(U, g, it.x0, yy, P, slot, lane);
         if (lane == 0) {
           const bool ok = yy >= 0 && yy < g.n;
-          cpa8(slot + 32 + 2 * P, ok ? gt + yy : gt, ok);  // g_l(y') for the RHS
+          cpa8(slot + (bars ? (P & 1) : 0) + MGT, ok ? gt + yy : gt, ok);  // g_l(y') for the RHS
         }
       },
       [&](int, double*) {}, [&](int) { return NoAux{}; },
       [&](int y, double au, const double* slot, const NoAux&) {
         const bool unk = unk1(x, g.n) && unk1(y, g.n);
-        const double f = gx * slot[32 + 2 * P];  // ((C g(x)) g(y))
+        const double f = gx * slot[MGT];  // ((C g(x)) g(y))
         const double t = unk ? f - au : 0.0;
         lv.T[(long long)y * g.NX + x] = t;
         ss = fma(t, t, ss);
         const long long blk = (long long)y * nxb + (it.x0 >> 5);
         warp_encode(t, a.wr, lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
-      });
+      },
+      bars);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
   if (lane == 0 && a.poff >= 0) c.pbase[a.poff + it.item] = ss;
@@ -301,7 +338,7 @@ __device__ __forceinline__ void m_residual_item(const MArgs& a, const Coefs& cf,
 template <int P>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_residual(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
@@ -330,7 +367,15 @@ __device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf,
     rv[s] = 0.0;
   }
   // fine row f staged as columns fxs .. fxs + 64 + 2H - 1
+  unsigned long long* bars = m_bars(a, msm);
   auto stage = [&](int fy, double* slot) {
+    if (bars) {
+      if (lane == 0) {
+        fence_async_smem();
+        tma_load_2d(slot, &a.tm, fxs - 1, fy, bars + (slot - ring) / MSLOT, (unsigned)(64 + 2 * H + 2) * 8u);
+      }
+      return;
+    }
     const bool rowok = fy >= 0 && fy < gf.NY;
     const double* rp = Tf + (long long)(rowok ? fy : 0) * gf.NX;
 #pragma unroll
@@ -354,8 +399,9 @@ __device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf,
     if (i + MPF < nin) stage(fy0 + i + MPF, ring + ((i + MPF) % MNB) * MSLOT);
     cp_commit();
     cp_wait<MPF>();
+    if (bars) mbar_wait(bars + i % MNB, (unsigned)(i / MNB) & 1u);
     __syncwarp();
-    const double* row = ring + (i % MNB) * MSLOT;
+    const double* row = ring + (i % MNB) * MSLOT + (bars ? 1 : 0);  // (TMA box starts at fxs - 1: H is odd)
     double v = 0.0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) v = fma(rw[s], row[2 * lane + s], v);  // (t = +0 at fine non-unknowns)
@@ -383,7 +429,7 @@ __device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf,
 template <int P>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_restrict(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
@@ -483,8 +529,13 @@ __device__ __forceinline__ void m_gs_item(const MArgs& a, const Coefs& cf, const
   double* __restrict__ Yv = c.Y[1];
   const int cx = a.step % (P + 1), cy = a.step / (P + 1);
   const bool colx = x % (P + 1) == cx;
+  unsigned long long* bars = m_bars(a, msm);
   march_A<P>(
-      cf, it.ys, it.ye, x, ring, [&](int yy, double* slot) { stage_row(Yv, g, it.x0, yy, P, slot, lane); },
+      cf, it.ys, it.ye, x, ring,
+      [&](int yy, double* slot) {
+        if (bars) stage_row_tma(&a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
+        else stage_row(Yv, g, it.x0, yy, P, slot, lane);
+      },
       [&](int, double*) {},
       [&](int yn) {
         const long long idx = (long long)yn * g.NX + x, blk = (long long)yn * nxb + (it.x0 >> 5);
@@ -506,12 +557,13 @@ __device__ __forceinline__ void m_gs_item(const MArgs& a, const Coefs& cf, const
         const double yv = mine ? yo + invd2(cf, P, g.n, x, y) * (p.b - ay) : yo;
         if (a.last) m_finalize_r(c, a, lv, idx, blk, yv, p.z, p.pu, p.w0, p.w1, p.e, lane);
         else if (mine) Yv[idx] = yv;
-      });
+      },
+      bars);
 }
 template <int P>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
@@ -533,8 +585,13 @@ __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, con
   const double* __restrict__ src = (j == 2) ? c.B : c.Y[(j - 1) & 1];
   const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);
   const double al = cf.cal[j - 1], be = cf.cbe[j - 1];
+  unsigned long long* bars = m_bars(a, msm);
   march_A<P>(
-      cf, it.ys, it.ye, x, ring, [&](int yy, double* slot) { stage_row(src, g, it.x0, yy, P, slot, lane); },
+      cf, it.ys, it.ye, x, ring,
+      [&](int yy, double* slot) {
+        if (bars) stage_row_tma(&a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
+        else stage_row(src, g, it.x0, yy, P, slot, lane);
+      },
       [&](int yy, double* slot) {
         if (j != 2) return;
         // y_1 = inv_theta (invD b) on the lane's own staged entries
@@ -572,12 +629,13 @@ __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, con
           c.Y[j & 1][idx] = yv;
           c.Dv[idx] = d;
         }
-      });
+      },
+      bars);
 }
 template <int P>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
@@ -588,7 +646,7 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx
 template <int P>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   MItem it;
@@ -597,7 +655,7 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* 
 }
 
 // ------------------------------------------------------------------ host --
-int march_smem() { return MW * MNB * MSLOT * 8; }
+int march_smem() { return MW * MNB * MSLOT * 8 + MW * MNB * 8; }
 int march_warps() { return MW; }
 
 #define M_DISPATCH(p, F)   \

@@ -69,6 +69,30 @@ __device__ __forceinline__ void stage_box(const double* __restrict__ src, const 
   }
 }
 
+// TMA variant of stage_box: one 40 x (TW3 + 2H) x 1 box from (x0 - He, y0 - H, z),
+// He = H rounded up to even (16-byte box start), row stride RS3 = 40; the
+// consumers read the slot shifted by H & 1; out-of-range elements zero-filled
+// by the map.  Issued by thread (0, 0) on the slot's barrier.
+__device__ __forceinline__ void stage_box_tma(const CUtensorMap* tm, int x0, int y0, int z, int H, double* slot,
+                                              unsigned long long* bar) {
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    fence_async_smem();
+    tma_load_3d(slot, tm, x0 - H - (H & 1), y0 - H, z, bar, (unsigned)(RS3 * (TW3 + 2 * H)) * 8u);
+  }
+}
+// The CTA's NB3 staging barriers (after XB), initialised; nullptr without TMA.
+__device__ __forceinline__ unsigned long long* m3_bars(const MArgs& a, double* after_xb) {
+  if (!a.tma) return nullptr;
+  unsigned long long* b = (unsigned long long*)after_xb;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < NB3; ++k) mbar_init(b + k, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  return b;
+}
+
 __device__ __forceinline__ double invd3(const Coefs& cf, int P, int n, int l, int x, int y, int z) {
   if (!unk1(x, n) || !unk1(y, n) || !unk1(z, n)) return 0.0;
   return cf.invd[((z % P) * P + y % P) * P + x % P] * pow2(l + 1);
@@ -81,7 +105,8 @@ __device__ __forceinline__ double invd3(const Coefs& cf, int P, int n, int l, in
 // of plane z, aux) runs for every output plane z in [zs, ze).
 template <int P, class Stage, class Xform, class Pre, class Out>
 __device__ __forceinline__ void march3_A(const Coefs& cf, const M3Item& it, int l, double* ring, double* XA,
-                                         double* XB, Stage stage, Xform xform, Pre pre, Out out) {
+                                         double* XB, Stage stage, Xform xform, Pre pre, Out out,
+                                         unsigned long long* bars = nullptr) {
   constexpr int R = 2 * P + 1, NR = TW3 + 2 * P;
   const int lane = threadIdx.x, w = threadIdx.y;
   const int x = it.x0 + lane, y = it.y0 + w;
@@ -96,6 +121,7 @@ __device__ __forceinline__ void march3_A(const Coefs& cf, const M3Item& it, int 
     sr[o] = 0.0;
   }
   const int nin = (it.ze - it.zs) + 2 * P, z0 = it.zs - P;
+  const int SH = bars ? (P & 1) : 0;  // TMA boxes start one column early for odd P
   using AuxT = decltype(pre(0));
   AuxT cur{}, nxt{};
 #pragma unroll
@@ -108,8 +134,9 @@ __device__ __forceinline__ void march3_A(const Coefs& cf, const M3Item& it, int 
     cp3_commit();
     if (i >= 2 * P - 1 && i + 1 < nin) nxt = pre(z0 + i + 1 - P);
     cp3_wait();
+    if (bars) mbar_wait(bars + i % NB3, (unsigned)(i / NB3) & 1u);
     __syncthreads();
-    double* slot = ring + (i % NB3) * (NR * RS3);
+    double* slot = ring + (i % NB3) * (NR * RS3) + SH;
     xform(z0 + i, slot);
     // x pass of the NR staged rows (warp w: rows w, w + 8, ...)
     for (int r = w; r < NR; r += TW3) {
@@ -148,7 +175,7 @@ __device__ __forceinline__ void march3_A(const Coefs& cf, const M3Item& it, int 
       for (int o = 0; o < R; ++o) acc = fma(cf.Kc[tz][o], cr[o], acc);
 #pragma unroll
       for (int o = 0; o < R; ++o) acc = fma(cf.Mc[tz][o], sr[o], acc);
-      out(z, acc * hl, ring + ((i - P) % NB3) * (NR * RS3), cur);
+      out(z, acc * hl, ring + ((i - P) % NB3) * (NR * RS3) + SH, cur);
     }
     cur = nxt;
   }
@@ -198,7 +225,7 @@ __device__ __forceinline__ size_t m3_ring_doubles() {
 template <int P>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_residual(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                             const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   M3Item it;
@@ -211,13 +238,17 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_residual(const
   double* ring = msm;
   double* XA = ring + m3_ring_doubles<P>();
   double* XB = XA + (TW3 + 2 * P) * 32;
+  unsigned long long* bars = m3_bars(a, XB + (TW3 + 2 * P) * 32);
   const double* __restrict__ U = lv.U;
   const double* __restrict__ gt = lv.gtab;
   const double gxy = (unk1(x, g.n) && unk1(y, g.n)) ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
   const int nxb = g.NX >> 5;
   double ss = 0.0;
   march3_A<P>(
-      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) { stage_box(U, g, it.x0, it.y0, zz, P, slot); },
+      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
+        if (bars) stage_box_tma(&a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        else stage_box(U, g, it.x0, it.y0, zz, P, slot);
+      },
       [&](int, double*) {},
       [&](int zn) {
         RAux3 r{};
@@ -233,7 +264,8 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_residual(const
         ss = fma(t, t, ss);
         const long long blk = ((long long)z * g.NY + y) * nxb + (it.x0 >> 5);
         warp_encode(t, a.wr, lv.rmant + blk * lv.rstride, lv.rexp + blk, lane, c.status);
-      });
+      },
+      bars);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
   if (lane == 0 && a.poff >= 0) c.pbase[a.poff + (long long)it.cta * TW3 + threadIdx.y] = ss;
@@ -254,7 +286,7 @@ __device__ __forceinline__ void m3_finalize(const MPtrs& c, const MArgs& a, cons
 template <int P>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                          const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   M3Item it;
@@ -267,9 +299,13 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
   double* ring = msm;
   double* XA = ring + m3_ring_doubles<P>();
   double* XB = XA + (TW3 + 2 * P) * 32;
+  unsigned long long* bars = m3_bars(a, XB + (TW3 + 2 * P) * 32);
   const int nxb = g.NX >> 5;
   march3_A<P>(
-      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) { stage_box(c.Z, g, it.x0, it.y0, zz, P, slot); },
+      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
+        if (bars) stage_box_tma(&a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        else stage_box(c.Z, g, it.x0, it.y0, zz, P, slot);
+      },
       [&](int, double*) {},
       [&](int zn) {
         CAux3 q{};
@@ -308,7 +344,8 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
         } else {
           c.B[idx] = b;
         }
-      });
+      },
+      bars);
 }
 
 // Chebyshev step j >= 2; step 2 stages b and forms
@@ -316,7 +353,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
 template <int P>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                         const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   M3Item it;
@@ -329,13 +366,17 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
   double* ring = msm;
   double* XA = ring + m3_ring_doubles<P>();
   double* XB = XA + (TW3 + 2 * P) * 32;
+  unsigned long long* bars = m3_bars(a, XB + (TW3 + 2 * P) * 32);
   const int nxb = g.NX >> 5;
   const int j = a.step;
   const double* __restrict__ src = (j == 2) ? c.B : c.Y[(j - 1) & 1];
   const double al = cf.cal[j - 1], be = cf.cbe[j - 1];
   constexpr int NR = TW3 + 2 * P;
   march3_A<P>(
-      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) { stage_box(src, g, it.x0, it.y0, zz, P, slot); },
+      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
+        if (bars) stage_box_tma(&a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        else stage_box(src, g, it.x0, it.y0, zz, P, slot);
+      },
       [&](int zz, double* slot) {
         if (j != 2) return;
         // y_1 = inv_theta (invD b) on the entries this thread staged
@@ -383,7 +424,8 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
           c.Y[j & 1][idx] = yv;
           c.Dv[idx] = d;
         }
-      });
+      },
+      bars);
 }
 
 // Multicolour Gauss-Seidel colour `a.step` (>= 1) in place on Y[1]
@@ -392,7 +434,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
 template <int P>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                       const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   M3Item it;
@@ -405,12 +447,16 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCt
   double* ring = msm;
   double* XA = ring + m3_ring_doubles<P>();
   double* XB = XA + (TW3 + 2 * P) * 32;
+  unsigned long long* bars = m3_bars(a, XB + (TW3 + 2 * P) * 32);
   const int nxb = g.NX >> 5;
   double* __restrict__ Yv = c.Y[1];
   const int cx = a.step % (P + 1), cy = (a.step / (P + 1)) % (P + 1), cz = a.step / ((P + 1) * (P + 1));
   const bool colxy = x % (P + 1) == cx && y % (P + 1) == cy;
   march3_A<P>(
-      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) { stage_box(Yv, g, it.x0, it.y0, zz, P, slot); },
+      cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
+        if (bars) stage_box_tma(&a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        else stage_box(Yv, g, it.x0, it.y0, zz, P, slot);
+      },
       [&](int, double*) {},
       [&](int zn) {
         CAux3 q{};
@@ -437,7 +483,8 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCt
         const double yv = mine ? yo + invd3(cf, P, g.n, a.l, x, y, z) * (q.b - ay) : yo;
         if (a.last) m3_finalize(c, a, lv, idx, blk, yv, q.z, q.pu, q.w0, q.w1, q.e, lane);
         else if (mine) Yv[idx] = yv;
-      });
+      },
+      bars);
 }
 
 // Pointwise prolongation march: for each fine (x, y) the x/y
@@ -531,7 +578,7 @@ constexpr int RPF3 = 2, RNB3 = 3, RRS3 = 80;
 template <int P>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                             const __grid_constant__ Coefs cf) {
-  extern __shared__ double msm[];
+  extern __shared__ __align__(128) double msm[];
   pdl_wait();
   pdl_trigger();
   M3Item it;
@@ -618,7 +665,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const
 }
 
 // ------------------------------------------------------------------ host --
-static int m3_smem_A(int p) { return (int)(((size_t)NB3 * (TW3 + 2 * p) * RS3 + 2 * (TW3 + 2 * p) * 32) * 8); }
+static int m3_smem_A(int p) { return (int)(((size_t)NB3 * (TW3 + 2 * p) * RS3 + 2 * (TW3 + 2 * p) * 32) * 8 + NB3 * 8); }
 static int m3_smem_R(int p) {
   const int FR = 2 * TW3 + 2 * (2 * p - 1);
   return (RNB3 * FR * RRS3 + FR * 32) * 8;
