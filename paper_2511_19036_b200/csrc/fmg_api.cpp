@@ -881,8 +881,15 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     c->buf[i] = (double*)dalloc(c, sizeof(double) * 2 * c->g[c->lc].size);
     if (!c->buf[i]) rc = FMG_ENOMEM;
   }
-  // TMA maps of the staged arrays (grid levels; env FMG_TMA=0 keeps cp.async staging)
-  c->tma = c->march && !(getenv("FMG_TMA") && atoi(getenv("FMG_TMA")) == 0);
+  // TMA maps of the staged arrays (grid levels).  Measured: 3D
+  // plane boxes gain 7-8 % (C3, C4) over per-lane cp.async, 2D rows of 36-40
+  // doubles lose 0.4 % (C2), so the default is TMA in 3D only; FMG_TMA=1 forces
+  // it in 2D too, FMG_TMA=0 turns it off.
+  {
+    const char* e = getenv("FMG_TMA");
+    const int want = e ? atoi(e) : -1;
+    c->tma = c->march && (want == 1 || (want < 0 && dim == 3));
+  }
   for (int l = 0; l <= Lmax && rc == FMG_OK && c->tma; ++l) {
     const Geom& g = c->g[l];
     bool ok = true;

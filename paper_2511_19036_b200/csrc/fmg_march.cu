@@ -81,8 +81,9 @@ __device__ __forceinline__ void stage_row(const double* __restrict__ src, const 
 __device__ __forceinline__ void stage_row_tma(const CUtensorMap* tm, int x0, int y, int H, double* slot,
                                               unsigned long long* bar, int lane) {
   if (lane == 0) {
+    // (no proxy fence: the slot's previous generic reads were consumed MNB - MPF
+    // rows ago behind __syncwarp; in-place writers fence themselves)
     const int He = H + (H & 1);
-    fence_async_smem();
     tma_load_2d(slot, tm, x0 - He, y, bar, (unsigned)(32 + 2 * He) * 8u);
   }
 }
@@ -371,7 +372,6 @@ __device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf,
   auto stage = [&](int fy, double* slot) {
     if (bars) {
       if (lane == 0) {
-        fence_async_smem();
         tma_load_2d(slot, &a.tm, fxs - 1, fy, bars + (slot - ring) / MSLOT, (unsigned)(64 + 2 * H + 2) * 8u);
       }
       return;
@@ -600,6 +600,7 @@ __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, con
           double& v = slot[lane < P ? lane : 32 + lane];
           v = cf.inv_theta * (invd2(cf, P, g.n, xh, yy) * v);
         }
+        if (bars) fence_async_smem();  // these generic writes precede a later TMA refill of the slot
         __syncwarp();
       },
       [&](int yn) {

@@ -125,6 +125,15 @@ def test_fmg_parity_small(P, d, p, levels):
     compare_solvers(P, d, p, levels)
 
 
+@pytest.mark.parametrize("tma", ["0", "1"])
+@pytest.mark.parametrize("d,p,levels", [(2, 1, 7), (2, 2, 6), (2, 3, 5), (3, 1, 5), (3, 2, 4), (3, 3, 4)])
+def test_fmg_parity_staging_paths(P, monkeypatch, tma, d, p, levels):
+    """Both staging paths of the march kernels: per-lane
+    cp.async and TMA boxes (FMG_TMA, read at context creation), bit-exact."""
+    monkeypatch.setenv("FMG_TMA", tma)
+    compare_solvers(P, d, p, levels)
+
+
 def test_fmg_parity_C1(P):
     c = CONFIGS["C1"]
     compare_solvers(P, c["dim"], c["p"], c["levels"])
@@ -278,10 +287,13 @@ def test_nccl_dist_single_rank(P):
 
 
 # ------------------------------------------ Gauss-Seidel smoother (§8f N1) --
+@pytest.mark.parametrize("tma", ["0", "1"])
 @pytest.mark.parametrize("d,p,levels", [(2, 1, 6), (2, 2, 5), (2, 3, 4), (3, 1, 5), (3, 2, 4), (3, 3, 3)])
-def test_fmg_parity_multicolour_gs(P, d, p, levels):
+def test_fmg_parity_multicolour_gs(P, monkeypatch, tma, d, p, levels):
     """Multicolour Gauss-Seidel smoother ((p+1)^d colours): GPU (KC + march
-    colour kernels) bit-identical to the oracle's mc_gauss_seidel."""
+    colour kernels) bit-identical to the oracle's mc_gauss_seidel, with both
+    staging paths (FMG_TMA)."""
+    monkeypatch.setenv("FMG_TMA", tma)
     so = O.schedule(d, p, smoother="mcgs")
     oc = O.CFMG(d, p, levels, so)
     oc.solve()
