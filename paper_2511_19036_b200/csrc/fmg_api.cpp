@@ -76,6 +76,7 @@ struct fmg_ctx {
   // buffers with each level's geometry
   bool tma = false;
   CUtensorMap tmU[kMaxLev]{}, tmT[kMaxLev]{}, tmB[4][kMaxLev]{};
+  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3] x kMaxLev
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
   // exchanged before each stencil consumer, t_{lc+1} is gathered before KC)
@@ -445,12 +446,13 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
   m.p = MPtrs{c->buf[0], c->buf[1], {c->buf[2], c->buf[3]}, c->buf[4], c->buf[5], c->pbase, c->status};
   if (c->tma) {
     const int l = o.l;
+    const CUtensorMap* U = c->tm_dev, *T = U + kMaxLev, *B = T + kMaxLev;  // device copies
     switch (o.type) {
-      case OP_RESIDUAL: m.tm = c->tmU[l]; break;
-      case OP_RESTRICT: if (c->dim == 2) m.tm = c->tmT[l + 1]; break;
-      case OP_CFAS1: if (c->dim == 3) m.tm = c->tmB[0][l]; break;
-      case OP_GS: m.tm = c->tmB[3][l]; break;
-      case OP_CHEB: m.tm = o.step == 2 ? c->tmB[1][l] : c->tmB[2 + ((o.step - 1) & 1)][l]; break;
+      case OP_RESIDUAL: m.tm = U + l; break;
+      case OP_RESTRICT: if (c->dim == 2) m.tm = T + l + 1; break;
+      case OP_CFAS1: if (c->dim == 3) m.tm = B + l; break;
+      case OP_GS: m.tm = B + 3 * kMaxLev + l; break;
+      case OP_CHEB: m.tm = B + (o.step == 2 ? 1 : 2 + ((o.step - 1) & 1)) * kMaxLev + l; break;
       default: break;
     }
     m.tma = (o.type == OP_RESIDUAL || o.type == OP_GS || o.type == OP_CHEB || (o.type == OP_RESTRICT && c->dim == 2) ||
@@ -904,6 +906,17 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
     }
     if (!ok) rc = FMG_ECUDA;
+  }
+  if (rc == FMG_OK && c->tma) {
+    std::vector<CUtensorMap> all(6 * kMaxLev);
+    for (int l = 0; l < kMaxLev; ++l) {
+      all[l] = c->tmU[l];
+      all[kMaxLev + l] = c->tmT[l];
+      for (int i = 0; i < 4; ++i) all[(2 + i) * kMaxLev + l] = c->tmB[i][l];
+    }
+    c->tm_dev = (CUtensorMap*)dalloc(c, sizeof(CUtensorMap) * all.size());  // (256-byte aligned)
+    if (!c->tm_dev) rc = FMG_ENOMEM;
+    else cudaMemcpy(c->tm_dev, all.data(), sizeof(CUtensorMap) * all.size(), cudaMemcpyHostToDevice);
   }
   if (rc == FMG_OK) {
     c->n0 = coarse_count(dim, p);

@@ -93,9 +93,10 @@ struct MArgs {
   MPtrs p;
   long long poff;            // norm partials (one per item) at pbase + poff, or -1
   // TMA map of the array this launch stages (2D rows / 3D plane boxes), or
-  // zero when the kernel stages nothing from global memory
+  // none when the kernel stages nothing from global memory;
+  // kept in device memory so the launch parameters stay small
   int tma;                   // 1: tm is valid and the kernel stages through it
-  alignas(64) CUtensorMap tm;
+  const CUtensorMap* tm;     // TMA map of the staged array, in device global memory
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_decode(const DevC
 }
 
 // t_L = f_L - A_L u_L, r_L = enc(t_L), ||t_L||^2 partial
-template <int P>
+template <int P, bool TMA>
 __device__ __forceinline__ void m_residual_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
   const MPtrs& c = a.p;
   const LevelDev& lv = a.lv;
@@ -310,21 +310,21 @@ __device__ __forceinline__ void m_residual_item(const MArgs& a, const Coefs& cf,
   const double* __restrict__ gt = lv.gtab;
   const double gx = unk1(x, g.n) ? cf.rhs_c * gt[x] : 0.0;
   double ss = 0.0;
-  unsigned long long* bars = m_bars(a, msm);
+  unsigned long long* bars = TMA ? m_bars(a, msm) : nullptr;  // (compile-time path)
   march_A<P>(
       cf, it.ys, it.ye, x, ring,
       [&](int yy, double* slot) {
-        if (bars) stage_row_tma(&a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
+        if (bars) stage_row_tma(a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
         else stage_row(U, g, it.x0, yy, P, slot, lane);
         if (lane == 0) {
           const bool ok = yy >= 0 && yy < g.n;
-          cpa8(slot + (bars ? (P & 1) : 0) + MGT, ok ? gt + yy : gt, ok);  // g_l(y') for the RHS
+          cpa8(slot + (TMA ? (P & 1) + MGT : 32 + 2 * P), ok ? gt + yy : gt, ok);  // g_l(y') for the RHS
         }
       },
       [&](int, double*) {}, [&](int) { return NoAux{}; },
       [&](int y, double au, const double* slot, const NoAux&) {
         const bool unk = unk1(x, g.n) && unk1(y, g.n);
-        const double f = gx * slot[MGT];  // ((C g(x)) g(y))
+        const double f = gx * slot[TMA ? MGT : 32 + 2 * P];  // ((C g(x)) g(y))
         const double t = unk ? f - au : 0.0;
         lv.T[(long long)y * g.NX + x] = t;
         ss = fma(t, t, ss);
@@ -336,7 +336,7 @@ __device__ __forceinline__ void m_residual_item(const MArgs& a, const Coefs& cf,
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
   if (lane == 0 && a.poff >= 0) c.pbase[a.poff + it.item] = ss;
 }
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_residual(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -344,12 +344,12 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_residual(const De
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  m_residual_item<P>(a, cf, it, msm);
+  m_residual_item<P, TMA>(a, cf, it, msm);
 }
 
 // t_l = R_{l+1} t_{l+1} (restricts t, not r: PAPER.md:742-744), r_l = enc(t_l).
 // The warp owns 32 coarse columns; every coarse row consumes two fine rows.
-template <int P>
+template <int P, bool TMA>
 __device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
   constexpr int NS = 4 * P - 1, H = 2 * P - 1;
   const MPtrs& c = a.p;
@@ -368,11 +368,11 @@ __device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf,
     rv[s] = 0.0;
   }
   // fine row f staged as columns fxs .. fxs + 64 + 2H - 1
-  unsigned long long* bars = m_bars(a, msm);
+  unsigned long long* bars = TMA ? m_bars(a, msm) : nullptr;  // (compile-time path)
   auto stage = [&](int fy, double* slot) {
     if (bars) {
       if (lane == 0) {
-        tma_load_2d(slot, &a.tm, fxs - 1, fy, bars + (slot - ring) / MSLOT, (unsigned)(64 + 2 * H + 2) * 8u);
+        tma_load_2d(slot, a.tm, fxs - 1, fy, bars + (slot - ring) / MSLOT, (unsigned)(64 + 2 * H + 2) * 8u);
       }
       return;
     }
@@ -426,7 +426,7 @@ __device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf,
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
   if (lane == 0 && a.poff >= 0) c.pbase[a.poff + it.item] = ss;
 }
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_restrict(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_restrict(const De
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  m_restrict_item<P>(a, cf, it, msm);
+  m_restrict_item<P, TMA>(a, cf, it, msm);
 }
 
 // ý_l = enc(y); w_l = z_l + dec ý_l (l < L); ú_l = enc(dec ú_l + dec ý_l);
@@ -519,7 +519,7 @@ __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, co
 // nodes of that colour y = y + invD (b - A y) (A on the current iterate; nodes
 // of one colour are uncoupled, so in-place is exact); the last colour
 // finalises every node of the row (oracle mc_gauss_seidel).
-template <int P>
+template <int P, bool TMA>
 __device__ __forceinline__ void m_gs_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
   const MPtrs& c = a.p;
   const LevelDev& lv = a.lv;
@@ -529,11 +529,11 @@ __device__ __forceinline__ void m_gs_item(const MArgs& a, const Coefs& cf, const
   double* __restrict__ Yv = c.Y[1];
   const int cx = a.step % (P + 1), cy = a.step / (P + 1);
   const bool colx = x % (P + 1) == cx;
-  unsigned long long* bars = m_bars(a, msm);
+  unsigned long long* bars = TMA ? m_bars(a, msm) : nullptr;  // (compile-time path)
   march_A<P>(
       cf, it.ys, it.ye, x, ring,
       [&](int yy, double* slot) {
-        if (bars) stage_row_tma(&a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
+        if (bars) stage_row_tma(a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
         else stage_row(Yv, g, it.x0, yy, P, slot, lane);
       },
       [&](int, double*) {},
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cfas1(const DevCt
 // Chebyshev step j >= 2: q = b - A y; d_j = fma(alpha_j, d_{j-1}, beta_j (invD q));
 // y_j = y_{j-1} + d_j.  Step 2 stages b and forms
 // y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
-template <int P>
+template <int P, bool TMA>
 __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
   const MPtrs& c = a.p;
   const LevelDev& lv = a.lv;
@@ -585,11 +585,11 @@ __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, con
   const double* __restrict__ src = (j == 2) ? c.B : c.Y[(j - 1) & 1];
   const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);
   const double al = cf.cal[j - 1], be = cf.cbe[j - 1];
-  unsigned long long* bars = m_bars(a, msm);
+  unsigned long long* bars = TMA ? m_bars(a, msm) : nullptr;  // (compile-time path)
   march_A<P>(
       cf, it.ys, it.ye, x, ring,
       [&](int yy, double* slot) {
-        if (bars) stage_row_tma(&a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
+        if (bars) stage_row_tma(a.tm, it.x0, yy, P, slot, bars + (slot - ring) / MSLOT, lane);
         else stage_row(src, g, it.x0, yy, P, slot, lane);
       },
       [&](int yy, double* slot) {
@@ -633,7 +633,7 @@ __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, con
       },
       bars);
 }
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -641,10 +641,10 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  m_cheb_item<P>(a, cf, it, msm);
+  m_cheb_item<P, TMA>(a, cf, it, msm);
 }
 
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -652,11 +652,11 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* 
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  m_gs_item<P>(a, cf, it, msm);
+  m_gs_item<P, TMA>(a, cf, it, msm);
 }
 
 // ------------------------------------------------------------------ host --
-int march_smem() { return MW * MNB * MSLOT * 8 + MW * MNB * 8; }
+int march_smem(bool tma) { return MW * MNB * MSLOT * 8 + (tma ? MW * MNB * 8 : 0); }
 int march_warps() { return MW; }
 
 #define M_DISPATCH(p, F)   \
@@ -667,12 +667,16 @@ int march_warps() { return MW; }
   } while (0)
 
 void march_set_attributes() {
-#define F(P)                                                                                            \
-  cudaFuncSetAttribute(k_m_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());     \
-  cudaFuncSetAttribute(k_m_restrict<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());     \
-  cudaFuncSetAttribute(k_m_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());        \
-  cudaFuncSetAttribute(k_m_cheb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());      \
-  cudaFuncSetAttribute(k_m_gs<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem());
+#define F(P)                                                                                                   \
+  cudaFuncSetAttribute(k_m_residual<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false)); \
+  cudaFuncSetAttribute(k_m_residual<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));   \
+  cudaFuncSetAttribute(k_m_restrict<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false)); \
+  cudaFuncSetAttribute(k_m_restrict<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));   \
+  cudaFuncSetAttribute(k_m_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));          \
+  cudaFuncSetAttribute(k_m_cheb<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));     \
+  cudaFuncSetAttribute(k_m_cheb<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));       \
+  cudaFuncSetAttribute(k_m_gs<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));       \
+  cudaFuncSetAttribute(k_m_gs<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));
   F(1) F(2) F(3)
 #undef F
 }
@@ -695,18 +699,21 @@ static void m_launch(K kernel, int nitems, int smem, cudaStream_t st, const DevC
 
 void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf) {
   const DevCtx* c = (const DevCtx*)devctx;
-  const int sm = march_smem();
-#define F(P)                                                                            \
-  switch (a.type) {                                                                     \
-    case OP_DECODE: m_launch(k_m_decode<P>, a.nitems, 0, st, c, a, cf); break;          \
-    case OP_RESIDUAL: m_launch(k_m_residual<P>, a.nitems, sm, st, c, a, cf); break;     \
-    case OP_RESTRICT: m_launch(k_m_restrict<P>, a.nitems, sm, st, c, a, cf); break;     \
-    case OP_CFAS1: m_launch(k_m_cfas1<P>, a.nitems, sm, st, c, a, cf); break;           \
-    case OP_GS: m_launch(k_m_gs<P>, a.nitems, sm, st, c, a, cf); break;                 \
-    default: m_launch(k_m_cheb<P>, a.nitems, sm, st, c, a, cf); break;                  \
+  const bool t = a.tma != 0;
+  const int sm = march_smem(t);
+#define TM(K, P) (t ? (void (*)(const DevCtx*, MArgs, Coefs))K<P, true> : (void (*)(const DevCtx*, MArgs, Coefs))K<P, false>)
+#define F(P)                                                                                     \
+  switch (a.type) {                                                                              \
+    case OP_DECODE: m_launch(k_m_decode<P>, a.nitems, 0, st, c, a, cf); break;                   \
+    case OP_RESIDUAL: m_launch(TM(k_m_residual, P), a.nitems, sm, st, c, a, cf); break;          \
+    case OP_RESTRICT: m_launch(TM(k_m_restrict, P), a.nitems, sm, st, c, a, cf); break;          \
+    case OP_CFAS1: m_launch(k_m_cfas1<P>, a.nitems, march_smem(false), st, c, a, cf); break;     \
+    case OP_GS: m_launch(TM(k_m_gs, P), a.nitems, sm, st, c, a, cf); break;                      \
+    default: m_launch(TM(k_m_cheb, P), a.nitems, sm, st, c, a, cf); break;                       \
   }
   M_DISPATCH(p, F);
 #undef F
+#undef TM
 }
 
 }  // namespace fmg

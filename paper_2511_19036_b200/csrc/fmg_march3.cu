@@ -222,7 +222,7 @@ __device__ __forceinline__ size_t m3_ring_doubles() {
 
 // ------------------------------------------------------------ kernels --
 // t_L = f_L - A_L u_L, r_L = enc(t_L), ||t_L||^2 partial
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_residual(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                             const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_residual(const
   double* ring = msm;
   double* XA = ring + m3_ring_doubles<P>();
   double* XB = XA + (TW3 + 2 * P) * 32;
-  unsigned long long* bars = m3_bars(a, XB + (TW3 + 2 * P) * 32);
+  unsigned long long* bars = TMA ? m3_bars(a, XB + (TW3 + 2 * P) * 32) : nullptr;  // (compile-time path)
   const double* __restrict__ U = lv.U;
   const double* __restrict__ gt = lv.gtab;
   const double gxy = (unk1(x, g.n) && unk1(y, g.n)) ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_residual(const
   double ss = 0.0;
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
-        if (bars) stage_box_tma(&a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(U, g, it.x0, it.y0, zz, P, slot);
       },
       [&](int, double*) {},
@@ -283,7 +283,7 @@ __device__ __forceinline__ void m3_finalize(const MPtrs& c, const MArgs& a, cons
   lv.U[idx] = uq + pu;
 }
 
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                          const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -299,11 +299,11 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
   double* ring = msm;
   double* XA = ring + m3_ring_doubles<P>();
   double* XB = XA + (TW3 + 2 * P) * 32;
-  unsigned long long* bars = m3_bars(a, XB + (TW3 + 2 * P) * 32);
+  unsigned long long* bars = TMA ? m3_bars(a, XB + (TW3 + 2 * P) * 32) : nullptr;  // (compile-time path)
   const int nxb = g.NX >> 5;
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
-        if (bars) stage_box_tma(&a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(c.Z, g, it.x0, it.y0, zz, P, slot);
       },
       [&](int, double*) {},
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
 
 // Chebyshev step j >= 2; step 2 stages b and forms
 // y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                         const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
   double* ring = msm;
   double* XA = ring + m3_ring_doubles<P>();
   double* XB = XA + (TW3 + 2 * P) * 32;
-  unsigned long long* bars = m3_bars(a, XB + (TW3 + 2 * P) * 32);
+  unsigned long long* bars = TMA ? m3_bars(a, XB + (TW3 + 2 * P) * 32) : nullptr;  // (compile-time path)
   const int nxb = g.NX >> 5;
   const int j = a.step;
   const double* __restrict__ src = (j == 2) ? c.B : c.Y[(j - 1) & 1];
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
   constexpr int NR = TW3 + 2 * P;
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
-        if (bars) stage_box_tma(&a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(src, g, it.x0, it.y0, zz, P, slot);
       },
       [&](int zz, double* slot) {
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
 // Multicolour Gauss-Seidel colour `a.step` (>= 1) in place on Y[1]
 // (oracle mc_gauss_seidel): y = y + invD (b - A y) at the nodes
 // of the colour, the last colour finalises every node.
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                       const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -447,14 +447,14 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCt
   double* ring = msm;
   double* XA = ring + m3_ring_doubles<P>();
   double* XB = XA + (TW3 + 2 * P) * 32;
-  unsigned long long* bars = m3_bars(a, XB + (TW3 + 2 * P) * 32);
+  unsigned long long* bars = TMA ? m3_bars(a, XB + (TW3 + 2 * P) * 32) : nullptr;  // (compile-time path)
   const int nxb = g.NX >> 5;
   double* __restrict__ Yv = c.Y[1];
   const int cx = a.step % (P + 1), cy = (a.step / (P + 1)) % (P + 1), cz = a.step / ((P + 1) * (P + 1));
   const bool colxy = x % (P + 1) == cx && y % (P + 1) == cy;
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
-        if (bars) stage_box_tma(&a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(Yv, g, it.x0, it.y0, zz, P, slot);
       },
       [&](int, double*) {},
@@ -665,7 +665,9 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const
 }
 
 // ------------------------------------------------------------------ host --
-static int m3_smem_A(int p) { return (int)(((size_t)NB3 * (TW3 + 2 * p) * RS3 + 2 * (TW3 + 2 * p) * 32) * 8 + NB3 * 8); }
+static int m3_smem_A(int p, bool tma = false) {
+  return (int)(((size_t)NB3 * (TW3 + 2 * p) * RS3 + 2 * (TW3 + 2 * p) * 32) * 8 + (tma ? NB3 * 8 : 0));
+}
 static int m3_smem_R(int p) {
   const int FR = 2 * TW3 + 2 * (2 * p - 1);
   return (RNB3 * FR * RRS3 + FR * 32) * 8;
@@ -674,10 +676,14 @@ int march3_rows() { return TW3; }
 
 void march3_set_attributes() {
 #define F(P)                                                                                             \
-  cudaFuncSetAttribute(k_m3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));     \
-  cudaFuncSetAttribute(k_m3_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));        \
-  cudaFuncSetAttribute(k_m3_cheb<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));         \
-  cudaFuncSetAttribute(k_m3_gs<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));           \
+  cudaFuncSetAttribute(k_m3_residual<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));      \
+  cudaFuncSetAttribute(k_m3_residual<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P, true)); \
+  cudaFuncSetAttribute(k_m3_cfas1<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));         \
+  cudaFuncSetAttribute(k_m3_cfas1<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P, true));    \
+  cudaFuncSetAttribute(k_m3_cheb<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));          \
+  cudaFuncSetAttribute(k_m3_cheb<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P, true));     \
+  cudaFuncSetAttribute(k_m3_gs<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));            \
+  cudaFuncSetAttribute(k_m3_gs<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P, true));       \
   cudaFuncSetAttribute(k_m3_restrict<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_R(P));
   F(1) F(2) F(3)
 #undef F
@@ -702,18 +708,21 @@ static void m3_launch(K kernel, int nctas, int smem, cudaStream_t st, const DevC
 void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf) {
   const DevCtx* c = (const DevCtx*)devctx;
   const int n = a.nitems;
+  const bool t = a.tma != 0;
+#define TM(K, P) (t ? (void (*)(const DevCtx*, MArgs, Coefs))K<P, true> : (void (*)(const DevCtx*, MArgs, Coefs))K<P, false>)
 #define F(P)                                                                                  \
   switch (a.type) {                                                                           \
     case OP_DECODE:                                                                           \
     case OP_PROLONG: m3_launch(k_m3_prolong<P>, n, 0, st, c, a, cf); break;                   \
-    case OP_RESIDUAL: m3_launch(k_m3_residual<P>, n, m3_smem_A(P), st, c, a, cf); break;      \
+    case OP_RESIDUAL: m3_launch(TM(k_m3_residual, P), n, m3_smem_A(P, t), st, c, a, cf); break; \
     case OP_RESTRICT: m3_launch(k_m3_restrict<P>, n, m3_smem_R(P), st, c, a, cf); break;      \
-    case OP_CFAS1: m3_launch(k_m3_cfas1<P>, n, m3_smem_A(P), st, c, a, cf); break;            \
-    case OP_GS: m3_launch(k_m3_gs<P>, n, m3_smem_A(P), st, c, a, cf); break;                  \
-    default: m3_launch(k_m3_cheb<P>, n, m3_smem_A(P), st, c, a, cf); break;                   \
+    case OP_CFAS1: m3_launch(TM(k_m3_cfas1, P), n, m3_smem_A(P, t), st, c, a, cf); break;     \
+    case OP_GS: m3_launch(TM(k_m3_gs, P), n, m3_smem_A(P, t), st, c, a, cf); break;           \
+    default: m3_launch(TM(k_m3_cheb, P), n, m3_smem_A(P, t), st, c, a, cf); break;            \
   }
   if (p == 1) { F(1) } else if (p == 2) { F(2) } else { F(3) }
 #undef F
+#undef TM
 }
 
 }  // namespace fmg
