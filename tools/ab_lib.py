@@ -33,10 +33,10 @@ for rnd in range(3):
                 L.fmg_solve_async(h)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
-            for _ in range(20):
+            for _ in range(int(os.environ.get("AB_N", "20"))):
                 L.fmg_solve_async(h)
             b.record(st)
         st.synchronize()
-        res[path].append(a.elapsed_time(b) / 20)
+        res[path].append(a.elapsed_time(b) / int(os.environ.get("AB_N", "20")))
 for p, v in res.items():
     print(f"{p}: " + " ".join(f"{x:.4f}" for x in v) + f"  min {min(v):.4f} ms")
