@@ -182,7 +182,8 @@ class Solver:
         self._h = h
 
     def close(self):
-        if getattr(self, "_h", None):
+        # (at interpreter shutdown the module globals may already be cleared)
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.fmg_destroy(self._h)
             self._h = None
 

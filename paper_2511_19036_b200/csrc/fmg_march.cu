@@ -156,6 +156,79 @@ __device__ __forceinline__ double invd2(const Coefs& cf, int P, int n, int x, in
   return (unk1(x, n) && unk1(y, n)) ? cf.invd[(y % P) * P + x % P] : 0.0;
 }
 
+// Sum-factorised prolongation march (cFas1): P_l c at fine (X, y) is
+//   accy = sum_t2 fma(Pw[ry][t2], accx(X, by + t2), accy),
+//   accx(X, cy) = sum_t1 fma(Pw[rx][t1], c(bx + t1, cy), accx)
+// (prolong_at's order exactly, so the values are bit-identical).  accx of a
+// coarse row is computed once, for every fine column the warp needs, into a
+// ring of P + 1 rows in shared memory; each fine row is then a (P + 1)-term
+// y pass.  The coarse row segment is loaded once (one coalesced load per
+// lane) and read through shuffles.
+template <int P>
+struct ProlongRing {
+  static constexpr int NCR = 4;          // ring slots (>= P + 1 coarse rows by .. by + P live at once)
+  static constexpr int XW = 32 + 2 * P;  // staged fine columns x0 - P .. x0 + 32 + P - 1
+  static constexpr int SLOT = XW + 32;   // w x-pass (XW) then u x-pass (own columns)
+  double* ring;                          // NCR * SLOT doubles (per warp)
+  int next;                              // next coarse row to x-pass
+  // accx of coarse row cy at fine column X (0 when X is not an unknown column)
+  __device__ __forceinline__ static double xpass_at(const Coefs& cf, double cv, int cb0, int X, int nf) {
+    const bool unk = unk1(X, nf);
+    const int Xc = unk ? X : 1;
+    const int rx = Xc % (2 * P), bx = P * (Xc / (2 * P));
+    double acc = 0.0;
+#pragma unroll
+    for (int t1 = 0; t1 <= P; ++t1) {
+      const double v = __shfl_sync(FULL, cv, (bx + t1 - cb0) & 31);
+      acc = fma(cf.Pw[rx][t1], v, acc);
+    }
+    return unk ? acc : 0.0;
+  }
+  // x passes of coarse rows next .. need of W (staged columns), then of U
+  // (own columns): each pass issues all its rows' loads before the first
+  // shuffle (one exposed latency per pass, not per row)
+  __device__ __forceinline__ void advance(const Coefs& cf, const double* __restrict__ W, const double* __restrict__ U,
+                                          const Geom& gc, int nf, int x0, int need, int lane) {
+    const int cb0 = P * ((x0 >= P ? x0 - P : 0) / (2 * P));  // first coarse column any unknown column needs
+    const int cx = cb0 + lane;
+    const int Xh = lane < P ? x0 - P + lane : x0 + 32 + (lane - P);
+    const int jh = lane < P ? lane : 32 + lane;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {  // w rows (staged columns), then u rows (own columns)
+      const double* __restrict__ src = pass == 0 ? W : U;
+      double cv[P + 1];
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        const int cy = next + k;
+        const bool ok = cy <= need && cy < gc.NY && cx < gc.NX;
+        cv[k] = ok ? src[(long long)cy * gc.NX + cx] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k <= P; ++k) {
+        const int cy = next + k;
+        if (cy > need) break;  // (warp-uniform)
+        double* r = ring + (cy & (NCR - 1)) * SLOT;
+        if (pass == 0) {
+          r[P + lane] = xpass_at(cf, cv[k], cb0, x0 + lane, nf);  // own column
+          const double hv = xpass_at(cf, cv[k], cb0, Xh, nf);     // halo columns (lanes < 2P)
+          if (lane < 2 * P) r[jh] = hv;
+        } else {
+          r[XW + lane] = xpass_at(cf, cv[k], cb0, x0 + lane, nf);
+        }
+      }
+    }
+    next = need + 1;
+  }
+  // y pass at fine row y for slot index j (0 .. XW-1), or the own column of U
+  __device__ __forceinline__ double ypass(const Coefs& cf, int y, int j, int off) const {
+    const int ry = y % (2 * P), by = P * (y / (2 * P));
+    double acc = 0.0;
+#pragma unroll
+    for (int t2 = 0; t2 <= P; ++t2) acc = fma(cf.Pw[ry][t2], ring[((by + t2) & (NCR - 1)) * SLOT + off + j], acc);
+    return acc;
+  }
+};
+
 // The A march: input rows y' = ys-P .. ye+P-1 are staged
 // (stage(y', slot), async or not), optionally transformed in place
 // (xform(y', slot)), x-passed (a = Mx u, b = Kx u) into the register ring;
@@ -472,21 +545,36 @@ __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, co
   const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
   double* ring = msm + threadIdx.y * (MNB * MSLOT);
   const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);  // halo column of lanes < 2P
+  ProlongRing<P> pr;
+  pr.ring = msm + MW * MNB * MSLOT + threadIdx.y * (ProlongRing<P>::NCR * ProlongRing<P>::SLOT);
+  pr.next = P * ((it.ys - P > 0 ? it.ys - P : 0) / (2 * P));
+  const bool unkx = unk1(x, g.n), unkh = unk1(xh, g.n);
   march_A<P>(
       cf, it.ys, it.ye, x, ring,
       [&](int yy, double* slot) {
-        // z row yy on the block columns and the x halo (0 outside the level)
-        const double zm = (yy >= 0 && yy < g.NY) ? prolong_at<P>(cf, lp.W, gp, g.n, x, yy) : 0.0;
-        slot[P + lane] = zm;
-        if (lane < 2 * P) {
-          const double zh = (yy >= 0 && yy < g.NY && xh >= 0 && xh < g.NX) ? prolong_at<P>(cf, lp.W, gp, g.n, xh, yy)
-                                                                            : 0.0;
-          slot[lane < P ? lane : 32 + lane] = zh;
+        // z row yy on the block columns and the x halo (0 outside the level),
+        // P u_{l-1} at the own columns of the output rows
+        const bool inrow = yy >= 0 && yy < g.NY;
+        double zm = 0.0, zh = 0.0, pu = 0.0;
+        if (inrow) {  // (warp-uniform)
+          const int need = P * (yy / (2 * P)) + P;  // coarse rows by .. by + P
+          if (pr.next <= need) {
+            __syncwarp();  // the previous row's y passes are done with the slots about to be refilled
+            pr.advance(cf, lp.W, lp.U, gp, g.n, it.x0, need, lane);
+            __syncwarp();
+          }
+          const bool unky = unk1(yy, g.n);
+          zm = (unkx && unky) ? pr.ypass(cf, yy, P + lane, 0) : 0.0;
+          const int jh = lane < P ? lane : 32 + lane;
+          zh = (unkh && unky && lane < 2 * P) ? pr.ypass(cf, yy, jh, 0) : 0.0;
+          if (yy >= it.ys && yy < it.ye) pu = (unkx && unky) ? pr.ypass(cf, yy, lane, ProlongRing<P>::XW) : 0.0;
         }
+        slot[P + lane] = zm;
+        if (lane < 2 * P) slot[lane < P ? lane : 32 + lane] = zh;
         if (yy >= it.ys && yy < it.ye) {
           const long long idx = (long long)yy * g.NX + x;
           if (a.l < a.L) c.Z[idx] = zm;
-          c.PU[idx] = prolong_at<P>(cf, lp.U, gp, g.n, x, yy);
+          c.PU[idx] = pu;
         }
       },
       [&](int, double*) {},
@@ -657,6 +745,8 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* 
 
 // ------------------------------------------------------------------ host --
 int march_smem(bool tma) { return MW * MNB * MSLOT * 8 + (tma ? MW * MNB * 8 : 0); }
+// cFas1: the rings plus the per-warp prolongation ring (ProlongRing)
+static int march_smem_cfas1(int p) { return MW * MNB * MSLOT * 8 + MW * 4 * (64 + 2 * p) * 8; }
 int march_warps() { return MW; }
 
 #define M_DISPATCH(p, F)   \
@@ -672,7 +762,7 @@ void march_set_attributes() {
   cudaFuncSetAttribute(k_m_residual<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));   \
   cudaFuncSetAttribute(k_m_restrict<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false)); \
   cudaFuncSetAttribute(k_m_restrict<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));   \
-  cudaFuncSetAttribute(k_m_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));          \
+  cudaFuncSetAttribute(k_m_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem_cfas1(P));        \
   cudaFuncSetAttribute(k_m_cheb<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));     \
   cudaFuncSetAttribute(k_m_cheb<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));       \
   cudaFuncSetAttribute(k_m_gs<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));       \
@@ -707,7 +797,7 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
     case OP_DECODE: m_launch(k_m_decode<P>, a.nitems, 0, st, c, a, cf); break;                   \
     case OP_RESIDUAL: m_launch(TM(k_m_residual, P), a.nitems, sm, st, c, a, cf); break;          \
     case OP_RESTRICT: m_launch(TM(k_m_restrict, P), a.nitems, sm, st, c, a, cf); break;          \
-    case OP_CFAS1: m_launch(k_m_cfas1<P>, a.nitems, march_smem(false), st, c, a, cf); break;     \
+    case OP_CFAS1: m_launch(k_m_cfas1<P>, a.nitems, march_smem_cfas1(P), st, c, a, cf); break;   \
     case OP_GS: m_launch(TM(k_m_gs, P), a.nitems, sm, st, c, a, cf); break;                      \
     default: m_launch(TM(k_m_cheb, P), a.nitems, sm, st, c, a, cf); break;                       \
   }
