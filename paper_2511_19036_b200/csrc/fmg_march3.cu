@@ -372,6 +372,20 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
   const double* __restrict__ src = (j == 2) ? c.B : c.Y[(j - 1) & 1];
   const double al = cf.cal[j - 1], be = cf.cbe[j - 1];
   constexpr int NR = TW3 + 2 * P;
+  // invd3's factors hoisted (same values: invd[type] 2^(l+1), 0 at non-unknowns):
+  // the thread's own / halo column and its staged rows are fixed for the march
+  const double isc = pow2(a.l + 1);
+  const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);
+  const bool ux = unk1(x, g.n), uxh = unk1(xh, g.n), uy = unk1(y, g.n);
+  const int tx = ux ? x % P : 0, txh = uxh ? xh % P : 0, ty = uy ? y % P : 0;
+  bool uyr[2];
+  int tyr[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int yy = it.y0 - P + w + k * TW3;
+    uyr[k] = w + k * TW3 < NR && unk1(yy, g.n);
+    tyr[k] = uyr[k] ? yy % P : 0;
+  }
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
         if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
@@ -379,15 +393,21 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
       },
       [&](int zz, double* slot) {
         if (j != 2) return;
-        // y_1 = inv_theta (invD b) on the entries this thread staged
-        for (int r = w; r < NR; r += TW3) {
-          const int yy = it.y0 - P + r;
+        // y_1 = inv_theta (invD b) on the entries of this thread's staged rows
+        const bool uz = unk1(zz, g.n);
+        const int tz = uz ? zz % P : 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int r = w + k * TW3;
+          if (r >= NR) break;
           double* row = slot + r * RS3;
-          row[P + lane] = cf.inv_theta * (invd3(cf, P, g.n, a.l, x, yy, zz) * row[P + lane]);
+          const int tb = (tz * P + tyr[k]) * P;
+          const double f = (ux && uyr[k] && uz) ? cf.invd[tb + tx] * isc : 0.0;
+          row[P + lane] = cf.inv_theta * (f * row[P + lane]);
           if (lane < 2 * P) {
-            const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);
+            const double fh = (uxh && uyr[k] && uz) ? cf.invd[tb + txh] * isc : 0.0;
             double& v = row[lane < P ? lane : 32 + lane];
-            v = cf.inv_theta * (invd3(cf, P, g.n, a.l, xh, yy, zz) * v);
+            v = cf.inv_theta * (fh * v);
           }
         }
         __syncthreads();
@@ -416,7 +436,9 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
         const double qq = q.b - ay;
         const double yprev = slot[(w + P) * RS3 + P + lane];
         const double dprev = (j == 2) ? yprev : q.dv;
-        const double d = fma(al, dprev, be * (invd3(cf, P, g.n, a.l, x, y, z) * qq));
+        const bool uz = unk1(z, g.n);
+        const double f = (ux && uy && uz) ? cf.invd[((uz ? z % P : 0) * P + ty) * P + tx] * isc : 0.0;
+        const double d = fma(al, dprev, be * (f * qq));
         const double yv = yprev + d;
         if (a.last) {
           m3_finalize(c, a, lv, idx, blk, yv, q.z, q.pu, q.w0, q.w1, q.e, lane);
