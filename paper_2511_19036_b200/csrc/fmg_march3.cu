@@ -560,8 +560,16 @@ __global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restric
     const bool okz = okxy && unk1(z, g.n);
     const int rz = okz ? z % (2 * P) : 0, bz = okz ? P * (z / (2 * P)) : 0;
     if (okz && bz != cz0) {
+      // consecutive windows bz .. bz + P share plane bz (= old bz + P): shift
+      // it down and compute only the P new planes
+      const int t0 = (bz == cz0 + P) ? 1 : 0;
+      if (t0) {
+        uv[0] = uv[P];
+        if (a.type != OP_DECODE) wv[0] = wv[P];
+      }
 #pragma unroll
       for (int t = 0; t <= P; ++t) {
+        if (t < t0) continue;
         const int cz = bz + t;
         if (a.type == OP_DECODE) {
           uv[t] = pxy<P>(cf, lp.U, gp, rx, bx, ry, by, cz);
