@@ -213,13 +213,21 @@ __device__ __forceinline__ void warp_pack(unsigned long long field, int w, uint3
 __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, int8_t* eptr, int lane,
                                               int* status) {
   unsigned long long bits = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
-  bool bad = bits >= 0x7ff0000000000000ULL;
-  unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
-  unsigned mh = __reduce_max_sync(FULL, hi);
-  unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
-  bool err = __any_sync(FULL, bad);
-  int q = w - 1, E = -128;
-  if (!err && (mh | ml) != 0u) {
+  const unsigned hi = (unsigned)(bits >> 32);
+  const unsigned mh = __reduce_max_sync(FULL, hi);
+  // The exponent needs only the maximum's high word; its bump test
+  //   RNE(mx 2^(q-E0)) == 2^q  <=>  frac(mx) >= 2^52 - 2^(52-q)   (mx normal; never for q = 53)
+  // is monotone in the bits, so it holds for the maximum iff it holds for some
+  // lane carrying the maximal high word: one redux and three independent
+  // ballots instead of two dependent reduxes.
+  const int q = w - 1;
+  const unsigned long long thr = q <= 52 ? (1ULL << 52) - (1ULL << (52 - q)) : ~0ULL;
+  const unsigned vbad = __ballot_sync(FULL, bits >= 0x7ff0000000000000ULL);
+  const unsigned vnz = __ballot_sync(FULL, bits != 0ULL);
+  const unsigned vbump = __ballot_sync(FULL, hi == mh && (bits & 0x000fffffffffffffULL) >= thr);
+  bool err = vbad != 0u;
+  int E = -128;
+  if (!err && vnz != 0u) {
     int ebits = (int)((mh >> 20) & 0x7FFu);
     int E0 = ebits == 0 ? -1100 : ebits - 1022;  // ilogb(mx) + 1; subnormal max -> saturates below
     if (E0 > 127) {
@@ -227,9 +235,7 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
     } else if (E0 < -127) {
       E = -127;
     } else {
-      // RNE(mx 2^(q-E0)) == 2^q  <=>  frac(mx) >= 2^52 - 2^(52-q) (mx normal; never for q = 53)
-      const unsigned long long frac = (((unsigned long long)(mh & 0xFFFFFu)) << 32) | ml;
-      E = E0 + (q <= 52 && frac >= (1ULL << 52) - (1ULL << (52 - q)) ? 1 : 0);
+      E = E0 + (vbump != 0u ? 1 : 0);
       if (E > 127) err = true;
     }
   }
