@@ -84,14 +84,15 @@ class Schedule(C.Structure):
 
     _fields_ = [("b_u", C.c_int), ("k_u", C.c_int), ("b_r", C.c_int), ("k_r", C.c_int),
                 ("n_ir", C.c_int), ("cheb_degree", C.c_int),
-                ("lambda_hi", C.c_double), ("alpha", C.c_double), ("smoother", C.c_int)]
+                ("lambda_hi", C.c_double), ("alpha", C.c_double), ("smoother", C.c_int),
+                ("nu", C.c_int)]
 
 
 SMOOTHERS = {"chebyshev": 0, "mcgs": 1, "lexgs": 2}
 
 
 def schedule(d: int, p: int, b_u=None, b_r=None, n_ir=None, k_u=None, k_r=1,
-             cheb_degree=None, lambda_hi=None, alpha=None, smoother="chebyshev") -> Schedule:
+             cheb_degree=None, lambda_hi=None, alpha=None, smoother="chebyshev", nu=1) -> Schedule:
     """Default schedule of DESIGN.md §5 (same numbers the product path uses)."""
     from fmg_inputs import default_schedule
     s = default_schedule(d, p)
@@ -101,7 +102,8 @@ def schedule(d: int, p: int, b_u=None, b_r=None, n_ir=None, k_u=None, k_r=1,
         if v is not None:
             s[k] = v
     return Schedule(s["b_u"], s["k_u"], s["b_r"], s["k_r"], s["n_ir"], s["cheb_degree"],
-                    s["lambda_hi"], s["alpha"], SMOOTHERS[smoother] if isinstance(smoother, str) else smoother)
+                    s["lambda_hi"], s["alpha"], SMOOTHERS[smoother] if isinstance(smoother, str) else smoother,
+                    nu)
 
 
 @dataclass

@@ -39,6 +39,10 @@ typedef struct {
   int smoother;      /* 0 Chebyshev-Jacobi (R4), 1 multicolor Gauss-Seidel with
                         (p+1)^d colours, 2 lexicographic Gauss-Seidel (PAPER.md:689-690,
                         1624; oracle only) -- SURVEY §8f N1 */
+  int nu;            /* V(0,1) cycles of cFas per IR iteration (Alg 3.1, PAPER.md:633-661;
+                        SURVEY §8f N2); cycles after the first start from the previous
+                        correction: fine-to-coarse s sweep and nonzero-guess terms
+                        (reading R23).  0 or 1: one cycle from zero. */
 } orc_schedule;
 
 /* ---- grid geometry of level l ---- */

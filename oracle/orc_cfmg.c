@@ -300,23 +300,67 @@ int orc_smooth(orc_ctx* c, int l, const double* b, double* y) {
   return ORC_OK;
 }
 
-/* Alg 3.1 cFas (nu = 1: y = 0, s = 0) followed by the correction PAPER.md:798. */
-int orc_cfas_correct(orc_ctx* c, int L) {
+/* The smoother of the schedule on A_l y = b from y = 0 (M_l b). */
+static void smooth0(const orc_ctx* c, int l, const double* b, double* y) {
+  if (c->s.smoother == 1) mc_gauss_seidel(c, l, b, y);
+  else if (c->s.smoother == 2) lex_gauss_seidel(c, l, b, y);
+  else chebyshev(c, l, b, y);
+}
+
+/* One compact V(0,1) cycle of Alg 3.1.  guess = 0: from
+ * ý = 0, so s = 0 and the fine-to-coarse sweep is left out;
+ * guess = 1 (cycles 2..nu): ý_{0..L} of the previous cycle is
+ * the initial guess:
+ *   fine-to-coarse  s_L = 0, s_l = R_{l+1} A_{l+1} ý_{l+1} + R_{l+1} s_{l+1}   (L-1 .. 0)
+ *   coarse          ý_0 = fix(ý_0 + M_0 (r_0 - s_0 - A_0 ý_0)), M_0 = A_0^{-1}
+ *   coarse-to-fine  z_l = P_l (ý_{l-1} + z_{l-1}),
+ *                   ý_l = fix(ý_l + M_l (r_l - s_l - A_l z_l - A_l ý_l))
+ * Reading R23: the operands are combined left to right as written, the
+ * restriction R (A ý + s) is applied to the sum (one R per level, the
+ * recursion of PAPER.md:603), and M_l is the smoother from zero on the
+ * bracket, added to the decoded ý_l. */
+static int cfas_cycle(orc_ctx* c, int L, int guess) {
   int d = c->d, p = c->p, rc;
+  double** sv = NULL;
+  if (L < 0 || L > c->Lmax) return ORC_EINVAL;
+  if (guess) {
+    sv = calloc((size_t)L + 1, sizeof(double*));
+    for (int l = 0; l <= L; ++l) sv[l] = calloc((size_t)c->g[l].size, sizeof(double));  /* s_L = 0 */
+    for (int l = L - 1; l >= 0; --l) {
+      const orc_level* gf = &c->g[l + 1];
+      double* yv = malloc(sizeof(double) * gf->size);
+      double* q = malloc(sizeof(double) * gf->size);
+      sec_decode(&c->y[l + 1], gf, yv);
+      orc_apply_A(d, p, l + 1, yv, q);
+      for (int64_t i = 0; i < gf->size; ++i) q[i] = q[i] + sv[l + 1][i];  /* A ý + s */
+      orc_restrict(d, p, l + 1, q, sv[l]);
+      free(yv); free(q);
+    }
+  }
   /* coarse level PAPER.md:640: y_0 = fix(M_0 r_0), M_0 = A_0^{-1} (reading R5) */
   {
     const orc_level* g = &c->g[0];
     double* r0 = malloc(sizeof(double) * g->size);
     double* y0 = malloc(sizeof(double) * g->size);
     sec_decode(&c->r[0], g, r0);
-    coarse_solve(c, r0, y0);
+    if (guess) {
+      double* yo = malloc(sizeof(double) * g->size);
+      double* ay = malloc(sizeof(double) * g->size);
+      sec_decode(&c->y[0], g, yo);
+      orc_apply_A(d, p, 0, yo, ay);
+      for (int64_t i = 0; i < g->size; ++i) r0[i] = (r0[i] - sv[0][i]) - ay[i];
+      coarse_solve(c, r0, y0);
+      for (int64_t i = 0; i < g->size; ++i) y0[i] = yo[i] + y0[i];
+      free(yo); free(ay);
+    } else {
+      coarse_solve(c, r0, y0);
+    }
     rc = sec_encode(&c->y[0], g, y0, wr(c, 0, L));
     free(r0); free(y0);
-    if (rc) return rc;
-    sec_decode(&c->y[0], g, c->wt[0]);   /* w_0 = z_0 + ý_0, z_0 = 0 */
+    if (!rc) sec_decode(&c->y[0], g, c->wt[0]);   /* w_0 = z_0 + ý_0, z_0 = 0 */
   }
   /* coarse-to-fine sweep PAPER.md:641-643 */
-  for (int l = 1; l <= L; ++l) {
+  for (int l = 1; l <= L && !rc; ++l) {
     const orc_level* g = &c->g[l];
     int64_t N = g->size;
     double* z = malloc(sizeof(double) * N);
@@ -326,16 +370,40 @@ int orc_cfas_correct(orc_ctx* c, int L) {
     orc_prolong(d, p, l, c->wt[l - 1], z);          /* z_l = P_l (ý_{l-1} + z_{l-1}) */
     orc_apply_A(d, p, l, z, az);
     sec_decode(&c->r[l], g, rb);
-    for (int64_t i = 0; i < N; ++i) rb[i] = rb[i] - az[i];  /* b = r_l - A_l z_l */
-    if (c->s.smoother == 1) mc_gauss_seidel(c, l, rb, yv);      /* smooth from ý_l = 0 */
-    else if (c->s.smoother == 2) lex_gauss_seidel(c, l, rb, yv);
-    else chebyshev(c, l, rb, yv);
+    if (guess) {
+      double* yo = malloc(sizeof(double) * N);
+      double* ay = malloc(sizeof(double) * N);
+      sec_decode(&c->y[l], g, yo);
+      orc_apply_A(d, p, l, yo, ay);
+      for (int64_t i = 0; i < N; ++i) rb[i] = ((rb[i] - sv[l][i]) - az[i]) - ay[i];
+      smooth0(c, l, rb, yv);                                   /* M_l (...) from zero */
+      for (int64_t i = 0; i < N; ++i) yv[i] = yo[i] + yv[i];  /* ý_l + M_l (...) */
+      free(yo); free(ay);
+    } else {
+      for (int64_t i = 0; i < N; ++i) rb[i] = rb[i] - az[i];  /* b = r_l - A_l z_l */
+      smooth0(c, l, rb, yv);                                   /* smooth from ý_l = 0 */
+    }
     rc = sec_encode(&c->y[l], g, yv, wr(c, l, L));   /* fix: store at w_r(l,L) */
     if (!rc) {
       sec_decode(&c->y[l], g, yv);
       for (int64_t i = 0; i < N; ++i) c->wt[l][i] = z[i] + yv[i];
     }
     free(z); free(az); free(rb); free(yv);
+  }
+  if (sv) {
+    for (int l = 0; l <= L; ++l) free(sv[l]);
+    free(sv);
+  }
+  return rc;
+}
+
+/* Alg 3.1 cFas (nu cycles; the first from y = 0, s = 0) followed by the
+ * correction PAPER.md:798. */
+int orc_cfas_correct(orc_ctx* c, int L) {
+  int rc;
+  const int nu = c->s.nu > 1 ? c->s.nu : 1;
+  for (int cyc = 0; cyc < nu; ++cyc) {
+    rc = cfas_cycle(c, L, cyc > 0);
     if (rc) return rc;
   }
   /* correction PAPER.md:798: ú_l <- reg(ú_l + ý_l) at w_u(l, L) */

@@ -748,7 +748,8 @@ int fmg_set_allocator(fmg_alloc_fn alloc, fmg_free_fn free_fn, void* user) {
 static int check_args(int dim, int p, int levels, const fmg_schedule* s) {
   if ((dim != 2 && dim != 3) || p < 1 || p > 3 || levels < 1 || levels > kMaxLev) return FMG_EINVAL;
   if (s->b_u < 2 || s->b_r < 2 || s->k_u < 0 || s->k_r < 0 || s->n_ir < 1 || s->cheb_degree < 1 ||
-      s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1) || s->smoother < 0 || s->smoother > 1)
+      s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1) || s->smoother < 0 || s->smoother > 1 ||
+      s->nu < 0 || s->nu > 1)  // (nu > 1: oracle only this round)
     return FMG_EINVAL;
   const int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
