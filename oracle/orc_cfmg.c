@@ -315,10 +315,12 @@ static void smooth0(const orc_ctx* c, int l, const double* b, double* y) {
  *   coarse          ý_0 = fix(ý_0 + M_0 (r_0 - s_0 - A_0 ý_0)), M_0 = A_0^{-1}
  *   coarse-to-fine  z_l = P_l (ý_{l-1} + z_{l-1}),
  *                   ý_l = fix(ý_l + M_l (r_l - s_l - A_l z_l - A_l ý_l))
- * Reading R23: the operands are combined left to right as written, the
+ * Reading R23: the level bracket is ((r_l - s_l) - A_l (z_l + ý_l)) -- the
+ * paper's A_l z_l + A_l ý_l as one operator application on the sum -- the
  * restriction R (A ý + s) is applied to the sum (one R per level, the
  * recursion of PAPER.md:603), and M_l is the smoother from zero on the
- * bracket, added to the decoded ý_l. */
+ * bracket, added to the decoded ý_l.  The coarse level keeps
+ * (r_0 - s_0) - A_0 ý_0 (z_0 = 0). */
 static int cfas_cycle(orc_ctx* c, int L, int guess) {
   int d = c->d, p = c->p, rc;
   double** sv = NULL;
@@ -371,14 +373,16 @@ static int cfas_cycle(orc_ctx* c, int L, int guess) {
     orc_apply_A(d, p, l, z, az);
     sec_decode(&c->r[l], g, rb);
     if (guess) {
+      /* A_l z_l + A_l ý_l = A_l (z_l + ý_l): one operator application (R23) */
       double* yo = malloc(sizeof(double) * N);
-      double* ay = malloc(sizeof(double) * N);
+      double* zy = malloc(sizeof(double) * N);
       sec_decode(&c->y[l], g, yo);
-      orc_apply_A(d, p, l, yo, ay);
-      for (int64_t i = 0; i < N; ++i) rb[i] = ((rb[i] - sv[l][i]) - az[i]) - ay[i];
+      for (int64_t i = 0; i < N; ++i) zy[i] = z[i] + yo[i];
+      orc_apply_A(d, p, l, zy, az);
+      for (int64_t i = 0; i < N; ++i) rb[i] = (rb[i] - sv[l][i]) - az[i];
       smooth0(c, l, rb, yv);                                   /* M_l (...) from zero */
       for (int64_t i = 0; i < N; ++i) yv[i] = yo[i] + yv[i];  /* ý_l + M_l (...) */
-      free(yo); free(ay);
+      free(yo); free(zy);
     } else {
       for (int64_t i = 0; i < N; ++i) rb[i] = rb[i] - az[i];  /* b = r_l - A_l z_l */
       smooth0(c, l, rb, yv);                                   /* smooth from ý_l = 0 */
