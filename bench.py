@@ -143,6 +143,7 @@ def run_ours(args, rank, world, local_rank):
     cfg = CONFIGS[args.config]
     sched = default_schedule(cfg["dim"], cfg["p"])
     sched["smoother"] = {"chebyshev": 0, "mcgs": 1}[args.smoother]
+    sched["nu"] = args.nu
     P.use_torch_allocator(True)
     stream = torch.cuda.current_stream()
     dist_slabs = world > 1 and cfg["dim"] == 3  # 3D: one problem in z slabs over the ranks (NCCL)
@@ -258,11 +259,11 @@ def run_ours(args, rank, world, local_rank):
         "clocks": ck,
     }
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args.config, args.smoother)
+        out["cpu_baseline"] = cpu_baseline(args.config, args.smoother, args.nu)
     print(json.dumps(out))
 
 
-def cpu_baseline(config, smoother="chebyshev"):
+def cpu_baseline(config, smoother="chebyshev", nu=1):
     import oracle as O
     cfg = CONFIGS[config]
     d, p, lev = cfg["dim"], cfg["p"], cfg["levels"]
@@ -271,7 +272,7 @@ def cpu_baseline(config, smoother="chebyshev"):
     sample_lev = lev
     while sample_lev > 2 and (p << sample_lev) ** d > 5_000_000:
         sample_lev -= 1
-    s = O.schedule(d, p, smoother=smoother)
+    s = O.schedule(d, p, smoother=smoother, nu=nu)
     c = O.CFMG(d, p, sample_lev, s)
     t0 = time.perf_counter()
     c.solve()
@@ -291,7 +292,7 @@ def run_reference(args, rank, world):
     sample_lev = lev
     while sample_lev > 2 and (p << sample_lev) ** d > 5_000_000:
         sample_lev -= 1
-    s = O.schedule(d, p, smoother=args.smoother)
+    s = O.schedule(d, p, smoother=args.smoother, nu=args.nu)
     c = O.CFMG(d, p, sample_lev, s)
     for _ in range(args.warmup):
         c.solve()
@@ -328,6 +329,8 @@ def main():
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the roofline kernel (profiles/)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nu", type=int, default=1,
+                    help="compact V(0,1) cycles per IR iteration (SURVEY 8f N2; GPU: 2D, Chebyshev)")
     ap.add_argument("--smoother", default="chebyshev", choices=["chebyshev", "mcgs"],
                     help="cFas smoother: Chebyshev-Jacobi (default) or multicolour Gauss-Seidel (SURVEY 8f N1)")
     args = ap.parse_args()

@@ -42,6 +42,7 @@ struct fmg_ctx {
   Geom g[kMaxLev];
   Coefs cf{};
   Sec u[kMaxLev]{}, r[kMaxLev]{};
+  Sec ysec[kMaxLev]{};            // nu > 1: the correction ý_l kept across cycles
   double* gtab[kMaxLev]{};
   int tiles[kMaxLev][3]{};
   double* Ainv = nullptr;
@@ -269,8 +270,80 @@ int ncolours(const fmg_ctx* c) {
 
 // One IR iteration at FMG level L: fmgResidual (Alg 3.2),
 // cFas V(0,1) (Alg 3.1, nu = 1), correction.  Levels <= lc run inside KC.
+// One IR iteration with nu > 1 compact V(0,1) cycles (Alg 3.1
+// PAPER.md:633-661, reading R23; oracle orc_cfas_correct).  2D, Chebyshev,
+// lc = 0: the grid kernels do every level >= 0 except the initial coarse solve.
+void build_iteration_nu(Builder& b, int L, int it) {
+  fmg_ctx* c = b.c;
+  const bool fine = L == c->Lmax;
+  const int row = L * c->s.n_ir + it;
+  const int nu = c->s.nu, k = c->s.cheb_degree;
+  // fmgResidual (Alg 3.2): t_L, r_L and the restriction sweep down to level 0
+  {
+    OpDesc o = mkop(OP_RESIDUAL, L, L);
+    o.wr = wr(c, L, L);
+    o.row = row;
+    o.poff = b.slot(row, L);
+    b.grid(o, fine ? 0 : -1);
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    OpDesc q = mkop(OP_RESTRICT, l, L);
+    q.wr = wr(c, l, L);
+    q.row = row;
+    q.poff = b.slot(row, l);
+    b.grid(q, (fine && l == L - 1) ? 3 : -1);
+  }
+  for (int cyc = 1; cyc <= nu; ++cyc) {
+    const int guess = cyc > 1, store = cyc < nu;
+    if (guess) {  // fine-to-coarse s sweep: q_{l+1} = A ý_{l+1} + s_{l+1} (into W), s_l = R q_{l+1} (into T)
+      for (int l = L - 1; l >= 0; --l) {
+        OpDesc q = mkop(OP_SQ, l + 1, L);
+        q.wr = wr(c, l + 1, L);
+        q.smode = (l + 1 == L);  // s_L = 0
+        b.grid(q);
+        OpDesc r = mkop(OP_RESTRICT, l, L);
+        r.smode = 1;
+        r.wr = wr(c, l, L);
+        b.grid(r);
+      }
+    }
+    {  // level 0: the bracket (cFas1 with z_0 = 0), then M_0 = A_0^{-1}, ý_0, w_0 (+ correction)
+      OpDesc q = mkop(OP_CFAS1, 0, L);
+      q.step = 1;
+      q.guess = guess;
+      q.wr = wr(c, 0, L);
+      b.grid(q);
+      OpDesc cc = mkop(OP_COARSE, 0, L);
+      cc.guess = guess;
+      cc.store = store;
+      cc.wr = wr(c, 0, L);
+      cc.wu_in = c->wu_cur[0];
+      cc.wu_out = wu(c, 0, L);
+      b.grid(cc);
+    }
+    for (int l = 1; l <= L; ++l) {
+      for (int step = 1; step <= k; ++step) {
+        OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
+        q.step = step;
+        q.last = step == k;
+        q.guess = guess;
+        q.store = store;
+        q.wr = wr(c, l, L);
+        q.wu_in = c->wu_cur[l];
+        q.wu_out = wu(c, l, L);
+        b.grid(q, (fine && l == L && !store) ? (step == k ? 5 : 1) : -1);
+      }
+    }
+  }
+  for (int l = 0; l <= L; ++l) c->wu_cur[l] = wu(c, l, L);
+}
+
 void build_iteration(Builder& b, int L, int it) {
   fmg_ctx* c = b.c;
+  if (c->s.nu > 1) {
+    build_iteration_nu(b, L, it);
+    return;
+  }
   const int lc = c->lc;
   const bool fine = L == c->Lmax;
   const int row = L * c->s.n_ir + it;
@@ -416,6 +489,9 @@ LevelDev level_dev(const fmg_ctx* c, int l) {
   v.U = c->Ul[l];
   v.T = c->Tl[l];
   v.W = c->Wl[l];
+  v.ymant = c->ysec[l].mant;
+  v.yexp = c->ysec[l].exps;
+  v.ystride = c->ysec[l].stride;
   return v;
 }
 
@@ -443,7 +519,11 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
   m.lv = level_dev(c, o.l);
   const int lo = o.type == OP_RESTRICT ? o.l + 1 : o.l - 1;
   if (lo >= 0 && lo <= c->Lmax) m.lo = level_dev(c, lo);
-  m.p = MPtrs{c->buf[0], c->buf[1], {c->buf[2], c->buf[3]}, c->buf[4], c->buf[5], c->pbase, c->status};
+  m.p = MPtrs{c->buf[0], c->buf[1], {c->buf[2], c->buf[3]}, c->buf[4], c->buf[5], c->buf[8], c->pbase, c->status};
+  m.guess = o.guess;
+  m.store = o.store;
+  m.smode = o.smode;
+  if (o.type == OP_RESTRICT && o.smode) m.lo.T = c->Wl[o.l + 1];  // s sweep: restrict q_{l+1} (in W)
   if (c->tma) {
     const int l = o.l;
     const CUtensorMap* U = c->tm_dev, *T = U + kMaxLev, *B = T + kMaxLev;  // device copies
@@ -455,8 +535,8 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
       case OP_CHEB: m.tm = B + (o.step == 2 ? 1 : 2 + ((o.step - 1) & 1)) * kMaxLev + l; break;
       default: break;
     }
-    m.tma = (o.type == OP_RESIDUAL || o.type == OP_GS || o.type == OP_CHEB || (o.type == OP_RESTRICT && c->dim == 2) ||
-             (o.type == OP_CFAS1 && c->dim == 3)) ? 1 : 0;
+    m.tma = (o.type == OP_RESIDUAL || o.type == OP_GS || o.type == OP_CHEB ||
+             (o.type == OP_RESTRICT && c->dim == 2 && !o.smode) || (o.type == OP_CFAS1 && c->dim == 3)) ? 1 : 0;
   }
   return m;
 }
@@ -471,7 +551,8 @@ void issue_item(fmg_ctx* c, const Item& it) {
     mark(c, it.timed_cls);
     if (c->march) {
       const MArgs m = march_args(c, it.op);
-      if (c->dim == 2) launch_march(c->p, c->cur, c->devctx, m, c->cf);
+      if (it.op.type == OP_COARSE) launch_coarse_nu(c->p, c->cur, c->devctx, m);
+      else if (c->dim == 2) launch_march(c->p, c->cur, c->devctx, m, c->cf);
       else launch_march3(c->p, c->cur, c->devctx, m, c->cf);
     } else {
       int tx = 1, ty = 1, tz = 1;
@@ -749,8 +830,10 @@ static int check_args(int dim, int p, int levels, const fmg_schedule* s) {
   if ((dim != 2 && dim != 3) || p < 1 || p > 3 || levels < 1 || levels > kMaxLev) return FMG_EINVAL;
   if (s->b_u < 2 || s->b_r < 2 || s->k_u < 0 || s->k_r < 0 || s->n_ir < 1 || s->cheb_degree < 1 ||
       s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1) || s->smoother < 0 || s->smoother > 1 ||
-      s->nu < 0 || s->nu > 1)  // (nu > 1: oracle only this round)
+      s->nu < 0 || s->nu > 8)
     return FMG_EINVAL;
+  // nu > 1 on the GPU: 2D, Chebyshev of degree >= 2
+  if (s->nu > 1 && (dim != 2 || s->smoother != 0 || s->cheb_degree < 2)) return FMG_EINVAL;
   const int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
   return FMG_OK;
@@ -773,7 +856,11 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   march_set_attributes();
   march3_set_attributes();
   c->march = !(getenv("FMG_MARCH") && atoi(getenv("FMG_MARCH")) == 0);
-  if (s->smoother == 1 && !c->march) {  // (the tile-box kernels implement Chebyshev only)
+  if ((s->smoother == 1 || s->nu > 1 || (s->nu > 1 && G > 1)) && !c->march) {  // (tile-box kernels: Chebyshev, nu = 1)
+    fmg_destroy(c);
+    return FMG_EINVAL;
+  }
+  if (s->nu > 1 && G > 1) {  // (z slabs are 3D; nu > 1 is 2D)
     fmg_destroy(c);
     return FMG_EINVAL;
   }
@@ -806,6 +893,12 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     c->u[l].exps = (int8_t*)dalloc(c, g.nblk);
     c->r[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->r[l].stride);
     c->r[l].exps = (int8_t*)dalloc(c, g.nblk);
+    if (s->nu > 1) {
+      c->ysec[l].stride = wr(c, l, Lmax);
+      c->ysec[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->ysec[l].stride);
+      c->ysec[l].exps = (int8_t*)dalloc(c, g.nblk);
+      if (!c->ysec[l].mant || !c->ysec[l].exps) { rc = FMG_ENOMEM; break; }
+    }
     c->gtab[l] = (double*)dalloc(c, sizeof(double) * g.n);
     if (!c->u[l].mant || !c->u[l].exps || !c->r[l].mant || !c->r[l].exps || !c->gtab[l]) { rc = FMG_ENOMEM; break; }
     std::vector<double> gt(g.n);
@@ -829,6 +922,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   if (rc == FMG_OK) {
     int lc_cap = Lmax;
     if (const char* e = getenv("FMG_LC")) lc_cap = std::min(lc_cap, atoi(e));
+    if (s->nu > 1) lc_cap = 0;  // nu > 1: KC runs the initial coarse solve only; the grid kernels do the rest
     int ust[kMaxLev], rst[kMaxLev];
     for (int l = 0; l <= Lmax; ++l) {
       ust[l] = c->u[l].stride;
@@ -879,6 +973,11 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     c->buf[i] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
     if (!c->buf[i]) rc = FMG_ENOMEM;
     else cudaMemset(c->buf[i], 0, sizeof(double) * c->g[Lmax].size);
+  }
+  if (rc == FMG_OK && s->nu > 1) {  // YO: dec ý of the previous cycle at the level being smoothed
+    c->buf[8] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
+    if (!c->buf[8]) rc = FMG_ENOMEM;
+    else cudaMemset(c->buf[8], 0, sizeof(double) * c->g[Lmax].size);
   }
   for (int i = 6; i < 8 && rc == FMG_OK; ++i) {
     c->buf[i] = (double*)dalloc(c, sizeof(double) * 2 * c->g[c->lc].size);

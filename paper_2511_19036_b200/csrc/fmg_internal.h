@@ -46,10 +46,11 @@ int coarse_count(int dim, int p);
 int build_coarse_inverse(int dim, int p, double* Ainv);  // 0 on success
 
 // Operation descriptors (mirrors the device Op).
-enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_CFAS1 = 6, OP_CHEB, OP_PROLONG, OP_GS };
+enum { OP_DECODE = 0, OP_RESIDUAL, OP_RESTRICT, OP_NORMS, OP_CFAS1 = 6, OP_CHEB, OP_PROLONG, OP_GS, OP_SQ, OP_COARSE };
 struct OpDesc {
   int type, l, L, step, last;
   int wr, wu_in, wu_out;
+  int guess, store, smode;  // nu > 1 cycles: see MArgs
   int row;
   long long poff;  // norm partials of this (FMG level, iteration, level): pbase + poff
 };
@@ -68,13 +69,17 @@ struct LevelDev {
   double* part;    // norm partials, one per tile
   int* count;      // arrival counter for the last-CTA norm reduction
   double* U;       // decoded u_l = dec ú_l + P_l u_{l-1} (padded level layout)
-  double* T;       // residual temporary t_l
-  double* W;       // w_l = z_l + dec ý_l
+  double* T;       // residual temporary t_l (nu > 1: s_l between cycles)
+  double* W;       // w_l = z_l + dec ý_l (nu > 1 s sweep: q_l = A ý_l + s_l)
+  uint32_t* ymant; // nu > 1: the correction ý_l kept across cycles (width w_r(l, L))
+  int8_t* yexp;
+  int ystride;
 };
 
 // Scratch and bookkeeping pointers of the march kernels.
 struct MPtrs {
   double *Z, *B, *Y[2], *Dv, *PU;
+  double* YO;      // nu > 1: dec ý_l of the previous cycle at the level being smoothed
   double* pbase;
   int* status;
 };
@@ -87,6 +92,10 @@ struct MArgs {
   int nyb, NZo;              // 3D: tile rows (of 8), output planes
   int zlo, zhi;              // 3D: the planes of this rank (z slab), [zlo, zhi)
   int gs;                    // smoother: multicolour Gauss-Seidel (cFas1 forms colour 0; OP_GS: colour `step`)
+  // nu > 1 cycles (Alg 3.1, reading R23):
+  int guess;                 // cFas1 / last step: ý of the previous cycle is the initial guess
+  int store;                 // last step: store ý_l (not the last cycle), no correction
+  int smode;                 // OP_RESTRICT: s sweep (no encode, no norm); OP_SQ: s_{l} = 0 (top level)
   // operands in the parameter space (no dependent global loads at kernel start)
   LevelDev lv;               // the output level l
   LevelDev lo;               // the other level: l-1 (decode, prolongation, cFas) or l+1 (restriction)
@@ -174,6 +183,7 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
 void march3_set_attributes();
 int march3_rows();
 void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);
+void launch_coarse_nu(int p, cudaStream_t st, const void* devctx, const MArgs& a);  // nu > 1 level 0 (2D)
 int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* rst, int n_ir, int lc_cap,
             KcLayout* ly, int* lc_out, int* cs_out);
 int kc_warps_per_cta();

@@ -491,7 +491,7 @@ __device__ __forceinline__ void m_restrict_item(const MArgs& a, const Coefs& cf,
       lc_.T[(long long)yc * gc.NX + xc] = t;
       ss = fma(t, t, ss);
       const long long blk = (long long)yc * nxb + (it.x0 >> 5);
-      warp_encode(t, a.wr, lc_.rmant + blk * lc_.rstride, lc_.rexp + blk, lane, c.status);
+      if (!a.smode) warp_encode(t, a.wr, lc_.rmant + blk * lc_.rstride, lc_.rexp + blk, lane, c.status);
     }
     __syncwarp();
   }
@@ -536,7 +536,7 @@ __device__ __forceinline__ void m_finalize_r(const MPtrs& c, const MArgs& a, con
 // Chebyshev step 1 with the prolongation fused:
 // z_l = P w_{l-1} computed on the staged rows, b = dec r_l - A z_l;
 // stores Z (l < L), PU = P u_{l-1}, B; k == 1 finalises directly.
-template <int P>
+template <int P, bool NU = false>
 __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
   const MPtrs& c = a.p;
   const LevelDev& lv = a.lv;
@@ -555,8 +555,8 @@ __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, co
         // z row yy on the block columns and the x halo (0 outside the level),
         // P u_{l-1} at the own columns of the output rows
         const bool inrow = yy >= 0 && yy < g.NY;
-        double zm = 0.0, zh = 0.0, pu = 0.0;
-        if (inrow) {  // (warp-uniform)
+        double zm = 0.0, zh = 0.0, pu = 0.0, yo = 0.0, yhv = 0.0;
+        if (inrow && (!NU || a.l > 0)) {  // (warp-uniform; nu > 1 level 0: z_0 = 0, no coarser u)
           const int need = P * (yy / (2 * P)) + P;  // coarse rows by .. by + P
           if (pr.next <= need) {
             __syncwarp();  // the previous row's y passes are done with the slots about to be refilled
@@ -569,12 +569,23 @@ __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, co
           zh = (unkh && unky && lane < 2 * P) ? pr.ypass(cf, yy, jh, 0) : 0.0;
           if (yy >= it.ys && yy < it.ye) pu = (unkx && unky) ? pr.ypass(cf, yy, lane, ProlongRing<P>::XW) : 0.0;
         }
-        slot[P + lane] = zm;
-        if (lane < 2 * P) slot[lane < P ? lane : 32 + lane] = zh;
+        if constexpr (NU) {
+          if (inrow && a.guess) {  // + dec ý of the previous cycle: A (z + ý) (reading R23)
+            const long long blk = (long long)yy * nxb + (it.x0 >> 5);
+            yo = warp_decode(lv.ymant + blk * lv.ystride, lv.yexp[blk], a.wr, lane);
+            if (lane < 2 * P && xh >= 0 && xh < g.NX) {
+              const long long hb = (long long)yy * nxb + (xh >> 5);
+              yhv = point_decode(lv.ymant + hb * lv.ystride, lv.yexp[hb], a.wr, xh & 31);
+            }
+          }
+        }
+        slot[P + lane] = (NU && a.guess) ? zm + yo : zm;
+        if (lane < 2 * P) slot[lane < P ? lane : 32 + lane] = (NU && a.guess) ? zh + yhv : zh;
         if (yy >= it.ys && yy < it.ye) {
           const long long idx = (long long)yy * g.NX + x;
           if (a.l < a.L) c.Z[idx] = zm;
           c.PU[idx] = pu;
+          if (NU && a.guess) c.YO[idx] = yo;
         }
       },
       [&](int, double*) {},
@@ -589,7 +600,8 @@ __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, co
       [&](int y, double az, const double* slot, const RAux& r) {
         const long long idx = (long long)y * g.NX + x, blk = (long long)y * nxb + (it.x0 >> 5);
         const double rv = warp_decode_r(r.w0, r.e, a.wr, lane, r.w1);
-        const double b = rv - az;
+        // nu > 1, cycles >= 2: ((r - s) - A (z + ý)), s_L = 0 (reading R23)
+        const double b = (NU && a.guess) ? (rv - (a.l < a.L ? lv.T[idx] : 0.0)) - az : rv - az;
         if (a.gs) {  // multicolour GS from y = 0: colour 0 gets y = 0 + invD (b - 0), others 0
           c.B[idx] = b;
           const bool c0 = x % (P + 1) == 0 && y % (P + 1) == 0;
@@ -648,7 +660,7 @@ __device__ __forceinline__ void m_gs_item(const MArgs& a, const Coefs& cf, const
       },
       bars);
 }
-template <int P>
+template <int P, bool NU>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -656,13 +668,13 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cfas1(const DevCt
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  m_cfas1_item<P>(a, cf, it, msm);
+  m_cfas1_item<P, NU>(a, cf, it, msm);
 }
 
 // Chebyshev step j >= 2: q = b - A y; d_j = fma(alpha_j, d_{j-1}, beta_j (invD q));
 // y_j = y_{j-1} + d_j.  Step 2 stages b and forms
 // y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
-template <int P, bool TMA>
+template <int P, bool TMA, bool NU = false>
 __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
   const MPtrs& c = a.p;
   const LevelDev& lv = a.lv;
@@ -713,7 +725,17 @@ __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, con
         const double d = fma(al, dprev, be * (invd2(cf, P, g.n, x, y) * q));
         const double yv = yprev + d;
         if (a.last) {
-          m_finalize_r(c, a, lv, idx, blk, yv, p.z, p.pu, p.w0, p.w1, p.e, lane);
+          if constexpr (NU) {  // nu > 1: ý_l + M_l(...), stored between cycles
+            const double yt = a.guess ? c.YO[idx] + yv : yv;
+            if (a.store) {
+              const double yq = warp_encode(yt, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
+              if (a.l < a.L) lv.W[idx] = p.z + yq;
+            } else {
+              m_finalize_r(c, a, lv, idx, blk, yt, p.z, p.pu, p.w0, p.w1, p.e, lane);
+            }
+          } else {
+            m_finalize_r(c, a, lv, idx, blk, yv, p.z, p.pu, p.w0, p.w1, p.e, lane);
+          }
         } else {
           c.Y[j & 1][idx] = yv;
           c.Dv[idx] = d;
@@ -721,7 +743,7 @@ __device__ __forceinline__ void m_cheb_item(const MArgs& a, const Coefs& cf, con
       },
       bars);
 }
-template <int P, bool TMA>
+template <int P, bool TMA, bool NU = false>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -729,7 +751,86 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  m_cheb_item<P, TMA>(a, cf, it, msm);
+  m_cheb_item<P, TMA, NU>(a, cf, it, msm);
+}
+
+// s sweep of nu > 1 cycles (Alg 3.1):
+// q_l = A_l dec ý_l + s_l into W_l (s_l = 0 on the top level, 0 at fine
+// non-unknowns); the restriction then forms s_{l-1} = R_l q_l.
+template <int P>
+__device__ __forceinline__ void m_sq_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
+  const LevelDev& lv = a.lv;
+  const Geom g = lv.g;
+  const int lane = threadIdx.x, x = it.x0 + lane, nxb = g.NX >> 5;
+  double* ring = msm + threadIdx.y * (MNB * MSLOT);
+  const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);
+  march_A<P>(
+      cf, it.ys, it.ye, x, ring,
+      [&](int yy, double* slot) {
+        double vo = 0.0, vh = 0.0;
+        if (yy >= 0 && yy < g.NY) {  // (warp-uniform)
+          const long long blk = (long long)yy * nxb + (it.x0 >> 5);
+          vo = warp_decode(lv.ymant + blk * lv.ystride, lv.yexp[blk], a.wr, lane);
+          if (lane < 2 * P && xh >= 0 && xh < g.NX) {
+            const long long hb = (long long)yy * nxb + (xh >> 5);
+            vh = point_decode(lv.ymant + hb * lv.ystride, lv.yexp[hb], a.wr, xh & 31);
+          }
+        }
+        slot[P + lane] = vo;
+        if (lane < 2 * P) slot[lane < P ? lane : 32 + lane] = vh;
+      },
+      [&](int, double*) {}, [&](int) { return NoAux{}; },
+      [&](int y, double ay, const double*, const NoAux&) {
+        const long long idx = (long long)y * g.NX + x;
+        const bool unk = unk1(x, g.n) && unk1(y, g.n);
+        lv.W[idx] = unk ? ay + (a.smode ? 0.0 : lv.T[idx]) : 0.0;
+      });
+}
+template <int P>
+__global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_sq(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+    const __grid_constant__ Coefs cf) {
+  extern __shared__ __align__(128) double msm[];
+  pdl_wait();
+  pdl_trigger();
+  MItem it;
+  if (!m_item(a, it)) return;
+  m_sq_item<P>(a, cf, it, msm);
+}
+
+// Level 0 of a nu > 1 cycle (2D; one warp; oracle cfas_cycle): y_0 = A_0^{-1} b_0
+// on the (2p-1)^2 unknowns (b_0 = the bracket cFas1 stored in B), + dec ý_0 of
+// the previous cycle (guess), ý_0 = enc_wr(y_0) stored, w_0 = dec ý_0; after
+// the last cycle ú_0 = enc_wu(dec ú_0 + dec ý_0) and u_0 = dec ú_0.
+template <int P>
+__global__ void __launch_bounds__(32) k_coarse_nu(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int m = 2 * P - 1, n0 = m * m;
+  __shared__ double sb[32];
+  const DevCtx& dc = *cp;
+  const MPtrs& c = a.p;
+  const LevelDev& lv = a.lv;
+  const Geom g = lv.g;
+  const int lane = threadIdx.x, nxb = g.NX >> 5;
+  for (int J = lane; J < n0; J += 32) sb[J] = c.B[(long long)(J / m + 1) * g.NX + (J % m + 1)];
+  __syncwarp();
+  for (int y = 0; y < g.NY; ++y) {
+    const int x = lane;
+    double s = 0.0;
+    if (unk1(x, g.n) && unk1(y, g.n)) {
+      const double* Ai = dc.Ainv + (long long)((y - 1) * m + (x - 1)) * n0;
+      for (int J = 0; J < n0; ++J) s = fma(Ai[J], sb[J], s);
+    }
+    const long long blk = (long long)y * nxb;
+    if (a.guess) s = warp_decode(lv.ymant + blk * lv.ystride, lv.yexp[blk], a.wr, lane) + s;
+    const double yq = warp_encode(s, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
+    lv.W[(long long)y * g.NX + x] = yq;
+    if (!a.store) {
+      const double uo = warp_decode(lv.umant + blk * lv.ustride, lv.uexp[blk], a.wu_in, lane);
+      const double uq = warp_encode(uo + yq, a.wu_out, lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
+      lv.U[(long long)y * g.NX + x] = uq;
+    }
+  }
 }
 
 template <int P, bool TMA>
@@ -762,7 +863,10 @@ void march_set_attributes() {
   cudaFuncSetAttribute(k_m_residual<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));   \
   cudaFuncSetAttribute(k_m_restrict<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false)); \
   cudaFuncSetAttribute(k_m_restrict<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));   \
-  cudaFuncSetAttribute(k_m_cfas1<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem_cfas1(P));        \
+  cudaFuncSetAttribute(k_m_cfas1<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem_cfas1(P)); \
+  cudaFuncSetAttribute(k_m_cfas1<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem_cfas1(P));  \
+  cudaFuncSetAttribute(k_m_cheb<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false)); \
+  cudaFuncSetAttribute(k_m_sq<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));               \
   cudaFuncSetAttribute(k_m_cheb<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));     \
   cudaFuncSetAttribute(k_m_cheb<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));       \
   cudaFuncSetAttribute(k_m_gs<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));       \
@@ -790,6 +894,7 @@ static void m_launch(K kernel, int nitems, int smem, cudaStream_t st, const DevC
 void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf) {
   const DevCtx* c = (const DevCtx*)devctx;
   const bool t = a.tma != 0;
+  const bool nu = a.guess || a.store;  // nu > 1 cycle kernels
   const int sm = march_smem(t);
 #define TM(K, P) (t ? (void (*)(const DevCtx*, MArgs, Coefs))K<P, true> : (void (*)(const DevCtx*, MArgs, Coefs))K<P, false>)
 #define F(P)                                                                                     \
@@ -797,13 +902,36 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
     case OP_DECODE: m_launch(k_m_decode<P>, a.nitems, 0, st, c, a, cf); break;                   \
     case OP_RESIDUAL: m_launch(TM(k_m_residual, P), a.nitems, sm, st, c, a, cf); break;          \
     case OP_RESTRICT: m_launch(TM(k_m_restrict, P), a.nitems, sm, st, c, a, cf); break;          \
-    case OP_CFAS1: m_launch(k_m_cfas1<P>, a.nitems, march_smem_cfas1(P), st, c, a, cf); break;   \
+    case OP_CFAS1:                                                                               \
+      if (nu) m_launch(k_m_cfas1<P, true>, a.nitems, march_smem_cfas1(P), st, c, a, cf);          \
+      else m_launch(k_m_cfas1<P, false>, a.nitems, march_smem_cfas1(P), st, c, a, cf);            \
+      break;                                                                                      \
+    case OP_SQ: m_launch(k_m_sq<P>, a.nitems, march_smem(false), st, c, a, cf); break;           \
     case OP_GS: m_launch(TM(k_m_gs, P), a.nitems, sm, st, c, a, cf); break;                      \
-    default: m_launch(TM(k_m_cheb, P), a.nitems, sm, st, c, a, cf); break;                       \
+    default:                                                                                     \
+      if (nu) m_launch(k_m_cheb<P, false, true>, a.nitems, march_smem(false), st, c, a, cf);      \
+      else m_launch(TM(k_m_cheb, P), a.nitems, sm, st, c, a, cf);                                 \
+      break;                                                                                      \
   }
   M_DISPATCH(p, F);
 #undef F
 #undef TM
+}
+
+void launch_coarse_nu(int p, cudaStream_t st, const void* devctx, const MArgs& a) {
+  const DevCtx* c = (const DevCtx*)devctx;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (p == 1) cudaLaunchKernelEx(&cfg, k_coarse_nu<1>, c, a);
+  else if (p == 2) cudaLaunchKernelEx(&cfg, k_coarse_nu<2>, c, a);
+  else cudaLaunchKernelEx(&cfg, k_coarse_nu<3>, c, a);
 }
 
 }  // namespace fmg

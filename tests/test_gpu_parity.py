@@ -142,17 +142,6 @@ def test_fmg_parity_tile_path(P, monkeypatch, d, p, levels):
     compare_solvers(P, d, p, levels)
 
 
-def test_nu_above_one_is_rejected_on_the_gpu(P):
-    """nu > 1 (§8f N2) is defined by the oracle only this round: the product
-    path refuses it instead of silently running one cycle."""
-    s = default_schedule(2, 1)
-    s["nu"] = 2
-    with pytest.raises(P.FmgError):
-        P.Solver(2, 1, 4, P.Schedule.from_dict(s))
-    s["nu"] = 1
-    P.Solver(2, 1, 4, P.Schedule.from_dict(s)).solve()
-
-
 def test_fmg_parity_C1(P):
     c = CONFIGS["C1"]
     compare_solvers(P, c["dim"], c["p"], c["levels"])
