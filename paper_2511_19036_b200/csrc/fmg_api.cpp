@@ -271,8 +271,8 @@ int ncolours(const fmg_ctx* c) {
 // One IR iteration at FMG level L: fmgResidual (Alg 3.2),
 // cFas V(0,1) (Alg 3.1, nu = 1), correction.  Levels <= lc run inside KC.
 // One IR iteration with nu > 1 compact V(0,1) cycles (Alg 3.1
-// PAPER.md:633-661, reading R23; oracle orc_cfas_correct).  2D, Chebyshev,
-// lc = 0: the grid kernels do every level >= 0 except the initial coarse solve.
+// PAPER.md:633-661, reading R23; oracle orc_cfas_correct).  Chebyshev, one
+// GPU, lc = 0: the grid kernels do every level >= 0 except the initial coarse solve.
 void build_iteration_nu(Builder& b, int L, int it) {
   fmg_ctx* c = b.c;
   const bool fine = L == c->Lmax;
@@ -308,6 +308,7 @@ void build_iteration_nu(Builder& b, int L, int it) {
       }
     }
     {  // level 0: the bracket (cFas1 with z_0 = 0), then M_0 = A_0^{-1}, ý_0, w_0 (+ correction)
+      if (c->dim == 3) b.grid(mkop(OP_PROLONG, 0, L));  // (3D: Z_0 = 0, P u_{-1} = 0)
       OpDesc q = mkop(OP_CFAS1, 0, L);
       q.step = 1;
       q.guess = guess;
@@ -322,6 +323,7 @@ void build_iteration_nu(Builder& b, int L, int it) {
       b.grid(cc);
     }
     for (int l = 1; l <= L; ++l) {
+      if (c->dim == 3) b.grid(mkop(OP_PROLONG, l, L));  // z_l = P w_{l-1}, P u_{l-1}
       for (int step = 1; step <= k; ++step) {
         OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
         q.step = step;
@@ -551,7 +553,7 @@ void issue_item(fmg_ctx* c, const Item& it) {
     mark(c, it.timed_cls);
     if (c->march) {
       const MArgs m = march_args(c, it.op);
-      if (it.op.type == OP_COARSE) launch_coarse_nu(c->p, c->cur, c->devctx, m);
+      if (it.op.type == OP_COARSE) launch_coarse_nu(c->dim, c->p, c->cur, c->devctx, m);
       else if (c->dim == 2) launch_march(c->p, c->cur, c->devctx, m, c->cf);
       else launch_march3(c->p, c->cur, c->devctx, m, c->cf);
     } else {
@@ -832,8 +834,8 @@ static int check_args(int dim, int p, int levels, const fmg_schedule* s) {
       s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1) || s->smoother < 0 || s->smoother > 1 ||
       s->nu < 0 || s->nu > 8)
     return FMG_EINVAL;
-  // nu > 1 on the GPU: 2D, Chebyshev of degree >= 2
-  if (s->nu > 1 && (dim != 2 || s->smoother != 0 || s->cheb_degree < 2)) return FMG_EINVAL;
+  // nu > 1 on the GPU: Chebyshev of degree >= 2, one GPU (no z slabs)
+  if (s->nu > 1 && (s->smoother != 0 || s->cheb_degree < 2)) return FMG_EINVAL;
   const int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
   return FMG_OK;
@@ -860,7 +862,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     fmg_destroy(c);
     return FMG_EINVAL;
   }
-  if (s->nu > 1 && G > 1) {  // (z slabs are 3D; nu > 1 is 2D)
+  if (s->nu > 1 && G > 1) {  // (nu > 1: single GPU this round)
     fmg_destroy(c);
     return FMG_EINVAL;
   }

@@ -183,7 +183,7 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
 void march3_set_attributes();
 int march3_rows();
 void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);
-void launch_coarse_nu(int p, cudaStream_t st, const void* devctx, const MArgs& a);  // nu > 1 level 0 (2D)
+void launch_coarse_nu(int dim, int p, cudaStream_t st, const void* devctx, const MArgs& a);  // nu > 1 level 0
 int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* rst, int n_ir, int lc_cap,
             KcLayout* ly, int* lc_out, int* cs_out);
 int kc_warps_per_cta();

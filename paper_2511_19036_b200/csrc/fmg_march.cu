@@ -797,38 +797,44 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_sq(const DevCtx* 
   m_sq_item<P>(a, cf, it, msm);
 }
 
-// Level 0 of a nu > 1 cycle (2D; one warp; oracle cfas_cycle): y_0 = A_0^{-1} b_0
-// on the (2p-1)^2 unknowns (b_0 = the bracket cFas1 stored in B), + dec ý_0 of
+// Level 0 of a nu > 1 cycle (one warp; oracle cfas_cycle): y_0 = A_0^{-1} b_0
+// on the (2p-1)^d unknowns (b_0 = the bracket cFas1 stored in B), + dec ý_0 of
 // the previous cycle (guess), ý_0 = enc_wr(y_0) stored, w_0 = dec ý_0; after
 // the last cycle ú_0 = enc_wu(dec ú_0 + dec ý_0) and u_0 = dec ú_0.
-template <int P>
+template <int D, int P>
 __global__ void __launch_bounds__(32) k_coarse_nu(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a) {
   pdl_wait();
   pdl_trigger();
-  constexpr int m = 2 * P - 1, n0 = m * m;
-  __shared__ double sb[32];
+  constexpr int m = 2 * P - 1, n0 = D == 3 ? m * m * m : m * m;
+  __shared__ double sb[128];
   const DevCtx& dc = *cp;
   const MPtrs& c = a.p;
   const LevelDev& lv = a.lv;
   const Geom g = lv.g;
   const int lane = threadIdx.x, nxb = g.NX >> 5;
-  for (int J = lane; J < n0; J += 32) sb[J] = c.B[(long long)(J / m + 1) * g.NX + (J % m + 1)];
+  for (int J = lane; J < n0; J += 32) {
+    const int jx = J % m + 1, jy = (J / m) % m + 1, jz = D == 3 ? J / (m * m) + 1 : 0;
+    sb[J] = c.B[((long long)jz * g.NY + jy) * g.NX + jx];
+  }
   __syncwarp();
-  for (int y = 0; y < g.NY; ++y) {
-    const int x = lane;
-    double s = 0.0;
-    if (unk1(x, g.n) && unk1(y, g.n)) {
-      const double* Ai = dc.Ainv + (long long)((y - 1) * m + (x - 1)) * n0;
-      for (int J = 0; J < n0; ++J) s = fma(Ai[J], sb[J], s);
-    }
-    const long long blk = (long long)y * nxb;
-    if (a.guess) s = warp_decode(lv.ymant + blk * lv.ystride, lv.yexp[blk], a.wr, lane) + s;
-    const double yq = warp_encode(s, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
-    lv.W[(long long)y * g.NX + x] = yq;
-    if (!a.store) {
-      const double uo = warp_decode(lv.umant + blk * lv.ustride, lv.uexp[blk], a.wu_in, lane);
-      const double uq = warp_encode(uo + yq, a.wu_out, lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
-      lv.U[(long long)y * g.NX + x] = uq;
+  for (int zr = 0; zr < (D == 3 ? g.NZ : 1); ++zr) {
+    for (int y = 0; y < g.NY; ++y) {
+      const int x = lane;
+      double s = 0.0;
+      if (unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(zr, g.n))) {
+        const int I = ((D == 3 ? zr - 1 : 0) * m + (y - 1)) * m + (x - 1);
+        const double* Ai = dc.Ainv + (long long)I * n0;
+        for (int J = 0; J < n0; ++J) s = fma(Ai[J], sb[J], s);
+      }
+      const long long row = (long long)zr * g.NY + y, blk = row * nxb;
+      if (a.guess) s = warp_decode(lv.ymant + blk * lv.ystride, lv.yexp[blk], a.wr, lane) + s;
+      const double yq = warp_encode(s, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
+      lv.W[row * g.NX + x] = yq;
+      if (!a.store) {
+        const double uo = warp_decode(lv.umant + blk * lv.ustride, lv.uexp[blk], a.wu_in, lane);
+        const double uq = warp_encode(uo + yq, a.wu_out, lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
+        lv.U[row * g.NX + x] = uq;
+      }
     }
   }
 }
@@ -918,7 +924,7 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
 #undef TM
 }
 
-void launch_coarse_nu(int p, cudaStream_t st, const void* devctx, const MArgs& a) {
+void launch_coarse_nu(int dim, int p, cudaStream_t st, const void* devctx, const MArgs& a) {
   const DevCtx* c = (const DevCtx*)devctx;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1);
@@ -929,9 +935,15 @@ void launch_coarse_nu(int p, cudaStream_t st, const void* devctx, const MArgs& a
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (p == 1) cudaLaunchKernelEx(&cfg, k_coarse_nu<1>, c, a);
-  else if (p == 2) cudaLaunchKernelEx(&cfg, k_coarse_nu<2>, c, a);
-  else cudaLaunchKernelEx(&cfg, k_coarse_nu<3>, c, a);
+  if (dim == 2) {
+    if (p == 1) cudaLaunchKernelEx(&cfg, k_coarse_nu<2, 1>, c, a);
+    else if (p == 2) cudaLaunchKernelEx(&cfg, k_coarse_nu<2, 2>, c, a);
+    else cudaLaunchKernelEx(&cfg, k_coarse_nu<2, 3>, c, a);
+  } else {
+    if (p == 1) cudaLaunchKernelEx(&cfg, k_coarse_nu<3, 1>, c, a);
+    else if (p == 2) cudaLaunchKernelEx(&cfg, k_coarse_nu<3, 2>, c, a);
+    else cudaLaunchKernelEx(&cfg, k_coarse_nu<3, 3>, c, a);
+  }
 }
 
 }  // namespace fmg

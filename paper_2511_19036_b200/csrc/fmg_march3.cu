@@ -283,7 +283,7 @@ __device__ __forceinline__ void m3_finalize(const MPtrs& c, const MArgs& a, cons
   lv.U[idx] = uq + pu;
 }
 
-template <int P, bool TMA>
+template <int P, bool TMA, bool NU = false>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                          const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -306,7 +306,34 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
         if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(c.Z, g, it.x0, it.y0, zz, P, slot);
       },
-      [&](int, double*) {},
+      [&](int zz, double* slot) {
+        if constexpr (NU) {
+          if (!a.guess) return;
+          // nu > 1: stage z + dec ý of the previous cycle (A (z + ý),
+          // reading R23) on this thread's staged rows; keep dec ý of the output
+          // points for the last Chebyshev step
+          constexpr int NR = TW3 + 2 * P;
+          const bool zok = zz >= 0 && zz < g.NZ;
+          const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);
+          for (int r = threadIdx.y; r < NR; r += TW3) {
+            const int yy = it.y0 - P + r;
+            if (!zok || yy < 0 || yy >= g.NY) continue;  // (warp-uniform)
+            const long long rb = ((long long)zz * g.NY + yy) * nxb;
+            const double yo = warp_decode(lv.ymant + (rb + (it.x0 >> 5)) * lv.ystride, lv.yexp[rb + (it.x0 >> 5)],
+                                          a.wr, lane);
+            double* row = slot + r * RS3;
+            row[P + lane] = row[P + lane] + yo;
+            if (lane < 2 * P && xh >= 0 && xh < g.NX) {
+              const long long hb = rb + (xh >> 5);
+              double& v = row[lane < P ? lane : 32 + lane];
+              v = v + point_decode(lv.ymant + hb * lv.ystride, lv.yexp[hb], a.wr, xh & 31);
+            }
+            if (zz >= it.zs && zz < it.ze && yy >= it.y0 && yy < it.y0 + TW3)
+              c.YO[((long long)zz * g.NY + yy) * g.NX + x] = yo;
+          }
+          __syncthreads();
+        }
+      },
       [&](int zn) {
         CAux3 q{};
         if (rowok) {
@@ -330,7 +357,8 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
         const long long idx = ((long long)z * g.NY + y) * g.NX + x;
         const long long blk = ((long long)z * g.NY + y) * nxb + (it.x0 >> 5);
         const double rv = warp_decode_r3(q.w0, q.e, a.wr, lane, q.w1);
-        const double b = rv - az;
+        // nu > 1, cycles >= 2: ((r - s) - A (z + ý)), s_L = 0 (reading R23)
+        const double b = (NU && a.guess) ? (rv - (a.l < a.L ? lv.T[idx] : 0.0)) - az : rv - az;
         if (a.gs) {  // multicolour GS from y = 0: colour 0 gets y = 0 + invD (b - 0), others 0
           c.B[idx] = b;
           const bool c0 = x % (P + 1) == 0 && y % (P + 1) == 0 && z % (P + 1) == 0;
@@ -350,7 +378,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
 
 // Chebyshev step j >= 2; step 2 stages b and forms
 // y_1 = d_1 = inv_theta (invD b) in place; the last step finalises.
-template <int P, bool TMA>
+template <int P, bool TMA, bool NU = false>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                         const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -441,7 +469,17 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
         const double d = fma(al, dprev, be * (f * qq));
         const double yv = yprev + d;
         if (a.last) {
-          m3_finalize(c, a, lv, idx, blk, yv, q.z, q.pu, q.w0, q.w1, q.e, lane);
+          if constexpr (NU) {  // nu > 1: ý_l + M_l(...), stored between cycles
+            const double yt = a.guess ? c.YO[idx] + yv : yv;
+            if (a.store) {
+              const double yqv = warp_encode(yt, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
+              if (a.l < a.L) lv.W[idx] = q.z + yqv;
+            } else {
+              m3_finalize(c, a, lv, idx, blk, yt, q.z, q.pu, q.w0, q.w1, q.e, lane);
+            }
+          } else {
+            m3_finalize(c, a, lv, idx, blk, yv, q.z, q.pu, q.w0, q.w1, q.e, lane);
+          }
         } else {
           c.Y[j & 1][idx] = yv;
           c.Dv[idx] = d;
@@ -600,6 +638,56 @@ __global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restric
   }
 }
 
+// s sweep of nu > 1 cycles: q_l = A_l dec ý_l + s_l into W_l
+// (s_l = 0 on the top level; 0 at non-unknowns); the staged boxes are the
+// decoded ý (own columns by warp decode, halo columns by point decode).
+template <int P>
+__global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_sq(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
+                                                      const __grid_constant__ Coefs cf) {
+  extern __shared__ __align__(128) double msm[];
+  pdl_wait();
+  pdl_trigger();
+  M3Item it;
+  m3_item(a, it);
+  const LevelDev& lv = a.lv;
+  const Geom g = lv.g;
+  const int lane = threadIdx.x, w = threadIdx.y, x = it.x0 + lane, y = it.y0 + w;
+  const bool rowok = y < g.NY;
+  double* ring = msm;
+  double* XA = ring + m3_ring_doubles<P>();
+  double* XB = XA + (TW3 + 2 * P) * 32;
+  const int nxb = g.NX >> 5;
+  constexpr int NR = TW3 + 2 * P;
+  const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);
+  march3_A<P>(
+      cf, it, a.l, ring, XA, XB,
+      [&](int zz, double* slot) {
+        const bool zok = zz >= 0 && zz < g.NZ;
+        for (int r = threadIdx.y; r < NR; r += TW3) {
+          const int yy = it.y0 - P + r;
+          double vo = 0.0, vh = 0.0;
+          if (zok && yy >= 0 && yy < g.NY) {  // (warp-uniform)
+            const long long rb = ((long long)zz * g.NY + yy) * nxb;
+            vo = warp_decode(lv.ymant + (rb + (it.x0 >> 5)) * lv.ystride, lv.yexp[rb + (it.x0 >> 5)], a.wr, lane);
+            if (lane < 2 * P && xh >= 0 && xh < g.NX) {
+              const long long hb = rb + (xh >> 5);
+              vh = point_decode(lv.ymant + hb * lv.ystride, lv.yexp[hb], a.wr, xh & 31);
+            }
+          }
+          double* row = slot + r * RS3;
+          row[P + lane] = vo;
+          if (lane < 2 * P) row[lane < P ? lane : 32 + lane] = vh;
+        }
+      },
+      [&](int, double*) {}, [&](int) { return NoAux3{}; },
+      [&](int z, double ay, const double*, const NoAux3&) {
+        if (!rowok) return;
+        const long long idx = ((long long)z * g.NY + y) * g.NX + x;
+        const bool unk = unk1(x, g.n) && unk1(y, g.n) && unk1(z, g.n);
+        lv.W[idx] = unk ? ay + (a.smode ? 0.0 : lv.T[idx]) : 0.0;
+      });
+}
+
 // Restriction march: the CTA owns 32 x 8 coarse points; each
 // fine plane box (64+4p-2 x 16+4p-2) is staged, x-passed to the coarse columns
 // and y-passed to the coarse rows; the z pass runs on a register ring of the
@@ -686,7 +774,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const
       lc_.T[idx] = t;
       ss = fma(t, t, ss);
       const long long blk = ((long long)zc * gc.NY + yc) * nxb + (it.x0 >> 5);
-      warp_encode(t, a.wr, lc_.rmant + blk * lc_.rstride, lc_.rexp + blk, lane, c.status);
+      if (!a.smode) warp_encode(t, a.wr, lc_.rmant + blk * lc_.rstride, lc_.rexp + blk, lane, c.status);
     }
   }
 #pragma unroll
@@ -713,6 +801,9 @@ void march3_set_attributes() {
   cudaFuncSetAttribute(k_m3_cheb<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));          \
   cudaFuncSetAttribute(k_m3_cheb<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P, true));     \
   cudaFuncSetAttribute(k_m3_gs<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));            \
+  cudaFuncSetAttribute(k_m3_cfas1<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));   \
+  cudaFuncSetAttribute(k_m3_cheb<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));    \
+  cudaFuncSetAttribute(k_m3_sq<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));                  \
   cudaFuncSetAttribute(k_m3_gs<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P, true));       \
   cudaFuncSetAttribute(k_m3_restrict<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_R(P));
   F(1) F(2) F(3)
@@ -739,6 +830,7 @@ void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, c
   const DevCtx* c = (const DevCtx*)devctx;
   const int n = a.nitems;
   const bool t = a.tma != 0;
+  const bool nu = a.guess || a.store;  // nu > 1 cycle kernels
 #define TM(K, P) (t ? (void (*)(const DevCtx*, MArgs, Coefs))K<P, true> : (void (*)(const DevCtx*, MArgs, Coefs))K<P, false>)
 #define F(P)                                                                                  \
   switch (a.type) {                                                                           \
@@ -746,9 +838,16 @@ void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, c
     case OP_PROLONG: m3_launch(k_m3_prolong<P>, n, 0, st, c, a, cf); break;                   \
     case OP_RESIDUAL: m3_launch(TM(k_m3_residual, P), n, m3_smem_A(P, t), st, c, a, cf); break; \
     case OP_RESTRICT: m3_launch(k_m3_restrict<P>, n, m3_smem_R(P), st, c, a, cf); break;      \
-    case OP_CFAS1: m3_launch(TM(k_m3_cfas1, P), n, m3_smem_A(P, t), st, c, a, cf); break;     \
+    case OP_CFAS1:                                                                            \
+      if (nu) m3_launch(k_m3_cfas1<P, false, true>, n, m3_smem_A(P), st, c, a, cf);            \
+      else m3_launch(TM(k_m3_cfas1, P), n, m3_smem_A(P, t), st, c, a, cf);                     \
+      break;                                                                                   \
+    case OP_SQ: m3_launch(k_m3_sq<P>, n, m3_smem_A(P), st, c, a, cf); break;                  \
     case OP_GS: m3_launch(TM(k_m3_gs, P), n, m3_smem_A(P, t), st, c, a, cf); break;           \
-    default: m3_launch(TM(k_m3_cheb, P), n, m3_smem_A(P, t), st, c, a, cf); break;            \
+    default:                                                                                  \
+      if (nu) m3_launch(k_m3_cheb<P, false, true>, n, m3_smem_A(P), st, c, a, cf);             \
+      else m3_launch(TM(k_m3_cheb, P), n, m3_smem_A(P, t), st, c, a, cf);                      \
+      break;                                                                                   \
   }
   if (p == 1) { F(1) } else if (p == 2) { F(2) } else { F(3) }
 #undef F

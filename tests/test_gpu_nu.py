@@ -1,8 +1,8 @@
 """GPU parity for nu > 1 compact V(0,1) cycles per IR iteration (§8(f) row N2;
 Alg 3.1, reading R23) against the oracle: every solution and
 residual section bit for bit, per-level norms within 1e-6, the decoded
-solution bit-identical.  The GPU path covers 2D with the Chebyshev smoother
-(degree >= 2); the other combinations are refused."""
+solution bit-identical.  The GPU path covers 2D and 3D (one GPU) with the
+Chebyshev smoother (degree >= 2); the other combinations are refused."""
 import numpy as np
 import pytest
 
@@ -44,7 +44,8 @@ def _compare(P, d, p, levels, nu, **kw):
 
 
 @pytest.mark.parametrize("nu", [2, 3])
-@pytest.mark.parametrize("d,p,levels", [(2, 1, 2), (2, 1, 6), (2, 2, 5), (2, 3, 4)])
+@pytest.mark.parametrize("d,p,levels", [(2, 1, 2), (2, 1, 6), (2, 2, 5), (2, 3, 4),
+                                        (3, 1, 2), (3, 1, 5), (3, 2, 4), (3, 3, 3)])
 def test_nu_parity(P, d, p, levels, nu):
     _compare(P, d, p, levels, nu)
 
@@ -59,10 +60,19 @@ def test_nu_parity_C2_full(P):
     _compare(P, c["dim"], c["p"], c["levels"], 2)
 
 
+def test_nu_parity_C3_full(P):
+    c = CONFIGS["C3"]
+    _compare(P, c["dim"], c["p"], 7, 2)  # (C3's geometry on 7 levels: the oracle stays in seconds)
+
+
 def test_nu_refused_outside_the_gpu_scope(P):
-    for d, p, over in [(3, 1, {}), (2, 1, {"smoother": 1}), (2, 1, {"cheb_degree": 1})]:
+    for d, p, over in [(2, 1, {"smoother": 1}), (3, 1, {"cheb_degree": 1})]:
         s = default_schedule(d, p)
         s.update(over)
         s["nu"] = 2
         with pytest.raises(P.FmgError):
             P.Solver(d, p, 3, P.Schedule.from_dict(s))
+    s = default_schedule(3, 1)
+    s["nu"] = 2
+    with pytest.raises(P.FmgError):  # z slabs: nu = 1 only this round
+        P.Solver(3, 1, 4, P.Schedule.from_dict(s), slabs=2)
