@@ -322,18 +322,20 @@ void build_iteration_nu(Builder& b, int L, int it) {
       cc.wu_out = wu(c, 0, L);
       b.grid(cc);
     }
+    const bool gs = c->s.smoother == 1;
+    const int nsteps = gs ? ncolours(c) : k;  // GS: colour 0 in cFas1, then colours 1 .. (p+1)^d - 1
     for (int l = 1; l <= L; ++l) {
       if (c->dim == 3) b.grid(mkop(OP_PROLONG, l, L));  // z_l = P w_{l-1}, P u_{l-1}
-      for (int step = 1; step <= k; ++step) {
-        OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
-        q.step = step;
-        q.last = step == k;
+      for (int step = 1; step <= nsteps; ++step) {
+        OpDesc q = mkop(step == 1 ? OP_CFAS1 : (gs ? OP_GS : OP_CHEB), l, L);
+        q.step = gs ? step - 1 : step;
+        q.last = step == nsteps;
         q.guess = guess;
         q.store = store;
         q.wr = wr(c, l, L);
         q.wu_in = c->wu_cur[l];
         q.wu_out = wu(c, l, L);
-        b.grid(q, (fine && l == L && !store) ? (step == k ? 5 : 1) : -1);
+        b.grid(q, (fine && l == L && !store) ? (step == nsteps ? 5 : 1) : -1);
       }
     }
   }
@@ -834,8 +836,8 @@ static int check_args(int dim, int p, int levels, const fmg_schedule* s) {
       s->cheb_degree > 8 || !(s->lambda_hi > 0) || !(s->alpha > 1) || s->smoother < 0 || s->smoother > 1 ||
       s->nu < 0 || s->nu > 8)
     return FMG_EINVAL;
-  // nu > 1 on the GPU: Chebyshev of degree >= 2, one GPU (no z slabs)
-  if (s->nu > 1 && (s->smoother != 0 || s->cheb_degree < 2)) return FMG_EINVAL;
+  // nu > 1 on the GPU: Chebyshev of degree >= 2 or multicolour GS; one GPU (no z slabs)
+  if (s->nu > 1 && s->smoother == 0 && s->cheb_degree < 2) return FMG_EINVAL;
   const int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
   return FMG_OK;

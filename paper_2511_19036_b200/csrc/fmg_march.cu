@@ -619,7 +619,7 @@ __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, co
 // nodes of that colour y = y + invD (b - A y) (A on the current iterate; nodes
 // of one colour are uncoupled, so in-place is exact); the last colour
 // finalises every node of the row (oracle mc_gauss_seidel).
-template <int P, bool TMA>
+template <int P, bool TMA, bool NU = false>
 __device__ __forceinline__ void m_gs_item(const MArgs& a, const Coefs& cf, const MItem& it, double* msm) {
   const MPtrs& c = a.p;
   const LevelDev& lv = a.lv;
@@ -655,8 +655,21 @@ __device__ __forceinline__ void m_gs_item(const MArgs& a, const Coefs& cf, const
         const bool mine = colx && y % (P + 1) == cy;
         const double yo = slot[P + lane];
         const double yv = mine ? yo + invd2(cf, P, g.n, x, y) * (p.b - ay) : yo;
-        if (a.last) m_finalize_r(c, a, lv, idx, blk, yv, p.z, p.pu, p.w0, p.w1, p.e, lane);
-        else if (mine) Yv[idx] = yv;
+        if (a.last) {
+          if constexpr (NU) {  // nu > 1: ý_l + M_l(...), stored between cycles
+            const double yt = a.guess ? c.YO[idx] + yv : yv;
+            if (a.store) {
+              const double yq = warp_encode(yt, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
+              if (a.l < a.L) lv.W[idx] = p.z + yq;
+            } else {
+              m_finalize_r(c, a, lv, idx, blk, yt, p.z, p.pu, p.w0, p.w1, p.e, lane);
+            }
+          } else {
+            m_finalize_r(c, a, lv, idx, blk, yv, p.z, p.pu, p.w0, p.w1, p.e, lane);
+          }
+        } else if (mine) {
+          Yv[idx] = yv;
+        }
       },
       bars);
 }
@@ -839,7 +852,7 @@ __global__ void __launch_bounds__(32) k_coarse_nu(const DevCtx* __restrict__ cp,
   }
 }
 
-template <int P, bool TMA>
+template <int P, bool TMA, bool NU = false>
 __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
     const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -847,7 +860,7 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* 
   pdl_trigger();
   MItem it;
   if (!m_item(a, it)) return;
-  m_gs_item<P, TMA>(a, cf, it, msm);
+  m_gs_item<P, TMA, NU>(a, cf, it, msm);
 }
 
 // ------------------------------------------------------------------ host --
@@ -873,6 +886,7 @@ void march_set_attributes() {
   cudaFuncSetAttribute(k_m_cfas1<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem_cfas1(P));  \
   cudaFuncSetAttribute(k_m_cheb<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false)); \
   cudaFuncSetAttribute(k_m_sq<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));               \
+  cudaFuncSetAttribute(k_m_gs<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));   \
   cudaFuncSetAttribute(k_m_cheb<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));     \
   cudaFuncSetAttribute(k_m_cheb<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));       \
   cudaFuncSetAttribute(k_m_gs<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));       \
@@ -913,7 +927,10 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
       else m_launch(k_m_cfas1<P, false>, a.nitems, march_smem_cfas1(P), st, c, a, cf);            \
       break;                                                                                      \
     case OP_SQ: m_launch(k_m_sq<P>, a.nitems, march_smem(false), st, c, a, cf); break;           \
-    case OP_GS: m_launch(TM(k_m_gs, P), a.nitems, sm, st, c, a, cf); break;                      \
+    case OP_GS:                                                                                  \
+      if (nu) m_launch(k_m_gs<P, false, true>, a.nitems, march_smem(false), st, c, a, cf);        \
+      else m_launch(TM(k_m_gs, P), a.nitems, sm, st, c, a, cf);                                   \
+      break;                                                                                      \
     default:                                                                                     \
       if (nu) m_launch(k_m_cheb<P, false, true>, a.nitems, march_smem(false), st, c, a, cf);      \
       else m_launch(TM(k_m_cheb, P), a.nitems, sm, st, c, a, cf);                                 \

@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
 // Multicolour Gauss-Seidel colour `a.step` (>= 1) in place on Y[1]
 // (oracle mc_gauss_seidel): y = y + invD (b - A y) at the nodes
 // of the colour, the last colour finalises every node.
-template <int P, bool TMA>
+template <int P, bool TMA, bool NU = false>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                       const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
@@ -541,8 +541,21 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCt
         const bool mine = colxy && z % (P + 1) == cz;
         const double yo = slot[(w + P) * RS3 + P + lane];
         const double yv = mine ? yo + invd3(cf, P, g.n, a.l, x, y, z) * (q.b - ay) : yo;
-        if (a.last) m3_finalize(c, a, lv, idx, blk, yv, q.z, q.pu, q.w0, q.w1, q.e, lane);
-        else if (mine) Yv[idx] = yv;
+        if (a.last) {
+          if constexpr (NU) {  // nu > 1: ý_l + M_l(...), stored between cycles
+            const double yt = a.guess ? c.YO[idx] + yv : yv;
+            if (a.store) {
+              const double yqv = warp_encode(yt, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
+              if (a.l < a.L) lv.W[idx] = q.z + yqv;
+            } else {
+              m3_finalize(c, a, lv, idx, blk, yt, q.z, q.pu, q.w0, q.w1, q.e, lane);
+            }
+          } else {
+            m3_finalize(c, a, lv, idx, blk, yv, q.z, q.pu, q.w0, q.w1, q.e, lane);
+          }
+        } else if (mine) {
+          Yv[idx] = yv;
+        }
       },
       bars);
 }
@@ -804,6 +817,7 @@ void march3_set_attributes() {
   cudaFuncSetAttribute(k_m3_cfas1<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));   \
   cudaFuncSetAttribute(k_m3_cheb<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));    \
   cudaFuncSetAttribute(k_m3_sq<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));                  \
+  cudaFuncSetAttribute(k_m3_gs<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));      \
   cudaFuncSetAttribute(k_m3_gs<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P, true));       \
   cudaFuncSetAttribute(k_m3_restrict<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_R(P));
   F(1) F(2) F(3)
@@ -843,7 +857,10 @@ void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, c
       else m3_launch(TM(k_m3_cfas1, P), n, m3_smem_A(P, t), st, c, a, cf);                     \
       break;                                                                                   \
     case OP_SQ: m3_launch(k_m3_sq<P>, n, m3_smem_A(P), st, c, a, cf); break;                  \
-    case OP_GS: m3_launch(TM(k_m3_gs, P), n, m3_smem_A(P, t), st, c, a, cf); break;           \
+    case OP_GS:                                                                               \
+      if (nu) m3_launch(k_m3_gs<P, false, true>, n, m3_smem_A(P), st, c, a, cf);               \
+      else m3_launch(TM(k_m3_gs, P), n, m3_smem_A(P, t), st, c, a, cf);                        \
+      break;                                                                                   \
     default:                                                                                  \
       if (nu) m3_launch(k_m3_cheb<P, false, true>, n, m3_smem_A(P), st, c, a, cf);             \
       else m3_launch(TM(k_m3_cheb, P), n, m3_smem_A(P, t), st, c, a, cf);                      \

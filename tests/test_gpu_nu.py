@@ -2,7 +2,8 @@
 Alg 3.1, reading R23) against the oracle: every solution and
 residual section bit for bit, per-level norms within 1e-6, the decoded
 solution bit-identical.  The GPU path covers 2D and 3D (one GPU) with the
-Chebyshev smoother (degree >= 2); the other combinations are refused."""
+Chebyshev (degree >= 2) or multicolour Gauss-Seidel smoother; Chebyshev of
+degree 1 and z slabs are refused."""
 import numpy as np
 import pytest
 
@@ -55,6 +56,12 @@ def test_nu_parity_schedules(P, kw):
     _compare(P, 2, 2, 5, 2, **kw)
 
 
+@pytest.mark.parametrize("d,p,levels", [(2, 1, 6), (2, 2, 5), (3, 1, 4), (3, 2, 3)])
+def test_nu_parity_multicolour_gs(P, d, p, levels):
+    """nu = 2 with the multicolour Gauss-Seidel smoother (N1 x N2)."""
+    _compare(P, d, p, levels, 2, smoother="mcgs")
+
+
 def test_nu_parity_C2_full(P):
     c = CONFIGS["C2"]
     _compare(P, c["dim"], c["p"], c["levels"], 2)
@@ -66,7 +73,7 @@ def test_nu_parity_C3_full(P):
 
 
 def test_nu_refused_outside_the_gpu_scope(P):
-    for d, p, over in [(2, 1, {"smoother": 1}), (3, 1, {"cheb_degree": 1})]:
+    for d, p, over in [(2, 1, {"cheb_degree": 1}), (3, 1, {"cheb_degree": 1})]:
         s = default_schedule(d, p)
         s.update(over)
         s["nu"] = 2
