@@ -312,6 +312,7 @@ void build_iteration_nu(Builder& b, int L, int it) {
       OpDesc q = mkop(OP_CFAS1, 0, L);
       q.step = 1;
       q.guess = guess;
+      q.store = 1;  // (selects the nu kernel: level 0 has no coarser level to prolongate from)
       q.wr = wr(c, 0, L);
       b.grid(q);
       OpDesc cc = mkop(OP_COARSE, 0, L);
