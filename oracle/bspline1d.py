@@ -190,31 +190,151 @@ def dec(sec) -> np.ndarray:
     return x[:n]
 
 
+# ------------------------------------------------- operator layouts (R27) --
+#
+# The GPU path (include/fmg1d.h) consumes the level operators in these
+# layouts, and the oracle evaluates every product in the order they define
+# (reading R27): a row's terms are summed from 0.0 in ascending storage index,
+# so both sides round identically.
+
+
+def band(K: np.ndarray, p: int) -> np.ndarray:
+    """A_l as an n x (2p+1) band: Ab[i, k] = K[i, i-p+k], 0 outside 0..n-1."""
+    n = K.shape[0]
+    Ab = np.zeros((n, 2 * p + 1))
+    for i in range(n):
+        for k in range(2 * p + 1):
+            j = i - p + k
+            if 0 <= j < n:
+                Ab[i, k] = K[i, j]
+    return Ab
+
+
+def two_scale_structure(fine: Level, coarse: Level):
+    """(j0, j1) per fine unknown i: the coarse unknowns j whose B-spline support
+    contains that of fine B-spline i, j0 <= j <= j1 -- the only columns where
+    the two-scale coefficient can be nonzero (a coarse B-spline is a
+    combination of the fine B-splines inside its support).  Knots are dyadic,
+    so the comparisons are exact."""
+    p, m = fine.p, fine.m
+    nf, nc = len(fine.free), len(coarse.free)
+    out = []
+    for i in range(nf):
+        I = i + m
+        a, b = fine.t[I], fine.t[I + p + 1]
+        js = [j for j in range(nc) if coarse.t[j + m] <= a and b <= coarse.t[j + m + p + 1]]
+        assert js == list(range(js[0], js[-1] + 1))
+        out.append((js[0], js[-1]))
+    return out
+
+
+def ell(P: np.ndarray, st) -> tuple:
+    """P in ELL form: vals[i, k] = P[i, c0[i] + k] for c0[i] + k <= j1(i), 0 beyond."""
+    kp = max(j1 - j0 + 1 for j0, j1 in st)
+    vals = np.zeros((len(st), kp))
+    c0 = np.array([j0 for j0, _ in st], dtype=np.int64)
+    for i, (j0, j1) in enumerate(st):
+        vals[i, : j1 - j0 + 1] = P[i, j0 : j1 + 1]
+    return vals, c0
+
+
+def ell_transpose(P: np.ndarray, st, nc: int) -> tuple:
+    """R = P^T in ELL form: for coarse j the fine rows i with j in st[i],
+    ascending."""
+    rows = [[i for i, (j0, j1) in enumerate(st) if j0 <= j <= j1] for j in range(nc)]
+    kr = max(len(r) for r in rows)
+    vals = np.zeros((nc, kr))
+    r0 = np.array([r[0] for r in rows], dtype=np.int64)
+    for j, r in enumerate(rows):
+        assert r == list(range(r[0], r[-1] + 1))
+        vals[j, : len(r)] = P[r, j]
+    return vals, r0
+
+
+def band_mv(Ab: np.ndarray, x: np.ndarray, p: int) -> np.ndarray:
+    """y_i = sum_k Ab[i, k] x[i-p+k], from 0.0, k ascending (R27)."""
+    n = len(x)
+    xp = np.concatenate([np.zeros(p), x, np.zeros(p)])
+    y = np.zeros(n)
+    for k in range(2 * p + 1):
+        y = y + Ab[:, k] * xp[k : k + n]
+    return y
+
+
+def ell_mv(vals: np.ndarray, c0: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """y_i = sum_k vals[i, k] x[c0[i] + k], from 0.0, k ascending (R27)."""
+    xp = np.concatenate([x, np.zeros(vals.shape[1])])
+    y = np.zeros(vals.shape[0])
+    for k in range(vals.shape[1]):
+        y = y + vals[:, k] * xp[c0 + k]
+    return y
+
+
+def dense_mv(A: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """y_i = sum_j A[i, j] x[j], from 0.0, j ascending (R27)."""
+    y = np.zeros(A.shape[0])
+    for j in range(A.shape[1]):
+        y = y + A[:, j] * x[j]
+    return y
+
+
 # ------------------------------------------------------------ compact FMG --
 
 
-def lex_gs(A: np.ndarray, b: np.ndarray, bw: int) -> np.ndarray:
-    """One forward Gauss-Seidel sweep from y = 0 (PAPER.md:689-690);
-    A is banded with half-bandwidth bw (B-splines of degree p: bw = p)."""
+def gs_row(Ab: np.ndarray, b: np.ndarray, y: np.ndarray, i: int, p: int) -> float:
+    """One Gauss-Seidel row update: (b_i - sum_{j != i} A_ij y_j) / A_ii, the
+    terms subtracted in ascending j over the band (R27)."""
     n = len(b)
-    y = np.zeros(n)
-    for i in range(n):
-        s = b[i]
-        for j in range(max(0, i - bw), min(n, i + bw + 1)):
-            if j != i:
-                s -= A[i, j] * y[j]
-        y[i] = s / A[i, i]
+    s = b[i]
+    for k in range(2 * p + 1):
+        j = i - p + k
+        if k != p and 0 <= j < n:
+            s = s - Ab[i, k] * y[j]
+    return s / Ab[i, p]
+
+
+def lex_gs(Ab: np.ndarray, b: np.ndarray, p: int) -> np.ndarray:
+    """One forward (lexicographic) Gauss-Seidel sweep from y = 0
+    (PAPER.md:689-690, 1624)."""
+    y = np.zeros(len(b))
+    for i in range(len(b)):
+        y[i] = gs_row(Ab, b, y, i, p)
+    return y
+
+
+def mc_gs(Ab: np.ndarray, b: np.ndarray, p: int) -> np.ndarray:
+    """One multicolour Gauss-Seidel sweep from y = 0 (§8(f) N1 carried to 1D):
+    colours c = 0..p, rows i = c mod (p+1) in ascending colour order.  Rows of
+    one colour are more than p apart, so they do not couple and the sweep is
+    parallel within a colour."""
+    y = np.zeros(len(b))
+    for c in range(p + 1):
+        for i in range(c, len(b), p + 1):
+            y[i] = gs_row(Ab, b, y, i, p)
     return y
 
 
 class CFMG1D:
-    """Alg 3.3 in 1D with B-splines, m in {1, 2}."""
+    """Alg 3.3 in 1D with B-splines, m in {1, 2}.
+    smoother: "lex" (the paper's lexicographic Gauss-Seidel) or "mcgs"."""
 
-    def __init__(self, p, m, levels, N, b1, b2, f):
+    def __init__(self, p, m, levels, N, b1, b2, f, smoother="lex"):
+        assert smoother in ("lex", "mcgs")
         self.p, self.m, self.levels, self.N, self.b1, self.b2 = p, m, levels, N, b1, b2
+        self.smoother = smoother
         self.lv = [assemble(p, m, l) for l in range(levels)]
         self.P = [None] + [two_scale(self.lv[l], self.lv[l - 1]) for l in range(1, levels)]
-        self.f = [load(lv, f) for lv in self.lv]
+        self.f = [load(lv, f) for lv in self.lv] if callable(f) else [np.asarray(v, dtype=float) for v in f]
+        # operators in the GPU layouts (R27); P entries outside the support
+        # structure are the L2 solve's rounding noise and are dropped
+        self.Ab = [band(lv.K, p) for lv in self.lv]
+        self.Pe = [None]
+        self.Re = [None]
+        for l in range(1, levels):
+            st = two_scale_structure(self.lv[l], self.lv[l - 1])
+            self.Pe.append(ell(self.P[l], st))
+            self.Re.append(ell_transpose(self.P[l], st, len(self.lv[l - 1].free)))
+        self.A0inv = np.linalg.inv(self.lv[0].K)
 
     def wu(self, l, L):
         return self.b1 + (self.p + 1) * (L - l)
@@ -222,17 +342,23 @@ class CFMG1D:
     def wr(self, l, L):
         return self.b2 + self.m * (L - l)
 
+    def prolong(self, l, x):
+        return ell_mv(*self.Pe[l], x)
+
+    def restrict(self, l, x):
+        return ell_mv(*self.Re[l], x)
+
     def std(self, secs, L):
         """Standard representation of a compact vector: u_l = dec ú_l + P_l u_{l-1}."""
         u = dec(secs[0])
         for l in range(1, L + 1):
-            u = dec(secs[l]) + self.P[l] @ u
+            u = dec(secs[l]) + self.prolong(l, u)
         return u
 
     def solve(self, Lstop=None):
         L0 = self.levels - 1 if Lstop is None else Lstop
         # coarse-grid solve PAPER.md:785-786
-        u0 = np.linalg.solve(self.lv[0].K, self.f[0])
+        u0 = dense_mv(self.A0inv, self.f[0])
         self.u = [enc(u0, self.wu(0, 0))]
         self.sols = {0: dec(self.u[0])}
         for L in range(1, L0 + 1):
@@ -243,25 +369,29 @@ class CFMG1D:
         return self.sols
 
     def iteration(self, L):
+        p = self.p
         # fmgResidual (Alg 3.2): t_L = f_L - A_L u_L, r_l = enc R ... R t_L
         uL = self.std(self.u, L)
-        t = self.f[L] - self.lv[L].K @ uL
+        t = self.f[L] - band_mv(self.Ab[L], uL, p)
         r = [None] * (L + 1)
         r[L] = enc(t, self.wr(L, L))
         for l in range(L - 1, -1, -1):
-            t = self.P[l + 1].T @ t
+            t = self.restrict(l + 1, t)
             r[l] = enc(t, self.wr(l, L))
         # cFas V(0,1) from zero (Alg 3.1)
         y = [None] * (L + 1)
-        y0 = np.linalg.solve(self.lv[0].K, dec(r[0]))
+        y0 = dense_mv(self.A0inv, dec(r[0]))
         y[0] = enc(y0, self.wr(0, L))
         w = dec(y[0])
+        gs = lex_gs if self.smoother == "lex" else mc_gs
         for l in range(1, L + 1):
-            z = self.P[l] @ w
-            b = dec(r[l]) - self.lv[l].K @ z
-            yl = lex_gs(self.lv[l].K, b, self.p)
+            z = self.prolong(l, w)
+            b = dec(r[l]) - band_mv(self.Ab[l], z, p)
+            yl = gs(self.Ab[l], b, p)
             y[l] = enc(yl, self.wr(l, L))
             w = z + dec(y[l])
+        self.y = y
+        self.r = r
         # correction PAPER.md:798
         for l in range(L + 1):
             self.u[l] = enc(dec(self.u[l]) + dec(y[l]), self.wu(l, L))

@@ -102,3 +102,91 @@ def test_wide_widths_reach_the_discrete_solution():
     lv = s.lv[5]
     ud = np.linalg.solve(lv.K, s.f[5])
     assert np.max(np.abs(sols[5] - ud)) < 1e-11 * np.max(np.abs(ud))
+
+
+# ---------------------------------------------- operator layouts (R27) --
+
+@pytest.mark.parametrize("p,m", [(1, 1), (2, 1), (3, 1), (3, 2), (5, 2), (7, 2)])
+def test_layouts_reproduce_the_dense_operators(p, m):
+    """band / ELL storage and their canonical products against dense numpy
+    products; the entries of P dropped outside the support structure are
+    rounding noise of the L2 solve."""
+    f, c = B.assemble(p, m, 4), B.assemble(p, m, 3)
+    P = B.two_scale(f, c)
+    st = B.two_scale_structure(f, c)
+    mask = np.zeros_like(P, dtype=bool)
+    for i, (j0, j1) in enumerate(st):
+        mask[i, j0:j1 + 1] = True
+    assert np.max(np.abs(P[~mask])) < 1e-12  # genuine coefficients are >= 2^-p
+    # interior rows: a fine support, (p+1)/2 coarse elements long and starting
+    # at a coarse knot or a midpoint, lies in the supports starting at the
+    # coarse knots j in [a - (p+1)/2, a]: (p+1)/2 or (p+3)/2 of them for odd p,
+    # p/2 + 1 for even p; near the ends the open knots widen it, never past p + 1
+    wid = [j1 - j0 + 1 for j0, j1 in st]
+    n = len(wid)
+    inner = {(p + 1) // 2, (p + 3) // 2} if p % 2 else {p // 2 + 1}
+    assert set(wid[n // 4: 3 * n // 4]) == inner and max(wid) <= p + 1
+    rng = np.random.default_rng(p + 10 * m)
+    xc = rng.standard_normal(P.shape[1])
+    xf = rng.standard_normal(P.shape[0])
+    Pv, c0 = B.ell(P, st)
+    Rv, r0 = B.ell_transpose(P, st, P.shape[1])
+    Pm = np.where(mask, P, 0.0)
+    assert np.allclose(B.ell_mv(Pv, c0, xc), Pm @ xc, rtol=0, atol=1e-14)
+    assert np.allclose(B.ell_mv(Rv, r0, xf), Pm.T @ xf, rtol=0, atol=1e-14)
+    Ab = B.band(f.K, p)
+    x = rng.standard_normal(f.K.shape[0])
+    assert np.allclose(B.band_mv(Ab, x, p), f.K @ x, rtol=1e-13, atol=1e-13 * np.abs(f.K).max())
+    A = rng.standard_normal((5, 7))
+    assert np.allclose(B.dense_mv(A, x[:7]), A @ x[:7], rtol=1e-14, atol=1e-14)
+
+
+def test_p1_two_scale_closed_form():
+    # linear B-splines: coarse hat j = fine hats (1/2, 1, 1/2) around node 2j+1
+    f, c = B.assemble(1, 1, 3), B.assemble(1, 1, 2)
+    st = B.two_scale_structure(f, c)
+    Pv, c0 = B.ell(B.two_scale(f, c), st)
+    P = np.zeros((len(f.free), len(c.free)))
+    for j in range(len(c.free)):
+        P[2 * j, j], P[2 * j + 1, j], P[2 * j + 2, j] = 0.5, 1.0, 0.5
+    for i in range(len(f.free)):
+        for k in range(Pv.shape[1]):
+            if c0[i] + k < len(c.free):
+                assert abs(Pv[i, k] - P[i, c0[i] + k]) < 1e-15
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_gauss_seidel_sweeps_are_triangular_solves(p):
+    """From y = 0 a lexicographic GS sweep solves (D + L) y = b; the multicolour
+    sweep does the same on the colour-permuted system."""
+    from scipy.linalg import solve_triangular
+    lv = B.assemble(p, 1 if p < 3 else 2, 4)
+    K = lv.K
+    n = K.shape[0]
+    b = np.random.default_rng(p).standard_normal(n)
+    Ab = B.band(K, p)
+    y = B.lex_gs(Ab, b, p)
+    assert np.allclose(y, solve_triangular(np.tril(K), b, lower=True), rtol=1e-12, atol=1e-12)
+    perm = np.concatenate([np.arange(c, n, p + 1) for c in range(p + 1)])
+    Kp = K[np.ix_(perm, perm)]
+    yp = solve_triangular(np.tril(Kp), b[perm], lower=True)
+    ym = B.mc_gs(Ab, b, p)
+    assert np.allclose(ym[perm], yp, rtol=1e-12, atol=1e-12)
+    assert not np.allclose(ym, y)  # the two orders differ
+
+
+@pytest.mark.parametrize("m,p", [(1, 1), (1, 3), (2, 3), (2, 5)])
+def test_multicolour_gs_meets_eq73(m, p):
+    """The GPU-parallel multicolour sweep keeps the Table-3 rows' accuracy
+    (Eq 7.3) with one more IR iteration than the paper's lexicographic sweep."""
+    row = dict(GOLD["poisson_1d" if m == 1 else "biharmonic_1d"][str(p)])
+    row["N"] += 1
+    uf, ff = (B.poisson_u, B.poisson_f) if m == 1 else (B.biharm_u, B.biharm_f)
+    Ltop = min(6, (53 - row["b3"]) // (p + m + 1))
+    s = B.CFMG1D(p, m, Ltop + 1, row["N"], row["b1"], row["b2"], ff, smoother="mcgs")
+    sols = s.solve()
+    for L in range(4, Ltop + 1):
+        lv = s.lv[L]
+        ec = B.hm_error(lv, sols[L], uf, m)
+        ed = B.hm_error(lv, np.linalg.solve(lv.K, s.f[L]), uf, m)
+        assert ec <= 2 * ed, (L, ec / ed)
