@@ -40,13 +40,19 @@ def knots(p: int, nel: int) -> np.ndarray:
     return np.concatenate([np.zeros(p + 1), inner, np.ones(p + 1)])
 
 
+def span(t: np.ndarray, p: int, x: float) -> int:
+    """Span index s with t[s] <= x < t[s+1] (x = 1 belongs to the last span);
+    only B-splines s-p .. s are nonzero at x."""
+    n = len(t) - p - 1
+    s = np.searchsorted(t, x, side="right") - 1
+    return int(min(max(s, p), n - 1))
+
+
 def basis_all(t: np.ndarray, p: int, x: float, nder: int) -> np.ndarray:
     """Values and derivatives (rows 0..nder) of all n = len(t)-p-1 B-splines
     at x, by the Cox-de Boor recursion and its derivative formula."""
     n = len(t) - p - 1
-    # span index s with t[s] <= x < t[s+1] (x = 1 belongs to the last span)
-    s = np.searchsorted(t, x, side="right") - 1
-    s = min(max(s, p), n - 1)
+    s = span(t, p, x)
     # degree-0 .. degree-p values on the span (standard triangular table)
     N = np.zeros((p + 1, p + 1))
     N[0, 0] = 1.0
@@ -132,8 +138,11 @@ def assemble(p: int, m: int, l: int) -> Level:
             x = a + 0.5 * h * (xg[q] + 1.0)
             w = 0.5 * h * wg[q]
             B = basis_all(t, p, x, m)
-            K += w * np.outer(B[m], B[m])
-            M += w * np.outer(B[0], B[0])
+            # only the (p+1) x (p+1) block of the functions nonzero at x: the
+            # other products are exact zeros, which leave every sum unchanged
+            sl = slice(span(t, p, x) - p, span(t, p, x) + 1)
+            K[sl, sl] += w * np.outer(B[m][sl], B[m][sl])
+            M[sl, sl] += w * np.outer(B[0][sl], B[0][sl])
     return Level(p, m, l, nel, t, n_all, free, K[np.ix_(free, free)], M)
 
 
@@ -162,7 +171,11 @@ def two_scale(fine: Level, coarse: Level) -> np.ndarray:
         for q in range(len(xg)):
             x = a + 0.5 * h * (xg[q] + 1.0)
             w = 0.5 * h * wg[q]
-            Mfc += w * np.outer(basis_all(fine.t, fine.p, x, 0)[0], basis_all(coarse.t, coarse.p, x, 0)[0])
+            sf = span(fine.t, fine.p, x)
+            sc = span(coarse.t, coarse.p, x)
+            fs = slice(sf - fine.p, sf + 1)
+            cs = slice(sc - coarse.p, sc + 1)
+            Mfc[fs, cs] += w * np.outer(basis_all(fine.t, fine.p, x, 0)[0][fs], basis_all(coarse.t, coarse.p, x, 0)[0][cs])
     Pall = np.linalg.solve(fine.M_all, Mfc)
     return Pall[np.ix_(fine.free, coarse.free)]
 
@@ -218,13 +231,15 @@ def two_scale_structure(fine: Level, coarse: Level):
     so the comparisons are exact."""
     p, m = fine.p, fine.m
     nf, nc = len(fine.free), len(coarse.free)
+    lo = coarse.t[m: m + nc]                   # coarse supports [lo_j, hi_j]
+    hi = coarse.t[m + p + 1: m + p + 1 + nc]
     out = []
     for i in range(nf):
         I = i + m
         a, b = fine.t[I], fine.t[I + p + 1]
-        js = [j for j in range(nc) if coarse.t[j + m] <= a and b <= coarse.t[j + m + p + 1]]
-        assert js == list(range(js[0], js[-1] + 1))
-        out.append((js[0], js[-1]))
+        js = np.nonzero((lo <= a) & (b <= hi))[0]
+        assert np.array_equal(js, np.arange(js[0], js[-1] + 1))
+        out.append((int(js[0]), int(js[-1])))
     return out
 
 
@@ -241,7 +256,9 @@ def ell(P: np.ndarray, st) -> tuple:
 def ell_transpose(P: np.ndarray, st, nc: int) -> tuple:
     """R = P^T in ELL form: for coarse j the fine rows i with j in st[i],
     ascending."""
-    rows = [[i for i, (j0, j1) in enumerate(st) if j0 <= j <= j1] for j in range(nc)]
+    j0s = np.array([a for a, _ in st])
+    j1s = np.array([b for _, b in st])
+    rows = [np.nonzero((j0s <= j) & (j <= j1s))[0].tolist() for j in range(nc)]
     kr = max(len(r) for r in rows)
     vals = np.zeros((nc, kr))
     r0 = np.array([r[0] for r in rows], dtype=np.int64)

@@ -376,3 +376,156 @@ def bfp_status(stream=None) -> int:
     import torch
     st = _stream_ptr(stream if stream is not None else torch.cuda.current_stream())
     return _lib.bfp_status(st)
+
+
+# ------------------------------------------------- 1D B-spline FMG (N4) --
+# include/fmg1d.h: the paper's 1D Poisson / biharmonic workloads, a batch of
+# problems per launch (one CTA per problem).  Marshalling only.
+FMG1D_LEX, FMG1D_MCGS = 0, 1
+
+
+class Schedule1D(C.Structure):
+    _fields_ = [("N", C.c_int), ("b1", C.c_int), ("b2", C.c_int), ("smoother", C.c_int)]
+
+
+_PP = C.POINTER(_vp)
+_lib.fmg1d_size.argtypes = [C.c_int, C.c_int, C.c_int]
+_lib.fmg1d_ell_width.argtypes = [C.c_int, C.c_int, C.c_int]
+_lib.fmg1d_assemble_operator.argtypes = [C.c_int, C.c_int, C.c_int, _vp]
+_lib.fmg1d_assemble_prolongation.argtypes = [C.c_int, C.c_int, C.c_int, _vp]
+_lib.fmg1d_assemble_load.argtypes = [C.c_int, C.c_int, C.c_int, _vp]
+_lib.fmg1d_create.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule1D), C.c_int, _PP, _PP, _vp, _vp,
+                              C.POINTER(_vp)]
+_lib.fmg1d_destroy.argtypes = [_vp]
+_lib.fmg1d_set_load.argtypes = [_vp, _PP]
+_lib.fmg1d_solve_async.argtypes = [_vp]
+_lib.fmg1d_sync.argtypes = [_vp]
+_lib.fmg1d_solve_host.argtypes = [_vp, _PP, _vp]
+_lib.fmg1d_solution.argtypes = [_vp, C.c_int, _vp]
+_lib.fmg1d_solution_device.argtypes = [_vp, C.POINTER(_vp)]
+_lib.fmg1d_section.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, C.POINTER(C.c_int)]
+
+EXPORTS += ["fmg1d_size", "fmg1d_ell_width", "fmg1d_assemble_operator", "fmg1d_assemble_prolongation",
+            "fmg1d_assemble_load", "fmg1d_create", "fmg1d_destroy", "fmg1d_set_load", "fmg1d_solve_async",
+            "fmg1d_sync", "fmg1d_solve_host", "fmg1d_solution", "fmg1d_solution_device", "fmg1d_section"]
+
+
+def fmg1d_size(p: int, m: int, l: int) -> int:
+    n = _lib.fmg1d_size(p, m, l)
+    if n < 0:
+        raise FmgError(FMG_EINVAL, "fmg1d_size")
+    return n
+
+
+def fmg1d_operator(p: int, m: int, l: int):
+    """Native band of A_l, shape (n_l, 2p+1) (host assembly)."""
+    import numpy as np
+    a = np.zeros((fmg1d_size(p, m, l), 2 * p + 1))
+    _check(_lib.fmg1d_assemble_operator(p, m, l, a.ctypes.data), "fmg1d_assemble_operator")
+    return a
+
+
+def fmg1d_prolongation(p: int, m: int, l: int):
+    """Native ELL values of P_l, shape (n_l, kp_l) (host assembly)."""
+    import numpy as np
+    a = np.zeros((fmg1d_size(p, m, l), _lib.fmg1d_ell_width(p, m, l)))
+    _check(_lib.fmg1d_assemble_prolongation(p, m, l, a.ctypes.data), "fmg1d_assemble_prolongation")
+    return a
+
+
+def fmg1d_load(p: int, m: int, l: int):
+    """Native load vector of the paper's manufactured problem at level l."""
+    import numpy as np
+    a = np.zeros(fmg1d_size(p, m, l))
+    _check(_lib.fmg1d_assemble_load(p, m, l, a.ctypes.data), "fmg1d_assemble_load")
+    return a
+
+
+def _ptr_array(arrs):
+    return (_vp * len(arrs))(*[None if a is None else a.ctypes.data for a in arrs])
+
+
+class Solver1D:
+    """A batch of 1D B-spline compact-FMG problems (fmg1d_create ... fmg1d_destroy).
+    Ab / Pv / A0inv: operator arrays in the layouts of include/fmg1d.h, or None
+    for the library's native assembly."""
+
+    def __init__(self, p: int, m: int, levels: int, N: int, b1: int, b2: int, smoother: str = "lex",
+                 batch: int = 1, Ab=None, Pv=None, A0inv=None, stream=None):
+        import numpy as np
+        self.p, self.m, self.levels, self.batch = p, m, levels, batch
+        self.n = [fmg1d_size(p, m, l) for l in range(levels)]
+        self.sched = Schedule1D(N, b1, b2, FMG1D_LEX if smoother == "lex" else FMG1D_MCGS)
+        keep = []
+        ab = pv = None
+        if Ab is not None:
+            keep += [np.ascontiguousarray(a, dtype=np.float64) for a in Ab]
+            ab = _ptr_array(keep[-len(Ab):])
+        if Pv is not None:
+            pvs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in Pv]
+            keep += [a for a in pvs if a is not None]
+            pv = _ptr_array(pvs)
+        a0 = None
+        if A0inv is not None:
+            a0 = np.ascontiguousarray(A0inv, dtype=np.float64)
+            keep.append(a0)
+        h = _vp()
+        _check(_lib.fmg1d_create(p, m, levels, C.byref(self.sched), batch, ab, pv,
+                                 None if a0 is None else a0.ctypes.data, _stream_ptr(stream), C.byref(h)),
+               "fmg1d_create")
+        self._h = h
+
+    def set_load(self, f):
+        """f[l]: (batch, n_l) or (n_l,) (broadcast over the batch) host arrays."""
+        import numpy as np
+        self._f = [np.ascontiguousarray(np.broadcast_to(np.asarray(v, dtype=np.float64), (self.batch, self.n[l])))
+                   for l, v in enumerate(f)]
+        _check(_lib.fmg1d_set_load(self._h, _ptr_array(self._f)), "fmg1d_set_load")
+
+    def solve_async(self):
+        _check(_lib.fmg1d_solve_async(self._h), "fmg1d_solve_async")
+
+    def sync(self):
+        _check(_lib.fmg1d_sync(self._h), "fmg1d_sync")
+
+    def solve(self):
+        self.solve_async()
+        self.sync()
+
+    def solve_host(self, f, out=None):
+        """End to end: host loads in, host solutions (batch, n_L) out."""
+        import numpy as np
+        self._f = [np.ascontiguousarray(np.broadcast_to(np.asarray(v, dtype=np.float64), (self.batch, self.n[l])))
+                   for l, v in enumerate(f)]
+        if out is None:
+            out = np.zeros((self.batch, self.n[-1]))
+        _check(_lib.fmg1d_solve_host(self._h, _ptr_array(self._f), out.ctypes.data), "fmg1d_solve_host")
+        return out
+
+    def solution(self, b: int = 0):
+        import numpy as np
+        u = np.zeros(self.n[-1])
+        _check(_lib.fmg1d_solution(self._h, b, u.ctypes.data), "fmg1d_solution")
+        return u
+
+    def section(self, which: int, l: int, b: int = 0):
+        """(mant, exps, w) of section which (0 u, 1 r, 2 y) at level l."""
+        import numpy as np
+        nblk = (self.n[l] + 31) // 32
+        mant = np.zeros(nblk * 64, dtype=np.uint32)
+        exps = np.zeros(nblk, dtype=np.int8)
+        w = C.c_int()
+        _check(_lib.fmg1d_section(self._h, which, l, b, mant.ctypes.data, exps.ctypes.data, C.byref(w)),
+               "fmg1d_section")
+        return mant[: nblk * w.value], exps, w.value
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.fmg1d_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

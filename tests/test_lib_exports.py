@@ -1,5 +1,5 @@
 """CPU checks of the C-ABI boundary: libfmg.so loads (no GPU needed for dlopen)
-and exports every function include/fmg.h declares; the oracle library builds.
+and exports every function include/*.h declares; the oracle library builds.
 No compute calls are made here."""
 import ctypes
 import os
@@ -9,15 +9,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_functions():
-    src = open(os.path.join(ROOT, "include", "fmg.h")).read()
+    inc = os.path.join(ROOT, "include")
+    src = "".join(open(os.path.join(inc, h)).read() for h in sorted(os.listdir(inc)) if h.endswith(".h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     names = re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\**(\w+)\s*\(", src, flags=re.M)
-    return sorted(set(n for n in names if n.startswith(("fmg_", "bfp_"))))
+    return sorted(set(n for n in names if n.startswith(("fmg_", "bfp_", "fmg1d_"))))
 
 
 def test_header_declares_boundary():
     names = declared_functions()
-    for n in ["fmg_create", "fmg_solve", "fmg_residual", "bfp_encode", "bfp_decode", "fmg_destroy"]:
+    for n in ["fmg_create", "fmg_solve", "fmg_residual", "bfp_encode", "bfp_decode", "fmg_destroy",
+              "fmg1d_create", "fmg1d_solve_async", "fmg1d_section", "fmg1d_assemble_operator"]:
         assert n in names
 
 
