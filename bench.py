@@ -263,6 +263,138 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(out))
 
 
+# ------------------------------------------------------------------ N4 --
+# the paper's 1D B-spline workloads (include/fmg1d.h), a
+# batch of independent problems per launch (one CTA per problem).  Default:
+# 1D Poisson, p = 1, Table 3's row (N = 4, b1 = 5, b2 = 3),
+# L = 15 (n_L = 65535, inside FP64's range b3 + (p+m+1) L <= 53), batch 592 =
+# 4 problems per SM, the paper's lexicographic Gauss-Seidel.
+N4_ROWS = {(1, 1): (4, 5, 3), (2, 1): (3, 5, 4), (3, 1): (4, 7, 4), (4, 1): (5, 8, 4), (5, 1): (9, 9, 5),
+           (3, 2): (6, 4, 4), (4, 2): (4, 6, 4), (5, 2): (5, 8, 5), (6, 2): (5, 11, 5), (7, 2): (11, 12, 6)}
+
+
+def n4_alg_bytes(p, m, levels, N, b1, b2):
+    """Algorithmic bytes of one 1D solve: per IR iteration at
+    FMG level L, f_L (8 B/DoF) plus, per level l <= L, the compact sections the
+    method reads and writes -- u_l read twice (standard form, correction) and
+    written once, r_l written and read, y_l written and read twice (cFas,
+    correction): (3 w_u + 5 w_r) / 8 B/DoF -- and the final solution (8 B/DoF)."""
+    n = [(1 << (l + 1)) + p - 2 * m for l in range(levels)]
+    tot = 0.0
+    for L in range(1, levels):
+        per_it = 8 * n[L] + sum(n[l] * (3 * (b1 + (p + 1) * (L - l)) + 5 * (b2 + m * (L - l))) / 8
+                                for l in range(L + 1))
+        tot += N * per_it
+    return tot + 8 * n[-1]
+
+
+def run_n4(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2511_19036_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    p, m, levels, batch = args.n4_p, args.n4_m, args.n4_levels, args.n4_batch
+    N, b1, b2 = N4_ROWS[(p, m)]
+    stream = torch.cuda.current_stream()
+    s = P.Solver1D(p, m, levels, N, b1, b2, smoother=args.n4_smoother, batch=batch, stream=stream)
+    loads = [P.fmg1d_load(p, m, l) for l in range(levels)]
+    # distinct problems: problem b solves with load (1 + b / batch) f
+    scale = 1.0 + np.arange(batch)[:, None] / batch
+    fb = [np.ascontiguousarray(scale * v[None, :]) for v in loads]
+    s.set_load(fb)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        s.solve_async()
+    s.sync()
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        tdist.barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    times = []
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.solve_async()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    s.sync()
+    if dist:
+        tdist.barrier()
+    ck = clocks.stop()
+    ms = reduce_max(sum(times) / len(times), dev)
+    # end to end: pinned host loads in, host solutions out, every step
+    fpin = [torch.from_numpy(v).pin_memory() for v in fb]
+    fnp = [t.numpy() for t in fpin]
+    upin = torch.empty((batch, s.n[-1]), dtype=torch.float64).pin_memory()
+    e2e = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s.solve_host(fnp, upin.numpy())
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = reduce_max(sum(e2e) / len(e2e), dev)
+    if rank != 0:
+        return
+    hbm, hbm_src = peaks()
+    byts = n4_alg_bytes(p, m, levels, N, b1, b2) * batch
+    unk = s.n[-1] * batch
+    roof = {"bound": "hbm", "achieved": byts / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "peak_source": hbm_src, "traffic": args.traffic,
+            "kernel": f"k_fmg1d<{p}> (the whole batched solve is one launch)",
+            "avg_launch_ms": ms, "alg_bytes_per_launch": byts,
+            "note": "compact-section bytes only (DESIGN.md §12); the lexicographic sweep is a "
+                    "sequential latency chain per problem, so the fraction is low by construction"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    out = {
+        "metric": METRIC,
+        "value": unk * world / (ms * 1e-3),
+        "unit": "DoF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the paper's manufactured 1D problems, loads scaled per problem; no dataset)",
+        "config": {"workload": f"N4: 1D {'Poisson' if m == 1 else 'biharmonic'} B-spline p={p}, "
+                               f"{levels} levels, batch {batch}, {args.n4_smoother} GS",
+                   "p": p, "m": m, "levels": levels, "batch": batch, "unknowns_per_problem": s.n[-1],
+                   "schedule": {"N": N, "b1": b1, "b2": b2, "smoother": args.n4_smoother},
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": roof,
+        "e2e": {"value": unk * world / (e2e_ms * 1e-3), "unit": "DoF/s",
+                "h2d_bytes_per_step": int(sum(v.nbytes for v in fb)), "d2h_bytes_per_step": int(upin.numel() * 8),
+                "ms_per_step": e2e_ms},
+        "gpu_launches": args.steps,
+        "clocks": ck,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = n4_oracle_sample(p, m, levels, args.n4_smoother)[0]
+    print(json.dumps(out))
+
+
+def n4_oracle_sample(p, m, levels, smoother):
+    """The oracle (oracle/bspline1d.py) on one problem of the workload, with
+    fewer levels when the full depth would exceed ~20 s; solve time only."""
+    import oracle.bspline1d as B
+    N, b1, b2 = N4_ROWS[(p, m)]
+    lev = min(levels, 12)
+    o = B.CFMG1D(p, m, lev, N, b1, b2, B.poisson_f if m == 1 else B.biharm_f, smoother=smoother)
+    t0 = time.perf_counter()
+    o.solve()
+    dt = time.perf_counter() - t0
+    n = len(o.f[-1])
+    return ({"value": n / dt, "unit": "DoF/s", "cores": 1, "kind": "oracle",
+             "sample": f"one 1D solve, p={p} m={m}, {lev} levels ({n} unknowns), {dt:.2f} s (solve only)"}, dt)
+
+
 def cpu_baseline(config, smoother="chebyshev", nu=1):
     import oracle as O
     cfg = CONFIGS[config]
@@ -333,12 +465,36 @@ def main():
                     help="compact V(0,1) cycles per IR iteration (SURVEY 8f N2; GPU: 2D, Chebyshev)")
     ap.add_argument("--smoother", default="chebyshev", choices=["chebyshev", "mcgs"],
                     help="cFas smoother: Chebyshev-Jacobi (default) or multicolour Gauss-Seidel (SURVEY 8f N1)")
+    ap.add_argument("--workload", default="fmg", choices=["fmg", "n4"],
+                    help="fmg: the 2D/3D compact FMG (--config); n4: the 1D B-spline batch (SURVEY 8f N4)")
+    ap.add_argument("--n4-p", type=int, default=1)
+    ap.add_argument("--n4-m", type=int, default=1)
+    ap.add_argument("--n4-levels", type=int, default=16)
+    ap.add_argument("--n4-batch", type=int, default=592)
+    ap.add_argument("--n4-smoother", default="lex", choices=["lex", "mcgs"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
+        if args.workload == "n4":
+            if rank == 0:
+                base, dt0 = n4_oracle_sample(args.n4_p, args.n4_m, args.n4_levels, args.n4_smoother)
+                ts = [n4_oracle_sample(args.n4_p, args.n4_m, args.n4_levels, args.n4_smoother)[1]
+                      for _ in range(args.steps)]
+                v = base["value"] * dt0 / (sum(ts) / len(ts))  # same problem each step
+                print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "DoF/s",
+                                  "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                                  "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True,
+                                  "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                                  "data": "synthetic (manufactured 1D problem)",
+                                  "config": {"workload": "N4 1D B-spline (oracle sample)", "p": args.n4_p,
+                                             "m": args.n4_m, "levels": args.n4_levels},
+                                  "cpu_baseline": dict(base, value=v),
+                                  "e2e": {"value": v, "unit": "DoF/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}))
+            return
         run_reference(args, rank, world)
         return
     if world > 1:
@@ -347,7 +503,10 @@ def main():
         torch.cuda.set_device(local_rank)
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.workload == "n4":
+            run_n4(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as tdist

@@ -162,4 +162,4 @@ def test_non_finite_load_reports_erange():
     s.solve_async()
     with pytest.raises(P.FmgError) as e:
         s.sync()
-    assert e.value.args[0] == P.FMG_ERANGE
+    assert e.value.code == P.FMG_ERANGE
