@@ -49,9 +49,10 @@ __device__ __forceinline__ void encode_level(const double* x, int n, int nblk, u
   }
 }
 
-template <int P>
-__global__ void __launch_bounds__(NT1) k_fmg1d(const __grid_constant__ Args1 a) {
+template <int P, bool LEX>
+__global__ void __launch_bounds__(NT1, 4) k_fmg1d(const __grid_constant__ Args1 a) {
   constexpr int W = 2 * P + 1;
+  __shared__ __align__(16) double gsb[LEX ? 2 * 32 * (W + 1) : 1];  // lexicographic sweep staging
   const int b = blockIdx.x, tid = threadIdx.x;
   const int nL = a.nL, Lmax = a.levels - 1;
   const double* f = a.f + (long long)b * a.ftot;
@@ -190,23 +191,61 @@ __global__ void __launch_bounds__(NT1) k_fmg1d(const __grid_constant__ Args1 a) 
         }
         __syncthreads();
         // one Gauss-Seidel sweep from zero
-        if (a.smoother == FMG1D_LEX) {
-          if (tid == 0) {
+        if constexpr (LEX) {
+          // The sequential chain runs in warp 0 over 32-row chunks: the warp
+          // stages chunk c+32's b and band rows into shared memory with
+          // cp.async (coalesced, behind the chain), lane j then holds row
+          // c+j, every lane evaluates its own row against the shared window
+          // y_{i-P..i-1}, and the shuffle from lane j yields y_{c+j}.  The
+          // chain itself carries no global memory access.
+          if (tid < 32) {
+            const int lane = tid;
             double win[P];  // y_{i-P} .. y_{i-1}
 #pragma unroll
             for (int k = 0; k < P; ++k) win[k] = 0.0;
-            for (int i = 0; i < v.n; ++i) {
-              const double* ar = v.Ab + (long long)i * W;
-              double s = Bv[i];
+            auto stage = [&](int c, int slot) {
+              double* sb = gsb + slot * 32 * (W + 1);
+              if (c < v.n) {
+                const int cnt = min(32, v.n - c);
+                fmg::cpa8(sb + lane, lane < cnt ? Bv + c + lane : Bv, lane < cnt);
+                const double* src = v.Ab + (long long)c * W;
 #pragma unroll
-              for (int k = 0; k < P; ++k)
-                if (i - P + k >= 0) s = s - ar[k] * win[k];
-              const double yi = s / ar[P];
-              Y[i] = yi;
+                for (int q = 0; q < W; ++q) {
+                  const int t = lane + 32 * q;
+                  fmg::cpa8(sb + 32 + t, t < cnt * W ? src + t : src, t < cnt * W);
+                }
+              }
+              asm volatile("cp.async.commit_group;\n" ::: "memory");
+            };
+            stage(0, 0);
+            int slot = 0;
+            for (int c = 0; c < v.n; c += 32, slot ^= 1) {
+              stage(c + 32, slot ^ 1);
+              asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+              __syncwarp();
+              const double* sb = gsb + slot * 32 * (W + 1);
+              const double bq = sb[lane];
+              double aq[P];
 #pragma unroll
-              for (int k = 0; k < P - 1; ++k) win[k] = win[k + 1];
-              win[P - 1] = yi;
+              for (int k = 0; k < P; ++k) aq[k] = sb[32 + lane * W + k];
+              const double dq = sb[32 + lane * W + P];
+              const int cnt = min(32, v.n - c);
+              double ymine = 0.0;
+              for (int j = 0; j < cnt; ++j) {
+                double s = bq;
+#pragma unroll
+                for (int k = 0; k < P; ++k)
+                  if (c + j - P + k >= 0) s = s - aq[k] * win[k];
+                const double y = __shfl_sync(FULL, s / dq, j);
+                if (lane == j) ymine = y;
+#pragma unroll
+                for (int k = 0; k < P - 1; ++k) win[k] = win[k + 1];
+                win[P - 1] = y;
+              }
+              if (lane < cnt) Y[c + lane] = ymine;
+              __syncwarp();  // the slot is restaged two chunks later
             }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
           }
           __syncthreads();
         } else {
@@ -285,6 +324,12 @@ void release(fmg1d_ctx* c) {
 }
 
 }  // namespace
+
+template <int P>
+void launch(fmg1d_ctx* c) {
+  if (c->a.smoother == FMG1D_LEX) k_fmg1d<P, true><<<c->batch, NT1, 0, c->st>>>(c->a);
+  else k_fmg1d<P, false><<<c->batch, NT1, 0, c->st>>>(c->a);
+}
 
 extern "C" {
 
@@ -428,13 +473,13 @@ int fmg1d_solve_async(fmg1d_ctx* c) {
   if (!c) return FMG_EINVAL;
   if (cudaMemsetAsync(c->a.status, 0, sizeof(int), c->st) != cudaSuccess) return FMG_ECUDA;
   switch (c->p) {
-    case 1: k_fmg1d<1><<<c->batch, NT1, 0, c->st>>>(c->a); break;
-    case 2: k_fmg1d<2><<<c->batch, NT1, 0, c->st>>>(c->a); break;
-    case 3: k_fmg1d<3><<<c->batch, NT1, 0, c->st>>>(c->a); break;
-    case 4: k_fmg1d<4><<<c->batch, NT1, 0, c->st>>>(c->a); break;
-    case 5: k_fmg1d<5><<<c->batch, NT1, 0, c->st>>>(c->a); break;
-    case 6: k_fmg1d<6><<<c->batch, NT1, 0, c->st>>>(c->a); break;
-    default: k_fmg1d<7><<<c->batch, NT1, 0, c->st>>>(c->a); break;
+    case 1: launch<1>(c); break;
+    case 2: launch<2>(c); break;
+    case 3: launch<3>(c); break;
+    case 4: launch<4>(c); break;
+    case 5: launch<5>(c); break;
+    case 6: launch<6>(c); break;
+    default: launch<7>(c); break;
   }
   return cudaGetLastError() == cudaSuccess ? FMG_OK : FMG_ECUDA;
 }
