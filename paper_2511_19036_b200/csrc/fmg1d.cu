@@ -29,8 +29,14 @@
 namespace fmg1d {
 using fmg::FULL;
 
-constexpr int NT1 = 256;  // threads per CTA (8 warps)
-constexpr int NW1 = NT1 / 32;
+// Threads per CTA: 256 for the multicolour sweep (every phase is parallel);
+// 128 for the lexicographic one, whose sequential chain runs in one warp --
+// smaller CTAs put 8 chains on an SM (measured: 64 threads / 16 chains is
+// slower, the parallel phases become latency-bound).
+template <bool LEX>
+constexpr int kThreads = LEX ? 128 : 256;
+template <bool LEX>
+constexpr int kMinBlocks = LEX ? 8 : 4;
 
 __device__ __forceinline__ double dec_at(const uint32_t* words, const int8_t* exps, int stride, int w, int i) {
   return fmg::point_decode(words + (long long)(i >> 5) * stride, exps[i >> 5], w, i & 31);
@@ -38,6 +44,7 @@ __device__ __forceinline__ double dec_at(const uint32_t* words, const int8_t* ex
 
 // Encode x[0..n) (zero-padded to the block boundary; x == nullptr: all zero)
 // into a section of width w.  If zv != nullptr, wv[i] = zv[i] + (quantised x_i).
+template <int NW1>
 __device__ __forceinline__ void encode_level(const double* x, int n, int nblk, uint32_t* words, int stride,
                                              int8_t* exps, int w, const double* zv, double* wv, int* status) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -50,8 +57,9 @@ __device__ __forceinline__ void encode_level(const double* x, int n, int nblk, u
 }
 
 template <int P, bool LEX>
-__global__ void __launch_bounds__(NT1, 4) k_fmg1d(const __grid_constant__ Args1 a) {
+__global__ void __launch_bounds__(kThreads<LEX>, kMinBlocks<LEX>) k_fmg1d(const __grid_constant__ Args1 a) {
   constexpr int W = 2 * P + 1;
+  constexpr int NT1 = kThreads<LEX>, NW1 = NT1 / 32;
   __shared__ __align__(16) double gsb[LEX ? 2 * 32 * (W + 1) : 1];  // lexicographic sweep staging
   const int b = blockIdx.x, tid = threadIdx.x;
   const int nL = a.nL, Lmax = a.levels - 1;
@@ -142,14 +150,14 @@ __global__ void __launch_bounds__(NT1, 4) k_fmg1d(const __grid_constant__ Args1 
   if (tid < kMaxLevels) wcur[tid] = 0;
   coarse_mv(f + a.foff[0], X0);
   __syncthreads();
-  encode_level(X0, n0, a.lv[0].nblk, U(0), a.lv[0].ustride, UE(0), wu(0, 0), nullptr, nullptr, a.status);
+  encode_level<NW1>(X0, n0, a.lv[0].nblk, U(0), a.lv[0].ustride, UE(0), wu(0, 0), nullptr, nullptr, a.status);
   if (tid == 0) wcur[0] = wu(0, 0);
   __syncthreads();
 
   for (int L = 1; L <= Lmax; ++L) {
     const Level1& vL = a.lv[L];
     // push level: u_L = 0
-    encode_level(nullptr, vL.n, vL.nblk, U(L), vL.ustride, UE(L), wu(L, L), nullptr, nullptr, a.status);
+    encode_level<NW1>(nullptr, vL.n, vL.nblk, U(L), vL.ustride, UE(L), wu(L, L), nullptr, nullptr, a.status);
     if (tid == 0) wcur[L] = wu(L, L);
     __syncthreads();
     for (int it = 0; it < a.N; ++it) {
@@ -158,12 +166,12 @@ __global__ void __launch_bounds__(NT1, 4) k_fmg1d(const __grid_constant__ Args1 
       const double* fL = f + a.foff[L];
       for (int i = tid; i < vL.n; i += NT1) T0[i] = fL[i] - band_row(vL, uL, i);
       __syncthreads();
-      encode_level(T0, vL.n, vL.nblk, Rs(L), vL.rstride, RE(L), wr(L, L), nullptr, nullptr, a.status);
+      encode_level<NW1>(T0, vL.n, vL.nblk, Rs(L), vL.rstride, RE(L), wr(L, L), nullptr, nullptr, a.status);
       double *tc = T0, *tn = T1;
       for (int l = L - 1; l >= 0; --l) {
         restrict_(l, tc, tn);
         __syncthreads();
-        encode_level(tn, a.lv[l].n, a.lv[l].nblk, Rs(l), a.lv[l].rstride, RE(l), wr(l, L), nullptr, nullptr,
+        encode_level<NW1>(tn, a.lv[l].n, a.lv[l].nblk, Rs(l), a.lv[l].rstride, RE(l), wr(l, L), nullptr, nullptr,
                      a.status);
         double* t = tc;
         tc = tn;
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(NT1, 4) k_fmg1d(const __grid_constant__ Args1 
       double* Wv = X0;  // w_l (the std buffers are free now)
       for (int i = tid; i < n0; i += NT1) Z[i] = 0.0;
       __syncthreads();
-      encode_level(Y, n0, a.lv[0].nblk, Ys(0), a.lv[0].rstride, YE(0), wr(0, L), Z, Wv, a.status);
+      encode_level<NW1>(Y, n0, a.lv[0].nblk, Ys(0), a.lv[0].rstride, YE(0), wr(0, L), Z, Wv, a.status);
       __syncthreads();
       for (int l = 1; l <= L; ++l) {
         const Level1& v = a.lv[l];
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(NT1, 4) k_fmg1d(const __grid_constant__ Args1 
           }
         }
         // y_l = enc y; w = z + dec y_l
-        encode_level(Y, v.n, v.nblk, Ys(l), v.rstride, YE(l), wr(l, L), Z, Wv, a.status);
+        encode_level<NW1>(Y, v.n, v.nblk, Ys(l), v.rstride, YE(l), wr(l, L), Z, Wv, a.status);
         __syncthreads();
       }
       // ---- correction u_l = enc(dec u_l + dec y_l) at w_u(l, L)
@@ -327,8 +335,8 @@ void release(fmg1d_ctx* c) {
 
 template <int P>
 void launch(fmg1d_ctx* c) {
-  if (c->a.smoother == FMG1D_LEX) k_fmg1d<P, true><<<c->batch, NT1, 0, c->st>>>(c->a);
-  else k_fmg1d<P, false><<<c->batch, NT1, 0, c->st>>>(c->a);
+  if (c->a.smoother == FMG1D_LEX) k_fmg1d<P, true><<<c->batch, kThreads<true>, 0, c->st>>>(c->a);
+  else k_fmg1d<P, false><<<c->batch, kThreads<false>, 0, c->st>>>(c->a);
 }
 
 extern "C" {
