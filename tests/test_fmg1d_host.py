@@ -70,3 +70,27 @@ def test_create_validates_before_any_device_call():
     bad = P.Schedule1D(4, 5, 3, 7)
     assert lib.fmg1d_create(3, 1, 4, C.byref(bad), 1, None, None, None, None, C.byref(h)) == P.FMG_EINVAL
     assert lib.fmg1d_size(3, 3, 2) == -1 and lib.fmg1d_ell_width(3, 1, 0) == -1
+
+
+def test_bench_n4_alg_bytes_by_hand():
+    """bench.py's N4 roofline numerator on a two-level case,
+    counted by hand: p = 1, m = 1, levels 2 (n_0 = 1, n_1 = 3), N = 2, b1 = 5,
+    b2 = 3.  One FMG level L = 1 with two iterations; per iteration f_1
+    (8 * 3 B) plus, for l = 0 (w_u = 5 + 2 = 7, w_r = 3 + 1 = 4) and l = 1
+    (w_u = 5, w_r = 3), n_l (3 w_u + 5 w_r) / 8; then the final solution."""
+    import bench
+    per_it = 8 * 3 + 1 * (3 * 7 + 5 * 4) / 8 + 3 * (3 * 5 + 5 * 3) / 8
+    assert bench.n4_alg_bytes(1, 1, 2, 2, 5, 3) == 2 * per_it + 8 * 3
+    assert bench.N4_ROWS[(1, 1)] == (4, 5, 3) and bench.N4_ROWS[(7, 2)] == (11, 12, 6)
+
+
+def test_bench_n4_rows_are_table3():
+    """The N4 bench schedules are Table 3's 1D rows (tests/golden)."""
+    import json
+    import os
+    import bench
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table3_poisson.json")))
+    for m, key in ((1, "poisson_1d"), (2, "biharmonic_1d")):
+        for p, row in g[key].items():
+            if not p.startswith("_"):
+                assert bench.N4_ROWS[(int(p), m)] == (row["N"], row["b1"], row["b2"])
