@@ -276,8 +276,8 @@ def run_ours(args, rank, world, local_rank):
 # batch of independent problems per launch (one CTA per problem).  Default:
 # 1D Poisson, p = 1, Table 3's row (N = 4, b1 = 5, b2 = 3),
 # L = 15 (n_L = 65535, inside FP64's range b3 + (p+m+1) L <= 53), the paper's
-# lexicographic Gauss-Seidel, batch 1184 = 8 problems per SM (one 128-thread
-# CTA each).
+# lexicographic Gauss-Seidel, batch 4736 = 32 problems per SM (one warp
+# each).
 N4_ROWS = {(1, 1): (4, 5, 3), (2, 1): (3, 5, 4), (3, 1): (4, 7, 4), (4, 1): (5, 8, 4), (5, 1): (9, 9, 5),
            (3, 2): (6, 4, 4), (4, 2): (4, 6, 4), (5, 2): (5, 8, 5), (6, 2): (5, 11, 5), (7, 2): (11, 12, 6)}
 
@@ -306,8 +306,10 @@ def run_n4(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     p, m, levels, batch = args.n4_p, args.n4_m, args.n4_levels, args.n4_batch
-    if batch is None:  # fill the resident CTAs once
-        batch = 148 * (8 if args.n4_smoother == "lex" else 4)
+    if batch is None:  # fill the resident problems once: 32 per SM
+        # with one warp per problem, 4 per SM with a 256-thread CTA per problem
+        warp_per_problem = args.n4_smoother == "lex" or (1 << levels) + p - 2 * m <= 2048
+        batch = 148 * (32 if warp_per_problem else 4)
     N, b1, b2 = N4_ROWS[(p, m)]
     stream = torch.cuda.current_stream()
     s = P.Solver1D(p, m, levels, N, b1, b2, smoother=args.n4_smoother, batch=batch, stream=stream)
@@ -482,7 +484,7 @@ def main():
     ap.add_argument("--n4-m", type=int, default=1)
     ap.add_argument("--n4-levels", type=int, default=16)
     ap.add_argument("--n4-batch", type=int, default=None,
-                    help="problems per launch (default: 8 per SM lexicographic, 4 per SM multicolour)")
+                    help="problems per launch (default: one resident wave, DESIGN.md §12)")
     ap.add_argument("--n4-smoother", default="lex", choices=["lex", "mcgs"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -7,7 +7,7 @@
 // (n_L ~ 10^3 - 10^4 at the FP64-representable depths, reading R26) are far
 // too small to spread over the GPU, so the batch dimension fills the 148 SMs
 // and the whole solve is ONE launch; the phases inside are separated by
-// __syncthreads, the working vectors stay in L1/L2.
+// group barriers (gsync), the working vectors stay in L1/L2.
 //
 // Arithmetic (reading R27, bit-identical to oracle/bspline1d.py): every row of
 // a product is summed from 0.0 in ascending storage index; the encode / decode
@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -33,10 +34,24 @@ using fmg::FULL;
 // 128 for the lexicographic one, whose sequential chain runs in one warp --
 // smaller CTAs put 8 chains on an SM (measured: 64 threads / 16 chains is
 // slower, the parallel phases become latency-bound).
-template <bool LEX>
-constexpr int kThreads = LEX ? 128 : 256;
-template <bool LEX>
-constexpr int kMinBlocks = LEX ? 8 : 4;
+// TP = threads per problem; a CTA of kCta<TP> threads holds kCta / TP problems
+// (TP = 32: one warp per problem, all syncs are __syncwarp).
+template <int TP>
+constexpr int kCta = TP < 128 ? 128 : TP;
+template <int TP>
+constexpr int kMinBlocks = TP == 256 ? 4 : 8;
+
+// barrier of one problem's thread group
+template <int TP>
+__device__ __forceinline__ void gsync(int grp) {
+  if constexpr (TP == 32) {
+    __syncwarp();
+  } else if constexpr (TP == kCta<TP>) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(TP) : "memory");
+  }
+}
 
 __device__ __forceinline__ double dec_at(const uint32_t* words, const int8_t* exps, int stride, int w, int i) {
   return fmg::point_decode(words + (long long)(i >> 5) * stride, exps[i >> 5], w, i & 31);
@@ -45,9 +60,9 @@ __device__ __forceinline__ double dec_at(const uint32_t* words, const int8_t* ex
 // Encode x[0..n) (zero-padded to the block boundary; x == nullptr: all zero)
 // into a section of width w.  If zv != nullptr, wv[i] = zv[i] + (quantised x_i).
 template <int NW1>
-__device__ __forceinline__ void encode_level(const double* x, int n, int nblk, uint32_t* words, int stride,
+__device__ __forceinline__ void encode_level(int tid, const double* x, int n, int nblk, uint32_t* words, int stride,
                                              int8_t* exps, int w, const double* zv, double* wv, int* status) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   for (int blk = warp; blk < nblk; blk += NW1) {
     const int i = blk * 32 + lane;
     const double v = (x && i < n) ? x[i] : 0.0;
@@ -56,12 +71,17 @@ __device__ __forceinline__ void encode_level(const double* x, int n, int nblk, u
   }
 }
 
-template <int P, bool LEX>
-__global__ void __launch_bounds__(kThreads<LEX>, kMinBlocks<LEX>) k_fmg1d(const __grid_constant__ Args1 a) {
+template <int P, bool LEX, int TP>
+__global__ void __launch_bounds__(kCta<TP>, kMinBlocks<TP>) k_fmg1d(const __grid_constant__ Args1 a) {
   constexpr int W = 2 * P + 1;
-  constexpr int NT1 = kThreads<LEX>, NW1 = NT1 / 32;
-  __shared__ __align__(16) double gsb[LEX ? 2 * 32 * (W + 1) : 1];  // lexicographic sweep staging
-  const int b = blockIdx.x, tid = threadIdx.x;
+  constexpr int NT1 = TP, NW1 = NT1 / 32, GPC = kCta<TP> / TP;
+  __shared__ __align__(16) double gsb_all[GPC][LEX ? 2 * 32 * (W + 1) : 1];  // lexicographic sweep staging
+  __shared__ int wcur_all[GPC][kMaxLevels];  // current width of each u section
+  const int grp = threadIdx.x / TP, tid = threadIdx.x % TP;
+  const int b = blockIdx.x * GPC + grp;
+  if (b >= a.batch) return;  // (whole groups only: no barrier is shared across groups)
+  double* gsb = gsb_all[grp];
+  int* wcur = wcur_all[grp];
   const int nL = a.nL, Lmax = a.levels - 1;
   const double* f = a.f + (long long)b * a.ftot;
   uint32_t* um = a.umant + (long long)b * a.mwords_u;
@@ -78,7 +98,6 @@ __global__ void __launch_bounds__(kThreads<LEX>, kMinBlocks<LEX>) k_fmg1d(const 
   double* Bv = X0 + 5 * nL;
   double* Y = X0 + 6 * nL;
   double* D = X0 + 7 * nL;
-  __shared__ int wcur[kMaxLevels];  // current width of each u section
   const int n0 = a.lv[0].n;
   auto wu = [&](int l, int L) { return a.b1 + (P + 1) * (L - l); };
   auto wr = [&](int l, int L) { return a.b2 + a.m * (L - l); };
@@ -134,11 +153,11 @@ __global__ void __launch_bounds__(kThreads<LEX>, kMinBlocks<LEX>) k_fmg1d(const 
   // standard form u_L = dec u_L + P_L(... dec u_0) into the returned buffer
   auto std_form = [&](int L) -> double* {
     for (int i = tid; i < n0; i += NT1) X0[i] = dec_at(U(0), UE(0), a.lv[0].ustride, wcur[0], i);
-    __syncthreads();
+    gsync<TP>(grp);
     double *cur = X0, *nxt = X1;
     for (int l = 1; l <= L; ++l) {
       prolong(l, cur, nxt, true);
-      __syncthreads();
+      gsync<TP>(grp);
       double* t = cur;
       cur = nxt;
       nxt = t;
@@ -149,55 +168,55 @@ __global__ void __launch_bounds__(kThreads<LEX>, kMinBlocks<LEX>) k_fmg1d(const 
   // ---- coarse-grid solve u_0 = A_0^-1 f_0
   if (tid < kMaxLevels) wcur[tid] = 0;
   coarse_mv(f + a.foff[0], X0);
-  __syncthreads();
-  encode_level<NW1>(X0, n0, a.lv[0].nblk, U(0), a.lv[0].ustride, UE(0), wu(0, 0), nullptr, nullptr, a.status);
+  gsync<TP>(grp);
+  encode_level<NW1>(tid, X0, n0, a.lv[0].nblk, U(0), a.lv[0].ustride, UE(0), wu(0, 0), nullptr, nullptr, a.status);
   if (tid == 0) wcur[0] = wu(0, 0);
-  __syncthreads();
+  gsync<TP>(grp);
 
   for (int L = 1; L <= Lmax; ++L) {
     const Level1& vL = a.lv[L];
     // push level: u_L = 0
-    encode_level<NW1>(nullptr, vL.n, vL.nblk, U(L), vL.ustride, UE(L), wu(L, L), nullptr, nullptr, a.status);
+    encode_level<NW1>(tid, nullptr, vL.n, vL.nblk, U(L), vL.ustride, UE(L), wu(L, L), nullptr, nullptr, a.status);
     if (tid == 0) wcur[L] = wu(L, L);
-    __syncthreads();
+    gsync<TP>(grp);
     for (int it = 0; it < a.N; ++it) {
       // ---- fmgResidual (Alg 3.2): t_L = f_L - A_L u_L; r_l = enc R..R t_L
       const double* uL = std_form(L);
       const double* fL = f + a.foff[L];
       for (int i = tid; i < vL.n; i += NT1) T0[i] = fL[i] - band_row(vL, uL, i);
-      __syncthreads();
-      encode_level<NW1>(T0, vL.n, vL.nblk, Rs(L), vL.rstride, RE(L), wr(L, L), nullptr, nullptr, a.status);
+      gsync<TP>(grp);
+      encode_level<NW1>(tid, T0, vL.n, vL.nblk, Rs(L), vL.rstride, RE(L), wr(L, L), nullptr, nullptr, a.status);
       double *tc = T0, *tn = T1;
       for (int l = L - 1; l >= 0; --l) {
         restrict_(l, tc, tn);
-        __syncthreads();
-        encode_level<NW1>(tn, a.lv[l].n, a.lv[l].nblk, Rs(l), a.lv[l].rstride, RE(l), wr(l, L), nullptr, nullptr,
+        gsync<TP>(grp);
+        encode_level<NW1>(tid, tn, a.lv[l].n, a.lv[l].nblk, Rs(l), a.lv[l].rstride, RE(l), wr(l, L), nullptr, nullptr,
                      a.status);
         double* t = tc;
         tc = tn;
         tn = t;
       }
-      __syncthreads();
+      gsync<TP>(grp);
       // ---- cFas V(0,1) from zero (Alg 3.1): y_0 = A_0^-1 r_0, w = dec y_0
       for (int i = tid; i < n0; i += NT1) D[i] = dec_at(Rs(0), RE(0), a.lv[0].rstride, wr(0, L), i);
-      __syncthreads();
+      gsync<TP>(grp);
       coarse_mv(D, Y);
-      __syncthreads();
+      gsync<TP>(grp);
       double* Wv = X0;  // w_l (the std buffers are free now)
       for (int i = tid; i < n0; i += NT1) Z[i] = 0.0;
-      __syncthreads();
-      encode_level<NW1>(Y, n0, a.lv[0].nblk, Ys(0), a.lv[0].rstride, YE(0), wr(0, L), Z, Wv, a.status);
-      __syncthreads();
+      gsync<TP>(grp);
+      encode_level<NW1>(tid, Y, n0, a.lv[0].nblk, Ys(0), a.lv[0].rstride, YE(0), wr(0, L), Z, Wv, a.status);
+      gsync<TP>(grp);
       for (int l = 1; l <= L; ++l) {
         const Level1& v = a.lv[l];
         // z = P_l w; b = dec r_l - A_l z; y = 0
         prolong(l, Wv, Z, false);
-        __syncthreads();
+        gsync<TP>(grp);
         for (int i = tid; i < v.n; i += NT1) {
           Bv[i] = dec_at(Rs(l), RE(l), v.rstride, wr(l, L), i) - band_row(v, Z, i);
           Y[i] = 0.0;
         }
-        __syncthreads();
+        gsync<TP>(grp);
         // one Gauss-Seidel sweep from zero
         if constexpr (LEX) {
           // The sequential chain runs in warp 0 over 32-row chunks: the warp
@@ -255,7 +274,7 @@ __global__ void __launch_bounds__(kThreads<LEX>, kMinBlocks<LEX>) k_fmg1d(const 
             }
             asm volatile("cp.async.wait_all;\n" ::: "memory");
           }
-          __syncthreads();
+          gsync<TP>(grp);
         } else {
           for (int c = 0; c <= P; ++c) {
             for (int i = c + (P + 1) * tid; i < v.n; i += (P + 1) * NT1) {
@@ -268,12 +287,12 @@ __global__ void __launch_bounds__(kThreads<LEX>, kMinBlocks<LEX>) k_fmg1d(const 
               }
               Y[i] = s / ar[P];
             }
-            __syncthreads();
+            gsync<TP>(grp);
           }
         }
         // y_l = enc y; w = z + dec y_l
-        encode_level<NW1>(Y, v.n, v.nblk, Ys(l), v.rstride, YE(l), wr(l, L), Z, Wv, a.status);
-        __syncthreads();
+        encode_level<NW1>(tid, Y, v.n, v.nblk, Ys(l), v.rstride, YE(l), wr(l, L), Z, Wv, a.status);
+        gsync<TP>(grp);
       }
       // ---- correction u_l = enc(dec u_l + dec y_l) at w_u(l, L)
       {
@@ -288,9 +307,9 @@ __global__ void __launch_bounds__(kThreads<LEX>, kMinBlocks<LEX>) k_fmg1d(const 
             fmg::warp_encode(s, wu(l, L), U(l) + (long long)blk * v.ustride, UE(l) + blk, lane, a.status);
           }
         }
-        __syncthreads();
+        gsync<TP>(grp);
         if (tid <= L) wcur[tid] = wu(tid, L);
-        __syncthreads();
+        gsync<TP>(grp);
       }
     }
   }
@@ -305,6 +324,7 @@ using namespace fmg1d;
 
 struct fmg1d_ctx {
   int p = 0, m = 0, levels = 0, batch = 0;
+  int tp = 0;  // threads per problem
   fmg1d_schedule s{};
   cudaStream_t st = nullptr;
   std::vector<void*> allocs;
@@ -333,10 +353,22 @@ void release(fmg1d_ctx* c) {
 
 }  // namespace
 
+template <int P, bool LEX, int TP>
+void launch_tp(fmg1d_ctx* c) {
+  constexpr int GPC = kCta<TP> / TP;
+  k_fmg1d<P, LEX, TP><<<(c->batch + GPC - 1) / GPC, kCta<TP>, 0, c->st>>>(c->a);
+}
+// Threads per problem: env FMG1D_TP in {32, 128, 256}
 template <int P>
 void launch(fmg1d_ctx* c) {
-  if (c->a.smoother == FMG1D_LEX) k_fmg1d<P, true><<<c->batch, kThreads<true>, 0, c->st>>>(c->a);
-  else k_fmg1d<P, false><<<c->batch, kThreads<false>, 0, c->st>>>(c->a);
+  const int tp = c->tp;
+  if (c->a.smoother == FMG1D_LEX) {
+    if (tp == 32) launch_tp<P, true, 32>(c);
+    else launch_tp<P, true, 128>(c);
+  } else {
+    if (tp == 32) launch_tp<P, false, 32>(c);
+    else launch_tp<P, false, 256>(c);
+  }
 }
 
 extern "C" {
@@ -357,7 +389,13 @@ int fmg1d_create(int p, int m, int levels, const fmg1d_schedule* s, int batch, c
   c->batch = batch;
   c->s = *s;
   c->st = (cudaStream_t)stream;
+  // threads per problem (measured): one warp for the
+  // lexicographic sweep and for small problems (n_L <= 2048), a 256-thread CTA
+  // for the multicolour sweep on large ones; FMG1D_TP = 32 / 128 / 256 forces it
+  c->tp = (s->smoother == FMG1D_LEX || n_unknowns(p, m, levels - 1) <= 2048) ? 32 : 256;
+  if (const char* e = getenv("FMG1D_TP")) c->tp = atoi(e) == 32 ? 32 : (s->smoother == FMG1D_LEX ? 128 : 256);
   Args1& a = c->a;
+  a.batch = batch;
   a.p = p;
   a.m = m;
   a.levels = levels;

@@ -37,6 +37,7 @@ struct Level1 {
 
 struct Args1 {
   int p, m, levels, N, b1, b2, smoother;
+  int batch;
   Level1 lv[kMaxLevels];
   const double* A0inv;   // n0 x n0
   const double* f;       // batch x ftot (b-major; level l at foff[l])

@@ -10,8 +10,11 @@ import torch
 
 import paper_2511_19036_b200 as P
 
+CFGS_ENV = os.environ.get("N4_CFGS")
 CFGS = [(1, 1, 16, "lex", 1184), (1, 1, 16, "lex", 2368), (1, 1, 16, "mcgs", 592), (1, 1, 12, "lex", 2368),
         (1, 1, 12, "mcgs", 1184), (3, 1, 10, "lex", 2368), (5, 2, 7, "lex", 2368), (5, 2, 7, "mcgs", 1184)]
+if CFGS_ENV:  # "p,m,levels,smoother,batch;..."
+    CFGS = [(int(a), int(b), int(c), d, int(e)) for a, b, c, d, e in (x.split(",") for x in CFGS_ENV.split(";"))]
 ROWS = {(1, 1): (4, 5, 3), (3, 1): (4, 7, 4), (5, 2): (5, 8, 5)}
 st = torch.cuda.Stream()
 for p, m, levels, sm, batch in CFGS:
