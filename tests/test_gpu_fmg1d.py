@@ -163,3 +163,23 @@ def test_non_finite_load_reports_erange():
     with pytest.raises(P.FmgError) as e:
         s.sync()
     assert e.value.code == P.FMG_ERANGE
+
+
+@pytest.mark.parametrize("tp", ["32", "256"])
+@pytest.mark.parametrize("smoother", ["lex", "mcgs"])
+@pytest.mark.parametrize("m,p,levels", [(1, 1, 9), (2, 5, 5), (1, 3, 7)])
+def test_thread_layouts_bit_exact(monkeypatch, tp, smoother, m, p, levels):
+    """Both thread layouts (one warp per problem; one CTA per problem:
+    FMG1D_TP) give the oracle's bits, batched with distinct loads."""
+    _need_gpu()
+    monkeypatch.setenv("FMG1D_TP", tp)
+    r = _row(m, p)
+    o = B.CFMG1D(p, m, levels, r["N"], r["b1"], r["b2"], B.poisson_f if m == 1 else B.biharm_f, smoother=smoother)
+    o.solve()
+    rng = np.random.default_rng(11)
+    other = [rng.standard_normal(len(v)) for v in o.f]
+    o2 = B.CFMG1D(p, m, levels, r["N"], r["b1"], r["b2"], other, smoother=smoother)
+    o2.solve()
+    s = _gpu_from_oracle(o, batch=5, loads=[np.stack([a, b, a, b, a]) for a, b in zip(o.f, other)])
+    for b in range(5):
+        _compare(o if b % 2 == 0 else o2, s, b)
