@@ -221,7 +221,8 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": hbm_src}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = args.traffic
-    if args.traffic is None:  # the committed ncu capture of this kernel (profiles/traffic.json)
+    if args.traffic is None and args.smoother == "chebyshev" and args.nu == 1:
+        # the committed ncu capture of this kernel (profiles/traffic.json)
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
                 t = json.load(fh)[args.config][str(args.roofline_class)]
