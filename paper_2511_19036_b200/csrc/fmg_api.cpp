@@ -934,6 +934,15 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       rst[l] = c->r[l].stride;
     }
     if (kc_plan(dim, p, Lmax, c->g, ust, rst, s->n_ir, lc_cap, &c->kcl, &c->lc, &c->kc_cluster)) rc = FMG_ECUDA;
+    // Measured (profiles/r1e_summary.md): KC beats the
+    // PDL-chained grid kernels only when it runs the whole FMG in one launch
+    // (lc = Lmax, e.g. C1). Otherwise, on one GPU, its levels 1..lc go to the
+    // grid path and KC keeps the coarse solve (C2 -6 %, C3 -1.3 %, C4 flat).
+    // Slab contexts keep the plan: their grid levels need NZ % G == 0.
+    // FMG_LC overrides.
+    else if (!getenv("FMG_LC") && G == 1 && c->lc > 0 && c->lc < Lmax) {
+      if (kc_plan(dim, p, Lmax, c->g, ust, rst, s->n_ir, 0, &c->kcl, &c->lc, &c->kc_cluster)) rc = FMG_ECUDA;
+    }
     c->kc_tw = c->kc_cluster * kc_warps_per_cta();
   }
   // z slabs: rank r owns planes [r NZ/G, (r+1) NZ/G) of every grid level l > lc

@@ -361,3 +361,20 @@ def test_fmg_parity_C4_full_oracle(P):
     error within 1e-3."""
     c = CONFIGS["C4"]
     compare_solvers(P, c["dim"], c["p"], c["levels"], check_r=False)
+
+
+@pytest.mark.parametrize("lc", ["1", "2", "3"])
+@pytest.mark.parametrize("d,p,levels", [(2, 2, 7), (2, 1, 8), (3, 1, 6), (3, 2, 5)])
+def test_kc_per_iteration_mode_parity(P, monkeypatch, lc, d, p, levels):
+    """KC's per-iteration mode (levels 0..lc of each IR iteration at L > lc).
+    On one GPU the default plan keeps KC either for the whole FMG or for the
+    coarse solve only, so FMG_LC forces the split here; the
+    multi-GPU slab plans use it by default."""
+    monkeypatch.setenv("FMG_LC", lc)
+    compare_solvers(P, d, p, levels)
+
+
+@pytest.mark.parametrize("d,p,levels", [(2, 2, 7), (3, 1, 6)])
+def test_kc_per_iteration_mode_parity_mcgs(P, monkeypatch, d, p, levels):
+    monkeypatch.setenv("FMG_LC", "2")
+    compare_solvers(P, d, p, levels, smoother="mcgs")
