@@ -345,7 +345,11 @@ void build_iteration_nu(Builder& b, int L, int it) {
 
 void build_iteration(Builder& b, int L, int it) {
   fmg_ctx* c = b.c;
-  if (c->s.nu > 1) {
+  // nu > 1, or KC kept for the initial coarse solve only (one GPU, lc = 0):
+  // every level of the iteration is a grid op, level 0 through cFas1 +
+  // k_coarse_nu (with nu = 1 its one cycle has guess = store = 0, i.e. the
+  // plain V(0,1) cycle of Alg 3.1)
+  if (c->s.nu > 1 || (c->lc == 0 && c->G == 1 && c->march)) {  // (the tile-box path has no level-0 grid ops)
     build_iteration_nu(b, L, it);
     return;
   }
