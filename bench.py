@@ -230,7 +230,9 @@ def run_ours(args, rank, world, local_rank):
             roof["traffic_source"] = t["source"]
         except (OSError, KeyError, ValueError):
             pass
-    roof["kernel"] = {0: "k_op OP_RESIDUAL (fine level)", 5: "k_op OP_CHEB final step (fine level)"}[args.roofline_class]
+    roof["kernel"] = {0: "k_op OP_RESIDUAL (fine level)",
+                      5: ("k_m_gs final colour step (fine level)" if args.smoother == "mcgs"
+                          else "k_op OP_CHEB final step (fine level)")}[args.roofline_class]
     roof["avg_launch_ms"] = avg_launch_ms
     roof["launches_timed"] = klaunch
     roof["alg_flops_per_launch"] = flops
