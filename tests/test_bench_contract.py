@@ -1,0 +1,60 @@
+"""The driver's bench.py contract: one JSON line with the required keys.
+The reference arm (the CPU oracle) runs here; the GPU arms are marked gpu."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _run(args, timeout=600):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT, capture_output=True,
+                         text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--workload", "n4", "--n4-levels", "8", "--steps", "1", "--warmup", "3"])
+    assert BASE_KEYS <= set(d) and d["impl"] == "reference"
+    assert d["value"] > 0 and d["unit"] == "DoF/s" and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def _check_gpu_line(d):
+    assert BASE_KEYS <= set(d)
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["warmup"] >= 3
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "alu", "tensor") and 0 < r["frac"] < 1 and r["peak"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert "sm_mhz" in d["clocks"] and isinstance(d["clocks"]["reasons"], list)
+
+
+@pytest.mark.gpu
+def test_default_line():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    d = _run(["--steps", "2", "--warmup", "3"])
+    _check_gpu_line(d)
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["config"]["workload"].startswith("C2")
+
+
+@pytest.mark.gpu
+def test_n4_line():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    d = _run(["--workload", "n4", "--n4-levels", "10", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"])
+    _check_gpu_line(d)
+    assert d["config"]["workload"].startswith("N4")
