@@ -4,11 +4,13 @@ One step = one full compact FMG solve (Alg 3.3, all FMG levels, N IR
 iterations each: every §8(a) row S1-S11) of the configured workload, issued
 through the C-ABI (fmg_solve_async) with the context resident in HBM.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
 
-Default workload: configs[1] = C2 (2D Q2, 1024^2 elements, 10-level FMG).
-Multi-GPU: 2D configs do not shard (replicas only), so each rank
-solves its own instance; value = total unknowns solved per second (weak).
+Default workload: C4 (3D Q3, 256^3 elements, 8-level FMG), the largest
+configuration that runs on one GPU (BASELINE.json configs[3]; C5 needs 8).
+Multi-GPU: 3D configs run ONE problem in z slabs over the ranks (NCCL halo
+exchange, strong scaling); 2D configs do not shard (replicas
+only), so each rank solves its own instance (weak).
 --impl reference: the CPU oracle (oracle/, plain sequential C) on the same
 config, rank 0 only.
 """
@@ -110,10 +112,16 @@ def aggregate(unknowns_per_rank: int, world: int, ms_max: float) -> float:
 
 
 def kernel_model(cfg, sched, cls):
-    """Algorithmic FP64 flops and HBM bytes per launch of a fine-level kernel
-    (DESIGN.md §7), counted per stored point of the finest level from what the
-    march kernels (fmg_march*.cu) must read and write (halos, the second L2
-    touch of the staged operand and the encode's integer work not counted)."""
+    """Algorithmic work of one launch of the roofline kernel,
+    counted per stored point of the finest level at the finest FMG level:
+
+    * flops: FP64 operations of the canonical expression trees (DESIGN.md §3;
+      an FMA counts 2), halo recompute and the codec's integer work excluded;
+    * section bytes: only the compact sections the launch must
+      read or write at their widths at FMG level L = Lmax, plus one int8
+      exponent per 32-entry block.  FP64 temporaries are not algorithmic
+      bytes: §8(d) defines them as on-chip values.
+    Returns (flops, section_bytes)."""
     d, p, levels = cfg["dim"], cfg["p"], cfg["levels"]
     n = p << levels
     NX = (n + 31) // 32 * 32
@@ -122,15 +130,59 @@ def kernel_model(cfg, sched, cls):
     a_flops = (8 * t + 1) if d == 2 else (14 * t + 2)   # canonical A tree, FMA = 2 flops
     wr_b = sched["b_r"] / 8 + 1 / 32
     wu_b = sched["b_u"] / 8 + 1 / 32
-    if cls == 0:   # residual: u_L in, t_L out (FP64), r_L out; f = ((C g) g) g
+    if cls == 0:   # residual: t_L = f - A u_L (f = ((C g) g) g), r_L = enc(t_L) written
         flops = a_flops + (d - 1) + 2
-        byts = 8 + 8 + wr_b
-    else:          # cls 5: last Chebyshev step (finalise) at the finest level (l = L: no w_L, z_L):
-        # b in (staged, transformed to y_1 = inv_theta invD b), P u_{L-1} in, u_L out, ú_L in + out;
-        # y_1 (2), A y_1, q, d, y (5), w-free correction (2 adds)
+        byts = wr_b
+    else:          # cls 5: last Chebyshev step (finalise) at the finest level:
+        # y_1 = inv_theta invD b (2), A y_1, q, d, y (5), correction (2 adds); ú_L read + written
         flops = 2 + a_flops + 5 + 2
-        byts = 8 + 8 + 8 + 2 * wu_b
+        byts = 2 * wu_b
     return flops * pts, byts * pts
+
+
+KERNEL_LABEL = {(2, 0): "k_m_residual (fine level)", (3, 0): "k_m3_residual (fine level)",
+                (2, 5): "k_m_cheb final step (fine level)", (3, 5): "k_m3_cheb final step (fine level)"}
+
+
+def roofline_entry(cfg, sched, args, avg_launch_ms, launches, hbm, hbm_src):
+    """The contract's roofline object for the fine-level roofline kernel.  The
+    binding roof is the larger of the two model times: FP64 flops at the
+    derived FP64 peak (the 3D configs: "alu") or the §8(d) section bytes at
+    the measured HBM copy bandwidth."""
+    flops, byts = kernel_model(cfg, sched, args.roofline_class)
+    t_hbm = byts / (hbm * 1e9)
+    t_alu = flops / (FP64_PEAK_TFLOPS * 1e12)
+    sec = avg_launch_ms * 1e-3
+    if t_alu >= t_hbm:
+        roof = {"bound": "alu", "achieved": flops / sec / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "peak_source": "derived FP64: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §7; "
+                               "tools/fp64_peak.cu measured 34.0)"}
+    else:
+        roof = {"bound": "hbm", "achieved": byts / sec / 1e9, "peak": hbm, "unit": "GB/s",
+                "peak_source": hbm_src}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["hbm_section_frac"] = byts / sec / 1e9 / hbm
+    roof["traffic"] = args.traffic
+    if args.traffic is None and args.smoother == "chebyshev" and args.nu == 1:
+        # the committed ncu capture of this kernel (profiles/traffic.json)
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+                t = json.load(fh)[args.config][str(args.roofline_class)]
+            roof["traffic"] = t["bytes"]
+            roof["traffic_source"] = t["source"]
+            if "fp64_pipe_pct" in t:
+                roof["fp64_pipe_frac_ncu"] = t["fp64_pipe_pct"] / 100.0
+        except (OSError, KeyError, ValueError):
+            pass
+    label = KERNEL_LABEL[(cfg["dim"], args.roofline_class)]
+    if args.smoother == "mcgs" and args.roofline_class == 5:
+        label = label.replace("cheb final step", "gs final colour step")
+    roof["kernel"] = label
+    roof["avg_launch_ms"] = avg_launch_ms
+    roof["launches_timed"] = launches
+    roof["alg_flops_per_launch"] = flops
+    roof["section_bytes_per_launch"] = byts
+    return roof
 
 
 def run_ours(args, rank, world, local_rank):
@@ -154,7 +206,6 @@ def run_ours(args, rank, world, local_rank):
         solver = P.Solver(cfg["dim"], cfg["p"], cfg["levels"], sched, stream=stream, dist=(rank, world, uid[0]))
     else:
         solver = P.Solver(cfg["dim"], cfg["p"], cfg["levels"], sched, stream=stream)
-    solver.enable_kernel_timing(args.roofline_class)
     info_unk = unknowns(cfg["dim"], cfg["p"], cfg["levels"])
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -163,13 +214,16 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     solver.solve()  # error check (FMG_ERANGE) once before timing
     info = solver.info()
+    exp_ref = torch.empty(solver.export_size(), dtype=torch.uint8).pin_memory()
+    solver.export_solution(exp_ref)
+    stream.synchronize()
 
     dist = world > 1
     if dist:
         import torch.distributed as tdist
     clocks = Clocks(local_rank)
     clocks.start()
-    times, ktimes, klaunch = [], 0.0, 0
+    times = []
     if dist:
         tdist.barrier()
     torch.cuda.synchronize()
@@ -182,14 +236,30 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-        kt, kn = solver.kernel_time()
-        ktimes += kt
-        klaunch += kn
     torch.cuda.synchronize()
     if dist:
         tdist.barrier()
     ck = clocks.stop()
     ms = reduce_max(sum(times) / len(times), dev)
+    # every repeat is bit-identical: the compact solution after
+    # the timed solves equals the one before them, byte for byte
+    exp_chk = torch.empty_like(exp_ref)
+    solver.export_solution(exp_chk)
+    stream.synchronize()
+    repeat_identical = bool(torch.equal(exp_ref, exp_chk))
+
+    # ---- roofline kernel: CUDA events around each launch of its class, in a
+    # separate graph and OUTSIDE the timed region above (the events would
+    # otherwise sit inside the timed solves)
+    solver.enable_kernel_timing(args.roofline_class)
+    ktimes, klaunch = 0.0, 0
+    for _ in range(max(2, min(args.steps, 5))):
+        flush.zero_()
+        solver.solve_async()
+        kt, kn = solver.kernel_time()
+        ktimes += kt
+        klaunch += kn
+    solver.enable_kernel_timing(-1)
 
     # ---- end to end through the C-ABI with host buffers --------------------
     rhs_host = torch.from_numpy(solver.get_rhs()).pin_memory()
@@ -209,34 +279,8 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     hbm, hbm_src = peaks()
-    flops, byts = kernel_model(cfg, sched, args.roofline_class)
     avg_launch_ms = ktimes / max(klaunch, 1)
-    t_hbm = byts / (hbm * 1e9)
-    t_alu = flops / (FP64_PEAK_TFLOPS * 1e12)
-    if t_alu >= t_hbm:
-        roof = {"bound": "alu", "achieved": flops / (avg_launch_ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "peak_source": "derived FP64 (DESIGN.md §7); measured 34.0"}
-    else:
-        roof = {"bound": "hbm", "achieved": byts / (avg_launch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                "peak_source": hbm_src}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = args.traffic
-    if args.traffic is None and args.smoother == "chebyshev" and args.nu == 1:
-        # the committed ncu capture of this kernel (profiles/traffic.json)
-        try:
-            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-                t = json.load(fh)[args.config][str(args.roofline_class)]
-            roof["traffic"] = t["bytes"]
-            roof["traffic_source"] = t["source"]
-        except (OSError, KeyError, ValueError):
-            pass
-    roof["kernel"] = {0: "k_op OP_RESIDUAL (fine level)",
-                      5: ("k_m_gs final colour step (fine level)" if args.smoother == "mcgs"
-                          else "k_op OP_CHEB final step (fine level)")}[args.roofline_class]
-    roof["avg_launch_ms"] = avg_launch_ms
-    roof["launches_timed"] = klaunch
-    roof["alg_flops_per_launch"] = flops
-    roof["alg_bytes_per_launch"] = byts
+    roof = roofline_entry(cfg, sched, args, avg_launch_ms, klaunch, hbm, hbm_src)
 
     eff_gbs = info["alg_bytes_per_solve"] / (ms * 1e-3) / 1e9
     nrep = 1 if dist_slabs else world  # slabs: one problem on all ranks (strong); else replicas (weak)
@@ -267,6 +311,7 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": rhs_host.numel() * 8, "d2h_bytes_per_step": exp_host.numel(),
                 "ms_per_step": e2e_ms},
         "gpu_launches": int(info["launches_per_solve"]) * args.steps,
+        "repeat_bit_identical": repeat_identical,
         "clocks": ck,
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -471,14 +516,14 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--roofline-class", type=int, default=5, choices=[0, 5])
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the roofline kernel (profiles/)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nu", type=int, default=1,
-                    help="compact V(0,1) cycles per IR iteration (SURVEY 8f N2; GPU: 2D, Chebyshev)")
+                    help="compact V(0,1) cycles per IR iteration (SURVEY 8f N2; one GPU, 2D/3D, Chebyshev degree >= 2 or mcgs)")
     ap.add_argument("--smoother", default="chebyshev", choices=["chebyshev", "mcgs"],
                     help="cFas smoother: Chebyshev-Jacobi (default) or multicolour Gauss-Seidel (SURVEY 8f N1)")
     ap.add_argument("--workload", default="fmg", choices=["fmg", "n4"],

@@ -60,10 +60,12 @@ typedef struct {
   int smoother; /* 0: Chebyshev-Jacobi of degree cheb_degree (R4);
                    1: one multicolour Gauss-Seidel sweep, (p+1)^d colours
                    (the paper's smoother family PAPER.md:1624) */
-  int nu;       /* compact V(0,1) cycles per IR iteration (Alg 3.1, SURVEY §8f
-                   N2).  0 or 1: the method of Alg 3.3.  > 1 is defined by the
-                   oracle (reading R23) and is not implemented on the GPU yet:
-                   fmg_create returns FMG_EINVAL. */
+  int nu;       /* compact V(0,1) cycles per IR iteration (Alg 3.1 PAPER.md:
+                   633-661).  0 or 1: the method of Alg 3.3.
+                   2..8: the nonzero-guess cycles of reading R23, on one GPU
+                   (2D and 3D) with the Chebyshev smoother of degree >= 2 or
+                   multicolour Gauss-Seidel; fmg_create returns FMG_EINVAL for
+                   nu > 8, Chebyshev degree 1 with nu > 1, and z slabs with nu > 1. */
 } fmg_schedule;
 
 typedef struct fmg_ctx fmg_ctx;

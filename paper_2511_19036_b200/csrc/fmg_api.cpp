@@ -62,6 +62,7 @@ struct fmg_ctx {
   cudaGraphExec_t graph = nullptr;
   int solved_L = -1;
   int wu_cur[kMaxLev]{};
+  int wu_graph[kMaxLev]{};        // section widths the captured solve graph leaves (restored on every replay)
   int lc = 0;                     // levels 0..lc run inside the cluster kernel KC
   int kc_cluster = 1;             // CTAs of the KC cluster
   KcLayout kcl{};                 // KC shared-memory layout
@@ -77,7 +78,16 @@ struct fmg_ctx {
   // buffers with each level's geometry
   bool tma = false;
   CUtensorMap tmU[kMaxLev]{}, tmT[kMaxLev]{}, tmB[4][kMaxLev]{};
-  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3] x kMaxLev
+  // finest-level kernels (fmg_fine3.cu): coarse boxes of u_l / w_l, fine boxes
+  // of t_l (= b_l) and of the Chebyshev direction
+  CUtensorMap tmCU[kMaxLev]{}, tmCW[kMaxLev]{}, tmFB[kMaxLev]{}, tmFD[kMaxLev]{};
+  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3 | CU | CW | FB | FD] x kMaxLev
+  // 3D, one GPU, Chebyshev degree 2-3, nu = 1: level L of each FMG level runs
+  // the finest-level kernels and keeps no u_L, z_L, P u_{L-1}, w_L or y arrays
+  // (DESIGN.md §4.3); the level arrays of l = Lmax that remain are t (= b)
+  // and, for degree 3, the direction d_2.  FMG_FINE3=0 selects the
+  // level-by-level kernels everywhere.
+  bool fine3 = false;
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
   // exchanged before each stencil consumer, t_{lc+1} is gathered before KC)
@@ -159,7 +169,8 @@ Launch L_(fmg_ctx* c) { return Launch{c->dim, c->p, c->cur}; }
 // level, or one launch of the coarse-hierarchy cluster kernel KC (levels
 // 0..lc).  DESIGN.md §4.
 struct Item {
-  int kind;          // 0 grid op, 1 KC, 2 ghost-plane exchange / gather (z slabs)
+  int kind;          // 0 grid op, 1 KC, 2 ghost-plane exchange / gather (z slabs), 3 finest-level op (fmg_fine3.cu)
+  int f3kind;        // kind 3: 0 residual, 1 cFas step 1, 2 Chebyshev step op.step
   OpDesc op;         // grid item
   KcDesc kc;         // KC item
   int timed_cls;     // kernel-timing class of a grid item (-1: none)
@@ -199,6 +210,14 @@ struct Builder {
     it.xdepth = depth;
     it.xgather = gather;
     it.timed_cls = -1;
+    items.push_back(it);
+  }
+  void fine(int f3kind, const OpDesc& op, int cls = -1) {
+    Item it{};
+    it.kind = 3;
+    it.f3kind = f3kind;
+    it.op = op;
+    it.timed_cls = cls;
     items.push_back(it);
   }
   void kc(const KcDesc& d) {
@@ -244,16 +263,19 @@ OpDesc mkop(int type, int l, int L) {
 // Grid-only fmgResidual (API paths): decode sweep, residual, restriction, norms.
 void build_residual_grid(Builder& b, int L, int row) {
   fmg_ctx* c = b.c;
-  for (int l = 0; l <= L; ++l) {
+  const bool f3 = c->fine3 && L >= 1;  // u_L generated on chip: decode only l < L
+  for (int l = 0; l <= (f3 ? L - 1 : L); ++l) {
     OpDesc o = mkop(OP_DECODE, l, L);
     o.wu_in = c->wu_cur[l];
     b.grid(o);
   }
   OpDesc o = mkop(OP_RESIDUAL, L, L);
   o.wr = wr(c, L, L);
+  o.wu_in = c->wu_cur[L];
   o.row = row;
   o.poff = b.slot(row, L);
-  b.grid(o);
+  if (f3) b.fine(0, o);
+  else b.grid(o);
   for (int l = L - 1; l >= 0; --l) {
     OpDesc q = mkop(OP_RESTRICT, l, L);
     q.wr = wr(c, l, L);
@@ -282,9 +304,11 @@ void build_iteration_nu(Builder& b, int L, int it) {
   {
     OpDesc o = mkop(OP_RESIDUAL, L, L);
     o.wr = wr(c, L, L);
+    o.wu_in = c->wu_cur[L];
     o.row = row;
     o.poff = b.slot(row, L);
-    b.grid(o, fine ? 0 : -1);
+    if (c->fine3) b.fine(0, o, fine ? 0 : -1);  // u_L generated on chip (fmg_fine3.cu)
+    else b.grid(o, fine ? 0 : -1);
   }
   for (int l = L - 1; l >= 0; --l) {
     OpDesc q = mkop(OP_RESTRICT, l, L);
@@ -326,6 +350,18 @@ void build_iteration_nu(Builder& b, int L, int it) {
     const bool gs = c->s.smoother == 1;
     const int nsteps = gs ? ncolours(c) : k;  // GS: colour 0 in cFas1, then colours 1 .. (p+1)^d - 1
     for (int l = 1; l <= L; ++l) {
+      if (c->fine3 && l == L) {  // z_L generated on chip; no w_L, u_L (fmg_fine3.cu)
+        for (int step = 1; step <= nsteps; ++step) {
+          OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
+          q.step = step;
+          q.last = step == nsteps;
+          q.wr = wr(c, l, L);
+          q.wu_in = c->wu_cur[l];
+          q.wu_out = wu(c, l, L);
+          b.fine(step == 1 ? 1 : 2, q, fine ? (step == nsteps ? 5 : 1) : -1);
+        }
+        continue;
+      }
       if (c->dim == 3) b.grid(mkop(OP_PROLONG, l, L));  // z_l = P w_{l-1}, P u_{l-1}
       for (int step = 1; step <= nsteps; ++step) {
         OpDesc q = mkop(step == 1 ? OP_CFAS1 : (gs ? OP_GS : OP_CHEB), l, L);
@@ -405,7 +441,7 @@ void build_iteration(Builder& b, int L, int it) {
       q.wr = wr(c, l, L);
       q.wu_in = c->wu_cur[l];
       q.wu_out = wu(c, l, L);
-      b.grid(q, (fine && l == L) ? (step == k ? 5 : 1) : -1);
+      b.grid(q, (fine && l == L) ? (step == nsteps ? 5 : 1) : -1);
     }
     c->wu_cur[l] = wu(c, l, L);
   }
@@ -440,9 +476,17 @@ void build_solve(Builder& b, int Lstop, int iters_last) {
     c->wu_cur[L] = wu(c, L, L);
     // u_L = dec ú_L + P u_{L-1} = P u_{L-1} for the first residual
     b.xchg(XA_U, L - 1, c->p);
-    OpDesc o = mkop(OP_DECODE, L, L);
-    o.wu_in = c->wu_cur[L];
-    b.grid(o, (L == c->Lmax) ? 2 : -1);
+    if (c->fine3) {
+      // u_{L-1} = dec ú_{L-1} + P u_{L-2}: level L-1 was the finest level of
+      // FMG level L-1, whose kernels keep no u array (fmg_fine3.cu)
+      OpDesc o = mkop(OP_DECODE, L - 1, L - 1);
+      o.wu_in = c->wu_cur[L - 1];
+      b.grid(o, -1);
+    } else {
+      OpDesc o = mkop(OP_DECODE, L, L);
+      o.wu_in = c->wu_cur[L];
+      b.grid(o, (L == c->Lmax) ? 2 : -1);
+    }
     int iters = (L == Lstop) ? iters_last : c->s.n_ir;
     for (int it = 0; it < iters; ++it) build_iteration(b, L, it);
   }
@@ -550,8 +594,52 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
   return m;
 }
 
+// Arguments of a finest-level op (fmg_fine3.cu).
+F3Args fine3_args(const fmg_ctx* c, const Item& it) {
+  const OpDesc& o = it.op;
+  const int l = o.l;
+  F3Args a{};
+  a.g = c->g[l];
+  a.l = l;
+  a.step = o.step;
+  a.last = o.last;
+  a.wr = o.wr;
+  a.wu = o.wu_in;
+  a.wu_out = o.wu_out;
+  a.RC = c->mrc[l];
+  a.nxb = c->g[l].NX / 32;
+  a.nyb = c->mnyb[l];
+  a.nitems = c->mitems[l];
+  a.zlo = c->zlo[l];
+  a.zhi = c->zhi[l];
+  a.umant = c->u[l].mant;
+  a.uexp = c->u[l].exps;
+  a.ustride = c->u[l].stride;
+  a.rmant = c->r[l].mant;
+  a.rexp = c->r[l].exps;
+  a.rstride = c->r[l].stride;
+  a.gtab = c->gtab[l];
+  a.T = c->Tl[l];
+  a.Dv = c->buf[4];
+  a.pbase = c->pbase;
+  a.poff = o.poff;
+  a.status = c->status;
+  const CUtensorMap* base = c->tm_dev;
+  if (l >= 1) a.tmc = base + (it.f3kind == 0 ? 6 : 7) * kMaxLev + (l - 1);
+  a.tmb = base + 8 * kMaxLev + l;
+  a.tmd = base + 9 * kMaxLev + l;
+  return a;
+}
+
 // Launch one op / KC item of the list on c->cur.
 void issue_item(fmg_ctx* c, const Item& it) {
+  if (it.kind == 3) {
+    mark(c, it.timed_cls);
+    launch_fine3(c->p, it.f3kind, c->cur, fine3_args(c, it), c->cf);
+    mark(c, it.timed_cls);
+    c->launches++;
+    return;
+  }
   if (it.kind == 1) {
     mark(c, -2);
     launch_kc(c->dim, c->p, c->cur, c->devctx, it.kc, c->kc_cluster, c->kcl.bytes);
@@ -864,6 +952,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   set_kernel_attributes();
   march_set_attributes();
   march3_set_attributes();
+  fine3_set_attributes();
   c->march = !(getenv("FMG_MARCH") && atoi(getenv("FMG_MARCH")) == 0);
   if ((s->smoother == 1 || s->nu > 1 || (s->nu > 1 && G > 1)) && !c->march) {  // (tile-box kernels: Chebyshev, nu = 1)
     fmg_destroy(c);
@@ -899,9 +988,9 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     c->u[l].stride = wu(c, l, Lmax);
     c->r[l].stride = wr(c, l, Lmax);
     c->u[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->u[l].stride);
-    c->u[l].exps = (int8_t*)dalloc(c, g.nblk);
+    c->u[l].exps = (int8_t*)dalloc(c, g.nblk + 16);  // (+16: aligned 4-byte exponent reads, fmg_fine3.cu)
     c->r[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->r[l].stride);
-    c->r[l].exps = (int8_t*)dalloc(c, g.nblk);
+    c->r[l].exps = (int8_t*)dalloc(c, g.nblk + 16);
     if (s->nu > 1) {
       c->ysec[l].stride = wr(c, l, Lmax);
       c->ysec[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->ysec[l].stride);
@@ -973,24 +1062,44 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       c->mitems[l] = tiles * nch;
     }
   }
-  // FP64 workspace: per-level u_l, t_l, w_l; finest-size Z, B, Y[2], Dv, PU;
-  // KC scratch of twice the level-lc size (3D restriction staging).
+  // Finest-level kernels (fmg_fine3.cu): 3D, one GPU,
+  // Chebyshev degree 2-3, nu = 1, KC for the coarse solve only.
+  {
+    const char* e = getenv("FMG_FINE3");
+    c->fine3 = rc == FMG_OK && dim == 3 && c->march && G == 1 && s->nu <= 1 && s->smoother == 0 &&
+               (s->cheb_degree == 2 || s->cheb_degree == 3) && c->lc == 0 && Lmax >= 1 && !(e && atoi(e) == 0);
+  }
+  // FP64 workspace.  Level arrays u_l, t_l, w_l (padded level layout); the
+  // scratch Z, B, Y[2], PU of the level-by-level kernels and the Chebyshev
+  // direction Dv, each used by one level at a time.  With fine3 the finest
+  // level keeps only t (which also holds b) and, for degree 3, Dv: its u, w
+  // and the scratch of levels < Lmax are one level smaller.
   for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
     size_t bytes = sizeof(double) * c->g[l].size;
-    c->Ul[l] = (double*)dalloc(c, bytes);
+    const bool top = c->fine3 && l == Lmax;
     c->Tl[l] = (double*)dalloc(c, bytes);
-    c->Wl[l] = (double*)dalloc(c, bytes);
-    if (!c->Ul[l] || !c->Tl[l] || !c->Wl[l]) rc = FMG_ENOMEM;
+    if (!top) {
+      c->Ul[l] = (double*)dalloc(c, bytes);
+      c->Wl[l] = (double*)dalloc(c, bytes);
+    }
+    if (!c->Tl[l] || (!top && (!c->Ul[l] || !c->Wl[l]))) rc = FMG_ENOMEM;
     else {
-      cudaMemset(c->Ul[l], 0, bytes);
       cudaMemset(c->Tl[l], 0, bytes);
-      cudaMemset(c->Wl[l], 0, bytes);
+      if (!top) {
+        cudaMemset(c->Ul[l], 0, bytes);
+        cudaMemset(c->Wl[l], 0, bytes);
+      }
     }
   }
-  for (int i = 0; i < 6 && rc == FMG_OK; ++i) {
-    c->buf[i] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
-    if (!c->buf[i]) rc = FMG_ENOMEM;
-    else cudaMemset(c->buf[i], 0, sizeof(double) * c->g[Lmax].size);
+  {
+    const size_t scratch = sizeof(double) * c->g[c->fine3 ? Lmax - 1 : Lmax].size;
+    const bool dv = !c->fine3 || s->cheb_degree >= 3;
+    for (int i = 0; i < 6 && rc == FMG_OK; ++i) {
+      const size_t bytes = i == 4 ? (dv ? sizeof(double) * c->g[Lmax].size : 16) : scratch;
+      c->buf[i] = (double*)dalloc(c, bytes);
+      if (!c->buf[i]) rc = FMG_ENOMEM;
+      else cudaMemset(c->buf[i], 0, bytes);
+    }
   }
   if (rc == FMG_OK && s->nu > 1) {  // YO: dec ý of the previous cycle at the level being smoothed
     c->buf[8] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
@@ -1019,18 +1128,39 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       ok &= make_tmap(&c->tmU[l], c->Ul[l], g.NX, g.NY, 0, 32 + 2 * pe, 1);
       ok &= make_tmap(&c->tmT[l], c->Tl[l], g.NX, g.NY, 0, 64 + 4 * p, 1);
       for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, 0, 32 + 2 * pe, 1);
-    } else {
+    } else if (!(c->fine3 && l == Lmax)) {  // (fine3: level Lmax has no u array, the scratch is one level smaller)
       ok &= make_tmap(&c->tmU[l], c->Ul[l], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
       for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
     }
     if (!ok) rc = FMG_ECUDA;
   }
-  if (rc == FMG_OK && c->tma) {
-    std::vector<CUtensorMap> all(6 * kMaxLev);
+  // finest-level kernels: coarse boxes of u_l, w_l (l < Lmax), fine boxes of
+  // t_l and of Dv (levels >= 1)
+  for (int l = 0; l <= Lmax && rc == FMG_OK && c->fine3; ++l) {
+    const Geom& g = c->g[l];
+    int cbx = 0, cby = 0, rs = 0, nr = 0;
+    fine3_box_dims(p, &cbx, &cby, &rs, &nr);
+    bool ok = true;
+    if (l < Lmax) {
+      ok &= make_tmap(&c->tmCU[l], c->Ul[l], g.NX, g.NY, g.NZ, cbx, cby);
+      ok &= make_tmap(&c->tmCW[l], c->Wl[l], g.NX, g.NY, g.NZ, cbx, cby);
+    }
+    if (l >= 1) {
+      ok &= make_tmap(&c->tmFB[l], c->Tl[l], g.NX, g.NY, g.NZ, rs, nr);
+      if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->buf[4], g.NX, g.NY, g.NZ, rs, nr);
+    }
+    if (!ok) rc = FMG_ECUDA;
+  }
+  if (rc == FMG_OK && (c->tma || c->fine3)) {
+    std::vector<CUtensorMap> all(10 * kMaxLev);
     for (int l = 0; l < kMaxLev; ++l) {
       all[l] = c->tmU[l];
       all[kMaxLev + l] = c->tmT[l];
       for (int i = 0; i < 4; ++i) all[(2 + i) * kMaxLev + l] = c->tmB[i][l];
+      all[6 * kMaxLev + l] = c->tmCU[l];
+      all[7 * kMaxLev + l] = c->tmCW[l];
+      all[8 * kMaxLev + l] = c->tmFB[l];
+      all[9 * kMaxLev + l] = c->tmFD[l];
     }
     c->tm_dev = (CUtensorMap*)dalloc(c, sizeof(CUtensorMap) * all.size());  // (256-byte aligned)
     if (!c->tm_dev) rc = FMG_ENOMEM;
@@ -1043,7 +1173,8 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     c->Ainv = (double*)dalloc(c, sizeof(double) * Ai.size());
     c->partials = (double*)dalloc(c, sizeof(double) * tot_parts);
     c->norms_dev = (double*)dalloc(c, sizeof(double) * levels * s->n_ir * levels);
-    c->err_part = (double*)dalloc(c, sizeof(double) * 2 * 148 * 16);
+    // error partials (2 per CTA of k_errors) and, on NCCL ranks, the norm log all-reduce
+    c->err_part = (double*)dalloc(c, sizeof(double) * std::max<size_t>(2 * 148 * 16, (size_t)levels * levels * s->n_ir));
     c->status = (int*)dalloc(c, sizeof(int));
     int* counters = (int*)dalloc(c, sizeof(int) * kMaxLev);
     if (counters) cudaMemset(counters, 0, sizeof(int) * kMaxLev);
@@ -1241,9 +1372,13 @@ int fmg_solve_async(fmg_ctx* c) {
     e = cudaGraphInstantiate(&c->graph, gr, 0);
     cudaGraphDestroy(gr);
     if (e != cudaSuccess) { c->graph = nullptr; return cuda_err(e); }
+    std::memcpy(c->wu_graph, c->wu_cur, sizeof(c->wu_graph));
   }
   cudaError_t e = cudaGraphLaunch(c->graph, c->st);
   if (e != cudaSuccess) return cuda_err(e);
+  // a replay leaves the sections at the widths of the captured build, whatever
+  // fmg_solve_upto ran in between (wu_cur went stale on replay)
+  std::memcpy(c->wu_cur, c->wu_graph, sizeof(c->wu_cur));
   c->solved_L = c->Lmax;
   return FMG_OK;
 }
@@ -1283,7 +1418,10 @@ static int norms_sq(fmg_ctx* c, double* host) {
     // NCCL ranks: sum the slab partials of levels > lc (KC levels from rank 0)
     for (size_t i = 0; i < n; ++i)
       if ((int)(i % c->levels) <= c->lc && c->rank != 0) host[i] = 0.0;
-    cudaMemcpy(c->err_part, host, sizeof(double) * n, cudaMemcpyHostToDevice);
+    e = cudaMemcpyAsync(c->err_part, host, sizeof(double) * n, cudaMemcpyHostToDevice, c->st);
+    if (e != cudaSuccess) return cuda_err(e);
+    e = cudaStreamSynchronize(c->st);  // (pageable source: the copy has completed before the all-reduce)
+    if (e != cudaSuccess) return cuda_err(e);
     if (nccl().allReduce(c->err_part, c->err_part, n, ncclDouble, ncclSum, (ncclComm_t)c->comm, c->st) != ncclSuccess)
       return FMG_ENCCL;
     e = cudaStreamSynchronize(c->st);
@@ -1337,6 +1475,12 @@ int fmg_residual(fmg_ctx* c, double* host_norms) {
 // û_L into the level-L u array (decode ops for l = 0..L, materialised).
 static int decode_solution(fmg_ctx* c, int* which) {
   int L = c->solved_L;
+  if (!c->Ul[L]) {  // fine3: the finest level has no u array until a solution is asked for
+    const size_t bytes = sizeof(double) * c->g[L].size;
+    c->Ul[L] = (double*)dalloc(c, bytes);
+    if (!c->Ul[L]) return FMG_ENOMEM;
+    cudaMemset(c->Ul[L], 0, bytes);
+  }
   Builder b = make_builder(c);
   for (int l = 0; l <= L; ++l) {
     OpDesc o = mkop(OP_DECODE, l, L);
@@ -1349,7 +1493,7 @@ static int decode_solution(fmg_ctx* c, int* which) {
 
 int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
   if (!c || !dst_dev) return FMG_EINVAL;
-  if (!c->sub.empty()) return FMG_EINVAL;
+  if (!c->sub.empty() || c->comm) return FMG_EINVAL;  // (slab ranks hold only their planes)
   if (c->solved_L < 0) return FMG_ESTATE;
   int which = 0;
   int rc = decode_solution(c, &which);
@@ -1361,7 +1505,7 @@ int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
 
 int fmg_errors(fmg_ctx* c, double* err3) {
   if (!c || !err3) return FMG_EINVAL;
-  if (!c->sub.empty()) return FMG_EINVAL;
+  if (!c->sub.empty() || c->comm) return FMG_EINVAL;  // (slab ranks hold only their planes)
   if (c->solved_L < 0) return FMG_ESTATE;
   int which = 0;
   int rc = decode_solution(c, &which);
@@ -1485,11 +1629,19 @@ int fmg_memory_model(int dim, int p, int levels, const fmg_schedule* s, double* 
     const int aL = s->b_u + s->k_u * L;
     tmp62 += 2.0 * aL * delta;                  // u and t at a_L bits (Eq 6.2)
     tmp63 += (double)(s->k_u * l + s->b_u) * delta;  // z, progressive (Eq 6.3)
-    fp64 += 3.0 * 8.0 * stored;                 // this implementation: full FP64 u_l, t_l, w_l
+    // this implementation's FP64 arrays (create_impl): u_l, t_l, w_l per level;
+    // scratch Z, B, Y[2], PU and the Chebyshev direction Dv.  With the
+    // finest-level kernels (3D, Chebyshev degree 2-3, nu = 1)
+    // level L keeps only t_L, the scratch is one level smaller and Dv exists
+    // for degree 3 only.
+    const bool f3 = dim == 3 && s->nu <= 1 && s->smoother == 0 && (s->cheb_degree == 2 || s->cheb_degree == 3) && L >= 1;
+    fp64 += (f3 && l == L ? 1.0 : 3.0) * 8.0 * stored;
+    if (f3 && l == L - 1) fp64 += 5.0 * 8.0 * stored;
     sec += 4.0 * (double)(NX * n * (dim == 3 ? n : 1) / 32) * (wul + wrl) + 2.0 * stored / 32.0;
     if (l == L) {
       nL = N;
-      fp64 += 6.0 * 8.0 * stored;               // finest-size Z, B, Y[2], Dv, PU
+      if (!f3) fp64 += 6.0 * 8.0 * stored;      // finest-size Z, B, Y[2], Dv, PU
+      else if (s->cheb_degree >= 3) fp64 += 8.0 * stored;  // Dv
     }
   }
   ub = (cst * s->b_u + cst / (two_d - 1.0) * s->k_u) * nL;

@@ -1,0 +1,937 @@
+// fmg_fine3.cu -- 3D kernels of the FINEST level of each FMG level (DESIGN.md
+// §4.3): the level where almost all of the work and all of the large FP64
+// temporaries are.
+//
+// Three plane-marching kernels replace, at l = L, the six of fmg_march3.cu
+// (prolong, residual, cfas1, Chebyshev steps) and drop every finest-size FP64
+// array except one (t_L, which also holds b_L after the restriction sweep has
+// consumed t_L) and, for Chebyshev degree 3, the direction d_2:
+//
+//   k_f3_residual  u_L = dec ú_L + P_L u_{L-1} is generated plane by plane on
+//                  chip (the coarse u_{L-1} boxes arrive by TMA; prolongation
+//                  x and y passes in shared memory, z pass from a ring of
+//                  coarse planes), then t_L = f_L - A_L u_L, r_L = enc(t_L),
+//                  ||t_L||^2 partials and t_L -> HBM for the restriction.
+//                  No u_L array exists (Alg 3.2).
+//   k_f3_cfas      z_L = P_L w_{L-1} generated the same way, b_L = dec r_L -
+//                  A_L z_L -> HBM (in the t_L buffer).  No z_L array
+//                  (Alg 3.1).
+//   k_f3_cheb      Chebyshev step j = 2..k (k <= 3): y_{j-1} is recomputed
+//                  from b (and d_2) on the staged boxes, A y_{j-1}; the last
+//                  step encodes ý_L and applies the correction ú_L =
+//                  enc(dec ú_L + dec ý_L).  At l = L
+//                  neither w_L nor u_L is needed, so neither is written.
+//
+// Instruction economy (profiles/r2_summary.md): the node types of the y and
+// z passes are warp- / CTA-uniform, so those passes are compile-time
+// specialised on the type (switch), which turns every coefficient into a
+// constant-bank operand and skips the taps that are structurally zero for
+// interior node types (exact: every chain starts from +0, so fma(0, v, acc)
+// = acc).  Section words are prefetched by cp.async several planes ahead.
+//
+// Every floating-point expression is the canonical tree of DESIGN.md §3
+// with explicit fma() (-fmad=false): bit-identical to fmg_march3.cu and to
+// the oracle.
+#include "fmg_device.cuh"
+
+#ifndef F3_PF
+#define F3_PF 2      // staging / section-word lookahead (planes)
+#endif
+
+namespace fmg {
+
+namespace {
+
+constexpr int FW = 8;  // warps per CTA = output rows of the 32 x 8 tile
+
+template <int P>
+struct F3 {
+  static constexpr int R = 2 * P + 1;          // stencil taps per direction
+  static constexpr int NR = FW + 2 * P;        // staged box rows
+  static constexpr int RS = 40;                // staged row stride (doubles; TMA box width)
+  static constexpr int BOX = NR * RS;          // doubles per staged plane box
+  static constexpr int SH = P & 1;             // TMA boxes start at an even column: consumers shift
+  static constexpr int PF = F3_PF;             // staging lookahead (planes)
+  static constexpr int NBF = PF + P + 1;       // staged fine-plane ring (cheb)
+  static constexpr int NW = PF + P + 1;        // section-word ring (planes)
+  // coarse boxes of the on-the-fly prolongation (fine box + halo -> coarse)
+  static constexpr int CBX = P == 3 ? 28 : 24;
+  static constexpr int CBY = P == 3 ? 14 : 10;
+  static constexpr int CBOX = CBX * CBY;
+  static constexpr int CBS = (CBOX + 15) & ~15;  // slot stride: TMA destinations are 128-byte aligned
+  static constexpr int NCB = P + 1;            // raw coarse box ring (TMA)
+  static constexpr int NCY = P + 1;            // xy-passed coarse plane ring
+};
+
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// -------------------------------------------------------- A passes ------
+// y pass at one output row of node type T (c = My a,
+// d = Ky a, e = My b; s = d + e), zero taps of interior types skipped.
+template <int P, int T>
+__device__ __forceinline__ void ypass_t(const Coefs& cf, const double* XA, const double* XB, int w, int lane, double& c,
+                                        double& s) {
+  constexpr int o0 = T == 0 ? 0 : P - T, o1 = T == 0 ? 2 * P : 2 * P - T;
+  double cc = 0.0, dd = 0.0, ee = 0.0;
+#pragma unroll
+  for (int o = o0; o <= o1; ++o) {
+    const double av = XA[(w + o) * 32 + lane], bv = XB[(w + o) * 32 + lane];
+    cc = fma(cf.Mc[T][o], av, cc);
+    dd = fma(cf.Kc[T][o], av, dd);
+    ee = fma(cf.Mc[T][o], bv, ee);
+  }
+  c = cc;
+  s = dd + ee;
+}
+template <int P>
+__device__ __forceinline__ void ypass(const Coefs& cf, int ty, const double* XA, const double* XB, int w, int lane,
+                                      double& c, double& s) {
+  if (P == 1 || ty == 0) ypass_t<P, 0>(cf, XA, XB, w, lane, c, s);
+  else if (P == 2 || ty == 1) ypass_t<P, (P >= 2 ? 1 : 0)>(cf, XA, XB, w, lane, c, s);
+  else ypass_t<P, (P >= 3 ? 2 : 0)>(cf, XA, XB, w, lane, c, s);
+}
+// z pass of node type T over the register rings (acc over Kz on c, then Mz on s)
+template <int P, int T>
+__device__ __forceinline__ double zpass_t(const Coefs& cf, const double* cr, const double* sr) {
+  constexpr int o0 = T == 0 ? 0 : P - T, o1 = T == 0 ? 2 * P : 2 * P - T;
+  double acc = 0.0;
+#pragma unroll
+  for (int o = o0; o <= o1; ++o) acc = fma(cf.Kc[T][o], cr[o], acc);
+#pragma unroll
+  for (int o = o0; o <= o1; ++o) acc = fma(cf.Mc[T][o], sr[o], acc);
+  return acc;
+}
+template <int P>
+__device__ __forceinline__ double zpass(const Coefs& cf, int tz, const double* cr, const double* sr) {
+  if (P == 1 || tz == 0) return zpass_t<P, 0>(cf, cr, sr);
+  if (P == 2 || tz == 1) return zpass_t<P, (P >= 2 ? 1 : 0)>(cf, cr, sr);
+  return zpass_t<P, (P >= 3 ? 2 : 0)>(cf, cr, sr);
+}
+
+// x pass of the staged box rows of warp w: a = Mx u, b = Kx u (lane = output
+// column x0 + lane; staged column c = fine x0 - P + c; `off` = TMA shift)
+template <int P>
+__device__ __forceinline__ void xpass(const double* box, int off, const double* km, const double* kk, double* XA,
+                                      double* XB, int w, int lane) {
+  constexpr int R = F3<P>::R, NR = F3<P>::NR, RS = F3<P>::RS;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int r = w + k * FW;
+    if (r < NR) {
+      const double* row = box + r * RS + off;
+      double s = 0.0, t = 0.0;
+#pragma unroll
+      for (int o = 0; o < R; ++o) {
+        const double v = row[lane + o];
+        s = fma(km[o], v, s);
+        t = fma(kk[o], v, t);
+      }
+      XA[r * 32 + lane] = s;
+      XB[r * 32 + lane] = t;
+    }
+  }
+}
+
+// ------------------------------------------------------ tile geometry ----
+struct F3Tile {
+  int x0, y0, zs, ze, cta;
+};
+__device__ __forceinline__ F3Tile f3_tile(const F3Args& a) {
+  F3Tile t;
+  const int cta = blockIdx.x, tiles = a.nxb * a.nyb;
+  const int q = cta % tiles, ch = cta / tiles;
+  t.x0 = (q % a.nxb) * 32;
+  t.y0 = (q / a.nxb) * FW;
+  t.zs = a.zlo + ch * a.RC;
+  t.ze = min(a.zhi, t.zs + a.RC);
+  t.cta = cta;
+  return t;
+}
+
+// Staged column of lane's halo element (lanes < 2P): left halo columns 0..P-1,
+// right halo columns 32+P..32+2P-1; the own column is P + lane.
+template <int P>
+__device__ __forceinline__ int halo_col(int lane) {
+  return lane < P ? lane : 32 + lane;
+}
+
+// ------------------------------------------------- section words ring ---
+// Section words are copied by cp.async into a ring of per-plane slots, PF
+// planes ahead.  Every lane owns one 4-byte source stream (a mantissa word or
+// an aligned exponent word) that advances by a fixed byte step per plane
+// (blocks per plane = NY nxb is a multiple of 4, so aligned exponent words
+// advance linearly too); no per-plane index arithmetic.
+struct WStream {
+  const char* src;  // this lane's source at plane z0 (dereferenced only when valid)
+  long long step;   // bytes per plane
+  int dst;          // word offset in the slot
+  bool on;          // this lane copies (row and block exist)
+};
+
+// Residual: box row fy, blocks xb-1, xb, xb+1 (3 w words: lane j < 3w) and
+// the two aligned exponent words covering their exponents (lanes 3w, 3w+1).
+// Record RW = 3 w + 2 words; `eoff` = byte offset of e(xb-1) in the pair.
+__device__ __forceinline__ WStream wstream3(const uint32_t* mant, const int8_t* exps, int stride, int w, const Geom& g,
+                                            int x0, int fy, int z0, int rec, bool rowon, int lane, int& eoff) {
+  WStream s{};
+  const int nxb = g.NX >> 5, xb = x0 >> 5;
+  const long long bpp = (long long)g.NY * nxb;  // blocks per plane (multiple of 4)
+  const long long b0 = ((long long)z0 * g.NY + fy) * nxb + xb;  // own block at plane z0
+  const long long ea = (b0 - 1) & ~3LL;                         // (floor: also for negative z0)
+  eoff = (int)((b0 - 1) - ea);
+  if (lane < 3 * w) {
+    const int k = lane / w, wd = lane - k * w;
+    const int xbk = xb - 1 + k;
+    s.on = rowon && xbk >= 0 && xbk < nxb;
+    s.src = (const char*)(mant + (b0 - 1 + k) * stride + wd);
+    s.step = bpp * stride * 4;
+    s.dst = rec + lane;
+  } else if (lane < 3 * w + 2) {
+    s.on = rowon;
+    s.src = (const char*)(exps + ea + 4 * (lane - 3 * w));
+    s.step = bpp;
+    s.dst = rec + lane;
+  }
+  return s;
+}
+// Own block of output row y: w words (lanes < w) and the aligned exponent
+// word (lane w); record RW = w + 1 words, `eoff` = byte of e(xb) in it.
+__device__ __forceinline__ WStream wstream1(const uint32_t* mant, const int8_t* exps, int stride, int w, const Geom& g,
+                                            int x0, int y, int z0, int rec, bool rowon, int lane, int& eoff) {
+  WStream s{};
+  const long long bpp = (long long)g.NY * (g.NX >> 5);
+  const long long b0 = ((long long)z0 * g.NY + y) * (g.NX >> 5) + (x0 >> 5);
+  const long long ea = b0 & ~3LL;
+  eoff = (int)(b0 - ea);
+  if (lane < w) {
+    s.on = rowon;
+    s.src = (const char*)(mant + b0 * stride + lane);
+    s.step = bpp * stride * 4;
+    s.dst = rec + lane;
+  } else if (lane == w) {
+    s.on = rowon;
+    s.src = (const char*)(exps + ea);
+    s.step = bpp;
+    s.dst = rec + lane;
+  }
+  return s;
+}
+__device__ __forceinline__ void wcopy(const WStream& s, unsigned slot_s, int plane_off) {  // slot: smem byte address
+  if (s.on)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(slot_s + 4u * (unsigned)s.dst),
+                 "l"(s.src + s.step * plane_off)
+                 : "memory");
+}
+__device__ __forceinline__ int rec_e(const uint32_t* ew, int off) {  // byte `off` of the exponent word pair
+  return (int)(int8_t)(ew[off >> 2] >> (8 * (off & 3)));
+}
+
+// ------------------------------------------- on-the-fly prolongation ----
+// Generates, plane by plane, v = P_l c_{l-1} on the staged box (32 + 2P) x
+// (8 + 2P) (x pass over coarse taps, then y, then z; one fma
+// chain per pass from +0; 0 at fine non-unknowns).  Coarse plane boxes CBX x
+// CBY arrive by TMA into a ring of NCB slots; their x and y passes go to a
+// ring of NCY xy-passed planes (rows and columns of the fine box), from which
+// each fine plane takes its z pass.
+//
+// Thread mapping: the box's NR x BW elements are dealt out linearly (element
+// e = tid + k NT), so every warp does the same work (no halo lanes); each
+// element carries its packed smem offset, coarse tap offsets and weight rows.
+// The x pass uses the same list with the row read as a coarse row (CBY <= NR).
+template <int P>
+struct Gen {
+  static constexpr int BW = 32 + 2 * P, NE = F3<P>::NR * BW, KB = (NE + 32 * FW - 1) / (32 * FW);
+  int off[KB];   // r RS + c; -1: inactive element
+  int pk[KB];    // bxo | byo << 8 | rx << 16 | ry << 20 | (r < CBY) << 24   (coarse offsets from the box origin)
+  int dk[KB];    // decode: record row offset | block << 10 | exponent byte << 12 | position << 16 | on << 24
+  int cx0, cy0;  // coarse box origin
+  int cfirst;    // first coarse plane of the march (ring slots and barrier phases count from it)
+  int clast;     // last coarse plane the march needs (no request beyond: no TMA left in flight)
+  int cdone;     // next coarse plane to xy-pass
+};
+
+// Element tables.  `rw` (record words per row, 0: no decode), `eoffr(r)`
+// (exponent byte of block xb - 1 for box row r) describe the section records.
+template <int P, class EO>
+__device__ __forceinline__ void gen_init(Gen<P>& gn, const Geom& g, int x0, int y0, int rw, int wu, EO eoffr) {
+  constexpr int NR = F3<P>::NR, RS = F3<P>::RS, CBY = F3<P>::CBY, BW = Gen<P>::BW;
+  const int n = g.n, tid = threadIdx.y * 32 + threadIdx.x;
+  gn.cx0 = (P * (max(x0 - P, 1) / (2 * P))) & ~1;
+  gn.cy0 = P * (max(y0 - P, 1) / (2 * P));
+#pragma unroll
+  for (int k = 0; k < Gen<P>::KB; ++k) {
+    const int e = tid + k * 32 * FW;
+    gn.off[k] = -1;
+    gn.pk[k] = 0;
+    gn.dk[k] = 0;
+    if (e < Gen<P>::NE) {
+      const int r = e / BW, c = e - r * BW;
+      const int fx = x0 - P + c, fy = y0 - P + r;
+      const bool okx = unk1(fx, n), oky = unk1(fy, n);
+      const int rx = okx ? fx % (2 * P) : 0, bxo = okx ? P * (fx / (2 * P)) - gn.cx0 : 0;
+      const int ry = oky ? fy % (2 * P) : 0, byo = oky ? P * (fy / (2 * P)) - gn.cy0 : 0;
+      gn.off[k] = r * RS + c;
+      // y pass reads PX[(byo + t) RS + c]: stored relative to the element's own offset
+      gn.pk[k] = bxo | ((byo - r + 32) << 8) | (rx << 16) | (ry << 20) | ((r < CBY ? 1 : 0) << 24) |
+                 ((okx ? 1 : 0) << 25) | ((oky ? 1 : 0) << 26);
+      if (rw > 0 && okx && oky) {
+        const int kb = c < P ? 0 : (c < 32 + P ? 1 : 2);
+        gn.dk[k] = (r * rw) | (kb << 10) | ((eoffr(r) + kb) << 12) | ((fx & 31) << 16) | (1 << 24);
+      }
+    }
+  }
+}
+
+// coarse plane index of the first tap of fine plane z (unknown z)
+template <int P>
+__device__ __forceinline__ int cbase(int z) {
+  return P * (z / (2 * P));
+}
+
+// x and y passes of coarse plane c (raw box in `cb`) into the xy ring slot.
+template <int P>
+__device__ __forceinline__ void gen_xy(const Gen<P>& gn, const double* pws, const double* cb, double* PX,
+                                       double* yv) {
+  constexpr int CBX = F3<P>::CBX, RS = F3<P>::RS;
+#pragma unroll
+  for (int k = 0; k < Gen<P>::KB; ++k) {
+    const int pk = gn.pk[k];
+    if (gn.off[k] >= 0 && (pk >> 24) & 1) {
+      const int r = gn.off[k] / RS;  // (coarse row = box row index)
+      double a = 0.0;
+      if ((pk >> 25) & 1) {
+        const double* wt = pws + ((pk >> 16) & 15) * (P + 1);
+        const double* row = cb + r * CBX + (pk & 255);
+#pragma unroll
+        for (int t = 0; t <= P; ++t) a = fma(wt[t], row[t], a);
+      }
+      PX[gn.off[k]] = a;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < Gen<P>::KB; ++k) {
+    const int pk = gn.pk[k];
+    if (gn.off[k] >= 0) {
+      double a = 0.0;
+      if ((pk >> 26) & 1) {
+        const double* wt = pws + ((pk >> 20) & 15) * (P + 1);
+        const double* col = PX + gn.off[k] + (((pk >> 8) & 255) - 32) * RS;
+#pragma unroll
+        for (int t = 0; t <= P; ++t) a = fma(wt[t], col[t * RS], a);
+      }
+      yv[gn.off[k]] = a;
+    }
+  }
+}
+
+// Request the TMA box of coarse plane c (thread 0); slot and barrier phase
+// count from the first plane of the march.
+template <int P>
+__device__ __forceinline__ void gen_request(const Gen<P>& gn, const CUtensorMap* tm, double* craw,
+                                            unsigned long long* cbar, int c) {
+  constexpr int NCB = F3<P>::NCB;
+  if (c > gn.clast) return;
+  const int k = (c - gn.cfirst) % NCB;
+  fence_async_smem();
+  tma_load_3d(craw + k * F3<P>::CBS, tm, gn.cx0, gn.cy0, c, cbar + k, (unsigned)(F3<P>::CBOX * 8));
+}
+// Coarse planes of a march over fine input planes [z0, z0 + nin): the first
+// and last unknown fine planes decide them (none: cfirst > clast).
+template <int P>
+__device__ __forceinline__ void gen_range(Gen<P>& gn, int z0, int nin, int n) {
+  const int zf = max(z0, 1), zl = min(z0 + nin - 1, n - 1);
+  gn.cfirst = P * (zf / (2 * P));
+  gn.clast = zf <= zl ? P * (zl / (2 * P)) + P : gn.cfirst - 1;
+  gn.cdone = gn.cfirst;
+}
+
+// Make the xy passes of every coarse plane <= cneed available.
+template <int P>
+__device__ __forceinline__ void gen_advance(Gen<P>& gn, const double* pws, const CUtensorMap* tm, double* craw,
+                                            unsigned long long* cbar, double* PX, double* yvring, int cneed) {
+  constexpr int NCB = F3<P>::NCB, NCY = F3<P>::NCY, BOX = F3<P>::BOX;
+  while (gn.cdone <= cneed) {
+    const int c = gn.cdone, k = c - gn.cfirst;
+    mbar_wait(cbar + (k % NCB), (unsigned)(k / NCB) & 1u);
+    gen_xy<P>(gn, pws, craw + (k % NCB) * F3<P>::CBS, PX, yvring + (c % NCY) * BOX);
+    // (gen_xy synchronised after its x pass: the raw slot is free)
+    if (threadIdx.x == 0 && threadIdx.y == 0) gen_request<P>(gn, tm, craw, cbar, c + NCB);
+    gn.cdone = c + 1;
+    __syncthreads();
+  }
+}
+
+// Fine plane z into the box: z pass of the xy ring (0 at non-unknown planes),
+// plus dec of the section record (residual, `rec` non-null).
+template <int P>
+__device__ __forceinline__ void gen_z(const Gen<P>& gn, const Coefs& cf, const double* yvring, int z, int n,
+                                     double* box, const uint32_t* rec, int wu) {
+  constexpr int NCY = F3<P>::NCY, BOX = F3<P>::BOX;
+  const bool okz = unk1(z, n);
+  const int rz = okz ? z % (2 * P) : 0, cb = okz ? cbase<P>(z) : 0;
+  double pz[P + 1];
+  const double* ys[P + 1];
+#pragma unroll
+  for (int t = 0; t <= P; ++t) {
+    pz[t] = cf.Pw[rz][t];
+    ys[t] = yvring + ((cb + t) % NCY) * BOX;
+  }
+#pragma unroll
+  for (int k = 0; k < Gen<P>::KB; ++k) {
+    const int o = gn.off[k];
+    if (o >= 0) {
+      double v = 0.0;
+      if (okz) {
+#pragma unroll
+        for (int t = 0; t <= P; ++t) v = fma(pz[t], ys[t][o], v);
+        const int dk = gn.dk[k];
+        if (rec && (dk >> 24)) {
+          const uint32_t* r0 = rec + (dk & 1023);
+          const double dv = point_decode(r0 + ((dk >> 10) & 3) * wu, rec_e(r0 + 3 * wu, (dk >> 12) & 15), wu,
+                                         (dk >> 16) & 31);
+          v = dv + v;  // u = dec ú + P u
+        }
+      }
+      box[o] = v;
+    }
+  }
+}
+
+}  // namespace
+
+// ================================================================ kernels ==
+// Shared-memory carve-up of the generating kernels (residual, cFas): raw
+// coarse boxes (TMA, 128-byte aligned slots), xy-passed coarse planes, the
+// generated box, the A x pass, the prolongation x pass, the P weight table,
+// then the section-word ring and the barriers.
+template <int P>
+struct GenSmem {
+  double *craw, *yvring, *box, *XA, *XB, *PX, *pws;
+  uint32_t* wring;
+  unsigned long long* cbar;
+};
+template <int P>
+__device__ __forceinline__ GenSmem<P> gen_smem(double* base, int ring_words) {
+  using C = F3<P>;
+  GenSmem<P> m;
+  m.craw = base;
+  m.yvring = m.craw + C::NCB * C::CBS;
+  m.box = m.yvring + C::NCY * C::BOX;
+  m.XA = m.box + C::BOX;
+  m.XB = m.XA + C::NR * 32;
+  m.PX = m.XB + C::NR * 32;
+  m.pws = m.PX + C::CBY * C::RS;
+  m.wring = (uint32_t*)(m.pws + 2 * P * (P + 1));
+  uintptr_t b = (uintptr_t)(m.wring + ring_words);
+  m.cbar = (unsigned long long*)((b + 7) & ~(uintptr_t)7);
+  return m;
+}
+template <int P>
+__host__ __device__ constexpr size_t gen_smem_bytes(int ring_words) {
+  using C = F3<P>;
+  return ((size_t)C::NCB * C::CBS + (size_t)C::NCY * C::BOX + C::BOX + 2 * C::NR * 32 + (size_t)C::CBY * C::RS +
+          2 * P * (P + 1)) * 8 + (size_t)ring_words * 4 + 8 + 8 * C::NCB;
+}
+
+// t_L = f_L - A_L u_L with u_L = dec ú_L + P u_{L-1} generated on chip;
+// r_L = enc(t_L); t_L -> HBM; ||t_L||^2 partial per warp (Alg 3.2).
+template <int P>
+__global__ void __launch_bounds__(32 * FW, 2) k_f3_residual(const __grid_constant__ F3Args a,
+                                                              const __grid_constant__ Coefs cf) {
+  using C = F3<P>;
+  constexpr int R = C::R, NR = C::NR, NW = C::NW, PF = C::PF;
+  extern __shared__ __align__(128) double fsm[];
+  const int RW = 3 * a.wu + 2;  // record words per box row
+  const GenSmem<P> m = gen_smem<P>(fsm, NW * NR * RW);
+  const unsigned wring_s = smem_u32(m.wring);
+
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const F3Tile tl = f3_tile(a);
+  const Geom g = a.g;
+  const int n = g.n;
+  const int x = tl.x0 + lane, y = tl.y0 + w;
+  const bool rowok = y < g.NY;
+  const int tx = x % P, ty = y % P;
+  double km[R], kk[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) {
+    km[o] = cf.Mc[tx][o];
+    kk[o] = cf.Kc[tx][o];
+  }
+  const double hl = pow2(-(a.l + 1));
+  const double* __restrict__ gt = a.gtab;
+  const bool uxy = unk1(x, n) && unk1(y, n);
+  const double gxy = uxy ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
+  const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
+  const int nxb = g.NX >> 5, xb = tl.x0 >> 5;
+  Gen<P> gn;
+  gen_init<P>(gn, g, tl.x0, tl.y0, RW, a.wu, [&](int r) {
+    const long long b0 = ((long long)z0 * g.NY + (tl.y0 - P + r)) * nxb + xb;
+    return (int)((b0 - 1) - ((b0 - 1) & ~3LL));
+  });
+  gen_range<P>(gn, z0, nin, n);
+  // section word streams of the warp's (up to) two box rows: only unknown
+  // rows are decoded (the section and u are 0 elsewhere)
+  WStream ws[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int r = w + k * FW, fy = tl.y0 - P + r;
+    int eo;
+    ws[k] = wstream3(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, fy, z0, r * RW, r < NR && unk1(fy, n), lane, eo);
+  }
+  // output pointers (advance one plane per output)
+  const long long tplane = (long long)g.NY * g.NX;
+  const long long bpp = (long long)g.NY * nxb;
+  double* Tp = a.T + ((long long)tl.zs * g.NY + y) * g.NX + x;
+  const long long blk0 = ((long long)tl.zs * g.NY + y) * nxb + xb;
+  uint32_t* rmp = a.rmant + blk0 * a.rstride;
+  int8_t* rep = a.rexp + blk0;
+
+  {
+    const int tid = w * 32 + lane;
+    if (tid < 2 * P * (P + 1)) m.pws[tid] = cf.Pw[tid / (P + 1)][tid % (P + 1)];
+  }
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < C::NCB; ++k) mbar_init(m.cbar + k, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    for (int k = 0; k < C::NCB; ++k) gen_request<P>(gn, a.tmc, m.craw, m.cbar, gn.cfirst + k);
+  auto words = [&](int i, int slot) {  // words of input plane z0 + i into ring slot `slot`
+    const int zz = z0 + i;
+    if (zz >= 1 && zz <= n - 1) {
+      const unsigned s = wring_s + (unsigned)(slot * NR * RW * 4);
+      wcopy(ws[0], s, i);
+      wcopy(ws[1], s, i);
+    }
+  };
+  int wsl = 0;  // ring slot of input plane i
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    if (i < nin) words(i, i);
+    cpa_commit();
+  }
+  double cr[R], sr[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
+  double ss = 0.0;
+  int tzo = ((z0 % P) + P) % P;  // node type of plane z0 + i (= of output plane z0 + i - P)
+  for (int i = 0; i < nin; ++i) {
+    const int zi = z0 + i;
+    const bool zu = zi >= 1 && zi <= n - 1;
+    if (i + PF < nin) words(i + PF, wsl + PF >= NW ? wsl + PF - NW : wsl + PF);
+    cpa_commit();
+    if (zu) gen_advance<P>(gn, m.pws, a.tmc, m.craw, m.cbar, m.PX, m.yvring, cbase<P>(zi) + P);
+    cpa_wait<PF>();
+    __syncthreads();  // (the words of plane zi, from every thread)
+    gen_z<P>(gn, cf, m.yvring, zi, n, m.box, zu ? m.wring + wsl * NR * RW : nullptr, a.wu);
+    wsl = wsl + 1 == NW ? 0 : wsl + 1;
+    __syncthreads();
+    xpass<P>(m.box, 0, km, kk, m.XA, m.XB, w, lane);
+    __syncthreads();
+    double c, s;
+    ypass<P>(cf, ty, m.XA, m.XB, w, lane, c, s);
+#pragma unroll
+    for (int o = 0; o < R - 1; ++o) {
+      cr[o] = cr[o + 1];
+      sr[o] = sr[o + 1];
+    }
+    cr[R - 1] = c;
+    sr[R - 1] = s;
+    if (i >= 2 * P) {
+      const int z = zi - P;
+      const double au = zpass<P>(cf, tzo, cr, sr) * hl;
+      if (rowok) {
+        const bool uz = unk1(z, n);
+        const double gz = uz ? gt[z] : 0.0;
+        const double t = (uxy && uz) ? gxy * gz - au : 0.0;  // (((C g(x)) g(y)) g(z)) - A u
+        *Tp = t;
+        ss = fma(t, t, ss);
+        warp_encode(t, a.wr, rmp, rep, lane, a.status);
+      }
+      Tp += tplane;
+      rmp += bpp * a.rstride;
+      rep += bpp;
+    }
+    tzo = tzo + 1 == P ? 0 : tzo + 1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+  if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)tl.cta * FW + w] = ss;
+}
+
+// b_L = dec r_L - A_L z_L with z_L = P w_{L-1} generated on chip -> B (the
+// t_L buffer).  Chebyshev step 1 (cFas1 of fmg_march3.cu).
+template <int P>
+__global__ void __launch_bounds__(32 * FW, 2) k_f3_cfas(const __grid_constant__ F3Args a,
+                                                          const __grid_constant__ Coefs cf) {
+  using C = F3<P>;
+  constexpr int R = C::R, NW = C::NW, PF = C::PF;
+  extern __shared__ __align__(128) double fsm[];
+  const int RW = a.wr + 1;
+  const GenSmem<P> m = gen_smem<P>(fsm, NW * FW * RW);
+  const unsigned wring_s = smem_u32(m.wring);
+
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const F3Tile tl = f3_tile(a);
+  const Geom g = a.g;
+  const int n = g.n;
+  const int x = tl.x0 + lane, y = tl.y0 + w;
+  const bool rowok = y < g.NY;
+  const int tx = x % P, ty = y % P;
+  double km[R], kk[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) {
+    km[o] = cf.Mc[tx][o];
+    kk[o] = cf.Kc[tx][o];
+  }
+  const double hl = pow2(-(a.l + 1));
+  const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
+  Gen<P> gn;
+  gen_init<P>(gn, g, tl.x0, tl.y0, 0, 0, [](int) { return 0; });
+  gen_range<P>(gn, z0, nin, n);
+  // r_L words of the warp's output row, output planes zs, zs + 1, ...
+  int eoff;
+  const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, a.wr, g, tl.x0, y, tl.zs, w * RW, rowok, lane, eoff);
+  const long long tplane = (long long)g.NY * g.NX;
+  double* Bp = a.T + ((long long)tl.zs * g.NY + y) * g.NX + x;
+  const int nout = tl.ze - tl.zs;
+  {
+    const int tid = w * 32 + lane;
+    if (tid < 2 * P * (P + 1)) m.pws[tid] = cf.Pw[tid / (P + 1)][tid % (P + 1)];
+  }
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < C::NCB; ++k) mbar_init(m.cbar + k, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    for (int k = 0; k < C::NCB; ++k) gen_request<P>(gn, a.tmc, m.craw, m.cbar, gn.cfirst + k);
+  // output plane j = 0..nout-1 (z = zs + j) is produced at iteration j + 2P;
+  // its words go to ring slot j % NW, issued PF outputs ahead
+#pragma unroll
+  for (int j = 0; j < PF; ++j) {
+    if (j < nout) wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
+    cpa_commit();
+  }
+  int osl = 0;  // ring slot of the next output plane
+  double cr[R], sr[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
+  int tzo = ((z0 % P) + P) % P;
+  for (int i = 0; i < nin; ++i) {
+    const int zi = z0 + i;
+    const bool produce = i >= 2 * P;
+    if (produce) {
+      const int j = i - 2 * P + PF;
+      if (j < nout) wcopy(ws, wring_s + (unsigned)((osl + PF >= NW ? osl + PF - NW : osl + PF) * FW * RW * 4), j);
+    }
+    cpa_commit();
+    if (zi >= 1 && zi <= n - 1) gen_advance<P>(gn, m.pws, a.tmc, m.craw, m.cbar, m.PX, m.yvring, cbase<P>(zi) + P);
+    gen_z<P>(gn, cf, m.yvring, zi, n, m.box, nullptr, 0);
+    cpa_wait<PF>();
+    __syncthreads();
+    xpass<P>(m.box, 0, km, kk, m.XA, m.XB, w, lane);
+    __syncthreads();
+    double c, s;
+    ypass<P>(cf, ty, m.XA, m.XB, w, lane, c, s);
+#pragma unroll
+    for (int o = 0; o < R - 1; ++o) {
+      cr[o] = cr[o + 1];
+      sr[o] = sr[o + 1];
+    }
+    cr[R - 1] = c;
+    sr[R - 1] = s;
+    if (produce) {
+      const double az = zpass<P>(cf, tzo, cr, sr) * hl;
+      if (rowok) {
+        const uint32_t* rec = m.wring + osl * FW * RW + w * RW;
+        const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
+        *Bp = rv - az;  // b = dec r - A z (B lives in the t_L buffer)
+      }
+      Bp += tplane;
+      osl = osl + 1 == NW ? 0 : osl + 1;
+    }
+    tzo = tzo + 1 == P ? 0 : tzo + 1;
+  }
+}
+
+// Chebyshev step j = J in {2, 3} at l = L: the staged boxes
+// are b (and d_2 for j = 3); y_{j-1} is recomputed on them (y_1 = inv_theta
+// (invD b), y_2 = y_1 + d_2), A y_{j-1}, then q = b - A y, d_j = fma(al_j,
+// d_{j-1}, be_j (invD q)), y_j = y_{j-1} + d_j.  A step below k stores d_j;
+// the last one encodes ý_L and applies the correction.
+template <int P, int J>
+__global__ void __launch_bounds__(32 * FW, 2) k_f3_cheb(const __grid_constant__ F3Args a,
+                                                          const __grid_constant__ Coefs cf) {
+  using C = F3<P>;
+  constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX, NBF = C::NBF, NW = C::NW, PF = C::PF;
+  constexpr int NA = J >= 3 ? 2 : 1;  // staged arrays: b (+ d_2)
+  extern __shared__ __align__(128) double fsm[];
+  double* ring = fsm;                        // NBF x NA boxes
+  double* yb = ring + NBF * NA * BOX;        // y_{j-1} on the current box
+  double* XA = yb + BOX;
+  double* XB = XA + NR * 32;
+  double* ivd = XB + NR * 32;                // invD factors: P node types x box
+  uint32_t* wring = (uint32_t*)(ivd + P * BOX);  // NW x FW x (w + 1) (last step: ú words)
+  const int RW = a.wu + 1;
+  unsigned long long* bars = (unsigned long long*)(wring + NW * FW * RW + 2);
+  bars = (unsigned long long*)(((uintptr_t)bars + 7) & ~(uintptr_t)7);
+
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const F3Tile tl = f3_tile(a);
+  const Geom g = a.g;
+  const int n = g.n;
+  const int x = tl.x0 + lane, y = tl.y0 + w;
+  const bool rowok = y < g.NY;
+  const int tx = x % P, ty = y % P;
+  double km[R], kk[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) {
+    km[o] = cf.Mc[tx][o];
+    kk[o] = cf.Kc[tx][o];
+  }
+  const double hl = pow2(-(a.l + 1));
+  const double al = cf.cal[J - 1], be = cf.cbe[J - 1], ith = cf.inv_theta;
+  const int hc = halo_col<P>(lane);
+  // invD factors of the thread's staged elements for every z node type
+  // (RN(1/diag) 2^(l+1), 0 at non-unknowns; the z-unknown test is per plane)
+  {
+    const double isc = pow2(a.l + 1);
+    const int xh = lane < P ? tl.x0 - P + lane : tl.x0 + 32 + lane - P;
+    const bool ux = unk1(x, n), uxh = lane < 2 * P && unk1(xh, n);
+    const int txo = ux ? x % P : 0, txh = uxh ? xh % P : 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int r = w + k * FW, yy = tl.y0 - P + r;
+      if (r < NR) {
+        const bool uy = unk1(yy, n);
+        const int tyy = uy ? yy % P : 0;
+#pragma unroll
+        for (int tz = 0; tz < P; ++tz) {
+          const int tb = (tz * P + tyy) * P;
+          ivd[tz * BOX + r * RS + P + lane] = (ux && uy) ? cf.invd[tb + txo] * isc : 0.0;
+          if (lane < 2 * P) ivd[tz * BOX + r * RS + hc] = (uxh && uy) ? cf.invd[tb + txh] * isc : 0.0;
+        }
+      }
+    }
+  }
+  const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
+  int eoff = 0;
+  const WStream ws = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, y, tl.zs, w * RW, rowok && a.last, lane,
+                              eoff);
+  const long long tplane = (long long)g.NY * g.NX;
+  const long long bpp = (long long)g.NY * (g.NX >> 5);
+  double* Dp = a.Dv + ((long long)tl.zs * g.NY + y) * g.NX + x;
+  const long long blk0 = ((long long)tl.zs * g.NY + y) * (g.NX >> 5) + (tl.x0 >> 5);
+  uint32_t* ump = a.umant + blk0 * a.ustride;
+  int8_t* uep = a.uexp + blk0;
+  const int nout = tl.ze - tl.zs;
+  const unsigned ring_s = smem_u32(ring), bars_s = smem_u32(bars), wring_s = smem_u32(wring);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < NBF; ++k) mbar_init(bars + k, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const int tmx = tl.x0 - P - (P & 1), tmy = tl.y0 - P;
+  auto stage = [&](int i, int slot) {  // input plane z0 + i into ring slot `slot` (TMA, thread 0)
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      const unsigned dst = ring_s + (unsigned)(slot * NA * BOX * 8), bar = bars_s + (unsigned)(slot * 8);
+      fence_async_smem();
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(NA * BOX * 8))
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];" ::"r"(dst),
+          "l"((unsigned long long)a.tmb), "r"(tmx), "r"(tmy), "r"(z0 + i), "r"(bar)
+          : "memory");
+      if (NA == 2)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+            "%4}], [%5];" ::"r"(dst + (unsigned)(BOX * 8)),
+            "l"((unsigned long long)a.tmd), "r"(tmx), "r"(tmy), "r"(z0 + i), "r"(bar)
+            : "memory");
+    }
+  };
+  // ring slots: input plane i -> slot i % NBF; ú words of output plane j -> slot j % NW
+#pragma unroll
+  for (int i = 0; i < PF; ++i)
+    if (i < nin) stage(i, i);
+#pragma unroll
+  for (int j = 0; j < PF; ++j) {
+    if (j < nout) wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
+    cpa_commit();
+  }
+  double cr[R], sr[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
+  int tz = ((z0 % P) + P) % P;   // node type of plane z0 + i (input; = output plane z0 + i - P)
+  int isl = 0, osl = 0, oisl = NBF - P;  // slots: input plane i, ú words of the next output, input plane i - P
+  unsigned par = 0;              // barrier phase of slot isl
+  for (int i = 0; i < nin; ++i) {
+    const int zi = z0 + i;
+    const bool produce = i >= 2 * P;
+    mbar_wait(bars + isl, par);
+    cpa_wait<PF - 1>();
+    __syncthreads();  // every thread is past iteration i - 1: slot (i + PF) % NBF is free
+    if (i + PF < nin) stage(i + PF, isl + PF >= NBF ? isl + PF - NBF : isl + PF);
+    if (produce) {
+      const int j = i - 2 * P + PF;
+      if (j < nout) wcopy(ws, wring_s + (unsigned)((osl + PF >= NW ? osl + PF - NW : osl + PF) * FW * RW * 4), j);
+    }
+    cpa_commit();
+    // y_{j-1} on the thread's staged elements of plane zi
+    {
+      const double* bb = ring + isl * NA * BOX + C::SH;
+      const double* iv = ivd + tz * BOX;
+      const bool uz = zi >= 1 && zi <= n - 1;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int r = w + k * FW;
+        if (r < NR) {
+          const int o = r * RS + P + lane;
+          const double f = uz ? iv[o] : 0.0;
+          double v = ith * (f * bb[o]);
+          if (J >= 3) v = v + bb[BOX + o];
+          yb[o] = v;
+          if (lane < 2 * P) {
+            const int oh = r * RS + hc;
+            const double fh = uz ? iv[oh] : 0.0;
+            double vh = ith * (fh * bb[oh]);
+            if (J >= 3) vh = vh + bb[BOX + oh];
+            yb[oh] = vh;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    xpass<P>(yb, 0, km, kk, XA, XB, w, lane);
+    __syncthreads();
+    double c, s;
+    ypass<P>(cf, ty, XA, XB, w, lane, c, s);
+#pragma unroll
+    for (int o = 0; o < R - 1; ++o) {
+      cr[o] = cr[o + 1];
+      sr[o] = sr[o + 1];
+    }
+    cr[R - 1] = c;
+    sr[R - 1] = s;
+    if (produce) {
+      const int z = zi - P;
+      const double ay = zpass<P>(cf, tz, cr, sr) * hl;
+      const int o = (w + P) * RS + P + lane;
+      const double* bo = ring + oisl * NA * BOX + C::SH + o;  // plane z, output point
+      const double b = bo[0];
+      const double f = (z >= 1 && z <= n - 1) ? ivd[tz * BOX + o] : 0.0;
+      double yprev = ith * (f * b);
+      double dprev = yprev;
+      if (J >= 3) {
+        dprev = bo[BOX];
+        yprev = yprev + dprev;
+      }
+      const double qq = b - ay;
+      const double d = fma(al, dprev, be * (f * qq));
+      const double yv = yprev + d;
+      if (a.last) {
+        const double yq = warp_encode(yv, a.wr, nullptr, nullptr, lane, a.status);
+        if (rowok) {
+          const uint32_t* rec = wring + osl * FW * RW + w * RW;
+          const double uo = warp_decode(rec, rec_e(rec + a.wu, eoff), a.wu, lane);
+          warp_encode(uo + yq, a.wu_out, ump, uep, lane, a.status);
+        }
+      } else if (rowok) {
+        *Dp = d;
+      }
+      Dp += tplane;
+      ump += bpp * a.ustride;
+      uep += bpp;
+      osl = osl + 1 == NW ? 0 : osl + 1;
+    }
+    tz = tz + 1 == P ? 0 : tz + 1;
+    oisl = oisl + 1 == NBF ? 0 : oisl + 1;
+    if (++isl == NBF) {
+      isl = 0;
+      par ^= 1u;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host --
+template <int P>
+static int smem_res(int wu) {
+  return (int)gen_smem_bytes<P>(F3<P>::NW * F3<P>::NR * (3 * wu + 2)) + 16;
+}
+template <int P>
+static int smem_cfas(int wr) {
+  return (int)gen_smem_bytes<P>(F3<P>::NW * FW * (wr + 1)) + 16;
+}
+template <int P>
+static int smem_cheb(int J, int wu) {
+  using C = F3<P>;
+  const int NA = J >= 3 ? 2 : 1;
+  size_t d = (size_t)C::NBF * NA * C::BOX + C::BOX + 2 * C::NR * 32 + (size_t)P * C::BOX;
+  size_t wbytes = (size_t)C::NW * FW * (wu + 1) * 4 + 8;
+  return (int)(d * 8 + wbytes + 8 + 8 * C::NBF + 16);
+}
+
+int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
+  switch (p) {
+    case 1: *cbx = F3<1>::CBX; *cby = F3<1>::CBY; *rs = F3<1>::RS; *nr = F3<1>::NR; return 0;
+    case 2: *cbx = F3<2>::CBX; *cby = F3<2>::CBY; *rs = F3<2>::RS; *nr = F3<2>::NR; return 0;
+    case 3: *cbx = F3<3>::CBX; *cby = F3<3>::CBY; *rs = F3<3>::RS; *nr = F3<3>::NR; return 0;
+    default: return -1;
+  }
+}
+
+void fine3_set_attributes() {
+  const int big = 200 * 1024;
+#define F(P)                                                                                 \
+  cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cfas<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);     \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  F(1) F(2) F(3)
+#undef F
+}
+
+template <typename K>
+static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Args& a, const Coefs& cf) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nctas);
+  cfg.blockDim = dim3(32, FW);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, a, cf);
+}
+
+// kind: 0 residual, 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3)
+void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf) {
+  const int n = a.nitems;
+#define F(P)                                                                                          \
+  if (kind == 0) f3_launch(k_f3_residual<P>, n, smem_res<P>(a.wu), st, a, cf);                        \
+  else if (kind == 1) f3_launch(k_f3_cfas<P>, n, smem_cfas<P>(a.wr), st, a, cf);                      \
+  else if (a.step == 2) f3_launch(k_f3_cheb<P, 2>, n, smem_cheb<P>(2, a.wu), st, a, cf);              \
+  else f3_launch(k_f3_cheb<P, 3>, n, smem_cheb<P>(3, a.wu), st, a, cf);
+  if (p == 1) { F(1) } else if (p == 2) { F(2) } else { F(3) }
+#undef F
+}
+
+}  // namespace fmg

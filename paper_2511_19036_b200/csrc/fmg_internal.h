@@ -108,6 +108,31 @@ struct MArgs {
   const CUtensorMap* tm;     // TMA map of the staged array, in device global memory
 };
 
+// Finest-level 3D kernels (fmg_fine3.cu): one launch of
+// k_f3_residual / k_f3_cfas / k_f3_cheb at level l = L of FMG level L.
+struct F3Args {
+  Geom g;                    // level l
+  int l, step, last;         // Chebyshev step (>= 2) and whether it is the last
+  int wr, wu, wu_out;        // w_r(L, L), current and new w_u of ú_L
+  int RC, nxb, nyb, nitems;  // planes per chunk, tile grid, CTAs
+  int zlo, zhi;              // planes of this rank
+  uint32_t* umant;
+  int8_t* uexp;
+  int ustride;
+  uint32_t* rmant;
+  int8_t* rexp;
+  int rstride;
+  const double* gtab;        // RHS table of level l
+  double* T;                 // t_L (residual) / b_L (cFas and Chebyshev: the same buffer)
+  double* Dv;                // Chebyshev direction d_2 (degree 3)
+  double* pbase;             // norm partials
+  long long poff;
+  int* status;
+  const CUtensorMap* tmc;    // coarse boxes of u_{L-1} (residual) / w_{L-1} (cFas), device copy
+  const CUtensorMap* tmb;    // fine boxes of b_L (the t_L buffer)
+  const CUtensorMap* tmd;    // fine boxes of d_2
+};
+
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.
 struct NormEntry {
   long long poff;
@@ -183,6 +208,9 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
 void march3_set_attributes();
 int march3_rows();
 void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);
+void fine3_set_attributes();
+int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr);
+void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf);
 void launch_coarse_nu(int dim, int p, cudaStream_t st, const void* devctx, const MArgs& a);  // nu > 1 level 0
 int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* rst, int n_ir, int lc_cap,
             KcLayout* ly, int* lc_out, int* cs_out);

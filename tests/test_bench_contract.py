@@ -47,7 +47,8 @@ def test_default_line():
     d = _run(["--steps", "2", "--warmup", "3"])
     _check_gpu_line(d)
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
-    assert d["config"]["workload"].startswith("C2")
+    assert d["config"]["workload"].startswith("C4")
+    assert d["repeat_bit_identical"] is True
 
 
 @pytest.mark.gpu

@@ -77,8 +77,8 @@ def test_eq61_constant_is_approached(d):
 def test_exponents_and_temporaries_sublinear(cfg):
     """Streaming exponents (N3) cost O(w) bits per section, far below one
     exponent per 32 entries; the streaming-window temporaries of Eq 6.2/6.3
-    are o(n_L) bits, while this implementation's full FP64 temporaries are
-    Theta(n_L) bytes (DESIGN.md §10)."""
+    are o(n_L) bits, while this implementation's FP64 temporaries are
+    Theta(n_L) bytes (DESIGN.md §4.3, §10)."""
     c = CONFIGS[cfg]
     d, p, lv = c["dim"], c["p"], c["levels"]
     m = P.memory_model(d, p, lv)
@@ -86,7 +86,16 @@ def test_exponents_and_temporaries_sublinear(cfg):
     assert m["exponent_bits_streaming"] < 0.01 * m["exponent_bits_fixed"]
     assert m["eq63_z_bits"] <= m["eq62_ut_bits"] / 2 + 1e-9
     assert m["eq62_ut_bits"] / n < 0.2 * (m["u_mantissa_bits"] / n)
-    assert m["fp64_temporary_bytes"] >= 9 * 8 * n
+    # hand count of the FP64 arrays create_impl allocates (stored points per level)
+    st = [(((p << (l + 1)) + 31) // 32 * 32) * (p << (l + 1)) ** (d - 1) for l in range(lv)]
+    L = lv - 1
+    k = default_schedule(d, p)["cheb_degree"]
+    if d == 3 and k in (2, 3):  # finest-level kernels: t_L (+ d_2 for degree 3); u, t, w below; scratch at L-1
+        want = st[L] * (1 + (k >= 3)) + 3 * sum(st[:L]) + 5 * st[L - 1]
+    else:                       # level-by-level kernels: u, t, w per level, six finest-size scratch arrays
+        want = 3 * sum(st) + 6 * st[L]
+    assert m["fp64_temporary_bytes"] == 8 * want
+    assert m["fp64_temporary_bytes"] >= 8 * n
 
 
 def test_memory_model_rejects_bad_arguments():
