@@ -37,6 +37,11 @@
 #ifndef F3_PF
 #define F3_PF 2      // staging / section-word lookahead (planes)
 #endif
+// CTAs per SM the register budget is sized for: P = 1 fits 3 (80 registers,
+// C3 -6 %), P = 3 needs ~128 registers (3 CTAs spill: C4 +18 %)
+#ifndef F3_MINB
+#define F3_MINB(P) ((P) == 3 ? 2 : 3)
+#endif
 
 namespace fmg {
 
@@ -63,6 +68,14 @@ struct F3 {
   static constexpr int NCY = P + 1;            // xy-passed coarse plane ring
 };
 
+__device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {  // bar: smem byte address
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -355,7 +368,7 @@ __device__ __forceinline__ void gen_advance(Gen<P>& gn, const double* pws, const
   constexpr int NCB = F3<P>::NCB, NCY = F3<P>::NCY, BOX = F3<P>::BOX;
   while (gn.cdone <= cneed) {
     const int c = gn.cdone, k = c - gn.cfirst;
-    mbar_wait(cbar + (k % NCB), (unsigned)(k / NCB) & 1u);
+    mbar_wait_s(smem_u32(cbar) + 8u * (unsigned)(k % NCB), (unsigned)(k / NCB) & 1u);
     gen_xy<P>(gn, pws, craw + (k % NCB) * F3<P>::CBS, PX, yvring + (c % NCY) * BOX);
     // (gen_xy synchronised after its x pass: the raw slot is free)
     if (threadIdx.x == 0 && threadIdx.y == 0) gen_request<P>(gn, tm, craw, cbar, c + NCB);
@@ -439,7 +452,7 @@ __host__ __device__ constexpr size_t gen_smem_bytes(int ring_words) {
 // t_L = f_L - A_L u_L with u_L = dec ú_L + P u_{L-1} generated on chip;
 // r_L = enc(t_L); t_L -> HBM; ||t_L||^2 partial per warp (Alg 3.2).
 template <int P>
-__global__ void __launch_bounds__(32 * FW, 2) k_f3_residual(const __grid_constant__ F3Args a,
+__global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual(const __grid_constant__ F3Args a,
                                                               const __grid_constant__ Coefs cf) {
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, NW = C::NW, PF = C::PF;
@@ -570,7 +583,7 @@ __global__ void __launch_bounds__(32 * FW, 2) k_f3_residual(const __grid_constan
 // b_L = dec r_L - A_L z_L with z_L = P w_{L-1} generated on chip -> B (the
 // t_L buffer).  Chebyshev step 1 (cFas1 of fmg_march3.cu).
 template <int P>
-__global__ void __launch_bounds__(32 * FW, 2) k_f3_cfas(const __grid_constant__ F3Args a,
+__global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_constant__ F3Args a,
                                                           const __grid_constant__ Coefs cf) {
   using C = F3<P>;
   constexpr int R = C::R, NW = C::NW, PF = C::PF;
@@ -672,7 +685,7 @@ __global__ void __launch_bounds__(32 * FW, 2) k_f3_cfas(const __grid_constant__ 
 // d_{j-1}, be_j (invD q)), y_j = y_{j-1} + d_j.  A step below k stores d_j;
 // the last one encodes ý_L and applies the correction.
 template <int P, int J>
-__global__ void __launch_bounds__(32 * FW, 2) k_f3_cheb(const __grid_constant__ F3Args a,
+__global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_constant__ F3Args a,
                                                           const __grid_constant__ Coefs cf) {
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX, NBF = C::NBF, NW = C::NW, PF = C::PF;
@@ -736,6 +749,7 @@ __global__ void __launch_bounds__(32 * FW, 2) k_f3_cheb(const __grid_constant__ 
   const long long blk0 = ((long long)tl.zs * g.NY + y) * (g.NX >> 5) + (tl.x0 >> 5);
   uint32_t* ump = a.umant + blk0 * a.ustride;
   int8_t* uep = a.uexp + blk0;
+  const long long ustep = bpp * a.ustride;
   const int nout = tl.ze - tl.zs;
   const unsigned ring_s = smem_u32(ring), bars_s = smem_u32(bars), wring_s = smem_u32(wring);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -784,7 +798,7 @@ __global__ void __launch_bounds__(32 * FW, 2) k_f3_cheb(const __grid_constant__ 
   for (int i = 0; i < nin; ++i) {
     const int zi = z0 + i;
     const bool produce = i >= 2 * P;
-    mbar_wait(bars + isl, par);
+    mbar_wait_s(bars_s + 8u * (unsigned)isl, par);
     cpa_wait<PF - 1>();
     __syncthreads();  // every thread is past iteration i - 1: slot (i + PF) % NBF is free
     if (i + PF < nin) stage(i + PF, isl + PF >= NBF ? isl + PF - NBF : isl + PF);
@@ -856,7 +870,7 @@ __global__ void __launch_bounds__(32 * FW, 2) k_f3_cheb(const __grid_constant__ 
         *Dp = d;
       }
       Dp += tplane;
-      ump += bpp * a.ustride;
+      ump += ustep;
       uep += bpp;
       osl = osl + 1 == NW ? 0 : osl + 1;
     }
