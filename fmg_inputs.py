@@ -15,6 +15,10 @@ CONFIGS = {
     "C3": dict(dim=3, p=1, levels=9, desc="3D Poisson Q1 512^3 elements, 9-level FMG"),
     "C4": dict(dim=3, p=3, levels=8, desc="3D Poisson Q3 256^3 elements, 8-level FMG"),
     "C5": dict(dim=3, p=1, levels=12, desc="3D Poisson Q1 4096^3 elements, 12-level FMG"),
+    # not a BASELINE config: C5's discretisation one level coarser, 8.6 G unknowns
+    # = C5's per-GPU share at 8 GPUs, the largest Q1 cube one B200 holds
+    # (SURVEY §8d-6 fallback: "a 2048^3 Q1 11-level problem")
+    "C5h": dict(dim=3, p=1, levels=11, desc="3D Poisson Q1 2048^3 elements, 11-level FMG (C5 per-GPU share)"),
 }
 
 # Chebyshev upper bounds: 1.05 x lambda_max(D^-1 A) from the p-periodic block

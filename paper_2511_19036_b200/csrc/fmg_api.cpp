@@ -1094,8 +1094,12 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   {
     const size_t scratch = sizeof(double) * c->g[c->fine3 ? Lmax - 1 : Lmax].size;
     const bool dv = !c->fine3 || s->cheb_degree >= 3;
+    // (fine3, degree 2: the level-by-level Chebyshev kernels of levels < L
+    // finish at step 2 and never write Y)
+    const bool y = !c->fine3 || s->cheb_degree >= 3;
     for (int i = 0; i < 6 && rc == FMG_OK; ++i) {
-      const size_t bytes = i == 4 ? (dv ? sizeof(double) * c->g[Lmax].size : 16) : scratch;
+      const size_t bytes = i == 4 ? (dv ? sizeof(double) * c->g[Lmax].size : 16)
+                                  : ((i == 2 || i == 3) && !y ? 16 : scratch);
       c->buf[i] = (double*)dalloc(c, bytes);
       if (!c->buf[i]) rc = FMG_ENOMEM;
       else cudaMemset(c->buf[i], 0, bytes);
@@ -1130,7 +1134,9 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, 0, 32 + 2 * pe, 1);
     } else if (!(c->fine3 && l == Lmax)) {  // (fine3: level Lmax has no u array, the scratch is one level smaller)
       ok &= make_tmap(&c->tmU[l], c->Ul[l], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
-      for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
+      for (int i = 0; i < 4; ++i)
+        if (!(c->fine3 && (i == 2 || i == 3) && s->cheb_degree < 3))
+          ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
     }
     if (!ok) rc = FMG_ECUDA;
   }
@@ -1636,7 +1642,7 @@ int fmg_memory_model(int dim, int p, int levels, const fmg_schedule* s, double* 
     // for degree 3 only.
     const bool f3 = dim == 3 && s->nu <= 1 && s->smoother == 0 && (s->cheb_degree == 2 || s->cheb_degree == 3) && L >= 1;
     fp64 += (f3 && l == L ? 1.0 : 3.0) * 8.0 * stored;
-    if (f3 && l == L - 1) fp64 += 5.0 * 8.0 * stored;
+    if (f3 && l == L - 1) fp64 += (s->cheb_degree >= 3 ? 5.0 : 3.0) * 8.0 * stored;  // Z, B, PU (+ Y[2])
     sec += 4.0 * (double)(NX * n * (dim == 3 ? n : 1) / 32) * (wul + wrl) + 2.0 * stored / 32.0;
     if (l == L) {
       nL = N;

@@ -91,7 +91,7 @@ def test_exponents_and_temporaries_sublinear(cfg):
     L = lv - 1
     k = default_schedule(d, p)["cheb_degree"]
     if d == 3 and k in (2, 3):  # finest-level kernels: t_L (+ d_2 for degree 3); u, t, w below; scratch at L-1
-        want = st[L] * (1 + (k >= 3)) + 3 * sum(st[:L]) + 5 * st[L - 1]
+        want = st[L] * (1 + (k >= 3)) + 3 * sum(st[:L]) + (5 if k >= 3 else 3) * st[L - 1]
     else:                       # level-by-level kernels: u, t, w per level, six finest-size scratch arrays
         want = 3 * sum(st) + 6 * st[L]
     assert m["fp64_temporary_bytes"] == 8 * want
