@@ -93,6 +93,12 @@ struct fmg_ctx {
   // exchanged before each stencil consumer, t_{lc+1} is gathered before KC)
   int G = 1, rank = 0;
   int zlo[kMaxLev]{}, zhi[kMaxLev]{};
+  // allocated plane window [wlo, whi) of every level array and section: the
+  // whole level, or on z slabs (levels > lc + 1) the rank's planes plus 2p
+  // ghost planes each side (memory partitioned over the ranks).
+  // Level pointers are shifted so that kernels index planes globally.
+  int wlo[kMaxLev]{}, whi[kMaxLev]{};
+  double* sbase[9]{};             // scratch allocations (buf[] are their level-0 views)
   std::vector<fmg_ctx*> sub;      // virtual slabs: G sub-contexts driven in lockstep (group handle)
   void* comm = nullptr;           // multi-GPU slabs: ncclComm_t (one rank per process)
   fmg_alloc_fn afn = nullptr;
@@ -548,6 +554,12 @@ LevelDev level_dev(const fmg_ctx* c, int l) {
   return v;
 }
 
+// Scratch buffer i as seen by level l: shifted so that level-l planes index
+// globally inside the level's window (z slabs; identity otherwise).
+double* sview(const fmg_ctx* c, int i, int l) {
+  return c->sbase[i] ? c->sbase[i] - (long long)c->g[l].NX * c->g[l].NY * c->wlo[l] : c->buf[i];
+}
+
 // March-kernel arguments of a grid op.
 MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
   MArgs m{};
@@ -572,7 +584,9 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
   m.lv = level_dev(c, o.l);
   const int lo = o.type == OP_RESTRICT ? o.l + 1 : o.l - 1;
   if (lo >= 0 && lo <= c->Lmax) m.lo = level_dev(c, lo);
-  m.p = MPtrs{c->buf[0], c->buf[1], {c->buf[2], c->buf[3]}, c->buf[4], c->buf[5], c->buf[8], c->pbase, c->status};
+  m.p = MPtrs{sview(c, 0, o.l), sview(c, 1, o.l), {sview(c, 2, o.l), sview(c, 3, o.l)}, sview(c, 4, o.l), sview(c, 5, o.l),
+              c->buf[8], c->pbase, c->status};
+  m.zoff = c->wlo[o.l];
   m.guess = o.guess;
   m.store = o.store;
   m.smode = o.smode;
@@ -620,7 +634,9 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.rstride = c->r[l].stride;
   a.gtab = c->gtab[l];
   a.T = c->Tl[l];
-  a.Dv = c->buf[4];
+  a.Dv = sview(c, 4, l);
+  a.zoff = c->wlo[l];
+  a.czoff = l >= 1 ? c->wlo[l - 1] : 0;
   a.pbase = c->pbase;
   a.poff = o.poff;
   a.status = c->status;
@@ -671,10 +687,10 @@ double* xarray(fmg_ctx* c, int arr, int l) {
     case XA_U: return c->Ul[l];
     case XA_T: return c->Tl[l];
     case XA_W: return c->Wl[l];
-    case XA_Z: return c->buf[0];
-    case XA_B: return c->buf[1];
-    case XA_Y0: return c->buf[2];
-    default: return c->buf[3];
+    case XA_Z: return sview(c, 0, l);
+    case XA_B: return sview(c, 1, l);
+    case XA_Y0: return sview(c, 2, l);
+    default: return sview(c, 3, l);
   }
 }
 
@@ -853,8 +869,10 @@ void issue_group(fmg_ctx* grp, const Builder& b) {
 
 void zero_sections(fmg_ctx* c) {
   for (int l = 0; l <= c->Lmax; ++l) {
-    cudaMemsetAsync(c->u[l].mant, 0, sizeof(uint32_t) * c->g[l].nblk * c->u[l].stride, c->cur);
-    cudaMemsetAsync(c->u[l].exps, 0x80, c->g[l].nblk, c->cur);
+    const long long bpp = (long long)(c->g[l].NX / 32) * c->g[l].NY, b0 = bpp * c->wlo[l];
+    const long long nb = bpp * (c->whi[l] - c->wlo[l]);
+    cudaMemsetAsync(c->u[l].mant + b0 * c->u[l].stride, 0, sizeof(uint32_t) * nb * c->u[l].stride, c->cur);
+    cudaMemsetAsync(c->u[l].exps + b0, 0x80, nb, c->cur);
   }
   cudaMemsetAsync(c->norms_dev, 0, sizeof(double) * c->levels * c->s.n_ir * c->levels, c->cur);
 }
@@ -987,18 +1005,8 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     int nt = c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2];
     c->u[l].stride = wu(c, l, Lmax);
     c->r[l].stride = wr(c, l, Lmax);
-    c->u[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->u[l].stride);
-    c->u[l].exps = (int8_t*)dalloc(c, g.nblk + 16);  // (+16: aligned 4-byte exponent reads, fmg_fine3.cu)
-    c->r[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->r[l].stride);
-    c->r[l].exps = (int8_t*)dalloc(c, g.nblk + 16);
-    if (s->nu > 1) {
-      c->ysec[l].stride = wr(c, l, Lmax);
-      c->ysec[l].mant = (uint32_t*)dalloc(c, sizeof(uint32_t) * g.nblk * c->ysec[l].stride);
-      c->ysec[l].exps = (int8_t*)dalloc(c, g.nblk);
-      if (!c->ysec[l].mant || !c->ysec[l].exps) { rc = FMG_ENOMEM; break; }
-    }
     c->gtab[l] = (double*)dalloc(c, sizeof(double) * g.n);
-    if (!c->u[l].mant || !c->u[l].exps || !c->r[l].mant || !c->r[l].exps || !c->gtab[l]) { rc = FMG_ENOMEM; break; }
+    if (!c->gtab[l]) { rc = FMG_ENOMEM; break; }
     std::vector<double> gt(g.n);
     build_rhs_table(p, l, gt.data());
     cudaMemcpy(c->gtab[l], gt.data(), sizeof(double) * g.n, cudaMemcpyHostToDevice);
@@ -1062,6 +1070,26 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       c->mitems[l] = tiles * nch;
     }
   }
+  // Plane windows (memory partition of z slabs) and the compact sections.
+  for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
+    const Geom& g = c->g[l];
+    const bool part = G > 1 && l > c->lc + 1;  // (level lc + 1: gathered in full for KC)
+    c->wlo[l] = part ? std::max(0, c->zlo[l] - 2 * p) : 0;
+    c->whi[l] = part ? std::min(g.NZ, c->zhi[l] + 2 * p) : g.NZ;
+    const long long bpp = (long long)(g.NX / 32) * g.NY, nb = bpp * (c->whi[l] - c->wlo[l]), b0 = bpp * c->wlo[l];
+    auto sec = [&](Sec& q, int stride) {
+      q.stride = stride;
+      uint32_t* m = (uint32_t*)dalloc(c, sizeof(uint32_t) * nb * stride);
+      int8_t* e = (int8_t*)dalloc(c, nb + 16);  // (+16: aligned 4-byte exponent reads, fmg_fine3.cu)
+      if (!m || !e) return false;
+      q.mant = m - b0 * stride;  // (global block indexing)
+      q.exps = e - b0;
+      return true;
+    };
+    if (!sec(c->u[l], wu(c, l, Lmax)) || !sec(c->r[l], wr(c, l, Lmax)) ||
+        (s->nu > 1 && !sec(c->ysec[l], wr(c, l, Lmax))))
+      rc = FMG_ENOMEM;
+  }
   // Finest-level kernels (fmg_fine3.cu): 3D, one GPU,
   // Chebyshev degree 2-3, nu = 1, KC for the coarse solve only.
   {
@@ -1075,32 +1103,31 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   // level keeps only t (which also holds b) and, for degree 3, Dv: its u, w
   // and the scratch of levels < Lmax are one level smaller.
   for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
-    size_t bytes = sizeof(double) * c->g[l].size;
+    const long long plane = (long long)c->g[l].NX * c->g[l].NY, off = plane * c->wlo[l];
+    const size_t bytes = sizeof(double) * plane * (c->whi[l] - c->wlo[l]);
     const bool top = c->fine3 && l == Lmax;
-    c->Tl[l] = (double*)dalloc(c, bytes);
-    if (!top) {
-      c->Ul[l] = (double*)dalloc(c, bytes);
-      c->Wl[l] = (double*)dalloc(c, bytes);
-    }
-    if (!c->Tl[l] || (!top && (!c->Ul[l] || !c->Wl[l]))) rc = FMG_ENOMEM;
-    else {
-      cudaMemset(c->Tl[l], 0, bytes);
-      if (!top) {
-        cudaMemset(c->Ul[l], 0, bytes);
-        cudaMemset(c->Wl[l], 0, bytes);
-      }
-    }
+    auto arr = [&](double*& a) {
+      double* q = (double*)dalloc(c, bytes);
+      if (q) cudaMemset(q, 0, bytes);
+      a = q ? q - off : nullptr;  // (global plane indexing)
+      return q != nullptr;
+    };
+    if (!arr(c->Tl[l]) || (!top && (!arr(c->Ul[l]) || !arr(c->Wl[l])))) rc = FMG_ENOMEM;
   }
   {
-    const size_t scratch = sizeof(double) * c->g[c->fine3 ? Lmax - 1 : Lmax].size;
+    // scratch: each buffer serves one level at a time with that level's
+    // window, so it is sized for the largest window it serves
+    auto win = [&](int l) { return (size_t)c->g[l].NX * c->g[l].NY * (c->whi[l] - c->wlo[l]); };
+    size_t scratch = 0;
+    for (int l = 0; l <= (c->fine3 ? Lmax - 1 : Lmax); ++l) scratch = std::max(scratch, win(l));
     const bool dv = !c->fine3 || s->cheb_degree >= 3;
     // (fine3, degree 2: the level-by-level Chebyshev kernels of levels < L
     // finish at step 2 and never write Y)
     const bool y = !c->fine3 || s->cheb_degree >= 3;
     for (int i = 0; i < 6 && rc == FMG_OK; ++i) {
-      const size_t bytes = i == 4 ? (dv ? sizeof(double) * c->g[Lmax].size : 16)
-                                  : ((i == 2 || i == 3) && !y ? 16 : scratch);
+      const size_t bytes = sizeof(double) * (i == 4 ? (dv ? win(Lmax) : 2) : ((i == 2 || i == 3) && !y ? 2 : scratch));
       c->buf[i] = (double*)dalloc(c, bytes);
+      c->sbase[i] = c->buf[i];
       if (!c->buf[i]) rc = FMG_ENOMEM;
       else cudaMemset(c->buf[i], 0, bytes);
     }
@@ -1133,10 +1160,13 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       ok &= make_tmap(&c->tmT[l], c->Tl[l], g.NX, g.NY, 0, 64 + 4 * p, 1);
       for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, 0, 32 + 2 * pe, 1);
     } else if (!(c->fine3 && l == Lmax)) {  // (fine3: level Lmax has no u array, the scratch is one level smaller)
-      ok &= make_tmap(&c->tmU[l], c->Ul[l], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
+      // maps over the level's plane window (TMA coordinates z - wlo)
+      const long long off = (long long)g.NX * g.NY * c->wlo[l];
+      const int nz = c->whi[l] - c->wlo[l];
+      ok &= make_tmap(&c->tmU[l], c->Ul[l] + off, g.NX, g.NY, nz, 40, 8 + 2 * p);
       for (int i = 0; i < 4; ++i)
         if (!(c->fine3 && (i == 2 || i == 3) && s->cheb_degree < 3))
-          ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, g.NZ, 40, 8 + 2 * p);
+          ok &= make_tmap(&c->tmB[i][l], c->sbase[i], g.NX, g.NY, nz, 40, 8 + 2 * p);
     }
     if (!ok) rc = FMG_ECUDA;
   }
@@ -1147,13 +1177,15 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     int cbx = 0, cby = 0, rs = 0, nr = 0;
     fine3_box_dims(p, &cbx, &cby, &rs, &nr);
     bool ok = true;
+    const long long off = (long long)g.NX * g.NY * c->wlo[l];
+    const int nz = c->whi[l] - c->wlo[l];
     if (l < Lmax) {
-      ok &= make_tmap(&c->tmCU[l], c->Ul[l], g.NX, g.NY, g.NZ, cbx, cby);
-      ok &= make_tmap(&c->tmCW[l], c->Wl[l], g.NX, g.NY, g.NZ, cbx, cby);
+      ok &= make_tmap(&c->tmCU[l], c->Ul[l] + off, g.NX, g.NY, nz, cbx, cby);
+      ok &= make_tmap(&c->tmCW[l], c->Wl[l] + off, g.NX, g.NY, nz, cbx, cby);
     }
     if (l >= 1) {
-      ok &= make_tmap(&c->tmFB[l], c->Tl[l], g.NX, g.NY, g.NZ, rs, nr);
-      if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->buf[4], g.NX, g.NY, g.NZ, rs, nr);
+      ok &= make_tmap(&c->tmFB[l], c->Tl[l] + off, g.NX, g.NY, nz, rs, nr);
+      if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->sbase[4], g.NX, g.NY, nz, rs, nr);
     }
     if (!ok) rc = FMG_ECUDA;
   }
@@ -1564,14 +1596,16 @@ int fmg_get_section(fmg_ctx* c, int which, int level, uint32_t* mant, int8_t* ex
   *width = w;
   cudaError_t e = cudaStreamSynchronize(c->st);
   if (e != cudaSuccess) return cuda_err(e);
+  // the allocated plane window (the whole level unless partitioned over z slabs)
+  const long long bpp = (long long)(g.NX / 32) * g.NY, b0 = bpp * c->wlo[level], nb = bpp * (c->whi[level] - c->wlo[level]);
   if (mant) {
-    std::vector<uint32_t> tmp((size_t)g.nblk * s.stride);
-    e = cudaMemcpy(tmp.data(), s.mant, sizeof(uint32_t) * tmp.size(), cudaMemcpyDeviceToHost);
+    std::vector<uint32_t> tmp((size_t)nb * s.stride);
+    e = cudaMemcpy(tmp.data(), s.mant + b0 * s.stride, sizeof(uint32_t) * tmp.size(), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_err(e);
-    for (long long b = 0; b < g.nblk; ++b) std::memcpy(mant + b * w, tmp.data() + b * s.stride, sizeof(uint32_t) * w);
+    for (long long b = 0; b < nb; ++b) std::memcpy(mant + (b0 + b) * w, tmp.data() + b * s.stride, sizeof(uint32_t) * w);
   }
   if (exps) {
-    e = cudaMemcpy(exps, s.exps, g.nblk, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(exps + b0, s.exps + b0, nb, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_err(e);
   }
   return FMG_OK;
@@ -1751,18 +1785,21 @@ int fmg_get_rhs(fmg_ctx* c, double* host) {
 
 int64_t fmg_export_solution(fmg_ctx* c, void* host, int64_t cap) {
   if (!c) return -FMG_EINVAL;
+  // every level's allocated window of ú (mantissa words, then exponents)
+  auto nblocks = [&](int l) { return (int64_t)(c->g[l].NX / 32) * c->g[l].NY * (c->whi[l] - c->wlo[l]); };
   int64_t need = 0;
-  for (int l = 0; l <= c->Lmax; ++l) need += (int64_t)c->g[l].nblk * (4 * c->u[l].stride + 1);
+  for (int l = 0; l <= c->Lmax; ++l) need += nblocks(l) * (4 * c->u[l].stride + 1);
   if (!host || cap < need) return need;
   char* dst = (char*)host;
   for (int l = 0; l <= c->Lmax; ++l) {
-    size_t mb = sizeof(uint32_t) * c->g[l].nblk * c->u[l].stride;
-    cudaError_t e = cudaMemcpyAsync(dst, c->u[l].mant, mb, cudaMemcpyDeviceToHost, c->st);
+    const int64_t b0 = (int64_t)(c->g[l].NX / 32) * c->g[l].NY * c->wlo[l], nb = nblocks(l);
+    size_t mb = sizeof(uint32_t) * nb * c->u[l].stride;
+    cudaError_t e = cudaMemcpyAsync(dst, c->u[l].mant + b0 * c->u[l].stride, mb, cudaMemcpyDeviceToHost, c->st);
     if (e != cudaSuccess) return -cuda_err(e);
     dst += mb;
-    e = cudaMemcpyAsync(dst, c->u[l].exps, c->g[l].nblk, cudaMemcpyDeviceToHost, c->st);
+    e = cudaMemcpyAsync(dst, c->u[l].exps + b0, nb, cudaMemcpyDeviceToHost, c->st);
     if (e != cudaSuccess) return -cuda_err(e);
-    dst += c->g[l].nblk;
+    dst += nb;
   }
   return need;
 }

@@ -263,6 +263,7 @@ struct Gen {
   int cfirst;    // first coarse plane of the march (ring slots and barrier phases count from it)
   int clast;     // last coarse plane the march needs (no request beyond: no TMA left in flight)
   int cdone;     // next coarse plane to xy-pass
+  int czoff;     // first allocated plane of the coarse array (TMA coordinates are window-relative)
 };
 
 // Element tables.  `rw` (record words per row, 0: no decode), `eoffr(r)`
@@ -349,7 +350,7 @@ __device__ __forceinline__ void gen_request(const Gen<P>& gn, const CUtensorMap*
   if (c > gn.clast) return;
   const int k = (c - gn.cfirst) % NCB;
   fence_async_smem();
-  tma_load_3d(craw + k * F3<P>::CBS, tm, gn.cx0, gn.cy0, c, cbar + k, (unsigned)(F3<P>::CBOX * 8));
+  tma_load_3d(craw + k * F3<P>::CBS, tm, gn.cx0, gn.cy0, c - gn.czoff, cbar + k, (unsigned)(F3<P>::CBOX * 8));
 }
 // Coarse planes of a march over fine input planes [z0, z0 + nin): the first
 // and last unknown fine planes decide them (none: cfirst > clast).
@@ -486,6 +487,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual(const __gri
     return (int)((b0 - 1) - ((b0 - 1) & ~3LL));
   });
   gen_range<P>(gn, z0, nin, n);
+  gn.czoff = a.czoff;
   // section word streams of the warp's (up to) two box rows: only unknown
   // rows are decoded (the section and u are 0 elsewhere)
   WStream ws[2];
@@ -610,6 +612,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_co
   Gen<P> gn;
   gen_init<P>(gn, g, tl.x0, tl.y0, 0, 0, [](int) { return 0; });
   gen_range<P>(gn, z0, nin, n);
+  gn.czoff = a.czoff;
   // r_L words of the warp's output row, output planes zs, zs + 1, ...
   int eoff;
   const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, a.wr, g, tl.x0, y, tl.zs, w * RW, rowok, lane, eoff);
@@ -770,13 +773,13 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
           "[%5];" ::"r"(dst),
-          "l"((unsigned long long)a.tmb), "r"(tmx), "r"(tmy), "r"(z0 + i), "r"(bar)
+          "l"((unsigned long long)a.tmb), "r"(tmx), "r"(tmy), "r"(z0 + i - a.zoff), "r"(bar)
           : "memory");
       if (NA == 2)
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
             "%4}], [%5];" ::"r"(dst + (unsigned)(BOX * 8)),
-            "l"((unsigned long long)a.tmd), "r"(tmx), "r"(tmy), "r"(z0 + i), "r"(bar)
+            "l"((unsigned long long)a.tmd), "r"(tmx), "r"(tmy), "r"(z0 + i - a.zoff), "r"(bar)
             : "memory");
     }
   };

@@ -105,6 +105,7 @@ struct MArgs {
   // none when the kernel stages nothing from global memory;
   // kept in device memory so the launch parameters stay small
   int tma;                   // 1: tm is valid and the kernel stages through it
+  int zoff;                  // first plane of the staged array's allocation (z slabs keep a plane window; 0 otherwise)
   const CUtensorMap* tm;     // TMA map of the staged array, in device global memory
 };
 
@@ -116,6 +117,7 @@ struct F3Args {
   int wr, wu, wu_out;        // w_r(L, L), current and new w_u of ú_L
   int RC, nxb, nyb, nitems;  // planes per chunk, tile grid, CTAs
   int zlo, zhi;              // planes of this rank
+  int zoff, czoff;           // first allocated plane of level l / l - 1 (TMA coordinates are window-relative)
   uint32_t* umant;
   int8_t* uexp;
   int ustride;

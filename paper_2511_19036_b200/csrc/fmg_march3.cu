@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_residual(const
   double ss = 0.0;
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
-        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz - a.zoff, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(U, g, it.x0, it.y0, zz, P, slot);
       },
       [&](int, double*) {},
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cfas1(const De
   const int nxb = g.NX >> 5;
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
-        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz - a.zoff, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(c.Z, g, it.x0, it.y0, zz, P, slot);
       },
       [&](int zz, double* slot) {
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_cheb(const Dev
   }
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
-        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz - a.zoff, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(src, g, it.x0, it.y0, zz, P, slot);
       },
       [&](int zz, double* slot) {
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_gs(const DevCt
   const bool colxy = x % (P + 1) == cx && y % (P + 1) == cy;
   march3_A<P>(
       cf, it, a.l, ring, XA, XB, [&](int zz, double* slot) {
-        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
+        if (bars) stage_box_tma(a.tm, it.x0, it.y0, zz - a.zoff, P, slot, bars + (slot - ring) / ((TW3 + 2 * P) * RS3));
         else stage_box(Yv, g, it.x0, it.y0, zz, P, slot);
       },
       [&](int, double*) {},

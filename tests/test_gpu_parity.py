@@ -270,6 +270,21 @@ def test_slab_decomposition_invariance(P, d, p, levels, G):
         assert np.array_equal(eo, eg) and np.array_equal(mo, mg), l
 
 
+def test_slab_memory_partitioned(P, monkeypatch):
+    """z slabs partition the memory: a rank allocates its own
+    planes plus 2p ghost planes each side of every level above the gathered
+    coarse levels, so G ranks together hold about what one undecomposed
+    context of the same kernels holds, not G times it."""
+    monkeypatch.setenv("FMG_FINE3", "0")  # (slab contexts run the level-by-level kernels)
+    one = P.Solver(3, 1, 8)
+    b1 = one.device_bytes()
+    one.close()
+    for G in (2, 4):
+        sg = P.Solver(3, 1, 8, slabs=G)
+        assert sg.device_bytes() <= 1.15 * b1, (G, sg.device_bytes(), b1)
+        sg.close()
+
+
 def test_slab_partial_solve(P):
     sg = P.Solver(3, 2, 5, slabs=4)
     sg.solve_upto(3, 2)
