@@ -88,6 +88,7 @@ struct fmg_ctx {
   // and, for degree 3, the direction d_2.  FMG_FINE3=0 selects the
   // level-by-level kernels everywhere.
   bool fine3 = false;
+  int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
   // exchanged before each stencil consumer, t_{lc+1} is gathered before KC)
@@ -182,7 +183,7 @@ struct Item {
   int timed_cls;     // kernel-timing class of a grid item (-1: none)
   int xarr, xl, xdepth, xgather;  // exchange item: array, level, ghost depth, gather-all
 };
-enum { XA_U = 0, XA_T, XA_W, XA_Z, XA_B, XA_Y0, XA_Y1 };
+enum { XA_U = 0, XA_T, XA_W, XA_Z, XA_B, XA_Y0, XA_Y1, XA_D, XA_SU };  // XA_SU: the ú section (BFP words + exponents)
 
 struct Builder {
   fmg_ctx* c;
@@ -400,12 +401,19 @@ void build_iteration(Builder& b, int L, int it) {
   const int row = L * c->s.n_ir + it;
   const int P = c->p;
   if (L > lc) {
-    b.xchg(XA_U, L, P);
     OpDesc o = mkop(OP_RESIDUAL, L, L);
     o.wr = wr(c, L, L);
+    o.wu_in = c->wu_cur[L];
     o.row = row;
     o.poff = b.slot(row, L);
-    b.grid(o, fine ? 0 : -1);
+    if (c->fine3) {  // u_L generated on chip from ú_L (BFP ghost planes) and u_{L-1} (fmg_fine3.cu)
+      b.xchg(XA_SU, L, P);
+      b.xchg(XA_U, L - 1, 2 * P);
+      b.fine(0, o, fine ? 0 : -1);
+    } else {
+      b.xchg(XA_U, L, P);
+      b.grid(o, fine ? 0 : -1);
+    }
     for (int l = L - 1; l > lc; --l) {
       b.xchg(XA_T, l + 1, 2 * P - 1);
       OpDesc q = mkop(OP_RESTRICT, l, L);
@@ -430,6 +438,22 @@ void build_iteration(Builder& b, int L, int it) {
   }
   const int k = c->s.cheb_degree;
   for (int l = lc + 1; l <= L; ++l) {
+    if (c->fine3 && l == L) {  // z_L generated on chip; b_L in the t_L buffer (fmg_fine3.cu)
+      b.xchg(XA_W, L - 1, 2 * P);
+      for (int step = 1; step <= k; ++step) {
+        if (step >= 2) b.xchg(XA_T, L, P);           // b_L
+        if (step >= 3) b.xchg(XA_D, L, P);           // d_2
+        OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
+        q.step = step;
+        q.last = step == k;
+        q.wr = wr(c, l, L);
+        q.wu_in = c->wu_cur[l];
+        q.wu_out = wu(c, l, L);
+        b.fine(step == 1 ? 1 : 2, q, fine ? (step == k ? 5 : 1) : -1);
+      }
+      c->wu_cur[l] = wu(c, l, L);
+      continue;
+    }
     if (c->march && c->dim == 3) {  // z_l = P w_{l-1}, P u_{l-1} (fmg_march3.cu k_m3_prolong)
       b.xchg(XA_W, l - 1, P);
       b.xchg(XA_U, l - 1, P);
@@ -481,14 +505,18 @@ void build_solve(Builder& b, int Lstop, int iters_last) {
     // ú_{0..L-1} is value-preserving and happens at the next encode.
     c->wu_cur[L] = wu(c, L, L);
     // u_L = dec ú_L + P u_{L-1} = P u_{L-1} for the first residual
-    b.xchg(XA_U, L - 1, c->p);
     if (c->fine3) {
-      // u_{L-1} = dec ú_{L-1} + P u_{L-2}: level L-1 was the finest level of
-      // FMG level L-1, whose kernels keep no u array (fmg_fine3.cu)
-      OpDesc o = mkop(OP_DECODE, L - 1, L - 1);
-      o.wu_in = c->wu_cur[L - 1];
-      b.grid(o, -1);
+      // u_{L-1} = dec ú_{L-1} + P u_{L-2}: a grid level L-1 was the finest
+      // level of FMG level L-1, whose kernels keep no u array (fmg_fine3.cu);
+      // the cluster kernel writes u_l of its levels <= lc itself
+      if (L - 1 > lc) {
+        b.xchg(XA_U, L - 2, c->p);
+        OpDesc o = mkop(OP_DECODE, L - 1, L - 1);
+        o.wu_in = c->wu_cur[L - 1];
+        b.grid(o, -1);
+      }
     } else {
+      b.xchg(XA_U, L - 1, c->p);
       OpDesc o = mkop(OP_DECODE, L, L);
       o.wu_in = c->wu_cur[L];
       b.grid(o, (L == c->Lmax) ? 2 : -1);
@@ -690,8 +718,27 @@ double* xarray(fmg_ctx* c, int arr, int l) {
     case XA_Z: return sview(c, 0, l);
     case XA_B: return sview(c, 1, l);
     case XA_Y0: return sview(c, 2, l);
+    case XA_D: return sview(c, 4, l);
     default: return sview(c, 3, l);
   }
+}
+// The raw buffers an exchange item moves, as (globally indexed base, bytes per
+// plane): one FP64 array, or a section's mantissa words and exponents (the
+// compressed ghost planes of the finest-level kernels).
+struct XBuf {
+  char* base;
+  size_t plane;
+};
+int xbufs(fmg_ctx* c, int arr, int l, XBuf* out) {
+  const Geom& g = c->g[l];
+  if (arr == XA_SU) {
+    const size_t bpp = (size_t)(g.NX / 32) * g.NY;
+    out[0] = {(char*)c->u[l].mant, bpp * c->u[l].stride * sizeof(uint32_t)};
+    out[1] = {(char*)c->u[l].exps, bpp};
+    return 2;
+  }
+  out[0] = {(char*)xarray(c, arr, l), (size_t)g.NX * g.NY * sizeof(double)};
+  return 1;
 }
 
 // ---- exchange plan (shared by virtual slabs and NCCL ranks) ----------------
@@ -781,26 +828,32 @@ NcclApi& nccl() {
 // Multi-GPU slabs: the same plan as grouped NCCL point-to-point transfers over
 // NVLink (a gather is an in-place all-gather), on the context stream (captured
 // into the solve graph).
-void nccl_exchange(fmg_ctx* c, const Item& it) {
+int nccl_exchange(fmg_ctx* c, const Item& it) {
   NcclApi& N = nccl();
   const int l = it.xl;
   const Geom& g = c->g[l];
-  const size_t plane = (size_t)g.NX * g.NY;
-  double* arr = xarray(c, it.xarr, l);
   ncclComm_t comm = (ncclComm_t)c->comm;
-  if (it.xgather) {
+  XBuf xb[2];
+  const int nb = xbufs(c, it.xarr, l, xb);
+  if (it.xgather) {  // (FP64 t of level lc + 1: full arrays)
+    const size_t plane = xb[0].plane;
     const size_t cnt = plane * (size_t)(g.NZ / c->G);
-    N.allGather(arr + (size_t)c->zlo[l] * plane, arr, cnt, ncclDouble, comm, c->cur);
-    return;
+    if (N.allGather(xb[0].base + (size_t)c->zlo[l] * plane, xb[0].base, cnt, ncclUint8, comm, c->cur) != ncclSuccess)
+      return FMG_ENCCL;
+    return FMG_OK;
   }
-  N.groupStart();
+  if (N.groupStart() != ncclSuccess) return FMG_ENCCL;
+  bool ok = true;
   for (const XPiece& q : slab_plan(g.NZ, c->G, c->rank, it.xdepth, 0)) {
-    double* p = arr + (size_t)q.z0 * plane;
-    const size_t cnt = plane * (size_t)(q.z1 - q.z0);
-    if (q.send) N.send(p, cnt, ncclDouble, q.peer, comm, c->cur);
-    else N.recv(p, cnt, ncclDouble, q.peer, comm, c->cur);
+    for (int k = 0; k < nb; ++k) {
+      char* p = xb[k].base + (size_t)q.z0 * xb[k].plane;
+      const size_t cnt = xb[k].plane * (size_t)(q.z1 - q.z0);
+      ok &= (q.send ? N.send(p, cnt, ncclUint8, q.peer, comm, c->cur)
+                    : N.recv(p, cnt, ncclUint8, q.peer, comm, c->cur)) == ncclSuccess;
+    }
   }
-  N.groupEnd();
+  ok &= N.groupEnd() == ncclSuccess;
+  return ok ? FMG_OK : FMG_ENCCL;
 }
 
 // Virtual z slabs: fill the ghost planes (or, for a gather, every foreign plane)
@@ -809,14 +862,16 @@ void nccl_exchange(fmg_ctx* c, const Item& it) {
 void group_exchange(fmg_ctx* grp, const Item& it) {
   const int G = (int)grp->sub.size(), l = it.xl;
   const Geom& g = grp->sub[0]->g[l];
-  const size_t plane = (size_t)g.NX * g.NY;
   for (int r = 0; r < G; ++r) {
     fmg_ctx* dst = grp->sub[r];
     for (const XPiece& q : slab_plan(g.NZ, G, r, it.xdepth, it.xgather)) {
       if (q.send) continue;  // (the receiving side performs each copy)
-      double* d = xarray(dst, it.xarr, l) + (size_t)q.z0 * plane;
-      const double* s = xarray(grp->sub[q.peer], it.xarr, l) + (size_t)q.z0 * plane;
-      cudaMemcpyAsync(d, s, sizeof(double) * plane * (q.z1 - q.z0), cudaMemcpyDeviceToDevice, dst->cur);
+      XBuf xd[2], xs[2];
+      const int nb = xbufs(dst, it.xarr, l, xd);
+      xbufs(grp->sub[q.peer], it.xarr, l, xs);
+      for (int k = 0; k < nb; ++k)
+        cudaMemcpyAsync(xd[k].base + (size_t)q.z0 * xd[k].plane, xs[k].base + (size_t)q.z0 * xs[k].plane,
+                        xd[k].plane * (q.z1 - q.z0), cudaMemcpyDeviceToDevice, dst->cur);
     }
   }
 }
@@ -833,7 +888,7 @@ void issue(fmg_ctx* c, const Builder& b) {
   for (size_t ii = 0; ii < b.items.size(); ++ii) {
     const Item& it = b.items[ii];
     if (it.kind == 2) {  // ghost planes: NCCL ranks (single-rank contexts have none)
-      if (c->comm) nccl_exchange(c, it);
+      if (c->comm && nccl_exchange(c, it) != FMG_OK) c->nccl_err = 1;
       continue;
     }
     issue_item(c, it);
@@ -907,9 +962,11 @@ int run_direct(fmg_ctx* c, Builder& b) {
   cudaStreamSynchronize(c->st);
   int prc = prepare(c, b, 1);
   if (prc) return prc;
+  c->nccl_err = 0;
   issue(c, b);
   c->timing_cls = save;
   c->launches = save_l;
+  if (c->nccl_err) return FMG_ENCCL;
   return sync_check(c);
 }
 
@@ -1090,12 +1147,13 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
         (s->nu > 1 && !sec(c->ysec[l], wr(c, l, Lmax))))
       rc = FMG_ENOMEM;
   }
-  // Finest-level kernels (fmg_fine3.cu): 3D, one GPU,
-  // Chebyshev degree 2-3, nu = 1, KC for the coarse solve only.
+  // Finest-level kernels (fmg_fine3.cu): 3D, Chebyshev
+  // degree 2-3, nu = 1, a grid level above the cluster kernel's, b_u <= 10
+  // (the residual's three-block section records fit one warp).
   {
     const char* e = getenv("FMG_FINE3");
-    c->fine3 = rc == FMG_OK && dim == 3 && c->march && G == 1 && s->nu <= 1 && s->smoother == 0 &&
-               (s->cheb_degree == 2 || s->cheb_degree == 3) && c->lc == 0 && Lmax >= 1 && !(e && atoi(e) == 0);
+    c->fine3 = rc == FMG_OK && dim == 3 && c->march && s->nu <= 1 && s->smoother == 0 &&
+               (s->cheb_degree == 2 || s->cheb_degree == 3) && Lmax > c->lc && s->b_u <= 10 && !(e && atoi(e) == 0);
   }
   // FP64 workspace.  Level arrays u_l, t_l, w_l (padded level layout); the
   // scratch Z, B, Y[2], PU of the level-by-level kernels and the Chebyshev
@@ -1403,10 +1461,12 @@ int fmg_solve_async(fmg_ctx* c) {
     cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return cuda_err(e);
     zero_sections(c);
+    c->nccl_err = 0;
     issue(c, b);
     cudaGraph_t gr;
     e = cudaStreamEndCapture(c->cap, &gr);
     if (e != cudaSuccess) return cuda_err(e);
+    if (c->nccl_err) return FMG_ENCCL;
     e = cudaGraphInstantiate(&c->graph, gr, 0);
     cudaGraphDestroy(gr);
     if (e != cudaSuccess) { c->graph = nullptr; return cuda_err(e); }
