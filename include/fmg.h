@@ -114,6 +114,26 @@ int fmg_nccl_unique_id(void* id);
 int fmg_create_dist(int dim, int p, int levels, const fmg_schedule* s, int nranks, int rank, const void* id,
                     void* stream, fmg_ctx** out);
 
+/* z slabs with a HOST-STAGED transport (one process per rank; ranks may share
+ * a device): the same decomposition, exchange plan and memory partition as
+ * fmg_create_dist, but every exchange is handed to the caller.  At each
+ * exchange the library synchronises the stream, copies the send pieces
+ * device -> host, calls
+ *     fn(user, n, peer[], send[], buf[], bytes[])
+ * with all n pieces of the exchange (send[i] = 1: buf[i] holds bytes[i] to
+ * deliver to rank peer[i]; 0: receive bytes[i] from peer[i] into buf[i]),
+ * and copies the received pieces host -> device.  fn must complete every
+ * piece before returning (e.g. torch.distributed isend/irecv over gloo, then
+ * wait) and return 0, else the solve fails with FMG_ENCCL.  Pieces are listed
+ * in the order of fmg_slab_plan.  Solves run directly on `stream` (no graph:
+ * the callback runs between kernels); fmg_norms sums the slab partials
+ * through fn as well.  The buffers are library-owned and valid only during
+ * the call.  Errors: as fmg_create_slabs. */
+typedef int (*fmg_xfer_fn)(void* user, int n, const int* peer, const int* send, void* const* buf,
+                           const int64_t* bytes);
+int fmg_create_hostx(int dim, int p, int levels, const fmg_schedule* s, int nranks, int rank, fmg_xfer_fn fn,
+                     void* user, void* stream, fmg_ctx** out);
+
 /* Host-only helper (no device work): the ghost-plane exchange plan of rank
  * `rank` of `nslabs` equal slabs of `nz` planes for halo depth `depth` (or a
  * gather of every foreign plane): up to `cap` pieces of 4 ints {peer, z0, z1,

@@ -53,6 +53,11 @@ _lib.fmg_create_slabs.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule)
 _lib.fmg_create_dist.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule), C.c_int, C.c_int, _vp, _vp,
                                  C.POINTER(_vp)]
 _lib.fmg_nccl_unique_id.argtypes = [_vp]
+# host-staged transport callback: fn(user, n, peer[], send[], buf[], bytes[]) -> 0
+_XFER_FN = C.CFUNCTYPE(C.c_int, _vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(_vp),
+                       C.POINTER(C.c_int64))
+_lib.fmg_create_hostx.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(Schedule), C.c_int, C.c_int, _XFER_FN, _vp,
+                                  _vp, C.POINTER(_vp)]
 _lib.fmg_slab_plan.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int]
 _lib.fmg_solve.argtypes = [_vp]
 _lib.fmg_solve_async.argtypes = [_vp]
@@ -147,6 +152,23 @@ def slab_plan(nz: int, nslabs: int, rank: int, depth: int, gather: bool = False)
     return [tuple(out[4 * i:4 * i + 4]) for i in range(n)]
 
 
+def host_transport_gloo(group=None):
+    """A host-staged transport for Solver(hostx=...): every piece of an
+    exchange as torch.distributed isend / irecv (e.g. over gloo), then wait."""
+    import torch
+    import torch.distributed as tdist
+
+    def transport(pieces):
+        reqs = []
+        for peer, send, arr in pieces:
+            t = torch.from_numpy(arr)
+            reqs.append(tdist.isend(t, peer, group=group) if send else tdist.irecv(t, peer, group=group))
+        for r in reqs:
+            r.wait()
+
+    return transport
+
+
 def _stream_ptr(stream):
     if stream is None:
         return None
@@ -157,10 +179,14 @@ class Solver:
     """A compact-FMG context (fmg_create ... fmg_destroy)."""
 
     def __init__(self, dim: int, p: int, levels: int, schedule: Schedule | dict | None = None,
-                 stream=None, slabs: int = 1, dist: tuple | None = None):
+                 stream=None, slabs: int = 1, dist: tuple | None = None, hostx: tuple | None = None):
         """slabs > 1: virtual z slabs on this device (fmg_create_slabs).
         dist = (rank, nranks, uid): this process is z-slab `rank` of `nranks`
-        GPUs (fmg_create_dist); uid from nccl_unique_id() on rank 0."""
+        GPUs (fmg_create_dist); uid from nccl_unique_id() on rank 0.
+        hostx = (rank, nranks, transport): z-slab `rank` with a host-staged
+        transport (fmg_create_hostx); transport(pieces) receives a list of
+        (peer, send, numpy uint8 view) and must complete every piece, e.g.
+        torch.distributed isend / irecv over gloo (see host_transport_gloo)."""
         if schedule is None:
             from fmg_inputs import default_schedule
             schedule = default_schedule(dim, p)
@@ -169,7 +195,27 @@ class Solver:
         self.dim, self.p, self.levels, self.schedule = dim, p, levels, schedule
         self.stream = stream
         h = C.c_void_p()
-        if dist is not None:
+        self._xfer = None
+        if hostx is not None:
+            rank, nranks, transport = hostx
+            import numpy as np
+
+            def _cb(user, n, peer, send, buf, nbytes):
+                try:
+                    pieces = [(peer[i], send[i], np.ctypeslib.as_array(C.cast(buf[i], C.POINTER(C.c_uint8)),
+                                                                        shape=(nbytes[i],)))
+                              for i in range(n)]
+                    transport(pieces)
+                    return 0
+                except Exception:  # (reported to the library as a transport failure)
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+
+            self._xfer = _XFER_FN(_cb)
+            _check(_lib.fmg_create_hostx(dim, p, levels, C.byref(schedule), nranks, rank, self._xfer, None,
+                                         _stream_ptr(stream), C.byref(h)), "fmg_create_hostx")
+        elif dist is not None:
             rank, nranks, uid = dist
             ub = C.create_string_buffer(bytes(uid), 128)
             _check(_lib.fmg_create_dist(dim, p, levels, C.byref(schedule), nranks, rank, ub, _stream_ptr(stream),

@@ -102,6 +102,8 @@ struct fmg_ctx {
   double* sbase[9]{};             // scratch allocations (buf[] are their level-0 views)
   std::vector<fmg_ctx*> sub;      // virtual slabs: G sub-contexts driven in lockstep (group handle)
   void* comm = nullptr;           // multi-GPU slabs: ncclComm_t (one rank per process)
+  fmg_xfer_fn xfer = nullptr;     // host-staged slabs (fmg_create_hostx): the caller's transport
+  void* xfer_user = nullptr;
   fmg_alloc_fn afn = nullptr;
   fmg_free_fn ffn = nullptr;
   void* auser = nullptr;
@@ -876,6 +878,39 @@ void group_exchange(fmg_ctx* grp, const Item& it) {
   }
 }
 
+// Host-staged slabs (fmg_create_hostx): the same plan, each piece copied
+// through host memory and delivered by the caller's transport.
+int host_exchange(fmg_ctx* c, const Item& it) {
+  const int l = it.xl;
+  const Geom& g = c->g[l];
+  XBuf xb[2];
+  const int nb = xbufs(c, it.xarr, l, xb);
+  if (cudaStreamSynchronize(c->cur) != cudaSuccess) return FMG_ECUDA;
+  std::vector<std::vector<char>> stage;
+  std::vector<int> peer, send;
+  std::vector<void*> buf;
+  std::vector<int64_t> bytes;
+  std::vector<char*> dev;
+  for (const XPiece& q : slab_plan(g.NZ, c->G, c->rank, it.xgather ? 0 : it.xdepth, it.xgather)) {
+    for (int k = 0; k < nb; ++k) {
+      char* d = xb[k].base + (size_t)q.z0 * xb[k].plane;
+      const size_t n = xb[k].plane * (size_t)(q.z1 - q.z0);
+      stage.emplace_back(n);
+      if (q.send && cudaMemcpy(stage.back().data(), d, n, cudaMemcpyDeviceToHost) != cudaSuccess) return FMG_ECUDA;
+      peer.push_back(q.peer);
+      send.push_back(q.send);
+      bytes.push_back((int64_t)n);
+      dev.push_back(d);
+    }
+  }
+  for (auto& v : stage) buf.push_back(v.data());
+  if (!buf.empty() && c->xfer(c->xfer_user, (int)buf.size(), peer.data(), send.data(), buf.data(), bytes.data()) != 0)
+    return FMG_ENCCL;
+  for (size_t i = 0; i < buf.size(); ++i)
+    if (!send[i] && cudaMemcpy(dev[i], buf[i], (size_t)bytes[i], cudaMemcpyHostToDevice) != cudaSuccess) return FMG_ECUDA;
+  return FMG_OK;
+}
+
 // Issue every item on c->cur (inside a capture or directly), then the deferred norms.
 void issue(fmg_ctx* c, const Builder& b) {
   // FMG_SYNC_DEBUG=1 (direct runs only): synchronise after every launch and
@@ -889,6 +924,7 @@ void issue(fmg_ctx* c, const Builder& b) {
     const Item& it = b.items[ii];
     if (it.kind == 2) {  // ghost planes: NCCL ranks (single-rank contexts have none)
       if (c->comm && nccl_exchange(c, it) != FMG_OK) c->nccl_err = 1;
+      if (c->xfer && host_exchange(c, it) != FMG_OK) c->nccl_err = 1;
       continue;
     }
     issue_item(c, it);
@@ -1364,6 +1400,16 @@ int fmg_create_dist(int dim, int p, int levels, const fmg_schedule* s, int nrank
   return FMG_OK;
 }
 
+int fmg_create_hostx(int dim, int p, int levels, const fmg_schedule* s, int nranks, int rank, fmg_xfer_fn fn,
+                     void* user, void* stream, fmg_ctx** out) {
+  if (!out || !fn || dim != 3 || nranks < 1 || rank < 0 || rank >= nranks) return FMG_EINVAL;
+  int rc = create_impl(dim, p, levels, s, stream, nranks, rank, out);
+  if (rc) return rc;
+  (*out)->xfer = fn;
+  (*out)->xfer_user = user;
+  return FMG_OK;
+}
+
 int fmg_slab_plan(int nz, int nslabs, int rank, int depth, int gather, int* out, int cap) {
   if (nz < 1 || nslabs < 1 || nz % nslabs != 0 || rank < 0 || rank >= nslabs || depth < 0) return -FMG_EINVAL;
   std::vector<XPiece> v = slab_plan(nz, nslabs, rank, depth, gather);
@@ -1450,6 +1496,7 @@ static int group_check(fmg_ctx* grp) {
 int fmg_solve_async(fmg_ctx* c) {
   if (!c) return FMG_EINVAL;
   if (!c->sub.empty()) return group_solve(c, c->Lmax, c->s.n_ir, true);
+  if (c->xfer) return fmg_solve_upto(c, c->Lmax, c->s.n_ir);  // (host transport: no graph)
   if (!c->graph) {
     Builder b = make_builder(c);
     c->launches = 0;
@@ -1512,6 +1559,28 @@ static int norms_sq(fmg_ctx* c, double* host) {
     cudaError_t e = cudaStreamSynchronize(c->st);
     if (e != cudaSuccess) return cuda_err(e);
     e = cudaMemcpy(host, c->norms_dev, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && c->xfer) {  // host transport: exchange the partial vectors, sum in rank order
+      for (size_t i = 0; i < n; ++i)
+        if ((int)(i % c->levels) <= c->lc && c->rank != 0) host[i] = 0.0;
+      std::vector<std::vector<double>> all(c->G, std::vector<double>(n));
+      all[c->rank].assign(host, host + n);
+      std::vector<int> peer, send;
+      std::vector<void*> buf;
+      std::vector<int64_t> bytes;
+      for (int r = 0; r < c->G; ++r) {
+        if (r == c->rank) continue;
+        peer.push_back(r); send.push_back(1); buf.push_back(all[c->rank].data()); bytes.push_back((int64_t)(8 * n));
+        peer.push_back(r); send.push_back(0); buf.push_back(all[r].data()); bytes.push_back((int64_t)(8 * n));
+      }
+      if (!buf.empty() && c->xfer(c->xfer_user, (int)buf.size(), peer.data(), send.data(), buf.data(), bytes.data()))
+        return FMG_ENCCL;
+      for (size_t i = 0; i < n; ++i) {
+        double t = 0.0;
+        for (int r = 0; r < c->G; ++r) t += all[r][i];
+        host[i] = t;
+      }
+      return FMG_OK;
+    }
     if (e != cudaSuccess || !c->comm) return cuda_err(e);
     // NCCL ranks: sum the slab partials of levels > lc (KC levels from rank 0)
     for (size_t i = 0; i < n; ++i)
@@ -1548,7 +1617,7 @@ int fmg_norms(fmg_ctx* c, double* host) {
 }
 
 int fmg_residual(fmg_ctx* c, double* host_norms) {
-  if (!c || !c->sub.empty() || c->comm) return FMG_EINVAL;  // (virtual-slab groups: solve / norms / sections only)
+  if (!c || !c->sub.empty() || c->comm || c->xfer) return FMG_EINVAL;  // (slab groups / ranks: solve / norms / sections only)
   if (c->solved_L < 0) return FMG_ESTATE;
   int L = c->solved_L;
   if (L < 1) return FMG_ESTATE;
@@ -1591,7 +1660,7 @@ static int decode_solution(fmg_ctx* c, int* which) {
 
 int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
   if (!c || !dst_dev) return FMG_EINVAL;
-  if (!c->sub.empty() || c->comm) return FMG_EINVAL;  // (slab ranks hold only their planes)
+  if (!c->sub.empty() || c->comm || c->xfer) return FMG_EINVAL;  // (slab ranks hold only their planes)
   if (c->solved_L < 0) return FMG_ESTATE;
   int which = 0;
   int rc = decode_solution(c, &which);
@@ -1603,7 +1672,7 @@ int fmg_get_solution(fmg_ctx* c, double* dst_dev) {
 
 int fmg_errors(fmg_ctx* c, double* err3) {
   if (!c || !err3) return FMG_EINVAL;
-  if (!c->sub.empty() || c->comm) return FMG_EINVAL;  // (slab ranks hold only their planes)
+  if (!c->sub.empty() || c->comm || c->xfer) return FMG_EINVAL;  // (slab ranks hold only their planes)
   if (c->solved_L < 0) return FMG_ESTATE;
   int which = 0;
   int rc = decode_solution(c, &which);

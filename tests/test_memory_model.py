@@ -107,3 +107,28 @@ def test_memory_model_rejects_bad_arguments():
     assert lib.fmg_memory_model(4, 2, 5, C.byref(s), out.ctypes.data_as(dp), 13) == 1
     assert lib.fmg_memory_model(2, 2, 5, C.byref(s), out.ctypes.data_as(dp), 12) == 1
     assert lib.fmg_memory_model(2, 2, 5, None, out.ctypes.data_as(dp), 13) == 1
+
+
+def test_c5_fits_eight_gpus_per_rank():
+    """C5 (4096^3 Q1, 12 levels) at 8 GPUs: with the z-slab memory partition
+    (a rank holds NZ_l / G planes + 2p ghost planes each side of
+    every level array and section) and the finest-level kernels (DESIGN.md
+    §4.3), one rank's device bytes fit a 180 GB B200.  Hand count of the
+    allocations in create_impl, every level partitioned (the replicated
+    coarse levels are a few MB)."""
+    c = CONFIGS["C5"]
+    d, p, lv = c["dim"], c["p"], c["levels"]
+    G, L = 8, lv - 1
+    sch = default_schedule(d, p)
+    tot = 0
+    for l in range(lv):
+        n = p << (l + 1)
+        NX = (n + 31) // 32 * 32
+        planes = min(n, n // G + 4 * p)
+        plane = NX * n
+        arrays = 1 if l == L else 3                      # t_L; u, t, w below
+        arrays += 3 if l == L - 1 else 0                 # Z, B, PU scratch (degree 2)
+        tot += 8 * plane * planes * arrays
+        wu, wr = sch["b_u"] + sch["k_u"] * (L - l), sch["b_r"] + sch["k_r"] * (L - l)
+        tot += (plane // 32) * planes * (4 * (wu + wr) + 2)  # section words + exponents
+    assert tot < 180e9 * 0.9, tot / 1e9
