@@ -88,6 +88,10 @@ struct fmg_ctx {
   // and, for degree 3, the direction d_2.  FMG_FINE3=0 selects the
   // level-by-level kernels everywhere.
   bool fine3 = false;
+  // fine3, memory permitting: the finest level keeps u_L and P u_{L-1} arrays
+  // too (the residual stages u_L instead of generating it).
+  // FMG_F3MAT=0/1 forces the choice.
+  bool f3mat = false;
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
@@ -269,6 +273,38 @@ OpDesc mkop(int type, int l, int L) {
   return o;
 }
 
+// cFas at level l of FMG level L with the finest-level kernels (fmg_fine3.cu,
+// DESIGN.md §4.3): [P u_{l-1} -> PU], z_l generated on chip -> b_l (+ z_l -> Z
+// below the finest level), Chebyshev steps 2..k; the last one applies the
+// correction and, below the finest level (or materialised), writes w_l and
+// u_l.  `xch`: z-slab ghost exchanges before each stencil consumer.
+void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
+  fmg_ctx* c = b.c;
+  const int P = c->p, k = c->s.cheb_degree;
+  const bool top = l == L, uout = !top || c->f3mat;
+  if (uout) {
+    if (xch) b.xchg(XA_U, l - 1, P);
+    OpDesc q = mkop(OP_PROLONG, l, L);
+    q.puonly = 1;
+    b.grid(q);
+  }
+  if (xch) b.xchg(XA_W, l - 1, 2 * P);
+  for (int step = 1; step <= k; ++step) {
+    if (xch && step >= 2) b.xchg(XA_T, l, P);  // b_l (the t_l buffer)
+    if (xch && step >= 3) b.xchg(XA_D, l, P);  // d_2
+    OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
+    q.step = step;
+    q.last = step == k;
+    q.wr = wr(c, l, L);
+    q.wu_in = c->wu_cur[l];
+    q.wu_out = wu(c, l, L);
+    q.zout = step == 1 && !top;
+    q.wout = q.last && !top;
+    q.uout = q.last && uout;
+    b.fine(step == 1 ? 1 : 2, q, (fine && top) ? (step == k ? 5 : 1) : -1);
+  }
+}
+
 // Grid-only fmgResidual (API paths): decode sweep, residual, restriction, norms.
 void build_residual_grid(Builder& b, int L, int row) {
   fmg_ctx* c = b.c;
@@ -316,7 +352,7 @@ void build_iteration_nu(Builder& b, int L, int it) {
     o.wu_in = c->wu_cur[L];
     o.row = row;
     o.poff = b.slot(row, L);
-    if (c->fine3) b.fine(0, o, fine ? 0 : -1);  // u_L generated on chip (fmg_fine3.cu)
+    if (c->fine3 && !c->f3mat) b.fine(0, o, fine ? 0 : -1);  // u_L generated on chip (fmg_fine3.cu)
     else b.grid(o, fine ? 0 : -1);
   }
   for (int l = L - 1; l >= 0; --l) {
@@ -359,16 +395,8 @@ void build_iteration_nu(Builder& b, int L, int it) {
     const bool gs = c->s.smoother == 1;
     const int nsteps = gs ? ncolours(c) : k;  // GS: colour 0 in cFas1, then colours 1 .. (p+1)^d - 1
     for (int l = 1; l <= L; ++l) {
-      if (c->fine3 && l == L) {  // z_L generated on chip; no w_L, u_L (fmg_fine3.cu)
-        for (int step = 1; step <= nsteps; ++step) {
-          OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
-          q.step = step;
-          q.last = step == nsteps;
-          q.wr = wr(c, l, L);
-          q.wu_in = c->wu_cur[l];
-          q.wu_out = wu(c, l, L);
-          b.fine(step == 1 ? 1 : 2, q, fine ? (step == nsteps ? 5 : 1) : -1);
-        }
+      if (c->fine3) {  // z_l generated on chip (fmg_fine3.cu); w_l, u_l materialised below the finest level
+        add_fine3_level(b, l, L, fine, false);
         continue;
       }
       if (c->dim == 3) b.grid(mkop(OP_PROLONG, l, L));  // z_l = P w_{l-1}, P u_{l-1}
@@ -408,7 +436,7 @@ void build_iteration(Builder& b, int L, int it) {
     o.wu_in = c->wu_cur[L];
     o.row = row;
     o.poff = b.slot(row, L);
-    if (c->fine3) {  // u_L generated on chip from ú_L (BFP ghost planes) and u_{L-1} (fmg_fine3.cu)
+    if (c->fine3 && !c->f3mat) {  // u_L generated on chip from ú_L (BFP ghost planes) and u_{L-1} (fmg_fine3.cu)
       b.xchg(XA_SU, L, P);
       b.xchg(XA_U, L - 1, 2 * P);
       b.fine(0, o, fine ? 0 : -1);
@@ -440,19 +468,8 @@ void build_iteration(Builder& b, int L, int it) {
   }
   const int k = c->s.cheb_degree;
   for (int l = lc + 1; l <= L; ++l) {
-    if (c->fine3 && l == L) {  // z_L generated on chip; b_L in the t_L buffer (fmg_fine3.cu)
-      b.xchg(XA_W, L - 1, 2 * P);
-      for (int step = 1; step <= k; ++step) {
-        if (step >= 2) b.xchg(XA_T, L, P);           // b_L
-        if (step >= 3) b.xchg(XA_D, L, P);           // d_2
-        OpDesc q = mkop(step == 1 ? OP_CFAS1 : OP_CHEB, l, L);
-        q.step = step;
-        q.last = step == k;
-        q.wr = wr(c, l, L);
-        q.wu_in = c->wu_cur[l];
-        q.wu_out = wu(c, l, L);
-        b.fine(step == 1 ? 1 : 2, q, fine ? (step == k ? 5 : 1) : -1);
-      }
+    if (c->fine3) {  // z_l generated on chip; b_l in the t_l buffer (fmg_fine3.cu)
+      add_fine3_level(b, l, L, fine, true);
       c->wu_cur[l] = wu(c, l, L);
       continue;
     }
@@ -507,7 +524,7 @@ void build_solve(Builder& b, int Lstop, int iters_last) {
     // ú_{0..L-1} is value-preserving and happens at the next encode.
     c->wu_cur[L] = wu(c, L, L);
     // u_L = dec ú_L + P u_{L-1} = P u_{L-1} for the first residual
-    if (c->fine3) {
+    if (c->fine3 && !c->f3mat) {
       // u_{L-1} = dec ú_{L-1} + P u_{L-2}: a grid level L-1 was the finest
       // level of FMG level L-1, whose kernels keep no u array (fmg_fine3.cu);
       // the cluster kernel writes u_l of its levels <= lc itself
@@ -619,6 +636,7 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
   m.zoff = c->wlo[o.l];
   m.guess = o.guess;
   m.store = o.store;
+  m.puonly = o.puonly;
   m.smode = o.smode;
   if (o.type == OP_RESTRICT && o.smode) m.lo.T = c->Wl[o.l + 1];  // s sweep: restrict q_{l+1} (in W)
   if (c->tma) {
@@ -665,6 +683,13 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.gtab = c->gtab[l];
   a.T = c->Tl[l];
   a.Dv = sview(c, 4, l);
+  a.Z = sview(c, 0, l);
+  a.PU = sview(c, 5, l);
+  a.U = c->Ul[l];
+  a.W = c->Wl[l];
+  a.zout = o.zout;
+  a.wout = o.wout;
+  a.uout = o.uout;
   a.zoff = c->wlo[l];
   a.czoff = l >= 1 ? c->wlo[l - 1] : 0;
   a.pbase = c->pbase;
@@ -1196,6 +1221,19 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   // direction Dv, each used by one level at a time.  With fine3 the finest
   // level keeps only t (which also holds b) and, for degree 3, Dv: its u, w
   // and the scratch of levels < Lmax are one level smaller.
+  if (c->fine3) {
+    // materialise u_L and P u_{L-1} when the two extra finest-size arrays fit
+    // comfortably (half the device memory with everything else): faster for
+    // Q3 and Q1 (the residual stages u_L; profiles/r2_summary.md); the lean
+    // form is what makes C5's per-GPU share fit
+    const char* e = getenv("FMG_F3MAT");
+    size_t freeb = 0, totalb = 0;
+    cudaMemGetInfo(&freeb, &totalb);
+    double need = 0.0;
+    for (int l = 0; l <= Lmax; ++l)
+      need += 8.0 * (double)c->g[l].NX * c->g[l].NY * (c->whi[l] - c->wlo[l]) * (l == Lmax ? 5.0 : 3.0);
+    c->f3mat = e ? atoi(e) != 0 : need < 0.5 * (double)totalb;
+  }
   for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
     const long long plane = (long long)c->g[l].NX * c->g[l].NY, off = plane * c->wlo[l];
     const size_t bytes = sizeof(double) * plane * (c->whi[l] - c->wlo[l]);
@@ -1206,7 +1244,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       a = q ? q - off : nullptr;  // (global plane indexing)
       return q != nullptr;
     };
-    if (!arr(c->Tl[l]) || (!top && (!arr(c->Ul[l]) || !arr(c->Wl[l])))) rc = FMG_ENOMEM;
+    if (!arr(c->Tl[l]) || ((!top || c->f3mat) && !arr(c->Ul[l])) || (!top && !arr(c->Wl[l]))) rc = FMG_ENOMEM;
   }
   {
     // scratch: each buffer serves one level at a time with that level's
@@ -1215,11 +1253,13 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     size_t scratch = 0;
     for (int l = 0; l <= (c->fine3 ? Lmax - 1 : Lmax); ++l) scratch = std::max(scratch, win(l));
     const bool dv = !c->fine3 || s->cheb_degree >= 3;
-    // (fine3, degree 2: the level-by-level Chebyshev kernels of levels < L
-    // finish at step 2 and never write Y)
-    const bool y = !c->fine3 || s->cheb_degree >= 3;
+    // (fine3: every level's cFas runs the finest-level kernels, whose b_l
+    // lives in the t_l buffer and whose y_{j-1} is recomputed: no B, Y scratch)
     for (int i = 0; i < 6 && rc == FMG_OK; ++i) {
-      const size_t bytes = sizeof(double) * (i == 4 ? (dv ? win(Lmax) : 2) : ((i == 2 || i == 3) && !y ? 2 : scratch));
+      size_t n = i == 4 ? (dv ? win(Lmax) : 2) : ((i >= 1 && i <= 3) && c->fine3 ? 2 : scratch);
+      if (i == 1 && c->fine3) n = win(0);  // (level 0's bracket b_0: cFas1 + k_coarse_nu)
+      if (i == 5 && c->f3mat) n = win(Lmax);  // (P u_{L-1} at the finest level)
+      const size_t bytes = sizeof(double) * n;
       c->buf[i] = (double*)dalloc(c, bytes);
       c->sbase[i] = c->buf[i];
       if (!c->buf[i]) rc = FMG_ENOMEM;
@@ -1253,13 +1293,17 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       ok &= make_tmap(&c->tmU[l], c->Ul[l], g.NX, g.NY, 0, 32 + 2 * pe, 1);
       ok &= make_tmap(&c->tmT[l], c->Tl[l], g.NX, g.NY, 0, 64 + 4 * p, 1);
       for (int i = 0; i < 4; ++i) ok &= make_tmap(&c->tmB[i][l], c->buf[i], g.NX, g.NY, 0, 32 + 2 * pe, 1);
-    } else if (!(c->fine3 && l == Lmax)) {  // (fine3: level Lmax has no u array, the scratch is one level smaller)
+    } else if (c->fine3 && l == Lmax) {  // (fine3: the scratch is one level smaller; u only if materialised)
+      if (c->f3mat)
+        ok &= make_tmap(&c->tmU[l], c->Ul[l] + (long long)g.NX * g.NY * c->wlo[l], g.NX, g.NY, c->whi[l] - c->wlo[l],
+                        40, 8 + 2 * p);
+    } else {
       // maps over the level's plane window (TMA coordinates z - wlo)
       const long long off = (long long)g.NX * g.NY * c->wlo[l];
       const int nz = c->whi[l] - c->wlo[l];
       ok &= make_tmap(&c->tmU[l], c->Ul[l] + off, g.NX, g.NY, nz, 40, 8 + 2 * p);
       for (int i = 0; i < 4; ++i)
-        if (!(c->fine3 && (i == 2 || i == 3) && s->cheb_degree < 3))
+        if (!(c->fine3 && i >= 1))
           ok &= make_tmap(&c->tmB[i][l], c->sbase[i], g.NX, g.NY, nz, 40, 8 + 2 * p);
     }
     if (!ok) rc = FMG_ECUDA;
@@ -1801,11 +1845,12 @@ int fmg_memory_model(int dim, int p, int levels, const fmg_schedule* s, double* 
     // this implementation's FP64 arrays (create_impl): u_l, t_l, w_l per level;
     // scratch Z, B, Y[2], PU and the Chebyshev direction Dv.  With the
     // finest-level kernels (3D, Chebyshev degree 2-3, nu = 1)
-    // level L keeps only t_L, the scratch is one level smaller and Dv exists
-    // for degree 3 only.
+    // level L keeps only t_L (lean form), the scratch is Z and PU one level
+    // smaller, and Dv exists for degree 3 only.
     const bool f3 = dim == 3 && s->nu <= 1 && s->smoother == 0 && (s->cheb_degree == 2 || s->cheb_degree == 3) && L >= 1;
     fp64 += (f3 && l == L ? 1.0 : 3.0) * 8.0 * stored;
-    if (f3 && l == L - 1) fp64 += (s->cheb_degree >= 3 ? 5.0 : 3.0) * 8.0 * stored;  // Z, B, PU (+ Y[2])
+    if (f3 && l == L - 1) fp64 += 2.0 * 8.0 * stored;  // Z, PU scratch (the lean form, FMG_F3MAT=0)
+    if (f3 && l == 0) fp64 += 8.0 * stored;           // B of level 0's bracket
     sec += 4.0 * (double)(NX * n * (dim == 3 ? n : 1) / 32) * (wul + wrl) + 2.0 * stored / 32.0;
     if (l == L) {
       nL = N;

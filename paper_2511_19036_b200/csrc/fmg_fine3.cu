@@ -259,6 +259,7 @@ struct Gen {
   int off[KB];   // r RS + c; -1: inactive element
   int pk[KB];    // bxo | byo << 8 | rx << 16 | ry << 20 | (r < CBY) << 24   (coarse offsets from the box origin)
   int dk[KB];    // decode: record row offset | block << 10 | exponent byte << 12 | position << 16 | on << 24
+  int zo[KB];    // output point of the tile (rows P..P+7, columns P..P+31): y NX + x in the plane; else -1
   int cx0, cy0;  // coarse box origin
   int cfirst;    // first coarse plane of the march (ring slots and barrier phases count from it)
   int clast;     // last coarse plane the march needs (no request beyond: no TMA left in flight)
@@ -280,6 +281,7 @@ __device__ __forceinline__ void gen_init(Gen<P>& gn, const Geom& g, int x0, int 
     gn.off[k] = -1;
     gn.pk[k] = 0;
     gn.dk[k] = 0;
+    gn.zo[k] = -1;
     if (e < Gen<P>::NE) {
       const int r = e / BW, c = e - r * BW;
       const int fx = x0 - P + c, fy = y0 - P + r;
@@ -287,6 +289,7 @@ __device__ __forceinline__ void gen_init(Gen<P>& gn, const Geom& g, int x0, int 
       const int rx = okx ? fx % (2 * P) : 0, bxo = okx ? P * (fx / (2 * P)) - gn.cx0 : 0;
       const int ry = oky ? fy % (2 * P) : 0, byo = oky ? P * (fy / (2 * P)) - gn.cy0 : 0;
       gn.off[k] = r * RS + c;
+      if (r >= P && r < P + FW && c >= P && c < P + 32 && fy < g.NY) gn.zo[k] = fy * g.NX + fx;
       // y pass reads PX[(byo + t) RS + c]: stored relative to the element's own offset
       gn.pk[k] = bxo | ((byo - r + 32) << 8) | (rx << 16) | (ry << 20) | ((r < CBY ? 1 : 0) << 24) |
                  ((okx ? 1 : 0) << 25) | ((oky ? 1 : 0) << 26);
@@ -655,6 +658,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_co
     cpa_commit();
     if (zi >= 1 && zi <= n - 1) gen_advance<P>(gn, m.pws, a.tmc, m.craw, m.cbar, m.PX, m.yvring, cbase<P>(zi) + P);
     gen_z<P>(gn, cf, m.yvring, zi, n, m.box, nullptr, 0);
+    if (a.zout && zi >= tl.zs && zi < tl.ze) {  // z_l at the tile's points (levels below the finest)
+      double* zp = a.Z + (long long)zi * tplane;
+#pragma unroll
+      for (int k = 0; k < Gen<P>::KB; ++k)
+        if (gn.zo[k] >= 0) zp[gn.zo[k]] = m.box[gn.off[k]];
+    }
     cpa_wait<PF>();
     __syncthreads();
     xpass<P>(m.box, 0, km, kk, m.XA, m.XB, w, lane);
@@ -699,7 +708,9 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
   double* XA = yb + BOX;
   double* XB = XA + NR * 32;
   double* ivd = XB + NR * 32;                // invD factors: P node types x box
-  uint32_t* wring = (uint32_t*)(ivd + P * BOX);  // NW x FW x (w + 1) (last step: ú words)
+  double* aring = ivd + P * BOX;             // NW x 2 x NT: z_l, P u_{l-1} at the output points (last step)
+  const bool aux = a.last && (a.wout || a.uout);
+  uint32_t* wring = (uint32_t*)(aring + (aux ? NW * 2 * 32 * FW : 0));  // NW x FW x (w + 1) (last step: ú words)
   const int RW = a.wu + 1;
   unsigned long long* bars = (unsigned long long*)(wring + NW * FW * RW + 2);
   bars = (unsigned long long*)(((uintptr_t)bars + 7) & ~(uintptr_t)7);
@@ -755,6 +766,19 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
   const long long ustep = bpp * a.ustride;
   const int nout = tl.ze - tl.zs;
   const unsigned ring_s = smem_u32(ring), bars_s = smem_u32(bars), wring_s = smem_u32(wring);
+  const unsigned aring_s = smem_u32(aring);
+  const int tid = w * 32 + lane;
+  const long long pbase0 = ((long long)tl.zs * g.NY + y) * g.NX + x;  // output point, plane zs
+  auto auxcopy = [&](int j, int slot) {  // z_l, P u_{l-1} of output plane zs + j -> aux ring slot
+    if (aux && rowok) {
+      const unsigned d = aring_s + (unsigned)(((slot * 2) * 32 * FW + tid) * 8);
+      if (a.wout)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(a.Z + pbase0 + j * tplane) : "memory");
+      if (a.uout)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 32 * FW * 8), "l"(a.PU + pbase0 + j * tplane)
+                     : "memory");
+    }
+  };
   if (threadIdx.x == 0 && threadIdx.y == 0) {
 #pragma unroll
     for (int k = 0; k < NBF; ++k) mbar_init(bars + k, 1);
@@ -789,7 +813,10 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
     if (i < nin) stage(i, i);
 #pragma unroll
   for (int j = 0; j < PF; ++j) {
-    if (j < nout) wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
+    if (j < nout) {
+      wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
+      auxcopy(j, j);
+    }
     cpa_commit();
   }
   double cr[R], sr[R];
@@ -807,7 +834,11 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
     if (i + PF < nin) stage(i + PF, isl + PF >= NBF ? isl + PF - NBF : isl + PF);
     if (produce) {
       const int j = i - 2 * P + PF;
-      if (j < nout) wcopy(ws, wring_s + (unsigned)((osl + PF >= NW ? osl + PF - NW : osl + PF) * FW * RW * 4), j);
+      const int sl = osl + PF >= NW ? osl + PF - NW : osl + PF;
+      if (j < nout) {
+        wcopy(ws, wring_s + (unsigned)(sl * FW * RW * 4), j);
+        auxcopy(j, sl);
+      }
     }
     cpa_commit();
     // y_{j-1} on the thread's staged elements of plane zi
@@ -865,9 +896,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
       if (a.last) {
         const double yq = warp_encode(yv, a.wr, nullptr, nullptr, lane, a.status);
         if (rowok) {
+          const double* ax = aring + osl * 2 * 32 * FW + tid;
+          if (a.wout) a.W[pbase0 + (long long)(z - tl.zs) * tplane] = ax[0] + yq;  // w_l = z_l + dec ý_l
           const uint32_t* rec = wring + osl * FW * RW + w * RW;
           const double uo = warp_decode(rec, rec_e(rec + a.wu, eoff), a.wu, lane);
-          warp_encode(uo + yq, a.wu_out, ump, uep, lane, a.status);
+          const double uq = warp_encode(uo + yq, a.wu_out, ump, uep, lane, a.status);
+          if (a.uout) a.U[pbase0 + (long long)(z - tl.zs) * tplane] = uq + ax[32 * FW];  // u_l = dec ú_l + P u_{l-1}
         }
       } else if (rowok) {
         *Dp = d;
@@ -896,10 +930,11 @@ static int smem_cfas(int wr) {
   return (int)gen_smem_bytes<P>(F3<P>::NW * FW * (wr + 1)) + 16;
 }
 template <int P>
-static int smem_cheb(int J, int wu) {
+static int smem_cheb(int J, int wu, bool aux) {
   using C = F3<P>;
   const int NA = J >= 3 ? 2 : 1;
-  size_t d = (size_t)C::NBF * NA * C::BOX + C::BOX + 2 * C::NR * 32 + (size_t)P * C::BOX;
+  size_t d = (size_t)C::NBF * NA * C::BOX + C::BOX + 2 * C::NR * 32 + (size_t)P * C::BOX +
+             (aux ? (size_t)C::NW * 2 * 32 * FW : 0);
   size_t wbytes = (size_t)C::NW * FW * (wu + 1) * 4 + 8;
   return (int)(d * 8 + wbytes + 8 + 8 * C::NBF + 16);
 }
@@ -942,11 +977,12 @@ static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Ar
 // kind: 0 residual, 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3)
 void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf) {
   const int n = a.nitems;
+  const bool aux = a.last && (a.wout || a.uout);
 #define F(P)                                                                                          \
   if (kind == 0) f3_launch(k_f3_residual<P>, n, smem_res<P>(a.wu), st, a, cf);                        \
   else if (kind == 1) f3_launch(k_f3_cfas<P>, n, smem_cfas<P>(a.wr), st, a, cf);                      \
-  else if (a.step == 2) f3_launch(k_f3_cheb<P, 2>, n, smem_cheb<P>(2, a.wu), st, a, cf);              \
-  else f3_launch(k_f3_cheb<P, 3>, n, smem_cheb<P>(3, a.wu), st, a, cf);
+  else if (a.step == 2) f3_launch(k_f3_cheb<P, 2>, n, smem_cheb<P>(2, a.wu, aux), st, a, cf);         \
+  else f3_launch(k_f3_cheb<P, 3>, n, smem_cheb<P>(3, a.wu, aux), st, a, cf);
   if (p == 1) { F(1) } else if (p == 2) { F(2) } else { F(3) }
 #undef F
 }

@@ -51,6 +51,7 @@ struct OpDesc {
   int type, l, L, step, last;
   int wr, wu_in, wu_out;
   int guess, store, smode;  // nu > 1 cycles: see MArgs
+  int zout, wout, uout, puonly;  // finest-level kernels (F3Args) / P u_{l-1}-only prolongation (MArgs)
   int row;
   long long poff;  // norm partials of this (FMG level, iteration, level): pbase + poff
 };
@@ -96,6 +97,7 @@ struct MArgs {
   int guess;                 // cFas1 / last step: ý of the previous cycle is the initial guess
   int store;                 // last step: store ý_l (not the last cycle), no correction
   int smode;                 // OP_RESTRICT: s sweep (no encode, no norm); OP_SQ: s_{l} = 0 (top level)
+  int puonly;                // OP_PROLONG (3D): P u_{l-1} only (the finest-level cFas kernel generates z)
   // operands in the parameter space (no dependent global loads at kernel start)
   LevelDev lv;               // the output level l
   LevelDev lo;               // the other level: l-1 (decode, prolongation, cFas) or l+1 (restriction)
@@ -133,6 +135,12 @@ struct F3Args {
   const CUtensorMap* tmc;    // coarse boxes of u_{L-1} (residual) / w_{L-1} (cFas), device copy
   const CUtensorMap* tmb;    // fine boxes of b_L (the t_L buffer)
   const CUtensorMap* tmd;    // fine boxes of d_2
+  // levels below the finest and the materialised mode:
+  double* Z;                 // cFas: z_l at the output points -> Z (zout)
+  double* PU;                // last Chebyshev step: P u_{l-1} at the output points (uout)
+  double* U;                 // last Chebyshev step: u_l = dec ú_l + P u_{l-1} -> U (uout)
+  double* W;                 // last Chebyshev step: w_l = z_l + dec ý_l -> W (wout)
+  int zout, wout, uout;
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.

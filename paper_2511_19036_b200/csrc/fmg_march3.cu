@@ -616,13 +616,13 @@ __global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restric
       const int t0 = (bz == cz0 + P) ? 1 : 0;
       if (t0) {
         uv[0] = uv[P];
-        if (a.type != OP_DECODE) wv[0] = wv[P];
+        if (a.type != OP_DECODE && !a.puonly) wv[0] = wv[P];
       }
 #pragma unroll
       for (int t = 0; t <= P; ++t) {
         if (t < t0) continue;
         const int cz = bz + t;
-        if (a.type == OP_DECODE) {
+        if (a.type == OP_DECODE || a.puonly) {
           uv[t] = pxy<P>(cf, lp.U, gp, rx, bx, ry, by, cz);
         } else {
           wv[t] = pxy<P>(cf, lp.W, gp, rx, bx, ry, by, cz);
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restric
 #pragma unroll
       for (int t = 0; t <= P; ++t) {
         pu = fma(cf.Pw[rz][t], uv[t], pu);
-        if (a.type != OP_DECODE) pw = fma(cf.Pw[rz][t], wv[t], pw);
+        if (a.type != OP_DECODE && !a.puonly) pw = fma(cf.Pw[rz][t], wv[t], pw);
       }
     }
     const long long idx = ((long long)z * g.NY + y) * g.NX + x;
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(32 * TW3) k_m3_prolong(const DevCtx* __restric
       const double dv = warp_decode(lv.umant + blk * lv.ustride, lv.uexp[blk], a.wu_in, lane);
       lv.U[idx] = dv + pu;
     } else {
-      c.Z[idx] = pw;
+      if (!a.puonly) c.Z[idx] = pw;
       c.PU[idx] = pu;
     }
   }

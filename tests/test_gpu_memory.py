@@ -9,9 +9,10 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
-def test_device_bytes_match_model(cfg):
+def test_device_bytes_match_model(cfg, monkeypatch):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
+    monkeypatch.setenv("FMG_F3MAT", "0")  # (the model describes the lean form of the 3D kernels)
     import paper_2511_19036_b200 as P
     c = CONFIGS[cfg]
     s = P.Solver(c["dim"], c["p"], c["levels"], default_schedule(c["dim"], c["p"]))

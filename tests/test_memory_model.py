@@ -90,8 +90,8 @@ def test_exponents_and_temporaries_sublinear(cfg):
     st = [(((p << (l + 1)) + 31) // 32 * 32) * (p << (l + 1)) ** (d - 1) for l in range(lv)]
     L = lv - 1
     k = default_schedule(d, p)["cheb_degree"]
-    if d == 3 and k in (2, 3):  # finest-level kernels: t_L (+ d_2 for degree 3); u, t, w below; scratch at L-1
-        want = st[L] * (1 + (k >= 3)) + 3 * sum(st[:L]) + (5 if k >= 3 else 3) * st[L - 1]
+    if d == 3 and k in (2, 3):  # finest-level kernels (lean): t_L (+ d_2 for degree 3); u, t, w below; Z, PU at L-1
+        want = st[L] * (1 + (k >= 3)) + 3 * sum(st[:L]) + 2 * st[L - 1] + st[0]
     else:                       # level-by-level kernels: u, t, w per level, six finest-size scratch arrays
         want = 3 * sum(st) + 6 * st[L]
     assert m["fp64_temporary_bytes"] == 8 * want
@@ -127,7 +127,7 @@ def test_c5_fits_eight_gpus_per_rank():
         planes = min(n, n // G + 4 * p)
         plane = NX * n
         arrays = 1 if l == L else 3                      # t_L; u, t, w below
-        arrays += 3 if l == L - 1 else 0                 # Z, B, PU scratch (degree 2)
+        arrays += 2 if l == L - 1 else 0                 # Z, PU scratch
         tot += 8 * plane * planes * arrays
         wu, wr = sch["b_u"] + sch["k_u"] * (L - l), sch["b_r"] + sch["k_r"] * (L - l)
         tot += (plane // 32) * planes * (4 * (wu + wr) + 2)  # section words + exponents
