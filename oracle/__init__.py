@@ -85,14 +85,15 @@ class Schedule(C.Structure):
     _fields_ = [("b_u", C.c_int), ("k_u", C.c_int), ("b_r", C.c_int), ("k_r", C.c_int),
                 ("n_ir", C.c_int), ("cheb_degree", C.c_int),
                 ("lambda_hi", C.c_double), ("alpha", C.c_double), ("smoother", C.c_int),
-                ("nu", C.c_int)]
+                ("nu", C.c_int), ("cfas_fp32", C.c_int)]
 
 
 SMOOTHERS = {"chebyshev": 0, "mcgs": 1, "lexgs": 2}
 
 
 def schedule(d: int, p: int, b_u=None, b_r=None, n_ir=None, k_u=None, k_r=1,
-             cheb_degree=None, lambda_hi=None, alpha=None, smoother="chebyshev", nu=1) -> Schedule:
+             cheb_degree=None, lambda_hi=None, alpha=None, smoother="chebyshev", nu=1,
+             cfas_fp32=0) -> Schedule:
     """Default schedule of DESIGN.md §5 (same numbers the product path uses)."""
     from fmg_inputs import default_schedule
     s = default_schedule(d, p)
@@ -103,7 +104,7 @@ def schedule(d: int, p: int, b_u=None, b_r=None, n_ir=None, k_u=None, k_r=1,
             s[k] = v
     return Schedule(s["b_u"], s["k_u"], s["b_r"], s["k_r"], s["n_ir"], s["cheb_degree"],
                     s["lambda_hi"], s["alpha"], SMOOTHERS[smoother] if isinstance(smoother, str) else smoother,
-                    nu)
+                    nu, int(cfas_fp32))
 
 
 @dataclass
@@ -173,6 +174,22 @@ def apply_A(d, p, l, u):
     u = np.ascontiguousarray(u, dtype=np.float64)
     out = np.zeros_like(u)
     lib().orc_apply_A(d, p, l, _dp(u), _dp(out))
+    return out
+
+
+def apply_A_f32(d, p, l, u):
+    u = np.ascontiguousarray(u, dtype=np.float32)
+    out = np.zeros_like(u)
+    fp = C.POINTER(C.c_float)
+    lib().orc_apply_A_f32(d, p, l, u.ctypes.data_as(fp), out.ctypes.data_as(fp))
+    return out
+
+
+def prolong_f32(d, p, lf, coarse):
+    coarse = np.ascontiguousarray(coarse, dtype=np.float32)
+    out = np.zeros(Geom(d, p, lf).shape, dtype=np.float32)
+    fp = C.POINTER(C.c_float)
+    lib().orc_prolong_f32(d, p, lf, coarse.ctypes.data_as(fp), out.ctypes.data_as(fp))
     return out
 
 

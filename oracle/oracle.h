@@ -43,6 +43,12 @@ typedef struct {
                         SURVEY §8f N2); cycles after the first start from the previous
                         correction: fine-to-coarse s sweep and nonzero-guess terms
                         (reading R23).  0 or 1: one cycle from zero. */
+  int cfas_fp32;     /* cFas in FP32 (tab:precisions PAPER.md:820-841: the cFas working
+                        precision is at most L + b_r <= 15 bits at the configurations;
+                        reading R28): z, b, the Chebyshev iterates and w in float with
+                        the FP64 constants rounded to float; the coarse solve, the
+                        correction and everything of the residual stay FP64.  Chebyshev,
+                        nu = 1 only. */
 } orc_schedule;
 
 /* ---- grid geometry of level l ---- */
@@ -76,6 +82,8 @@ void orc_coef_A(int p, double* Kc, double* Mc); /* [p][2p+1] assembled 1D rows *
 void orc_coef_P(int p, double* W);              /* [2p][p+1] prolongation weights */
 void orc_coef_R(int p, double* Rw);             /* [p][4p-1] restriction weights  */
 void orc_apply_A(int d, int p, int l, const double* u, double* out);
+void orc_apply_A_f32(int d, int p, int l, const float* u, float* out);   /* same tree in float */
+void orc_prolong_f32(int d, int p, int lf, const float* coarse, float* fine);
 void orc_prolong(int d, int p, int lf, const double* coarse, double* fine);
 void orc_restrict(int d, int p, int lf, const double* fine, double* coarse);
 void orc_rhs_table(int p, int l, double* g);    /* g[0..n-1], 1D load integrals */

@@ -105,6 +105,7 @@ void orc_destroy(orc_ctx* c) {
 }
 
 int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out) {
+  if (s && s->cfas_fp32 && (s->smoother != 0 || s->nu > 1)) return ORC_EINVAL;  /* (reading R28: Chebyshev, nu = 1) */
   *out = NULL;
   if ((d != 2 && d != 3) || p < 1 || p > 3 || levels < 1 || levels > ORC_MAXLEV) return ORC_EINVAL;
   if (s->b_u < 2 || s->b_r < 2 || s->n_ir < 1 || s->cheb_degree < 1 || s->cheb_degree > 8) return ORC_EINVAL;
@@ -217,6 +218,30 @@ static void chebyshev(const orc_ctx* c, int l, const double* b, double* y) {
     for (int64_t i = 0; i < g->size; ++i) {
       double q = b[i] - ay[i];
       dv[i] = fma(c->cal[j - 1], dv[i], c->cbe[j - 1] * (iD[i] * q));
+      y[i] = y[i] + dv[i];
+    }
+  }
+  free(dv); free(ay);
+}
+
+/* FP32 cFas (reading R28): the Chebyshev-Jacobi smoother of chebyshev() in
+ * float, the FP64 constants rounded to float. */
+static void chebyshev_f32(const orc_ctx* c, int l, const float* b, float* y) {
+  const orc_level* g = &c->g[l];
+  const double* iD = c->invD[l];
+  const float ith = (float)c->inv_theta;
+  float* dv = malloc(sizeof(float) * g->size);
+  float* ay = malloc(sizeof(float) * g->size);
+  for (int64_t i = 0; i < g->size; ++i) {
+    dv[i] = ith * ((float)iD[i] * b[i]);
+    y[i] = dv[i];
+  }
+  for (int j = 2; j <= c->s.cheb_degree; ++j) {
+    const float al = (float)c->cal[j - 1], be = (float)c->cbe[j - 1];
+    orc_apply_A_f32(c->d, c->p, l, y, ay);
+    for (int64_t i = 0; i < g->size; ++i) {
+      float q = b[i] - ay[i];
+      dv[i] = fmaf(al, dv[i], be * ((float)iD[i] * q));
       y[i] = y[i] + dv[i];
     }
   }
@@ -361,8 +386,35 @@ static int cfas_cycle(orc_ctx* c, int L, int guess) {
     free(r0); free(y0);
     if (!rc) sec_decode(&c->y[0], g, c->wt[0]);   /* w_0 = z_0 + ý_0, z_0 = 0 */
   }
-  /* coarse-to-fine sweep PAPER.md:641-643 */
-  for (int l = 1; l <= L && !rc; ++l) {
+  /* coarse-to-fine sweep PAPER.md:641-643; FP32 cFas (reading R28): the same
+   * steps in float, w_l kept as the double of a float */
+  const int f32 = c->s.cfas_fp32 && !guess;
+  for (int l = 1; l <= L && !rc && f32; ++l) {
+    const orc_level* g = &c->g[l];
+    const orc_level* gc = &c->g[l - 1];
+    int64_t N = g->size;
+    float* wc = malloc(sizeof(float) * gc->size);
+    float* z = malloc(sizeof(float) * N);
+    float* az = malloc(sizeof(float) * N);
+    float* rb = malloc(sizeof(float) * N);
+    float* yf = malloc(sizeof(float) * N);
+    double* rv = malloc(sizeof(double) * N);
+    double* yv = malloc(sizeof(double) * N);
+    for (int64_t i = 0; i < gc->size; ++i) wc[i] = (float)c->wt[l - 1][i];   /* (exact: a float) */
+    orc_prolong_f32(d, p, l, wc, z);                  /* z_l = P_l w_{l-1} */
+    orc_apply_A_f32(d, p, l, z, az);
+    sec_decode(&c->r[l], g, rv);
+    for (int64_t i = 0; i < N; ++i) rb[i] = (float)rv[i] - az[i];    /* b = r_l - A_l z_l */
+    chebyshev_f32(c, l, rb, yf);
+    for (int64_t i = 0; i < N; ++i) yv[i] = (double)yf[i];
+    rc = sec_encode(&c->y[l], g, yv, wr(c, l, L));
+    if (!rc) {
+      sec_decode(&c->y[l], g, yv);
+      for (int64_t i = 0; i < N; ++i) c->wt[l][i] = (double)(z[i] + (float)yv[i]);
+    }
+    free(wc); free(z); free(az); free(rb); free(yf); free(rv); free(yv);
+  }
+  for (int l = 1; l <= L && !rc && !f32; ++l) {
     const orc_level* g = &c->g[l];
     int64_t N = g->size;
     double* z = malloc(sizeof(double) * N);

@@ -230,6 +230,130 @@ void orc_apply_A(int d, int p, int l, const double* u, double* out) {
   free(a); free(b); free(dd); free(e);
 }
 
+/* ------------------------------------------------- FP32 cFas (reading R28) --
+ * The same 1D passes and trees in float (fmaf from +0.0f, taps in increasing
+ * index order); the float constants are the FP64 constants rounded to float
+ * (the prolongation weights are dyadic, hence exact). */
+static void pass1d_f32(int p, int kind, const float* C, int axis,
+                       const float* in, dims_t di, float* out, dims_t dout) {
+  int nout = dout.n[axis], nin = di.n[axis];
+  int64_t sin[3] = {1, di.sx, (int64_t)di.sx * di.n[1]};
+  for (int z = 0; z < dout.n[2]; ++z)
+    for (int y = 0; y < dout.n[1]; ++y)
+      for (int x = 0; x < dout.sx; ++x) {
+        int c[3] = {x, y, z};
+        int64_t o_idx = ((int64_t)z * dout.n[1] + y) * dout.sx + x;
+        int i = c[axis];
+        if (i < 1 || i > nout - 1 || x >= dout.n[0]) {
+          out[o_idx] = 0.0f;
+          continue;
+        }
+        c[axis] = 0;
+        int64_t base_idx = (int64_t)c[2] * sin[2] + (int64_t)c[1] * sin[1] + c[0];
+        float acc = 0.0f;
+        if (kind == TAP_A) {
+          int tau = i % p;
+          for (int o = -p; o <= p; ++o) {
+            int j = i + o;
+            float v = (j >= 1 && j <= nin - 1) ? in[base_idx + (int64_t)j * sin[axis]] : 0.0f;
+            acc = fmaf(C[tau * (2 * p + 1) + o + p], v, acc);
+          }
+        } else {
+          int r = i % (2 * p), b = p * (i / (2 * p));
+          for (int t = 0; t <= p; ++t) {
+            int j = b + t;
+            float v = (j >= 1 && j <= nin - 1) ? in[base_idx + (int64_t)j * sin[axis]] : 0.0f;
+            acc = fmaf(C[r * (p + 1) + t], v, acc);
+          }
+        }
+        out[o_idx] = acc;
+      }
+}
+
+static void coefs_f32(int p, float* Kf, float* Mf) {
+  double Kc[3 * 7], Mc[3 * 7];
+  orc_coef_A(p, Kc, Mc);
+  for (int i = 0; i < 3 * 7; ++i) {
+    Kf[i] = (float)Kc[i];
+    Mf[i] = (float)Mc[i];
+  }
+}
+
+void orc_apply_A_f32(int d, int p, int l, const float* u, float* out) {
+  int n = p << (l + 1);
+  dims_t g = mkdims(n, n, d == 3 ? n : 1);
+  int64_t N = dsize(g);
+  float Kc[3 * 7], Mc[3 * 7];
+  coefs_f32(p, Kc, Mc);
+  float* a = malloc(sizeof(float) * N);
+  float* b = malloc(sizeof(float) * N);
+  float* dd = malloc(sizeof(float) * N);
+  float* e = malloc(sizeof(float) * N);
+  pass1d_f32(p, TAP_A, Mc, 0, u, g, a, g);
+  pass1d_f32(p, TAP_A, Kc, 0, u, g, b, g);
+  pass1d_f32(p, TAP_A, Kc, 1, a, g, dd, g);
+  pass1d_f32(p, TAP_A, Mc, 1, b, g, e, g);
+  if (d == 2) {
+    for (int64_t i = 0; i < N; ++i) out[i] = dd[i] + e[i];
+  } else {
+    float* c = malloc(sizeof(float) * N);
+    pass1d_f32(p, TAP_A, Mc, 1, a, g, c, g);
+    for (int64_t i = 0; i < N; ++i) dd[i] = dd[i] + e[i]; /* s */
+    const float h = ldexpf(1.0f, -(l + 1));
+    int64_t sz = (int64_t)g.sx * g.n[1];
+    for (int z = 0; z < n; ++z)
+      for (int y = 0; y < n; ++y)
+        for (int x = 0; x < g.sx; ++x) {
+          int64_t idx = ((int64_t)z * n + y) * g.sx + x;
+          if (z < 1) { out[idx] = 0.0f; continue; }
+          int tau = z % p;
+          float acc = 0.0f;
+          for (int o = -p; o <= p; ++o) {
+            int j = z + o;
+            float v = (j >= 1 && j <= n - 1) ? c[idx + (int64_t)o * sz] : 0.0f;
+            acc = fmaf(Kc[tau * (2 * p + 1) + o + p], v, acc);
+          }
+          for (int o = -p; o <= p; ++o) {
+            int j = z + o;
+            float v = (j >= 1 && j <= n - 1) ? dd[idx + (int64_t)o * sz] : 0.0f;
+            acc = fmaf(Mc[tau * (2 * p + 1) + o + p], v, acc);
+          }
+          out[idx] = h * acc;
+        }
+    free(c);
+  }
+  for (int z = 0; z < g.n[2]; ++z)   /* mask_unknowns */
+    for (int y = 0; y < g.n[1]; ++y)
+      for (int x = 0; x < g.sx; ++x) {
+        int ok = (x >= 1 && x < g.n[0] && y >= 1 && y < g.n[1] && (d == 2 || z >= 1));
+        if (!ok) out[((int64_t)z * g.n[1] + y) * g.sx + x] = 0.0f;
+      }
+  free(a); free(b); free(dd); free(e);
+}
+
+void orc_prolong_f32(int d, int p, int lf, const float* coarse, float* fine) {
+  int nf = p << (lf + 1), nc = nf / 2;
+  double W[6 * 4];
+  float Wf[6 * 4];
+  orc_coef_P(p, W);
+  for (int i = 0; i < 6 * 4; ++i) Wf[i] = (float)W[i];
+  if (d == 2) {
+    dims_t g0 = mkdims(nc, nc, 1), g1 = mkdims(nf, nc, 1), g2 = mkdims(nf, nf, 1);
+    float* t1 = malloc(sizeof(float) * dsize(g1));
+    pass1d_f32(p, TAP_P, Wf, 0, coarse, g0, t1, g1);
+    pass1d_f32(p, TAP_P, Wf, 1, t1, g1, fine, g2);
+    free(t1);
+  } else {
+    dims_t g0 = mkdims(nc, nc, nc), g1 = mkdims(nf, nc, nc), g2 = mkdims(nf, nf, nc), g3 = mkdims(nf, nf, nf);
+    float* t1 = malloc(sizeof(float) * dsize(g1));
+    float* t2 = malloc(sizeof(float) * dsize(g2));
+    pass1d_f32(p, TAP_P, Wf, 0, coarse, g0, t1, g1);
+    pass1d_f32(p, TAP_P, Wf, 1, t1, g1, t2, g2);
+    pass1d_f32(p, TAP_P, Wf, 2, t2, g2, fine, g3);
+    free(t1); free(t2);
+  }
+}
+
 /* fine = P_lf coarse: x pass, then y, then z. */
 void orc_prolong(int d, int p, int lf, const double* coarse, double* fine) {
   int nf = p << (lf + 1), nc = nf / 2;
