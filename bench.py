@@ -198,6 +198,7 @@ def run_ours(args, rank, world, local_rank):
     sched = default_schedule(cfg["dim"], cfg["p"])
     sched["smoother"] = {"chebyshev": 0, "mcgs": 1}[args.smoother]
     sched["nu"] = args.nu
+    sched["cfas_fp32"] = int(args.cfas_fp32)
     P.use_torch_allocator(True)
     stream = torch.cuda.current_stream()
     dist_slabs = world > 1 and cfg["dim"] == 3  # 3D: one problem in z slabs over the ranks (NCCL)
@@ -297,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "strong" if dist_slabs else "weak",
         "vs_baseline": None,
-        "dtype": "f64",
+        "dtype": "f64 (cFas f32)" if args.cfas_fp32 else "f64",
         "data": "synthetic (manufactured solution u = prod sin(pi x_k); no dataset)",
         "config": {"workload": args.config + ": " + cfg["desc"], "dim": cfg["dim"], "p": cfg["p"],
                    "levels": cfg["levels"], "unknowns": info_unk,
@@ -526,6 +527,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nu", type=int, default=1,
                     help="compact V(0,1) cycles per IR iteration (SURVEY 8f N2; one GPU, 2D/3D, Chebyshev degree >= 2 or mcgs)")
+    ap.add_argument("--cfas-fp32", action="store_true",
+                    help="cFas in FP32 (DESIGN.md reading R28; 3D, Chebyshev): z, b, y, w in float")
     ap.add_argument("--smoother", default="chebyshev", choices=["chebyshev", "mcgs"],
                     help="cFas smoother: Chebyshev-Jacobi (default) or multicolour Gauss-Seidel (SURVEY 8f N1)")
     ap.add_argument("--workload", default="fmg", choices=["fmg", "n4"],

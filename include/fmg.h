@@ -66,6 +66,13 @@ typedef struct {
                    (2D and 3D) with the Chebyshev smoother of degree >= 2 or
                    multicolour Gauss-Seidel; fmg_create returns FMG_EINVAL for
                    nu > 8, Chebyshev degree 1 with nu > 1, and z slabs with nu > 1. */
+  int cfas_fp32; /* 1: cFas in FP32 (tab:precisions PAPER.md:820-841 bounds the
+                   cFas working precision by L + b_r <= 15 bits at the
+                   configurations; reading R28): z, b, the Chebyshev
+                   iterates and w in float with the FP64 constants rounded to
+                   float.  The coarse solve, the correction and the residual
+                   stay FP64.  3D with the Chebyshev smoother of degree 2-3 and
+                   nu = 1 only (else FMG_EINVAL).  0: everything FP64. */
 } fmg_schedule;
 
 typedef struct fmg_ctx fmg_ctx;

@@ -34,14 +34,14 @@ class Schedule(C.Structure):
     _fields_ = [("b_u", C.c_int), ("k_u", C.c_int), ("b_r", C.c_int), ("k_r", C.c_int),
                 ("n_ir", C.c_int), ("cheb_degree", C.c_int),
                 ("lambda_hi", C.c_double), ("alpha", C.c_double), ("smoother", C.c_int),
-                ("nu", C.c_int)]
+                ("nu", C.c_int), ("cfas_fp32", C.c_int)]
 
     @classmethod
     def from_dict(cls, d: dict) -> "Schedule":
         sm = d.get("smoother", 0)
         sm = {"chebyshev": 0, "mcgs": 1}[sm] if isinstance(sm, str) else sm
         return cls(d["b_u"], d["k_u"], d["b_r"], d["k_r"], d["n_ir"], d["cheb_degree"],
-                   d["lambda_hi"], d["alpha"], sm, d.get("nu", 1))
+                   d["lambda_hi"], d["alpha"], sm, d.get("nu", 1), int(d.get("cfas_fp32", 0)))
 
 
 _vp = C.c_void_p

@@ -706,7 +706,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
 void issue_item(fmg_ctx* c, const Item& it) {
   if (it.kind == 3) {
     mark(c, it.timed_cls);
-    launch_fine3(c->p, it.f3kind, c->cur, fine3_args(c, it), c->cf);
+    launch_fine3(c->p, it.f3kind, c->cur, fine3_args(c, it), c->cf, c->s.cfas_fp32);
     mark(c, it.timed_cls);
     c->launches++;
     return;
@@ -1067,6 +1067,9 @@ static int check_args(int dim, int p, int levels, const fmg_schedule* s) {
     return FMG_EINVAL;
   // nu > 1 on the GPU: Chebyshev of degree >= 2 or multicolour GS; one GPU (no z slabs)
   if (s->nu > 1 && s->smoother == 0 && s->cheb_degree < 2) return FMG_EINVAL;
+  // FP32 cFas (reading R28): the finest-level kernels' Chebyshev path only
+  if (s->cfas_fp32 && (dim != 3 || s->smoother != 0 || s->nu > 1 || s->cheb_degree < 2 || s->cheb_degree > 3))
+    return FMG_EINVAL;
   const int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return FMG_EINVAL;
   return FMG_OK;
@@ -1216,6 +1219,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     c->fine3 = rc == FMG_OK && dim == 3 && c->march && s->nu <= 1 && s->smoother == 0 &&
                (s->cheb_degree == 2 || s->cheb_degree == 3) && Lmax > c->lc && s->b_u <= 10 && !(e && atoi(e) == 0);
   }
+  if (rc == FMG_OK && s->cfas_fp32 && !c->fine3) rc = FMG_EINVAL;  // (FP32 cFas runs in the finest-level kernels)
   // FP64 workspace.  Level arrays u_l, t_l, w_l (padded level layout); the
   // scratch Z, B, Y[2], PU of the level-by-level kernels and the Chebyshev
   // direction Dv, each used by one level at a time.  With fine3 the finest

@@ -68,6 +68,14 @@ struct F3 {
   static constexpr int NCY = P + 1;            // xy-passed coarse plane ring
 };
 
+// Coefficients in the cFas working type T (double; float for FP32 cFas,
+// reading R28: the FP64 constants rounded to float, as the oracle does).
+template <class T>
+struct CoefT {
+  T Kc[3][7], Mc[3][7], Pw[6][4], invd[27], inv_theta, cal[8], cbe[8];
+  double rhs_c;
+};
+
 __device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {  // bar: smem byte address
   asm volatile(
       "{\n.reg .pred P1;\nWAIT_%=:\n"
@@ -83,41 +91,40 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %
 // -------------------------------------------------------- A passes ------
 // y pass at one output row of node type T (c = My a,
 // d = Ky a, e = My b; s = d + e), zero taps of interior types skipped.
-template <int P, int T>
-__device__ __forceinline__ void ypass_t(const Coefs& cf, const double* XA, const double* XB, int w, int lane, double& c,
-                                        double& s) {
-  constexpr int o0 = T == 0 ? 0 : P - T, o1 = T == 0 ? 2 * P : 2 * P - T;
-  double cc = 0.0, dd = 0.0, ee = 0.0;
+template <int P, int TY, class T>
+__device__ __forceinline__ void ypass_t(const CoefT<T>& cf, const T* XA, const T* XB, int w, int lane, T& c, T& s) {
+  constexpr int o0 = TY == 0 ? 0 : P - TY, o1 = TY == 0 ? 2 * P : 2 * P - TY;
+  T cc = 0, dd = 0, ee = 0;
 #pragma unroll
   for (int o = o0; o <= o1; ++o) {
-    const double av = XA[(w + o) * 32 + lane], bv = XB[(w + o) * 32 + lane];
-    cc = fma(cf.Mc[T][o], av, cc);
-    dd = fma(cf.Kc[T][o], av, dd);
-    ee = fma(cf.Mc[T][o], bv, ee);
+    const T av = XA[(w + o) * 32 + lane], bv = XB[(w + o) * 32 + lane];
+    cc = fma(cf.Mc[TY][o], av, cc);
+    dd = fma(cf.Kc[TY][o], av, dd);
+    ee = fma(cf.Mc[TY][o], bv, ee);
   }
   c = cc;
   s = dd + ee;
 }
-template <int P>
-__device__ __forceinline__ void ypass(const Coefs& cf, int ty, const double* XA, const double* XB, int w, int lane,
-                                      double& c, double& s) {
+template <int P, class T>
+__device__ __forceinline__ void ypass(const CoefT<T>& cf, int ty, const T* XA, const T* XB, int w, int lane, T& c,
+                                      T& s) {
   if (P == 1 || ty == 0) ypass_t<P, 0>(cf, XA, XB, w, lane, c, s);
   else if (P == 2 || ty == 1) ypass_t<P, (P >= 2 ? 1 : 0)>(cf, XA, XB, w, lane, c, s);
   else ypass_t<P, (P >= 3 ? 2 : 0)>(cf, XA, XB, w, lane, c, s);
 }
-// z pass of node type T over the register rings (acc over Kz on c, then Mz on s)
-template <int P, int T>
-__device__ __forceinline__ double zpass_t(const Coefs& cf, const double* cr, const double* sr) {
-  constexpr int o0 = T == 0 ? 0 : P - T, o1 = T == 0 ? 2 * P : 2 * P - T;
-  double acc = 0.0;
+// z pass of node type TZ over the register rings (acc over Kz on c, then Mz on s)
+template <int P, int TZ, class T>
+__device__ __forceinline__ T zpass_t(const CoefT<T>& cf, const T* cr, const T* sr) {
+  constexpr int o0 = TZ == 0 ? 0 : P - TZ, o1 = TZ == 0 ? 2 * P : 2 * P - TZ;
+  T acc = 0;
 #pragma unroll
-  for (int o = o0; o <= o1; ++o) acc = fma(cf.Kc[T][o], cr[o], acc);
+  for (int o = o0; o <= o1; ++o) acc = fma(cf.Kc[TZ][o], cr[o], acc);
 #pragma unroll
-  for (int o = o0; o <= o1; ++o) acc = fma(cf.Mc[T][o], sr[o], acc);
+  for (int o = o0; o <= o1; ++o) acc = fma(cf.Mc[TZ][o], sr[o], acc);
   return acc;
 }
-template <int P>
-__device__ __forceinline__ double zpass(const Coefs& cf, int tz, const double* cr, const double* sr) {
+template <int P, class T>
+__device__ __forceinline__ T zpass(const CoefT<T>& cf, int tz, const T* cr, const T* sr) {
   if (P == 1 || tz == 0) return zpass_t<P, 0>(cf, cr, sr);
   if (P == 2 || tz == 1) return zpass_t<P, (P >= 2 ? 1 : 0)>(cf, cr, sr);
   return zpass_t<P, (P >= 3 ? 2 : 0)>(cf, cr, sr);
@@ -125,19 +132,18 @@ __device__ __forceinline__ double zpass(const Coefs& cf, int tz, const double* c
 
 // x pass of the staged box rows of warp w: a = Mx u, b = Kx u (lane = output
 // column x0 + lane; staged column c = fine x0 - P + c; `off` = TMA shift)
-template <int P>
-__device__ __forceinline__ void xpass(const double* box, int off, const double* km, const double* kk, double* XA,
-                                      double* XB, int w, int lane) {
+template <int P, class T>
+__device__ __forceinline__ void xpass(const T* box, int off, const T* km, const T* kk, T* XA, T* XB, int w, int lane) {
   constexpr int R = F3<P>::R, NR = F3<P>::NR, RS = F3<P>::RS;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int r = w + k * FW;
     if (r < NR) {
-      const double* row = box + r * RS + off;
-      double s = 0.0, t = 0.0;
+      const T* row = box + r * RS + off;
+      T s = 0, t = 0;
 #pragma unroll
       for (int o = 0; o < R; ++o) {
-        const double v = row[lane + o];
+        const T v = row[lane + o];
         s = fma(km[o], v, s);
         t = fma(kk[o], v, t);
       }
@@ -308,21 +314,20 @@ __device__ __forceinline__ int cbase(int z) {
 }
 
 // x and y passes of coarse plane c (raw box in `cb`) into the xy ring slot.
-template <int P>
-__device__ __forceinline__ void gen_xy(const Gen<P>& gn, const double* pws, const double* cb, double* PX,
-                                       double* yv) {
+template <int P, class T>
+__device__ __forceinline__ void gen_xy(const Gen<P>& gn, const T* pws, const double* cb, T* PX, T* yv) {
   constexpr int CBX = F3<P>::CBX, RS = F3<P>::RS;
 #pragma unroll
   for (int k = 0; k < Gen<P>::KB; ++k) {
     const int pk = gn.pk[k];
     if (gn.off[k] >= 0 && (pk >> 24) & 1) {
       const int r = gn.off[k] / RS;  // (coarse row = box row index)
-      double a = 0.0;
+      T a = 0;
       if ((pk >> 25) & 1) {
-        const double* wt = pws + ((pk >> 16) & 15) * (P + 1);
+        const T* wt = pws + ((pk >> 16) & 15) * (P + 1);
         const double* row = cb + r * CBX + (pk & 255);
 #pragma unroll
-        for (int t = 0; t <= P; ++t) a = fma(wt[t], row[t], a);
+        for (int t = 0; t <= P; ++t) a = fma(wt[t], (T)row[t], a);
       }
       PX[gn.off[k]] = a;
     }
@@ -332,10 +337,10 @@ __device__ __forceinline__ void gen_xy(const Gen<P>& gn, const double* pws, cons
   for (int k = 0; k < Gen<P>::KB; ++k) {
     const int pk = gn.pk[k];
     if (gn.off[k] >= 0) {
-      double a = 0.0;
+      T a = 0;
       if ((pk >> 26) & 1) {
-        const double* wt = pws + ((pk >> 20) & 15) * (P + 1);
-        const double* col = PX + gn.off[k] + (((pk >> 8) & 255) - 32) * RS;
+        const T* wt = pws + ((pk >> 20) & 15) * (P + 1);
+        const T* col = PX + gn.off[k] + (((pk >> 8) & 255) - 32) * RS;
 #pragma unroll
         for (int t = 0; t <= P; ++t) a = fma(wt[t], col[t * RS], a);
       }
@@ -366,14 +371,14 @@ __device__ __forceinline__ void gen_range(Gen<P>& gn, int z0, int nin, int n) {
 }
 
 // Make the xy passes of every coarse plane <= cneed available.
-template <int P>
-__device__ __forceinline__ void gen_advance(Gen<P>& gn, const double* pws, const CUtensorMap* tm, double* craw,
-                                            unsigned long long* cbar, double* PX, double* yvring, int cneed) {
+template <int P, class T>
+__device__ __forceinline__ void gen_advance(Gen<P>& gn, const T* pws, const CUtensorMap* tm, double* craw,
+                                            unsigned long long* cbar, T* PX, T* yvring, int cneed) {
   constexpr int NCB = F3<P>::NCB, NCY = F3<P>::NCY, BOX = F3<P>::BOX;
   while (gn.cdone <= cneed) {
     const int c = gn.cdone, k = c - gn.cfirst;
     mbar_wait_s(smem_u32(cbar) + 8u * (unsigned)(k % NCB), (unsigned)(k / NCB) & 1u);
-    gen_xy<P>(gn, pws, craw + (k % NCB) * F3<P>::CBS, PX, yvring + (c % NCY) * BOX);
+    gen_xy<P, T>(gn, pws, craw + (k % NCB) * F3<P>::CBS, PX, yvring + (c % NCY) * BOX);
     // (gen_xy synchronised after its x pass: the raw slot is free)
     if (threadIdx.x == 0 && threadIdx.y == 0) gen_request<P>(gn, tm, craw, cbar, c + NCB);
     gn.cdone = c + 1;
@@ -383,14 +388,14 @@ __device__ __forceinline__ void gen_advance(Gen<P>& gn, const double* pws, const
 
 // Fine plane z into the box: z pass of the xy ring (0 at non-unknown planes),
 // plus dec of the section record (residual, `rec` non-null).
-template <int P>
-__device__ __forceinline__ void gen_z(const Gen<P>& gn, const Coefs& cf, const double* yvring, int z, int n,
-                                     double* box, const uint32_t* rec, int wu) {
+template <int P, class T>
+__device__ __forceinline__ void gen_z(const Gen<P>& gn, const CoefT<T>& cf, const T* yvring, int z, int n, T* box,
+                                     const uint32_t* rec, int wu) {
   constexpr int NCY = F3<P>::NCY, BOX = F3<P>::BOX;
   const bool okz = unk1(z, n);
   const int rz = okz ? z % (2 * P) : 0, cb = okz ? cbase<P>(z) : 0;
-  double pz[P + 1];
-  const double* ys[P + 1];
+  T pz[P + 1];
+  const T* ys[P + 1];
 #pragma unroll
   for (int t = 0; t <= P; ++t) {
     pz[t] = cf.Pw[rz][t];
@@ -400,16 +405,16 @@ __device__ __forceinline__ void gen_z(const Gen<P>& gn, const Coefs& cf, const d
   for (int k = 0; k < Gen<P>::KB; ++k) {
     const int o = gn.off[k];
     if (o >= 0) {
-      double v = 0.0;
+      T v = 0;
       if (okz) {
 #pragma unroll
         for (int t = 0; t <= P; ++t) v = fma(pz[t], ys[t][o], v);
         const int dk = gn.dk[k];
         if (rec && (dk >> 24)) {
           const uint32_t* r0 = rec + (dk & 1023);
-          const double dv = point_decode(r0 + ((dk >> 10) & 3) * wu, rec_e(r0 + 3 * wu, (dk >> 12) & 15), wu,
-                                         (dk >> 16) & 31);
-          v = dv + v;  // u = dec ú + P u
+          const T dv = (T)point_decode(r0 + ((dk >> 10) & 3) * wu, rec_e(r0 + 3 * wu, (dk >> 12) & 15), wu,
+                                       (dk >> 16) & 31);
+          v = dv + v;  // u = dec ú + P u (the residual: T = double)
         }
       }
       box[o] = v;
@@ -424,18 +429,19 @@ __device__ __forceinline__ void gen_z(const Gen<P>& gn, const Coefs& cf, const d
 // coarse boxes (TMA, 128-byte aligned slots), xy-passed coarse planes, the
 // generated box, the A x pass, the prolongation x pass, the P weight table,
 // then the section-word ring and the barriers.
-template <int P>
+template <int P, class T>
 struct GenSmem {
-  double *craw, *yvring, *box, *XA, *XB, *PX, *pws;
+  double* craw;  // TMA boxes of the coarse FP64 array
+  T *yvring, *box, *XA, *XB, *PX, *pws;
   uint32_t* wring;
   unsigned long long* cbar;
 };
-template <int P>
-__device__ __forceinline__ GenSmem<P> gen_smem(double* base, int ring_words) {
+template <int P, class T>
+__device__ __forceinline__ GenSmem<P, T> gen_smem(double* base, int ring_words) {
   using C = F3<P>;
-  GenSmem<P> m;
+  GenSmem<P, T> m;
   m.craw = base;
-  m.yvring = m.craw + C::NCB * C::CBS;
+  m.yvring = (T*)(m.craw + C::NCB * C::CBS);
   m.box = m.yvring + C::NCY * C::BOX;
   m.XA = m.box + C::BOX;
   m.XB = m.XA + C::NR * 32;
@@ -446,23 +452,24 @@ __device__ __forceinline__ GenSmem<P> gen_smem(double* base, int ring_words) {
   m.cbar = (unsigned long long*)((b + 7) & ~(uintptr_t)7);
   return m;
 }
-template <int P>
+template <int P, class T>
 __host__ __device__ constexpr size_t gen_smem_bytes(int ring_words) {
   using C = F3<P>;
-  return ((size_t)C::NCB * C::CBS + (size_t)C::NCY * C::BOX + C::BOX + 2 * C::NR * 32 + (size_t)C::CBY * C::RS +
-          2 * P * (P + 1)) * 8 + (size_t)ring_words * 4 + 8 + 8 * C::NCB;
+  return (size_t)C::NCB * C::CBS * 8 +
+         ((size_t)C::NCY * C::BOX + C::BOX + 2 * C::NR * 32 + (size_t)C::CBY * C::RS + 2 * P * (P + 1)) * sizeof(T) +
+         (size_t)ring_words * 4 + 8 + 8 * C::NCB;
 }
 
 // t_L = f_L - A_L u_L with u_L = dec ú_L + P u_{L-1} generated on chip;
 // r_L = enc(t_L); t_L -> HBM; ||t_L||^2 partial per warp (Alg 3.2).
 template <int P>
 __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual(const __grid_constant__ F3Args a,
-                                                              const __grid_constant__ Coefs cf) {
+                                                              const __grid_constant__ CoefT<double> cf) {
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, NW = C::NW, PF = C::PF;
   extern __shared__ __align__(128) double fsm[];
   const int RW = 3 * a.wu + 2;  // record words per box row
-  const GenSmem<P> m = gen_smem<P>(fsm, NW * NR * RW);
+  const GenSmem<P, double> m = gen_smem<P, double>(fsm, NW * NR * RW);
   const unsigned wring_s = smem_u32(m.wring);
 
   const int lane = threadIdx.x, w = threadIdx.y;
@@ -587,14 +594,14 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual(const __gri
 
 // b_L = dec r_L - A_L z_L with z_L = P w_{L-1} generated on chip -> B (the
 // t_L buffer).  Chebyshev step 1 (cFas1 of fmg_march3.cu).
-template <int P>
+template <int P, class T>
 __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_constant__ F3Args a,
-                                                          const __grid_constant__ Coefs cf) {
+                                                          const __grid_constant__ CoefT<T> cf) {
   using C = F3<P>;
   constexpr int R = C::R, NW = C::NW, PF = C::PF;
   extern __shared__ __align__(128) double fsm[];
   const int RW = a.wr + 1;
-  const GenSmem<P> m = gen_smem<P>(fsm, NW * FW * RW);
+  const GenSmem<P, T> m = gen_smem<P, T>(fsm, NW * FW * RW);
   const unsigned wring_s = smem_u32(m.wring);
 
   const int lane = threadIdx.x, w = threadIdx.y;
@@ -604,13 +611,13 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_co
   const int x = tl.x0 + lane, y = tl.y0 + w;
   const bool rowok = y < g.NY;
   const int tx = x % P, ty = y % P;
-  double km[R], kk[R];
+  T km[R], kk[R];
 #pragma unroll
   for (int o = 0; o < R; ++o) {
     km[o] = cf.Mc[tx][o];
     kk[o] = cf.Kc[tx][o];
   }
-  const double hl = pow2(-(a.l + 1));
+  const T hl = (T)pow2(-(a.l + 1));
   const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
   Gen<P> gn;
   gen_init<P>(gn, g, tl.x0, tl.y0, 0, 0, [](int) { return 0; });
@@ -644,9 +651,9 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_co
     cpa_commit();
   }
   int osl = 0;  // ring slot of the next output plane
-  double cr[R], sr[R];
+  T cr[R], sr[R];
 #pragma unroll
-  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
+  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0;
   int tzo = ((z0 % P) + P) % P;
   for (int i = 0; i < nin; ++i) {
     const int zi = z0 + i;
@@ -662,13 +669,13 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_co
       double* zp = a.Z + (long long)zi * tplane;
 #pragma unroll
       for (int k = 0; k < Gen<P>::KB; ++k)
-        if (gn.zo[k] >= 0) zp[gn.zo[k]] = m.box[gn.off[k]];
+        if (gn.zo[k] >= 0) zp[gn.zo[k]] = (double)m.box[gn.off[k]];
     }
     cpa_wait<PF>();
     __syncthreads();
     xpass<P>(m.box, 0, km, kk, m.XA, m.XB, w, lane);
     __syncthreads();
-    double c, s;
+    T c, s;
     ypass<P>(cf, ty, m.XA, m.XB, w, lane, c, s);
 #pragma unroll
     for (int o = 0; o < R - 1; ++o) {
@@ -678,11 +685,11 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_co
     cr[R - 1] = c;
     sr[R - 1] = s;
     if (produce) {
-      const double az = zpass<P>(cf, tzo, cr, sr) * hl;
+      const T az = zpass<P>(cf, tzo, cr, sr) * hl;
       if (rowok) {
         const uint32_t* rec = m.wring + osl * FW * RW + w * RW;
         const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
-        *Bp = rv - az;  // b = dec r - A z (B lives in the t_L buffer)
+        *Bp = (double)((T)rv - az);  // b = dec r - A z (B lives in the t_L buffer)
       }
       Bp += tplane;
       osl = osl + 1 == NW ? 0 : osl + 1;
@@ -696,19 +703,19 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_co
 // (invD b), y_2 = y_1 + d_2), A y_{j-1}, then q = b - A y, d_j = fma(al_j,
 // d_{j-1}, be_j (invD q)), y_j = y_{j-1} + d_j.  A step below k stores d_j;
 // the last one encodes ý_L and applies the correction.
-template <int P, int J>
+template <int P, int J, class T>
 __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_constant__ F3Args a,
-                                                          const __grid_constant__ Coefs cf) {
+                                                          const __grid_constant__ CoefT<T> cf) {
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX, NBF = C::NBF, NW = C::NW, PF = C::PF;
   constexpr int NA = J >= 3 ? 2 : 1;  // staged arrays: b (+ d_2)
   extern __shared__ __align__(128) double fsm[];
   double* ring = fsm;                        // NBF x NA boxes
-  double* yb = ring + NBF * NA * BOX;        // y_{j-1} on the current box
-  double* XA = yb + BOX;
-  double* XB = XA + NR * 32;
-  double* ivd = XB + NR * 32;                // invD factors: P node types x box
-  double* aring = ivd + P * BOX;             // NW x 2 x NT: z_l, P u_{l-1} at the output points (last step)
+  T* yb = (T*)(ring + NBF * NA * BOX);      // y_{j-1} on the current box
+  T* XA = yb + BOX;
+  T* XB = XA + NR * 32;
+  T* ivd = XB + NR * 32;                     // invD factors: P node types x box
+  double* aring = (double*)(ivd + P * BOX);  // NW x 2 x NT: z_l, P u_{l-1} at the output points (last step)
   const bool aux = a.last && (a.wout || a.uout);
   uint32_t* wring = (uint32_t*)(aring + (aux ? NW * 2 * 32 * FW : 0));  // NW x FW x (w + 1) (last step: ú words)
   const int RW = a.wu + 1;
@@ -722,19 +729,19 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
   const int x = tl.x0 + lane, y = tl.y0 + w;
   const bool rowok = y < g.NY;
   const int tx = x % P, ty = y % P;
-  double km[R], kk[R];
+  T km[R], kk[R];
 #pragma unroll
   for (int o = 0; o < R; ++o) {
     km[o] = cf.Mc[tx][o];
     kk[o] = cf.Kc[tx][o];
   }
-  const double hl = pow2(-(a.l + 1));
-  const double al = cf.cal[J - 1], be = cf.cbe[J - 1], ith = cf.inv_theta;
+  const T hl = (T)pow2(-(a.l + 1));
+  const T al = cf.cal[J - 1], be = cf.cbe[J - 1], ith = cf.inv_theta;
   const int hc = halo_col<P>(lane);
   // invD factors of the thread's staged elements for every z node type
   // (RN(1/diag) 2^(l+1), 0 at non-unknowns; the z-unknown test is per plane)
   {
-    const double isc = pow2(a.l + 1);
+    const T isc = (T)pow2(a.l + 1);
     const int xh = lane < P ? tl.x0 - P + lane : tl.x0 + 32 + lane - P;
     const bool ux = unk1(x, n), uxh = lane < 2 * P && unk1(xh, n);
     const int txo = ux ? x % P : 0, txh = uxh ? xh % P : 0;
@@ -747,8 +754,8 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
 #pragma unroll
         for (int tz = 0; tz < P; ++tz) {
           const int tb = (tz * P + tyy) * P;
-          ivd[tz * BOX + r * RS + P + lane] = (ux && uy) ? cf.invd[tb + txo] * isc : 0.0;
-          if (lane < 2 * P) ivd[tz * BOX + r * RS + hc] = (uxh && uy) ? cf.invd[tb + txh] * isc : 0.0;
+          ivd[tz * BOX + r * RS + P + lane] = (ux && uy) ? cf.invd[tb + txo] * isc : (T)0;
+          if (lane < 2 * P) ivd[tz * BOX + r * RS + hc] = (uxh && uy) ? cf.invd[tb + txh] * isc : (T)0;
         }
       }
     }
@@ -819,9 +826,9 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
     }
     cpa_commit();
   }
-  double cr[R], sr[R];
+  T cr[R], sr[R];
 #pragma unroll
-  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
+  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0;
   int tz = ((z0 % P) + P) % P;   // node type of plane z0 + i (input; = output plane z0 + i - P)
   int isl = 0, osl = 0, oisl = NBF - P;  // slots: input plane i, ú words of the next output, input plane i - P
   unsigned par = 0;              // barrier phase of slot isl
@@ -844,22 +851,22 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
     // y_{j-1} on the thread's staged elements of plane zi
     {
       const double* bb = ring + isl * NA * BOX + C::SH;
-      const double* iv = ivd + tz * BOX;
+      const T* iv = ivd + tz * BOX;
       const bool uz = zi >= 1 && zi <= n - 1;
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int r = w + k * FW;
         if (r < NR) {
           const int o = r * RS + P + lane;
-          const double f = uz ? iv[o] : 0.0;
-          double v = ith * (f * bb[o]);
-          if (J >= 3) v = v + bb[BOX + o];
+          const T f = uz ? iv[o] : (T)0;
+          T v = ith * (f * (T)bb[o]);
+          if (J >= 3) v = v + (T)bb[BOX + o];
           yb[o] = v;
           if (lane < 2 * P) {
             const int oh = r * RS + hc;
-            const double fh = uz ? iv[oh] : 0.0;
-            double vh = ith * (fh * bb[oh]);
-            if (J >= 3) vh = vh + bb[BOX + oh];
+            const T fh = uz ? iv[oh] : (T)0;
+            T vh = ith * (fh * (T)bb[oh]);
+            if (J >= 3) vh = vh + (T)bb[BOX + oh];
             yb[oh] = vh;
           }
         }
@@ -868,7 +875,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
     __syncthreads();
     xpass<P>(yb, 0, km, kk, XA, XB, w, lane);
     __syncthreads();
-    double c, s;
+    T c, s;
     ypass<P>(cf, ty, XA, XB, w, lane, c, s);
 #pragma unroll
     for (int o = 0; o < R - 1; ++o) {
@@ -879,32 +886,32 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
     sr[R - 1] = s;
     if (produce) {
       const int z = zi - P;
-      const double ay = zpass<P>(cf, tz, cr, sr) * hl;
+      const T ay = zpass<P>(cf, tz, cr, sr) * hl;
       const int o = (w + P) * RS + P + lane;
       const double* bo = ring + oisl * NA * BOX + C::SH + o;  // plane z, output point
-      const double b = bo[0];
-      const double f = (z >= 1 && z <= n - 1) ? ivd[tz * BOX + o] : 0.0;
-      double yprev = ith * (f * b);
-      double dprev = yprev;
+      const T b = (T)bo[0];
+      const T f = (z >= 1 && z <= n - 1) ? ivd[tz * BOX + o] : (T)0;
+      T yprev = ith * (f * b);
+      T dprev = yprev;
       if (J >= 3) {
-        dprev = bo[BOX];
+        dprev = (T)bo[BOX];
         yprev = yprev + dprev;
       }
-      const double qq = b - ay;
-      const double d = fma(al, dprev, be * (f * qq));
-      const double yv = yprev + d;
+      const T qq = b - ay;
+      const T d = fma(al, dprev, be * (f * qq));
+      const T yv = yprev + d;
       if (a.last) {
-        const double yq = warp_encode(yv, a.wr, nullptr, nullptr, lane, a.status);
+        const double yq = warp_encode((double)yv, a.wr, nullptr, nullptr, lane, a.status);
         if (rowok) {
           const double* ax = aring + osl * 2 * 32 * FW + tid;
-          if (a.wout) a.W[pbase0 + (long long)(z - tl.zs) * tplane] = ax[0] + yq;  // w_l = z_l + dec ý_l
+          if (a.wout) a.W[pbase0 + (long long)(z - tl.zs) * tplane] = (double)((T)ax[0] + (T)yq);  // w_l = z_l + dec ý_l
           const uint32_t* rec = wring + osl * FW * RW + w * RW;
           const double uo = warp_decode(rec, rec_e(rec + a.wu, eoff), a.wu, lane);
           const double uq = warp_encode(uo + yq, a.wu_out, ump, uep, lane, a.status);
           if (a.uout) a.U[pbase0 + (long long)(z - tl.zs) * tplane] = uq + ax[32 * FW];  // u_l = dec ú_l + P u_{l-1}
         }
       } else if (rowok) {
-        *Dp = d;
+        *Dp = (double)d;
       }
       Dp += tplane;
       ump += ustep;
@@ -923,20 +930,20 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
 // ------------------------------------------------------------------ host --
 template <int P>
 static int smem_res(int wu) {
-  return (int)gen_smem_bytes<P>(F3<P>::NW * F3<P>::NR * (3 * wu + 2)) + 16;
+  return (int)gen_smem_bytes<P, double>(F3<P>::NW * F3<P>::NR * (3 * wu + 2)) + 16;
 }
-template <int P>
+template <int P, class T>
 static int smem_cfas(int wr) {
-  return (int)gen_smem_bytes<P>(F3<P>::NW * FW * (wr + 1)) + 16;
+  return (int)gen_smem_bytes<P, T>(F3<P>::NW * FW * (wr + 1)) + 16;
 }
-template <int P>
+template <int P, class T>
 static int smem_cheb(int J, int wu, bool aux) {
   using C = F3<P>;
   const int NA = J >= 3 ? 2 : 1;
-  size_t d = (size_t)C::NBF * NA * C::BOX + C::BOX + 2 * C::NR * 32 + (size_t)P * C::BOX +
-             (aux ? (size_t)C::NW * 2 * 32 * FW : 0);
-  size_t wbytes = (size_t)C::NW * FW * (wu + 1) * 4 + 8;
-  return (int)(d * 8 + wbytes + 8 + 8 * C::NBF + 16);
+  const size_t d = (size_t)C::NBF * NA * C::BOX * 8 + (C::BOX + 2 * C::NR * 32 + (size_t)P * C::BOX) * sizeof(T) +
+                   (aux ? (size_t)C::NW * 2 * 32 * FW * 8 : 0);
+  const size_t wbytes = (size_t)C::NW * FW * (wu + 1) * 4 + 8;
+  return (int)(d + wbytes + 8 + 8 * C::NBF + 16);
 }
 
 int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
@@ -950,17 +957,40 @@ int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
 
 void fine3_set_attributes() {
   const int big = 200 * 1024;
-#define F(P)                                                                                 \
-  cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cfas<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);     \
-  cudaFuncSetAttribute(k_f3_cheb<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
-  cudaFuncSetAttribute(k_f3_cheb<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+#define F(P)                                                                                        \
+  cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);        \
+  cudaFuncSetAttribute(k_f3_cfas<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);    \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cfas<P, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);     \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   F(1) F(2) F(3)
 #undef F
 }
 
-template <typename K>
-static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Args& a, const Coefs& cf) {
+template <class T>
+static CoefT<T> coefs_as(const Coefs& c) {  // (FP32: the FP64 constants rounded to float, reading R28)
+  CoefT<T> t{};
+  for (int i = 0; i < 3; ++i)
+    for (int o = 0; o < 7; ++o) {
+      t.Kc[i][o] = (T)c.Kc[i][o];
+      t.Mc[i][o] = (T)c.Mc[i][o];
+    }
+  for (int r = 0; r < 6; ++r)
+    for (int k = 0; k < 4; ++k) t.Pw[r][k] = (T)c.Pw[r][k];
+  for (int i = 0; i < 27; ++i) t.invd[i] = (T)c.invd[i];
+  t.inv_theta = (T)c.inv_theta;
+  for (int j = 0; j < 8; ++j) {
+    t.cal[j] = (T)c.cal[j];
+    t.cbe[j] = (T)c.cbe[j];
+  }
+  t.rhs_c = c.rhs_c;
+  return t;
+}
+
+template <typename K, class CF>
+static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Args& a, const CF& cf) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nctas);
   cfg.blockDim = dim3(32, FW);
@@ -974,17 +1004,36 @@ static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Ar
   cudaLaunchKernelEx(&cfg, kernel, a, cf);
 }
 
-// kind: 0 residual, 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3)
-void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf) {
+template <int P, class T>
+static void launch_cfas_cheb(int kind, cudaStream_t st, const F3Args& a, const CoefT<T>& ct) {
   const int n = a.nitems;
   const bool aux = a.last && (a.wout || a.uout);
-#define F(P)                                                                                          \
-  if (kind == 0) f3_launch(k_f3_residual<P>, n, smem_res<P>(a.wu), st, a, cf);                        \
-  else if (kind == 1) f3_launch(k_f3_cfas<P>, n, smem_cfas<P>(a.wr), st, a, cf);                      \
-  else if (a.step == 2) f3_launch(k_f3_cheb<P, 2>, n, smem_cheb<P>(2, a.wu, aux), st, a, cf);         \
-  else f3_launch(k_f3_cheb<P, 3>, n, smem_cheb<P>(3, a.wu, aux), st, a, cf);
-  if (p == 1) { F(1) } else if (p == 2) { F(2) } else { F(3) }
-#undef F
+  if (kind == 1) f3_launch(k_f3_cfas<P, T>, n, smem_cfas<P, T>(a.wr), st, a, ct);
+  else if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T>, n, smem_cheb<P, T>(2, a.wu, aux), st, a, ct);
+  else f3_launch(k_f3_cheb<P, 3, T>, n, smem_cheb<P, T>(3, a.wu, aux), st, a, ct);
+}
+
+// kind: 0 residual, 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3);
+// `fp32`: FP32 cFas (kinds 1, 2; reading R28)
+void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf, int fp32) {
+  if (kind == 0) {
+    const CoefT<double> ct = coefs_as<double>(cf);
+    if (p == 1) f3_launch(k_f3_residual<1>, a.nitems, smem_res<1>(a.wu), st, a, ct);
+    else if (p == 2) f3_launch(k_f3_residual<2>, a.nitems, smem_res<2>(a.wu), st, a, ct);
+    else f3_launch(k_f3_residual<3>, a.nitems, smem_res<3>(a.wu), st, a, ct);
+    return;
+  }
+  if (fp32) {
+    const CoefT<float> ct = coefs_as<float>(cf);
+    if (p == 1) launch_cfas_cheb<1>(kind, st, a, ct);
+    else if (p == 2) launch_cfas_cheb<2>(kind, st, a, ct);
+    else launch_cfas_cheb<3>(kind, st, a, ct);
+  } else {
+    const CoefT<double> ct = coefs_as<double>(cf);
+    if (p == 1) launch_cfas_cheb<1>(kind, st, a, ct);
+    else if (p == 2) launch_cfas_cheb<2>(kind, st, a, ct);
+    else launch_cfas_cheb<3>(kind, st, a, ct);
+  }
 }
 
 }  // namespace fmg

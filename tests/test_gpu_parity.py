@@ -416,3 +416,18 @@ def test_kc_per_iteration_mode_parity(P, monkeypatch, lc, d, p, levels):
 def test_kc_per_iteration_mode_parity_mcgs(P, monkeypatch, d, p, levels):
     monkeypatch.setenv("FMG_LC", "2")
     compare_solvers(P, d, p, levels, smoother="mcgs")
+
+
+@pytest.mark.parametrize("d,p,levels", [(3, 1, 5), (3, 2, 4), (3, 3, 4), (3, 1, 7), (3, 3, 5)])
+def test_fmg_parity_fp32_cfas(P, d, p, levels):
+    """FP32 cFas (reading R28): every u and r section bit-identical to the
+    oracle's FP32-cFas solve (float trees with the FP64 constants rounded to
+    float), norms within 1e-6, H1 error within 1e-3."""
+    compare_solvers(P, d, p, levels, cfas_fp32=1)
+
+
+def test_fp32_cfas_refused_outside_its_path(P):
+    with pytest.raises(P.FmgError):
+        P.Solver(2, 1, 4, _gpu_sched(P, 2, 1, cfas_fp32=1))
+    with pytest.raises(P.FmgError):
+        P.Solver(3, 1, 4, _gpu_sched(P, 3, 1, cfas_fp32=1, smoother=1))
