@@ -94,7 +94,8 @@ _ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
 _FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p)
 _lib.fmg_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, C.c_void_p]
 
-EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_create_slabs", "fmg_create_dist", "fmg_nccl_unique_id",
+EXPORTS = ["fmg_set_allocator", "fmg_create", "fmg_create_slabs", "fmg_create_dist", "fmg_create_hostx",
+           "fmg_nccl_unique_id",
            "fmg_slab_plan", "fmg_solve_async", "fmg_solve", "fmg_solve_upto",
            "fmg_norms", "fmg_residual", "fmg_get_solution", "fmg_errors", "fmg_get_section",
            "fmg_info", "fmg_memory_model", "fmg_device_bytes", "fmg_enable_kernel_timing", "fmg_kernel_time", "fmg_kernel_times", "fmg_destroy",
