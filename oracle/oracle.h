@@ -61,6 +61,11 @@ typedef struct {
 } orc_level;
 
 void orc_level_geom(int d, int p, int l, orc_level* g);
+/* OpenMP threads the oracle's per-point loops use (OMP_NUM_THREADS; results
+ * do not depend on it: every output is one canonical chain of one thread,
+ * every norm a sequential sum). */
+int orc_threads(void);
+void orc_set_threads(int n);
 
 /* ---- BFP codec (orc_bfp.c) ---- */
 int orc_block_encode(const double* x, int w, int64_t* m, int* E);

@@ -74,6 +74,7 @@ static void sec_zero(sec_t* s, const orc_level* g, int w) {
 
 /* x = dec(section) (mantissa scaled by the block exponent) */
 static void sec_decode(const sec_t* s, const orc_level* g, double* x) {
+#pragma omp parallel for schedule(static)
   for (int64_t b = 0; b < g->nblk; ++b)
     for (int j = 0; j < 32; ++j)
       x[32 * b + j] = orc_block_decode_one(s->m[32 * b + j], s->E[b], s->w);
@@ -82,13 +83,15 @@ static void sec_decode(const sec_t* s, const orc_level* g, double* x) {
 /* section = enc_w(x): RNE per block (reading R8) */
 static int sec_encode(sec_t* s, const orc_level* g, const double* x, int w) {
   s->w = w;
+  int err = ORC_OK;
+#pragma omp parallel for schedule(static) reduction(max : err)
   for (int64_t b = 0; b < g->nblk; ++b) {
     int E;
     int rc = orc_block_encode(x + 32 * b, w, s->m + 32 * b, &E);
-    if (rc) return rc;
+    if (rc) err = rc > err ? rc : err;
     s->E[b] = (int8_t)E;
   }
-  return ORC_OK;
+  return err;
 }
 
 void orc_destroy(orc_ctx* c) {
@@ -172,6 +175,7 @@ int orc_residual(orc_ctx* c, int L, double* norms) {
     double* pu = malloc(sizeof(double) * g->size);
     orc_prolong(d, p, l, c->ut[l - 1], pu);
     sec_decode(&c->u[l], g, c->ut[l]);
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < g->size; ++i) c->ut[l][i] = c->ut[l][i] + pu[i];
     free(pu);
   }
@@ -180,6 +184,7 @@ int orc_residual(orc_ctx* c, int L, double* norms) {
     const orc_level* g = &c->g[L];
     double* au = malloc(sizeof(double) * g->size);
     orc_apply_A(d, p, L, c->ut[L], au);
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < g->size; ++i) c->tt[L][i] = c->f[L][i] - au[i];
     free(au);
   }
@@ -215,6 +220,7 @@ static void chebyshev(const orc_ctx* c, int l, const double* b, double* y) {
   }
   for (int j = 2; j <= c->s.cheb_degree; ++j) {
     orc_apply_A(c->d, c->p, l, y, ay);
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < g->size; ++i) {
       double q = b[i] - ay[i];
       dv[i] = fma(c->cal[j - 1], dv[i], c->cbe[j - 1] * (iD[i] * q));
@@ -560,6 +566,7 @@ int orc_decode_solution(orc_ctx* c, int L, double* uhat) {
     double* pu = malloc(sizeof(double) * g->size);
     orc_prolong(c->d, c->p, l, c->ut[l - 1], pu);
     sec_decode(&c->u[l], g, c->ut[l]);
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < g->size; ++i) c->ut[l][i] = c->ut[l][i] + pu[i];
     free(pu);
   }

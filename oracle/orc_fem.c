@@ -130,6 +130,9 @@ static void pass1d(int p, int kind, const double* C, int axis,
                    const double* in, dims_t di, double* out, dims_t dout) {
   int nout = dout.n[axis], nin = di.n[axis];
   int64_t sin[3] = {1, di.sx, (int64_t)di.sx * di.n[1]};
+  /* (OpenMP over output rows: every output is one canonical chain computed by
+   * one thread, so the result does not depend on the thread count) */
+#pragma omp parallel for collapse(2) schedule(static)
   for (int z = 0; z < dout.n[2]; ++z)
     for (int y = 0; y < dout.n[1]; ++y)
       for (int x = 0; x < dout.sx; ++x) {
@@ -205,6 +208,7 @@ void orc_apply_A(int d, int p, int l, const double* u, double* out) {
     for (int64_t i = 0; i < N; ++i) dd[i] = dd[i] + e[i]; /* s */
     double h = ldexp(1.0, -(l + 1));
     int64_t sz = (int64_t)g.sx * g.n[1];
+#pragma omp parallel for collapse(2) schedule(static)
     for (int z = 0; z < n; ++z)
       for (int y = 0; y < n; ++y)
         for (int x = 0; x < g.sx; ++x) {
@@ -238,6 +242,7 @@ static void pass1d_f32(int p, int kind, const float* C, int axis,
                        const float* in, dims_t di, float* out, dims_t dout) {
   int nout = dout.n[axis], nin = di.n[axis];
   int64_t sin[3] = {1, di.sx, (int64_t)di.sx * di.n[1]};
+#pragma omp parallel for collapse(2) schedule(static)
   for (int z = 0; z < dout.n[2]; ++z)
     for (int y = 0; y < dout.n[1]; ++y)
       for (int x = 0; x < dout.sx; ++x) {
@@ -301,6 +306,7 @@ void orc_apply_A_f32(int d, int p, int l, const float* u, float* out) {
     for (int64_t i = 0; i < N; ++i) dd[i] = dd[i] + e[i]; /* s */
     const float h = ldexpf(1.0f, -(l + 1));
     int64_t sz = (int64_t)g.sx * g.n[1];
+#pragma omp parallel for collapse(2) schedule(static)
     for (int z = 0; z < n; ++z)
       for (int y = 0; y < n; ++y)
         for (int x = 0; x < g.sx; ++x) {
@@ -607,3 +613,13 @@ void orc_cheb_coefs(const orc_schedule* s, double* inv_theta, double* al, double
     rho = rn;
   }
 }
+
+/* Threads the OpenMP loops of the oracle use (1 without OpenMP). */
+#ifdef _OPENMP
+#include <omp.h>
+int orc_threads(void) { return omp_get_max_threads(); }
+void orc_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
+#else
+int orc_threads(void) { return 1; }
+void orc_set_threads(int n) { (void)n; }
+#endif
