@@ -815,39 +815,47 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_sq(const DevCtx* 
 // the previous cycle (guess), ý_0 = enc_wr(y_0) stored, w_0 = dec ý_0; after
 // the last cycle ú_0 = enc_wu(dec ú_0 + dec ý_0) and u_0 = dec ú_0.
 template <int D, int P>
-__global__ void __launch_bounds__(32) k_coarse_nu(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a) {
+__global__ void __launch_bounds__(128) k_coarse_nu(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a) {
   pdl_wait();
   pdl_trigger();
   constexpr int m = 2 * P - 1, n0 = D == 3 ? m * m * m : m * m;
-  __shared__ double sb[128];
+  __shared__ double sb[128], sy[128];
   const DevCtx& dc = *cp;
   const MPtrs& c = a.p;
   const LevelDev& lv = a.lv;
   const Geom g = lv.g;
-  const int lane = threadIdx.x, nxb = g.NX >> 5;
-  for (int J = lane; J < n0; J += 32) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nxb = g.NX >> 5;
+  for (int J = tid; J < n0; J += 128) {
     const int jx = J % m + 1, jy = (J / m) % m + 1, jz = D == 3 ? J / (m * m) + 1 : 0;
     sb[J] = c.B[((long long)jz * g.NY + jy) * g.NX + jx];
   }
-  __syncwarp();
-  for (int zr = 0; zr < (D == 3 ? g.NZ : 1); ++zr) {
-    for (int y = 0; y < g.NY; ++y) {
-      const int x = lane;
-      double s = 0.0;
-      if (unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(zr, g.n))) {
-        const int I = ((D == 3 ? zr - 1 : 0) * m + (y - 1)) * m + (x - 1);
-        const double* Ai = dc.Ainv + (long long)I * n0;
-        for (int J = 0; J < n0; ++J) s = fma(Ai[J], sb[J], s);
-      }
-      const long long row = (long long)zr * g.NY + y, blk = row * nxb;
-      if (a.guess) s = warp_decode(lv.ymant + blk * lv.ystride, lv.yexp[blk], a.wr, lane) + s;
-      const double yq = warp_encode(s, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
-      lv.W[row * g.NX + x] = yq;
-      if (!a.store) {
-        const double uo = warp_decode(lv.umant + blk * lv.ustride, lv.uexp[blk], a.wu_in, lane);
-        const double uq = warp_encode(uo + yq, a.wu_out, lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
-        lv.U[row * g.NX + x] = uq;
-      }
+  __syncthreads();
+  // y_0 = A_0^{-1} b_0: one unknown per thread, acc = fma(Ainv[I][J], b_J, acc)
+  // over J ascending; the row's loads are independent of the
+  // chain, so they are unrolled ahead of it
+  for (int I = tid; I < n0; I += 128) {
+    const double* Ai = dc.Ainv + (long long)I * n0;
+    double s = 0.0;
+#pragma unroll 8
+    for (int J = 0; J < n0; ++J) s = fma(Ai[J], sb[J], s);
+    sy[I] = s;
+  }
+  __syncthreads();
+  // codec rows (warp-cooperative): ý_0, w_0 and the ú_0 correction
+  const int nrows = (D == 3 ? g.NZ : 1) * g.NY;
+  for (int row = wid; row < nrows; row += 4) {
+    const int zr = D == 3 ? row / g.NY : 0, y = row - zr * g.NY, x = lane;
+    double s = 0.0;
+    if (unk1(x, g.n) && unk1(y, g.n) && (D == 2 || unk1(zr, g.n)))
+      s = sy[((D == 3 ? zr - 1 : 0) * m + (y - 1)) * m + (x - 1)];
+    const long long blk = (long long)row * nxb;
+    if (a.guess) s = warp_decode(lv.ymant + blk * lv.ystride, lv.yexp[blk], a.wr, lane) + s;
+    const double yq = warp_encode(s, a.wr, lv.ymant + blk * lv.ystride, lv.yexp + blk, lane, c.status);
+    lv.W[(long long)row * g.NX + x] = yq;
+    if (!a.store) {
+      const double uo = warp_decode(lv.umant + blk * lv.ustride, lv.uexp[blk], a.wu_in, lane);
+      const double uq = warp_encode(uo + yq, a.wu_out, lv.umant + blk * lv.ustride, lv.uexp + blk, lane, c.status);
+      lv.U[(long long)row * g.NX + x] = uq;
     }
   }
 }
@@ -945,7 +953,7 @@ void launch_coarse_nu(int dim, int p, cudaStream_t st, const void* devctx, const
   const DevCtx* c = (const DevCtx*)devctx;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1);
-  cfg.blockDim = dim3(32);
+  cfg.blockDim = dim3(128);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
