@@ -1,0 +1,18 @@
+# Round-2 evidence (one gpurun call): bench lines, launch lists and the ncu
+# capture of the roofline kernel.  /usr/local/graft/bin/gpurun --timeout 3000 -- 'bash tools/evidence_r2.sh'
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/ev
+make -s -C oracle > /dev/null 2>&1
+nproc > gpurun_out/ev/nproc.txt
+B="timeout 900 python bench.py"
+$B > gpurun_out/ev/bench_C4.json 2> gpurun_out/ev/bench_C4.err; echo C4 $?
+for c in C3 C2 C1 C5h; do $B --config $c --steps 5 --warmup 3 > gpurun_out/ev/bench_$c.json 2> gpurun_out/ev/bench_$c.err; echo $c $?; done
+$B --cfas-fp32 --steps 5 --warmup 3 > gpurun_out/ev/bench_C4_fp32.json 2>/dev/null; echo C4fp32 $?
+$B --config C3 --cfas-fp32 --steps 5 --warmup 3 > gpurun_out/ev/bench_C3_fp32.json 2>/dev/null; echo C3fp32 $?
+FMG_F3MAT=0 $B --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_C4_lean.json 2>/dev/null; echo C4lean $?
+FMG_FINE3=0 $B --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_C4_level_by_level.json 2>/dev/null; echo C4old $?
+$B --impl reference --steps 3 --warmup 3 > gpurun_out/ev/bench_C4_reference.json 2>/dev/null; echo ref $?
+$B --workload n4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_n4.json 2>/dev/null; echo n4 $?
+timeout 300 python tools/profile_one.py C4 1 > /dev/null 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/ev/c4_launches.csv python tools/profile_one.py C4 1 > /dev/null 2>&1; echo list4 $?
+timeout 300 python tools/profile_one.py C3 1 > /dev/null 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/ev/c3_launches.csv python tools/profile_one.py C3 1 > /dev/null 2>&1; echo list3 $?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_f3|k_m3_residual|k_m3_restrict|k_m3_prolong" -s 391 -c 6 -o gpurun_out/ev/c4_full python tools/profile_one.py C4 1 > gpurun_out/ev/ncu_full.log 2>&1; echo full $?
