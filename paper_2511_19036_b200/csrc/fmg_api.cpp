@@ -282,11 +282,11 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
   fmg_ctx* c = b.c;
   const int P = c->p, k = c->s.cheb_degree;
   const bool top = l == L, uout = !top || c->f3mat;
-  if (uout) {
+  if (uout) {  // P u_{l-1} at the level's points (k_f3_prolong)
     if (xch) b.xchg(XA_U, l - 1, P);
     OpDesc q = mkop(OP_PROLONG, l, L);
-    q.puonly = 1;
-    b.grid(q);
+    q.step = 0;
+    b.fine(3, q);
   }
   if (xch) b.xchg(XA_W, l - 1, 2 * P);
   for (int step = 1; step <= k; ++step) {
@@ -532,13 +532,19 @@ void build_solve(Builder& b, int Lstop, int iters_last) {
         b.xchg(XA_U, L - 2, c->p);
         OpDesc o = mkop(OP_DECODE, L - 1, L - 1);
         o.wu_in = c->wu_cur[L - 1];
-        b.grid(o, -1);
+        o.step = 1;
+        b.fine(3, o, -1);  // (L - 1 > lc >= 0: a coarser level exists)
       }
     } else {
       b.xchg(XA_U, L - 1, c->p);
       OpDesc o = mkop(OP_DECODE, L, L);
       o.wu_in = c->wu_cur[L];
-      b.grid(o, (L == c->Lmax) ? 2 : -1);
+      if (c->fine3) {  // (materialised: u_L = P u_{L-1}, ú_L = 0)
+        o.step = 1;
+        b.fine(3, o, (L == c->Lmax) ? 2 : -1);
+      } else {
+        b.grid(o, (L == c->Lmax) ? 2 : -1);
+      }
     }
     int iters = (L == Lstop) ? iters_last : c->s.n_ir;
     for (int it = 0; it < iters; ++it) build_iteration(b, L, it);
@@ -696,7 +702,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.poff = o.poff;
   a.status = c->status;
   const CUtensorMap* base = c->tm_dev;
-  if (l >= 1) a.tmc = base + (it.f3kind == 0 ? 6 : 7) * kMaxLev + (l - 1);
+  if (l >= 1) a.tmc = base + (it.f3kind == 0 || it.f3kind == 3 ? 6 : 7) * kMaxLev + (l - 1);
   a.tmb = base + 8 * kMaxLev + l;
   a.tmd = base + 9 * kMaxLev + l;
   return a;

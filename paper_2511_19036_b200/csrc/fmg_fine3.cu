@@ -927,6 +927,130 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
   }
 }
 
+// P u_{l-1} at the points of the 32 x 8 tile, marched along z (no halo): the
+// P-u-only prolongation of the finest-level path (PU for the last Chebyshev
+// step) and the level-push decode u_l = dec ú_l + P u_{l-1}.  Same coarse-box
+// TMA ring and canonical x, y, z passes as the generating kernels (DESIGN.md
+// §3.3), but one point per thread: warp w's x pass covers coarse rows w,
+// w + 8 of the box, its y pass and z pass fine row y0 + w.  Replaces
+// k_m3_prolong's per-point (p+1)^2 global loads by shared boxes.
+template <int P>
+__global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant__ F3Args a,
+                                                            const __grid_constant__ CoefT<double> cf) {
+  using C = F3<P>;
+  constexpr int CBX = C::CBX, CBY = C::CBY, NCB = C::NCB, NCY = C::NCY, PF = C::PF, NW = C::NW;
+  extern __shared__ __align__(128) double fsm[];
+  double* craw = fsm;                         // NCB coarse boxes (TMA)
+  double* PX = craw + NCB * C::CBS;           // CBY x 32: x pass
+  double* yv = PX + CBY * 32;                 // NCY x FW x 32: xy-passed coarse planes at the tile
+  uint32_t* wring = (uint32_t*)(yv + NCY * FW * 32);  // NW x FW x (w + 1): ú words (decode mode)
+  const int RW = a.wu + 1;
+  unsigned long long* cbar = (unsigned long long*)(wring + NW * FW * RW + 2);
+  cbar = (unsigned long long*)(((uintptr_t)cbar + 7) & ~(uintptr_t)7);
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const F3Tile tl = f3_tile(a);
+  const Geom g = a.g;
+  const int n = g.n;
+  const int x = tl.x0 + lane, y = tl.y0 + w;
+  const bool rowok = y < g.NY;
+  const bool okx = unk1(x, n), oky = unk1(y, n);
+  Gen<P> gn;  // (only the coarse-box bookkeeping: origin, plane range, TMA ring)
+  gn.cx0 = (P * (max(tl.x0 - P, 1) / (2 * P))) & ~1;
+  gn.cy0 = P * (max(tl.y0 - P, 1) / (2 * P));
+  gn.czoff = a.czoff;
+  gen_range<P>(gn, tl.zs, tl.ze - tl.zs, n);
+  const int bxo = okx ? P * (x / (2 * P)) - gn.cx0 : 0, rx = okx ? x % (2 * P) : 0;
+  const int byo = oky ? P * (y / (2 * P)) - gn.cy0 : 0, ry = oky ? y % (2 * P) : 0;
+  double pwx[P + 1], pwy[P + 1];
+#pragma unroll
+  for (int t = 0; t <= P; ++t) {
+    pwx[t] = cf.Pw[rx][t];
+    pwy[t] = cf.Pw[ry][t];
+  }
+  const bool decode = a.step == 1;  // (1: u_l = dec ú_l + P u_{l-1} -> U; 0: P u_{l-1} -> PU)
+  int eoff = 0;
+  const WStream ws = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, y, tl.zs, w * RW, rowok && decode, lane,
+                              eoff);
+  const unsigned wring_s = smem_u32(wring);
+  const long long tplane = (long long)g.NY * g.NX;
+  double* out = (decode ? a.U : a.PU) + ((long long)tl.zs * g.NY + y) * g.NX + x;
+  const int nout = tl.ze - tl.zs;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < NCB; ++k) mbar_init(cbar + k, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    for (int k = 0; k < NCB; ++k) gen_request<P>(gn, a.tmc, craw, cbar, gn.cfirst + k);
+#pragma unroll
+  for (int j = 0; j < PF; ++j) {
+    if (j < nout) wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
+    cpa_commit();
+  }
+  int osl = 0;
+  for (int j = 0; j < nout; ++j) {
+    const int z = tl.zs + j;
+    {
+      const int sl = osl + PF >= NW ? osl + PF - NW : osl + PF;
+      if (j + PF < nout) wcopy(ws, wring_s + (unsigned)(sl * FW * RW * 4), j + PF);
+    }
+    cpa_commit();
+    const bool okz = unk1(z, n);
+    if (okz) {
+      const int cneed = cbase<P>(z) + P;
+      while (gn.cdone <= cneed) {  // x and y passes of the next coarse plane
+        const int c = gn.cdone, k = c - gn.cfirst;
+        mbar_wait_s(smem_u32(cbar) + 8u * (unsigned)(k % NCB), (unsigned)(k / NCB) & 1u);
+        const double* cb = craw + (k % NCB) * C::CBS;
+#pragma unroll
+        for (int q = 0; q < (CBY + FW - 1) / FW; ++q) {
+          const int cr = w + q * FW;
+          if (cr < CBY) {
+            double acc = 0.0;
+            if (okx) {
+#pragma unroll
+              for (int t = 0; t <= P; ++t) acc = fma(pwx[t], cb[cr * CBX + bxo + t], acc);
+            }
+            PX[cr * 32 + lane] = acc;
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && threadIdx.y == 0) gen_request<P>(gn, a.tmc, craw, cbar, c + NCB);
+        double acc = 0.0;
+        if (oky) {
+#pragma unroll
+          for (int t = 0; t <= P; ++t) acc = fma(pwy[t], PX[(byo + t) * 32 + lane], acc);
+        }
+        yv[((c % NCY) * FW + w) * 32 + lane] = acc;
+        gn.cdone = c + 1;
+        __syncthreads();
+      }
+    }
+    double pu = 0.0;
+    if (okz) {
+      const int rz = z % (2 * P), cb0 = cbase<P>(z);
+#pragma unroll
+      for (int t = 0; t <= P; ++t) pu = fma(cf.Pw[rz][t], yv[(((cb0 + t) % NCY) * FW + w) * 32 + lane], pu);
+    }
+    if (decode) {
+      cpa_wait<PF>();
+      __syncwarp();
+      if (rowok) {
+        const uint32_t* rec = wring + osl * FW * RW + w * RW;
+        const double dv = warp_decode(rec, rec_e(rec + a.wu, eoff), a.wu, lane);
+        *out = dv + pu;  // u_l = dec ú_l + P u_{l-1}
+      }
+    } else if (rowok) {
+      *out = pu;
+    }
+    out += tplane;
+    osl = osl + 1 == NW ? 0 : osl + 1;
+  }
+}
+
 // ------------------------------------------------------------------ host --
 template <int P>
 static int smem_res(int wu) {
@@ -946,6 +1070,13 @@ static int smem_cheb(int J, int wu, bool aux) {
   return (int)(d + wbytes + 8 + 8 * C::NBF + 16);
 }
 
+template <int P>
+static int smem_prolong(int wu) {
+  using C = F3<P>;
+  const size_t d = (size_t)C::NCB * C::CBS + C::CBY * 32 + (size_t)C::NCY * FW * 32;
+  return (int)(d * 8 + (size_t)C::NW * FW * (wu + 1) * 4 + 8 + 8 + 8 * C::NCB + 16);
+}
+
 int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
   switch (p) {
     case 1: *cbx = F3<1>::CBX; *cby = F3<1>::CBY; *rs = F3<1>::RS; *nr = F3<1>::NR; return 0;
@@ -959,6 +1090,7 @@ void fine3_set_attributes() {
   const int big = 200 * 1024;
 #define F(P)                                                                                        \
   cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);        \
+  cudaFuncSetAttribute(k_f3_prolong<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);         \
   cudaFuncSetAttribute(k_f3_cfas<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);    \
   cudaFuncSetAttribute(k_f3_cheb<P, 2, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cheb<P, 3, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -1013,9 +1145,16 @@ static void launch_cfas_cheb(int kind, cudaStream_t st, const F3Args& a, const C
   else f3_launch(k_f3_cheb<P, 3, T>, n, smem_cheb<P, T>(3, a.wu, aux), st, a, ct);
 }
 
-// kind: 0 residual, 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3);
+// kind: 0 residual, 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3), 3 prolongation;
 // `fp32`: FP32 cFas (kinds 1, 2; reading R28)
 void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf, int fp32) {
+  if (kind == 3) {  // P u_{l-1} (step 0) or u_l = dec ú_l + P u_{l-1} (step 1) at the tile points
+    const CoefT<double> ct = coefs_as<double>(cf);
+    if (p == 1) f3_launch(k_f3_prolong<1>, a.nitems, smem_prolong<1>(a.wu), st, a, ct);
+    else if (p == 2) f3_launch(k_f3_prolong<2>, a.nitems, smem_prolong<2>(a.wu), st, a, ct);
+    else f3_launch(k_f3_prolong<3>, a.nitems, smem_prolong<3>(a.wu), st, a, ct);
+    return;
+  }
   if (kind == 0) {
     const CoefT<double> ct = coefs_as<double>(cf);
     if (p == 1) f3_launch(k_f3_residual<1>, a.nitems, smem_res<1>(a.wu), st, a, ct);
