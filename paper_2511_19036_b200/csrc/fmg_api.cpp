@@ -70,7 +70,6 @@ struct fmg_ctx {
   double* Ul[kMaxLev]{};          // per-level u_l, t_l, w_l (padded level layout)
   double* Tl[kMaxLev]{};
   double* Wl[kMaxLev]{};
-  bool march = false;             // grid levels run the march kernels (fmg_march.cu 2D, fmg_march3.cu 3D)
   int mrc[kMaxLev]{}, mitems[kMaxLev]{};  // march rows / planes per chunk, work items (3D: CTAs) per level
   int mnyb[kMaxLev]{};
   // TMA maps of the staged arrays (march kernels): u_l rows /
@@ -198,8 +197,7 @@ struct Builder {
   long long ptot = 0;  // (set past the KC partial region by make_builder)
   // reserve partial slots for (row, level l) and record the deferred norm
   long long slot(int row, int l) {
-    int nt = !c->march ? c->tiles[l][0] * c->tiles[l][1] * c->tiles[l][2]
-                       : (c->dim == 2 ? c->mitems[l] : c->mitems[l] * march3_rows());
+    int nt = c->dim == 2 ? c->mitems[l] : c->mitems[l] * march3_rows();
     long long off = ptot;
     ptot += nt;
     NormEntry e{off, row, l, nt, 0};
@@ -422,7 +420,7 @@ void build_iteration(Builder& b, int L, int it) {
   // every level of the iteration is a grid op, level 0 through cFas1 +
   // k_coarse_nu (with nu = 1 its one cycle has guess = store = 0, i.e. the
   // plain V(0,1) cycle of Alg 3.1)
-  if (c->s.nu > 1 || (c->lc == 0 && c->G == 1 && c->march)) {  // (the tile-box path has no level-0 grid ops)
+  if (c->s.nu > 1 || (c->lc == 0 && c->G == 1)) {
     build_iteration_nu(b, L, it);
     return;
   }
@@ -473,7 +471,7 @@ void build_iteration(Builder& b, int L, int it) {
       c->wu_cur[l] = wu(c, l, L);
       continue;
     }
-    if (c->march && c->dim == 3) {  // z_l = P w_{l-1}, P u_{l-1} (fmg_march3.cu k_m3_prolong)
+    if (c->dim == 3) {  // z_l = P w_{l-1}, P u_{l-1} (fmg_march3.cu k_m3_prolong)
       b.xchg(XA_W, l - 1, P);
       b.xchg(XA_U, l - 1, P);
       OpDesc q = mkop(OP_PROLONG, l, L);
@@ -723,19 +721,11 @@ void issue_item(fmg_ctx* c, const Item& it) {
     mark(c, -2);
   } else {
     mark(c, it.timed_cls);
-    if (c->march) {
+    {
       const MArgs m = march_args(c, it.op);
       if (it.op.type == OP_COARSE) launch_coarse_nu(c->dim, c->p, c->cur, c->devctx, m);
       else if (c->dim == 2) launch_march(c->p, c->cur, c->devctx, m, c->cf);
       else launch_march3(c->p, c->cur, c->devctx, m, c->cf);
-    } else {
-      int tx = 1, ty = 1, tz = 1;
-      if (it.op.type != OP_NORMS) {
-        tx = c->tiles[it.op.l][0];
-        ty = c->tiles[it.op.l][1];
-        tz = c->tiles[it.op.l][2];
-      }
-      launch_op(c->dim, c->p, c->cur, c->devctx, it.op, tx, ty, tz);
     }
     mark(c, it.timed_cls);
   }
@@ -1098,11 +1088,6 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   march_set_attributes();
   march3_set_attributes();
   fine3_set_attributes();
-  c->march = !(getenv("FMG_MARCH") && atoi(getenv("FMG_MARCH")) == 0);
-  if ((s->smoother == 1 || s->nu > 1 || (s->nu > 1 && G > 1)) && !c->march) {  // (tile-box kernels: Chebyshev, nu = 1)
-    fmg_destroy(c);
-    return FMG_EINVAL;
-  }
   if (s->nu > 1 && G > 1) {  // (nu > 1: single GPU this round)
     fmg_destroy(c);
     return FMG_EINVAL;
@@ -1112,8 +1097,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     if (e != cudaSuccess) fprintf(stderr, "[fmg] set_kernel_attributes: %s\n", cudaGetErrorString(e));
   }
   build_coefs(dim, p, s->lambda_hi, s->alpha, s->cheb_degree, &c->cf);
-  int TY, TZ;
-  tile_shape(dim, p, &TY, &TZ);
+  const int TY = dim == 3 ? 8 : 16, TZ = dim == 3 ? 4 : 1;  // (tile counts of the norm-partial table)
   int rc = FMG_OK;
   long long tot_parts = 0;
   DevCtxDesc dd{};
@@ -1222,7 +1206,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   // (the residual's three-block section records fit one warp).
   {
     const char* e = getenv("FMG_FINE3");
-    c->fine3 = rc == FMG_OK && dim == 3 && c->march && s->nu <= 1 && s->smoother == 0 &&
+    c->fine3 = rc == FMG_OK && dim == 3 && s->nu <= 1 && s->smoother == 0 &&
                (s->cheb_degree == 2 || s->cheb_degree == 3) && Lmax > c->lc && s->b_u <= 10 && !(e && atoi(e) == 0);
   }
   if (rc == FMG_OK && s->cfas_fp32 && !c->fine3) rc = FMG_EINVAL;  // (FP32 cFas runs in the finest-level kernels)
@@ -1292,7 +1276,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
   {
     const char* e = getenv("FMG_TMA");
     const int want = e ? atoi(e) : -1;
-    c->tma = c->march && (want == 1 || (want < 0 && dim == 3));
+    c->tma = want == 1 || (want < 0 && dim == 3);
   }
   for (int l = 0; l <= Lmax && rc == FMG_OK && c->tma; ++l) {
     const Geom& g = c->g[l];

@@ -205,14 +205,9 @@ struct Launch {
 
 // Kernel side (fmg_kernels.cu).
 void set_kernel_attributes();
-int smem_bytes(int dim, int p);
-void tile_shape(int dim, int p, int* TY, int* TZ);
 size_t devctx_size();
 void set_devctx_pbase(void* host_buf, double* pbase);
-size_t op_size();
 void fill_devctx(void* host_buf, const DevCtxDesc& d);
-void pack_op(void* dst, const OpDesc& od);
-void launch_op(int dim, int p, cudaStream_t st, const void* devctx, const OpDesc& od, int tx, int ty, int tz);
 void march_set_attributes();
 void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);
 void march3_set_attributes();

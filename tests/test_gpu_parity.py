@@ -134,14 +134,6 @@ def test_fmg_parity_staging_paths(P, monkeypatch, tma, d, p, levels):
     compare_solvers(P, d, p, levels)
 
 
-@pytest.mark.parametrize("d,p,levels", [(2, 1, 6), (2, 2, 5), (2, 3, 4), (3, 1, 4), (3, 2, 3), (3, 3, 3)])
-def test_fmg_parity_tile_path(P, monkeypatch, d, p, levels):
-    """The tile-box kernels (FMG_MARCH=0, the first-round design kept for A/B
-    comparison) stay bit-exact too."""
-    monkeypatch.setenv("FMG_MARCH", "0")
-    compare_solvers(P, d, p, levels)
-
-
 def test_fmg_parity_C1(P):
     c = CONFIGS["C1"]
     compare_solvers(P, c["dim"], c["p"], c["levels"])
