@@ -37,10 +37,11 @@
 #ifndef F3_PF
 #define F3_PF 2      // staging / section-word lookahead (planes)
 #endif
-// CTAs per SM the register budget is sized for: P = 1 fits 3 (80 registers,
-// C3 -6 %), P = 3 needs ~128 registers (3 CTAs spill: C4 +18 %)
+// CTAs per SM the register budget is sized for (measured): P = 1 fits 4 (64
+// registers; C3 -1.3 % against 3, -6 % for 3 against 2), P = 2 fits 3, P = 3
+// needs ~128 registers (3 CTAs spill: C4 +18 %)
 #ifndef F3_MINB
-#define F3_MINB(P) ((P) == 3 ? 2 : 3)
+#define F3_MINB(P) ((P) == 3 ? 2 : ((P) == 1 ? 4 : 3))
 #endif
 
 namespace fmg {
