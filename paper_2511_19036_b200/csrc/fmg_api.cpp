@@ -350,7 +350,7 @@ void build_iteration_nu(Builder& b, int L, int it) {
     o.wu_in = c->wu_cur[L];
     o.row = row;
     o.poff = b.slot(row, L);
-    if (c->fine3 && !c->f3mat) b.fine(0, o, fine ? 0 : -1);  // u_L generated on chip (fmg_fine3.cu)
+    if (c->fine3) b.fine(c->f3mat ? 4 : 0, o, fine ? 0 : -1);  // u_L generated on chip / staged (fmg_fine3.cu)
     else b.grid(o, fine ? 0 : -1);
   }
   for (int l = L - 1; l >= 0; --l) {
@@ -440,7 +440,8 @@ void build_iteration(Builder& b, int L, int it) {
       b.fine(0, o, fine ? 0 : -1);
     } else {
       b.xchg(XA_U, L, P);
-      b.grid(o, fine ? 0 : -1);
+      if (c->fine3) b.fine(4, o, fine ? 0 : -1);
+      else b.grid(o, fine ? 0 : -1);
     }
     for (int l = L - 1; l > lc; --l) {
       b.xchg(XA_T, l + 1, 2 * P - 1);
@@ -701,7 +702,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.status = c->status;
   const CUtensorMap* base = c->tm_dev;
   if (l >= 1) a.tmc = base + (it.f3kind == 0 || it.f3kind == 3 ? 6 : 7) * kMaxLev + (l - 1);
-  a.tmb = base + 8 * kMaxLev + l;
+  a.tmb = base + (it.f3kind == 4 ? 0 : 8) * kMaxLev + l;  // (kind 4: the u_l boxes)
   a.tmd = base + 9 * kMaxLev + l;
   return a;
 }

@@ -1052,6 +1052,120 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
   }
 }
 
+// t_L = f_L - A_L u_L with u_L staged by TMA (the materialised form,
+// DESIGN.md §4.3); r_L = enc(t_L); t_L -> HBM; ||t_L||^2 partial per warp.
+// The skeleton of k_f3_cheb (specialised y / z passes, incremental slots)
+// around the old k_m3_residual's arithmetic.
+template <int P>
+__global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual_s(const __grid_constant__ F3Args a,
+                                                                         const __grid_constant__ CoefT<double> cf) {
+  using C = F3<P>;
+  constexpr int R = C::R, NR = C::NR, BOX = C::BOX, NBF = C::NBF, PF = C::PF;
+  extern __shared__ __align__(128) double fsm[];
+  double* ring = fsm;  // NBF boxes of u_L
+  double* XA = ring + NBF * BOX;
+  double* XB = XA + NR * 32;
+  unsigned long long* bars = (unsigned long long*)(XB + NR * 32);
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const F3Tile tl = f3_tile(a);
+  const Geom g = a.g;
+  const int n = g.n;
+  const int x = tl.x0 + lane, y = tl.y0 + w;
+  const bool rowok = y < g.NY;
+  const int tx = x % P, ty = y % P;
+  double km[R], kk[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) {
+    km[o] = cf.Mc[tx][o];
+    kk[o] = cf.Kc[tx][o];
+  }
+  const double hl = pow2(-(a.l + 1));
+  const double* __restrict__ gt = a.gtab;
+  const bool uxy = unk1(x, n) && unk1(y, n);
+  const double gxy = uxy ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
+  const int nxb = g.NX >> 5;
+  const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
+  const long long tplane = (long long)g.NY * g.NX, bpp = (long long)g.NY * nxb;
+  double* Tp = a.T + ((long long)tl.zs * g.NY + y) * g.NX + x;
+  const long long blk0 = ((long long)tl.zs * g.NY + y) * nxb + (tl.x0 >> 5);
+  uint32_t* rmp = a.rmant + blk0 * a.rstride;
+  int8_t* rep = a.rexp + blk0;
+  const long long rstep = bpp * a.rstride;
+  const unsigned ring_s = smem_u32(ring), bars_s = smem_u32(bars);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < NBF; ++k) mbar_init(bars + k, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const int tmx = tl.x0 - P - (P & 1), tmy = tl.y0 - P;
+  auto stage = [&](int i, int slot) {  // plane z0 + i of u_L into ring slot `slot` (TMA, thread 0)
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      const unsigned dst = ring_s + (unsigned)(slot * BOX * 8), bar = bars_s + (unsigned)(slot * 8);
+      fence_async_smem();
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(BOX * 8))
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];" ::"r"(dst),
+          "l"((unsigned long long)a.tmb), "r"(tmx), "r"(tmy), "r"(z0 + i - a.zoff), "r"(bar)
+          : "memory");
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < PF; ++i)
+    if (i < nin) stage(i, i);
+  double cr[R], sr[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
+  double ss = 0.0;
+  int tz = ((z0 % P) + P) % P;
+  int isl = 0;
+  unsigned par = 0;
+  for (int i = 0; i < nin; ++i) {
+    const int zi = z0 + i;
+    mbar_wait_s(bars_s + 8u * (unsigned)isl, par);
+    __syncthreads();  // every thread is past iteration i - 1 (slot and XA/XB reuse)
+    if (i + PF < nin) stage(i + PF, isl + PF >= NBF ? isl + PF - NBF : isl + PF);
+    xpass<P>(ring + isl * BOX, C::SH, km, kk, XA, XB, w, lane);
+    __syncthreads();
+    double c, s;
+    ypass<P>(cf, ty, XA, XB, w, lane, c, s);
+#pragma unroll
+    for (int o = 0; o < R - 1; ++o) {
+      cr[o] = cr[o + 1];
+      sr[o] = sr[o + 1];
+    }
+    cr[R - 1] = c;
+    sr[R - 1] = s;
+    if (i >= 2 * P) {
+      const int z = zi - P;
+      const double au = zpass<P>(cf, tz, cr, sr) * hl;
+      if (rowok) {
+        const bool uz = unk1(z, n);
+        const double gz = uz ? gt[z] : 0.0;
+        const double t = (uxy && uz) ? gxy * gz - au : 0.0;  // (((C g(x)) g(y)) g(z)) - A u
+        *Tp = t;
+        ss = fma(t, t, ss);
+        warp_encode(t, a.wr, rmp, rep, lane, a.status);
+      }
+      Tp += tplane;
+      rmp += rstep;
+      rep += bpp;
+    }
+    tz = tz + 1 == P ? 0 : tz + 1;
+    if (++isl == NBF) {
+      isl = 0;
+      par ^= 1u;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+  if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)tl.cta * FW + w] = ss;
+}
+
 // ------------------------------------------------------------------ host --
 template <int P>
 static int smem_res(int wu) {
@@ -1071,6 +1185,11 @@ static int smem_cheb(int J, int wu, bool aux) {
   return (int)(d + wbytes + 8 + 8 * C::NBF + 16);
 }
 
+template <int P>
+static int smem_res_s() {
+  using C = F3<P>;
+  return (int)(((size_t)C::NBF * C::BOX + 2 * C::NR * 32) * 8 + 8 * C::NBF + 16);
+}
 template <int P>
 static int smem_prolong(int wu) {
   using C = F3<P>;
@@ -1092,6 +1211,7 @@ void fine3_set_attributes() {
 #define F(P)                                                                                        \
   cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);        \
   cudaFuncSetAttribute(k_f3_prolong<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);         \
+  cudaFuncSetAttribute(k_f3_residual_s<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
   cudaFuncSetAttribute(k_f3_cfas<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);    \
   cudaFuncSetAttribute(k_f3_cheb<P, 2, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cheb<P, 3, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -1146,9 +1266,17 @@ static void launch_cfas_cheb(int kind, cudaStream_t st, const F3Args& a, const C
   else f3_launch(k_f3_cheb<P, 3, T>, n, smem_cheb<P, T>(3, a.wu, aux), st, a, ct);
 }
 
-// kind: 0 residual, 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3), 3 prolongation;
+// kind: 0 residual (u generated), 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3), 3 prolongation,
+// 4 residual (u staged);
 // `fp32`: FP32 cFas (kinds 1, 2; reading R28)
 void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf, int fp32) {
+  if (kind == 4) {  // residual with u_L staged (materialised form)
+    const CoefT<double> ct = coefs_as<double>(cf);
+    if (p == 1) f3_launch(k_f3_residual_s<1>, a.nitems, smem_res_s<1>(), st, a, ct);
+    else if (p == 2) f3_launch(k_f3_residual_s<2>, a.nitems, smem_res_s<2>(), st, a, ct);
+    else f3_launch(k_f3_residual_s<3>, a.nitems, smem_res_s<3>(), st, a, ct);
+    return;
+  }
   if (kind == 3) {  // P u_{l-1} (step 0) or u_l = dec ú_l + P u_{l-1} (step 1) at the tile points
     const CoefT<double> ct = coefs_as<double>(cf);
     if (p == 1) f3_launch(k_f3_prolong<1>, a.nitems, smem_prolong<1>(a.wu), st, a, ct);
