@@ -56,6 +56,9 @@ def lib():
         L.orc_coarse_inverse.argtypes = [C.c_int, C.c_int, dp]
         L.orc_cheb_coefs.argtypes = [C.c_void_p, dp, dp, dp]
         L.orc_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.orc_create_streamed.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.orc_stream_bytes.argtypes = [C.c_void_p]
+        L.orc_stream_bytes.restype = C.c_int64
         L.orc_destroy.argtypes = [C.c_void_p]
         L.orc_solve.argtypes = [C.c_void_p]
         L.orc_solve_upto.argtypes = [C.c_void_p, C.c_int, C.c_int]
@@ -287,11 +290,14 @@ def vcycle_rho(d, p, levels, s: Schedule, iters=30):
 class CFMG:
     """Oracle compact FMG context (orc_ctx)."""
 
-    def __init__(self, d: int, p: int, levels: int, s: Schedule):
+    def __init__(self, d: int, p: int, levels: int, s: Schedule, streamed: bool = False):
+        """streamed: the plane-streamed mode (Alg 5.3/5.4 at plane granularity,
+        orc_stream.c), bit-identical to the simple mode in linear space."""
         self.d, self.p, self.levels, self.s = d, p, levels, s
         self.Lmax = levels - 1
         h = C.c_void_p()
-        rc = lib().orc_create(d, p, levels, C.byref(s), C.byref(h))
+        create = lib().orc_create_streamed if streamed else lib().orc_create
+        rc = create(d, p, levels, C.byref(s), C.byref(h))
         if rc:
             raise ValueError(f"orc_create failed rc={rc}")
         self.h = h
@@ -328,6 +334,10 @@ class CFMG:
     def cfas_correct(self, L):
         rc = lib().orc_cfas_correct(self.h, L)
         assert rc == 0
+
+    def stream_bytes(self) -> int:
+        """Peak bytes of the streamed mode's plane windows (0 in simple mode)."""
+        return int(lib().orc_stream_bytes(self.h))
 
     def norms(self):
         n = (self.Lmax + 1) * self.s.n_ir * (self.Lmax + 1)

@@ -104,6 +104,13 @@ void orc_cheb_coefs(const orc_schedule* s, double* inv_theta, double* alpha, dou
 /* ---- compact FMG (orc_cfmg.c) ---- */
 typedef struct orc_ctx orc_ctx;
 int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out);
+/* Plane-streamed mode (orc_stream.c; Alg 5.3/5.4 PAPER.md:999-1157 at plane
+ * granularity): the same sections and norms as orc_create's simple mode, bit
+ * for bit, with O(planes) FP64 temporaries instead of full-size arrays.
+ * Chebyshev smoother, nu = 1, FP64 cFas; orc_get_array (l > 0),
+ * orc_decode_solution and orc_smooth return ORC_EINVAL on such a context. */
+int orc_create_streamed(int d, int p, int levels, const orc_schedule* s, orc_ctx** out);
+int64_t orc_stream_bytes(const orc_ctx* c);   /* peak bytes of its plane windows */
 void orc_destroy(orc_ctx* c);
 int orc_solve(orc_ctx* c);                         /* Alg 3.3 from scratch */
 int orc_smooth(orc_ctx* c, int l, const double* b, double* y); /* cFas smoother from y = 0 */

@@ -28,34 +28,10 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
-#include "oracle.h"
+#include "orc_internal.h"
 
-typedef struct {
-  int w;          /* current stored width */
-  int64_t* m;     /* mantissas, one per stored entry */
-  int8_t* E;      /* one exponent per 32-entry block */
-} sec_t;
-
-struct orc_ctx {
-  int d, p, levels, Lmax;
-  orc_schedule s;
-  orc_level g[ORC_MAXLEV];
-  sec_t u[ORC_MAXLEV];    /* compact solution sections ú_l */
-  sec_t r[ORC_MAXLEV];    /* residual sections r_l */
-  sec_t y[ORC_MAXLEV];    /* correction sections ý_l */
-  double* f[ORC_MAXLEV];  /* f_l (only the current FMG level is used) */
-  double* invD[ORC_MAXLEV];
-  double* ut[ORC_MAXLEV]; /* decoded standard representation temporaries u_l */
-  double* tt[ORC_MAXLEV]; /* residual temporaries t_l */
-  double* wt[ORC_MAXLEV]; /* w_l = z_l + dec ý_l */
-  double* Ainv;
-  int n0;
-  double inv_theta, cal[8], cbe[8];
-  double* norms;          /* [Lmax+1][N][Lmax+1] */
-};
-
-static int wu(const orc_ctx* c, int l, int L) { return c->s.b_u + c->s.k_u * (L - l); }
-static int wr(const orc_ctx* c, int l, int L) { return c->s.b_r + c->s.k_r * (L - l); }
+int orc_wu(const orc_ctx* c, int l, int L) { return c->s.b_u + c->s.k_u * (L - l); }
+int orc_wr(const orc_ctx* c, int l, int L) { return c->s.b_r + c->s.k_r * (L - l); }
 
 static int sec_alloc(sec_t* s, const orc_level* g) {
   s->m = calloc(g->size, sizeof(int64_t));
@@ -73,7 +49,7 @@ static void sec_zero(sec_t* s, const orc_level* g, int w) {
 }
 
 /* x = dec(section) (mantissa scaled by the block exponent) */
-static void sec_decode(const sec_t* s, const orc_level* g, double* x) {
+void orc_sec_decode(const sec_t* s, const orc_level* g, double* x) {
 #pragma omp parallel for schedule(static)
   for (int64_t b = 0; b < g->nblk; ++b)
     for (int j = 0; j < 32; ++j)
@@ -81,7 +57,7 @@ static void sec_decode(const sec_t* s, const orc_level* g, double* x) {
 }
 
 /* section = enc_w(x): RNE per block (reading R8) */
-static int sec_encode(sec_t* s, const orc_level* g, const double* x, int w) {
+int orc_sec_encode(sec_t* s, const orc_level* g, const double* x, int w) {
   s->w = w;
   int err = ORC_OK;
 #pragma omp parallel for schedule(static) reduction(max : err)
@@ -107,17 +83,20 @@ void orc_destroy(orc_ctx* c) {
   free(c);
 }
 
-int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out) {
+static int create(int d, int p, int levels, const orc_schedule* s, int streamed, orc_ctx** out) {
   if (s && s->cfas_fp32 && (s->smoother != 0 || s->nu > 1)) return ORC_EINVAL;  /* (reading R28: Chebyshev, nu = 1) */
   *out = NULL;
   if ((d != 2 && d != 3) || p < 1 || p > 3 || levels < 1 || levels > ORC_MAXLEV) return ORC_EINVAL;
   if (s->b_u < 2 || s->b_r < 2 || s->n_ir < 1 || s->cheb_degree < 1 || s->cheb_degree > 8) return ORC_EINVAL;
   if (s->smoother < 0 || s->smoother > 2) return ORC_EINVAL;
+  /* plane-streamed mode (orc_stream.c): Chebyshev, nu = 1, FP64 cFas */
+  if (streamed && (s->smoother != 0 || s->nu > 1 || s->cfas_fp32)) return ORC_EINVAL;
   int Lmax = levels - 1;
   if (s->b_u + s->k_u * Lmax > 54 || s->b_r + s->k_r * Lmax > 54) return ORC_EINVAL;
   orc_ctx* c = calloc(1, sizeof(orc_ctx));
   if (!c) return ORC_ENOMEM;
   c->d = d; c->p = p; c->levels = levels; c->Lmax = Lmax; c->s = *s;
+  c->streamed = streamed;
   for (int l = 0; l <= Lmax; ++l) {
     orc_level_geom(d, p, l, &c->g[l]);
     const orc_level* g = &c->g[l];
@@ -125,6 +104,7 @@ int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out) {
       orc_destroy(c);
       return ORC_ENOMEM;
     }
+    if (streamed && l > 0) continue;   /* no full-size FP64 temporaries above level 0 */
     c->f[l] = malloc(sizeof(double) * g->size);
     c->invD[l] = malloc(sizeof(double) * g->size);
     c->ut[l] = calloc(g->size, sizeof(double));
@@ -146,9 +126,21 @@ int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out) {
   return ORC_OK;
 }
 
+int orc_create(int d, int p, int levels, const orc_schedule* s, orc_ctx** out) {
+  return create(d, p, levels, s, 0, out);
+}
+
+/* The plane-streamed mode (Alg 5.3/5.4 at plane granularity, orc_stream.c):
+ * same results, bit for bit, in linear space. */
+int orc_create_streamed(int d, int p, int levels, const orc_schedule* s, orc_ctx** out) {
+  return create(d, p, levels, s, 1, out);
+}
+
+int64_t orc_stream_bytes(const orc_ctx* c) { return c->stream_bytes; }
+
 /* y = A_0^{-1} x on level 0 (full stored layout in and out); canonical mat-vec
  * acc = 0; acc = fma(Ainv[I][J], x_J, acc) over J in unknown order. */
-static void coarse_solve(const orc_ctx* c, const double* x, double* y) {
+void orc_coarse_solve(const orc_ctx* c, const double* x, double* y) {
   const orc_level* g = &c->g[0];
   int m = 2 * c->p - 1, n0 = c->n0;
   double xv[125];
@@ -168,13 +160,15 @@ static void coarse_solve(const orc_ctx* c, const double* x, double* y) {
 /* Alg 3.2 fmgResidual at FMG level L; norms[l] = ||t_l||_2. */
 int orc_residual(orc_ctx* c, int L, double* norms) {
   int d = c->d, p = c->p;
+  if (L < 0 || L > c->Lmax) return ORC_EINVAL;
+  if (c->streamed) return orc_stream_residual(c, L, norms);
   /* decode sweep PAPER.md:733-735: u_0 = ú_0; u_l = ú_l + P_l u_{l-1} */
-  sec_decode(&c->u[0], &c->g[0], c->ut[0]);
+  orc_sec_decode(&c->u[0], &c->g[0], c->ut[0]);
   for (int l = 1; l <= L; ++l) {
     const orc_level* g = &c->g[l];
     double* pu = malloc(sizeof(double) * g->size);
     orc_prolong(d, p, l, c->ut[l - 1], pu);
-    sec_decode(&c->u[l], g, c->ut[l]);
+    orc_sec_decode(&c->u[l], g, c->ut[l]);
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < g->size; ++i) c->ut[l][i] = c->ut[l][i] + pu[i];
     free(pu);
@@ -189,12 +183,12 @@ int orc_residual(orc_ctx* c, int L, double* norms) {
     free(au);
   }
   /* truncate PAPER.md:739 */
-  int rc = sec_encode(&c->r[L], &c->g[L], c->tt[L], wr(c, L, L));
+  int rc = orc_sec_encode(&c->r[L], &c->g[L], c->tt[L], orc_wr(c, L, L));
   if (rc) return rc;
   /* restriction sweep PAPER.md:742-744 (restricts t, not r; R11) */
   for (int l = L - 1; l >= 0; --l) {
     orc_restrict(d, p, l + 1, c->tt[l + 1], c->tt[l]);
-    rc = sec_encode(&c->r[l], &c->g[l], c->tt[l], wr(c, l, L));
+    rc = orc_sec_encode(&c->r[l], &c->g[l], c->tt[l], orc_wr(c, l, L));
     if (rc) return rc;
   }
   if (norms)
@@ -324,7 +318,7 @@ static void lex_gauss_seidel(const orc_ctx* c, int l, const double* b, double* y
 
 /* The cFas smoother of the schedule on level l from y = 0 (test access). */
 int orc_smooth(orc_ctx* c, int l, const double* b, double* y) {
-  if (l < 1 || l > c->Lmax) return ORC_EINVAL;
+  if (l < 1 || l > c->Lmax || c->streamed) return ORC_EINVAL;
   if (c->s.smoother == 1) mc_gauss_seidel(c, l, b, y);
   else if (c->s.smoother == 2) lex_gauss_seidel(c, l, b, y);
   else chebyshev(c, l, b, y);
@@ -363,7 +357,7 @@ static int cfas_cycle(orc_ctx* c, int L, int guess) {
       const orc_level* gf = &c->g[l + 1];
       double* yv = malloc(sizeof(double) * gf->size);
       double* q = malloc(sizeof(double) * gf->size);
-      sec_decode(&c->y[l + 1], gf, yv);
+      orc_sec_decode(&c->y[l + 1], gf, yv);
       orc_apply_A(d, p, l + 1, yv, q);
       for (int64_t i = 0; i < gf->size; ++i) q[i] = q[i] + sv[l + 1][i];  /* A ý + s */
       orc_restrict(d, p, l + 1, q, sv[l]);
@@ -375,22 +369,22 @@ static int cfas_cycle(orc_ctx* c, int L, int guess) {
     const orc_level* g = &c->g[0];
     double* r0 = malloc(sizeof(double) * g->size);
     double* y0 = malloc(sizeof(double) * g->size);
-    sec_decode(&c->r[0], g, r0);
+    orc_sec_decode(&c->r[0], g, r0);
     if (guess) {
       double* yo = malloc(sizeof(double) * g->size);
       double* ay = malloc(sizeof(double) * g->size);
-      sec_decode(&c->y[0], g, yo);
+      orc_sec_decode(&c->y[0], g, yo);
       orc_apply_A(d, p, 0, yo, ay);
       for (int64_t i = 0; i < g->size; ++i) r0[i] = (r0[i] - sv[0][i]) - ay[i];
-      coarse_solve(c, r0, y0);
+      orc_coarse_solve(c, r0, y0);
       for (int64_t i = 0; i < g->size; ++i) y0[i] = yo[i] + y0[i];
       free(yo); free(ay);
     } else {
-      coarse_solve(c, r0, y0);
+      orc_coarse_solve(c, r0, y0);
     }
-    rc = sec_encode(&c->y[0], g, y0, wr(c, 0, L));
+    rc = orc_sec_encode(&c->y[0], g, y0, orc_wr(c, 0, L));
     free(r0); free(y0);
-    if (!rc) sec_decode(&c->y[0], g, c->wt[0]);   /* w_0 = z_0 + ý_0, z_0 = 0 */
+    if (!rc) orc_sec_decode(&c->y[0], g, c->wt[0]);   /* w_0 = z_0 + ý_0, z_0 = 0 */
   }
   /* coarse-to-fine sweep PAPER.md:641-643; FP32 cFas (reading R28): the same
    * steps in float, w_l kept as the double of a float */
@@ -409,13 +403,13 @@ static int cfas_cycle(orc_ctx* c, int L, int guess) {
     for (int64_t i = 0; i < gc->size; ++i) wc[i] = (float)c->wt[l - 1][i];   /* (exact: a float) */
     orc_prolong_f32(d, p, l, wc, z);                  /* z_l = P_l w_{l-1} */
     orc_apply_A_f32(d, p, l, z, az);
-    sec_decode(&c->r[l], g, rv);
+    orc_sec_decode(&c->r[l], g, rv);
     for (int64_t i = 0; i < N; ++i) rb[i] = (float)rv[i] - az[i];    /* b = r_l - A_l z_l */
     chebyshev_f32(c, l, rb, yf);
     for (int64_t i = 0; i < N; ++i) yv[i] = (double)yf[i];
-    rc = sec_encode(&c->y[l], g, yv, wr(c, l, L));
+    rc = orc_sec_encode(&c->y[l], g, yv, orc_wr(c, l, L));
     if (!rc) {
-      sec_decode(&c->y[l], g, yv);
+      orc_sec_decode(&c->y[l], g, yv);
       for (int64_t i = 0; i < N; ++i) c->wt[l][i] = (double)(z[i] + (float)yv[i]);
     }
     free(wc); free(z); free(az); free(rb); free(yf); free(rv); free(yv);
@@ -429,12 +423,12 @@ static int cfas_cycle(orc_ctx* c, int L, int guess) {
     double* yv = malloc(sizeof(double) * N);
     orc_prolong(d, p, l, c->wt[l - 1], z);          /* z_l = P_l (ý_{l-1} + z_{l-1}) */
     orc_apply_A(d, p, l, z, az);
-    sec_decode(&c->r[l], g, rb);
+    orc_sec_decode(&c->r[l], g, rb);
     if (guess) {
       /* A_l z_l + A_l ý_l = A_l (z_l + ý_l): one operator application (R23) */
       double* yo = malloc(sizeof(double) * N);
       double* zy = malloc(sizeof(double) * N);
-      sec_decode(&c->y[l], g, yo);
+      orc_sec_decode(&c->y[l], g, yo);
       for (int64_t i = 0; i < N; ++i) zy[i] = z[i] + yo[i];
       orc_apply_A(d, p, l, zy, az);
       for (int64_t i = 0; i < N; ++i) rb[i] = (rb[i] - sv[l][i]) - az[i];
@@ -445,9 +439,9 @@ static int cfas_cycle(orc_ctx* c, int L, int guess) {
       for (int64_t i = 0; i < N; ++i) rb[i] = rb[i] - az[i];  /* b = r_l - A_l z_l */
       smooth0(c, l, rb, yv);                                   /* smooth from ý_l = 0 */
     }
-    rc = sec_encode(&c->y[l], g, yv, wr(c, l, L));   /* fix: store at w_r(l,L) */
+    rc = orc_sec_encode(&c->y[l], g, yv, orc_wr(c, l, L));   /* fix: store at w_r(l,L) */
     if (!rc) {
-      sec_decode(&c->y[l], g, yv);
+      orc_sec_decode(&c->y[l], g, yv);
       for (int64_t i = 0; i < N; ++i) c->wt[l][i] = z[i] + yv[i];
     }
     free(z); free(az); free(rb); free(yv);
@@ -463,6 +457,11 @@ static int cfas_cycle(orc_ctx* c, int L, int guess) {
  * correction PAPER.md:798. */
 int orc_cfas_correct(orc_ctx* c, int L) {
   int rc;
+  if (L < 0 || L > c->Lmax) return ORC_EINVAL;
+  if (c->streamed) {
+    rc = orc_stream_cfas(c, L);
+    return rc ? rc : orc_stream_correct(c, L);
+  }
   const int nu = c->s.nu > 1 ? c->s.nu : 1;
   for (int cyc = 0; cyc < nu; ++cyc) {
     rc = cfas_cycle(c, L, cyc > 0);
@@ -473,10 +472,10 @@ int orc_cfas_correct(orc_ctx* c, int L) {
     const orc_level* g = &c->g[l];
     double* a = malloc(sizeof(double) * g->size);
     double* b = malloc(sizeof(double) * g->size);
-    sec_decode(&c->u[l], g, a);
-    sec_decode(&c->y[l], g, b);
+    orc_sec_decode(&c->u[l], g, a);
+    orc_sec_decode(&c->y[l], g, b);
     for (int64_t i = 0; i < g->size; ++i) a[i] = a[i] + b[i];
-    rc = sec_encode(&c->u[l], g, a, wu(c, l, L));
+    rc = orc_sec_encode(&c->u[l], g, a, orc_wu(c, l, L));
     free(a); free(b);
     if (rc) return rc;
   }
@@ -497,8 +496,8 @@ int orc_solve_upto(orc_ctx* c, int Lstop, int iters_last) {
   {
     const orc_level* g = &c->g[0];
     double* y0 = malloc(sizeof(double) * g->size);
-    coarse_solve(c, c->f[0], y0);
-    rc = sec_encode(&c->u[0], g, y0, wu(c, 0, 0));
+    orc_coarse_solve(c, c->f[0], y0);
+    rc = orc_sec_encode(&c->u[0], g, y0, orc_wu(c, 0, 0));
     free(y0);
     if (rc) return rc;
   }
@@ -506,7 +505,7 @@ int orc_solve_upto(orc_ctx* c, int Lstop, int iters_last) {
     /* push level PAPER.md:788: ú_L = 0; the widening of ú_{0..L-1} by k_u bits is
      * exact (m <- m 2^k_u with the same exponent), so sections keep
      * their mantissas until the next correction re-encodes them at w_u(l, L). */
-    sec_zero(&c->u[L], &c->g[L], wu(c, L, L));
+    sec_zero(&c->u[L], &c->g[L], orc_wu(c, L, L));
     for (int l = 0; l < L; ++l) {
       const orc_level* g = &c->g[l];
       int k = c->s.k_u;
@@ -546,12 +545,12 @@ int orc_get_section(orc_ctx* c, int which, int l, uint32_t* mant, int8_t* exps, 
 int orc_set_section(orc_ctx* c, int which, int l, const double* x, int width) {
   if (l < 0 || l > c->Lmax || which < 0 || which > 2) return ORC_EINVAL;
   sec_t* s = which == 0 ? &c->u[l] : which == 1 ? &c->r[l] : &c->y[l];
-  return sec_encode(s, &c->g[l], x, width);
+  return orc_sec_encode(s, &c->g[l], x, width);
 }
 
 /* which: 0 = u_l (decoded, from the last residual), 1 = t_l, 2 = w_l. */
 int orc_get_array(orc_ctx* c, int which, int l, double* dst) {
-  if (l < 0 || l > c->Lmax) return ORC_EINVAL;
+  if (l < 0 || l > c->Lmax || (c->streamed && l > 0)) return ORC_EINVAL;
   const double* s = which == 0 ? c->ut[l] : which == 1 ? c->tt[l] : c->wt[l];
   memcpy(dst, s, sizeof(double) * c->g[l].size);
   return ORC_OK;
@@ -560,12 +559,13 @@ int orc_get_array(orc_ctx* c, int which, int l, double* dst) {
 /* û_L = ú_L + P_L(ú_{L-1} + ... ) (eq:compact-to-standard PAPER.md:186). */
 int orc_decode_solution(orc_ctx* c, int L, double* uhat) {
   if (L < 0 || L > c->Lmax) return ORC_EINVAL;
-  sec_decode(&c->u[0], &c->g[0], c->ut[0]);
+  if (c->streamed) return ORC_EINVAL;   /* (the full û is not a streamed-mode output) */
+  orc_sec_decode(&c->u[0], &c->g[0], c->ut[0]);
   for (int l = 1; l <= L; ++l) {
     const orc_level* g = &c->g[l];
     double* pu = malloc(sizeof(double) * g->size);
     orc_prolong(c->d, c->p, l, c->ut[l - 1], pu);
-    sec_decode(&c->u[l], g, c->ut[l]);
+    orc_sec_decode(&c->u[l], g, c->ut[l]);
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < g->size; ++i) c->ut[l][i] = c->ut[l][i] + pu[i];
     free(pu);

@@ -19,7 +19,7 @@
 #include <quadmath.h>
 #include <stdlib.h>
 #include <string.h>
-#include "oracle.h"
+#include "orc_internal.h"
 
 void orc_level_geom(int d, int p, int l, orc_level* g) {
   g->n = p << (l + 1);
@@ -181,6 +181,11 @@ static void mask_unknowns(int d, dims_t g, double* v) {
         int ok = (x >= 1 && x < g.n[0] && y >= 1 && y < g.n[1] && (d == 2 || z >= 1));
         if (!ok) v[((int64_t)z * g.n[1] + y) * g.sx + x] = 0.0;
       }
+}
+
+void orc_pass1d(int p, int kind, const double* C, int axis, const double* in, const int nin[3],
+                double* out, const int nout[3]) {
+  pass1d(p, kind, C, axis, in, mkdims(nin[0], nin[1], nin[2]), out, mkdims(nout[0], nout[1], nout[2]));
 }
 
 /* A_l u, A_l = h^(d-2) Â, Â = Kz My Mx + Mz Ky Mx + Mz My Kx:
@@ -464,24 +469,32 @@ void orc_rhs_table(int p, int l, double* g) {
 double orc_rhs_const(int d) { return (double)((__float128)d * M_PIq * M_PIq); }
 
 /* f_l at node (i,j,k) = ((C_d g(i)) g(j)) g(k), C_d = RN(d pi^2);
- * 0 at non-unknowns. */
+ * 0 at non-unknowns.  orc_rhs_plane: plane z of the last axis (3D z, 2D y). */
+void orc_rhs_plane(int d, int p, int l, const double* g, int z, double* f) {
+  orc_level G;
+  orc_level_geom(d, p, l, &G);
+  double C = orc_rhs_const(d);
+  int ny = d == 3 ? G.NY : 1;
+  for (int yy = 0; yy < ny; ++yy)
+    for (int x = 0; x < G.NX; ++x) {
+      int y = d == 3 ? yy : z;
+      int64_t idx = (int64_t)yy * G.NX + x;
+      int ok = (x >= 1 && x < G.n && y >= 1 && (d == 2 || z >= 1));
+      if (!ok) { f[idx] = 0.0; continue; }
+      double v = C * g[x];
+      v = v * g[y];
+      if (d == 3) v = v * g[z];
+      f[idx] = v;
+    }
+}
+
 void orc_rhs(int d, int p, int l, double* f) {
   orc_level G;
   orc_level_geom(d, p, l, &G);
   double* g = malloc(sizeof(double) * G.n);
   orc_rhs_table(p, l, g);
-  double C = orc_rhs_const(d);
-  for (int z = 0; z < G.NZ; ++z)
-    for (int y = 0; y < G.NY; ++y)
-      for (int x = 0; x < G.NX; ++x) {
-        int64_t idx = ((int64_t)z * G.NY + y) * G.NX + x;
-        int ok = (x >= 1 && x < G.n && y >= 1 && (d == 2 || z >= 1));
-        if (!ok) { f[idx] = 0.0; continue; }
-        double v = C * g[x];
-        v = v * g[y];
-        if (d == 3) v = v * g[z];
-        f[idx] = v;
-      }
+  int64_t ps = (int64_t)G.NX * (d == 3 ? G.NY : 1);
+  for (int z = 0; z < G.n; ++z) orc_rhs_plane(d, p, l, g, z, f + z * ps);
   free(g);
 }
 
@@ -508,20 +521,30 @@ void orc_inv_diag_ref(int d, int p, double* invd) {
       }
 }
 
-/* invD of A_l = h^(d-2) Â: invD_ref * 2^((l+1)(d-2)), 0 at non-unknowns. */
+/* invD of A_l = h^(d-2) Â: invD_ref * 2^((l+1)(d-2)), 0 at non-unknowns.
+ * orc_inv_diag_plane: plane z of the last axis (3D z, 2D y); ref from
+ * orc_inv_diag_ref. */
+void orc_inv_diag_plane(int d, int p, int l, const double* ref, int z, double* invD) {
+  orc_level G;
+  orc_level_geom(d, p, l, &G);
+  double sc = ldexp(1.0, (l + 1) * (d - 2));
+  int ny = d == 3 ? G.NY : 1;
+  for (int yy = 0; yy < ny; ++yy)
+    for (int x = 0; x < G.NX; ++x) {
+      int y = d == 3 ? yy : z;
+      int64_t idx = (int64_t)yy * G.NX + x;
+      int ok = (x >= 1 && x < G.n && y >= 1 && (d == 2 || z >= 1));
+      invD[idx] = ok ? ref[((d == 3 ? z % p : 0) * p + y % p) * p + x % p] * sc : 0.0;
+    }
+}
+
 void orc_inv_diag(int d, int p, int l, double* invD) {
   orc_level G;
   orc_level_geom(d, p, l, &G);
   double ref[27];
   orc_inv_diag_ref(d, p, ref);
-  double sc = ldexp(1.0, (l + 1) * (d - 2));
-  for (int z = 0; z < G.NZ; ++z)
-    for (int y = 0; y < G.NY; ++y)
-      for (int x = 0; x < G.NX; ++x) {
-        int64_t idx = ((int64_t)z * G.NY + y) * G.NX + x;
-        int ok = (x >= 1 && x < G.n && y >= 1 && (d == 2 || z >= 1));
-        invD[idx] = ok ? ref[((d == 3 ? z % p : 0) * p + y % p) * p + x % p] * sc : 0.0;
-      }
+  int64_t ps = (int64_t)G.NX * (d == 3 ? G.NY : 1);
+  for (int z = 0; z < G.n; ++z) orc_inv_diag_plane(d, p, l, ref, z, invD + z * ps);
 }
 
 /* ----------------------------------------------------------- coarse grid -- */
