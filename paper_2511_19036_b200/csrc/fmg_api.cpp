@@ -91,6 +91,7 @@ struct fmg_ctx {
   // too (the residual stages u_L instead of generating it).
   // FMG_F3MAT=0/1 forces the choice.
   bool f3mat = false;
+  bool tpb = false;  // thread-per-block epilogues of the finest-level kernels (k_f3_tpb; needs f3mat's memory)
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
@@ -695,6 +696,11 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.zout = o.zout;
   a.wout = o.wout;
   a.uout = o.uout;
+  // (levels of >= 2^16 blocks: below that the extra launch costs more than the
+  // warp-cooperative codec it replaces)
+  a.tpb = c->tpb && (it.f3kind == 2 || it.f3kind == 4) && a.wu <= 32 && a.wu_out <= 32 && a.wr <= 32 &&
+          (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= (1LL << 16);
+  a.Yb = sview(c, 2, l);
   a.zoff = c->wlo[l];
   a.czoff = l >= 1 ? c->wlo[l - 1] : 0;
   a.pbase = c->pbase;
@@ -1228,6 +1234,12 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     for (int l = 0; l <= Lmax; ++l)
       need += 8.0 * (double)c->g[l].NX * c->g[l].NY * (c->whi[l] - c->wlo[l]) * (l == Lmax ? 5.0 : 3.0);
     c->f3mat = e ? atoi(e) != 0 : need < 0.5 * (double)totalb;
+    // thread-per-block epilogues (fmg_fine3.cu k_f3_tpb): one more finest-size
+    // array (y_k of the last Chebyshev step), with the materialised form;
+    // measured faster (profiles/r2_summary.md).  FMG_TPB=0 disables.
+    const char* et = getenv("FMG_TPB");
+    const double ytop = 8.0 * (double)c->g[Lmax].NX * c->g[Lmax].NY * (c->whi[Lmax] - c->wlo[Lmax]);
+    c->tpb = c->f3mat && (et ? atoi(et) != 0 : (e != nullptr || need + ytop < 0.5 * (double)totalb));
   }
   for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
     const long long plane = (long long)c->g[l].NX * c->g[l].NY, off = plane * c->wlo[l];
@@ -1254,6 +1266,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       size_t n = i == 4 ? (dv ? win(Lmax) : 2) : ((i >= 1 && i <= 3) && c->fine3 ? 2 : scratch);
       if (i == 1 && c->fine3) n = win(0);  // (level 0's bracket b_0: cFas1 + k_coarse_nu)
       if (i == 5 && c->f3mat) n = win(Lmax);  // (P u_{L-1} at the finest level)
+      if (i == 2 && c->tpb) n = win(Lmax);    // (y_k of the last Chebyshev step, k_f3_tpb)
       const size_t bytes = sizeof(double) * n;
       c->buf[i] = (double*)dalloc(c, bytes);
       c->sbase[i] = c->buf[i];

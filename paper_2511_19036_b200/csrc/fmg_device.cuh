@@ -309,6 +309,34 @@ __device__ __forceinline__ void tpb_pack(const double* row, int E, int w, uint32
   }
 }
 
+// Quantise one block in place with exponent E (E = -128: zeros): row[e] =
+// m 2^(E-q), the value warp_encode returns, without packing.
+__device__ __forceinline__ void tpb_quant(double* row, int E, int w) {
+  const int q = w - 1;
+  const double s = E == -128 ? 0.0 : pow2(q - E);
+  const double sb = E == -128 ? 0.0 : pow2(E - q);
+#pragma unroll 8
+  for (int e = 0; e < 32; ++e) row[e] = i2d(rne_int(row[e] * s, w), w) * sb;
+}
+
+// row[e] = dec(entry e) + row[e] (the unpack of tpb_unpack, added in place).
+__device__ __forceinline__ void tpb_unpack_add(const uint32_t* wrow, int E, int w, double* row) {
+  const double sb = E == -128 ? 0.0 : pow2(E - (w - 1));
+  unsigned long long acc = 0ULL;
+  int nb = 0, k = 0;
+#pragma unroll 4
+  for (int e = 0; e < 32; ++e) {
+    if (nb < w) {
+      acc |= (unsigned long long)wrow[k++] << nb;
+      nb += 32;
+    }
+    const long long m = (long long)(acc << (64 - w)) >> (64 - w);
+    acc >>= w;
+    nb -= w;
+    row[e] = i2d(m, w) * sb + row[e];
+  }
+}
+
 // Unpack and scale one block into row[0..32).
 __device__ __forceinline__ void tpb_unpack(const uint32_t* wrow, int E, int w, double* row) {
   const double sb = E == -128 ? 0.0 : pow2(E - (w - 1));

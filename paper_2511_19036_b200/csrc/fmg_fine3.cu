@@ -43,6 +43,15 @@
 #ifndef F3_MINB
 #define F3_MINB(P) ((P) == 3 ? 2 : ((P) == 1 ? 4 : 3))
 #endif
+#ifndef F3_MINB_CF
+#define F3_MINB_CF(P) F3_MINB(P)  // k_f3_cfas
+#endif
+#ifndef F3_MINB_CH
+#define F3_MINB_CH(P, J) F3_MINB(P)  // k_f3_cheb
+#endif
+#ifndef F3_MINB_RS
+#define F3_MINB_RS(P) F3_MINB(P)  // k_f3_residual_s
+#endif
 
 namespace fmg {
 
@@ -596,7 +605,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual(const __gri
 // b_L = dec r_L - A_L z_L with z_L = P w_{L-1} generated on chip -> B (the
 // t_L buffer).  Chebyshev step 1 (cFas1 of fmg_march3.cu).
 template <int P, class T>
-__global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_constant__ F3Args a,
+__global__ void __launch_bounds__(32 * FW, F3_MINB_CF(P)) k_f3_cfas(const __grid_constant__ F3Args a,
                                                           const __grid_constant__ CoefT<T> cf) {
   using C = F3<P>;
   constexpr int R = C::R, NW = C::NW, PF = C::PF;
@@ -704,8 +713,11 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cfas(const __grid_co
 // (invD b), y_2 = y_1 + d_2), A y_{j-1}, then q = b - A y, d_j = fma(al_j,
 // d_{j-1}, be_j (invD q)), y_j = y_{j-1} + d_j.  A step below k stores d_j;
 // the last one encodes ý_L and applies the correction.
-template <int P, int J, class T>
-__global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_constant__ F3Args a,
+// FIN (the last step with the thread-per-block finalisation):
+// y_k goes to a.Dv (the host points it at the Y buffer) as FP64, and
+// k_f3_tpb<1> then encodes ý, updates ú and writes w_l, u_l.
+template <int P, int J, class T, bool FIN>
+__global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __grid_constant__ F3Args a,
                                                           const __grid_constant__ CoefT<T> cf) {
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX, NBF = C::NBF, NW = C::NW, PF = C::PF;
@@ -717,7 +729,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
   T* XB = XA + NR * 32;
   T* ivd = XB + NR * 32;                     // invD factors: P node types x box
   double* aring = (double*)(ivd + P * BOX);  // NW x 2 x NT: z_l, P u_{l-1} at the output points (last step)
-  const bool aux = a.last && (a.wout || a.uout);
+  const bool aux = !FIN && a.last && (a.wout || a.uout);
   uint32_t* wring = (uint32_t*)(aring + (aux ? NW * 2 * 32 * FW : 0));  // NW x FW x (w + 1) (last step: ú words)
   const int RW = a.wu + 1;
   unsigned long long* bars = (unsigned long long*)(wring + NW * FW * RW + 2);
@@ -763,8 +775,8 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
   }
   const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
   int eoff = 0;
-  const WStream ws = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, y, tl.zs, w * RW, rowok && a.last, lane,
-                              eoff);
+  const WStream ws = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, y, tl.zs, w * RW, rowok && a.last && !FIN,
+                              lane, eoff);
   const long long tplane = (long long)g.NY * g.NX;
   const long long bpp = (long long)g.NY * (g.NX >> 5);
   double* Dp = a.Dv + ((long long)tl.zs * g.NY + y) * g.NX + x;
@@ -901,7 +913,9 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_cheb(const __grid_co
       const T qq = b - ay;
       const T d = fma(al, dprev, be * (f * qq));
       const T yv = yprev + d;
-      if (a.last) {
+      if (FIN) {
+        if (rowok) *Dp = (double)yv;  // y_k -> Y (k_f3_tpb<1> finalises)
+      } else if (a.last) {
         const double yq = warp_encode((double)yv, a.wr, nullptr, nullptr, lane, a.status);
         if (rowok) {
           const double* ax = aring + osl * 2 * 32 * FW + tid;
@@ -1056,8 +1070,9 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
 // DESIGN.md §4.3); r_L = enc(t_L); t_L -> HBM; ||t_L||^2 partial per warp.
 // The skeleton of k_f3_cheb (specialised y / z passes, incremental slots)
 // around the old k_m3_residual's arithmetic.
-template <int P>
-__global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual_s(const __grid_constant__ F3Args a,
+// ENC = false: r_L is encoded afterwards from t_L by k_f3_tpb<0> (thread per block).
+template <int P, bool ENC>
+__global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const __grid_constant__ F3Args a,
                                                                          const __grid_constant__ CoefT<double> cf) {
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, BOX = C::BOX, NBF = C::NBF, PF = C::PF;
@@ -1149,7 +1164,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual_s(const __g
         const double t = (uxy && uz) ? gxy * gz - au : 0.0;  // (((C g(x)) g(y)) g(z)) - A u
         *Tp = t;
         ss = fma(t, t, ss);
-        warp_encode(t, a.wr, rmp, rep, lane, a.status);
+        if (ENC) warp_encode(t, a.wr, rmp, rep, lane, a.status);
       }
       Tp += tplane;
       rmp += rstep;
@@ -1164,6 +1179,108 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual_s(const __g
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
   if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)tl.cta * FW + w] = ss;
+}
+
+// Thread-per-block epilogues: the BFP codec of the
+// finest-level kernels' outputs moved out of the plane march, where the
+// warp-cooperative codec (a block is one 32-point row) cost ~40 % of the last
+// Chebyshev step's instructions.  A warp takes 32 consecutive blocks of the
+// rank's planes [zlo, zhi): their doubles arrive by cp.async into a padded
+// tile, one lane per block runs the codec (fmg_device.cuh tpb_*, the same
+// arithmetic as warp_encode / warp_decode: reading R8), and the results leave
+// through coalesced copies.
+//   MODE 0: r_l = enc_{w_r}(t_l)                       (after k_f3_residual_s<P, false>)
+//   MODE 1: ý = enc_{w_r}(y_k) (values only), ú_l <- enc_{w_u'}(dec ú_l + ý),
+//           w_l = z_l + ý (wout), u_l = ú_l + P u_{l-1} (uout)   (after k_f3_cheb<..., FIN>)
+// Widths <= 32 (tpb_*).  T: the cFas arithmetic of w_l (FP32 cFas, R28).
+constexpr int TP_WARPS = 4, TP_RS = 33, TP_WS = 33;
+constexpr int tpb_smem_bytes() { return TP_WARPS * (32 * TP_RS * 8 + 32 * TP_WS * 4); }
+
+template <int MODE, class T>
+__global__ void __launch_bounds__(TP_WARPS * 32) k_f3_tpb(const __grid_constant__ F3Args a) {
+  extern __shared__ __align__(16) double tsm[];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  double* A = tsm + wp * 32 * TP_RS;  // t_l (MODE 0) / y_k -> ý -> dec ú_l + ý -> the new ú_l (MODE 1)
+  uint32_t* wt = (uint32_t*)(tsm + TP_WARPS * 32 * TP_RS) + wp * 32 * TP_WS;
+  const Geom g = a.g;
+  const long long bpp = (long long)g.NY * (g.NX >> 5);
+  const long long bfirst = (long long)a.zlo * bpp, nblk = (long long)(a.zhi - a.zlo) * bpp;
+  const long long ntile = (nblk + 31) / 32;
+  const long long wg = (long long)blockIdx.x * TP_WARPS + wp, nw = (long long)gridDim.x * TP_WARPS;
+  const double* X = MODE == 1 ? a.Dv : a.T;
+  const int wi = MODE == 1 ? a.wu : 0, wo = MODE == 1 ? a.wu_out : a.wr;
+  uint32_t* mant = MODE == 1 ? a.umant : a.rmant;
+  int8_t* exps = MODE == 1 ? a.uexp : a.rexp;
+  const int stride = MODE == 1 ? a.ustride : a.rstride;
+  const unsigned mi = (unsigned)((0x100000000ULL + wi - 1) / (wi > 0 ? wi : 1));  // t / w for t < 2^16
+  const unsigned mo = (unsigned)((0x100000000ULL + wo - 1) / wo);
+  const double* __restrict__ Zr = a.Z;  // (read-only here)
+  const double* __restrict__ Pr = a.PU;
+  double* __restrict__ Wr = a.W;
+  double* __restrict__ Ur = a.U;
+  pdl_wait();
+  pdl_trigger();
+  bool bad = false;
+  for (long long t = wg; t < ntile; t += nw) {
+    const long long b0 = bfirst + t * 32;
+    const int nb = (int)(nblk - t * 32 < 32 ? nblk - t * 32 : 32);
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) cpa8(A + r * TP_RS + lane, X + (b0 + r) * 32 + lane, r < nb);
+    if (MODE == 1)
+      for (int o = lane; o < nb * wi; o += 32) {
+        const int j = (int)__umulhi((unsigned)o, mi);
+        cpa4(wt + j * TP_WS + (o - j * wi), mant + (b0 + j) * stride + (o - j * wi));
+      }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const int Eu = MODE == 1 && lane < nb ? (int)exps[b0 + lane] : -128;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+    double* row = A + lane * TP_RS;
+    const long long p0 = b0 * 32 + lane;
+    if (MODE == 0) {
+      const int E = tpb_exponent(row, wo, bad);
+      tpb_pack(row, E, wo, wt + lane * TP_WS, nullptr);
+      if (lane < nb) exps[b0 + lane] = (int8_t)E;
+    } else {
+      const int Ey = tpb_exponent(row, a.wr, bad);  // ý = enc_{w_r}(y_k): values only (never stored)
+      tpb_quant(row, Ey, a.wr);
+      __syncwarp();
+      if (a.wout) {  // w_l = z_l + dec ý_l (loads 8 rows deep)
+#pragma unroll 1
+        for (int r0 = 0; r0 < nb; r0 += 8) {
+          double zv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) zv[k] = r0 + k < nb ? __ldg(Zr + p0 + (r0 + k) * 32) : 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (r0 + k < nb) Wr[p0 + (r0 + k) * 32] = (double)((T)zv[k] + (T)A[(r0 + k) * TP_RS + lane]);
+        }
+        __syncwarp();
+      }
+      tpb_unpack_add(wt + lane * TP_WS, Eu, wi, row);  // dec ú_l + ý
+      const int En = tpb_exponent(row, wo, bad);
+      tpb_pack(row, En, wo, wt + lane * TP_WS, row);  // ú_l <- enc(dec ú_l + ý); row = its value
+      if (lane < nb) exps[b0 + lane] = (int8_t)En;
+    }
+    __syncwarp();
+    for (int o = lane; o < nb * wo; o += 32) {
+      const int j = (int)__umulhi((unsigned)o, mo);
+      mant[(b0 + j) * stride + (o - j * wo)] = wt[j * TP_WS + (o - j * wo)];
+    }
+    if (MODE == 1 && a.uout) {  // u_l = dec ú_l + P u_{l-1}
+#pragma unroll 1
+      for (int r0 = 0; r0 < nb; r0 += 8) {
+        double pv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pv[k] = r0 + k < nb ? __ldg(Pr + p0 + (r0 + k) * 32) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (r0 + k < nb) Ur[p0 + (r0 + k) * 32] = A[(r0 + k) * TP_RS + lane] + pv[k];
+      }
+    }
+    __syncwarp();
+  }
+  if (__any_sync(FULL, bad) && lane == 0) atomicOr(a.status, 1);
 }
 
 // ------------------------------------------------------------------ host --
@@ -1211,15 +1328,23 @@ void fine3_set_attributes() {
 #define F(P)                                                                                        \
   cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);        \
   cudaFuncSetAttribute(k_f3_prolong<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);         \
-  cudaFuncSetAttribute(k_f3_residual_s<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
+  cudaFuncSetAttribute(k_f3_residual_s<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_residual_s<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cfas<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);    \
-  cudaFuncSetAttribute(k_f3_cheb<P, 2, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cheb<P, 3, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cfas<P, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);     \
-  cudaFuncSetAttribute(k_f3_cheb<P, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
-  cudaFuncSetAttribute(k_f3_cheb<P, 3, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   F(1) F(2) F(3)
 #undef F
+  cudaFuncSetAttribute(k_f3_tpb<0, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
+  cudaFuncSetAttribute(k_f3_tpb<1, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
+  cudaFuncSetAttribute(k_f3_tpb<1, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
 }
 
 template <class T>
@@ -1257,13 +1382,48 @@ static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Ar
   cudaLaunchKernelEx(&cfg, kernel, a, cf);
 }
 
+// thread-per-block epilogue over the rank's planes (PDL-chained like the march kernels)
+template <int MODE, class T>
+static void tpb_launch(cudaStream_t st, const F3Args& a) {
+  const long long bpp = (long long)a.g.NY * (a.g.NX >> 5), nblk = (long long)(a.zhi - a.zlo) * bpp;
+  const long long want = (nblk + 32 * TP_WARPS - 1) / (32 * TP_WARPS);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = (int)std::max(1LL, std::min(want, (long long)sms * 4));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TP_WARPS * 32);
+  cfg.dynamicSmemBytes = tpb_smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_f3_tpb<MODE, T>, a);
+}
+
 template <int P, class T>
 static void launch_cfas_cheb(int kind, cudaStream_t st, const F3Args& a, const CoefT<T>& ct) {
   const int n = a.nitems;
   const bool aux = a.last && (a.wout || a.uout);
-  if (kind == 1) f3_launch(k_f3_cfas<P, T>, n, smem_cfas<P, T>(a.wr), st, a, ct);
-  else if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T>, n, smem_cheb<P, T>(2, a.wu, aux), st, a, ct);
-  else f3_launch(k_f3_cheb<P, 3, T>, n, smem_cheb<P, T>(3, a.wu, aux), st, a, ct);
+  if (kind == 1) {
+    f3_launch(k_f3_cfas<P, T>, n, smem_cfas<P, T>(a.wr), st, a, ct);
+  } else if (a.last && a.tpb) {  // y_k -> Y, then the thread-per-block finalisation
+    F3Args b = a;
+    b.Dv = a.Yb;
+    if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T, true>, n, smem_cheb<P, T>(2, a.wu, false), st, b, ct);
+    else f3_launch(k_f3_cheb<P, 3, T, true>, n, smem_cheb<P, T>(3, a.wu, false), st, b, ct);
+    tpb_launch<1, T>(st, b);
+  } else if (a.step == 2) {
+    f3_launch(k_f3_cheb<P, 2, T, false>, n, smem_cheb<P, T>(2, a.wu, aux), st, a, ct);
+  } else {
+    f3_launch(k_f3_cheb<P, 3, T, false>, n, smem_cheb<P, T>(3, a.wu, aux), st, a, ct);
+  }
 }
 
 // kind: 0 residual (u generated), 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3), 3 prolongation,
@@ -1272,9 +1432,16 @@ static void launch_cfas_cheb(int kind, cudaStream_t st, const F3Args& a, const C
 void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf, int fp32) {
   if (kind == 4) {  // residual with u_L staged (materialised form)
     const CoefT<double> ct = coefs_as<double>(cf);
-    if (p == 1) f3_launch(k_f3_residual_s<1>, a.nitems, smem_res_s<1>(), st, a, ct);
-    else if (p == 2) f3_launch(k_f3_residual_s<2>, a.nitems, smem_res_s<2>(), st, a, ct);
-    else f3_launch(k_f3_residual_s<3>, a.nitems, smem_res_s<3>(), st, a, ct);
+    if (a.tpb) {  // r_L encoded afterwards, thread per block
+      if (p == 1) f3_launch(k_f3_residual_s<1, false>, a.nitems, smem_res_s<1>(), st, a, ct);
+      else if (p == 2) f3_launch(k_f3_residual_s<2, false>, a.nitems, smem_res_s<2>(), st, a, ct);
+      else f3_launch(k_f3_residual_s<3, false>, a.nitems, smem_res_s<3>(), st, a, ct);
+      tpb_launch<0, double>(st, a);
+      return;
+    }
+    if (p == 1) f3_launch(k_f3_residual_s<1, true>, a.nitems, smem_res_s<1>(), st, a, ct);
+    else if (p == 2) f3_launch(k_f3_residual_s<2, true>, a.nitems, smem_res_s<2>(), st, a, ct);
+    else f3_launch(k_f3_residual_s<3, true>, a.nitems, smem_res_s<3>(), st, a, ct);
     return;
   }
   if (kind == 3) {  // P u_{l-1} (step 0) or u_l = dec ú_l + P u_{l-1} (step 1) at the tile points

@@ -141,6 +141,8 @@ struct F3Args {
   double* U;                 // last Chebyshev step: u_l = dec ú_l + P u_{l-1} -> U (uout)
   double* W;                 // last Chebyshev step: w_l = z_l + dec ý_l -> W (wout)
   int zout, wout, uout;
+  int tpb;                   // thread-per-block epilogues (k_f3_tpb): r_L after the residual, the last step's codec
+  double* Yb;                // (tpb) y_k of the last Chebyshev step, FP64, level window
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.

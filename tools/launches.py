@@ -52,5 +52,24 @@ def main():
         print(f"{t / 1e3:10.1f} us {100 * t / tot:5.1f}% n={cnt[k]:4d} {k}  " + " ".join(extra))
 
 
+def fine_window(path, regex, first, n):
+    """The --launch-skip (counted over kernels matching regex) that starts an
+    n-launch window at the longest `first` launch followed by n-1 matches."""
+    import re
+    per, names = load(path)
+    ids = sorted(per, key=int)
+    m = [i for i in ids if re.search(regex, names[i])]
+    best, at = -1.0, 0
+    for j, i in enumerate(m[:len(m) - n + 1]):
+        if first in names[i]:
+            t = sum(per[k].get("gpu__time_duration.sum", 0.0) for k in m[j:j + n])
+            if t > best:
+                best, at = t, j
+    return at
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1] == "--skip":
+        print(fine_window(sys.argv[2], sys.argv[3], sys.argv[4], int(sys.argv[5])))
+    else:
+        main()

@@ -4,7 +4,9 @@
 
 Joins ncu's per-SASS "Instructions Executed" (source page) with the line
 table nvdisasm -g prints for the same function (build with -lineinfo).
-`units` divides the counts (e.g. 32-point warp rows of the launch)."""
+`units` divides the counts (e.g. 32-point warp rows of the launch).  A
+kernel regex of the form re@skip#column attributes another source-page
+column (e.g. stall_wait, stall_short_sb)."""
 import collections
 import csv
 import io
@@ -18,6 +20,9 @@ def main():
     units = float(sys.argv[5]) if len(sys.argv) > 5 else 1.0
     top = int(sys.argv[6]) if len(sys.argv) > 6 else 40
     skip = "0"
+    col = "Instructions Executed"
+    if "#" in kre:  # kernel regex#column: attribute another source-page column (e.g. stall_wait)
+        kre, col = kre.split("#")
     if "@" in kre:
         kre, skip = kre.split("@")
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
@@ -25,7 +30,7 @@ def main():
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[1]
-    ai, ei, si = h.index("Address"), h.index("Instructions Executed"), h.index("Source")
+    ai, ei, si = h.index("Address"), h.index(col), h.index("Source")
     counts = []
     for r in rows[2:]:
         if len(r) > ei:
