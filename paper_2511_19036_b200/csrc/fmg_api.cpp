@@ -79,8 +79,8 @@ struct fmg_ctx {
   CUtensorMap tmU[kMaxLev]{}, tmT[kMaxLev]{}, tmB[4][kMaxLev]{};
   // finest-level kernels (fmg_fine3.cu): coarse boxes of u_l / w_l, fine boxes
   // of t_l (= b_l) and of the Chebyshev direction
-  CUtensorMap tmCU[kMaxLev]{}, tmCW[kMaxLev]{}, tmFB[kMaxLev]{}, tmFD[kMaxLev]{};
-  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3 | CU | CW | FB | FD] x kMaxLev
+  CUtensorMap tmCU[kMaxLev]{}, tmCW[kMaxLev]{}, tmFB[kMaxLev]{}, tmFD[kMaxLev]{}, tmYB[kMaxLev]{};
+  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3 | CU | CW | FB | FD | YB] x kMaxLev
   // 3D, one GPU, Chebyshev degree 2-3, nu = 1: level L of each FMG level runs
   // the finest-level kernels and keeps no u_L, z_L, P u_{L-1}, w_L or y arrays
   // (DESIGN.md §4.3); the level arrays of l = Lmax that remain are t (= b)
@@ -92,6 +92,7 @@ struct fmg_ctx {
   // FMG_F3MAT=0/1 forces the choice.
   bool f3mat = false;
   bool tpb = false;  // thread-per-block epilogues of the finest-level kernels (k_f3_tpb; needs f3mat's memory)
+  bool cfs = false;  // top-level cFas step 1 from a materialised z_L (k_f3_prolong + k_f3_staged<P, 2>; in Y)
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
@@ -701,6 +702,8 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.tpb = c->tpb && (it.f3kind == 2 || it.f3kind == 4) && a.wu <= 32 && a.wu_out <= 32 && a.wr <= 32 &&
           (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= (1LL << 16);
   a.Yb = sview(c, 2, l);
+  a.cfs = c->cfs && it.f3kind == 1 && o.l == o.L && (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= (1LL << 16);
+  a.tmy = c->tm_dev + 10 * kMaxLev + l;
   a.zoff = c->wlo[l];
   a.czoff = l >= 1 ? c->wlo[l - 1] : 0;
   a.pbase = c->pbase;
@@ -1240,6 +1243,10 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     const char* et = getenv("FMG_TPB");
     const double ytop = 8.0 * (double)c->g[Lmax].NX * c->g[Lmax].NY * (c->whi[Lmax] - c->wlo[Lmax]);
     c->tpb = c->f3mat && (et ? atoi(et) != 0 : (e != nullptr || need + ytop < 0.5 * (double)totalb));
+    // z_L = P w_{L-1} materialised in Y for the top level's cFas step 1 (one
+    // GPU: its ghost planes would need an exchange).  FMG_CFS=0 disables.
+    const char* ec = getenv("FMG_CFS");
+    c->cfs = c->tpb && c->G == 1 && !s->cfas_fp32 && !(ec && atoi(ec) == 0);
   }
   for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
     const long long plane = (long long)c->g[l].NX * c->g[l].NY, off = plane * c->wlo[l];
@@ -1292,7 +1299,9 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     const int want = e ? atoi(e) : -1;
     c->tma = want == 1 || (want < 0 && dim == 3);
   }
-  for (int l = 0; l <= Lmax && rc == FMG_OK && c->tma; ++l) {
+  // (3D with the finest-level kernels: the maps are built with FMG_TMA=0 too;
+  // k_f3_staged reads u_l through them, the march kernels go by c->tma)
+  for (int l = 0; l <= Lmax && rc == FMG_OK && (c->tma || (dim == 3 && c->fine3)); ++l) {
     const Geom& g = c->g[l];
     bool ok = true;
     if (dim == 2) {
@@ -1332,11 +1341,12 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     if (l >= 1) {
       ok &= make_tmap(&c->tmFB[l], c->Tl[l] + off, g.NX, g.NY, nz, rs, nr);
       if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->sbase[4], g.NX, g.NY, nz, rs, nr);
+      if (c->cfs) ok &= make_tmap(&c->tmYB[l], c->sbase[2], g.NX, g.NY, nz, rs, nr);
     }
     if (!ok) rc = FMG_ECUDA;
   }
   if (rc == FMG_OK && (c->tma || c->fine3)) {
-    std::vector<CUtensorMap> all(10 * kMaxLev);
+    std::vector<CUtensorMap> all(11 * kMaxLev);
     for (int l = 0; l < kMaxLev; ++l) {
       all[l] = c->tmU[l];
       all[kMaxLev + l] = c->tmT[l];
@@ -1345,6 +1355,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       all[7 * kMaxLev + l] = c->tmCW[l];
       all[8 * kMaxLev + l] = c->tmFB[l];
       all[9 * kMaxLev + l] = c->tmFD[l];
+      all[10 * kMaxLev + l] = c->tmYB[l];
     }
     c->tm_dev = (CUtensorMap*)dalloc(c, sizeof(CUtensorMap) * all.size());  // (256-byte aligned)
     if (!c->tm_dev) rc = FMG_ENOMEM;

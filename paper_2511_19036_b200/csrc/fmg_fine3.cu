@@ -1066,21 +1066,26 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
   }
 }
 
-// t_L = f_L - A_L u_L with u_L staged by TMA (the materialised form,
-// DESIGN.md §4.3); r_L = enc(t_L); t_L -> HBM; ||t_L||^2 partial per warp.
-// The skeleton of k_f3_cheb (specialised y / z passes, incremental slots)
-// around the old k_m3_residual's arithmetic.
-// ENC = false: r_L is encoded afterwards from t_L by k_f3_tpb<0> (thread per block).
-template <int P, bool ENC>
-__global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const __grid_constant__ F3Args a,
-                                                                         const __grid_constant__ CoefT<double> cf) {
+// Staged-input sweeps of the materialised form: the
+// skeleton of k_f3_cheb (specialised y / z passes, incremental slots) over a
+// TMA-staged FP64 input v, then per output point:
+//   K = 0, 1: t_L = f_L - A_L u_L (v = u_L); t_L -> HBM; ||t_L||^2 partial per
+//             warp; K = 0 also r_L = enc(t_L) (K = 1: k_f3_tpb<0> encodes);
+//   K = 2:    b_L = dec r_L - A_L z_L (v = z_L = P w_{L-1}, materialised by
+//             k_f3_prolong) -> the t_L buffer: cFas step 1 at the top level.
+template <int P, int K>
+__global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __grid_constant__ F3Args a,
+                                                                     const __grid_constant__ CoefT<double> cf) {
   using C = F3<P>;
-  constexpr int R = C::R, NR = C::NR, BOX = C::BOX, NBF = C::NBF, PF = C::PF;
+  constexpr int R = C::R, NR = C::NR, BOX = C::BOX, NBF = C::NBF, PF = C::PF, NW = C::NW;
   extern __shared__ __align__(128) double fsm[];
-  double* ring = fsm;  // NBF boxes of u_L
+  double* ring = fsm;  // NBF boxes of v
   double* XA = ring + NBF * BOX;
   double* XB = XA + NR * 32;
-  unsigned long long* bars = (unsigned long long*)(XB + NR * 32);
+  uint32_t* wring = (uint32_t*)(XB + NR * 32);  // (K = 2) NW x FW x (w_r + 1): r_L words
+  const int RW = a.wr + 1;
+  unsigned long long* bars = (unsigned long long*)(wring + (K == 2 ? NW * FW * RW + 2 : 0));
+  bars = (unsigned long long*)(((uintptr_t)bars + 7) & ~(uintptr_t)7);
   const int lane = threadIdx.x, w = threadIdx.y;
   const F3Tile tl = f3_tile(a);
   const Geom g = a.g;
@@ -1097,7 +1102,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const 
   const double hl = pow2(-(a.l + 1));
   const double* __restrict__ gt = a.gtab;
   const bool uxy = unk1(x, n) && unk1(y, n);
-  const double gxy = uxy ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
+  const double gxy = K < 2 && uxy ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
   const int nxb = g.NX >> 5;
   const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
   const long long tplane = (long long)g.NY * g.NX, bpp = (long long)g.NY * nxb;
@@ -1106,7 +1111,11 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const 
   uint32_t* rmp = a.rmant + blk0 * a.rstride;
   int8_t* rep = a.rexp + blk0;
   const long long rstep = bpp * a.rstride;
-  const unsigned ring_s = smem_u32(ring), bars_s = smem_u32(bars);
+  const unsigned ring_s = smem_u32(ring), bars_s = smem_u32(bars), wring_s = smem_u32(wring);
+  const int nout = tl.ze - tl.zs;
+  int eoff = 0;
+  const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, a.wr, g, tl.x0, y, tl.zs, w * RW, K == 2 && rowok, lane,
+                              eoff);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
 #pragma unroll
     for (int k = 0; k < NBF; ++k) mbar_init(bars + k, 1);
@@ -1116,7 +1125,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const 
   pdl_wait();
   pdl_trigger();
   const int tmx = tl.x0 - P - (P & 1), tmy = tl.y0 - P;
-  auto stage = [&](int i, int slot) {  // plane z0 + i of u_L into ring slot `slot` (TMA, thread 0)
+  auto stage = [&](int i, int slot) {  // plane z0 + i of v into ring slot `slot` (TMA, thread 0)
     if (threadIdx.x == 0 && threadIdx.y == 0) {
       const unsigned dst = ring_s + (unsigned)(slot * BOX * 8), bar = bars_s + (unsigned)(slot * 8);
       fence_async_smem();
@@ -1132,18 +1141,34 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const 
 #pragma unroll
   for (int i = 0; i < PF; ++i)
     if (i < nin) stage(i, i);
+  if (K == 2) {  // r_L words of output planes 0..PF-1 -> word slots 0..PF-1
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      if (j < nout) wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
+      cpa_commit();
+    }
+  }
   double cr[R], sr[R];
 #pragma unroll
   for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
   double ss = 0.0;
   int tz = ((z0 % P) + P) % P;
-  int isl = 0;
+  int isl = 0, osl = 0;
   unsigned par = 0;
   for (int i = 0; i < nin; ++i) {
     const int zi = z0 + i;
+    const bool produce = i >= 2 * P;
     mbar_wait_s(bars_s + 8u * (unsigned)isl, par);
+    if (K == 2) cpa_wait<PF - 1>();
     __syncthreads();  // every thread is past iteration i - 1 (slot and XA/XB reuse)
     if (i + PF < nin) stage(i + PF, isl + PF >= NBF ? isl + PF - NBF : isl + PF);
+    if (K == 2) {
+      if (produce) {
+        const int j = i - 2 * P + PF;
+        if (j < nout) wcopy(ws, wring_s + (unsigned)((osl + PF >= NW ? osl + PF - NW : osl + PF) * FW * RW * 4), j);
+      }
+      cpa_commit();
+    }
     xpass<P>(ring + isl * BOX, C::SH, km, kk, XA, XB, w, lane);
     __syncthreads();
     double c, s;
@@ -1155,16 +1180,23 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const 
     }
     cr[R - 1] = c;
     sr[R - 1] = s;
-    if (i >= 2 * P) {
+    if (produce) {
       const int z = zi - P;
-      const double au = zpass<P>(cf, tz, cr, sr) * hl;
-      if (rowok) {
+      const double av = zpass<P>(cf, tz, cr, sr) * hl;
+      if (K == 2) {
+        if (rowok) {
+          const uint32_t* rec = wring + osl * FW * RW + w * RW;
+          const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
+          *Tp = rv - av;  // b = dec r - A z (B lives in the t_L buffer)
+        }
+        osl = osl + 1 == NW ? 0 : osl + 1;
+      } else if (rowok) {
         const bool uz = unk1(z, n);
         const double gz = uz ? gt[z] : 0.0;
-        const double t = (uxy && uz) ? gxy * gz - au : 0.0;  // (((C g(x)) g(y)) g(z)) - A u
+        const double t = (uxy && uz) ? gxy * gz - av : 0.0;  // (((C g(x)) g(y)) g(z)) - A u
         *Tp = t;
         ss = fma(t, t, ss);
-        if (ENC) warp_encode(t, a.wr, rmp, rep, lane, a.status);
+        if (K == 0) warp_encode(t, a.wr, rmp, rep, lane, a.status);
       }
       Tp += tplane;
       rmp += rstep;
@@ -1176,9 +1208,11 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const 
       par ^= 1u;
     }
   }
+  if (K < 2) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
-  if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)tl.cta * FW + w] = ss;
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+    if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)tl.cta * FW + w] = ss;
+  }
 }
 
 // Thread-per-block epilogues: the BFP codec of the
@@ -1189,7 +1223,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_residual_s(const 
 // tile, one lane per block runs the codec (fmg_device.cuh tpb_*, the same
 // arithmetic as warp_encode / warp_decode: reading R8), and the results leave
 // through coalesced copies.
-//   MODE 0: r_l = enc_{w_r}(t_l)                       (after k_f3_residual_s<P, false>)
+//   MODE 0: r_l = enc_{w_r}(t_l)                       (after k_f3_staged<P, 1>)
 //   MODE 1: ý = enc_{w_r}(y_k) (values only), ú_l <- enc_{w_u'}(dec ú_l + ý),
 //           w_l = z_l + ý (wout), u_l = ú_l + P u_{l-1} (uout)   (after k_f3_cheb<..., FIN>)
 // Widths <= 32 (tpb_*).  T: the cFas arithmetic of w_l (FP32 cFas, R28).
@@ -1303,9 +1337,10 @@ static int smem_cheb(int J, int wu, bool aux) {
 }
 
 template <int P>
-static int smem_res_s() {
+static int smem_staged(int wr) {  // (wr > 0: the r_L word ring of K = 2)
   using C = F3<P>;
-  return (int)(((size_t)C::NBF * C::BOX + 2 * C::NR * 32) * 8 + 8 * C::NBF + 16);
+  const size_t wb = wr > 0 ? (size_t)C::NW * FW * (wr + 1) * 4 + 8 : 0;
+  return (int)(((size_t)C::NBF * C::BOX + 2 * C::NR * 32) * 8 + wb + 8 * C::NBF + 16);
 }
 template <int P>
 static int smem_prolong(int wu) {
@@ -1328,8 +1363,9 @@ void fine3_set_attributes() {
 #define F(P)                                                                                        \
   cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);        \
   cudaFuncSetAttribute(k_f3_prolong<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);         \
-  cudaFuncSetAttribute(k_f3_residual_s<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_residual_s<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cfas<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);    \
   cudaFuncSetAttribute(k_f3_cheb<P, 2, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cheb<P, 3, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -1433,15 +1469,15 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
   if (kind == 4) {  // residual with u_L staged (materialised form)
     const CoefT<double> ct = coefs_as<double>(cf);
     if (a.tpb) {  // r_L encoded afterwards, thread per block
-      if (p == 1) f3_launch(k_f3_residual_s<1, false>, a.nitems, smem_res_s<1>(), st, a, ct);
-      else if (p == 2) f3_launch(k_f3_residual_s<2, false>, a.nitems, smem_res_s<2>(), st, a, ct);
-      else f3_launch(k_f3_residual_s<3, false>, a.nitems, smem_res_s<3>(), st, a, ct);
+      if (p == 1) f3_launch(k_f3_staged<1, 1>, a.nitems, smem_staged<1>(0), st, a, ct);
+      else if (p == 2) f3_launch(k_f3_staged<2, 1>, a.nitems, smem_staged<2>(0), st, a, ct);
+      else f3_launch(k_f3_staged<3, 1>, a.nitems, smem_staged<3>(0), st, a, ct);
       tpb_launch<0, double>(st, a);
       return;
     }
-    if (p == 1) f3_launch(k_f3_residual_s<1, true>, a.nitems, smem_res_s<1>(), st, a, ct);
-    else if (p == 2) f3_launch(k_f3_residual_s<2, true>, a.nitems, smem_res_s<2>(), st, a, ct);
-    else f3_launch(k_f3_residual_s<3, true>, a.nitems, smem_res_s<3>(), st, a, ct);
+    if (p == 1) f3_launch(k_f3_staged<1, 0>, a.nitems, smem_staged<1>(0), st, a, ct);
+    else if (p == 2) f3_launch(k_f3_staged<2, 0>, a.nitems, smem_staged<2>(0), st, a, ct);
+    else f3_launch(k_f3_staged<3, 0>, a.nitems, smem_staged<3>(0), st, a, ct);
     return;
   }
   if (kind == 3) {  // P u_{l-1} (step 0) or u_l = dec ú_l + P u_{l-1} (step 1) at the tile points
@@ -1456,6 +1492,24 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
     if (p == 1) f3_launch(k_f3_residual<1>, a.nitems, smem_res<1>(a.wu), st, a, ct);
     else if (p == 2) f3_launch(k_f3_residual<2>, a.nitems, smem_res<2>(a.wu), st, a, ct);
     else f3_launch(k_f3_residual<3>, a.nitems, smem_res<3>(a.wu), st, a, ct);
+    return;
+  }
+  if (kind == 1 && a.cfs && !fp32) {  // top level, materialised: z_L = P w_{L-1} -> Y, then b_L from staged z_L
+    const CoefT<double> ct = coefs_as<double>(cf);
+    F3Args b = a;
+    b.step = 0;
+    b.PU = a.Yb;
+    b.tmb = a.tmy;
+    if (p == 1) {
+      f3_launch(k_f3_prolong<1>, a.nitems, smem_prolong<1>(a.wu), st, b, ct);
+      f3_launch(k_f3_staged<1, 2>, a.nitems, smem_staged<1>(a.wr), st, b, ct);
+    } else if (p == 2) {
+      f3_launch(k_f3_prolong<2>, a.nitems, smem_prolong<2>(a.wu), st, b, ct);
+      f3_launch(k_f3_staged<2, 2>, a.nitems, smem_staged<2>(a.wr), st, b, ct);
+    } else {
+      f3_launch(k_f3_prolong<3>, a.nitems, smem_prolong<3>(a.wu), st, b, ct);
+      f3_launch(k_f3_staged<3, 2>, a.nitems, smem_staged<3>(a.wr), st, b, ct);
+    }
     return;
   }
   if (fp32) {

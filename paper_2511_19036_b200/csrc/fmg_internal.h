@@ -143,6 +143,8 @@ struct F3Args {
   int zout, wout, uout;
   int tpb;                   // thread-per-block epilogues (k_f3_tpb): r_L after the residual, the last step's codec
   double* Yb;                // (tpb) y_k of the last Chebyshev step, FP64, level window
+  int cfs;                   // cFas step 1 at the top level from a materialised z_L (in Yb; k_f3_staged<P, 2>)
+  const CUtensorMap* tmy;    // fine boxes of Yb (cfs)
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.
