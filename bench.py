@@ -140,8 +140,9 @@ def kernel_model(cfg, sched, cls):
     return flops * pts, byts * pts
 
 
-KERNEL_LABEL = {(2, 0): "k_m_residual (fine level)", (3, 0): "k_f3_residual (fine level)",
-                (2, 5): "k_m_cheb final step (fine level)", (3, 5): "k_f3_cheb final step (fine level)"}
+KERNEL_LABEL = {(2, 0): "k_m_residual (fine level)", (3, 0): "k_f3_staged / k_f3_residual (fine level)",
+                (2, 5): "k_m_cheb final step (fine level)",
+                (3, 5): "k_f3_cheb final step + k_f3_tpb<1> finalisation (fine level)"}
 
 
 def roofline_entry(cfg, sched, args, avg_launch_ms, launches, hbm, hbm_src):
@@ -176,7 +177,7 @@ def roofline_entry(cfg, sched, args, avg_launch_ms, launches, hbm, hbm_src):
             pass
     label = KERNEL_LABEL[(cfg["dim"], args.roofline_class)]
     if cfg["dim"] == 3 and (args.smoother == "mcgs" or args.nu > 1):  # (level-by-level kernels, fmg_march3.cu)
-        label = label.replace("k_f3_", "k_m3_")
+        label = {0: "k_m3_residual (fine level)", 5: "k_m3_cheb final step (fine level)"}.get(args.roofline_class, label)
     if args.smoother == "mcgs" and args.roofline_class == 5:
         label = label.replace("cheb final step", "gs final colour step")
     roof["kernel"] = label

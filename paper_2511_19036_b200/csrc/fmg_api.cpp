@@ -282,7 +282,10 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
   fmg_ctx* c = b.c;
   const int P = c->p, k = c->s.cheb_degree;
   const bool top = l == L, uout = !top || c->f3mat;
-  if (uout) {  // P u_{l-1} at the level's points (k_f3_prolong)
+  // top level of the materialised form on one GPU (levels of >= 2^16 blocks):
+  // z_L = P w_{L-1} materialised for cFas step 1, P u_{L-1} in the same launch
+  const bool cfs = c->cfs && top && (long long)(c->zhi[l] - c->zlo[l]) * c->g[l].NY * (c->g[l].NX / 32) >= (1LL << 16);
+  if (uout && !cfs) {  // P u_{l-1} at the level's points (k_f3_prolong)
     if (xch) b.xchg(XA_U, l - 1, P);
     OpDesc q = mkop(OP_PROLONG, l, L);
     q.step = 0;
@@ -301,6 +304,7 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
     q.zout = step == 1 && !top;
     q.wout = q.last && !top;
     q.uout = q.last && uout;
+    q.cfs = step == 1 && cfs ? (uout ? 2 : 1) : 0;
     b.fine(step == 1 ? 1 : 2, q, (fine && top) ? (step == k ? 5 : 1) : -1);
   }
 }
@@ -702,8 +706,9 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.tpb = c->tpb && (it.f3kind == 2 || it.f3kind == 4) && a.wu <= 32 && a.wu_out <= 32 && a.wr <= 32 &&
           (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= (1LL << 16);
   a.Yb = sview(c, 2, l);
-  a.cfs = c->cfs && it.f3kind == 1 && o.l == o.L && (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= (1LL << 16);
+  a.cfs = it.f3kind == 1 ? o.cfs : 0;
   a.tmy = c->tm_dev + 10 * kMaxLev + l;
+  if (l >= 1) a.tmcu = c->tm_dev + 6 * kMaxLev + (l - 1);
   a.zoff = c->wlo[l];
   a.czoff = l >= 1 ? c->wlo[l - 1] : 0;
   a.pbase = c->pbase;

@@ -949,19 +949,21 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
 // §3.3), but one point per thread: warp w's x pass covers coarse rows w,
 // w + 8 of the box, its y pass and z pass fine row y0 + w.  Replaces
 // k_m3_prolong's per-point (p+1)^2 global loads by shared boxes.
-template <int P>
+// NA = 2 (the top level of the materialised form): the same for two coarse
+// arrays at once, u_{l-1} -> PU and w_{l-1} -> a.out2 (z_l for k_f3_staged<P, 2>).
+template <int P, int NA>
 __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant__ F3Args a,
                                                             const __grid_constant__ CoefT<double> cf) {
   using C = F3<P>;
   constexpr int CBX = C::CBX, CBY = C::CBY, NCB = C::NCB, NCY = C::NCY, PF = C::PF, NW = C::NW;
   extern __shared__ __align__(128) double fsm[];
-  double* craw = fsm;                         // NCB coarse boxes (TMA)
-  double* PX = craw + NCB * C::CBS;           // CBY x 32: x pass
-  double* yv = PX + CBY * 32;                 // NCY x FW x 32: xy-passed coarse planes at the tile
-  uint32_t* wring = (uint32_t*)(yv + NCY * FW * 32);  // NW x FW x (w + 1): ú words (decode mode)
+  double* craw = fsm;                         // NA x NCB coarse boxes (TMA)
+  double* PX = craw + NA * NCB * C::CBS;      // NA x CBY x 32: x pass
+  double* yv = PX + NA * CBY * 32;            // NA x NCY x FW x 32: xy-passed coarse planes at the tile
+  uint32_t* wring = (uint32_t*)(yv + NA * NCY * FW * 32);  // NW x FW x (w + 1): ú words (decode mode)
   const int RW = a.wu + 1;
   unsigned long long* cbar = (unsigned long long*)(wring + NW * FW * RW + 2);
-  cbar = (unsigned long long*)(((uintptr_t)cbar + 7) & ~(uintptr_t)7);
+  cbar = (unsigned long long*)(((uintptr_t)cbar + 7) & ~(uintptr_t)7);  // NA x NCB
   const int lane = threadIdx.x, w = threadIdx.y;
   const F3Tile tl = f3_tile(a);
   const Geom g = a.g;
@@ -982,24 +984,29 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
     pwx[t] = cf.Pw[rx][t];
     pwy[t] = cf.Pw[ry][t];
   }
-  const bool decode = a.step == 1;  // (1: u_l = dec ú_l + P u_{l-1} -> U; 0: P u_{l-1} -> PU)
+  const bool decode = NA == 1 && a.step == 1;  // (1: u_l = dec ú_l + P u_{l-1} -> U; 0: P u_{l-1} -> PU)
   int eoff = 0;
   const WStream ws = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, y, tl.zs, w * RW, rowok && decode, lane,
                               eoff);
   const unsigned wring_s = smem_u32(wring);
   const long long tplane = (long long)g.NY * g.NX;
-  double* out = (decode ? a.U : a.PU) + ((long long)tl.zs * g.NY + y) * g.NX + x;
+  const long long o0 = ((long long)tl.zs * g.NY + y) * g.NX + x;
+  double* out = (decode ? a.U : a.PU) + o0;
+  double* out2 = NA == 2 ? a.out2 + o0 : nullptr;
+  const CUtensorMap* tms[2] = {a.tmc, NA == 2 ? a.tmc2 : a.tmc};
   const int nout = tl.ze - tl.zs;
   if (threadIdx.x == 0 && threadIdx.y == 0) {
 #pragma unroll
-    for (int k = 0; k < NCB; ++k) mbar_init(cbar + k, 1);
+    for (int k = 0; k < NA * NCB; ++k) mbar_init(cbar + k, 1);
     mbar_init_fence();
   }
   __syncthreads();
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x == 0 && threadIdx.y == 0)
-    for (int k = 0; k < NCB; ++k) gen_request<P>(gn, a.tmc, craw, cbar, gn.cfirst + k);
+    for (int q = 0; q < NA; ++q)
+      for (int k = 0; k < NCB; ++k)
+        gen_request<P>(gn, tms[q], craw + q * NCB * C::CBS, cbar + q * NCB, gn.cfirst + k);
 #pragma unroll
   for (int j = 0; j < PF; ++j) {
     if (j < nout) wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
@@ -1018,37 +1025,49 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
       const int cneed = cbase<P>(z) + P;
       while (gn.cdone <= cneed) {  // x and y passes of the next coarse plane
         const int c = gn.cdone, k = c - gn.cfirst;
-        mbar_wait_s(smem_u32(cbar) + 8u * (unsigned)(k % NCB), (unsigned)(k / NCB) & 1u);
-        const double* cb = craw + (k % NCB) * C::CBS;
 #pragma unroll
-        for (int q = 0; q < (CBY + FW - 1) / FW; ++q) {
-          const int cr = w + q * FW;
-          if (cr < CBY) {
-            double acc = 0.0;
-            if (okx) {
+        for (int q = 0; q < NA; ++q) {
+          mbar_wait_s(smem_u32(cbar + q * NCB) + 8u * (unsigned)(k % NCB), (unsigned)(k / NCB) & 1u);
+          const double* cb = craw + (q * NCB + k % NCB) * C::CBS;
 #pragma unroll
-              for (int t = 0; t <= P; ++t) acc = fma(pwx[t], cb[cr * CBX + bxo + t], acc);
+          for (int r = 0; r < (CBY + FW - 1) / FW; ++r) {
+            const int cr = w + r * FW;
+            if (cr < CBY) {
+              double acc = 0.0;
+              if (okx) {
+#pragma unroll
+                for (int t = 0; t <= P; ++t) acc = fma(pwx[t], cb[cr * CBX + bxo + t], acc);
+              }
+              PX[(q * CBY + cr) * 32 + lane] = acc;
             }
-            PX[cr * 32 + lane] = acc;
           }
         }
         __syncthreads();
-        if (threadIdx.x == 0 && threadIdx.y == 0) gen_request<P>(gn, a.tmc, craw, cbar, c + NCB);
-        double acc = 0.0;
-        if (oky) {
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+          for (int q = 0; q < NA; ++q) gen_request<P>(gn, tms[q], craw + q * NCB * C::CBS, cbar + q * NCB, c + NCB);
 #pragma unroll
-          for (int t = 0; t <= P; ++t) acc = fma(pwy[t], PX[(byo + t) * 32 + lane], acc);
+        for (int q = 0; q < NA; ++q) {
+          double acc = 0.0;
+          if (oky) {
+#pragma unroll
+            for (int t = 0; t <= P; ++t) acc = fma(pwy[t], PX[(q * CBY + byo + t) * 32 + lane], acc);
+          }
+          yv[((q * NCY + c % NCY) * FW + w) * 32 + lane] = acc;
         }
-        yv[((c % NCY) * FW + w) * 32 + lane] = acc;
         gn.cdone = c + 1;
         __syncthreads();
       }
     }
-    double pu = 0.0;
-    if (okz) {
-      const int rz = z % (2 * P), cb0 = cbase<P>(z);
+    double pu[NA];
 #pragma unroll
-      for (int t = 0; t <= P; ++t) pu = fma(cf.Pw[rz][t], yv[(((cb0 + t) % NCY) * FW + w) * 32 + lane], pu);
+    for (int q = 0; q < NA; ++q) {
+      pu[q] = 0.0;
+      if (okz) {
+        const int rz = z % (2 * P), cb0 = cbase<P>(z);
+#pragma unroll
+        for (int t = 0; t <= P; ++t)
+          pu[q] = fma(cf.Pw[rz][t], yv[((q * NCY + (cb0 + t) % NCY) * FW + w) * 32 + lane], pu[q]);
+      }
     }
     if (decode) {
       cpa_wait<PF>();
@@ -1056,12 +1075,14 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
       if (rowok) {
         const uint32_t* rec = wring + osl * FW * RW + w * RW;
         const double dv = warp_decode(rec, rec_e(rec + a.wu, eoff), a.wu, lane);
-        *out = dv + pu;  // u_l = dec ú_l + P u_{l-1}
+        *out = dv + pu[0];  // u_l = dec ú_l + P u_{l-1}
       }
     } else if (rowok) {
-      *out = pu;
+      *out = pu[0];
+      if (NA == 2) *out2 = pu[NA - 1];
     }
     out += tplane;
+    if (NA == 2) out2 += tplane;
     osl = osl + 1 == NW ? 0 : osl + 1;
   }
 }
@@ -1267,10 +1288,15 @@ __global__ void __launch_bounds__(TP_WARPS * 32) k_f3_tpb(const __grid_constant_
       }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     const int Eu = MODE == 1 && lane < nb ? (int)exps[b0 + lane] : -128;
+    const long long p0 = b0 * 32 + lane;
+    double pv[MODE == 1 ? 32 : 1];  // P u_{l-1} of the tile, loaded now, used after the codec
+    if (MODE == 1) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) pv[r] = a.uout && r < nb ? __ldg(Pr + p0 + r * 32) : 0.0;
+    }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
     double* row = A + lane * TP_RS;
-    const long long p0 = b0 * 32 + lane;
     if (MODE == 0) {
       const int E = tpb_exponent(row, wo, bad);
       tpb_pack(row, E, wo, wt + lane * TP_WS, nullptr);
@@ -1302,15 +1328,9 @@ __global__ void __launch_bounds__(TP_WARPS * 32) k_f3_tpb(const __grid_constant_
       mant[(b0 + j) * stride + (o - j * wo)] = wt[j * TP_WS + (o - j * wo)];
     }
     if (MODE == 1 && a.uout) {  // u_l = dec ú_l + P u_{l-1}
-#pragma unroll 1
-      for (int r0 = 0; r0 < nb; r0 += 8) {
-        double pv[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) pv[k] = r0 + k < nb ? __ldg(Pr + p0 + (r0 + k) * 32) : 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (r0 + k < nb) Ur[p0 + (r0 + k) * 32] = A[(r0 + k) * TP_RS + lane] + pv[k];
-      }
+      for (int r = 0; r < 32; ++r)
+        if (r < nb) Ur[p0 + r * 32] = A[r * TP_RS + lane] + pv[r];
     }
     __syncwarp();
   }
@@ -1343,10 +1363,10 @@ static int smem_staged(int wr) {  // (wr > 0: the r_L word ring of K = 2)
   return (int)(((size_t)C::NBF * C::BOX + 2 * C::NR * 32) * 8 + wb + 8 * C::NBF + 16);
 }
 template <int P>
-static int smem_prolong(int wu) {
+static int smem_prolong(int wu, int na = 1) {
   using C = F3<P>;
-  const size_t d = (size_t)C::NCB * C::CBS + C::CBY * 32 + (size_t)C::NCY * FW * 32;
-  return (int)(d * 8 + (size_t)C::NW * FW * (wu + 1) * 4 + 8 + 8 + 8 * C::NCB + 16);
+  const size_t d = ((size_t)C::NCB * C::CBS + C::CBY * 32 + (size_t)C::NCY * FW * 32) * na;
+  return (int)(d * 8 + (size_t)C::NW * FW * (wu + 1) * 4 + 8 + 8 + 8 * C::NCB * na + 16);
 }
 
 int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
@@ -1362,7 +1382,8 @@ void fine3_set_attributes() {
   const int big = 200 * 1024;
 #define F(P)                                                                                        \
   cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);        \
-  cudaFuncSetAttribute(k_f3_prolong<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);         \
+  cudaFuncSetAttribute(k_f3_prolong<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
+  cudaFuncSetAttribute(k_f3_prolong<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
   cudaFuncSetAttribute(k_f3_staged<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -1482,9 +1503,9 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
   }
   if (kind == 3) {  // P u_{l-1} (step 0) or u_l = dec ú_l + P u_{l-1} (step 1) at the tile points
     const CoefT<double> ct = coefs_as<double>(cf);
-    if (p == 1) f3_launch(k_f3_prolong<1>, a.nitems, smem_prolong<1>(a.wu), st, a, ct);
-    else if (p == 2) f3_launch(k_f3_prolong<2>, a.nitems, smem_prolong<2>(a.wu), st, a, ct);
-    else f3_launch(k_f3_prolong<3>, a.nitems, smem_prolong<3>(a.wu), st, a, ct);
+    if (p == 1) f3_launch(k_f3_prolong<1, 1>, a.nitems, smem_prolong<1>(a.wu), st, a, ct);
+    else if (p == 2) f3_launch(k_f3_prolong<2, 1>, a.nitems, smem_prolong<2>(a.wu), st, a, ct);
+    else f3_launch(k_f3_prolong<3, 1>, a.nitems, smem_prolong<3>(a.wu), st, a, ct);
     return;
   }
   if (kind == 0) {
@@ -1495,21 +1516,31 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
     return;
   }
   if (kind == 1 && a.cfs && !fp32) {  // top level, materialised: z_L = P w_{L-1} -> Y, then b_L from staged z_L
+    // (a.cfs == 2: P u_{L-1} -> PU in the same prolongation launch)
     const CoefT<double> ct = coefs_as<double>(cf);
     F3Args b = a;
     b.step = 0;
-    b.PU = a.Yb;
     b.tmb = a.tmy;
-    if (p == 1) {
-      f3_launch(k_f3_prolong<1>, a.nitems, smem_prolong<1>(a.wu), st, b, ct);
-      f3_launch(k_f3_staged<1, 2>, a.nitems, smem_staged<1>(a.wr), st, b, ct);
-    } else if (p == 2) {
-      f3_launch(k_f3_prolong<2>, a.nitems, smem_prolong<2>(a.wu), st, b, ct);
-      f3_launch(k_f3_staged<2, 2>, a.nitems, smem_staged<2>(a.wr), st, b, ct);
+    const int na = a.cfs == 2 ? 2 : 1;
+    if (na == 2) {
+      b.tmc2 = a.tmc;     // w_{L-1} -> Y
+      b.out2 = a.Yb;
+      b.tmc = a.tmcu;     // u_{L-1} -> PU
     } else {
-      f3_launch(k_f3_prolong<3>, a.nitems, smem_prolong<3>(a.wu), st, b, ct);
-      f3_launch(k_f3_staged<3, 2>, a.nitems, smem_staged<3>(a.wr), st, b, ct);
+      b.PU = a.Yb;
     }
+#define PRO(PP)                                                                                          \
+  if (na == 2) f3_launch(k_f3_prolong<PP, 2>, a.nitems, smem_prolong<PP>(a.wu, 2), st, b, ct);         \
+  else f3_launch(k_f3_prolong<PP, 1>, a.nitems, smem_prolong<PP>(a.wu), st, b, ct);                    \
+  f3_launch(k_f3_staged<PP, 2>, a.nitems, smem_staged<PP>(a.wr), st, b, ct);
+    if (p == 1) {
+      PRO(1)
+    } else if (p == 2) {
+      PRO(2)
+    } else {
+      PRO(3)
+    }
+#undef PRO
     return;
   }
   if (fp32) {

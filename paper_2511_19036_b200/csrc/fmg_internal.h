@@ -52,6 +52,7 @@ struct OpDesc {
   int wr, wu_in, wu_out;
   int guess, store, smode;  // nu > 1 cycles: see MArgs
   int zout, wout, uout, puonly;  // finest-level kernels (F3Args) / P u_{l-1}-only prolongation (MArgs)
+  int cfs;                       // finest-level cFas step 1 from a materialised z_L (F3Args::cfs)
   int row;
   long long poff;  // norm partials of this (FMG level, iteration, level): pbase + poff
 };
@@ -143,8 +144,12 @@ struct F3Args {
   int zout, wout, uout;
   int tpb;                   // thread-per-block epilogues (k_f3_tpb): r_L after the residual, the last step's codec
   double* Yb;                // (tpb) y_k of the last Chebyshev step, FP64, level window
-  int cfs;                   // cFas step 1 at the top level from a materialised z_L (in Yb; k_f3_staged<P, 2>)
+  int cfs;                   // cFas step 1 at the top level from a materialised z_L (in Yb; k_f3_staged<P, 2>);
+                             // 2: P u_{L-1} -> PU in the same prolongation launch
   const CUtensorMap* tmy;    // fine boxes of Yb (cfs)
+  const CUtensorMap* tmcu;   // coarse boxes of u_{L-1} (cfs == 2)
+  const CUtensorMap* tmc2;   // (k_f3_prolong<P, 2>) second coarse array and its output
+  double* out2;
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.
