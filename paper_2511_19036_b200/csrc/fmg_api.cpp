@@ -79,8 +79,8 @@ struct fmg_ctx {
   CUtensorMap tmU[kMaxLev]{}, tmT[kMaxLev]{}, tmB[4][kMaxLev]{};
   // finest-level kernels (fmg_fine3.cu): coarse boxes of u_l / w_l, fine boxes
   // of t_l (= b_l) and of the Chebyshev direction
-  CUtensorMap tmCU[kMaxLev]{}, tmCW[kMaxLev]{}, tmFB[kMaxLev]{}, tmFD[kMaxLev]{}, tmYB[kMaxLev]{};
-  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3 | CU | CW | FB | FD | YB] x kMaxLev
+  CUtensorMap tmCU[kMaxLev]{}, tmCW[kMaxLev]{}, tmFB[kMaxLev]{}, tmFD[kMaxLev]{}, tmYB[kMaxLev]{}, tmX1[kMaxLev]{};
+  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3 | CU | CW | FB | FD | YB | X1] x kMaxLev
   // 3D, one GPU, Chebyshev degree 2-3, nu = 1: level L of each FMG level runs
   // the finest-level kernels and keeps no u_L, z_L, P u_{L-1}, w_L or y arrays
   // (DESIGN.md §4.3); the level arrays of l = Lmax that remain are t (= b)
@@ -93,6 +93,7 @@ struct fmg_ctx {
   bool f3mat = false;
   bool tpb = false;  // thread-per-block epilogues of the finest-level kernels (k_f3_tpb; needs f3mat's memory)
   bool cfs = false;  // top-level cFas step 1 from a materialised z_L (k_f3_prolong + k_f3_staged<P, 2>; in Y)
+  bool csc = false;  // with cfs: the Chebyshev steps staged from the materialised y_{j-1} (X1, Y)
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
@@ -304,7 +305,7 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
     q.zout = step == 1 && !top;
     q.wout = q.last && !top;
     q.uout = q.last && uout;
-    q.cfs = step == 1 && cfs ? (uout ? 2 : 1) : 0;
+    q.cfs = !cfs ? 0 : step == 1 ? (uout ? 2 : 1) : (c->csc ? 3 : 0);
     b.fine(step == 1 ? 1 : 2, q, (fine && top) ? (step == k ? 5 : 1) : -1);
   }
 }
@@ -706,7 +707,10 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.tpb = c->tpb && (it.f3kind == 2 || it.f3kind == 4) && a.wu <= 32 && a.wu_out <= 32 && a.wr <= 32 &&
           (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= (1LL << 16);
   a.Yb = sview(c, 2, l);
-  a.cfs = it.f3kind == 1 ? o.cfs : 0;
+  a.cfs = (it.f3kind == 1 || it.f3kind == 2) ? o.cfs : 0;
+  a.csc = c->csc;
+  a.X1b = sview(c, 3, l);
+  a.tmx1 = c->tm_dev + 11 * kMaxLev + l;
   a.tmy = c->tm_dev + 10 * kMaxLev + l;
   if (l >= 1) a.tmcu = c->tm_dev + 6 * kMaxLev + (l - 1);
   a.zoff = c->wlo[l];
@@ -1252,6 +1256,12 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     // GPU: its ghost planes would need an exchange).  FMG_CFS=0 disables.
     const char* ec = getenv("FMG_CFS");
     c->cfs = c->tpb && c->G == 1 && !s->cfas_fp32 && !(ec && atoi(ec) == 0);
+    // ... and the Chebyshev steps from materialised y_1, y_2 (one more
+    // finest-size array X1; k_f3_staged<P, 3 / 4>): measured faster for
+    // p = 3 (C4 145.2 -> 136.4 ms), flat for p = 1 (C3 20.35 / 20.49 ms), so
+    // the default is p = 3; FMG_CSC=0/1 forces it.
+    const char* es = getenv("FMG_CSC");
+    c->csc = c->cfs && (es ? atoi(es) != 0 : p == 3);
   }
   for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
     const long long plane = (long long)c->g[l].NX * c->g[l].NY, off = plane * c->wlo[l];
@@ -1279,6 +1289,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       if (i == 1 && c->fine3) n = win(0);  // (level 0's bracket b_0: cFas1 + k_coarse_nu)
       if (i == 5 && c->f3mat) n = win(Lmax);  // (P u_{L-1} at the finest level)
       if (i == 2 && c->tpb) n = win(Lmax);    // (y_k of the last Chebyshev step, k_f3_tpb)
+      if (i == 3 && c->csc) n = win(Lmax);    // (X1: y_1, y_3 of the staged Chebyshev steps)
       const size_t bytes = sizeof(double) * n;
       c->buf[i] = (double*)dalloc(c, bytes);
       c->sbase[i] = c->buf[i];
@@ -1347,11 +1358,12 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       ok &= make_tmap(&c->tmFB[l], c->Tl[l] + off, g.NX, g.NY, nz, rs, nr);
       if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->sbase[4], g.NX, g.NY, nz, rs, nr);
       if (c->cfs) ok &= make_tmap(&c->tmYB[l], c->sbase[2], g.NX, g.NY, nz, rs, nr);
+      if (c->csc) ok &= make_tmap(&c->tmX1[l], c->sbase[3], g.NX, g.NY, nz, rs, nr);
     }
     if (!ok) rc = FMG_ECUDA;
   }
   if (rc == FMG_OK && (c->tma || c->fine3)) {
-    std::vector<CUtensorMap> all(11 * kMaxLev);
+    std::vector<CUtensorMap> all(12 * kMaxLev);
     for (int l = 0; l < kMaxLev; ++l) {
       all[l] = c->tmU[l];
       all[kMaxLev + l] = c->tmT[l];
@@ -1361,6 +1373,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       all[8 * kMaxLev + l] = c->tmFB[l];
       all[9 * kMaxLev + l] = c->tmFD[l];
       all[10 * kMaxLev + l] = c->tmYB[l];
+      all[11 * kMaxLev + l] = c->tmX1[l];
     }
     c->tm_dev = (CUtensorMap*)dalloc(c, sizeof(CUtensorMap) * all.size());  // (256-byte aligned)
     if (!c->tm_dev) rc = FMG_ENOMEM;

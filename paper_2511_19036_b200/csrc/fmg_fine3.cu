@@ -1093,17 +1093,26 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
 //   K = 0, 1: t_L = f_L - A_L u_L (v = u_L); t_L -> HBM; ||t_L||^2 partial per
 //             warp; K = 0 also r_L = enc(t_L) (K = 1: k_f3_tpb<0> encodes);
 //   K = 2:    b_L = dec r_L - A_L z_L (v = z_L = P w_{L-1}, materialised by
-//             k_f3_prolong) -> the t_L buffer: cFas step 1 at the top level.
+//             k_f3_prolong) -> the t_L buffer: cFas step 1 at the top level;
+//             with a.yout also y_1 = inv_theta (invD b) -> a.yout;
+//   K = 3, 4: Chebyshev step j = K - 1 from v = y_{j-1} (materialised by the
+//             step before): b (and d_2 for j = 3) are read at the output
+//             point only, d_j = fma(al_j, d_{j-1}, be_j (invD (b - A y_{j-1}))),
+//             y_j = y_{j-1} + d_j -> a.yout, and d_2 -> a.Dv when j = 2 is
+//             not the last step.  Same expressions as k_f3_cheb (which
+//             recomputes y_{j-1} on its staged b / d_2 boxes instead).
 template <int P, int K>
 __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __grid_constant__ F3Args a,
                                                                      const __grid_constant__ CoefT<double> cf) {
   using C = F3<P>;
-  constexpr int R = C::R, NR = C::NR, BOX = C::BOX, NBF = C::NBF, PF = C::PF, NW = C::NW;
+  constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX, NBF = C::NBF, PF = C::PF, NW = C::NW;
+  constexpr int NX_ = K == 4 ? 2 : 1;  // point arrays of K = 3, 4: b (+ d_2)
   extern __shared__ __align__(128) double fsm[];
   double* ring = fsm;  // NBF boxes of v
   double* XA = ring + NBF * BOX;
   double* XB = XA + NR * 32;
-  uint32_t* wring = (uint32_t*)(XB + NR * 32);  // (K = 2) NW x FW x (w_r + 1): r_L words
+  double* aring = XB + NR * 32;  // (K >= 3) NW x NX_ x 256: b (+ d_2) at the output points
+  uint32_t* wring = (uint32_t*)(aring + (K >= 3 ? NW * NX_ * 32 * FW : 0));  // (K = 2) NW x FW x (w_r + 1)
   const int RW = a.wr + 1;
   unsigned long long* bars = (unsigned long long*)(wring + (K == 2 ? NW * FW * RW + 2 : 0));
   bars = (unsigned long long*)(((uintptr_t)bars + 7) & ~(uintptr_t)7);
@@ -1124,19 +1133,38 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
   const double* __restrict__ gt = a.gtab;
   const bool uxy = unk1(x, n) && unk1(y, n);
   const double gxy = K < 2 && uxy ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
+  // invD at the output point per z node type (RN(1/diag) 2^(l+1), 0 at non-unknowns)
+  double fv[P];
+#pragma unroll
+  for (int t = 0; t < P; ++t) fv[t] = uxy ? cf.invd[(t * P + ty) * P + tx] * pow2(a.l + 1) : 0.0;
+  const double al = cf.cal[K - 2 > 0 ? K - 2 : 0], be = cf.cbe[K - 2 > 0 ? K - 2 : 0], ith = cf.inv_theta;
   const int nxb = g.NX >> 5;
   const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
   const long long tplane = (long long)g.NY * g.NX, bpp = (long long)g.NY * nxb;
-  double* Tp = a.T + ((long long)tl.zs * g.NY + y) * g.NX + x;
+  const long long pbase0 = ((long long)tl.zs * g.NY + y) * g.NX + x;
+  double* Tp = a.T + pbase0;
+  double* Yo = a.yout ? a.yout + pbase0 : nullptr;
+  double* Dp = a.Dv + pbase0;
   const long long blk0 = ((long long)tl.zs * g.NY + y) * nxb + (tl.x0 >> 5);
   uint32_t* rmp = a.rmant + blk0 * a.rstride;
   int8_t* rep = a.rexp + blk0;
   const long long rstep = bpp * a.rstride;
   const unsigned ring_s = smem_u32(ring), bars_s = smem_u32(bars), wring_s = smem_u32(wring);
+  const unsigned aring_s = smem_u32(aring);
+  const int tid = w * 32 + lane;
   const int nout = tl.ze - tl.zs;
   int eoff = 0;
   const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, a.wr, g, tl.x0, y, tl.zs, w * RW, K == 2 && rowok, lane,
                               eoff);
+  auto pcopy = [&](int j, int slot) {  // (K >= 3) b (+ d_2) of output plane zs + j -> aux slot
+    if (K >= 3 && rowok) {
+      const unsigned d = aring_s + (unsigned)(((slot * NX_) * 32 * FW + tid) * 8);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(a.T + pbase0 + j * tplane) : "memory");
+      if (K == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 32 * FW * 8), "l"(a.Dv + pbase0 + j * tplane)
+                     : "memory");
+    }
+  };
   if (threadIdx.x == 0 && threadIdx.y == 0) {
 #pragma unroll
     for (int k = 0; k < NBF; ++k) mbar_init(bars + k, 1);
@@ -1162,10 +1190,13 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
 #pragma unroll
   for (int i = 0; i < PF; ++i)
     if (i < nin) stage(i, i);
-  if (K == 2) {  // r_L words of output planes 0..PF-1 -> word slots 0..PF-1
+  if (K >= 2) {  // r_L words (K = 2) / point values (K >= 3) of output planes 0..PF-1 -> slots 0..PF-1
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
-      if (j < nout) wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
+      if (j < nout) {
+        if (K == 2) wcopy(ws, wring_s + (unsigned)(j * FW * RW * 4), j);
+        else pcopy(j, j);
+      }
       cpa_commit();
     }
   }
@@ -1174,19 +1205,23 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
   for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
   double ss = 0.0;
   int tz = ((z0 % P) + P) % P;
-  int isl = 0, osl = 0;
+  int isl = 0, osl = 0, oisl = NBF - P;  // slots: input plane i, words / points of the next output, input plane i - P
   unsigned par = 0;
   for (int i = 0; i < nin; ++i) {
     const int zi = z0 + i;
     const bool produce = i >= 2 * P;
     mbar_wait_s(bars_s + 8u * (unsigned)isl, par);
-    if (K == 2) cpa_wait<PF - 1>();
+    if (K >= 2) cpa_wait<PF - 1>();
     __syncthreads();  // every thread is past iteration i - 1 (slot and XA/XB reuse)
     if (i + PF < nin) stage(i + PF, isl + PF >= NBF ? isl + PF - NBF : isl + PF);
-    if (K == 2) {
+    if (K >= 2) {
       if (produce) {
         const int j = i - 2 * P + PF;
-        if (j < nout) wcopy(ws, wring_s + (unsigned)((osl + PF >= NW ? osl + PF - NW : osl + PF) * FW * RW * 4), j);
+        const int sl = osl + PF >= NW ? osl + PF - NW : osl + PF;
+        if (j < nout) {
+          if (K == 2) wcopy(ws, wring_s + (unsigned)(sl * FW * RW * 4), j);
+          else pcopy(j, sl);
+        }
       }
       cpa_commit();
     }
@@ -1204,15 +1239,42 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
     if (produce) {
       const int z = zi - P;
       const double av = zpass<P>(cf, tz, cr, sr) * hl;
-      if (K == 2) {
+      const bool uz = unk1(z, n);
+      if (K >= 3) {
+        if (rowok) {
+          const double* ax = aring + osl * NX_ * 32 * FW + tid;
+          const double b = ax[0];
+          double f = fv[0];  // (selected with constant indices: fv stays in registers)
+#pragma unroll
+          for (int t = 1; t < P; ++t) f = tz == t ? fv[t] : f;
+          f = uz ? f : 0.0;
+          const double yprev = ring[oisl * BOX + C::SH + (w + P) * RS + P + lane];  // y_{j-1} at the point
+          const double dprev = K == 4 ? ax[32 * FW] : yprev;                        // d_{j-1} (d_1 = y_1)
+          const double qq = b - av;
+          const double d = fma(al, dprev, be * (f * qq));
+          const double yv = yprev + d;
+          *Yo = yv;
+          if (!a.last) *Dp = d;
+        }
+        Yo += tplane;
+        Dp += tplane;
+        osl = osl + 1 == NW ? 0 : osl + 1;
+      } else if (K == 2) {
         if (rowok) {
           const uint32_t* rec = wring + osl * FW * RW + w * RW;
           const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
-          *Tp = rv - av;  // b = dec r - A z (B lives in the t_L buffer)
+          const double b = rv - av;  // b = dec r - A z (B lives in the t_L buffer)
+          *Tp = b;
+          if (Yo) {
+            double f = fv[0];
+#pragma unroll
+            for (int t = 1; t < P; ++t) f = tz == t ? fv[t] : f;
+            *Yo = ith * ((uz ? f : 0.0) * b);  // y_1 = inv_theta (invD b)
+          }
         }
+        if (Yo) Yo += tplane;
         osl = osl + 1 == NW ? 0 : osl + 1;
       } else if (rowok) {
-        const bool uz = unk1(z, n);
         const double gz = uz ? gt[z] : 0.0;
         const double t = (uxy && uz) ? gxy * gz - av : 0.0;  // (((C g(x)) g(y)) g(z)) - A u
         *Tp = t;
@@ -1224,6 +1286,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
       rep += bpp;
     }
     tz = tz + 1 == P ? 0 : tz + 1;
+    oisl = oisl + 1 == NBF ? 0 : oisl + 1;
     if (++isl == NBF) {
       isl = 0;
       par ^= 1u;
@@ -1357,10 +1420,11 @@ static int smem_cheb(int J, int wu, bool aux) {
 }
 
 template <int P>
-static int smem_staged(int wr) {  // (wr > 0: the r_L word ring of K = 2)
+static int smem_staged(int wr, int nx = 0) {  // (wr > 0: the r_L word ring of K = 2; nx: point arrays of K >= 3)
   using C = F3<P>;
   const size_t wb = wr > 0 ? (size_t)C::NW * FW * (wr + 1) * 4 + 8 : 0;
-  return (int)(((size_t)C::NBF * C::BOX + 2 * C::NR * 32) * 8 + wb + 8 * C::NBF + 16);
+  const size_t xb = (size_t)C::NW * nx * 32 * FW * 8;
+  return (int)(((size_t)C::NBF * C::BOX + 2 * C::NR * 32) * 8 + xb + wb + 8 * C::NBF + 16);
 }
 template <int P>
 static int smem_prolong(int wu, int na = 1) {
@@ -1387,6 +1451,8 @@ void fine3_set_attributes() {
   cudaFuncSetAttribute(k_f3_staged<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cfas<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);    \
   cudaFuncSetAttribute(k_f3_cheb<P, 2, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cheb<P, 3, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -1487,6 +1553,30 @@ static void launch_cfas_cheb(int kind, cudaStream_t st, const F3Args& a, const C
 // 4 residual (u staged);
 // `fp32`: FP32 cFas (kinds 1, 2; reading R28)
 void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf, int fp32) {
+  if (kind == 2 && a.cfs == 3 && !fp32) {  // staged Chebyshev step j from y_{j-1} (top level, materialised)
+    const CoefT<double> ct = coefs_as<double>(cf);
+    F3Args b = a;
+    const bool j2 = a.step == 2;
+    b.tmb = j2 ? a.tmx1 : a.tmy;     // y_1 in X1 / y_2 in Y
+    b.yout = j2 ? a.Yb : a.X1b;      // y_2 -> Y, y_3 -> X1
+#define ST(PP)                                                                                              \
+  if (j2) f3_launch(k_f3_staged<PP, 3>, a.nitems, smem_staged<PP>(0, 1), st, b, ct);                      \
+  else f3_launch(k_f3_staged<PP, 4>, a.nitems, smem_staged<PP>(0, 2), st, b, ct);
+    if (p == 1) {
+      ST(1)
+    } else if (p == 2) {
+      ST(2)
+    } else {
+      ST(3)
+    }
+#undef ST
+    if (a.last) {  // the thread-per-block finalisation from y_k
+      F3Args t = a;
+      t.Dv = b.yout;
+      tpb_launch<1, double>(st, t);
+    }
+    return;
+  }
   if (kind == 4) {  // residual with u_L staged (materialised form)
     const CoefT<double> ct = coefs_as<double>(cf);
     if (a.tpb) {  // r_L encoded afterwards, thread per block
@@ -1522,6 +1612,7 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
     b.step = 0;
     b.tmb = a.tmy;
     const int na = a.cfs == 2 ? 2 : 1;
+    b.yout = a.csc ? a.X1b : nullptr;  // y_1 for the staged Chebyshev steps
     if (na == 2) {
       b.tmc2 = a.tmc;     // w_{L-1} -> Y
       b.out2 = a.Yb;

@@ -150,6 +150,12 @@ struct F3Args {
   const CUtensorMap* tmcu;   // coarse boxes of u_{L-1} (cfs == 2)
   const CUtensorMap* tmc2;   // (k_f3_prolong<P, 2>) second coarse array and its output
   double* out2;
+  // staged Chebyshev steps (cfs == 3 on a Chebyshev item; k_f3_staged<P, 3 / 4>):
+  // y_1 -> X1 (cFas step 1), y_2 -> Yb (step 2), y_3 -> X1 (step 3)
+  double* X1b;
+  const CUtensorMap* tmx1;   // fine boxes of X1b
+  int csc;                   // (cFas step 1 with cfs) the Chebyshev steps are staged: write y_1
+  double* yout;              // (k_f3_staged) where y_j goes
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.
