@@ -1251,7 +1251,8 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     // measured faster (profiles/r2_summary.md).  FMG_TPB=0 disables.
     const char* et = getenv("FMG_TPB");
     const double ytop = 8.0 * (double)c->g[Lmax].NX * c->g[Lmax].NY * (c->whi[Lmax] - c->wlo[Lmax]);
-    c->tpb = c->f3mat && (et ? atoi(et) != 0 : (e != nullptr || need + ytop < 0.5 * (double)totalb));
+    // (with room for X1 of the staged Chebyshev steps too: two more arrays)
+    c->tpb = c->f3mat && (et ? atoi(et) != 0 : (e != nullptr || need + 2.0 * ytop < 0.5 * (double)totalb));
     // z_L = P w_{L-1} materialised in Y for the top level's cFas step 1 (one
     // GPU: its ghost planes would need an exchange).  FMG_CFS=0 disables.
     const char* ec = getenv("FMG_CFS");
