@@ -316,6 +316,7 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_step": e2e_ms},
         "gpu_launches": int(info["launches_per_solve"]) * args.steps,
         "repeat_bit_identical": repeat_identical,
+        "device_bytes": solver.device_bytes(),
         "clocks": ck,
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -283,9 +283,10 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
   fmg_ctx* c = b.c;
   const int P = c->p, k = c->s.cheb_degree;
   const bool top = l == L, uout = !top || c->f3mat;
-  // top level of the materialised form on one GPU (levels of >= 2^16 blocks):
-  // z_L = P w_{L-1} materialised for cFas step 1, P u_{L-1} in the same launch
-  const bool cfs = c->cfs && top && (long long)(c->zhi[l] - c->zlo[l]) * c->g[l].NY * (c->g[l].NX / 32) >= (1LL << 16);
+  // materialised form on one GPU, levels of >= 2^16 blocks: z_l = P w_{l-1}
+  // materialised for cFas step 1 (in Y at the top level, in the Z scratch
+  // below it, where the last step needs z_l again), P u_{l-1} in the same launch
+  const bool cfs = c->cfs && (long long)(c->zhi[l] - c->zlo[l]) * c->g[l].NY * (c->g[l].NX / 32) >= (1LL << 16);
   if (uout && !cfs) {  // P u_{l-1} at the level's points (k_f3_prolong)
     if (xch) b.xchg(XA_U, l - 1, P);
     OpDesc q = mkop(OP_PROLONG, l, L);
@@ -305,7 +306,7 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
     q.zout = step == 1 && !top;
     q.wout = q.last && !top;
     q.uout = q.last && uout;
-    q.cfs = !cfs ? 0 : step == 1 ? (uout ? 2 : 1) : (c->csc ? 3 : 0);
+    q.cfs = !cfs ? 0 : step == 1 ? (!top ? 5 : uout ? 2 : 1) : (c->csc ? 3 : 0);
     b.fine(step == 1 ? 1 : 2, q, (fine && top) ? (step == k ? 5 : 1) : -1);
   }
 }
@@ -711,6 +712,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.csc = c->csc;
   a.X1b = sview(c, 3, l);
   a.tmx1 = c->tm_dev + 11 * kMaxLev + l;
+  a.tmz = c->tm_dev + 2 * kMaxLev + l;  // (fine boxes of the Z scratch, levels < Lmax)
   a.tmy = c->tm_dev + 10 * kMaxLev + l;
   if (l >= 1) a.tmcu = c->tm_dev + 6 * kMaxLev + (l - 1);
   a.zoff = c->wlo[l];

@@ -1610,13 +1610,14 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
     const CoefT<double> ct = coefs_as<double>(cf);
     F3Args b = a;
     b.step = 0;
-    b.tmb = a.tmy;
-    const int na = a.cfs == 2 ? 2 : 1;
+    const bool below = a.cfs == 5;  // (z_l in the Z scratch: the last step's w_l = z_l + ý needs it)
+    b.tmb = below ? a.tmz : a.tmy;
+    const int na = a.cfs == 1 ? 1 : 2;
     b.yout = a.csc ? a.X1b : nullptr;  // y_1 for the staged Chebyshev steps
     if (na == 2) {
-      b.tmc2 = a.tmc;     // w_{L-1} -> Y
-      b.out2 = a.Yb;
-      b.tmc = a.tmcu;     // u_{L-1} -> PU
+      b.tmc2 = a.tmc;     // w_{l-1} -> Y / Z
+      b.out2 = below ? a.Z : a.Yb;
+      b.tmc = a.tmcu;     // u_{l-1} -> PU
     } else {
       b.PU = a.Yb;
     }

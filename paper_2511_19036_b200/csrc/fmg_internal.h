@@ -144,8 +144,9 @@ struct F3Args {
   int zout, wout, uout;
   int tpb;                   // thread-per-block epilogues (k_f3_tpb): r_L after the residual, the last step's codec
   double* Yb;                // (tpb) y_k of the last Chebyshev step, FP64, level window
-  int cfs;                   // cFas step 1 at the top level from a materialised z_L (in Yb; k_f3_staged<P, 2>);
-                             // 2: P u_{L-1} -> PU in the same prolongation launch
+  int cfs;                   // cFas step 1 from a materialised z_l (k_f3_staged<P, 2>): 1 top level, z_L in Yb;
+                             // 2: also P u_{L-1} -> PU in the same prolongation launch; 5: below the top
+                             // level, z_l -> the Z scratch and P u_{l-1} -> PU; 3 (Chebyshev item): staged step
   const CUtensorMap* tmy;    // fine boxes of Yb (cfs)
   const CUtensorMap* tmcu;   // coarse boxes of u_{L-1} (cfs == 2)
   const CUtensorMap* tmc2;   // (k_f3_prolong<P, 2>) second coarse array and its output
@@ -155,6 +156,7 @@ struct F3Args {
   double* X1b;
   const CUtensorMap* tmx1;   // fine boxes of X1b
   int csc;                   // (cFas step 1 with cfs) the Chebyshev steps are staged: write y_1
+  const CUtensorMap* tmz;    // (cfs == 5, below the top level) fine boxes of the Z scratch
   double* yout;              // (k_f3_staged) where y_j goes
 };
 

@@ -16,5 +16,5 @@ $B --workload n4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_n4
 timeout 300 python tools/profile_one.py C4 1 > /dev/null 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/ev/c4_launches.csv python tools/profile_one.py C4 1 > /dev/null 2>&1; echo list4 $?
 timeout 300 python tools/profile_one.py C3 1 > /dev/null 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/ev/c3_launches.csv python tools/profile_one.py C3 1 > /dev/null 2>&1; echo list3 $?
 RX="k_f3|k_m3_restrict"
-SK=$(python tools/launches.py --skip gpurun_out/ev/c4_launches.csv "$RX" k_f3_prolong 6); echo skip $SK
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$RX" -s $SK -c 6 -o gpurun_out/ev/c4_full python tools/profile_one.py C4 1 > gpurun_out/ev/ncu_full.log 2>&1; echo full $?
+SK=$(python tools/launches.py --skip gpurun_out/ev/c4_launches.csv "$RX" k_f3_prolong 8); echo skip $SK
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$RX" -s $SK -c 8 -o gpurun_out/ev/c4_full python tools/profile_one.py C4 1 > gpurun_out/ev/ncu_full.log 2>&1; echo full $?
