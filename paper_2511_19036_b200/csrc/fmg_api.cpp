@@ -657,14 +657,15 @@ MArgs march_args(const fmg_ctx* c, const OpDesc& o) {
     const CUtensorMap* U = c->tm_dev, *T = U + kMaxLev, *B = T + kMaxLev;  // device copies
     switch (o.type) {
       case OP_RESIDUAL: m.tm = U + l; break;
-      case OP_RESTRICT: if (c->dim == 2) m.tm = T + l + 1; break;
+      case OP_RESTRICT: m.tm = T + l + 1; break;
       case OP_CFAS1: if (c->dim == 3) m.tm = B + l; break;
       case OP_GS: m.tm = B + 3 * kMaxLev + l; break;
       case OP_CHEB: m.tm = B + (o.step == 2 ? 1 : 2 + ((o.step - 1) & 1)) * kMaxLev + l; break;
       default: break;
     }
-    m.tma = (o.type == OP_RESIDUAL || o.type == OP_GS || o.type == OP_CHEB ||
-             (o.type == OP_RESTRICT && c->dim == 2 && !o.smode) || (o.type == OP_CFAS1 && c->dim == 3)) ? 1 : 0;
+    m.tma = (o.type == OP_RESIDUAL || o.type == OP_GS || o.type == OP_CHEB || (o.type == OP_RESTRICT && !o.smode) ||
+             (o.type == OP_CFAS1 && c->dim == 3)) ? 1 : 0;
+    if (o.type == OP_RESTRICT && c->dim == 3) m.zoff = c->wlo[l + 1];  // (the staged array is t_{l+1})
   }
   return m;
 }
@@ -1343,6 +1344,14 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
           ok &= make_tmap(&c->tmB[i][l], c->sbase[i], g.NX, g.NY, nz, 40, 8 + 2 * p);
     }
     if (!ok) rc = FMG_ECUDA;
+  }
+  // 3D restriction (k_m3_restrict, TMA form): fine-plane boxes of t_l, l >= 1,
+  // 64 + 4p wide from an even column, 16 + 4p - 2 rows
+  for (int l = 1; l <= Lmax && rc == FMG_OK && c->tma && dim == 3; ++l) {
+    const Geom& g = c->g[l];
+    const long long off = (long long)g.NX * g.NY * c->wlo[l];
+    if (!make_tmap(&c->tmT[l], c->Tl[l] + off, g.NX, g.NY, c->whi[l] - c->wlo[l], 64 + 4 * p, 16 + 4 * p - 2))
+      rc = FMG_ECUDA;
   }
   // finest-level kernels: coarse boxes of u_l, w_l (l < Lmax), fine boxes of
   // t_l and of Dv (levels >= 1)

@@ -706,15 +706,33 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_sq(const DevCt
 // and y-passed to the coarse rows; the z pass runs on a register ring of the
 // last 4p-1 fine planes (two new planes per coarse output plane).
 constexpr int RPF3 = 2, RNB3 = 3, RRS3 = 80;
+// TMA form (a.tma): the fine plane box starts at the even column 2 x0 - 2p and
+// is 64 + 4p doubles wide (16-byte rows), so fine column fxs sits at index 1.
 template <int P>
+__host__ __device__ constexpr int rbox_w() { return 64 + 4 * P; }
+template <int P>
+__host__ __device__ constexpr int rbox_slot() {  // doubles per ring slot (128-byte multiple)
+  return ((2 * TW3 + 2 * (2 * P - 1)) * rbox_w<P>() + 15) & ~15;
+}
+template <int P, bool TMA>
 __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const DevCtx* __restrict__ cp, const __grid_constant__ MArgs a,
                                                             const __grid_constant__ Coefs cf) {
   extern __shared__ __align__(128) double msm[];
+  constexpr int NS = 4 * P - 1, H = 2 * P - 1, FR = 2 * TW3 + 2 * H, FW = 64 + 2 * H;
+  constexpr int SROW = TMA ? rbox_w<P>() : RRS3, SLOT = TMA ? rbox_slot<P>() : FR * RRS3, SX = TMA ? 1 : 0;
+  double* ring = msm;                // RNB3 x SLOT
+  double* XR = ring + RNB3 * SLOT;   // FR x 32
+  unsigned long long* bars = (unsigned long long*)(XR + FR * 32);  // (TMA) RNB3
+  if (TMA && threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < RNB3; ++k) mbar_init(bars + k, 1);
+    mbar_init_fence();
+  }
+  if (TMA) __syncthreads();
   pdl_wait();
   pdl_trigger();
   M3Item it;
   m3_item(a, it);
-  constexpr int NS = 4 * P - 1, H = 2 * P - 1, FR = 2 * TW3 + 2 * H, FW = 64 + 2 * H;
   const MPtrs& c = a.p;
   const LevelDev& lc_ = a.lv;
   const LevelDev& lf = a.lo;
@@ -723,8 +741,6 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const
   const bool rowok = yc < gc.NY;
   const int txc = xc % P, tyc = yc % P;
   const int fxs = 2 * it.x0 - H, fys = 2 * it.y0 - H;
-  double* ring = msm;                    // RNB3 x FR x RRS3
-  double* XR = ring + RNB3 * FR * RRS3;  // FR x 32
   const double* __restrict__ Tf = lf.T;
   const int nxb = gc.NX >> 5;
   double rw[NS], rv[NS];
@@ -733,15 +749,23 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const
     rw[s] = cf.Rw[txc][s];
     rv[s] = 0.0;
   }
-  auto stage = [&](int fz, double* slot) {
+  auto stage = [&](int fz, int k) {  // fine plane fz into ring slot k
+    double* slot = ring + k * SLOT;
+    if (TMA) {
+      if (threadIdx.x == 0 && threadIdx.y == 0) {
+        fence_async_smem();
+        tma_load_3d(slot, a.tm, fxs - SX, fys, fz - a.zoff, bars + k, (unsigned)(FR * SROW * 8));
+      }
+      return;
+    }
     const bool zok = fz >= 0 && fz < gf.NZ;
     for (int r = w; r < FR; r += TW3) {
       const int fy = fys + r;
       const bool rok = zok && fy >= 0 && fy < gf.NY;
       const double* rp = Tf + ((long long)(rok ? fz : 0) * gf.NY + (rok ? fy : 0)) * gf.NX;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const int jx = lane + 32 * k;
+      for (int kk = 0; kk < 3; ++kk) {
+        const int jx = lane + 32 * kk;
         if (jx < FW) {
           const int fx = fxs + jx;
           const bool ok = rok && fx >= 0 && fx < gf.NX;
@@ -754,17 +778,21 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const
   double ss = 0.0;
 #pragma unroll
   for (int i = 0; i < RPF3; ++i) {
-    if (i < nin) stage(fz0 + i, ring + (i % RNB3) * FR * RRS3);
-    cp3_commit();
+    if (i < nin) stage(fz0 + i, i % RNB3);
+    if (!TMA) cp3_commit();
   }
   for (int i = 0; i < nin; ++i) {
-    if (i + RPF3 < nin) stage(fz0 + i + RPF3, ring + ((i + RPF3) % RNB3) * FR * RRS3);
-    cp3_commit();
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(RPF3) : "memory");
+    if (i + RPF3 < nin) stage(fz0 + i + RPF3, (i + RPF3) % RNB3);
+    if (TMA) {
+      mbar_wait(bars + i % RNB3, (unsigned)(i / RNB3) & 1u);
+    } else {
+      cp3_commit();
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(RPF3) : "memory");
+    }
     __syncthreads();
-    const double* slot = ring + (i % RNB3) * FR * RRS3;
+    const double* slot = ring + (i % RNB3) * SLOT + SX;
     for (int r = w; r < FR; r += TW3) {
-      const double* row = slot + r * RRS3;
+      const double* row = slot + r * SROW;
       double v = 0.0;
 #pragma unroll
       for (int s = 0; s < NS; ++s) v = fma(rw[s], row[2 * lane + s], v);  // (t = +0 at fine non-unknowns)
@@ -799,9 +827,10 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const
 static int m3_smem_A(int p, bool tma = false) {
   return (int)(((size_t)NB3 * (TW3 + 2 * p) * RS3 + 2 * (TW3 + 2 * p) * 32) * 8 + (tma ? NB3 * 8 : 0));
 }
-static int m3_smem_R(int p) {
+static int m3_smem_R(int p, bool tma = false) {
   const int FR = 2 * TW3 + 2 * (2 * p - 1);
-  return (RNB3 * FR * RRS3 + FR * 32) * 8;
+  const int slot = tma ? (p == 1 ? rbox_slot<1>() : p == 2 ? rbox_slot<2>() : rbox_slot<3>()) : FR * RRS3;
+  return (RNB3 * slot + FR * 32) * 8 + (tma ? RNB3 * 8 : 0);
 }
 int march3_rows() { return TW3; }
 
@@ -819,7 +848,8 @@ void march3_set_attributes() {
   cudaFuncSetAttribute(k_m3_sq<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));                  \
   cudaFuncSetAttribute(k_m3_gs<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P));      \
   cudaFuncSetAttribute(k_m3_gs<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_A(P, true));       \
-  cudaFuncSetAttribute(k_m3_restrict<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_R(P));
+  cudaFuncSetAttribute(k_m3_restrict<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_R(P));      \
+  cudaFuncSetAttribute(k_m3_restrict<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, m3_smem_R(P, true));
   F(1) F(2) F(3)
 #undef F
 }
@@ -851,7 +881,7 @@ void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, c
     case OP_DECODE:                                                                           \
     case OP_PROLONG: m3_launch(k_m3_prolong<P>, n, 0, st, c, a, cf); break;                   \
     case OP_RESIDUAL: m3_launch(TM(k_m3_residual, P), n, m3_smem_A(P, t), st, c, a, cf); break; \
-    case OP_RESTRICT: m3_launch(k_m3_restrict<P>, n, m3_smem_R(P), st, c, a, cf); break;      \
+    case OP_RESTRICT: m3_launch(TM(k_m3_restrict, P), n, m3_smem_R(P, t), st, c, a, cf); break; \
     case OP_CFAS1:                                                                            \
       if (nu) m3_launch(k_m3_cfas1<P, false, true>, n, m3_smem_A(P), st, c, a, cf);            \
       else m3_launch(TM(k_m3_cfas1, P), n, m3_smem_A(P, t), st, c, a, cf);                     \
