@@ -265,13 +265,8 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
 
 // Exponent of one block (R8): E = -128 for an all-zero block; *bad on a
 // non-finite entry or E > 127.
-__device__ __forceinline__ int tpb_exponent(const double* row, int w, bool& bad) {
-  unsigned long long mx = 0ULL;
-#pragma unroll 8
-  for (int e = 0; e < 32; ++e) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(row[e]) & 0x7fffffffffffffffULL;
-    mx = b > mx ? b : mx;
-  }
+// E from the block's largest |x| bit pattern mx (R8; see tpb_exponent).
+__device__ __forceinline__ int tpb_exp_of_max(unsigned long long mx, int w, bool& bad) {
   if (mx >= 0x7ff0000000000000ULL) { bad = true; return -128; }
   if (mx == 0ULL) return -128;
   const int q = w - 1;
@@ -283,6 +278,45 @@ __device__ __forceinline__ int tpb_exponent(const double* row, int w, bool& bad)
   if (rint(__longlong_as_double((long long)mx) * pow2(q - E0)) == pow2(q)) E = E0 + 1;
   if (E > 127) { bad = true; return -128; }
   return E;
+}
+__device__ __forceinline__ int tpb_exponent(const double* row, int w, bool& bad) {
+  unsigned long long mx = 0ULL;
+#pragma unroll 8
+  for (int e = 0; e < 32; ++e) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(row[e]) & 0x7fffffffffffffffULL;
+    mx = b > mx ? b : mx;
+  }
+  return tpb_exp_of_max(mx, w, bad);
+}
+
+// One pass of the correction (S9 + S10 on one block): row holds y_k; with
+// the ý exponent Ey, row[e] <- dec ú_e + enc_{wr}(y_e) (the sum the ú encode
+// takes, same operands and order as tpb_quant + tpb_unpack_add); returns the
+// largest |sum| bit pattern for tpb_exp_of_max.
+__device__ __forceinline__ unsigned long long tpb_quant_add(double* row, int Ey, int wr, const uint32_t* wrow, int Eu,
+                                                            int wu) {
+  const int q = wr - 1;
+  const double s = Ey == -128 ? 0.0 : pow2(q - Ey);
+  const double sbq = Ey == -128 ? 0.0 : pow2(Ey - q);
+  const double sbu = Eu == -128 ? 0.0 : pow2(Eu - (wu - 1));
+  unsigned long long acc = 0ULL, mx = 0ULL;
+  int nb = 0, k = 0;
+#pragma unroll 4
+  for (int e = 0; e < 32; ++e) {
+    if (nb < wu) {
+      acc |= (unsigned long long)wrow[k++] << nb;
+      nb += 32;
+    }
+    const long long m = (long long)(acc << (64 - wu)) >> (64 - wu);
+    acc >>= wu;
+    nb -= wu;
+    const double yq = i2d(rne_int(row[e] * s, wr), wr) * sbq;
+    const double v = i2d(m, wu) * sbu + yq;
+    row[e] = v;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
+    mx = b > mx ? b : mx;
+  }
+  return mx;
 }
 
 // Quantise and pack one block with exponent E (E = -128: zeros).  When

@@ -1366,6 +1366,13 @@ __global__ void __launch_bounds__(TP_WARPS * 32) k_f3_tpb(const __grid_constant_
       if (lane < nb) exps[b0 + lane] = (int8_t)E;
     } else {
       const int Ey = tpb_exponent(row, a.wr, bad);  // ý = enc_{w_r}(y_k): values only (never stored)
+      if (!a.wout) {  // (no w_l: ý, dec ú + ý and the new exponent's max in one pass)
+        const unsigned long long mx = tpb_quant_add(row, Ey, a.wr, wt + lane * TP_WS, Eu, wi);
+        const int En = tpb_exp_of_max(mx, wo, bad);
+        tpb_pack(row, En, wo, wt + lane * TP_WS, row);
+        if (lane < nb) exps[b0 + lane] = (int8_t)En;
+        goto packed;
+      }
       tpb_quant(row, Ey, a.wr);
       __syncwarp();
       if (a.wout) {  // w_l = z_l + dec ý_l (loads 8 rows deep)
@@ -1385,6 +1392,7 @@ __global__ void __launch_bounds__(TP_WARPS * 32) k_f3_tpb(const __grid_constant_
       tpb_pack(row, En, wo, wt + lane * TP_WS, row);  // ú_l <- enc(dec ú_l + ý); row = its value
       if (lane < nb) exps[b0 + lane] = (int8_t)En;
     }
+  packed:
     __syncwarp();
     for (int o = lane; o < nb * wo; o += 32) {
       const int j = (int)__umulhi((unsigned)o, mo);
