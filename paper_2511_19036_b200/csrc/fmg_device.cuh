@@ -389,6 +389,80 @@ __device__ __forceinline__ void tpb_unpack(const uint32_t* wrow, int E, int w, d
   }
 }
 
+// ---- compile-time-width lane routines (W <= 32): every bit position of the
+// packed stream is a constant, the 32 entries are unrolled, the words live in
+// registers.  Same arithmetic as the runtime-width routines above.
+__device__ __forceinline__ double i2d32(int m) {  // exact int -> double (the 1.5 2^52 magic)
+  return __longlong_as_double(0x4338000000000000LL + (long long)m) - 6755399441055744.0;
+}
+__device__ __forceinline__ int rne32(double x) { return (int)__double2loint(x + 6755399441055744.0); }
+__device__ __forceinline__ unsigned long long absbits(double v) {
+  return (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
+}
+template <int W>
+__device__ __forceinline__ int tpb_field(const uint32_t (&wv)[W], int e) {  // entry e (e constant after unrolling)
+  const int p = e * W, j0 = p >> 5, sh = p & 31;
+  uint32_t f = wv[j0] >> sh;
+  if (sh + W > 32) f |= wv[j0 + 1] << (32 - sh);
+  return (int)(f << (32 - W)) >> (32 - W);
+}
+template <int W>
+__device__ __forceinline__ void tpb_put(uint32_t (&ov)[W], int e, int m) {
+  const int p = e * W, j0 = p >> 5, sh = p & 31;
+  const uint32_t f = (uint32_t)m & (W == 32 ? 0xffffffffu : ((1u << W) - 1u));
+  ov[j0] |= f << sh;
+  if (sh + W > 32) ov[j0 + 1] |= f >> (32 - sh);
+}
+// Encode one block (row: 32 values) at width W with exponent E: the words to
+// wout, the quantised values to qrow (may alias row, may be null).
+template <int W>
+__device__ __forceinline__ void tpb_pack_w(const double* row, int E, uint32_t* wout, double* qrow) {
+  const double s = E == -128 ? 0.0 : pow2(W - 1 - E);
+  const double sb = E == -128 ? 0.0 : pow2(E - (W - 1));
+  uint32_t ov[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) ov[j] = 0u;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    const int m = rne32(row[e] * s);
+    if (qrow) qrow[e] = i2d32(m) * sb;
+    tpb_put<W>(ov, e, m);
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j) wout[j] = ov[j];
+}
+// The correction of one block (k_f3_tpb<1>, no w_l): row holds y_k; ý =
+// enc_{WR}(y), row <- enc_{W}(dec ú + ý) (values), the new words to wout;
+// returns the new exponent.  The operand order of tpb_quant_add / tpb_pack.
+template <int W, int WR>
+__device__ __forceinline__ int tpb_correct_w(double* row, const uint32_t* win, int Eu, uint32_t* wout, bool& bad) {
+  unsigned long long mx = 0ULL;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    const unsigned long long b = absbits(row[e]);
+    mx = b > mx ? b : mx;
+  }
+  const int Ey = tpb_exp_of_max(mx, WR, bad);
+  const double s = Ey == -128 ? 0.0 : pow2(WR - 1 - Ey);
+  const double sbq = Ey == -128 ? 0.0 : pow2(Ey - (WR - 1));
+  const double sbu = Eu == -128 ? 0.0 : pow2(Eu - (W - 1));
+  uint32_t wv[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) wv[j] = win[j];
+  unsigned long long m2 = 0ULL;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    const double yq = i2d32(rne32(row[e] * s)) * sbq;
+    const double v = i2d32(tpb_field<W>(wv, e)) * sbu + yq;
+    row[e] = v;
+    const unsigned long long b = absbits(v);
+    m2 = b > m2 ? b : m2;
+  }
+  const int En = tpb_exp_of_max(m2, W, bad);
+  tpb_pack_w<W>(row, En, wout, row);
+  return En;
+}
+
 // ------------------------------------------------------------- contexts --
 // Device-side context (lives in global memory, built by fmg_api.cpp).
 // (LevelDev: fmg_internal.h)

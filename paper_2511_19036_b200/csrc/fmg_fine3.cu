@@ -1314,8 +1314,10 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
 constexpr int TP_WARPS = 4, TP_RS = 33, TP_WS = 33;
 constexpr int tpb_smem_bytes() { return TP_WARPS * (32 * TP_RS * 8 + 32 * TP_WS * 4); }
 
-template <int MODE, class T>
-__global__ void __launch_bounds__(TP_WARPS * 32) k_f3_tpb(const __grid_constant__ F3Args a) {
+// W, WR > 0: compile-time widths (tpb_*_w): MODE 1 without w_l with w_u = W,
+// w_r = WR; MODE 0 with w_r = WR.  0: the runtime-width routines.
+template <int MODE, class T, int W = 0, int WR = 0>
+__global__ void __launch_bounds__(TP_WARPS * 32, 4) k_f3_tpb(const __grid_constant__ F3Args a) {
   extern __shared__ __align__(16) double tsm[];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   double* A = tsm + wp * 32 * TP_RS;  // t_l (MODE 0) / y_k -> ý -> dec ú_l + ý -> the new ú_l (MODE 1)
@@ -1362,8 +1364,12 @@ __global__ void __launch_bounds__(TP_WARPS * 32) k_f3_tpb(const __grid_constant_
     double* row = A + lane * TP_RS;
     if (MODE == 0) {
       const int E = tpb_exponent(row, wo, bad);
-      tpb_pack(row, E, wo, wt + lane * TP_WS, nullptr);
+      if (WR > 0) tpb_pack_w<(WR > 0 ? WR : 1)>(row, E, wt + lane * TP_WS, nullptr);
+      else tpb_pack(row, E, wo, wt + lane * TP_WS, nullptr);
       if (lane < nb) exps[b0 + lane] = (int8_t)E;
+    } else if (W > 0) {  // (no w_l; compile-time widths)
+      const int En = tpb_correct_w<(W > 0 ? W : 1), (WR > 0 ? WR : 1)>(row, wt + lane * TP_WS, Eu, wt + lane * TP_WS, bad);
+      if (lane < nb) exps[b0 + lane] = (int8_t)En;
     } else {
       const int Ey = tpb_exponent(row, a.wr, bad);  // ý = enc_{w_r}(y_k): values only (never stored)
       if (!a.wout) {  // (no w_l: ý, dec ú + ý and the new exponent's max in one pass)
@@ -1473,6 +1479,13 @@ void fine3_set_attributes() {
   cudaFuncSetAttribute(k_f3_cheb<P, 3, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   F(1) F(2) F(3)
 #undef F
+#define TW(T_, W_, R_) \
+  cudaFuncSetAttribute(k_f3_tpb<1, T_, W_, R_>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
+#define TWS(T_) TW(T_, 4, 4) TW(T_, 6, 4) TW(T_, 6, 5) TW(T_, 8, 5) TW(T_, 8, 6) TW(T_, 10, 5) TW(T_, 14, 6) TW(T_, 5, 4) TW(T_, 8, 4)
+  TWS(double) TWS(float)
+#undef TWS
+#undef TW
+  cudaFuncSetAttribute(k_f3_tpb<0, double, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
   cudaFuncSetAttribute(k_f3_tpb<0, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
   cudaFuncSetAttribute(k_f3_tpb<1, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
   cudaFuncSetAttribute(k_f3_tpb<1, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
@@ -1514,8 +1527,24 @@ static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Ar
 }
 
 // thread-per-block epilogue over the rank's planes (PDL-chained like the march kernels)
+template <int MODE, class T, int W = 0, int WR = 0>
+static void tpb_launch_w(cudaStream_t st, const F3Args& a);
+// compile-time widths for the common cases (the top levels of the bench
+// schedules), the runtime-width kernel otherwise
 template <int MODE, class T>
 static void tpb_launch(cudaStream_t st, const F3Args& a) {
+  if constexpr (MODE == 0) {
+    if (a.wr == 4) return tpb_launch_w<MODE, T, 0, 4>(st, a);
+  } else if (!a.wout && a.wu == a.wu_out) {
+#define TW(W_, R_) \
+  if (a.wu == W_ && a.wr == R_) return tpb_launch_w<MODE, T, W_, R_>(st, a);
+    TW(4, 4) TW(6, 4) TW(6, 5) TW(8, 5) TW(8, 6) TW(10, 5) TW(14, 6) TW(5, 4) TW(8, 4)
+#undef TW
+  }
+  tpb_launch_w<MODE, T>(st, a);
+}
+template <int MODE, class T, int W, int WR>
+static void tpb_launch_w(cudaStream_t st, const F3Args& a) {
   const long long bpp = (long long)a.g.NY * (a.g.NX >> 5), nblk = (long long)(a.zhi - a.zlo) * bpp;
   const long long want = (nblk + 32 * TP_WARPS - 1) / (32 * TP_WARPS);
   static int sms = 0;
@@ -1535,7 +1564,7 @@ static void tpb_launch(cudaStream_t st, const F3Args& a) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_f3_tpb<MODE, T>, a);
+  cudaLaunchKernelEx(&cfg, k_f3_tpb<MODE, T, W, WR>, a);
 }
 
 template <int P, class T>
