@@ -94,6 +94,7 @@ struct fmg_ctx {
   bool tpb = false;  // thread-per-block epilogues of the finest-level kernels (k_f3_tpb; needs f3mat's memory)
   bool cfs = false;  // top-level cFas step 1 from a materialised z_L (k_f3_prolong + k_f3_staged<P, 2>; in Y)
   bool csc = false;  // with cfs: the Chebyshev steps staged from the materialised y_{j-1} (X1, Y)
+  long long tpb_min = 1LL << 16;  // levels of at least this many blocks take tpb / cfs (FMG_TPB_MIN_BLOCKS: tests)
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
@@ -286,7 +287,7 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
   // materialised form on one GPU, levels of >= 2^16 blocks: z_l = P w_{l-1}
   // materialised for cFas step 1 (in Y at the top level, in the Z scratch
   // below it, where the last step needs z_l again), P u_{l-1} in the same launch
-  const bool cfs = c->cfs && (long long)(c->zhi[l] - c->zlo[l]) * c->g[l].NY * (c->g[l].NX / 32) >= (1LL << 16);
+  const bool cfs = c->cfs && (long long)(c->zhi[l] - c->zlo[l]) * c->g[l].NY * (c->g[l].NX / 32) >= c->tpb_min;
   if (uout && !cfs) {  // P u_{l-1} at the level's points (k_f3_prolong)
     if (xch) b.xchg(XA_U, l - 1, P);
     OpDesc q = mkop(OP_PROLONG, l, L);
@@ -707,7 +708,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   // (levels of >= 2^16 blocks: below that the extra launch costs more than the
   // warp-cooperative codec it replaces)
   a.tpb = c->tpb && (it.f3kind == 2 || it.f3kind == 4) && a.wu <= 32 && a.wu_out <= 32 && a.wr <= 32 &&
-          (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= (1LL << 16);
+          (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= c->tpb_min;
   a.Yb = sview(c, 2, l);
   a.cfs = (it.f3kind == 1 || it.f3kind == 2) ? o.cfs : 0;
   a.csc = c->csc;
@@ -1264,6 +1265,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     // finest-size array X1; k_f3_staged<P, 3 / 4>): measured faster for
     // p = 3 (C4 145.2 -> 136.4 ms), flat for p = 1 (C3 20.35 / 20.49 ms), so
     // the default is p = 3; FMG_CSC=0/1 forces it.
+    if (const char* em = getenv("FMG_TPB_MIN_BLOCKS")) c->tpb_min = atoll(em);
     const char* es = getenv("FMG_CSC");
     c->csc = c->cfs && (es ? atoi(es) != 0 : p == 3);
   }

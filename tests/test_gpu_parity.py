@@ -423,3 +423,35 @@ def test_fp32_cfas_refused_outside_its_path(P):
         P.Solver(2, 1, 4, _gpu_sched(P, 2, 1, cfas_fp32=1))
     with pytest.raises(P.FmgError):
         P.Solver(3, 1, 4, _gpu_sched(P, 3, 1, cfas_fp32=1, smoother=1))
+
+
+# The materialised form's variants run by default only on
+# levels of >= 2^16 blocks; FMG_TPB_MIN_BLOCKS=0 applies them to every level of
+# small problems, so every (d = 3, p) path is compared with the oracle:
+# thread-per-block epilogues (compile-time and runtime widths), the
+# materialised z_l for cFas step 1 (top and lower levels), the staged
+# Chebyshev steps for every p, and each switched off in turn.
+_F3_VARIANTS = {
+    "all": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="1", FMG_CSC="1"),
+    "no_csc": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="1", FMG_CSC="0"),
+    "no_cfs": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="0"),
+    "fused_codec": dict(FMG_F3MAT="1", FMG_TPB="0"),
+    "lean": dict(FMG_F3MAT="0"),
+}
+
+
+@pytest.mark.parametrize("variant", sorted(_F3_VARIANTS))
+@pytest.mark.parametrize("d,p,levels", [(3, 1, 5), (3, 2, 4), (3, 3, 4), (3, 1, 6), (3, 3, 5)])
+def test_fmg_parity_fine3_variants(P, monkeypatch, variant, d, p, levels):
+    monkeypatch.setenv("FMG_TPB_MIN_BLOCKS", "0")
+    for k, v in _F3_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    compare_solvers(P, d, p, levels)
+
+
+@pytest.mark.parametrize("d,p,levels", [(3, 1, 5), (3, 3, 4)])
+def test_fmg_parity_fine3_variants_fp32(P, monkeypatch, d, p, levels):
+    """FP32 cFas with the thread-per-block epilogues on every level."""
+    monkeypatch.setenv("FMG_TPB_MIN_BLOCKS", "0")
+    monkeypatch.setenv("FMG_F3MAT", "1")
+    compare_solvers(P, d, p, levels, cfas_fp32=1)
