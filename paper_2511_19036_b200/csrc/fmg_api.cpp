@@ -95,6 +95,7 @@ struct fmg_ctx {
   bool cfs = false;  // top-level cFas step 1 from a materialised z_L (k_f3_prolong + k_f3_staged<P, 2>; in Y)
   bool csc = false;  // with cfs: the Chebyshev steps staged from the materialised y_{j-1} (X1, Y)
   long long tpb_min = 1LL << 16;  // levels of at least this many blocks take tpb / cfs (FMG_TPB_MIN_BLOCKS: tests)
+  bool tpb0 = false;  // lean form: the generating residual's r_L encoded thread per block (k_f3_tpb<0>)
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
@@ -707,8 +708,9 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.uout = o.uout;
   // (levels of >= 2^16 blocks: below that the extra launch costs more than the
   // warp-cooperative codec it replaces)
-  a.tpb = c->tpb && (it.f3kind == 2 || it.f3kind == 4) && a.wu <= 32 && a.wu_out <= 32 && a.wr <= 32 &&
-          (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= c->tpb_min;
+  // (the residual's r_L encode needs no extra array: the lean form takes it too)
+  a.tpb = (c->tpb ? (it.f3kind == 2 || it.f3kind == 4) : (it.f3kind == 0 && c->tpb0)) && a.wu <= 32 &&
+          a.wu_out <= 32 && a.wr <= 32 && (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= c->tpb_min;
   a.Yb = sview(c, 2, l);
   a.cfs = (it.f3kind == 1 || it.f3kind == 2) ? o.cfs : 0;
   a.csc = c->csc;
@@ -1266,6 +1268,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     // p = 3 (C4 145.2 -> 136.4 ms), flat for p = 1 (C3 20.35 / 20.49 ms), so
     // the default is p = 3; FMG_CSC=0/1 forces it.
     if (const char* em = getenv("FMG_TPB_MIN_BLOCKS")) c->tpb_min = atoll(em);
+    c->tpb0 = !(et && atoi(et) == 0);
     const char* es = getenv("FMG_CSC");
     c->csc = c->cfs && (es ? atoi(es) != 0 : p == 3);
   }

@@ -472,7 +472,8 @@ __host__ __device__ constexpr size_t gen_smem_bytes(int ring_words) {
 
 // t_L = f_L - A_L u_L with u_L = dec ú_L + P u_{L-1} generated on chip;
 // r_L = enc(t_L); t_L -> HBM; ||t_L||^2 partial per warp (Alg 3.2).
-template <int P>
+// ENC = false: r_L is encoded afterwards from t_L by k_f3_tpb<0> (thread per block).
+template <int P, bool ENC>
 __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual(const __grid_constant__ F3Args a,
                                                               const __grid_constant__ CoefT<double> cf) {
   using C = F3<P>;
@@ -589,7 +590,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB(P)) k_f3_residual(const __gri
         const double t = (uxy && uz) ? gxy * gz - au : 0.0;  // (((C g(x)) g(y)) g(z)) - A u
         *Tp = t;
         ss = fma(t, t, ss);
-        warp_encode(t, a.wr, rmp, rep, lane, a.status);
+        if (ENC) warp_encode(t, a.wr, rmp, rep, lane, a.status);
       }
       Tp += tplane;
       rmp += bpp * a.rstride;
@@ -1459,7 +1460,8 @@ int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
 void fine3_set_attributes() {
   const int big = 200 * 1024;
 #define F(P)                                                                                        \
-  cudaFuncSetAttribute(k_f3_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);        \
+  cudaFuncSetAttribute(k_f3_residual<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
+  cudaFuncSetAttribute(k_f3_residual<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_prolong<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
   cudaFuncSetAttribute(k_f3_prolong<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
   cudaFuncSetAttribute(k_f3_staged<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -1637,9 +1639,16 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
   }
   if (kind == 0) {
     const CoefT<double> ct = coefs_as<double>(cf);
-    if (p == 1) f3_launch(k_f3_residual<1>, a.nitems, smem_res<1>(a.wu), st, a, ct);
-    else if (p == 2) f3_launch(k_f3_residual<2>, a.nitems, smem_res<2>(a.wu), st, a, ct);
-    else f3_launch(k_f3_residual<3>, a.nitems, smem_res<3>(a.wu), st, a, ct);
+    if (a.tpb) {  // (lean form: r_L encoded afterwards from t_L, thread per block)
+      if (p == 1) f3_launch(k_f3_residual<1, false>, a.nitems, smem_res<1>(a.wu), st, a, ct);
+      else if (p == 2) f3_launch(k_f3_residual<2, false>, a.nitems, smem_res<2>(a.wu), st, a, ct);
+      else f3_launch(k_f3_residual<3, false>, a.nitems, smem_res<3>(a.wu), st, a, ct);
+      tpb_launch<0, double>(st, a);
+      return;
+    }
+    if (p == 1) f3_launch(k_f3_residual<1, true>, a.nitems, smem_res<1>(a.wu), st, a, ct);
+    else if (p == 2) f3_launch(k_f3_residual<2, true>, a.nitems, smem_res<2>(a.wu), st, a, ct);
+    else f3_launch(k_f3_residual<3, true>, a.nitems, smem_res<3>(a.wu), st, a, ct);
     return;
   }
   if (kind == 1 && a.cfs && !fp32) {  // top level, materialised: z_L = P w_{L-1} -> Y, then b_L from staged z_L
