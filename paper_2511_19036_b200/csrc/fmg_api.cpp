@@ -96,6 +96,9 @@ struct fmg_ctx {
   bool csc = false;  // with cfs: the Chebyshev steps staged from the materialised y_{j-1} (X1, Y)
   long long tpb_min = 1LL << 16;  // levels of at least this many blocks take tpb / cfs (FMG_TPB_MIN_BLOCKS: tests)
   bool tpb0 = false;  // lean form: the generating residual's r_L encoded thread per block (k_f3_tpb<0>)
+  bool tpby = false;  // lean form: the top level's last step stores ý as int8 mantissas (k_f3_tpb<2>)
+  int8_t* my_base = nullptr;  // (tpby) finest-window points
+  int8_t* ey_base = nullptr;  // (tpby) finest-window blocks
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
   // z-slab decomposition (3D): this context computes planes
   // [zlo, zhi) of every grid level l > lc (full-size arrays; ghost planes are
@@ -712,6 +715,13 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.tpb = (c->tpb ? (it.f3kind == 2 || it.f3kind == 4) : (it.f3kind == 0 && c->tpb0)) && a.wu <= 32 &&
           a.wu_out <= 32 && a.wr <= 32 && (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= c->tpb_min;
   a.Yb = sview(c, 2, l);
+  {
+    const long long plane = (long long)c->g[l].NX * c->g[l].NY;
+    a.my = c->my_base ? c->my_base - plane * c->wlo[l] : nullptr;
+    a.ey = c->ey_base ? c->ey_base - plane / 32 * c->wlo[l] : nullptr;
+    a.tpby = c->tpby && it.f3kind == 2 && o.last && !o.wout && !o.uout && o.wu_in == o.wu_out && o.wr <= 8 &&
+             fine3_tpby_width(o.wu_in, o.wr) && (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= c->tpb_min;
+  }
   a.cfs = (it.f3kind == 1 || it.f3kind == 2) ? o.cfs : 0;
   a.csc = c->csc;
   a.X1b = sview(c, 3, l);
@@ -1304,6 +1314,19 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       c->sbase[i] = c->buf[i];
       if (!c->buf[i]) rc = FMG_ENOMEM;
       else cudaMemset(c->buf[i], 0, bytes);
+    }
+  }
+  // lean form: ý of the top level's last step as int8 mantissas + exponents
+  // (1 byte per point) when that fits, for the thread-per-block correction
+  // (k_f3_tpb<2>).  FMG_TPBY=0 disables.
+  if (rc == FMG_OK && c->fine3 && !c->f3mat && !(getenv("FMG_TPBY") && atoi(getenv("FMG_TPBY")) == 0)) {
+    const size_t pts = (size_t)c->g[Lmax].NX * c->g[Lmax].NY * (c->whi[Lmax] - c->wlo[Lmax]);
+    size_t freeb = 0, totalb = 0;
+    cudaMemGetInfo(&freeb, &totalb);
+    if (freeb > pts + pts / 32 + ((size_t)4 << 30)) {
+      c->my_base = (int8_t*)dalloc(c, pts + 64);
+      c->ey_base = (int8_t*)dalloc(c, pts / 32 + 64);
+      c->tpby = c->my_base && c->ey_base;
     }
   }
   if (rc == FMG_OK && s->nu > 1) {  // YO: dec ý of the previous cycle at the level being smoothed

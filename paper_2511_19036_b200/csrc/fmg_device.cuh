@@ -211,7 +211,7 @@ __device__ __forceinline__ void warp_pack(unsigned long long field, int w, uint3
 // Writes the w words and the exponent when `words` is non-null; returns the
 // quantised value m 2^(E-q).  Non-finite input or E > 127 sets *status.
 __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, int8_t* eptr, int lane,
-                                              int* status) {
+                                              int* status, long long* mout = nullptr, int* Eout = nullptr) {
   unsigned long long bits = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffULL;
   const unsigned hi = (unsigned)(bits >> 32);
   const unsigned mh = __reduce_max_sync(FULL, hi);
@@ -249,6 +249,10 @@ __device__ __forceinline__ double warp_encode(double v, int w, uint32_t* words, 
   if (words) {
     warp_pack((unsigned long long)m & ((1ULL << w) - 1ULL), w, words, lane);
     if (lane == 0) *eptr = (int8_t)E;
+  }
+  if (mout) {  // (the mantissa and exponent themselves: k_f3_cheb's FIN = 2 mode)
+    *mout = m;
+    *Eout = E;
   }
   return E == -128 ? 0.0 : i2d(m, w) * pow2(E - q);
 }
@@ -460,6 +464,43 @@ __device__ __forceinline__ int tpb_correct_w(double* row, const uint32_t* win, i
   }
   const int En = tpb_exp_of_max(m2, W, bad);
   tpb_pack_w<W>(row, En, wout, row);
+  return En;
+}
+
+// The correction of one block from ý given as mantissas (int8, the k_f3_cheb
+// FIN = 2 store) and its exponent Ey: row <- enc_{W}(dec ú + ý) values are
+// not kept; the new words to wout; returns the new exponent.  Same operands
+// and order as tpb_correct_w (ý = m 2^(Ey - q_r) is what warp_encode returns).
+template <int W, int WR>
+__device__ __forceinline__ int tpb_correct_m(const int8_t* my, int Ey, const uint32_t* win, int Eu, uint32_t* wout,
+                                             bool& bad) {
+  const double sbq = Ey == -128 ? 0.0 : pow2(Ey - (WR - 1));
+  const double sbu = Eu == -128 ? 0.0 : pow2(Eu - (W - 1));
+  uint32_t wv[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) wv[j] = win[j];
+  int4 q0 = *(const int4*)my, q1 = *(const int4*)(my + 16);
+  const int8_t* mb0 = (const int8_t*)&q0;
+  const int8_t* mb1 = (const int8_t*)&q1;
+  double v[32];
+  unsigned long long m2 = 0ULL;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    const int mq = e < 16 ? (int)mb0[e] : (int)mb1[e - 16];
+    const double yq = i2d32(mq) * sbq;
+    v[e] = i2d32(tpb_field<W>(wv, e)) * sbu + yq;
+    const unsigned long long b = absbits(v[e]);
+    m2 = b > m2 ? b : m2;
+  }
+  const int En = tpb_exp_of_max(m2, W, bad);
+  const double s = En == -128 ? 0.0 : pow2(W - 1 - En);
+  uint32_t ov[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) ov[j] = 0u;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) tpb_put<W>(ov, e, rne32(v[e] * s));
+#pragma unroll
+  for (int j = 0; j < W; ++j) wout[j] = ov[j];
   return En;
 }
 

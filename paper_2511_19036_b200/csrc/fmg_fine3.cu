@@ -717,7 +717,9 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CF(P)) k_f3_cfas(const __grid
 // FIN (the last step with the thread-per-block finalisation):
 // y_k goes to a.Dv (the host points it at the Y buffer) as FP64, and
 // k_f3_tpb<1> then encodes ý, updates ú and writes w_l, u_l.
-template <int P, int J, class T, bool FIN>
+// FIN = 2 (the lean form's top level, no u_l / w_l): ý's mantissas (int8)
+// and block exponents go to a.my / a.ey; k_f3_tpb<2> updates ú from them.
+template <int P, int J, class T, int FIN>
 __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __grid_constant__ F3Args a,
                                                           const __grid_constant__ CoefT<T> cf) {
   using C = F3<P>;
@@ -914,8 +916,16 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
       const T qq = b - ay;
       const T d = fma(al, dprev, be * (f * qq));
       const T yv = yprev + d;
-      if (FIN) {
+      if (FIN == 1) {
         if (rowok) *Dp = (double)yv;  // y_k -> Y (k_f3_tpb<1> finalises)
+      } else if (FIN == 2) {  // ý = enc_{w_r}(y_k) as mantissa + exponent (k_f3_tpb<2> finalises)
+        long long mq = 0;
+        int Eq = -128;
+        warp_encode((double)yv, a.wr, nullptr, nullptr, lane, a.status, &mq, &Eq);
+        if (rowok) {
+          a.my[pbase0 + (long long)(z - tl.zs) * tplane] = (int8_t)mq;
+          if (lane == 0) a.ey[uep - a.uexp] = (int8_t)Eq;
+        }
       } else if (a.last) {
         const double yq = warp_encode((double)yv, a.wr, nullptr, nullptr, lane, a.status);
         if (rowok) {
@@ -1329,10 +1339,10 @@ __global__ void __launch_bounds__(TP_WARPS * 32, 4) k_f3_tpb(const __grid_consta
   const long long ntile = (nblk + 31) / 32;
   const long long wg = (long long)blockIdx.x * TP_WARPS + wp, nw = (long long)gridDim.x * TP_WARPS;
   const double* X = MODE == 1 ? a.Dv : a.T;
-  const int wi = MODE == 1 ? a.wu : 0, wo = MODE == 1 ? a.wu_out : a.wr;
-  uint32_t* mant = MODE == 1 ? a.umant : a.rmant;
-  int8_t* exps = MODE == 1 ? a.uexp : a.rexp;
-  const int stride = MODE == 1 ? a.ustride : a.rstride;
+  const int wi = MODE >= 1 ? a.wu : 0, wo = MODE >= 1 ? a.wu_out : a.wr;
+  uint32_t* mant = MODE >= 1 ? a.umant : a.rmant;
+  int8_t* exps = MODE >= 1 ? a.uexp : a.rexp;
+  const int stride = MODE >= 1 ? a.ustride : a.rstride;
   const unsigned mi = (unsigned)((0x100000000ULL + wi - 1) / (wi > 0 ? wi : 1));  // t / w for t < 2^16
   const unsigned mo = (unsigned)((0x100000000ULL + wo - 1) / wo);
   const double* __restrict__ Zr = a.Z;  // (read-only here)
@@ -1345,6 +1355,29 @@ __global__ void __launch_bounds__(TP_WARPS * 32, 4) k_f3_tpb(const __grid_consta
   for (long long t = wg; t < ntile; t += nw) {
     const long long b0 = bfirst + t * 32;
     const int nb = (int)(nblk - t * 32 < 32 ? nblk - t * 32 : 32);
+    if (MODE == 2) {  // ý from mantissas + exponents (k_f3_cheb FIN = 2), compile-time widths
+      for (int o = lane; o < nb * wi; o += 32) {
+        const int j = (int)__umulhi((unsigned)o, mi);
+        cpa4(wt + j * TP_WS + (o - j * wi), mant + (b0 + j) * stride + (o - j * wi));
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      const int Eu = lane < nb ? (int)exps[b0 + lane] : -128;
+      const int Ey = lane < nb ? (int)a.ey[b0 + lane] : -128;
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncwarp();
+      if (lane < nb) {
+        const int En = tpb_correct_m<(W > 0 ? W : 1), (WR > 0 ? WR : 1)>(a.my + (b0 + lane) * 32, Ey,
+                                                                            wt + lane * TP_WS, Eu, wt + lane * TP_WS, bad);
+        exps[b0 + lane] = (int8_t)En;
+      }
+      __syncwarp();
+      for (int o = lane; o < nb * wo; o += 32) {
+        const int j = (int)__umulhi((unsigned)o, mo);
+        mant[(b0 + j) * stride + (o - j * wo)] = wt[j * TP_WS + (o - j * wo)];
+      }
+      __syncwarp();
+      continue;
+    }
 #pragma unroll 8
     for (int r = 0; r < 32; ++r) cpa8(A + r * TP_RS + lane, X + (b0 + r) * 32 + lane, r < nb);
     if (MODE == 1)
@@ -1470,15 +1503,17 @@ void fine3_set_attributes() {
   cudaFuncSetAttribute(k_f3_staged<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cfas<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);    \
-  cudaFuncSetAttribute(k_f3_cheb<P, 2, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cheb<P, 3, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cheb<P, 2, double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cheb<P, 3, double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, double, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, double, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cfas<P, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);     \
-  cudaFuncSetAttribute(k_f3_cheb<P, 2, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cheb<P, 3, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cheb<P, 2, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cheb<P, 3, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 2, float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   F(1) F(2) F(3)
 #undef F
 #define TW(T_, W_, R_) \
@@ -1488,6 +1523,10 @@ void fine3_set_attributes() {
 #undef TWS
 #undef TW
   cudaFuncSetAttribute(k_f3_tpb<0, double, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
+#define TW(W_, R_) \
+  cudaFuncSetAttribute(k_f3_tpb<2, double, W_, R_>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
+  TW(4, 4) TW(6, 4) TW(6, 5) TW(8, 5) TW(8, 6) TW(10, 5) TW(14, 6) TW(5, 4) TW(8, 4)
+#undef TW
   cudaFuncSetAttribute(k_f3_tpb<0, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
   cudaFuncSetAttribute(k_f3_tpb<1, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
   cudaFuncSetAttribute(k_f3_tpb<1, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
@@ -1537,13 +1576,13 @@ template <int MODE, class T>
 static void tpb_launch(cudaStream_t st, const F3Args& a) {
   if constexpr (MODE == 0) {
     if (a.wr == 4) return tpb_launch_w<MODE, T, 0, 4>(st, a);
-  } else if (!a.wout && a.wu == a.wu_out) {
+  } else if (MODE == 2 || (!a.wout && a.wu == a.wu_out)) {
 #define TW(W_, R_) \
   if (a.wu == W_ && a.wr == R_) return tpb_launch_w<MODE, T, W_, R_>(st, a);
     TW(4, 4) TW(6, 4) TW(6, 5) TW(8, 5) TW(8, 6) TW(10, 5) TW(14, 6) TW(5, 4) TW(8, 4)
 #undef TW
   }
-  tpb_launch_w<MODE, T>(st, a);
+  if constexpr (MODE != 2) tpb_launch_w<MODE, T>(st, a);  // (MODE 2 only for the listed widths: fine3_tpby_width)
 }
 template <int MODE, class T, int W, int WR>
 static void tpb_launch_w(cudaStream_t st, const F3Args& a) {
@@ -1575,17 +1614,28 @@ static void launch_cfas_cheb(int kind, cudaStream_t st, const F3Args& a, const C
   const bool aux = a.last && (a.wout || a.uout);
   if (kind == 1) {
     f3_launch(k_f3_cfas<P, T>, n, smem_cfas<P, T>(a.wr), st, a, ct);
+  } else if (a.last && a.tpby && sizeof(T) == 8) {  // lean top level: ý mantissas, then k_f3_tpb<2>
+    if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T, 2>, n, smem_cheb<P, T>(2, a.wu, false), st, a, ct);
+    else f3_launch(k_f3_cheb<P, 3, T, 2>, n, smem_cheb<P, T>(3, a.wu, false), st, a, ct);
+    tpb_launch<2, T>(st, a);
   } else if (a.last && a.tpb) {  // y_k -> Y, then the thread-per-block finalisation
     F3Args b = a;
     b.Dv = a.Yb;
-    if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T, true>, n, smem_cheb<P, T>(2, a.wu, false), st, b, ct);
-    else f3_launch(k_f3_cheb<P, 3, T, true>, n, smem_cheb<P, T>(3, a.wu, false), st, b, ct);
+    if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T, 1>, n, smem_cheb<P, T>(2, a.wu, false), st, b, ct);
+    else f3_launch(k_f3_cheb<P, 3, T, 1>, n, smem_cheb<P, T>(3, a.wu, false), st, b, ct);
     tpb_launch<1, T>(st, b);
   } else if (a.step == 2) {
-    f3_launch(k_f3_cheb<P, 2, T, false>, n, smem_cheb<P, T>(2, a.wu, aux), st, a, ct);
+    f3_launch(k_f3_cheb<P, 2, T, 0>, n, smem_cheb<P, T>(2, a.wu, aux), st, a, ct);
   } else {
-    f3_launch(k_f3_cheb<P, 3, T, false>, n, smem_cheb<P, T>(3, a.wu, aux), st, a, ct);
+    f3_launch(k_f3_cheb<P, 3, T, 0>, n, smem_cheb<P, T>(3, a.wu, aux), st, a, ct);
   }
+}
+
+// widths k_f3_tpb<2> is compiled for (w_u = w_u', w_r <= 8: the int8 ý mantissas)
+bool fine3_tpby_width(int wu, int wr) {
+  return (wu == 4 && wr == 4) || (wu == 6 && wr == 4) || (wu == 6 && wr == 5) || (wu == 8 && wr == 5) ||
+         (wu == 8 && wr == 6) || (wu == 10 && wr == 5) || (wu == 14 && wr == 6) || (wu == 5 && wr == 4) ||
+         (wu == 8 && wr == 4);
 }
 
 // kind: 0 residual (u generated), 1 cfas (step 1), 2 Chebyshev step a.step (2 or 3), 3 prolongation,

@@ -158,6 +158,9 @@ struct F3Args {
   int csc;                   // (cFas step 1 with cfs) the Chebyshev steps are staged: write y_1
   const CUtensorMap* tmz;    // (cfs == 5, below the top level) fine boxes of the Z scratch
   double* yout;              // (k_f3_staged) where y_j goes
+  int tpby;                  // lean top level: the last step stores ý as int8 mantissas + exponents (my, ey)
+  int8_t* my;                //   per point (level window)
+  int8_t* ey;                //   per block
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.
@@ -233,6 +236,7 @@ void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, c
 void fine3_set_attributes();
 int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr);
 void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf, int fp32);
+bool fine3_tpby_width(int wu, int wr);
 void launch_coarse_nu(int dim, int p, cudaStream_t st, const void* devctx, const MArgs& a);  // nu > 1 level 0
 int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* rst, int n_ir, int lc_cap,
             KcLayout* ly, int* lc_out, int* cs_out);
