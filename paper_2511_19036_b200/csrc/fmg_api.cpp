@@ -97,6 +97,7 @@ struct fmg_ctx {
   long long tpb_min = 1LL << 16;  // levels of at least this many blocks take tpb / cfs (FMG_TPB_MIN_BLOCKS: tests)
   bool tpb0 = false;  // lean form: the generating residual's r_L encoded thread per block (k_f3_tpb<0>)
   bool tpby = false;  // lean form: the top level's last step stores ý as int8 mantissas (k_f3_tpb<2>)
+  bool s2 = false;    // staged kernels two input planes per iteration (k_f3_staged2; FMG_S2)
   int8_t* my_base = nullptr;  // (tpby) finest-window points
   int8_t* ey_base = nullptr;  // (tpby) finest-window blocks
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
@@ -727,6 +728,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.X1b = sview(c, 3, l);
   a.tmx1 = c->tm_dev + 11 * kMaxLev + l;
   a.tmz = c->tm_dev + 2 * kMaxLev + l;  // (fine boxes of the Z scratch, levels < Lmax)
+  a.s2 = c->s2;
   a.tmy = c->tm_dev + 10 * kMaxLev + l;
   if (l >= 1) a.tmcu = c->tm_dev + 6 * kMaxLev + (l - 1);
   a.zoff = c->wlo[l];
@@ -1278,6 +1280,10 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     // p = 3 (C4 145.2 -> 136.4 ms), flat for p = 1 (C3 20.35 / 20.49 ms), so
     // the default is p = 3; FMG_CSC=0/1 forces it.
     if (const char* em = getenv("FMG_TPB_MIN_BLOCKS")) c->tpb_min = atoll(em);
+    // two input planes per iteration in the staged kernels: C4 126.9 -> 120.4 ms,
+    // C3 flat (18.84 / 18.87), so the default is p = 3; FMG_S2=0/1 forces it
+    c->s2 = p == 3;
+    if (const char* e2 = getenv("FMG_S2")) c->s2 = atoi(e2) != 0;
     c->tpb0 = !(et && atoi(et) == 0);
     const char* es = getenv("FMG_CSC");
     c->csc = c->cfs && (es ? atoi(es) != 0 : p == 3);

@@ -1310,6 +1310,263 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
   }
 }
 
+// Two input planes per iteration: k_f3_staged with one
+// barrier pair per two planes and twice the independent fma chains in the x,
+// y and z passes (the single-plane kernel is latency bound: fixed-latency
+// dependences and barrier waits).  Same expressions, same order per output.
+template <int P>
+struct F3S2 {
+  static constexpr int PF = 2;              // planes staged ahead (one pair)
+  static constexpr int NBF = P + 4;         // ring slots: pair being read, pair in flight, centre planes i - P
+  static constexpr int NW = PF + 4;         // word / point slots per output
+};
+template <int P, int K>
+__global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __grid_constant__ F3Args a,
+                                                                      const __grid_constant__ CoefT<double> cf) {
+  using C = F3<P>;
+  constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX;
+  constexpr int NBF = F3S2<P>::NBF, PF = F3S2<P>::PF, NW = F3S2<P>::NW;
+  constexpr int NX_ = K == 4 ? 2 : 1;
+  extern __shared__ __align__(128) double fsm[];
+  double* ring = fsm;                     // NBF boxes of v
+  double* XA = ring + NBF * BOX;          // 2 planes x NR x 32
+  double* XB = XA + 2 * NR * 32;
+  double* aring = XB + 2 * NR * 32;       // (K >= 3) NW x NX_ x 256
+  uint32_t* wring = (uint32_t*)(aring + (K >= 3 ? NW * NX_ * 32 * FW : 0));  // (K = 2) NW x FW x (w_r + 1)
+  const int RW = a.wr + 1;
+  unsigned long long* bars = (unsigned long long*)(wring + (K == 2 ? NW * FW * RW + 2 : 0));
+  bars = (unsigned long long*)(((uintptr_t)bars + 7) & ~(uintptr_t)7);
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const F3Tile tl = f3_tile(a);
+  const Geom g = a.g;
+  const int n = g.n;
+  const int x = tl.x0 + lane, y = tl.y0 + w;
+  const bool rowok = y < g.NY;
+  const int tx = x % P, ty = y % P;
+  double km[R], kk[R];
+#pragma unroll
+  for (int o = 0; o < R; ++o) {
+    km[o] = cf.Mc[tx][o];
+    kk[o] = cf.Kc[tx][o];
+  }
+  const double hl = pow2(-(a.l + 1));
+  const double* __restrict__ gt = a.gtab;
+  const bool uxy = unk1(x, n) && unk1(y, n);
+  const double gxy = K < 2 && uxy ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
+  double fv[P];
+#pragma unroll
+  for (int t = 0; t < P; ++t) fv[t] = uxy ? cf.invd[(t * P + ty) * P + tx] * pow2(a.l + 1) : 0.0;
+  const double al = cf.cal[K - 2 > 0 ? K - 2 : 0], be = cf.cbe[K - 2 > 0 ? K - 2 : 0], ith = cf.inv_theta;
+  const int nxb = g.NX >> 5;
+  const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
+  const long long tplane = (long long)g.NY * g.NX, bpp = (long long)g.NY * nxb;
+  const long long pbase0 = ((long long)tl.zs * g.NY + y) * g.NX + x;
+  double* Tp = a.T + pbase0;
+  double* Yo = a.yout ? a.yout + pbase0 : nullptr;
+  double* Dp = a.Dv + pbase0;
+  const long long blk0 = ((long long)tl.zs * g.NY + y) * nxb + (tl.x0 >> 5);
+  uint32_t* rmp = a.rmant + blk0 * a.rstride;
+  int8_t* rep = a.rexp + blk0;
+  const long long rstep = bpp * a.rstride;
+  const unsigned ring_s = smem_u32(ring), bars_s = smem_u32(bars), wring_s = smem_u32(wring);
+  const unsigned aring_s = smem_u32(aring);
+  const int tid = w * 32 + lane;
+  const int nout = tl.ze - tl.zs;
+  int eoff = 0;
+  const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, a.wr, g, tl.x0, y, tl.zs, w * RW, K == 2 && rowok, lane,
+                              eoff);
+  auto pcopy = [&](int j, int slot) {
+    if (K >= 3 && rowok) {
+      const unsigned d = aring_s + (unsigned)(((slot * NX_) * 32 * FW + tid) * 8);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(a.T + pbase0 + j * tplane) : "memory");
+      if (K == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 32 * FW * 8), "l"(a.Dv + pbase0 + j * tplane)
+                     : "memory");
+    }
+  };
+  auto ocopy = [&](int j, int slot) {  // words (K = 2) / point values (K >= 3) of output plane zs + j
+    if (j < nout) {
+      if (K == 2) wcopy(ws, wring_s + (unsigned)(slot * FW * RW * 4), j);
+      else if (K >= 3) pcopy(j, slot);
+    }
+  };
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < NBF; ++k) mbar_init(bars + k, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const int tmx = tl.x0 - P - (P & 1), tmy = tl.y0 - P;
+  auto stage = [&](int i, int slot) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      const unsigned dst = ring_s + (unsigned)(slot * BOX * 8), bar = bars_s + (unsigned)(slot * 8);
+      fence_async_smem();
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(BOX * 8))
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];" ::"r"(dst),
+          "l"((unsigned long long)a.tmb), "r"(tmx), "r"(tmy), "r"(z0 + i - a.zoff), "r"(bar)
+          : "memory");
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < PF; ++i)
+    if (i < nin) stage(i, i);
+  if (K >= 2) {  // outputs 0, 1 -> slots 0, 1 (one group)
+    ocopy(0, 0);
+    ocopy(1, 1);
+    cpa_commit();
+  }
+  double cr[R + 1], sr[R + 1];
+#pragma unroll
+  for (int o = 0; o <= R; ++o) cr[o] = sr[o] = 0.0;
+  double ss = 0.0;
+  int tz = ((z0 % P) + P) % P;           // node type of input plane i (= of output plane i - P)
+  int isl = 0, osl = 0, oisl = NBF - P;  // slots: input plane i, words / points of output i - 2P, input plane i - P
+  unsigned par = 0;                      // barrier phase of slot isl
+  auto emit = [&](int z, double av, int tzo, int ois, int os) {  // the output at plane z
+    const bool uz = unk1(z, n);
+    if (K >= 3) {
+      if (rowok) {
+        const double* ax = aring + os * NX_ * 32 * FW + tid;
+        const double b = ax[0];
+        double f = fv[0];
+#pragma unroll
+        for (int t = 1; t < P; ++t) f = tzo == t ? fv[t] : f;
+        f = uz ? f : 0.0;
+        const double yprev = ring[ois * BOX + C::SH + (w + P) * RS + P + lane];
+        const double dprev = K == 4 ? ax[32 * FW] : yprev;
+        const double qq = b - av;
+        const double d = fma(al, dprev, be * (f * qq));
+        const double yv = yprev + d;
+        *Yo = yv;
+        if (!a.last) *Dp = d;
+      }
+      Yo += tplane;
+      Dp += tplane;
+    } else if (K == 2) {
+      if (rowok) {
+        const uint32_t* rec = wring + os * FW * RW + w * RW;
+        const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
+        const double b = rv - av;
+        *Tp = b;
+        if (Yo) {
+          double f = fv[0];
+#pragma unroll
+          for (int t = 1; t < P; ++t) f = tzo == t ? fv[t] : f;
+          *Yo = ith * ((uz ? f : 0.0) * b);
+        }
+      }
+      if (Yo) Yo += tplane;
+    } else if (rowok) {
+      const double gz = uz ? gt[z] : 0.0;
+      const double t = (uxy && uz) ? gxy * gz - av : 0.0;
+      *Tp = t;
+      ss = fma(t, t, ss);
+      if (K == 0) warp_encode(t, a.wr, rmp, rep, lane, a.status);
+    }
+    Tp += tplane;
+    rmp += rstep;
+    rep += bpp;
+  };
+  for (int i = 0; i < nin; i += 2) {
+    const bool two = i + 1 < nin;
+    const int isl1 = isl + 1 == NBF ? 0 : isl + 1;
+    const unsigned par1 = isl + 1 == NBF ? par ^ 1u : par;
+    mbar_wait_s(bars_s + 8u * (unsigned)isl, par);
+    if (two) mbar_wait_s(bars_s + 8u * (unsigned)isl1, par1);
+    if (K >= 2) cpa_wait<0>();
+    __syncthreads();  // every thread is past the previous pair (slots, XA/XB, output slots)
+    {
+      int s2 = isl + PF;
+      s2 = s2 >= NBF ? s2 - NBF : s2;
+      if (i + PF < nin) stage(i + PF, s2);
+      if (i + PF + 1 < nin) stage(i + PF + 1, s2 + 1 == NBF ? 0 : s2 + 1);
+    }
+    if (K >= 2) {  // the outputs of the next pair (outputs start at i = 2P, even)
+      if (i >= 2 * P) {
+        const int j = i - 2 * P + PF;
+        int sl = osl + PF;
+        sl = sl >= NW ? sl - NW : sl;
+        ocopy(j, sl);
+        ocopy(j + 1, sl + 1 == NW ? 0 : sl + 1);
+      }
+      cpa_commit();
+    }
+    // x pass of both planes: rows w, w + 8 of each (four independent pairs of chains)
+    {
+      const double* b0 = ring + isl * BOX + C::SH;
+      const double* b1 = ring + isl1 * BOX + C::SH;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int r = w + k * FW;
+        if (r < NR) {
+          double s0 = 0, t0 = 0, s1 = 0, t1 = 0;
+#pragma unroll
+          for (int o = 0; o < R; ++o) {
+            const double v0 = b0[r * RS + lane + o];
+            s0 = fma(km[o], v0, s0);
+            t0 = fma(kk[o], v0, t0);
+            if (two) {
+              const double v1 = b1[r * RS + lane + o];
+              s1 = fma(km[o], v1, s1);
+              t1 = fma(kk[o], v1, t1);
+            }
+          }
+          XA[r * 32 + lane] = s0;
+          XB[r * 32 + lane] = t0;
+          XA[(NR + r) * 32 + lane] = s1;
+          XB[(NR + r) * 32 + lane] = t1;
+        }
+      }
+    }
+    __syncthreads();
+    double c0, s0, c1 = 0.0, s1 = 0.0;
+    ypass<P>(cf, ty, XA, XB, w, lane, c0, s0);
+    if (two) ypass<P>(cf, ty, XA + NR * 32, XB + NR * 32, w, lane, c1, s1);
+#pragma unroll
+    for (int o = 0; o < R - 1; ++o) {
+      cr[o] = cr[o + 2];
+      sr[o] = sr[o + 2];
+    }
+    cr[R - 1] = c0;
+    sr[R - 1] = s0;
+    cr[R] = c1;
+    sr[R] = s1;
+    // (ring: cr[k] = plane i + 1 - R + k; output of plane i uses cr[0..R-1], of plane i + 1 cr[1..R])
+    const int tz1 = tz + 1 == P ? 0 : tz + 1;
+    const int oisl1 = oisl + 1 == NBF ? 0 : oisl + 1;
+    const int osl1 = osl + 1 == NW ? 0 : osl + 1;
+    if (i >= 2 * P) {
+      const double av0 = zpass<P>(cf, tz, cr, sr) * hl;
+      if (two) {
+        const double av1 = zpass<P>(cf, tz1, cr + 1, sr + 1) * hl;
+        emit(z0 + i - P, av0, tz, oisl, osl);
+        emit(z0 + i + 1 - P, av1, tz1, oisl1, osl1);
+      } else {
+        emit(z0 + i - P, av0, tz, oisl, osl);
+      }
+      osl = osl1 + 1 == NW ? 0 : osl1 + 1;
+    } else if (two && i + 1 >= 2 * P) {
+      const double av1 = zpass<P>(cf, tz1, cr + 1, sr + 1) * hl;
+      emit(z0 + i + 1 - P, av1, tz1, oisl1, osl);
+      osl = osl1;
+    }
+    tz = tz1 + 1 == P ? 0 : tz1 + 1;
+    oisl = oisl1 + 1 == NBF ? 0 : oisl1 + 1;
+    isl = isl1 + 1 == NBF ? 0 : isl1 + 1;
+    par = (isl1 + 1 == NBF) ? par1 ^ 1u : par1;
+  }
+  if (K < 2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+    if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)tl.cta * FW + w] = ss;
+  }
+}
+
 // Thread-per-block epilogues: the BFP codec of the
 // finest-level kernels' outputs moved out of the plane march, where the
 // warp-cooperative codec (a block is one 32-point row) cost ~40 % of the last
@@ -1468,7 +1725,24 @@ static int smem_cheb(int J, int wu, bool aux) {
 }
 
 template <int P>
-static int smem_staged(int wr, int nx = 0) {  // (wr > 0: the r_L word ring of K = 2; nx: point arrays of K >= 3)
+static int smem_staged2(int wr, int nx);
+template <int P>
+static int smem_staged(int wr, int nx);
+// k_f3_staged (one plane per iteration) or k_f3_staged2 (two; F3Args::s2)
+template <int P, int K>
+static void staged_launch(cudaStream_t st, const F3Args& a, const CoefT<double>& ct, int wr, int nx) {
+  if (a.s2) f3_launch(k_f3_staged2<P, K>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
+  else f3_launch(k_f3_staged<P, K>, a.nitems, smem_staged<P>(wr, nx), st, a, ct);
+}
+template <int P>
+static int smem_staged2(int wr, int nx) {
+  using C = F3<P>;
+  const size_t wb = wr > 0 ? (size_t)F3S2<P>::NW * FW * (wr + 1) * 4 + 8 : 0;
+  const size_t xb = (size_t)F3S2<P>::NW * nx * 32 * FW * 8;
+  return (int)(((size_t)F3S2<P>::NBF * C::BOX + 4 * C::NR * 32) * 8 + xb + wb + 8 * F3S2<P>::NBF + 16);
+}
+template <int P>
+static int smem_staged(int wr, int nx) {  // (wr > 0: the r_L word ring of K = 2; nx: point arrays of K >= 3)
   using C = F3<P>;
   const size_t wb = wr > 0 ? (size_t)C::NW * FW * (wr + 1) * 4 + 8 : 0;
   const size_t xb = (size_t)C::NW * nx * 32 * FW * 8;
@@ -1498,6 +1772,11 @@ void fine3_set_attributes() {
   cudaFuncSetAttribute(k_f3_prolong<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
   cudaFuncSetAttribute(k_f3_prolong<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
   cudaFuncSetAttribute(k_f3_staged<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged2<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged2<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged2<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged2<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged2<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -1649,8 +1928,8 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
     b.tmb = j2 ? a.tmx1 : a.tmy;     // y_1 in X1 / y_2 in Y
     b.yout = j2 ? a.Yb : a.X1b;      // y_2 -> Y, y_3 -> X1
 #define ST(PP)                                                                                              \
-  if (j2) f3_launch(k_f3_staged<PP, 3>, a.nitems, smem_staged<PP>(0, 1), st, b, ct);                      \
-  else f3_launch(k_f3_staged<PP, 4>, a.nitems, smem_staged<PP>(0, 2), st, b, ct);
+  if (j2) staged_launch<PP, 3>(st, b, ct, 0, 1);                      \
+  else staged_launch<PP, 4>(st, b, ct, 0, 2);
     if (p == 1) {
       ST(1)
     } else if (p == 2) {
@@ -1669,15 +1948,15 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
   if (kind == 4) {  // residual with u_L staged (materialised form)
     const CoefT<double> ct = coefs_as<double>(cf);
     if (a.tpb) {  // r_L encoded afterwards, thread per block
-      if (p == 1) f3_launch(k_f3_staged<1, 1>, a.nitems, smem_staged<1>(0), st, a, ct);
-      else if (p == 2) f3_launch(k_f3_staged<2, 1>, a.nitems, smem_staged<2>(0), st, a, ct);
-      else f3_launch(k_f3_staged<3, 1>, a.nitems, smem_staged<3>(0), st, a, ct);
+      if (p == 1) staged_launch<1, 1>(st, a, ct, 0, 0);
+      else if (p == 2) staged_launch<2, 1>(st, a, ct, 0, 0);
+      else staged_launch<3, 1>(st, a, ct, 0, 0);
       tpb_launch<0, double>(st, a);
       return;
     }
-    if (p == 1) f3_launch(k_f3_staged<1, 0>, a.nitems, smem_staged<1>(0), st, a, ct);
-    else if (p == 2) f3_launch(k_f3_staged<2, 0>, a.nitems, smem_staged<2>(0), st, a, ct);
-    else f3_launch(k_f3_staged<3, 0>, a.nitems, smem_staged<3>(0), st, a, ct);
+    if (p == 1) staged_launch<1, 0>(st, a, ct, 0, 0);
+    else if (p == 2) staged_launch<2, 0>(st, a, ct, 0, 0);
+    else staged_launch<3, 0>(st, a, ct, 0, 0);
     return;
   }
   if (kind == 3) {  // P u_{l-1} (step 0) or u_l = dec ú_l + P u_{l-1} (step 1) at the tile points
@@ -1720,7 +1999,7 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
 #define PRO(PP)                                                                                          \
   if (na == 2) f3_launch(k_f3_prolong<PP, 2>, a.nitems, smem_prolong<PP>(a.wu, 2), st, b, ct);         \
   else f3_launch(k_f3_prolong<PP, 1>, a.nitems, smem_prolong<PP>(a.wu), st, b, ct);                    \
-  f3_launch(k_f3_staged<PP, 2>, a.nitems, smem_staged<PP>(a.wr), st, b, ct);
+  staged_launch<PP, 2>(st, b, ct, a.wr, 0);
     if (p == 1) {
       PRO(1)
     } else if (p == 2) {

@@ -158,6 +158,7 @@ struct F3Args {
   int csc;                   // (cFas step 1 with cfs) the Chebyshev steps are staged: write y_1
   const CUtensorMap* tmz;    // (cfs == 5, below the top level) fine boxes of the Z scratch
   double* yout;              // (k_f3_staged) where y_j goes
+  int s2;                    // k_f3_staged2 (two input planes per iteration) instead of k_f3_staged
   int tpby;                  // lean top level: the last step stores ý as int8 mantissas + exponents (my, ey)
   int8_t* my;                //   per point (level window)
   int8_t* ey;                //   per block

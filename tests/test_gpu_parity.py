@@ -432,7 +432,8 @@ def test_fp32_cfas_refused_outside_its_path(P):
 # materialised z_l for cFas step 1 (top and lower levels), the staged
 # Chebyshev steps for every p, and each switched off in turn.
 _F3_VARIANTS = {
-    "all": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="1", FMG_CSC="1"),
+    "all": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="1", FMG_CSC="1", FMG_S2="1"),
+    "all_s1": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="1", FMG_CSC="1", FMG_S2="0"),
     "no_csc": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="1", FMG_CSC="0"),
     "no_cfs": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="0"),
     "fused_codec": dict(FMG_F3MAT="1", FMG_TPB="0"),
