@@ -80,7 +80,8 @@ struct fmg_ctx {
   // finest-level kernels (fmg_fine3.cu): coarse boxes of u_l / w_l, fine boxes
   // of t_l (= b_l) and of the Chebyshev direction
   CUtensorMap tmCU[kMaxLev]{}, tmCW[kMaxLev]{}, tmFB[kMaxLev]{}, tmFD[kMaxLev]{}, tmYB[kMaxLev]{}, tmX1[kMaxLev]{};
-  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3 | CU | CW | FB | FD | YB | X1] x kMaxLev
+  CUtensorMap tmCH[kMaxLev]{};
+  CUtensorMap* tm_dev = nullptr;  // device copy: [U | T | B0..B3 | CU | CW | FB | FD | YB | X1 | CH] x kMaxLev
   // 3D, one GPU, Chebyshev degree 2-3, nu = 1: level L of each FMG level runs
   // the finest-level kernels and keeps no u_L, z_L, P u_{L-1}, w_L or y arrays
   // (DESIGN.md §4.3); the level arrays of l = Lmax that remain are t (= b)
@@ -98,6 +99,9 @@ struct fmg_ctx {
   bool tpb0 = false;  // lean form: the generating residual's r_L encoded thread per block (k_f3_tpb<0>)
   bool tpby = false;  // lean form: the top level's last step stores ý as int8 mantissas (k_f3_tpb<2>)
   bool s2 = false;    // staged kernels two input planes per iteration (k_f3_staged2; FMG_S2)
+  bool chk = false;   // lean form in z chunks: u_L / z_L materialised chunk by chunk (FMG_CHK)
+  int chk_rc = 0;     // planes per chunk
+  double* chkbuf = nullptr;
   int8_t* my_base = nullptr;  // (tpby) finest-window points
   int8_t* ey_base = nullptr;  // (tpby) finest-window blocks
   int nccl_err = 0;               // an NCCL call of the last issue failed (reported by the solve)
@@ -205,8 +209,8 @@ struct Builder {
   std::vector<NormEntry> norms;
   long long ptot = 0;  // (set past the KC partial region by make_builder)
   // reserve partial slots for (row, level l) and record the deferred norm
-  long long slot(int row, int l) {
-    int nt = c->dim == 2 ? c->mitems[l] : c->mitems[l] * march3_rows();
+  long long slot(int row, int l, long long items = -1) {
+    int nt = c->dim == 2 ? c->mitems[l] : (int)((items >= 0 ? items : c->mitems[l]) * march3_rows());
     long long off = ptot;
     ptot += nt;
     NormEntry e{off, row, l, nt, 0};
@@ -313,6 +317,7 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
     q.wout = q.last && !top;
     q.uout = q.last && uout;
     q.cfs = !cfs ? 0 : step == 1 ? (!top ? 5 : uout ? 2 : 1) : (c->csc ? 3 : 0);
+    if (!cfs && step == 1 && top && c->chk && !c->f3mat && !c->s.cfas_fp32) q.cfs = 6;  // (lean, z chunks)
     b.fine(step == 1 ? 1 : 2, q, (fine && top) ? (step == k ? 5 : 1) : -1);
   }
 }
@@ -364,7 +369,15 @@ void build_iteration_nu(Builder& b, int L, int it) {
     o.wu_in = c->wu_cur[L];
     o.row = row;
     o.poff = b.slot(row, L);
-    if (c->fine3) b.fine(c->f3mat ? 4 : 0, o, fine ? 0 : -1);  // u_L generated on chip / staged (fmg_fine3.cu)
+    if (c->fine3 && !c->f3mat && c->chk && L >= 1) {  // (lean, z chunks: one partial row of CTAs per chunk)
+      b.norms.pop_back();
+      b.ptot = o.poff;
+      const int nch = (c->g[L].n + c->chk_rc - 1) / c->chk_rc;
+      o.poff = b.slot(row, L, (long long)(c->g[L].NX / 32) * c->mnyb[L] * nch);
+      b.fine(5, o, fine ? 0 : -1);
+    } else if (c->fine3) {
+      b.fine(c->f3mat ? 4 : 0, o, fine ? 0 : -1);  // u_L generated on chip / staged (fmg_fine3.cu)
+    }
     else b.grid(o, fine ? 0 : -1);
   }
   for (int l = L - 1; l >= 0; --l) {
@@ -713,7 +726,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   // (levels of >= 2^16 blocks: below that the extra launch costs more than the
   // warp-cooperative codec it replaces)
   // (the residual's r_L encode needs no extra array: the lean form takes it too)
-  a.tpb = (c->tpb ? (it.f3kind == 2 || it.f3kind == 4) : (it.f3kind == 0 && c->tpb0)) && a.wu <= 32 &&
+  a.tpb = (c->tpb ? (it.f3kind == 2 || it.f3kind == 4) : ((it.f3kind == 0 || it.f3kind == 5) && c->tpb0)) && a.wu <= 32 &&
           a.wu_out <= 32 && a.wr <= 32 && (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= c->tpb_min;
   a.Yb = sview(c, 2, l);
   {
@@ -729,6 +742,9 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.tmx1 = c->tm_dev + 11 * kMaxLev + l;
   a.tmz = c->tm_dev + 2 * kMaxLev + l;  // (fine boxes of the Z scratch, levels < Lmax)
   a.s2 = c->s2;
+  a.chk = c->chkbuf;
+  a.chkrc = c->chk_rc;
+  a.tmch = c->tm_dev + 12 * kMaxLev + l;
   a.tmy = c->tm_dev + 10 * kMaxLev + l;
   if (l >= 1) a.tmcu = c->tm_dev + 6 * kMaxLev + (l - 1);
   a.zoff = c->wlo[l];
@@ -737,7 +753,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.poff = o.poff;
   a.status = c->status;
   const CUtensorMap* base = c->tm_dev;
-  if (l >= 1) a.tmc = base + (it.f3kind == 0 || it.f3kind == 3 ? 6 : 7) * kMaxLev + (l - 1);
+  if (l >= 1) a.tmc = base + (it.f3kind == 0 || it.f3kind == 3 || it.f3kind == 5 ? 6 : 7) * kMaxLev + (l - 1);
   a.tmb = base + (it.f3kind == 4 ? 0 : 8) * kMaxLev + l;  // (kind 4: the u_l boxes)
   a.tmd = base + 9 * kMaxLev + l;
   return a;
@@ -1335,6 +1351,28 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       c->tpby = c->my_base && c->ey_base;
     }
   }
+  // lean form on one GPU: the finest level's u_L (residual) and z_L (cFas
+  // step 1) materialised in z chunks of chk_rc planes (+ the 2p halo) for the
+  // staged kernels, instead of generated on every staged box (FMG_CHK=0:
+  // generating kernels).  The buffer takes at most a quarter of the free memory
+  // and 8 GB.
+  if (rc == FMG_OK && c->fine3 && !c->f3mat && c->G == 1 && s->smoother == 0 &&
+      !(getenv("FMG_CHK") && atoi(getenv("FMG_CHK")) == 0)) {
+    const long long plane = (long long)c->g[Lmax].NX * c->g[Lmax].NY;
+    size_t freeb = 0, totalb = 0;
+    cudaMemGetInfo(&freeb, &totalb);
+    const double budget = std::min((double)freeb / 4.0, 8.0 * (1 << 30));
+    long long rcz = (long long)(budget / (8.0 * plane)) - 2 * p;
+    if (const char* er = getenv("FMG_CHK_PLANES")) rcz = atoll(er);
+    rcz = std::min<long long>(rcz, c->g[Lmax].n);
+    if (rcz >= 8) {
+      c->chkbuf = (double*)dalloc(c, sizeof(double) * plane * (rcz + 2 * p));
+      if (c->chkbuf) {
+        c->chk = true;
+        c->chk_rc = (int)rcz;
+      }
+    }
+  }
   if (rc == FMG_OK && s->nu > 1) {  // YO: dec ý of the previous cycle at the level being smoothed
     c->buf[8] = (double*)dalloc(c, sizeof(double) * c->g[Lmax].size);
     if (!c->buf[8]) rc = FMG_ENOMEM;
@@ -1405,11 +1443,12 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->sbase[4], g.NX, g.NY, nz, rs, nr);
       if (c->cfs) ok &= make_tmap(&c->tmYB[l], c->sbase[2], g.NX, g.NY, nz, rs, nr);
       if (c->csc) ok &= make_tmap(&c->tmX1[l], c->sbase[3], g.NX, g.NY, nz, rs, nr);
+      if (c->chk) ok &= make_tmap(&c->tmCH[l], c->chkbuf, g.NX, g.NY, std::min<long long>(g.NZ, c->chk_rc + 2 * p), rs, nr);
     }
     if (!ok) rc = FMG_ECUDA;
   }
   if (rc == FMG_OK && (c->tma || c->fine3)) {
-    std::vector<CUtensorMap> all(12 * kMaxLev);
+    std::vector<CUtensorMap> all(13 * kMaxLev);
     for (int l = 0; l < kMaxLev; ++l) {
       all[l] = c->tmU[l];
       all[kMaxLev + l] = c->tmT[l];
@@ -1420,6 +1459,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       all[9 * kMaxLev + l] = c->tmFD[l];
       all[10 * kMaxLev + l] = c->tmYB[l];
       all[11 * kMaxLev + l] = c->tmX1[l];
+      all[12 * kMaxLev + l] = c->tmCH[l];
     }
     c->tm_dev = (CUtensorMap*)dalloc(c, sizeof(CUtensorMap) * all.size());  // (256-byte aligned)
     if (!c->tm_dev) rc = FMG_ENOMEM;

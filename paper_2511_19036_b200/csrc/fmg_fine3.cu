@@ -1306,7 +1306,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
   if (K < 2) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
-    if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)tl.cta * FW + w] = ss;
+    if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)(a.ctaoff + tl.cta) * FW + w] = ss;
   }
 }
 
@@ -1563,7 +1563,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __g
   if (K < 2) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
-    if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)tl.cta * FW + w] = ss;
+    if (lane == 0 && a.poff >= 0) a.pbase[a.poff + (long long)(a.ctaoff + tl.cta) * FW + w] = ss;
   }
 }
 
@@ -1943,6 +1943,56 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
       t.Dv = b.yout;
       tpb_launch<1, double>(st, t);
     }
+    return;
+  }
+  if (kind == 5 || (kind == 1 && a.cfs == 6)) {  // lean form in z chunks: u_L / z_L
+    // materialised chunk by chunk in a.chk (a.chkrc planes + the 2P halo), then the staged kernel on it
+    const CoefT<double> ct = coefs_as<double>(cf);
+    const int n = a.g.n, P_ = p, rc = a.chkrc;
+    const long long plane = (long long)a.g.NY * a.g.NX;
+    const int tiles = a.nxb * a.nyb;
+    int ci = 0;
+    for (int za = a.zlo; za < a.zhi; za += rc, ++ci) {
+      const int zb = std::min(a.zhi, za + rc), lo = std::max(0, za - P_), hi = std::min(n, zb + P_);
+      F3Args g_ = a;  // generation: u_L = dec ú_L + P u_{L-1} (kind 5) / z_L = P w_{L-1} (cFas) over [lo, hi)
+      g_.step = kind == 5 ? 1 : 0;
+      g_.zlo = lo;
+      g_.zhi = hi;
+      g_.RC = hi - lo;
+      g_.nitems = tiles;
+      g_.U = a.chk - plane * lo;
+      g_.PU = a.chk - plane * lo;
+      F3Args s_ = a;  // the staged sweep over [za, zb)
+      s_.zlo = za;
+      s_.zhi = zb;
+      s_.RC = zb - za;
+      s_.nitems = tiles;
+      s_.tmb = a.tmch;
+      s_.zoff = lo;
+      s_.ctaoff = ci * tiles;
+      s_.yout = nullptr;
+#define CH(PP)                                                                                   \
+  f3_launch(k_f3_prolong<PP, 1>, tiles, smem_prolong<PP>(a.wu), st, g_, ct);                    \
+  if (kind == 5) {                                                                               \
+    if (a.tpb) staged_launch<PP, 1>(st, s_, ct, 0, 0);                                           \
+    else staged_launch<PP, 0>(st, s_, ct, 0, 0);                                                 \
+  } else {                                                                                       \
+    staged_launch<PP, 2>(st, s_, ct, a.wr, 0);                                                   \
+  }
+      // (the planes past the level, up to zb + P, read as zero: the map's extent
+      // is the buffer's, so clear them where the chunk ends at the level's end)
+      if (zb + P_ > hi)
+        cudaMemsetAsync(a.chk + (long long)(hi - lo) * plane, 0, sizeof(double) * plane * (zb + P_ - hi), st);
+      if (p == 1) {
+        CH(1)
+      } else if (p == 2) {
+        CH(2)
+      } else {
+        CH(3)
+      }
+#undef CH
+    }
+    if (kind == 5 && a.tpb) tpb_launch<0, double>(st, a);
     return;
   }
   if (kind == 4) {  // residual with u_L staged (materialised form)

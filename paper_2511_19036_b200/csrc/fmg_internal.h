@@ -159,6 +159,10 @@ struct F3Args {
   const CUtensorMap* tmz;    // (cfs == 5, below the top level) fine boxes of the Z scratch
   double* yout;              // (k_f3_staged) where y_j goes
   int s2;                    // k_f3_staged2 (two input planes per iteration) instead of k_f3_staged
+  int ctaoff;                // (k_f3_staged) first norm-partial CTA index of this launch (z chunks)
+  double* chk;               // lean form in z chunks: the chunk buffer (a.chkrc + 2P planes)
+  int chkrc;
+  const CUtensorMap* tmch;   // fine boxes of the chunk buffer
   int tpby;                  // lean top level: the last step stores ý as int8 mantissas + exponents (my, ey)
   int8_t* my;                //   per point (level window)
   int8_t* ey;                //   per block

@@ -438,6 +438,8 @@ _F3_VARIANTS = {
     "no_cfs": dict(FMG_F3MAT="1", FMG_TPB="1", FMG_CFS="0"),
     "fused_codec": dict(FMG_F3MAT="1", FMG_TPB="0"),
     "lean": dict(FMG_F3MAT="0"),
+    "lean_chunks8": dict(FMG_F3MAT="0", FMG_CHK="1", FMG_CHK_PLANES="8"),
+    "lean_nochunk": dict(FMG_F3MAT="0", FMG_CHK="0"),
     "lean_no_tpby": dict(FMG_F3MAT="0", FMG_TPBY="0"),
     "lean_fused": dict(FMG_F3MAT="0", FMG_TPB="0", FMG_TPBY="0"),
 }
