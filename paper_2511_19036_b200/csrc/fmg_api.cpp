@@ -742,6 +742,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
   a.tmx1 = c->tm_dev + 11 * kMaxLev + l;
   a.tmz = c->tm_dev + 2 * kMaxLev + l;  // (fine boxes of the Z scratch, levels < Lmax)
   a.s2 = c->s2;
+  a.pr2 = !(getenv("FMG_PR2") && atoi(getenv("FMG_PR2")) == 0);
   a.chk = c->chkbuf;
   a.chkrc = c->chk_rc;
   a.tmch = c->tm_dev + 12 * kMaxLev + l;

@@ -1098,6 +1098,179 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
   }
 }
 
+// k_f3_prolong with 32 x 16 tiles: each warp produces fine rows y0 + w and
+// y0 + w + 8 (two independent chains in the y and z passes, half the barriers
+// per point).  p = 1, 3 (the coarse box covers 16 fine rows there).  Same
+// passes and order as k_f3_prolong.
+template <int P, int NA>
+__global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constant__ F3Args a,
+                                                             const __grid_constant__ CoefT<double> cf) {
+  using C = F3<P>;
+  constexpr int CBX = C::CBX, CBY = C::CBY, NCB = C::NCB, NCY = C::NCY, PF = C::PF, NW = C::NW, TH = 2 * FW;
+  extern __shared__ __align__(128) double fsm[];
+  double* craw = fsm;                          // NA x NCB coarse boxes (TMA)
+  double* PX = craw + NA * NCB * C::CBS;       // NA x CBY x 32: x pass
+  double* yv = PX + NA * CBY * 32;             // NA x NCY x TH x 32
+  uint32_t* wring = (uint32_t*)(yv + NA * NCY * TH * 32);  // NW x TH x (w + 1): ú words (decode mode)
+  const int RW = a.wu + 1;
+  unsigned long long* cbar = (unsigned long long*)(wring + NW * TH * RW + 2);
+  cbar = (unsigned long long*)(((uintptr_t)cbar + 7) & ~(uintptr_t)7);
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const Geom g = a.g;
+  const int n = g.n;
+  // tile: 32 x 16 columns, z chunk of a.RC planes (a.nyb: tile rows of 16)
+  F3Tile tl;
+  {
+    const int tiles = a.nxb * a.nyb, q = blockIdx.x % tiles, ch = blockIdx.x / tiles;
+    tl.x0 = (q % a.nxb) * 32;
+    tl.y0 = (q / a.nxb) * TH;
+    tl.zs = a.zlo + ch * a.RC;
+    tl.ze = min(a.zhi, tl.zs + a.RC);
+    tl.cta = blockIdx.x;
+  }
+  const int x = tl.x0 + lane;
+  const bool okx = unk1(x, n);
+  Gen<P> gn;
+  gn.cx0 = (P * (max(tl.x0 - P, 1) / (2 * P))) & ~1;
+  gn.cy0 = P * (max(tl.y0 - P, 1) / (2 * P));
+  gn.czoff = a.czoff;
+  gen_range<P>(gn, tl.zs, tl.ze - tl.zs, n);
+  const int bxo = okx ? P * (x / (2 * P)) - gn.cx0 : 0, rx = okx ? x % (2 * P) : 0;
+  double pwx[P + 1];
+#pragma unroll
+  for (int t = 0; t <= P; ++t) pwx[t] = cf.Pw[rx][t];
+  int byo[2], ry[2];
+  bool oky[2], rowok[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int y = tl.y0 + w + h * FW;
+    rowok[h] = y < g.NY;
+    oky[h] = unk1(y, n);
+    byo[h] = oky[h] ? P * (y / (2 * P)) - gn.cy0 : 0;
+    ry[h] = oky[h] ? y % (2 * P) : 0;
+  }
+  const bool decode = NA == 1 && a.step == 1;
+  int eoff[2] = {0, 0};
+  const WStream ws0 = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, tl.y0 + w, tl.zs, w * RW,
+                               rowok[0] && decode, lane, eoff[0]);
+  const WStream ws1 = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, tl.y0 + w + FW, tl.zs, (w + FW) * RW,
+                               rowok[1] && decode, lane, eoff[1]);
+  const unsigned wring_s = smem_u32(wring);
+  const long long tplane = (long long)g.NY * g.NX;
+  const long long o0 = ((long long)tl.zs * g.NY + tl.y0 + w) * g.NX + x;
+  double* out = (decode ? a.U : a.PU) + o0;
+  double* out2 = NA == 2 ? a.out2 + o0 : nullptr;
+  const long long rs8 = (long long)FW * g.NX;  // the second row, 8 rows down
+  const CUtensorMap* tms[2] = {a.tmc, NA == 2 ? a.tmc2 : a.tmc};
+  const int nout = tl.ze - tl.zs;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int k = 0; k < NA * NCB; ++k) mbar_init(cbar + k, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    for (int q = 0; q < NA; ++q)
+      for (int k = 0; k < NCB; ++k)
+        gen_request<P>(gn, tms[q], craw + q * NCB * C::CBS, cbar + q * NCB, gn.cfirst + k);
+#pragma unroll
+  for (int j = 0; j < PF; ++j) {
+    if (j < nout) {
+      wcopy(ws0, wring_s + (unsigned)(j * TH * RW * 4), j);
+      wcopy(ws1, wring_s + (unsigned)(j * TH * RW * 4), j);
+    }
+    cpa_commit();
+  }
+  int osl = 0;
+  for (int j = 0; j < nout; ++j) {
+    const int z = tl.zs + j;
+    {
+      const int sl = osl + PF >= NW ? osl + PF - NW : osl + PF;
+      if (j + PF < nout) {
+        wcopy(ws0, wring_s + (unsigned)(sl * TH * RW * 4), j + PF);
+        wcopy(ws1, wring_s + (unsigned)(sl * TH * RW * 4), j + PF);
+      }
+    }
+    cpa_commit();
+    const bool okz = unk1(z, n);
+    if (okz) {
+      const int cneed = cbase<P>(z) + P;
+      while (gn.cdone <= cneed) {
+        const int c = gn.cdone, k = c - gn.cfirst;
+#pragma unroll
+        for (int q = 0; q < NA; ++q) {
+          mbar_wait_s(smem_u32(cbar + q * NCB) + 8u * (unsigned)(k % NCB), (unsigned)(k / NCB) & 1u);
+          const double* cb = craw + (q * NCB + k % NCB) * C::CBS;
+#pragma unroll
+          for (int r = 0; r < (CBY + FW - 1) / FW; ++r) {
+            const int cr = w + r * FW;
+            if (cr < CBY) {
+              double acc = 0.0;
+              if (okx) {
+#pragma unroll
+                for (int t = 0; t <= P; ++t) acc = fma(pwx[t], cb[cr * CBX + bxo + t], acc);
+              }
+              PX[(q * CBY + cr) * 32 + lane] = acc;
+            }
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+          for (int q = 0; q < NA; ++q) gen_request<P>(gn, tms[q], craw + q * NCB * C::CBS, cbar + q * NCB, c + NCB);
+#pragma unroll
+        for (int q = 0; q < NA; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double acc = 0.0;
+            if (oky[h]) {
+#pragma unroll
+              for (int t = 0; t <= P; ++t) acc = fma(cf.Pw[ry[h]][t], PX[(q * CBY + byo[h] + t) * 32 + lane], acc);
+            }
+            yv[((q * NCY + c % NCY) * TH + w + h * FW) * 32 + lane] = acc;
+          }
+        gn.cdone = c + 1;
+        __syncthreads();
+      }
+    }
+    double pu[NA][2];
+#pragma unroll
+    for (int q = 0; q < NA; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        pu[q][h] = 0.0;
+        if (okz) {
+          const int rz = z % (2 * P), cb0 = cbase<P>(z);
+#pragma unroll
+          for (int t = 0; t <= P; ++t)
+            pu[q][h] = fma(cf.Pw[rz][t], yv[((q * NCY + (cb0 + t) % NCY) * TH + w + h * FW) * 32 + lane], pu[q][h]);
+        }
+      }
+    if (decode) {
+      cpa_wait<PF>();
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (rowok[h]) {
+          const uint32_t* rec = wring + osl * TH * RW + (w + h * FW) * RW;
+          const double dv = warp_decode(rec, rec_e(rec + a.wu, eoff[h]), a.wu, lane);
+          out[h * rs8] = dv + pu[0][h];  // u_l = dec ú_l + P u_{l-1}
+        }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (rowok[h]) {
+          out[h * rs8] = pu[0][h];
+          if (NA == 2) out2[h * rs8] = pu[NA - 1][h];
+        }
+    }
+    out += tplane;
+    if (NA == 2) out2 += tplane;
+    osl = osl + 1 == NW ? 0 : osl + 1;
+  }
+}
+
 // Staged-input sweeps of the materialised form: the
 // skeleton of k_f3_cheb (specialised y / z passes, incremental slots) over a
 // TMA-staged FP64 input v, then per output point:
@@ -1749,7 +1922,30 @@ static int smem_staged(int wr, int nx) {  // (wr > 0: the r_L word ring of K = 2
   return (int)(((size_t)C::NBF * C::BOX + 2 * C::NR * 32) * 8 + xb + wb + 8 * C::NBF + 16);
 }
 template <int P>
-static int smem_prolong(int wu, int na = 1) {
+static int smem_prolong2(int wu, int na) {
+  using C = F3<P>;
+  const size_t d = ((size_t)C::NCB * C::CBS + C::CBY * 32 + (size_t)C::NCY * 2 * FW * 32) * na;
+  return (int)(d * 8 + (size_t)C::NW * 2 * FW * (wu + 1) * 4 + 8 + 8 + 8 * C::NCB * na + 16);
+}
+template <int P>
+static int smem_prolong(int wu, int na = 1);
+// k_f3_prolong2 (32 x 16 tiles, p = 1, 3) or k_f3_prolong (32 x 8)
+template <int P, int NA>
+static void prolong_launch(cudaStream_t st, const F3Args& a, const CoefT<double>& ct) {
+  if constexpr (P == 1 || P == 3) {
+    if (a.pr2) {
+      F3Args b = a;
+      const int nch = a.nitems / (a.nxb * a.nyb);
+      b.nyb = (a.g.NY + 2 * FW - 1) / (2 * FW);
+      b.nitems = a.nxb * b.nyb * nch;
+      f3_launch(k_f3_prolong2<P, NA>, b.nitems, smem_prolong2<P>(a.wu, NA), st, b, ct);
+      return;
+    }
+  }
+  f3_launch(k_f3_prolong<P, NA>, a.nitems, smem_prolong<P>(a.wu, NA), st, a, ct);
+}
+template <int P>
+static int smem_prolong(int wu, int na) {
   using C = F3<P>;
   const size_t d = ((size_t)C::NCB * C::CBS + C::CBY * 32 + (size_t)C::NCY * FW * 32) * na;
   return (int)(d * 8 + (size_t)C::NW * FW * (wu + 1) * 4 + 8 + 8 + 8 * C::NCB * na + 16);
@@ -1771,6 +1967,8 @@ void fine3_set_attributes() {
   cudaFuncSetAttribute(k_f3_residual<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_prolong<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
   cudaFuncSetAttribute(k_f3_prolong<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);      \
+  cudaFuncSetAttribute(k_f3_prolong2<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);     \
+  cudaFuncSetAttribute(k_f3_prolong2<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);     \
   cudaFuncSetAttribute(k_f3_staged<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged2<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_staged2<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -1972,7 +2170,7 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
       s_.ctaoff = ci * tiles;
       s_.yout = nullptr;
 #define CH(PP)                                                                                   \
-  f3_launch(k_f3_prolong<PP, 1>, tiles, smem_prolong<PP>(a.wu), st, g_, ct);                    \
+  prolong_launch<PP, 1>(st, g_, ct);                    \
   if (kind == 5) {                                                                               \
     if (a.tpb) staged_launch<PP, 1>(st, s_, ct, 0, 0);                                           \
     else staged_launch<PP, 0>(st, s_, ct, 0, 0);                                                 \
@@ -2011,9 +2209,9 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
   }
   if (kind == 3) {  // P u_{l-1} (step 0) or u_l = dec ú_l + P u_{l-1} (step 1) at the tile points
     const CoefT<double> ct = coefs_as<double>(cf);
-    if (p == 1) f3_launch(k_f3_prolong<1, 1>, a.nitems, smem_prolong<1>(a.wu), st, a, ct);
-    else if (p == 2) f3_launch(k_f3_prolong<2, 1>, a.nitems, smem_prolong<2>(a.wu), st, a, ct);
-    else f3_launch(k_f3_prolong<3, 1>, a.nitems, smem_prolong<3>(a.wu), st, a, ct);
+    if (p == 1) prolong_launch<1, 1>(st, a, ct);
+    else if (p == 2) prolong_launch<2, 1>(st, a, ct);
+    else prolong_launch<3, 1>(st, a, ct);
     return;
   }
   if (kind == 0) {
@@ -2047,8 +2245,8 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
       b.PU = a.Yb;
     }
 #define PRO(PP)                                                                                          \
-  if (na == 2) f3_launch(k_f3_prolong<PP, 2>, a.nitems, smem_prolong<PP>(a.wu, 2), st, b, ct);         \
-  else f3_launch(k_f3_prolong<PP, 1>, a.nitems, smem_prolong<PP>(a.wu), st, b, ct);                    \
+  if (na == 2) prolong_launch<PP, 2>(st, b, ct);         \
+  else prolong_launch<PP, 1>(st, b, ct);                    \
   staged_launch<PP, 2>(st, b, ct, a.wr, 0);
     if (p == 1) {
       PRO(1)

@@ -160,6 +160,7 @@ struct F3Args {
   double* yout;              // (k_f3_staged) where y_j goes
   int s2;                    // k_f3_staged2 (two input planes per iteration) instead of k_f3_staged
   int ctaoff;                // (k_f3_staged) first norm-partial CTA index of this launch (z chunks)
+  int pr2;                   // k_f3_prolong2 (32 x 16 tiles) for p = 1, 3
   double* chk;               // lean form in z chunks: the chunk buffer (a.chkrc + 2P planes)
   int chkrc;
   const CUtensorMap* tmch;   // fine boxes of the chunk buffer
