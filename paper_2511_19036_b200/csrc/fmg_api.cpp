@@ -764,9 +764,10 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
 void issue_item(fmg_ctx* c, const Item& it) {
   if (it.kind == 3) {
     mark(c, it.timed_cls);
+    fine3_take_launches();
     launch_fine3(c->p, it.f3kind, c->cur, fine3_args(c, it), c->cf, c->s.cfas_fp32);
     mark(c, it.timed_cls);
-    c->launches++;
+    c->launches += fine3_take_launches();  // (an item can be several kernels: tpb epilogues, z chunks)
     return;
   }
   if (it.kind == 1) {

@@ -2029,8 +2029,15 @@ static CoefT<T> coefs_as(const Coefs& c) {  // (FP32: the FP64 constants rounded
   return t;
 }
 
+static int g_f3_launches = 0;  // kernels issued by launch_fine3 since the last fine3_take_launches()
+int fine3_take_launches() {
+  const int n = g_f3_launches;
+  g_f3_launches = 0;
+  return n;
+}
 template <typename K, class CF>
 static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Args& a, const CF& cf) {
+  ++g_f3_launches;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nctas);
   cfg.blockDim = dim3(32, FW);
@@ -2082,6 +2089,7 @@ static void tpb_launch_w(cudaStream_t st, const F3Args& a) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  ++g_f3_launches;
   cudaLaunchKernelEx(&cfg, k_f3_tpb<MODE, T, W, WR>, a);
 }
 

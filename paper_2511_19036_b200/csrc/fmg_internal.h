@@ -243,6 +243,7 @@ void fine3_set_attributes();
 int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr);
 void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf, int fp32);
 bool fine3_tpby_width(int wu, int wr);
+int fine3_take_launches();  // kernels launch_fine3 issued since the last call
 void launch_coarse_nu(int dim, int p, cudaStream_t st, const void* devctx, const MArgs& a);  // nu > 1 level 0
 int kc_plan(int dim, int p, int Lmax, const Geom* g, const int* ust, const int* rst, int n_ir, int lc_cap,
             KcLayout* ly, int* lc_out, int* cs_out);
