@@ -13,7 +13,8 @@ def test_device_bytes_match_model(cfg, monkeypatch):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     monkeypatch.setenv("FMG_F3MAT", "0")  # (the model describes the lean form of the 3D kernels,
-    monkeypatch.setenv("FMG_TPBY", "0")   #  without its optional 1 byte per point of ý mantissas)
+    monkeypatch.setenv("FMG_TPBY", "0")   #  without its optional 1 byte per point of ý mantissas
+    monkeypatch.setenv("FMG_CHK", "0")    #  and without the optional z-chunk buffer)
     import paper_2511_19036_b200 as P
     c = CONFIGS[cfg]
     s = P.Solver(c["dim"], c["p"], c["levels"], default_schedule(c["dim"], c["p"]))
