@@ -1224,11 +1224,43 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       c->zhi[l] = g.NZ;
     }
     if (dim == 3) {
-      // 3D plane march: CTAs of 32 x 8 columns over this rank's planes, ~4 waves of 2 CTAs per SM
+      // 3D plane march: CTAs of 32 x 8 columns over this rank's planes, the
+      // planes in nch z chunks of rcz.  Measured (tools/ab_env.py, FMG_NCHL;
+      // DESIGN.md §4.3): large p = 1 levels gain from ~10 waves of the staged
+      // kernels' CTAs (C3 finest 2 -> 6 chunks: -0.47 ms), small levels whose
+      // chunks would be shorter than the 2p halo planes from one wave of long
+      // chunks (C4 levels 3, 4: -1.8 ms); the rest keeps ~4 waves of 2 CTAs
+      // per SM.  FMG_NCH forces the count (0: the round-1 rule everywhere).
       const int nxb = g.NX / 32, nz = c->zhi[l] - c->zlo[l];
       int nyb = (g.NY + march3_rows() - 1) / march3_rows();
       int tiles = nxb * nyb;
-      int nch = std::max(1, std::min(nz, (148 * 2 * 4 + tiles - 1) / tiles));
+      const char* ev = getenv("FMG_NCH");
+      const int fz = ev ? atoi(ev) : -1;
+      const int nch0 = std::min(nz, (148 * 2 * 4 + tiles - 1) / tiles);
+      // (the march3 kernels' per-tile partial table holds nxb (NY/8) (NZ/4) slots, 8 per CTA)
+      const int nchmax = std::max(nch0, std::min(nz, (c->tiles[l][1] * c->tiles[l][2]) / (8 * nyb)));
+      int nch = nch0;
+      if (fz > 0) {
+        nch = fz;
+      } else if (fz < 0) {
+        const int slots = 148 * (p == 1 ? 4 : p == 2 ? 3 : 2);  // staged kernels' CTAs per SM
+        const int rk0 = (nz + nch0 - 1) / nch0;
+        if (2 * tiles >= slots) {
+          if (p == 1) nch = std::max(nch0, std::min((10 * slots + tiles - 1) / tiles, nz / 8));
+        } else if (rk0 < 2 * p) {
+          nch = std::max(1, std::min(nz, slots / tiles));
+        }
+      }
+      if (const char* el = getenv("FMG_NCHL")) {  // per-level override "l:n,l:n" (tools/ab_env.py)
+        for (const char* q = el; *q;) {
+          int ll = 0, nn = 0, used = 0;
+          if (sscanf(q, "%d:%d%n", &ll, &nn, &used) != 2) break;
+          if (ll == l && nn > 0) nch = nn;
+          q += used;
+          if (*q == ',') ++q;
+        }
+      }
+      nch = std::max(1, std::min({nch, nz, nchmax}));
       int rcz = (nz + nch - 1) / nch;
       nch = (nz + rcz - 1) / rcz;
       c->mnyb[l] = nyb;
