@@ -1324,7 +1324,10 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     // z_L = P w_{L-1} materialised in Y for the top level's cFas step 1 (one
     // GPU: its ghost planes would need an exchange).  FMG_CFS=0 disables.
     const char* ec = getenv("FMG_CFS");
-    c->cfs = c->tpb && c->G == 1 && !s->cfas_fp32 && !(ec && atoi(ec) == 0);
+    // FP32 cFas too (P w_{l-1}, b_l and y_j in float; FMG_CFS32=0 keeps its
+    // generating kernels for the A/B)
+    const char* e32 = getenv("FMG_CFS32");
+    c->cfs = c->tpb && c->G == 1 && !(s->cfas_fp32 && e32 && atoi(e32) == 0) && !(ec && atoi(ec) == 0);
     // ... and the Chebyshev steps from materialised y_1, y_2 (one more
     // finest-size array X1; k_f3_staged<P, 3 / 4>): measured faster for
     // p = 3 (C4 145.2 -> 136.4 ms), flat for p = 1 (C3 20.35 / 20.49 ms), so

@@ -32,6 +32,8 @@
 // Every floating-point expression is the canonical tree of DESIGN.md §3
 // with explicit fma() (-fmad=false): bit-identical to fmg_march3.cu and to
 // the oracle.
+#include <type_traits>
+
 #include "fmg_device.cuh"
 
 #ifndef F3_PF
@@ -52,6 +54,10 @@
 #ifndef F3_MINB_RS
 #define F3_MINB_RS(P) F3_MINB(P)  // k_f3_residual_s
 #endif
+#ifndef F3_MINB_RS32
+#define F3_MINB_RS32(P) ((P) == 3 ? 3 : F3_MINB(P))  // the staged kernels in FP32 cFas (fewer registers)
+#endif
+#define F3_MINB_ST(P, T) (sizeof(T) == 4 ? F3_MINB_RS32(P) : F3_MINB_RS(P))
 
 namespace fmg {
 
@@ -142,18 +148,18 @@ __device__ __forceinline__ T zpass(const CoefT<T>& cf, int tz, const T* cr, cons
 
 // x pass of the staged box rows of warp w: a = Mx u, b = Kx u (lane = output
 // column x0 + lane; staged column c = fine x0 - P + c; `off` = TMA shift)
-template <int P, class T>
-__device__ __forceinline__ void xpass(const T* box, int off, const T* km, const T* kk, T* XA, T* XB, int w, int lane) {
+template <int P, class T, class S>
+__device__ __forceinline__ void xpass(const S* box, int off, const T* km, const T* kk, T* XA, T* XB, int w, int lane) {
   constexpr int R = F3<P>::R, NR = F3<P>::NR, RS = F3<P>::RS;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int r = w + k * FW;
     if (r < NR) {
-      const T* row = box + r * RS + off;
+      const S* row = box + r * RS + off;
       T s = 0, t = 0;
 #pragma unroll
       for (int o = 0; o < R; ++o) {
-        const T v = row[lane + o];
+        const T v = (T)row[lane + o];  // (FP32 cFas from an FP64 staged box: exact, it holds float values)
         s = fma(km[o], v, s);
         t = fma(kk[o], v, t);
       }
@@ -962,7 +968,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
 // k_m3_prolong's per-point (p+1)^2 global loads by shared boxes.
 // NA = 2 (the top level of the materialised form): the same for two coarse
 // arrays at once, u_{l-1} -> PU and w_{l-1} -> a.out2 (z_l for k_f3_staged<P, 2>).
-template <int P, int NA>
+template <int P, int NA, class TW = double>
 __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant__ F3Args a,
                                                             const __grid_constant__ CoefT<double> cf) {
   using C = F3<P>;
@@ -990,11 +996,15 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
   const int bxo = okx ? P * (x / (2 * P)) - gn.cx0 : 0, rx = okx ? x % (2 * P) : 0;
   const int byo = oky ? P * (y / (2 * P)) - gn.cy0 : 0, ry = oky ? y % (2 * P) : 0;
   double pwx[P + 1], pwy[P + 1];
+  TW pwxw[P + 1], pwyw[P + 1];  // (NA = 2, TW = float: P w_{l-1} in FP32 cFas, reading R28)
 #pragma unroll
   for (int t = 0; t <= P; ++t) {
     pwx[t] = cf.Pw[rx][t];
     pwy[t] = cf.Pw[ry][t];
+    pwxw[t] = (TW)pwx[t];
+    pwyw[t] = (TW)pwy[t];
   }
+  constexpr bool FW2 = NA == 2 && sizeof(TW) == 4;  // the second array in float
   const bool decode = NA == 1 && a.step == 1;  // (1: u_l = dec ú_l + P u_{l-1} -> U; 0: P u_{l-1} -> PU)
   int eoff = 0;
   const WStream ws = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, y, tl.zs, w * RW, rowok && decode, lane,
@@ -1044,12 +1054,21 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
           for (int r = 0; r < (CBY + FW - 1) / FW; ++r) {
             const int cr = w + r * FW;
             if (cr < CBY) {
-              double acc = 0.0;
-              if (okx) {
+              if (FW2 && q == 1) {
+                TW acc = 0;
+                if (okx) {
 #pragma unroll
-                for (int t = 0; t <= P; ++t) acc = fma(pwx[t], cb[cr * CBX + bxo + t], acc);
+                  for (int t = 0; t <= P; ++t) acc = fma(pwxw[t], (TW)cb[cr * CBX + bxo + t], acc);
+                }
+                PX[(q * CBY + cr) * 32 + lane] = (double)acc;
+              } else {
+                double acc = 0.0;
+                if (okx) {
+#pragma unroll
+                  for (int t = 0; t <= P; ++t) acc = fma(pwx[t], cb[cr * CBX + bxo + t], acc);
+                }
+                PX[(q * CBY + cr) * 32 + lane] = acc;
               }
-              PX[(q * CBY + cr) * 32 + lane] = acc;
             }
           }
         }
@@ -1058,12 +1077,21 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
           for (int q = 0; q < NA; ++q) gen_request<P>(gn, tms[q], craw + q * NCB * C::CBS, cbar + q * NCB, c + NCB);
 #pragma unroll
         for (int q = 0; q < NA; ++q) {
-          double acc = 0.0;
-          if (oky) {
+          if (FW2 && q == 1) {
+            TW acc = 0;
+            if (oky) {
 #pragma unroll
-            for (int t = 0; t <= P; ++t) acc = fma(pwy[t], PX[(q * CBY + byo + t) * 32 + lane], acc);
+              for (int t = 0; t <= P; ++t) acc = fma(pwyw[t], (TW)PX[(q * CBY + byo + t) * 32 + lane], acc);
+            }
+            yv[((q * NCY + c % NCY) * FW + w) * 32 + lane] = (double)acc;
+          } else {
+            double acc = 0.0;
+            if (oky) {
+#pragma unroll
+              for (int t = 0; t <= P; ++t) acc = fma(pwy[t], PX[(q * CBY + byo + t) * 32 + lane], acc);
+            }
+            yv[((q * NCY + c % NCY) * FW + w) * 32 + lane] = acc;
           }
-          yv[((q * NCY + c % NCY) * FW + w) * 32 + lane] = acc;
         }
         gn.cdone = c + 1;
         __syncthreads();
@@ -1075,9 +1103,17 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
       pu[q] = 0.0;
       if (okz) {
         const int rz = z % (2 * P), cb0 = cbase<P>(z);
+        if (FW2 && q == 1) {
+          TW acc = 0;
 #pragma unroll
-        for (int t = 0; t <= P; ++t)
-          pu[q] = fma(cf.Pw[rz][t], yv[((q * NCY + (cb0 + t) % NCY) * FW + w) * 32 + lane], pu[q]);
+          for (int t = 0; t <= P; ++t)
+            acc = fma((TW)cf.Pw[rz][t], (TW)yv[((q * NCY + (cb0 + t) % NCY) * FW + w) * 32 + lane], acc);
+          pu[q] = (double)acc;
+        } else {
+#pragma unroll
+          for (int t = 0; t <= P; ++t)
+            pu[q] = fma(cf.Pw[rz][t], yv[((q * NCY + (cb0 + t) % NCY) * FW + w) * 32 + lane], pu[q]);
+        }
       }
     }
     if (decode) {
@@ -1102,7 +1138,7 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
 // y0 + w + 8 (two independent chains in the y and z passes, half the barriers
 // per point).  p = 1, 3 (the coarse box covers 16 fine rows there).  Same
 // passes and order as k_f3_prolong.
-template <int P, int NA>
+template <int P, int NA, class TW = double>
 __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constant__ F3Args a,
                                                              const __grid_constant__ CoefT<double> cf) {
   using C = F3<P>;
@@ -1137,8 +1173,13 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
   gen_range<P>(gn, tl.zs, tl.ze - tl.zs, n);
   const int bxo = okx ? P * (x / (2 * P)) - gn.cx0 : 0, rx = okx ? x % (2 * P) : 0;
   double pwx[P + 1];
+  TW pwxw[P + 1];  // (NA = 2, TW = float: P w_{l-1} in FP32 cFas, reading R28)
 #pragma unroll
-  for (int t = 0; t <= P; ++t) pwx[t] = cf.Pw[rx][t];
+  for (int t = 0; t <= P; ++t) {
+    pwx[t] = cf.Pw[rx][t];
+    pwxw[t] = (TW)pwx[t];
+  }
+  constexpr bool FW2 = NA == 2 && sizeof(TW) == 4;  // the second array in float
   int byo[2], ry[2];
   bool oky[2], rowok[2];
 #pragma unroll
@@ -1207,12 +1248,21 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
           for (int r = 0; r < (CBY + FW - 1) / FW; ++r) {
             const int cr = w + r * FW;
             if (cr < CBY) {
-              double acc = 0.0;
-              if (okx) {
+              if (FW2 && q == 1) {
+                TW acc = 0;
+                if (okx) {
 #pragma unroll
-                for (int t = 0; t <= P; ++t) acc = fma(pwx[t], cb[cr * CBX + bxo + t], acc);
+                  for (int t = 0; t <= P; ++t) acc = fma(pwxw[t], (TW)cb[cr * CBX + bxo + t], acc);
+                }
+                PX[(q * CBY + cr) * 32 + lane] = (double)acc;
+              } else {
+                double acc = 0.0;
+                if (okx) {
+#pragma unroll
+                  for (int t = 0; t <= P; ++t) acc = fma(pwx[t], cb[cr * CBX + bxo + t], acc);
+                }
+                PX[(q * CBY + cr) * 32 + lane] = acc;
               }
-              PX[(q * CBY + cr) * 32 + lane] = acc;
             }
           }
         }
@@ -1223,12 +1273,22 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
         for (int q = 0; q < NA; ++q)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            double acc = 0.0;
-            if (oky[h]) {
+            if (FW2 && q == 1) {
+              TW acc = 0;
+              if (oky[h]) {
 #pragma unroll
-              for (int t = 0; t <= P; ++t) acc = fma(cf.Pw[ry[h]][t], PX[(q * CBY + byo[h] + t) * 32 + lane], acc);
+                for (int t = 0; t <= P; ++t)
+                  acc = fma((TW)cf.Pw[ry[h]][t], (TW)PX[(q * CBY + byo[h] + t) * 32 + lane], acc);
+              }
+              yv[((q * NCY + c % NCY) * TH + w + h * FW) * 32 + lane] = (double)acc;
+            } else {
+              double acc = 0.0;
+              if (oky[h]) {
+#pragma unroll
+                for (int t = 0; t <= P; ++t) acc = fma(cf.Pw[ry[h]][t], PX[(q * CBY + byo[h] + t) * 32 + lane], acc);
+              }
+              yv[((q * NCY + c % NCY) * TH + w + h * FW) * 32 + lane] = acc;
             }
-            yv[((q * NCY + c % NCY) * TH + w + h * FW) * 32 + lane] = acc;
           }
         gn.cdone = c + 1;
         __syncthreads();
@@ -1242,9 +1302,17 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
         pu[q][h] = 0.0;
         if (okz) {
           const int rz = z % (2 * P), cb0 = cbase<P>(z);
+          if (FW2 && q == 1) {
+            TW acc = 0;
 #pragma unroll
-          for (int t = 0; t <= P; ++t)
-            pu[q][h] = fma(cf.Pw[rz][t], yv[((q * NCY + (cb0 + t) % NCY) * TH + w + h * FW) * 32 + lane], pu[q][h]);
+            for (int t = 0; t <= P; ++t)
+              acc = fma((TW)cf.Pw[rz][t], (TW)yv[((q * NCY + (cb0 + t) % NCY) * TH + w + h * FW) * 32 + lane], acc);
+            pu[q][h] = (double)acc;
+          } else {
+#pragma unroll
+            for (int t = 0; t <= P; ++t)
+              pu[q][h] = fma(cf.Pw[rz][t], yv[((q * NCY + (cb0 + t) % NCY) * TH + w + h * FW) * 32 + lane], pu[q][h]);
+          }
         }
       }
     if (decode) {
@@ -1285,17 +1353,18 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
 //             y_j = y_{j-1} + d_j -> a.yout, and d_2 -> a.Dv when j = 2 is
 //             not the last step.  Same expressions as k_f3_cheb (which
 //             recomputes y_{j-1} on its staged b / d_2 boxes instead).
-template <int P, int K>
-__global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __grid_constant__ F3Args a,
-                                                                     const __grid_constant__ CoefT<double> cf) {
+template <int P, int K, class T = double>
+__global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const __grid_constant__ F3Args a,
+                                                                     const __grid_constant__ CoefT<T> cf) {
+  static_assert(K >= 2 || sizeof(T) == 8, "the residual is FP64");
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX, NBF = C::NBF, PF = C::PF, NW = C::NW;
   constexpr int NX_ = K == 4 ? 2 : 1;  // point arrays of K = 3, 4: b (+ d_2)
   extern __shared__ __align__(128) double fsm[];
   double* ring = fsm;  // NBF boxes of v
-  double* XA = ring + NBF * BOX;
-  double* XB = XA + NR * 32;
-  double* aring = XB + NR * 32;  // (K >= 3) NW x NX_ x 256: b (+ d_2) at the output points
+  T* XA = (T*)(ring + NBF * BOX);  // (T = float: FP32 cFas, reading R28; the staged arrays stay FP64 holding float values)
+  T* XB = XA + NR * 32;
+  double* aring = ring + NBF * BOX + 2 * NR * 32;  // (K >= 3) NW x NX_ x 256: b (+ d_2) at the output points
   uint32_t* wring = (uint32_t*)(aring + (K >= 3 ? NW * NX_ * 32 * FW : 0));  // (K = 2) NW x FW x (w_r + 1)
   const int RW = a.wr + 1;
   unsigned long long* bars = (unsigned long long*)(wring + (K == 2 ? NW * FW * RW + 2 : 0));
@@ -1307,21 +1376,21 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
   const int x = tl.x0 + lane, y = tl.y0 + w;
   const bool rowok = y < g.NY;
   const int tx = x % P, ty = y % P;
-  double km[R], kk[R];
+  T km[R], kk[R];
 #pragma unroll
   for (int o = 0; o < R; ++o) {
     km[o] = cf.Mc[tx][o];
     kk[o] = cf.Kc[tx][o];
   }
-  const double hl = pow2(-(a.l + 1));
+  const T hl = (T)pow2(-(a.l + 1));
   const double* __restrict__ gt = a.gtab;
   const bool uxy = unk1(x, n) && unk1(y, n);
   const double gxy = K < 2 && uxy ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
   // invD at the output point per z node type (RN(1/diag) 2^(l+1), 0 at non-unknowns)
-  double fv[P];
+  T fv[P];
 #pragma unroll
-  for (int t = 0; t < P; ++t) fv[t] = uxy ? cf.invd[(t * P + ty) * P + tx] * pow2(a.l + 1) : 0.0;
-  const double al = cf.cal[K - 2 > 0 ? K - 2 : 0], be = cf.cbe[K - 2 > 0 ? K - 2 : 0], ith = cf.inv_theta;
+  for (int t = 0; t < P; ++t) fv[t] = uxy ? cf.invd[(t * P + ty) * P + tx] * (T)pow2(a.l + 1) : (T)0;
+  const T al = cf.cal[K - 2 > 0 ? K - 2 : 0], be = cf.cbe[K - 2 > 0 ? K - 2 : 0], ith = cf.inv_theta;
   const int nxb = g.NX >> 5;
   const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
   const long long tplane = (long long)g.NY * g.NX, bpp = (long long)g.NY * nxb;
@@ -1384,9 +1453,9 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
       cpa_commit();
     }
   }
-  double cr[R], sr[R];
+  T cr[R], sr[R];
 #pragma unroll
-  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0.0;
+  for (int o = 0; o < R; ++o) cr[o] = sr[o] = 0;
   double ss = 0.0;
   int tz = ((z0 % P) + P) % P;
   int isl = 0, osl = 0, oisl = NBF - P;  // slots: input plane i, words / points of the next output, input plane i - P
@@ -1411,7 +1480,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
     }
     xpass<P>(ring + isl * BOX, C::SH, km, kk, XA, XB, w, lane);
     __syncthreads();
-    double c, s;
+    T c, s;
     ypass<P>(cf, ty, XA, XB, w, lane, c, s);
 #pragma unroll
     for (int o = 0; o < R - 1; ++o) {
@@ -1422,23 +1491,23 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
     sr[R - 1] = s;
     if (produce) {
       const int z = zi - P;
-      const double av = zpass<P>(cf, tz, cr, sr) * hl;
+      const T av = zpass<P>(cf, tz, cr, sr) * hl;
       const bool uz = unk1(z, n);
       if (K >= 3) {
         if (rowok) {
           const double* ax = aring + osl * NX_ * 32 * FW + tid;
-          const double b = ax[0];
-          double f = fv[0];  // (selected with constant indices: fv stays in registers)
+          const T b = (T)ax[0];
+          T f = fv[0];  // (selected with constant indices: fv stays in registers)
 #pragma unroll
           for (int t = 1; t < P; ++t) f = tz == t ? fv[t] : f;
-          f = uz ? f : 0.0;
-          const double yprev = ring[oisl * BOX + C::SH + (w + P) * RS + P + lane];  // y_{j-1} at the point
-          const double dprev = K == 4 ? ax[32 * FW] : yprev;                        // d_{j-1} (d_1 = y_1)
-          const double qq = b - av;
-          const double d = fma(al, dprev, be * (f * qq));
-          const double yv = yprev + d;
-          *Yo = yv;
-          if (!a.last) *Dp = d;
+          f = uz ? f : (T)0;
+          const T yprev = (T)ring[oisl * BOX + C::SH + (w + P) * RS + P + lane];  // y_{j-1} at the point
+          const T dprev = K == 4 ? (T)ax[32 * FW] : yprev;                        // d_{j-1} (d_1 = y_1)
+          const T qq = b - av;
+          const T d = fma(al, dprev, be * (f * qq));
+          const T yv = yprev + d;
+          *Yo = (double)yv;
+          if (!a.last) *Dp = (double)d;
         }
         Yo += tplane;
         Dp += tplane;
@@ -1447,13 +1516,13 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged(const __gr
         if (rowok) {
           const uint32_t* rec = wring + osl * FW * RW + w * RW;
           const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
-          const double b = rv - av;  // b = dec r - A z (B lives in the t_L buffer)
-          *Tp = b;
+          const T b = (T)rv - av;  // b = dec r - A z (B lives in the t_L buffer)
+          *Tp = (double)b;
           if (Yo) {
-            double f = fv[0];
+            T f = fv[0];
 #pragma unroll
             for (int t = 1; t < P; ++t) f = tz == t ? fv[t] : f;
-            *Yo = ith * ((uz ? f : 0.0) * b);  // y_1 = inv_theta (invD b)
+            *Yo = (double)(ith * ((uz ? f : (T)0) * b));  // y_1 = inv_theta (invD b)
           }
         }
         if (Yo) Yo += tplane;
@@ -1493,18 +1562,19 @@ struct F3S2 {
   static constexpr int NBF = P + 4;         // ring slots: pair being read, pair in flight, centre planes i - P
   static constexpr int NW = PF + 4;         // word / point slots per output
 };
-template <int P, int K>
-__global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __grid_constant__ F3Args a,
-                                                                      const __grid_constant__ CoefT<double> cf) {
+template <int P, int K, class T = double>
+__global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const __grid_constant__ F3Args a,
+                                                                      const __grid_constant__ CoefT<T> cf) {
+  static_assert(K >= 2 || sizeof(T) == 8, "the residual is FP64");
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX;
   constexpr int NBF = F3S2<P>::NBF, PF = F3S2<P>::PF, NW = F3S2<P>::NW;
   constexpr int NX_ = K == 4 ? 2 : 1;
   extern __shared__ __align__(128) double fsm[];
   double* ring = fsm;                     // NBF boxes of v
-  double* XA = ring + NBF * BOX;          // 2 planes x NR x 32
-  double* XB = XA + 2 * NR * 32;
-  double* aring = XB + 2 * NR * 32;       // (K >= 3) NW x NX_ x 256
+  T* XA = (T*)(ring + NBF * BOX);         // 2 planes x NR x 32 (T = float: FP32 cFas, reading R28)
+  T* XB = XA + 2 * NR * 32;
+  double* aring = ring + NBF * BOX + 4 * NR * 32;  // (K >= 3) NW x NX_ x 256
   uint32_t* wring = (uint32_t*)(aring + (K >= 3 ? NW * NX_ * 32 * FW : 0));  // (K = 2) NW x FW x (w_r + 1)
   const int RW = a.wr + 1;
   unsigned long long* bars = (unsigned long long*)(wring + (K == 2 ? NW * FW * RW + 2 : 0));
@@ -1516,20 +1586,20 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __g
   const int x = tl.x0 + lane, y = tl.y0 + w;
   const bool rowok = y < g.NY;
   const int tx = x % P, ty = y % P;
-  double km[R], kk[R];
+  T km[R], kk[R];
 #pragma unroll
   for (int o = 0; o < R; ++o) {
     km[o] = cf.Mc[tx][o];
     kk[o] = cf.Kc[tx][o];
   }
-  const double hl = pow2(-(a.l + 1));
+  const T hl = (T)pow2(-(a.l + 1));
   const double* __restrict__ gt = a.gtab;
   const bool uxy = unk1(x, n) && unk1(y, n);
   const double gxy = K < 2 && uxy ? (cf.rhs_c * gt[x]) * gt[y] : 0.0;
-  double fv[P];
+  T fv[P];
 #pragma unroll
-  for (int t = 0; t < P; ++t) fv[t] = uxy ? cf.invd[(t * P + ty) * P + tx] * pow2(a.l + 1) : 0.0;
-  const double al = cf.cal[K - 2 > 0 ? K - 2 : 0], be = cf.cbe[K - 2 > 0 ? K - 2 : 0], ith = cf.inv_theta;
+  for (int t = 0; t < P; ++t) fv[t] = uxy ? cf.invd[(t * P + ty) * P + tx] * (T)pow2(a.l + 1) : (T)0;
+  const T al = cf.cal[K - 2 > 0 ? K - 2 : 0], be = cf.cbe[K - 2 > 0 ? K - 2 : 0], ith = cf.inv_theta;
   const int nxb = g.NX >> 5;
   const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
   const long long tplane = (long long)g.NY * g.NX, bpp = (long long)g.NY * nxb;
@@ -1593,30 +1663,30 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __g
     ocopy(1, 1);
     cpa_commit();
   }
-  double cr[R + 1], sr[R + 1];
+  T cr[R + 1], sr[R + 1];
 #pragma unroll
-  for (int o = 0; o <= R; ++o) cr[o] = sr[o] = 0.0;
+  for (int o = 0; o <= R; ++o) cr[o] = sr[o] = 0;
   double ss = 0.0;
   int tz = ((z0 % P) + P) % P;           // node type of input plane i (= of output plane i - P)
   int isl = 0, osl = 0, oisl = NBF - P;  // slots: input plane i, words / points of output i - 2P, input plane i - P
   unsigned par = 0;                      // barrier phase of slot isl
-  auto emit = [&](int z, double av, int tzo, int ois, int os) {  // the output at plane z
+  auto emit = [&](int z, T av, int tzo, int ois, int os) {  // the output at plane z
     const bool uz = unk1(z, n);
     if (K >= 3) {
       if (rowok) {
         const double* ax = aring + os * NX_ * 32 * FW + tid;
-        const double b = ax[0];
-        double f = fv[0];
+        const T b = (T)ax[0];
+        T f = fv[0];
 #pragma unroll
         for (int t = 1; t < P; ++t) f = tzo == t ? fv[t] : f;
-        f = uz ? f : 0.0;
-        const double yprev = ring[ois * BOX + C::SH + (w + P) * RS + P + lane];
-        const double dprev = K == 4 ? ax[32 * FW] : yprev;
-        const double qq = b - av;
-        const double d = fma(al, dprev, be * (f * qq));
-        const double yv = yprev + d;
-        *Yo = yv;
-        if (!a.last) *Dp = d;
+        f = uz ? f : (T)0;
+        const T yprev = (T)ring[ois * BOX + C::SH + (w + P) * RS + P + lane];
+        const T dprev = K == 4 ? (T)ax[32 * FW] : yprev;
+        const T qq = b - av;
+        const T d = fma(al, dprev, be * (f * qq));
+        const T yv = yprev + d;
+        *Yo = (double)yv;
+        if (!a.last) *Dp = (double)d;
       }
       Yo += tplane;
       Dp += tplane;
@@ -1624,13 +1694,13 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __g
       if (rowok) {
         const uint32_t* rec = wring + os * FW * RW + w * RW;
         const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
-        const double b = rv - av;
-        *Tp = b;
+        const T b = (T)rv - av;
+        *Tp = (double)b;
         if (Yo) {
-          double f = fv[0];
+          T f = fv[0];
 #pragma unroll
           for (int t = 1; t < P; ++t) f = tzo == t ? fv[t] : f;
-          *Yo = ith * ((uz ? f : 0.0) * b);
+          *Yo = (double)(ith * ((uz ? f : (T)0) * b));
         }
       }
       if (Yo) Yo += tplane;
@@ -1677,14 +1747,14 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __g
       for (int k = 0; k < 2; ++k) {
         const int r = w + k * FW;
         if (r < NR) {
-          double s0 = 0, t0 = 0, s1 = 0, t1 = 0;
+          T s0 = 0, t0 = 0, s1 = 0, t1 = 0;
 #pragma unroll
           for (int o = 0; o < R; ++o) {
-            const double v0 = b0[r * RS + lane + o];
+            const T v0 = (T)b0[r * RS + lane + o];
             s0 = fma(km[o], v0, s0);
             t0 = fma(kk[o], v0, t0);
             if (two) {
-              const double v1 = b1[r * RS + lane + o];
+              const T v1 = (T)b1[r * RS + lane + o];
               s1 = fma(km[o], v1, s1);
               t1 = fma(kk[o], v1, t1);
             }
@@ -1697,7 +1767,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __g
       }
     }
     __syncthreads();
-    double c0, s0, c1 = 0.0, s1 = 0.0;
+    T c0, s0, c1 = 0, s1 = 0;
     ypass<P>(cf, ty, XA, XB, w, lane, c0, s0);
     if (two) ypass<P>(cf, ty, XA + NR * 32, XB + NR * 32, w, lane, c1, s1);
 #pragma unroll
@@ -1714,9 +1784,9 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __g
     const int oisl1 = oisl + 1 == NBF ? 0 : oisl + 1;
     const int osl1 = osl + 1 == NW ? 0 : osl + 1;
     if (i >= 2 * P) {
-      const double av0 = zpass<P>(cf, tz, cr, sr) * hl;
+      const T av0 = zpass<P>(cf, tz, cr, sr) * hl;
       if (two) {
-        const double av1 = zpass<P>(cf, tz1, cr + 1, sr + 1) * hl;
+        const T av1 = zpass<P>(cf, tz1, cr + 1, sr + 1) * hl;
         emit(z0 + i - P, av0, tz, oisl, osl);
         emit(z0 + i + 1 - P, av1, tz1, oisl1, osl1);
       } else {
@@ -1724,7 +1794,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_RS(P)) k_f3_staged2(const __g
       }
       osl = osl1 + 1 == NW ? 0 : osl1 + 1;
     } else if (two && i + 1 >= 2 * P) {
-      const double av1 = zpass<P>(cf, tz1, cr + 1, sr + 1) * hl;
+      const T av1 = zpass<P>(cf, tz1, cr + 1, sr + 1) * hl;
       emit(z0 + i + 1 - P, av1, tz1, oisl1, osl);
       osl = osl1;
     }
@@ -1902,10 +1972,10 @@ static int smem_staged2(int wr, int nx);
 template <int P>
 static int smem_staged(int wr, int nx);
 // k_f3_staged (one plane per iteration) or k_f3_staged2 (two; F3Args::s2)
-template <int P, int K>
-static void staged_launch(cudaStream_t st, const F3Args& a, const CoefT<double>& ct, int wr, int nx) {
-  if (a.s2) f3_launch(k_f3_staged2<P, K>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
-  else f3_launch(k_f3_staged<P, K>, a.nitems, smem_staged<P>(wr, nx), st, a, ct);
+template <int P, int K, class T = double>
+static void staged_launch(cudaStream_t st, const F3Args& a, const CoefT<T>& ct, int wr, int nx) {
+  if (a.s2) f3_launch(k_f3_staged2<P, K, T>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
+  else f3_launch(k_f3_staged<P, K, T>, a.nitems, smem_staged<P>(wr, nx), st, a, ct);
 }
 template <int P>
 static int smem_staged2(int wr, int nx) {
@@ -1930,7 +2000,7 @@ static int smem_prolong2(int wu, int na) {
 template <int P>
 static int smem_prolong(int wu, int na = 1);
 // k_f3_prolong2 (32 x 16 tiles, p = 1, 3) or k_f3_prolong (32 x 8)
-template <int P, int NA>
+template <int P, int NA, class TW = double>
 static void prolong_launch(cudaStream_t st, const F3Args& a, const CoefT<double>& ct) {
   if constexpr (P == 1 || P == 3) {
     if (a.pr2) {
@@ -1938,11 +2008,11 @@ static void prolong_launch(cudaStream_t st, const F3Args& a, const CoefT<double>
       const int nch = a.nitems / (a.nxb * a.nyb);
       b.nyb = (a.g.NY + 2 * FW - 1) / (2 * FW);
       b.nitems = a.nxb * b.nyb * nch;
-      f3_launch(k_f3_prolong2<P, NA>, b.nitems, smem_prolong2<P>(a.wu, NA), st, b, ct);
+      f3_launch(k_f3_prolong2<P, NA, TW>, b.nitems, smem_prolong2<P>(a.wu, NA), st, b, ct);
       return;
     }
   }
-  f3_launch(k_f3_prolong<P, NA>, a.nitems, smem_prolong<P>(a.wu, NA), st, a, ct);
+  f3_launch(k_f3_prolong<P, NA, TW>, a.nitems, smem_prolong<P>(a.wu, NA), st, a, ct);
 }
 template <int P>
 static int smem_prolong(int wu, int na) {
@@ -1990,7 +2060,15 @@ void fine3_set_attributes() {
   cudaFuncSetAttribute(k_f3_cheb<P, 2, float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cheb<P, 3, float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
   cudaFuncSetAttribute(k_f3_cheb<P, 2, float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
-  cudaFuncSetAttribute(k_f3_cheb<P, 3, float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_f3_cheb<P, 3, float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_prolong<P, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
+  cudaFuncSetAttribute(k_f3_prolong2<P, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged<P, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);   \
+  cudaFuncSetAttribute(k_f3_staged<P, 3, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);   \
+  cudaFuncSetAttribute(k_f3_staged<P, 4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);   \
+  cudaFuncSetAttribute(k_f3_staged2<P, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
+  cudaFuncSetAttribute(k_f3_staged2<P, 3, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
+  cudaFuncSetAttribute(k_f3_staged2<P, 4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   F(1) F(2) F(3)
 #undef F
 #define TW(T_, W_, R_) \
@@ -2127,28 +2205,32 @@ bool fine3_tpby_width(int wu, int wr) {
 // 4 residual (u staged);
 // `fp32`: FP32 cFas (kinds 1, 2; reading R28)
 void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs& cf, int fp32) {
-  if (kind == 2 && a.cfs == 3 && !fp32) {  // staged Chebyshev step j from y_{j-1} (top level, materialised)
-    const CoefT<double> ct = coefs_as<double>(cf);
+  if (kind == 2 && a.cfs == 3) {  // staged Chebyshev step j from y_{j-1} (top level, materialised)
     F3Args b = a;
     const bool j2 = a.step == 2;
     b.tmb = j2 ? a.tmx1 : a.tmy;     // y_1 in X1 / y_2 in Y
     b.yout = j2 ? a.Yb : a.X1b;      // y_2 -> Y, y_3 -> X1
+    auto run = [&](auto ct) {  // (CoefT<double>, or CoefT<float> for FP32 cFas: reading R28)
+      using T = std::remove_reference_t<decltype(ct.inv_theta)>;
 #define ST(PP)                                                                                              \
-  if (j2) staged_launch<PP, 3>(st, b, ct, 0, 1);                      \
-  else staged_launch<PP, 4>(st, b, ct, 0, 2);
-    if (p == 1) {
-      ST(1)
-    } else if (p == 2) {
-      ST(2)
-    } else {
-      ST(3)
-    }
+  if (j2) staged_launch<PP, 3, T>(st, b, ct, 0, 1);                      \
+  else staged_launch<PP, 4, T>(st, b, ct, 0, 2);
+      if (p == 1) {
+        ST(1)
+      } else if (p == 2) {
+        ST(2)
+      } else {
+        ST(3)
+      }
 #undef ST
-    if (a.last) {  // the thread-per-block finalisation from y_k
-      F3Args t = a;
-      t.Dv = b.yout;
-      tpb_launch<1, double>(st, t);
-    }
+      if (a.last) {  // the thread-per-block finalisation from y_k
+        F3Args t = a;
+        t.Dv = b.yout;
+        tpb_launch<1, T>(st, t);
+      }
+    };
+    if (fp32) run(coefs_as<float>(cf));
+    else run(coefs_as<double>(cf));
     return;
   }
   if (kind == 5 || (kind == 1 && a.cfs == 6)) {  // lean form in z chunks: u_L / z_L
@@ -2236,9 +2318,11 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
     else f3_launch(k_f3_residual<3, true>, a.nitems, smem_res<3>(a.wu), st, a, ct);
     return;
   }
-  if (kind == 1 && a.cfs && !fp32) {  // top level, materialised: z_L = P w_{L-1} -> Y, then b_L from staged z_L
-    // (a.cfs == 2: P u_{L-1} -> PU in the same prolongation launch)
+  if (kind == 1 && a.cfs && (!fp32 || a.cfs != 1)) {  // materialised: z_l = P w_{l-1} -> Y / Z, then b_l from staged z_l
+    // (a.cfs == 2 / 5: P u_{l-1} -> PU in the same prolongation launch; FP32
+    // cFas: P w_{l-1} and b_l, y_1 in float, reading R28)
     const CoefT<double> ct = coefs_as<double>(cf);
+    const CoefT<float> ctf = coefs_as<float>(cf);
     F3Args b = a;
     b.step = 0;
     const bool below = a.cfs == 5;  // (z_l in the Z scratch: the last step's w_l = z_l + ý needs it)
@@ -2253,9 +2337,14 @@ void launch_fine3(int p, int kind, cudaStream_t st, const F3Args& a, const Coefs
       b.PU = a.Yb;
     }
 #define PRO(PP)                                                                                          \
-  if (na == 2) prolong_launch<PP, 2>(st, b, ct);         \
-  else prolong_launch<PP, 1>(st, b, ct);                    \
-  staged_launch<PP, 2>(st, b, ct, a.wr, 0);
+  if (fp32) {                                                                                            \
+    prolong_launch<PP, 2, float>(st, b, ct);                                                             \
+    staged_launch<PP, 2, float>(st, b, ctf, a.wr, 0);                                                    \
+  } else {                                                                                               \
+    if (na == 2) prolong_launch<PP, 2>(st, b, ct);                                                       \
+    else prolong_launch<PP, 1>(st, b, ct);                                                               \
+    staged_launch<PP, 2>(st, b, ct, a.wr, 0);                                                            \
+  }
     if (p == 1) {
       PRO(1)
     } else if (p == 2) {

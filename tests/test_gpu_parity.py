@@ -454,9 +454,25 @@ def test_fmg_parity_fine3_variants(P, monkeypatch, variant, d, p, levels):
     compare_solvers(P, d, p, levels)
 
 
-@pytest.mark.parametrize("d,p,levels", [(3, 1, 5), (3, 3, 4)])
-def test_fmg_parity_fine3_variants_fp32(P, monkeypatch, d, p, levels):
-    """FP32 cFas with the thread-per-block epilogues on every level."""
+_F3_VARIANTS_FP32 = {
+    # FP32 cFas in the staged kernels: P w_{l-1} (prolongation, second array),
+    # b_l, y_1 (k_f3_staged<P, 2, float>) and the staged Chebyshev steps
+    "staged": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="1"),
+    "staged_s1": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="0"),
+    "staged_no_csc": dict(FMG_CFS="1", FMG_CSC="0"),
+    # the generating cFas kernels (k_f3_cfas / k_f3_cheb<P, J, float>)
+    "generating": dict(FMG_CFS32="0"),
+}
+
+
+@pytest.mark.parametrize("variant", sorted(_F3_VARIANTS_FP32))
+@pytest.mark.parametrize("d,p,levels", [(3, 1, 5), (3, 2, 4), (3, 3, 4), (3, 1, 6), (3, 3, 5)])
+def test_fmg_parity_fine3_variants_fp32(P, monkeypatch, variant, d, p, levels):
+    """FP32 cFas with the thread-per-block epilogues on every level, each
+    cFas kernel family in turn: bit-identical to the oracle's FP32 mode."""
     monkeypatch.setenv("FMG_TPB_MIN_BLOCKS", "0")
     monkeypatch.setenv("FMG_F3MAT", "1")
+    monkeypatch.setenv("FMG_TPB", "1")
+    for k, v in _F3_VARIANTS_FP32[variant].items():
+        monkeypatch.setenv(k, v)
     compare_solvers(P, d, p, levels, cfas_fp32=1)

@@ -1,6 +1,6 @@
 """A/B of env-var settings read at fmg_create (tools only):
    python tools/ab_env.py CFG "FMG_LC=3" "FMG_LC=4" ...
-Creates one context per setting in one process, then times them alternately
+AB_FP32=1: FP32 cFas schedules.  Creates one context per setting in one process, then times them alternately
 (CUDA events, no L2 flush), 3 rounds."""
 import os
 import sys
@@ -18,7 +18,10 @@ for spec in sys.argv[2:]:
     for kv in spec.split():
         k, v = kv.split("=", 1)
         os.environ[k] = v
-    s = P.Solver(cfg["dim"], cfg["p"], cfg["levels"], default_schedule(cfg["dim"], cfg["p"]))
+    sch = default_schedule(cfg["dim"], cfg["p"])
+    if os.environ.get("AB_FP32") == "1":  # FP32 cFas (reading R28)
+        sch["cfas_fp32"] = 1
+    s = P.Solver(cfg["dim"], cfg["p"], cfg["levels"], sch)
     s.solve()  # graph captured under this setting
     os.environ.clear()
     os.environ.update(saved)
