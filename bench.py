@@ -32,6 +32,7 @@ from fmg_inputs import CONFIGS, default_schedule, unknowns  # noqa: E402
 METRIC = "FMG solve DoF/s and effective HBM GB/s vs 8 TB/s roofline at 1/2/4/8 B200"
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_TFLOPS = 37.2  # 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz; measured 34.0
+FP32_PEAK_TFLOPS = 74.4  # 148 SMs x 128 FFMA/clk x 2 x 1.965 GHz (the FP32 cFas lines, reading R28)
 
 
 def peaks():
@@ -142,7 +143,8 @@ def kernel_model(cfg, sched, cls):
 
 KERNEL_LABEL = {(2, 0): "k_m_residual (fine level)", (3, 0): "k_f3_staged / k_f3_residual (fine level)",
                 (2, 5): "k_m_cheb final step (fine level)",
-                (3, 5): "k_f3_cheb final step + k_f3_tpb<1> finalisation (fine level)"}
+                (3, 5): "last Chebyshev step (k_f3_staged2<3, 4> at p = 3, k_f3_cheb at p = 1) + k_f3_tpb<1> "
+                        "finalisation (fine level)"}
 
 
 def roofline_entry(cfg, sched, args, avg_launch_ms, launches, hbm, hbm_src):
@@ -154,7 +156,11 @@ def roofline_entry(cfg, sched, args, avg_launch_ms, launches, hbm, hbm_src):
     t_hbm = byts / (hbm * 1e9)
     t_alu = flops / (FP64_PEAK_TFLOPS * 1e12)
     sec = avg_launch_ms * 1e-3
-    if t_alu >= t_hbm:
+    if t_alu >= t_hbm and sched.get("cfas_fp32") and args.roofline_class == 5:
+        # FP32 cFas: the Chebyshev step's arithmetic is float (the correction's 2 adds excepted)
+        roof = {"bound": "alu", "achieved": flops / sec / 1e12, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "peak_source": "derived FP32: 148 SMs x 128 FFMA/clk x 2 x 1.965 GHz (DESIGN.md §7)"}
+    elif t_alu >= t_hbm:
         roof = {"bound": "alu", "achieved": flops / sec / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "peak_source": "derived FP64: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §7; "
                                "tools/fp64_peak.cu measured 34.0)"}
@@ -164,7 +170,7 @@ def roofline_entry(cfg, sched, args, avg_launch_ms, launches, hbm, hbm_src):
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["hbm_section_frac"] = byts / sec / 1e9 / hbm
     roof["traffic"] = args.traffic
-    if args.traffic is None and args.smoother == "chebyshev" and args.nu == 1:
+    if args.traffic is None and args.smoother == "chebyshev" and args.nu == 1 and not sched.get("cfas_fp32"):
         # the committed ncu capture of this kernel (profiles/traffic.json)
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
