@@ -137,6 +137,23 @@ __device__ __forceinline__ long long warp_unpack(const uint32_t* words, int w, i
 __device__ __forceinline__ double warp_decode(const uint32_t* words, int E, int w, int lane) {
   return i2d(warp_unpack(words, w, lane), w) * pow2(E - (w - 1));
 }
+// The same with a compile-time width W <= 32, the words in SHARED memory:
+// lane j loads the one or two words holding its field directly (broadcast
+// loads, no shuffles; the field never reaches a third word for W <= 32).
+// Bit-identical to warp_decode.
+template <int W>
+__device__ __forceinline__ double warp_decode_w(const uint32_t* words, int E, int lane) {
+  static_assert(W >= 1 && W <= 32, "compile-time widths <= 32");
+  const int o = lane * W, j0 = o >> 5, s = o & 31;
+  unsigned long long field;
+  if (32 % W == 0) {
+    field = words[j0] >> s;
+  } else {  // (j0 + 1 <= W: the exponent word at most, whose bits the shift drops)
+    field = ((unsigned long long)words[j0] | ((unsigned long long)words[j0 + 1] << 32)) >> s;
+  }
+  const long long m = (long long)(field << (64 - W)) >> (64 - W);
+  return i2d(m, W) * pow2(E - (W - 1));
+}
 
 // Single-entry decode (entry j of a block), for halo points.
 __device__ __forceinline__ double point_decode(const uint32_t* words, int E, int w, int j) {

@@ -262,6 +262,13 @@ __device__ __forceinline__ void wcopy(const WStream& s, unsigned slot_s, int pla
 __device__ __forceinline__ int rec_e(const uint32_t* ew, int off) {  // byte `off` of the exponent word pair
   return (int)(int8_t)(ew[off >> 2] >> (8 * (off & 3)));
 }
+// r_L decode of the staged cFas step 1: compile-time width WR > 0 (the
+// common top-level widths, warp_decode_w) or the runtime width.
+template <int WR>
+__device__ __forceinline__ double dec_rec(const uint32_t* rec, int E, int w, int lane) {
+  if constexpr (WR > 0) return warp_decode_w<WR>(rec, E, lane);
+  else return warp_decode(rec, E, w, lane);
+}
 
 // ------------------------------------------- on-the-fly prolongation ----
 // Generates, plane by plane, v = P_l c_{l-1} on the staged box (32 + 2P) x
@@ -1353,7 +1360,7 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
 //             y_j = y_{j-1} + d_j -> a.yout, and d_2 -> a.Dv when j = 2 is
 //             not the last step.  Same expressions as k_f3_cheb (which
 //             recomputes y_{j-1} on its staged b / d_2 boxes instead).
-template <int P, int K, class T = double>
+template <int P, int K, class T = double, int WR = 0>
 __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const __grid_constant__ F3Args a,
                                                                      const __grid_constant__ CoefT<T> cf) {
   static_assert(K >= 2 || sizeof(T) == 8, "the residual is FP64");
@@ -1366,7 +1373,8 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
   T* XB = XA + NR * 32;
   double* aring = ring + NBF * BOX + 2 * NR * 32;  // (K >= 3) NW x NX_ x 256: b (+ d_2) at the output points
   uint32_t* wring = (uint32_t*)(aring + (K >= 3 ? NW * NX_ * 32 * FW : 0));  // (K = 2) NW x FW x (w_r + 1)
-  const int RW = a.wr + 1;
+  const int wr_ = WR > 0 ? WR : a.wr;  // (K = 2: w_r(L, L), compile-time for the common widths)
+  const int RW = wr_ + 1;
   unsigned long long* bars = (unsigned long long*)(wring + (K == 2 ? NW * FW * RW + 2 : 0));
   bars = (unsigned long long*)(((uintptr_t)bars + 7) & ~(uintptr_t)7);
   const int lane = threadIdx.x, w = threadIdx.y;
@@ -1407,7 +1415,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
   const int tid = w * 32 + lane;
   const int nout = tl.ze - tl.zs;
   int eoff = 0;
-  const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, a.wr, g, tl.x0, y, tl.zs, w * RW, K == 2 && rowok, lane,
+  const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, wr_, g, tl.x0, y, tl.zs, w * RW, K == 2 && rowok, lane,
                               eoff);
   auto pcopy = [&](int j, int slot) {  // (K >= 3) b (+ d_2) of output plane zs + j -> aux slot
     if (K >= 3 && rowok) {
@@ -1515,7 +1523,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
       } else if (K == 2) {
         if (rowok) {
           const uint32_t* rec = wring + osl * FW * RW + w * RW;
-          const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
+          const double rv = dec_rec<WR>(rec, rec_e(rec + wr_, eoff), wr_, lane);
           const T b = (T)rv - av;  // b = dec r - A z (B lives in the t_L buffer)
           *Tp = (double)b;
           if (Yo) {
@@ -1562,7 +1570,7 @@ struct F3S2 {
   static constexpr int NBF = P + 4;         // ring slots: pair being read, pair in flight, centre planes i - P
   static constexpr int NW = PF + 4;         // word / point slots per output
 };
-template <int P, int K, class T = double>
+template <int P, int K, class T = double, int WR = 0>
 __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const __grid_constant__ F3Args a,
                                                                       const __grid_constant__ CoefT<T> cf) {
   static_assert(K >= 2 || sizeof(T) == 8, "the residual is FP64");
@@ -1576,7 +1584,8 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
   T* XB = XA + 2 * NR * 32;
   double* aring = ring + NBF * BOX + 4 * NR * 32;  // (K >= 3) NW x NX_ x 256
   uint32_t* wring = (uint32_t*)(aring + (K >= 3 ? NW * NX_ * 32 * FW : 0));  // (K = 2) NW x FW x (w_r + 1)
-  const int RW = a.wr + 1;
+  const int wr_ = WR > 0 ? WR : a.wr;  // (K = 2: w_r(L, L), compile-time for the common widths)
+  const int RW = wr_ + 1;
   unsigned long long* bars = (unsigned long long*)(wring + (K == 2 ? NW * FW * RW + 2 : 0));
   bars = (unsigned long long*)(((uintptr_t)bars + 7) & ~(uintptr_t)7);
   const int lane = threadIdx.x, w = threadIdx.y;
@@ -1616,7 +1625,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
   const int tid = w * 32 + lane;
   const int nout = tl.ze - tl.zs;
   int eoff = 0;
-  const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, a.wr, g, tl.x0, y, tl.zs, w * RW, K == 2 && rowok, lane,
+  const WStream ws = wstream1(a.rmant, a.rexp, a.rstride, wr_, g, tl.x0, y, tl.zs, w * RW, K == 2 && rowok, lane,
                               eoff);
   auto pcopy = [&](int j, int slot) {
     if (K >= 3 && rowok) {
@@ -1693,7 +1702,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
     } else if (K == 2) {
       if (rowok) {
         const uint32_t* rec = wring + os * FW * RW + w * RW;
-        const double rv = warp_decode(rec, rec_e(rec + a.wr, eoff), a.wr, lane);
+        const double rv = dec_rec<WR>(rec, rec_e(rec + wr_, eoff), wr_, lane);
         const T b = (T)rv - av;
         *Tp = (double)b;
         if (Yo) {
@@ -1972,10 +1981,22 @@ static int smem_staged2(int wr, int nx);
 template <int P>
 static int smem_staged(int wr, int nx);
 // k_f3_staged (one plane per iteration) or k_f3_staged2 (two; F3Args::s2)
+template <int P, int K, class T, int WR>
+static void staged_launch_w(cudaStream_t st, const F3Args& a, const CoefT<T>& ct, int wr, int nx) {
+  if (a.s2) f3_launch(k_f3_staged2<P, K, T, WR>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
+  else f3_launch(k_f3_staged<P, K, T, WR>, a.nitems, smem_staged<P>(wr, nx), st, a, ct);
+}
+// (K = 2: compile-time r_L widths 4, 5, 6 -- b_r = 4, k_r = 1 at the top
+// three levels of every bench schedule; FMG_WR0=1 forces the runtime width)
 template <int P, int K, class T = double>
 static void staged_launch(cudaStream_t st, const F3Args& a, const CoefT<T>& ct, int wr, int nx) {
-  if (a.s2) f3_launch(k_f3_staged2<P, K, T>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
-  else f3_launch(k_f3_staged<P, K, T>, a.nitems, smem_staged<P>(wr, nx), st, a, ct);
+  if constexpr (K == 2) {
+    const bool rt = getenv("FMG_WR0") && atoi(getenv("FMG_WR0")) != 0;  // (read at graph build)
+    if (!rt && wr == 4) return staged_launch_w<P, K, T, 4>(st, a, ct, wr, nx);
+    if (!rt && wr == 5) return staged_launch_w<P, K, T, 5>(st, a, ct, wr, nx);
+    if (!rt && wr == 6) return staged_launch_w<P, K, T, 6>(st, a, ct, wr, nx);
+  }
+  staged_launch_w<P, K, T, 0>(st, a, ct, wr, nx);
 }
 template <int P>
 static int smem_staged2(int wr, int nx) {
@@ -2032,6 +2053,11 @@ int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
 
 void fine3_set_attributes() {
   const int big = 200 * 1024;
+#define W2(P, W)                                                                                           \
+  cudaFuncSetAttribute(k_f3_staged<P, 2, double, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
+  cudaFuncSetAttribute(k_f3_staged2<P, 2, double, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  cudaFuncSetAttribute(k_f3_staged<P, 2, float, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);   \
+  cudaFuncSetAttribute(k_f3_staged2<P, 2, float, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
 #define F(P)                                                                                        \
   cudaFuncSetAttribute(k_f3_residual<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
   cudaFuncSetAttribute(k_f3_residual<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -2067,10 +2093,12 @@ void fine3_set_attributes() {
   cudaFuncSetAttribute(k_f3_staged<P, 3, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);   \
   cudaFuncSetAttribute(k_f3_staged<P, 4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);   \
   cudaFuncSetAttribute(k_f3_staged2<P, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
+  W2(P, 4) W2(P, 5) W2(P, 6)                                                                          \
   cudaFuncSetAttribute(k_f3_staged2<P, 3, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
   cudaFuncSetAttribute(k_f3_staged2<P, 4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   F(1) F(2) F(3)
 #undef F
+#undef W2
 #define TW(T_, W_, R_) \
   cudaFuncSetAttribute(k_f3_tpb<1, T_, W_, R_>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
 #define TWS(T_) TW(T_, 4, 4) TW(T_, 6, 4) TW(T_, 6, 5) TW(T_, 8, 5) TW(T_, 8, 6) TW(T_, 10, 5) TW(T_, 14, 6) TW(T_, 5, 4) TW(T_, 8, 4)

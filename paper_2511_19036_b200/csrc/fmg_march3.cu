@@ -705,7 +705,13 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_sq(const DevCt
 // fine plane box (64+4p-2 x 16+4p-2) is staged, x-passed to the coarse columns
 // and y-passed to the coarse rows; the z pass runs on a register ring of the
 // last 4p-1 fine planes (two new planes per coarse output plane).
-constexpr int RPF3 = 2, RNB3 = 3, RRS3 = 80;
+#ifndef FMG_RPF3
+#define FMG_RPF3 2
+#endif
+#ifndef FMG_RNB3
+#define FMG_RNB3 3
+#endif
+constexpr int RPF3 = FMG_RPF3, RNB3 = FMG_RNB3, RRS3 = 80;  // planes staged ahead, ring slots, cp.async row stride
 // TMA form (a.tma): the fine plane box starts at the even column 2 x0 - 2p and
 // is 64 + 4p doubles wide (16-byte rows), so fine column fxs sits at index 1.
 template <int P>
@@ -794,8 +800,21 @@ __global__ void __launch_bounds__(32 * TW3, FMG_MARCH3_MINB) k_m3_restrict(const
     for (int r = w; r < FR; r += TW3) {
       const double* row = slot + r * SROW;
       double v = 0.0;
+      if (TMA) {
+        // (slot index 1 + even + 2 lane + s: taps s = 1, 2 | 3, 4 | ... sit at
+        // 16-byte aligned pairs -> one 128-bit load each, half the wavefronts of
+        // the stride-2 double loads; same fma order)
+        v = fma(rw[0], row[2 * lane], v);
 #pragma unroll
-      for (int s = 0; s < NS; ++s) v = fma(rw[s], row[2 * lane + s], v);  // (t = +0 at fine non-unknowns)
+        for (int k = 0; k < (NS - 1) / 2; ++k) {
+          const double2 q = *reinterpret_cast<const double2*>(row + 2 * lane + 1 + 2 * k);
+          v = fma(rw[1 + 2 * k], q.x, v);
+          v = fma(rw[2 + 2 * k], q.y, v);
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) v = fma(rw[s], row[2 * lane + s], v);  // (t = +0 at fine non-unknowns)
+      }
       XR[r * 32 + lane] = v;
     }
     __syncthreads();
