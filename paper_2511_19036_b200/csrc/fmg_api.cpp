@@ -99,6 +99,7 @@ struct fmg_ctx {
   bool tpb0 = false;  // lean form: the generating residual's r_L encoded thread per block (k_f3_tpb<0>)
   bool tpby = false;  // lean form: the top level's last step stores ý as int8 mantissas (k_f3_tpb<2>)
   bool s2 = false;    // staged kernels two input planes per iteration (k_f3_staged2; FMG_S2)
+  bool f32s = false;  // FP32 cFas with float storage of z_l, b_l, y_j, d_2 at the staged levels (FMG_F32S)
   bool chk = false;   // lean form in z chunks: u_L / z_L materialised chunk by chunk (FMG_CHK)
   int chk_rc = 0;     // planes per chunk
   double* chkbuf = nullptr;
@@ -148,17 +149,17 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   return fn;
 }
 
-// FP64 tiled map over a [nz][ny][nx] array (rank 2 when nz == 0), box
-// bx x by x 1, out-of-range elements zero-filled.
-bool make_tmap(CUtensorMap* m, const double* base, long long nx, long long ny, long long nz, int bx, int by) {
+// FP64 (esz = 8) or FP32 (esz = 4) tiled map over a [nz][ny][nx] array
+// (rank 2 when nz == 0), box bx x by x 1, out-of-range elements zero-filled.
+bool make_tmap(CUtensorMap* m, const void* base, long long nx, long long ny, long long nz, int bx, int by, int esz = 8) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tma_encoder();
   if (!enc || !base) return false;
   const cuuint32_t rank = nz > 0 ? 3 : 2;
   cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)(nz > 0 ? nz : 1)};
-  cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
+  cuuint64_t strides[2] = {(cuuint64_t)nx * esz, (cuuint64_t)nx * ny * esz};
   cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, (void*)base, dims, strides, box, es,
+  CUresult r = enc(m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, (void*)base, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -737,6 +738,7 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
              fine3_tpby_width(o.wu_in, o.wr) && (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= c->tpb_min;
   }
   a.cfs = (it.f3kind == 1 || it.f3kind == 2) ? o.cfs : 0;
+  a.f32s = c->f32s && a.cfs != 0;
   a.csc = c->csc;
   a.X1b = sview(c, 3, l);
   a.tmx1 = c->tm_dev + 11 * kMaxLev + l;
@@ -1340,6 +1342,11 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     c->tpb0 = !(et && atoi(et) == 0);
     const char* es = getenv("FMG_CSC");
     c->csc = c->cfs && (es ? atoi(es) != 0 : p == 3);
+    // FP32 cFas with the staged Chebyshev steps: z_l, b_l, y_j and d_2 stored
+    // as float (half the bytes of the staged kernels, which are HBM-bound in
+    // FP32: profiles/r2b_summary.md).  FMG_F32S=0 keeps FP64 storage.
+    const char* efs = getenv("FMG_F32S");
+    c->f32s = s->cfas_fp32 && c->csc && c->s2 && !(efs && atoi(efs) == 0);
   }
   for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
     const long long plane = (long long)c->g[l].NX * c->g[l].NY, off = plane * c->wlo[l];
@@ -1478,8 +1485,10 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     if (l >= 1) {
       ok &= make_tmap(&c->tmFB[l], c->Tl[l] + off, g.NX, g.NY, nz, rs, nr);
       if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->sbase[4], g.NX, g.NY, nz, rs, nr);
-      if (c->cfs) ok &= make_tmap(&c->tmYB[l], c->sbase[2], g.NX, g.NY, nz, rs, nr);
-      if (c->csc) ok &= make_tmap(&c->tmX1[l], c->sbase[3], g.NX, g.NY, nz, rs, nr);
+      const int es = c->f32s ? 4 : 8;  // (float storage: float boxes of Y, X1 and the Z scratch)
+      if (c->cfs) ok &= make_tmap(&c->tmYB[l], c->sbase[2], g.NX, g.NY, nz, rs, nr, es);
+      if (c->csc) ok &= make_tmap(&c->tmX1[l], c->sbase[3], g.NX, g.NY, nz, rs, nr, es);
+      if (c->f32s && l < Lmax) ok &= make_tmap(&c->tmB[0][l], c->sbase[0], g.NX, g.NY, nz, rs, nr, 4);
       if (c->chk) ok &= make_tmap(&c->tmCH[l], c->chkbuf, g.NX, g.NY, std::min<long long>(g.NZ, c->chk_rc + 2 * p), rs, nr);
     }
     if (!ok) rc = FMG_ECUDA;

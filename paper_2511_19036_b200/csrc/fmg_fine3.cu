@@ -1021,6 +1021,8 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
   const long long o0 = ((long long)tl.zs * g.NY + y) * g.NX + x;
   double* out = (decode ? a.U : a.PU) + o0;
   double* out2 = NA == 2 ? a.out2 + o0 : nullptr;
+  float* out2f = NA == 2 ? (float*)a.out2 + o0 : nullptr;  // (FP32 cFas, float storage: z_l as float)
+  const bool fs2 = FW2 && a.f32s;
   const CUtensorMap* tms[2] = {a.tmc, NA == 2 ? a.tmc2 : a.tmc};
   const int nout = tl.ze - tl.zs;
   if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -1133,10 +1135,13 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong(const __grid_constant
       }
     } else if (rowok) {
       *out = pu[0];
-      if (NA == 2) *out2 = pu[NA - 1];
+      if (NA == 2) {
+        if (fs2) *out2f = (float)pu[NA - 1];
+        else *out2 = pu[NA - 1];
+      }
     }
     out += tplane;
-    if (NA == 2) out2 += tplane;
+    if (NA == 2) out2 += tplane, out2f += tplane;
     osl = osl + 1 == NW ? 0 : osl + 1;
   }
 }
@@ -1208,6 +1213,8 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
   const long long o0 = ((long long)tl.zs * g.NY + tl.y0 + w) * g.NX + x;
   double* out = (decode ? a.U : a.PU) + o0;
   double* out2 = NA == 2 ? a.out2 + o0 : nullptr;
+  float* out2f = NA == 2 ? (float*)a.out2 + o0 : nullptr;  // (FP32 cFas, float storage: z_l as float)
+  const bool fs2 = FW2 && a.f32s;
   const long long rs8 = (long long)FW * g.NX;  // the second row, 8 rows down
   const CUtensorMap* tms[2] = {a.tmc, NA == 2 ? a.tmc2 : a.tmc};
   const int nout = tl.ze - tl.zs;
@@ -1337,11 +1344,14 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
       for (int h = 0; h < 2; ++h)
         if (rowok[h]) {
           out[h * rs8] = pu[0][h];
-          if (NA == 2) out2[h * rs8] = pu[NA - 1][h];
+          if (NA == 2) {
+            if (fs2) out2f[h * rs8] = (float)pu[NA - 1][h];
+            else out2[h * rs8] = pu[NA - 1][h];
+          }
         }
     }
     out += tplane;
-    if (NA == 2) out2 += tplane;
+    if (NA == 2) out2 += tplane, out2f += tplane;
     osl = osl + 1 == NW ? 0 : osl + 1;
   }
 }
@@ -1570,7 +1580,7 @@ struct F3S2 {
   static constexpr int NBF = P + 4;         // ring slots: pair being read, pair in flight, centre planes i - P
   static constexpr int NW = PF + 4;         // word / point slots per output
 };
-template <int P, int K, class T = double, int WR = 0>
+template <int P, int K, class T = double, int WR = 0, bool FS = false>
 __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const __grid_constant__ F3Args a,
                                                                       const __grid_constant__ CoefT<T> cf) {
   static_assert(K >= 2 || sizeof(T) == 8, "the residual is FP64");
@@ -1578,11 +1588,18 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
   constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX;
   constexpr int NBF = F3S2<P>::NBF, PF = F3S2<P>::PF, NW = F3S2<P>::NW;
   constexpr int NX_ = K == 4 ? 2 : 1;
+  // FS: FP32 cFas with float storage: the staged input and
+  // the point arrays (z_l, b, y_j, d_2) are float arrays over the same
+  // buffers, float TMA boxes start at x0 - 4 (16-byte aligned), shift 4 - P
+  static_assert(!FS || (sizeof(T) == 4 && K >= 2), "float storage: FP32 cFas only");
+  using S = typename std::conditional<FS, float, double>::type;
+  constexpr int SHS = FS ? 4 - P : (P & 1);
+  constexpr int BOXS = FS ? ((BOX + 31) & ~31) : BOX;  // ring slot stride (TMA destinations 128-byte aligned)
   extern __shared__ __align__(128) double fsm[];
-  double* ring = fsm;                     // NBF boxes of v
-  T* XA = (T*)(ring + NBF * BOX);         // 2 planes x NR x 32 (T = float: FP32 cFas, reading R28)
+  S* ring = (S*)fsm;                      // NBF boxes of v
+  T* XA = (T*)(fsm + NBF * BOX);          // 2 planes x NR x 32 (T = float: FP32 cFas, reading R28)
   T* XB = XA + 2 * NR * 32;
-  double* aring = ring + NBF * BOX + 4 * NR * 32;  // (K >= 3) NW x NX_ x 256
+  S* aring = (S*)(fsm + NBF * BOX + 4 * NR * 32);  // (K >= 3) NW x NX_ x 256
   uint32_t* wring = (uint32_t*)(aring + (K >= 3 ? NW * NX_ * 32 * FW : 0));  // (K = 2) NW x FW x (w_r + 1)
   const int wr_ = WR > 0 ? WR : a.wr;  // (K = 2: w_r(L, L), compile-time for the common widths)
   const int RW = wr_ + 1;
@@ -1613,9 +1630,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
   const int z0 = tl.zs - P, nin = (tl.ze - tl.zs) + 2 * P;
   const long long tplane = (long long)g.NY * g.NX, bpp = (long long)g.NY * nxb;
   const long long pbase0 = ((long long)tl.zs * g.NY + y) * g.NX + x;
-  double* Tp = a.T + pbase0;
-  double* Yo = a.yout ? a.yout + pbase0 : nullptr;
-  double* Dp = a.Dv + pbase0;
+  double* Tp = a.T + pbase0;                               // (K < 2: t_L)
+  S* Bp = (S*)a.T + pbase0;                                // (K = 2: b_l)
+  S* Yo = a.yout ? (S*)a.yout + pbase0 : nullptr;
+  S* Dp = (S*)a.Dv + pbase0;
+  const S* Tsrc = (const S*)a.T + pbase0;
+  const S* Dsrc = (const S*)a.Dv + pbase0;
   const long long blk0 = ((long long)tl.zs * g.NY + y) * nxb + (tl.x0 >> 5);
   uint32_t* rmp = a.rmant + blk0 * a.rstride;
   int8_t* rep = a.rexp + blk0;
@@ -1629,10 +1649,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
                               eoff);
   auto pcopy = [&](int j, int slot) {
     if (K >= 3 && rowok) {
-      const unsigned d = aring_s + (unsigned)(((slot * NX_) * 32 * FW + tid) * 8);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(a.T + pbase0 + j * tplane) : "memory");
+      constexpr unsigned SZ = sizeof(S);
+      const unsigned d = aring_s + (unsigned)(((slot * NX_) * 32 * FW + tid) * SZ);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d), "l"(Tsrc + j * tplane), "n"(SZ) : "memory");
       if (K == 4)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 32 * FW * 8), "l"(a.Dv + pbase0 + j * tplane)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d + 32 * FW * SZ), "l"(Dsrc + j * tplane),
+                     "n"(SZ)
                      : "memory");
     }
   };
@@ -1650,12 +1672,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
   __syncthreads();
   pdl_wait();
   pdl_trigger();
-  const int tmx = tl.x0 - P - (P & 1), tmy = tl.y0 - P;
+  const int tmx = tl.x0 - P - SHS, tmy = tl.y0 - P;
   auto stage = [&](int i, int slot) {
     if (threadIdx.x == 0 && threadIdx.y == 0) {
-      const unsigned dst = ring_s + (unsigned)(slot * BOX * 8), bar = bars_s + (unsigned)(slot * 8);
+      const unsigned dst = ring_s + (unsigned)(slot * BOXS * sizeof(S)), bar = bars_s + (unsigned)(slot * 8);
       fence_async_smem();
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(BOX * 8))
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(BOX * sizeof(S)))
                    : "memory");
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -1683,19 +1705,19 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
     const bool uz = unk1(z, n);
     if (K >= 3) {
       if (rowok) {
-        const double* ax = aring + os * NX_ * 32 * FW + tid;
+        const S* ax = aring + os * NX_ * 32 * FW + tid;
         const T b = (T)ax[0];
         T f = fv[0];
 #pragma unroll
         for (int t = 1; t < P; ++t) f = tzo == t ? fv[t] : f;
         f = uz ? f : (T)0;
-        const T yprev = (T)ring[ois * BOX + C::SH + (w + P) * RS + P + lane];
+        const T yprev = (T)ring[ois * BOXS + SHS + (w + P) * RS + P + lane];
         const T dprev = K == 4 ? (T)ax[32 * FW] : yprev;
         const T qq = b - av;
         const T d = fma(al, dprev, be * (f * qq));
         const T yv = yprev + d;
-        *Yo = (double)yv;
-        if (!a.last) *Dp = (double)d;
+        *Yo = (S)yv;
+        if (!a.last) *Dp = (S)d;
       }
       Yo += tplane;
       Dp += tplane;
@@ -1704,12 +1726,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
         const uint32_t* rec = wring + os * FW * RW + w * RW;
         const double rv = dec_rec<WR>(rec, rec_e(rec + wr_, eoff), wr_, lane);
         const T b = (T)rv - av;
-        *Tp = (double)b;
+        *Bp = (S)b;
         if (Yo) {
           T f = fv[0];
 #pragma unroll
           for (int t = 1; t < P; ++t) f = tzo == t ? fv[t] : f;
-          *Yo = (double)(ith * ((uz ? f : (T)0) * b));
+          *Yo = (S)(ith * ((uz ? f : (T)0) * b));
         }
       }
       if (Yo) Yo += tplane;
@@ -1721,6 +1743,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
       if (K == 0) warp_encode(t, a.wr, rmp, rep, lane, a.status);
     }
     Tp += tplane;
+    Bp += tplane;
     rmp += rstep;
     rep += bpp;
   };
@@ -1750,8 +1773,8 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
     }
     // x pass of both planes: rows w, w + 8 of each (four independent pairs of chains)
     {
-      const double* b0 = ring + isl * BOX + C::SH;
-      const double* b1 = ring + isl1 * BOX + C::SH;
+      const S* b0 = ring + isl * BOXS + SHS;
+      const S* b1 = ring + isl1 * BOXS + SHS;
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int r = w + k * FW;
@@ -1836,8 +1859,9 @@ constexpr int tpb_smem_bytes() { return TP_WARPS * (32 * TP_RS * 8 + 32 * TP_WS 
 
 // W, WR > 0: compile-time widths (tpb_*_w): MODE 1 without w_l with w_u = W,
 // w_r = WR; MODE 0 with w_r = WR.  0: the runtime-width routines.
-template <int MODE, class T, int W = 0, int WR = 0>
+template <int MODE, class T, int W = 0, int WR = 0, bool FS = false>
 __global__ void __launch_bounds__(TP_WARPS * 32, 4) k_f3_tpb(const __grid_constant__ F3Args a) {
+  static_assert(!FS || (MODE == 1 && sizeof(T) == 4), "float storage: FP32 cFas, MODE 1");
   extern __shared__ __align__(16) double tsm[];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   double* A = tsm + wp * 32 * TP_RS;  // t_l (MODE 0) / y_k -> ý -> dec ú_l + ý -> the new ú_l (MODE 1)
@@ -1887,8 +1911,14 @@ __global__ void __launch_bounds__(TP_WARPS * 32, 4) k_f3_tpb(const __grid_consta
       __syncwarp();
       continue;
     }
+    if constexpr (FS) {  // y_k stored as float (exact: it is a float value)
+      const float* Xf = (const float*)a.Dv;
 #pragma unroll 8
-    for (int r = 0; r < 32; ++r) cpa8(A + r * TP_RS + lane, X + (b0 + r) * 32 + lane, r < nb);
+      for (int r = 0; r < 32; ++r) A[r * TP_RS + lane] = r < nb ? (double)__ldg(Xf + (b0 + r) * 32 + lane) : 0.0;
+    } else {
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) cpa8(A + r * TP_RS + lane, X + (b0 + r) * 32 + lane, r < nb);
+    }
     if (MODE == 1)
       for (int o = lane; o < nb * wi; o += 32) {
         const int j = (int)__umulhi((unsigned)o, mi);
@@ -1929,7 +1959,9 @@ __global__ void __launch_bounds__(TP_WARPS * 32, 4) k_f3_tpb(const __grid_consta
         for (int r0 = 0; r0 < nb; r0 += 8) {
           double zv[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) zv[k] = r0 + k < nb ? __ldg(Zr + p0 + (r0 + k) * 32) : 0.0;
+          for (int k = 0; k < 8; ++k)
+            zv[k] = r0 + k < nb ? (FS ? (double)__ldg((const float*)Zr + p0 + (r0 + k) * 32) : __ldg(Zr + p0 + (r0 + k) * 32))
+                                : 0.0;
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             if (r0 + k < nb) Wr[p0 + (r0 + k) * 32] = (double)((T)zv[k] + (T)A[(r0 + k) * TP_RS + lane]);
@@ -1981,15 +2013,29 @@ static int smem_staged2(int wr, int nx);
 template <int P>
 static int smem_staged(int wr, int nx);
 // k_f3_staged (one plane per iteration) or k_f3_staged2 (two; F3Args::s2)
-template <int P, int K, class T, int WR>
+template <int P, int K, class T, int WR, bool FS = false>
 static void staged_launch_w(cudaStream_t st, const F3Args& a, const CoefT<T>& ct, int wr, int nx) {
-  if (a.s2) f3_launch(k_f3_staged2<P, K, T, WR>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
-  else f3_launch(k_f3_staged<P, K, T, WR>, a.nitems, smem_staged<P>(wr, nx), st, a, ct);
+  if constexpr (FS) {  // (float storage: two planes per iteration only; the host requires s2)
+    f3_launch(k_f3_staged2<P, K, T, WR, true>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
+  } else {
+    if (a.s2) f3_launch(k_f3_staged2<P, K, T, WR>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
+    else f3_launch(k_f3_staged<P, K, T, WR>, a.nitems, smem_staged<P>(wr, nx), st, a, ct);
+  }
 }
 // (K = 2: compile-time r_L widths 4, 5, 6 -- b_r = 4, k_r = 1 at the top
 // three levels of every bench schedule; FMG_WR0=1 forces the runtime width)
 template <int P, int K, class T = double>
 static void staged_launch(cudaStream_t st, const F3Args& a, const CoefT<T>& ct, int wr, int nx) {
+  if constexpr (sizeof(T) == 4 && K >= 2) {
+    if (a.f32s) {  // FP32 cFas with float storage
+      if constexpr (K == 2) {
+        if (wr == 4) return staged_launch_w<P, K, T, 4, true>(st, a, ct, wr, nx);
+        if (wr == 5) return staged_launch_w<P, K, T, 5, true>(st, a, ct, wr, nx);
+        if (wr == 6) return staged_launch_w<P, K, T, 6, true>(st, a, ct, wr, nx);
+      }
+      return staged_launch_w<P, K, T, 0, true>(st, a, ct, wr, nx);
+    }
+  }
   if constexpr (K == 2) {
     const bool rt = getenv("FMG_WR0") && atoi(getenv("FMG_WR0")) != 0;  // (read at graph build)
     if (!rt && wr == 4) return staged_launch_w<P, K, T, 4>(st, a, ct, wr, nx);
@@ -2053,6 +2099,8 @@ int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
 
 void fine3_set_attributes() {
   const int big = 200 * 1024;
+#define FS2(P, K, W) \
+  cudaFuncSetAttribute(k_f3_staged2<P, K, float, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
 #define W2(P, W)                                                                                           \
   cudaFuncSetAttribute(k_f3_staged<P, 2, double, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
   cudaFuncSetAttribute(k_f3_staged2<P, 2, double, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -2094,16 +2142,22 @@ void fine3_set_attributes() {
   cudaFuncSetAttribute(k_f3_staged<P, 4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);   \
   cudaFuncSetAttribute(k_f3_staged2<P, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
   W2(P, 4) W2(P, 5) W2(P, 6)                                                                          \
+  FS2(P, 2, 0) FS2(P, 2, 4) FS2(P, 2, 5) FS2(P, 2, 6) FS2(P, 3, 0) FS2(P, 4, 0)                        \
   cudaFuncSetAttribute(k_f3_staged2<P, 3, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
   cudaFuncSetAttribute(k_f3_staged2<P, 4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   F(1) F(2) F(3)
 #undef F
 #undef W2
+#undef FS2
 #define TW(T_, W_, R_) \
   cudaFuncSetAttribute(k_f3_tpb<1, T_, W_, R_>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
 #define TWS(T_) TW(T_, 4, 4) TW(T_, 6, 4) TW(T_, 6, 5) TW(T_, 8, 5) TW(T_, 8, 6) TW(T_, 10, 5) TW(T_, 14, 6) TW(T_, 5, 4) TW(T_, 8, 4)
   TWS(double) TWS(float)
 #undef TWS
+#undef TW
+#define TW(W_, R_) \
+  cudaFuncSetAttribute(k_f3_tpb<1, float, W_, R_, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
+  TW(4, 4) TW(6, 4) TW(6, 5) TW(8, 5) TW(8, 6) TW(10, 5) TW(14, 6) TW(5, 4) TW(8, 4) TW(0, 0)
 #undef TW
   cudaFuncSetAttribute(k_f3_tpb<0, double, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tpb_smem_bytes());
 #define TW(W_, R_) \
@@ -2158,23 +2212,30 @@ static void f3_launch(K kernel, int nctas, int smem, cudaStream_t st, const F3Ar
 }
 
 // thread-per-block epilogue over the rank's planes (PDL-chained like the march kernels)
-template <int MODE, class T, int W = 0, int WR = 0>
+template <int MODE, class T, int W = 0, int WR = 0, bool FS = false>
 static void tpb_launch_w(cudaStream_t st, const F3Args& a);
 // compile-time widths for the common cases (the top levels of the bench
 // schedules), the runtime-width kernel otherwise
-template <int MODE, class T>
-static void tpb_launch(cudaStream_t st, const F3Args& a) {
+template <int MODE, class T, bool FS>
+static void tpb_launch_fs(cudaStream_t st, const F3Args& a) {
   if constexpr (MODE == 0) {
     if (a.wr == 4) return tpb_launch_w<MODE, T, 0, 4>(st, a);
   } else if (MODE == 2 || (!a.wout && a.wu == a.wu_out)) {
 #define TW(W_, R_) \
-  if (a.wu == W_ && a.wr == R_) return tpb_launch_w<MODE, T, W_, R_>(st, a);
+  if (a.wu == W_ && a.wr == R_) return tpb_launch_w<MODE, T, W_, R_, FS>(st, a);
     TW(4, 4) TW(6, 4) TW(6, 5) TW(8, 5) TW(8, 6) TW(10, 5) TW(14, 6) TW(5, 4) TW(8, 4)
 #undef TW
   }
-  if constexpr (MODE != 2) tpb_launch_w<MODE, T>(st, a);  // (MODE 2 only for the listed widths: fine3_tpby_width)
+  if constexpr (MODE != 2) tpb_launch_w<MODE, T, 0, 0, FS>(st, a);  // (MODE 2 only for the listed widths: fine3_tpby_width)
 }
-template <int MODE, class T, int W, int WR>
+template <int MODE, class T>
+static void tpb_launch(cudaStream_t st, const F3Args& a) {
+  if constexpr (MODE == 1 && sizeof(T) == 4) {
+    if (a.f32s) return tpb_launch_fs<MODE, T, true>(st, a);  // (y_k, z_l stored as float)
+  }
+  tpb_launch_fs<MODE, T, false>(st, a);
+}
+template <int MODE, class T, int W, int WR, bool FS>
 static void tpb_launch_w(cudaStream_t st, const F3Args& a) {
   const long long bpp = (long long)a.g.NY * (a.g.NX >> 5), nblk = (long long)(a.zhi - a.zlo) * bpp;
   const long long want = (nblk + 32 * TP_WARPS - 1) / (32 * TP_WARPS);
@@ -2196,7 +2257,7 @@ static void tpb_launch_w(cudaStream_t st, const F3Args& a) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   ++g_f3_launches;
-  cudaLaunchKernelEx(&cfg, k_f3_tpb<MODE, T, W, WR>, a);
+  cudaLaunchKernelEx(&cfg, k_f3_tpb<MODE, T, W, WR, FS>, a);
 }
 
 template <int P, class T>

@@ -167,6 +167,7 @@ struct F3Args {
   int tpby;                  // lean top level: the last step stores ý as int8 mantissas + exponents (my, ey)
   int8_t* my;                //   per point (level window)
   int8_t* ey;                //   per block
+  int f32s;                  // FP32 cFas with float storage at this level: z_l, b_l, y_j, d_2 are float arrays
 };
 
 // One deferred norm: ||t_l||_2 of norm row `row` from `count` partials at pbase + poff.

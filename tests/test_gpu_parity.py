@@ -457,7 +457,8 @@ def test_fmg_parity_fine3_variants(P, monkeypatch, variant, d, p, levels):
 _F3_VARIANTS_FP32 = {
     # FP32 cFas in the staged kernels: P w_{l-1} (prolongation, second array),
     # b_l, y_1 (k_f3_staged<P, 2, float>) and the staged Chebyshev steps
-    "staged": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="1"),
+    "staged": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="1"),  # (float storage of z, b, y, d_2)
+    "staged_f64_storage": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="1", FMG_F32S="0"),
     "staged_s1": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="0"),
     "staged_no_csc": dict(FMG_CFS="1", FMG_CSC="0"),
     # the generating cFas kernels (k_f3_cfas / k_f3_cheb<P, J, float>)
