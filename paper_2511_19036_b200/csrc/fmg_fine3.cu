@@ -1202,6 +1202,15 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
     byo[h] = oky[h] ? P * (y / (2 * P)) - gn.cy0 : 0;
     ry[h] = oky[h] ? y % (2 * P) : 0;
   }
+  double pwy[2][P + 1];  // y-pass weights of the warp's two rows (registers, not per-tap constant loads)
+  TW pwyw[2][P + 1];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int t = 0; t <= P; ++t) {
+      pwy[h][t] = cf.Pw[ry[h]][t];
+      pwyw[h][t] = (TW)pwy[h][t];
+    }
   const bool decode = NA == 1 && a.step == 1;
   int eoff[2] = {0, 0};
   const WStream ws0 = wstream1(a.umant, a.uexp, a.ustride, a.wu, g, tl.x0, tl.y0 + w, tl.zs, w * RW,
@@ -1291,15 +1300,14 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
               TW acc = 0;
               if (oky[h]) {
 #pragma unroll
-                for (int t = 0; t <= P; ++t)
-                  acc = fma((TW)cf.Pw[ry[h]][t], (TW)PX[(q * CBY + byo[h] + t) * 32 + lane], acc);
+                for (int t = 0; t <= P; ++t) acc = fma(pwyw[h][t], (TW)PX[(q * CBY + byo[h] + t) * 32 + lane], acc);
               }
               yv[((q * NCY + c % NCY) * TH + w + h * FW) * 32 + lane] = (double)acc;
             } else {
               double acc = 0.0;
               if (oky[h]) {
 #pragma unroll
-                for (int t = 0; t <= P; ++t) acc = fma(cf.Pw[ry[h]][t], PX[(q * CBY + byo[h] + t) * 32 + lane], acc);
+                for (int t = 0; t <= P; ++t) acc = fma(pwy[h][t], PX[(q * CBY + byo[h] + t) * 32 + lane], acc);
               }
               yv[((q * NCY + c % NCY) * TH + w + h * FW) * 32 + lane] = acc;
             }
@@ -1309,23 +1317,33 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
       }
     }
     double pu[NA][2];
+    // z pass: per plane the P + 1 weights and the ring rows of the taps once
+    // (shared by both arrays and both rows; constant offsets below)
+    const int rz = okz ? z % (2 * P) : 0, cb0 = okz ? cbase<P>(z) : 0;
+    double pz[P + 1];
+    TW pzw[P + 1];
+    const double* ys[P + 1];
+#pragma unroll
+    for (int t = 0; t <= P; ++t) {
+      pz[t] = cf.Pw[rz][t];
+      pzw[t] = (TW)pz[t];
+      ys[t] = yv + (((cb0 + t) % NCY) * TH + w) * 32 + lane;
+    }
 #pragma unroll
     for (int q = 0; q < NA; ++q)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         pu[q][h] = 0.0;
         if (okz) {
-          const int rz = z % (2 * P), cb0 = cbase<P>(z);
+          const int off = (q * NCY * TH + h * FW) * 32;
           if (FW2 && q == 1) {
             TW acc = 0;
 #pragma unroll
-            for (int t = 0; t <= P; ++t)
-              acc = fma((TW)cf.Pw[rz][t], (TW)yv[((q * NCY + (cb0 + t) % NCY) * TH + w + h * FW) * 32 + lane], acc);
+            for (int t = 0; t <= P; ++t) acc = fma(pzw[t], (TW)ys[t][off], acc);
             pu[q][h] = (double)acc;
           } else {
 #pragma unroll
-            for (int t = 0; t <= P; ++t)
-              pu[q][h] = fma(cf.Pw[rz][t], yv[((q * NCY + (cb0 + t) % NCY) * TH + w + h * FW) * 32 + lane], pu[q][h]);
+            for (int t = 0; t <= P; ++t) pu[q][h] = fma(pz[t], ys[t][off], pu[q][h]);
           }
         }
       }
