@@ -393,6 +393,25 @@ def test_fmg_parity_C4_full_oracle(P):
     compare_solvers(P, c["dim"], c["p"], c["levels"], check_r=False)
 
 
+@pytest.mark.skipif(os.environ.get("FMG_FULL_ORACLE") != "1",
+                    reason="C3 full-size FP32-cFas oracle solve takes ~6 min and ~21 GB host RAM (opt-in)")
+def test_fmg_parity_C3_full_oracle_fp32(P):
+    """C3 at full size with FP32 cFas (reading R28; the p = 1 staged kernels
+    with FP64 storage) against the oracle's FP32 mode: every solution section
+    bit-identical."""
+    c = CONFIGS["C3"]
+    compare_solvers(P, c["dim"], c["p"], c["levels"], check_r=False, cfas_fp32=1)
+
+
+@pytest.mark.skipif(os.environ.get("FMG_FULL_ORACLE") != "1",
+                    reason="C4 full-size FP32-cFas oracle solve takes ~12 min and ~70 GB host RAM (opt-in)")
+def test_fmg_parity_C4_full_oracle_fp32(P):
+    """C4 at full size with FP32 cFas (the float-storage staged kernels)
+    against the oracle's FP32 mode: every solution section bit-identical."""
+    c = CONFIGS["C4"]
+    compare_solvers(P, c["dim"], c["p"], c["levels"], check_r=False, cfas_fp32=1)
+
+
 @pytest.mark.parametrize("lc", ["1", "2", "3"])
 @pytest.mark.parametrize("d,p,levels", [(2, 2, 7), (2, 1, 8), (3, 1, 6), (3, 2, 5)])
 def test_kc_per_iteration_mode_parity(P, monkeypatch, lc, d, p, levels):
