@@ -54,6 +54,9 @@
 #ifndef F3_MINB_RS
 #define F3_MINB_RS(P) F3_MINB(P)  // k_f3_residual_s
 #endif
+#ifndef FMG_S2T
+#define FMG_S2T 1
+#endif
 #ifndef F3_MINB_RS32
 #define F3_MINB_RS32(P) ((P) == 3 ? 3 : F3_MINB(P))  // the staged kernels in FP32 cFas (fewer registers)
 #endif
@@ -1765,8 +1768,15 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
     rmp += rstep;
     rep += bpp;
   };
-  for (int i = 0; i < nin; i += 2) {
+  // (the loop body specialised on whether the pair is complete: all pairs
+  // but a possible last single plane; FMG_S2T=0 build flag restores one body)
+  auto body = [&](int i, auto twoc) {
+#if FMG_S2T
+    constexpr bool two = decltype(twoc)::value;
+#else
+    (void)twoc;
     const bool two = i + 1 < nin;
+#endif
     const int isl1 = isl + 1 == NBF ? 0 : isl + 1;
     const unsigned par1 = isl + 1 == NBF ? par ^ 1u : par;
     mbar_wait_s(bars_s + 8u * (unsigned)isl, par);
@@ -1852,6 +1862,11 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
     oisl = oisl1 + 1 == NBF ? 0 : oisl1 + 1;
     isl = isl1 + 1 == NBF ? 0 : isl1 + 1;
     par = (isl1 + 1 == NBF) ? par1 ^ 1u : par1;
+  };
+  {
+    int i = 0;
+    for (; i + 1 < nin; i += 2) body(i, std::true_type{});
+    if (i < nin) body(i, std::false_type{});
   }
   if (K < 2) {
 #pragma unroll
