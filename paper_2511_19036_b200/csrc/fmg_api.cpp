@@ -289,6 +289,13 @@ OpDesc mkop(int type, int l, int L) {
 // DESIGN.md §4.3): [P u_{l-1} -> PU], z_l generated on chip -> b_l (+ z_l -> Z
 // below the finest level), Chebyshev steps 2..k; the last one applies the
 // correction and, below the finest level (or materialised), writes w_l and
+// Levels of >= tpb_min blocks in the materialised form on one GPU: cFas step 1
+// from a materialised z_l (k_f3_staged<P, 2>), and with FP32 cFas the float
+// storage of the cFas arrays.
+static bool level_cfs(const fmg_ctx* c, int l) {
+  return c->cfs && (long long)(c->zhi[l] - c->zlo[l]) * c->g[l].NY * (c->g[l].NX / 32) >= c->tpb_min;
+}
+
 // u_l.  `xch`: z-slab ghost exchanges before each stencil consumer.
 void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
   fmg_ctx* c = b.c;
@@ -297,7 +304,7 @@ void add_fine3_level(Builder& b, int l, int L, bool fine, bool xch) {
   // materialised form on one GPU, levels of >= 2^16 blocks: z_l = P w_{l-1}
   // materialised for cFas step 1 (in Y at the top level, in the Z scratch
   // below it, where the last step needs z_l again), P u_{l-1} in the same launch
-  const bool cfs = c->cfs && (long long)(c->zhi[l] - c->zlo[l]) * c->g[l].NY * (c->g[l].NX / 32) >= c->tpb_min;
+  const bool cfs = level_cfs(c, l);
   if (uout && !cfs) {  // P u_{l-1} at the level's points (k_f3_prolong)
     if (xch) b.xchg(XA_U, l - 1, P);
     OpDesc q = mkop(OP_PROLONG, l, L);
@@ -738,7 +745,8 @@ F3Args fine3_args(const fmg_ctx* c, const Item& it) {
              fine3_tpby_width(o.wu_in, o.wr) && (long long)(a.zhi - a.zlo) * a.g.NY * a.nxb >= c->tpb_min;
   }
   a.cfs = (it.f3kind == 1 || it.f3kind == 2) ? o.cfs : 0;
-  a.f32s = c->f32s && a.cfs != 0;
+  // (the staged levels: cFas step 1 from a materialised z_l, add_fine3_level)
+  a.f32s = c->f32s && (it.f3kind == 1 || it.f3kind == 2) && level_cfs(c, l);
   a.csc = c->csc;
   a.X1b = sview(c, 3, l);
   a.tmx1 = c->tm_dev + 11 * kMaxLev + l;
@@ -1346,7 +1354,7 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
     // as float (half the bytes of the staged kernels, which are HBM-bound in
     // FP32: profiles/r2b_summary.md).  FMG_F32S=0 keeps FP64 storage.
     const char* efs = getenv("FMG_F32S");
-    c->f32s = s->cfas_fp32 && c->csc && c->s2 && !(efs && atoi(efs) == 0);
+    c->f32s = s->cfas_fp32 && c->cfs && (!c->csc || c->s2) && !(efs && atoi(efs) == 0);
   }
   for (int l = 0; l <= Lmax && rc == FMG_OK; ++l) {
     const long long plane = (long long)c->g[l].NX * c->g[l].NY, off = plane * c->wlo[l];
@@ -1483,8 +1491,9 @@ static int create_impl(int dim, int p, int levels, const fmg_schedule* s, void* 
       ok &= make_tmap(&c->tmCW[l], c->Wl[l] + off, g.NX, g.NY, nz, cbx, cby);
     }
     if (l >= 1) {
-      ok &= make_tmap(&c->tmFB[l], c->Tl[l] + off, g.NX, g.NY, nz, rs, nr);
-      if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->sbase[4], g.NX, g.NY, nz, rs, nr);
+      const int ef = c->f32s && level_cfs(c, l) ? 4 : 8;  // (float storage of b, d_2 at the staged levels)
+      ok &= make_tmap(&c->tmFB[l], c->Tl[l] + off, g.NX, g.NY, nz, rs, nr, ef);
+      if (s->cheb_degree >= 3) ok &= make_tmap(&c->tmFD[l], c->sbase[4], g.NX, g.NY, nz, rs, nr, ef);
       const int es = c->f32s ? 4 : 8;  // (float storage: float boxes of Y, X1 and the Z scratch)
       if (c->cfs) ok &= make_tmap(&c->tmYB[l], c->sbase[2], g.NX, g.NY, nz, rs, nr, es);
       if (c->csc) ok &= make_tmap(&c->tmX1[l], c->sbase[3], g.NX, g.NY, nz, rs, nr, es);

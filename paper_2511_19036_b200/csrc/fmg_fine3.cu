@@ -54,9 +54,6 @@
 #ifndef F3_MINB_RS
 #define F3_MINB_RS(P) F3_MINB(P)  // k_f3_residual_s
 #endif
-#ifndef FMG_S2T
-#define FMG_S2T 1
-#endif
 #ifndef F3_MINB_RS32
 #define F3_MINB_RS32(P) ((P) == 3 ? 3 : F3_MINB(P))  // the staged kernels in FP32 cFas (fewer registers)
 #endif
@@ -735,15 +732,21 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CF(P)) k_f3_cfas(const __grid
 // k_f3_tpb<1> then encodes ý, updates ú and writes w_l, u_l.
 // FIN = 2 (the lean form's top level, no u_l / w_l): ý's mantissas (int8)
 // and block exponents go to a.my / a.ey; k_f3_tpb<2> updates ú from them.
-template <int P, int J, class T, int FIN>
+template <int P, int J, class T, int FIN, bool FS = false>
 __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __grid_constant__ F3Args a,
                                                           const __grid_constant__ CoefT<T> cf) {
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX, NBF = C::NBF, NW = C::NW, PF = C::PF;
   constexpr int NA = J >= 3 ? 2 : 1;  // staged arrays: b (+ d_2)
+  // FS: FP32 cFas with float storage (b, d_2, y_k float arrays; float boxes
+  // from x0 - 4, shift 4 - P, 128-byte aligned box slots), FIN = 1 or 0
+  static_assert(!FS || (sizeof(T) == 4 && FIN < 2), "float storage: FP32 cFas, FIN 0 / 1");
+  using S = typename std::conditional<FS, float, double>::type;
+  constexpr int SHS = FS ? 4 - P : (P & 1);
+  constexpr int BOXS = FS ? ((BOX + 31) & ~31) : BOX;
   extern __shared__ __align__(128) double fsm[];
-  double* ring = fsm;                        // NBF x NA boxes
-  T* yb = (T*)(ring + NBF * NA * BOX);      // y_{j-1} on the current box
+  S* ring = (S*)fsm;                         // NBF x NA boxes
+  T* yb = (T*)(fsm + NBF * NA * BOX);       // y_{j-1} on the current box
   T* XA = yb + BOX;
   T* XB = XA + NR * 32;
   T* ivd = XB + NR * 32;                     // invD factors: P node types x box
@@ -798,7 +801,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
                               lane, eoff);
   const long long tplane = (long long)g.NY * g.NX;
   const long long bpp = (long long)g.NY * (g.NX >> 5);
-  double* Dp = a.Dv + ((long long)tl.zs * g.NY + y) * g.NX + x;
+  S* Dp = (S*)a.Dv + ((long long)tl.zs * g.NY + y) * g.NX + x;
   const long long blk0 = ((long long)tl.zs * g.NY + y) * (g.NX >> 5) + (tl.x0 >> 5);
   uint32_t* ump = a.umant + blk0 * a.ustride;
   int8_t* uep = a.uexp + blk0;
@@ -826,12 +829,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
   __syncthreads();
   pdl_wait();
   pdl_trigger();
-  const int tmx = tl.x0 - P - (P & 1), tmy = tl.y0 - P;
+  const int tmx = tl.x0 - P - SHS, tmy = tl.y0 - P;
   auto stage = [&](int i, int slot) {  // input plane z0 + i into ring slot `slot` (TMA, thread 0)
     if (threadIdx.x == 0 && threadIdx.y == 0) {
-      const unsigned dst = ring_s + (unsigned)(slot * NA * BOX * 8), bar = bars_s + (unsigned)(slot * 8);
+      const unsigned dst = ring_s + (unsigned)(slot * NA * BOXS * sizeof(S)), bar = bars_s + (unsigned)(slot * 8);
       fence_async_smem();
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(NA * BOX * 8))
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(NA * BOX * sizeof(S)))
                    : "memory");
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -841,7 +844,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
       if (NA == 2)
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-            "%4}], [%5];" ::"r"(dst + (unsigned)(BOX * 8)),
+            "%4}], [%5];" ::"r"(dst + (unsigned)(BOXS * sizeof(S))),
             "l"((unsigned long long)a.tmd), "r"(tmx), "r"(tmy), "r"(z0 + i - a.zoff), "r"(bar)
             : "memory");
     }
@@ -882,7 +885,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
     cpa_commit();
     // y_{j-1} on the thread's staged elements of plane zi
     {
-      const double* bb = ring + isl * NA * BOX + C::SH;
+      const S* bb = ring + isl * NA * BOXS + SHS;
       const T* iv = ivd + tz * BOX;
       const bool uz = zi >= 1 && zi <= n - 1;
 #pragma unroll
@@ -892,13 +895,13 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
           const int o = r * RS + P + lane;
           const T f = uz ? iv[o] : (T)0;
           T v = ith * (f * (T)bb[o]);
-          if (J >= 3) v = v + (T)bb[BOX + o];
+          if (J >= 3) v = v + (T)bb[BOXS + o];
           yb[o] = v;
           if (lane < 2 * P) {
             const int oh = r * RS + hc;
             const T fh = uz ? iv[oh] : (T)0;
             T vh = ith * (fh * (T)bb[oh]);
-            if (J >= 3) vh = vh + (T)bb[BOX + oh];
+            if (J >= 3) vh = vh + (T)bb[BOXS + oh];
             yb[oh] = vh;
           }
         }
@@ -920,20 +923,20 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
       const int z = zi - P;
       const T ay = zpass<P>(cf, tz, cr, sr) * hl;
       const int o = (w + P) * RS + P + lane;
-      const double* bo = ring + oisl * NA * BOX + C::SH + o;  // plane z, output point
+      const S* bo = ring + oisl * NA * BOXS + SHS + o;  // plane z, output point
       const T b = (T)bo[0];
       const T f = (z >= 1 && z <= n - 1) ? ivd[tz * BOX + o] : (T)0;
       T yprev = ith * (f * b);
       T dprev = yprev;
       if (J >= 3) {
-        dprev = (T)bo[BOX];
+        dprev = (T)bo[BOXS];
         yprev = yprev + dprev;
       }
       const T qq = b - ay;
       const T d = fma(al, dprev, be * (f * qq));
       const T yv = yprev + d;
       if (FIN == 1) {
-        if (rowok) *Dp = (double)yv;  // y_k -> Y (k_f3_tpb<1> finalises)
+        if (rowok) *Dp = (S)yv;  // y_k -> Y (k_f3_tpb<1> finalises)
       } else if (FIN == 2) {  // ý = enc_{w_r}(y_k) as mantissa + exponent (k_f3_tpb<2> finalises)
         long long mq = 0;
         int Eq = -128;
@@ -953,7 +956,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_CH(P, J)) k_f3_cheb(const __g
           if (a.uout) a.U[pbase0 + (long long)(z - tl.zs) * tplane] = uq + ax[32 * FW];  // u_l = dec ú_l + P u_{l-1}
         }
       } else if (rowok) {
-        *Dp = (double)d;
+        *Dp = (S)d;
       }
       Dp += tplane;
       ump += ustep;
@@ -1391,18 +1394,23 @@ __global__ void __launch_bounds__(32 * FW, 4) k_f3_prolong2(const __grid_constan
 //             y_j = y_{j-1} + d_j -> a.yout, and d_2 -> a.Dv when j = 2 is
 //             not the last step.  Same expressions as k_f3_cheb (which
 //             recomputes y_{j-1} on its staged b / d_2 boxes instead).
-template <int P, int K, class T = double, int WR = 0>
+template <int P, int K, class T = double, int WR = 0, bool FS = false>
 __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const __grid_constant__ F3Args a,
                                                                      const __grid_constant__ CoefT<T> cf) {
   static_assert(K >= 2 || sizeof(T) == 8, "the residual is FP64");
   using C = F3<P>;
   constexpr int R = C::R, NR = C::NR, RS = C::RS, BOX = C::BOX, NBF = C::NBF, PF = C::PF, NW = C::NW;
   constexpr int NX_ = K == 4 ? 2 : 1;  // point arrays of K = 3, 4: b (+ d_2)
+  // FS: FP32 cFas with float storage (as k_f3_staged2): cFas step 1 only
+  static_assert(!FS || (sizeof(T) == 4 && K == 2), "float storage: FP32 cFas step 1");
+  using S = typename std::conditional<FS, float, double>::type;
+  constexpr int SHS = FS ? 4 - P : (P & 1);
+  constexpr int BOXS = FS ? ((BOX + 31) & ~31) : BOX;
   extern __shared__ __align__(128) double fsm[];
-  double* ring = fsm;  // NBF boxes of v
-  T* XA = (T*)(ring + NBF * BOX);  // (T = float: FP32 cFas, reading R28; the staged arrays stay FP64 holding float values)
+  S* ring = (S*)fsm;  // NBF boxes of v
+  T* XA = (T*)(fsm + NBF * BOX);  // (T = float: FP32 cFas, reading R28)
   T* XB = XA + NR * 32;
-  double* aring = ring + NBF * BOX + 2 * NR * 32;  // (K >= 3) NW x NX_ x 256: b (+ d_2) at the output points
+  double* aring = fsm + NBF * BOX + 2 * NR * 32;  // (K >= 3) NW x NX_ x 256: b (+ d_2) at the output points
   uint32_t* wring = (uint32_t*)(aring + (K >= 3 ? NW * NX_ * 32 * FW : 0));  // (K = 2) NW x FW x (w_r + 1)
   const int wr_ = WR > 0 ? WR : a.wr;  // (K = 2: w_r(L, L), compile-time for the common widths)
   const int RW = wr_ + 1;
@@ -1435,7 +1443,8 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
   const long long tplane = (long long)g.NY * g.NX, bpp = (long long)g.NY * nxb;
   const long long pbase0 = ((long long)tl.zs * g.NY + y) * g.NX + x;
   double* Tp = a.T + pbase0;
-  double* Yo = a.yout ? a.yout + pbase0 : nullptr;
+  S* Bp = (S*)a.T + pbase0;  // (K = 2: b_l)
+  S* Yo = a.yout ? (S*)a.yout + pbase0 : nullptr;
   double* Dp = a.Dv + pbase0;
   const long long blk0 = ((long long)tl.zs * g.NY + y) * nxb + (tl.x0 >> 5);
   uint32_t* rmp = a.rmant + blk0 * a.rstride;
@@ -1465,12 +1474,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
   __syncthreads();
   pdl_wait();
   pdl_trigger();
-  const int tmx = tl.x0 - P - (P & 1), tmy = tl.y0 - P;
+  const int tmx = tl.x0 - P - SHS, tmy = tl.y0 - P;
   auto stage = [&](int i, int slot) {  // plane z0 + i of v into ring slot `slot` (TMA, thread 0)
     if (threadIdx.x == 0 && threadIdx.y == 0) {
-      const unsigned dst = ring_s + (unsigned)(slot * BOX * 8), bar = bars_s + (unsigned)(slot * 8);
+      const unsigned dst = ring_s + (unsigned)(slot * BOXS * sizeof(S)), bar = bars_s + (unsigned)(slot * 8);
       fence_async_smem();
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(BOX * 8))
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(BOX * sizeof(S)))
                    : "memory");
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -1517,7 +1526,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
       }
       cpa_commit();
     }
-    xpass<P>(ring + isl * BOX, C::SH, km, kk, XA, XB, w, lane);
+    xpass<P>(ring + isl * BOXS, SHS, km, kk, XA, XB, w, lane);
     __syncthreads();
     T c, s;
     ypass<P>(cf, ty, XA, XB, w, lane, c, s);
@@ -1540,12 +1549,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
 #pragma unroll
           for (int t = 1; t < P; ++t) f = tz == t ? fv[t] : f;
           f = uz ? f : (T)0;
-          const T yprev = (T)ring[oisl * BOX + C::SH + (w + P) * RS + P + lane];  // y_{j-1} at the point
+          const T yprev = (T)ring[oisl * BOXS + SHS + (w + P) * RS + P + lane];  // y_{j-1} at the point
           const T dprev = K == 4 ? (T)ax[32 * FW] : yprev;                        // d_{j-1} (d_1 = y_1)
           const T qq = b - av;
           const T d = fma(al, dprev, be * (f * qq));
           const T yv = yprev + d;
-          *Yo = (double)yv;
+          *Yo = (S)yv;
           if (!a.last) *Dp = (double)d;
         }
         Yo += tplane;
@@ -1556,12 +1565,12 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
           const uint32_t* rec = wring + osl * FW * RW + w * RW;
           const double rv = dec_rec<WR>(rec, rec_e(rec + wr_, eoff), wr_, lane);
           const T b = (T)rv - av;  // b = dec r - A z (B lives in the t_L buffer)
-          *Tp = (double)b;
+          *Bp = (S)b;
           if (Yo) {
             T f = fv[0];
 #pragma unroll
             for (int t = 1; t < P; ++t) f = tz == t ? fv[t] : f;
-            *Yo = (double)(ith * ((uz ? f : (T)0) * b));  // y_1 = inv_theta (invD b)
+            *Yo = (S)(ith * ((uz ? f : (T)0) * b));  // y_1 = inv_theta (invD b)
           }
         }
         if (Yo) Yo += tplane;
@@ -1574,6 +1583,7 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged(const _
         if (K == 0) warp_encode(t, a.wr, rmp, rep, lane, a.status);
       }
       Tp += tplane;
+      Bp += tplane;
       rmp += rstep;
       rep += bpp;
     }
@@ -1768,15 +1778,8 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
     rmp += rstep;
     rep += bpp;
   };
-  // (the loop body specialised on whether the pair is complete: all pairs
-  // but a possible last single plane; FMG_S2T=0 build flag restores one body)
-  auto body = [&](int i, auto twoc) {
-#if FMG_S2T
-    constexpr bool two = decltype(twoc)::value;
-#else
-    (void)twoc;
+  for (int i = 0; i < nin; i += 2) {
     const bool two = i + 1 < nin;
-#endif
     const int isl1 = isl + 1 == NBF ? 0 : isl + 1;
     const unsigned par1 = isl + 1 == NBF ? par ^ 1u : par;
     mbar_wait_s(bars_s + 8u * (unsigned)isl, par);
@@ -1862,11 +1865,6 @@ __global__ void __launch_bounds__(32 * FW, F3_MINB_ST(P, T)) k_f3_staged2(const 
     oisl = oisl1 + 1 == NBF ? 0 : oisl1 + 1;
     isl = isl1 + 1 == NBF ? 0 : isl1 + 1;
     par = (isl1 + 1 == NBF) ? par1 ^ 1u : par1;
-  };
-  {
-    int i = 0;
-    for (; i + 1 < nin; i += 2) body(i, std::true_type{});
-    if (i < nin) body(i, std::false_type{});
   }
   if (K < 2) {
 #pragma unroll
@@ -2048,7 +2046,10 @@ static int smem_staged(int wr, int nx);
 // k_f3_staged (one plane per iteration) or k_f3_staged2 (two; F3Args::s2)
 template <int P, int K, class T, int WR, bool FS = false>
 static void staged_launch_w(cudaStream_t st, const F3Args& a, const CoefT<T>& ct, int wr, int nx) {
-  if constexpr (FS) {  // (float storage: two planes per iteration only; the host requires s2)
+  if constexpr (FS) {  // (float storage; one plane per iteration for cFas step 1 only: the host requires s2 with csc)
+    if constexpr (K == 2) {
+      if (!a.s2) return f3_launch(k_f3_staged<P, K, T, WR, true>, a.nitems, smem_staged<P>(wr, nx), st, a, ct);
+    }
     f3_launch(k_f3_staged2<P, K, T, WR, true>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
   } else {
     if (a.s2) f3_launch(k_f3_staged2<P, K, T, WR>, a.nitems, smem_staged2<P>(wr, nx), st, a, ct);
@@ -2133,7 +2134,14 @@ int fine3_box_dims(int p, int* cbx, int* cby, int* rs, int* nr) {
 void fine3_set_attributes() {
   const int big = 200 * 1024;
 #define FS2(P, K, W) \
-  cudaFuncSetAttribute(k_f3_staged2<P, K, float, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  cudaFuncSetAttribute(k_f3_staged2<P, K, float, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  if (K == 2) cudaFuncSetAttribute(k_f3_staged<P, 2, float, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  if (K == 3 && W == 0) {                                                                              \
+    cudaFuncSetAttribute(k_f3_cheb<P, 2, float, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+    cudaFuncSetAttribute(k_f3_cheb<P, 3, float, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+    cudaFuncSetAttribute(k_f3_cheb<P, 2, float, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+    cudaFuncSetAttribute(k_f3_cheb<P, 3, float, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
+  }
 #define W2(P, W)                                                                                           \
   cudaFuncSetAttribute(k_f3_staged<P, 2, double, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);  \
   cudaFuncSetAttribute(k_f3_staged2<P, 2, double, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, big); \
@@ -2306,9 +2314,18 @@ static void launch_cfas_cheb(int kind, cudaStream_t st, const F3Args& a, const C
   } else if (a.last && a.tpb) {  // y_k -> Y, then the thread-per-block finalisation
     F3Args b = a;
     b.Dv = a.Yb;
-    if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T, 1>, n, smem_cheb<P, T>(2, a.wu, false), st, b, ct);
-    else f3_launch(k_f3_cheb<P, 3, T, 1>, n, smem_cheb<P, T>(3, a.wu, false), st, b, ct);
+    if (sizeof(T) == 4 && a.f32s) {  // (FP32 cFas, float storage)
+      if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T, 1, (sizeof(T) == 4)>, n, smem_cheb<P, T>(2, a.wu, false), st, b, ct);
+      else f3_launch(k_f3_cheb<P, 3, T, 1, (sizeof(T) == 4)>, n, smem_cheb<P, T>(3, a.wu, false), st, b, ct);
+    } else if (a.step == 2) {
+      f3_launch(k_f3_cheb<P, 2, T, 1>, n, smem_cheb<P, T>(2, a.wu, false), st, b, ct);
+    } else {
+      f3_launch(k_f3_cheb<P, 3, T, 1>, n, smem_cheb<P, T>(3, a.wu, false), st, b, ct);
+    }
     tpb_launch<1, T>(st, b);
+  } else if (sizeof(T) == 4 && a.f32s && !a.last) {  // a step below the last (d_2 as float)
+    if (a.step == 2) f3_launch(k_f3_cheb<P, 2, T, 0, (sizeof(T) == 4)>, n, smem_cheb<P, T>(2, a.wu, false), st, a, ct);
+    else f3_launch(k_f3_cheb<P, 3, T, 0, (sizeof(T) == 4)>, n, smem_cheb<P, T>(3, a.wu, false), st, a, ct);
   } else if (a.step == 2) {
     f3_launch(k_f3_cheb<P, 2, T, 0>, n, smem_cheb<P, T>(2, a.wu, aux), st, a, ct);
   } else {

@@ -479,7 +479,8 @@ _F3_VARIANTS_FP32 = {
     "staged": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="1"),  # (float storage of z, b, y, d_2)
     "staged_f64_storage": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="1", FMG_F32S="0"),
     "staged_s1": dict(FMG_CFS="1", FMG_CSC="1", FMG_S2="0"),
-    "staged_no_csc": dict(FMG_CFS="1", FMG_CSC="0"),
+    "staged_no_csc": dict(FMG_CFS="1", FMG_CSC="0"),  # (float storage via k_f3_cheb<.., true>)
+    "staged_no_csc_f64_storage": dict(FMG_CFS="1", FMG_CSC="0", FMG_F32S="0"),
     # the generating cFas kernels (k_f3_cfas / k_f3_cheb<P, J, float>)
     "generating": dict(FMG_CFS32="0"),
 }
