@@ -42,8 +42,14 @@
 // CTAs per SM the register budget is sized for (measured): P = 1 fits 4 (64
 // registers; C3 -1.3 % against 3, -6 % for 3 against 2), P = 2 fits 3, P = 3
 // needs ~128 registers (3 CTAs spill: C4 +18 %)
+#ifndef F3_TPB_MINB
+#define F3_TPB_MINB 4  // k_f3_tpb CTAs per SM the register budget is sized for
+#endif
+#ifndef F3_MINB_P1
+#define F3_MINB_P1 4
+#endif
 #ifndef F3_MINB
-#define F3_MINB(P) ((P) == 3 ? 2 : ((P) == 1 ? 4 : 3))
+#define F3_MINB(P) ((P) == 3 ? 2 : ((P) == 1 ? F3_MINB_P1 : 3))
 #endif
 #ifndef F3_MINB_CF
 #define F3_MINB_CF(P) F3_MINB(P)  // k_f3_cfas
@@ -1891,7 +1897,7 @@ constexpr int tpb_smem_bytes() { return TP_WARPS * (32 * TP_RS * 8 + 32 * TP_WS 
 // W, WR > 0: compile-time widths (tpb_*_w): MODE 1 without w_l with w_u = W,
 // w_r = WR; MODE 0 with w_r = WR.  0: the runtime-width routines.
 template <int MODE, class T, int W = 0, int WR = 0, bool FS = false>
-__global__ void __launch_bounds__(TP_WARPS * 32, 4) k_f3_tpb(const __grid_constant__ F3Args a) {
+__global__ void __launch_bounds__(TP_WARPS * 32, F3_TPB_MINB) k_f3_tpb(const __grid_constant__ F3Args a) {
   static_assert(!FS || (MODE == 1 && sizeof(T) == 4), "float storage: FP32 cFas, MODE 1");
   extern __shared__ __align__(16) double tsm[];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
