@@ -393,6 +393,17 @@ def test_fmg_parity_C4_full_oracle(P):
     compare_solvers(P, c["dim"], c["p"], c["levels"], check_r=False)
 
 
+@pytest.mark.skipif(os.environ.get("FMG_BIG_ORACLE") != "1",
+                    reason="1024^3 Q1 oracle solve takes ~1 h and ~80 GB host RAM (opt-in)")
+def test_fmg_parity_1024_lean_oracle(P, monkeypatch):
+    """3D Q1 at 1024^3 elements (10 levels, 1.07 G unknowns; C5's
+    discretisation one level short of its per-GPU share C5h) in the lean form
+    with z chunks, the path C5h runs (FMG_F3MAT=0), against the oracle: every
+    solution section bit-identical, norms within 1e-6, H1 error within 1e-3."""
+    monkeypatch.setenv("FMG_F3MAT", "0")
+    compare_solvers(P, 3, 1, 10, check_r=False)
+
+
 @pytest.mark.skipif(os.environ.get("FMG_FULL_ORACLE") != "1",
                     reason="C3 full-size FP32-cFas oracle solve takes ~6 min and ~21 GB host RAM (opt-in)")
 def test_fmg_parity_C3_full_oracle_fp32(P):
