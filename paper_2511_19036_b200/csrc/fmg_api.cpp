@@ -997,8 +997,21 @@ int host_exchange(fmg_ctx* c, const Item& it) {
   return FMG_OK;
 }
 
+// A grid item k_m_fused can take (2D, one GPU, Chebyshev, nu = 1, untimed): a
+// restriction / cFas step 1 / Chebyshev step whose level has at most
+// march_fused_warps() work items.  FMG_FUSE2=0 disables the fusion.
+static bool fusible(const fmg_ctx* c, const Item& it) {
+  if (it.kind != 0 || it.timed_cls >= 0 || c->dim != 2 || c->tma || c->s.smoother != 0 || c->timing_cls == 4)
+    return false;
+  const OpDesc& o = it.op;
+  if (o.guess || o.store || o.smode) return false;
+  if (o.type != OP_RESTRICT && o.type != OP_CFAS1 && o.type != OP_CHEB) return false;
+  return c->mitems[o.l] <= march_fused_warps();
+}
+
 // Issue every item on c->cur (inside a capture or directly), then the deferred norms.
 void issue(fmg_ctx* c, const Builder& b) {
+  const bool fuse2 = getenv("FMG_FUSE2") && atoi(getenv("FMG_FUSE2")) != 0;  // (read at every capture; off until measured)
   // FMG_SYNC_DEBUG=1 (direct runs only): synchronise after every launch and
   // report the first failing item.
   const bool dbg = c->cur == c->st && getenv("FMG_SYNC_DEBUG") != nullptr;
@@ -1012,6 +1025,17 @@ void issue(fmg_ctx* c, const Builder& b) {
       if (c->comm && nccl_exchange(c, it) != FMG_OK) c->nccl_err = 1;
       if (c->xfer && host_exchange(c, it) != FMG_OK) c->nccl_err = 1;
       continue;
+    }
+    if (fuse2 && !dbg && fusible(c, it)) {  // a run of dependent small 2D ops: one launch
+      size_t jj = ii;
+      MFused f{};
+      while (jj < b.items.size() && f.n < MFUSED_OPS && fusible(c, b.items[jj])) f.op[f.n++] = march_args(c, b.items[jj++].op);
+      if (f.n >= 2) {
+        launch_march_fused(c->p, c->cur, c->devctx, f, c->cf);
+        c->launches++;
+        ii = jj - 1;
+        continue;
+      }
     }
     issue_item(c, it);
     if (dbg) {

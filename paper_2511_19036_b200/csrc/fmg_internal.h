@@ -237,6 +237,14 @@ void set_devctx_pbase(void* host_buf, double* pbase);
 void fill_devctx(void* host_buf, const DevCtxDesc& d);
 void march_set_attributes();
 void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);
+// Small 2D levels: a run of up to MFUSED_OPS dependent ops in one launch (fmg_march.cu k_m_fused)
+constexpr int MFUSED_WARPS = 16, MFUSED_OPS = 8;
+struct MFused {
+  MArgs op[MFUSED_OPS];
+  int n;
+};
+void launch_march_fused(int p, cudaStream_t st, const void* devctx, const MFused& f, const Coefs& cf);
+int march_fused_warps();
 void march3_set_attributes();
 int march3_rows();
 void launch_march3(int p, cudaStream_t st, const void* devctx, const MArgs& a, const Coefs& cf);

@@ -26,6 +26,7 @@ namespace fmg {
 #define FMG_MARCH_MINB 3     // CTAs per SM the register budget is sized for
 #endif
 constexpr int MW = 8;        // warps per CTA
+constexpr int MFW = MFUSED_WARPS;  // warps of the fused small-level kernel (k_m_fused)
 constexpr int MNB = 8;       // staged rows per warp (ring; >= MPF + p + 1, >= 2p + 1)
 constexpr int MPF = 4;       // rows staged ahead
 constexpr int MSLOT = 80;    // doubles per staged row (>= 64 + 4p - 2 + 1)
@@ -546,7 +547,7 @@ __device__ __forceinline__ void m_cfas1_item(const MArgs& a, const Coefs& cf, co
   double* ring = msm + threadIdx.y * (MNB * MSLOT);
   const int xh = lane < P ? it.x0 - P + lane : it.x0 + 32 + (lane - P);  // halo column of lanes < 2P
   ProlongRing<P> pr;
-  pr.ring = msm + MW * MNB * MSLOT + threadIdx.y * (ProlongRing<P>::NCR * ProlongRing<P>::SLOT);
+  pr.ring = msm + blockDim.y * MNB * MSLOT + threadIdx.y * (ProlongRing<P>::NCR * ProlongRing<P>::SLOT);  // (after every warp's ring)
   pr.next = P * ((it.ys - P > 0 ? it.ys - P : 0) / (2 * P));
   const bool unkx = unk1(x, g.n), unkh = unk1(xh, g.n);
   march_A<P>(
@@ -767,6 +768,30 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_cheb(const DevCtx
   m_cheb_item<P, TMA, NU>(a, cf, it, msm);
 }
 
+// Small 2D levels: a run of consecutive restriction / cFas
+// step 1 / Chebyshev ops whose levels have at most MFW work items runs as ONE
+// launch of one CTA, a warp per item and a CTA barrier between the ops, the
+// same item code as the one-op kernels (bit-identical).  Removes the launch
+// and grid-drain latency between the dependent small ops of a V-cycle.
+template <int P>
+__global__ void __launch_bounds__(32 * MFW, 1) k_m_fused(const DevCtx* __restrict__ cp, const __grid_constant__ MFused f,
+                                                        const __grid_constant__ Coefs cf) {
+  extern __shared__ __align__(128) double msm[];
+  pdl_wait();
+  pdl_trigger();
+  for (int k = 0; k < f.n; ++k) {
+    const MArgs& a = f.op[k];
+    if ((int)threadIdx.y < a.nitems) {
+      MItem it;
+      m_item_at(a, threadIdx.y, it);
+      if (a.type == OP_RESTRICT) m_restrict_item<P, false>(a, cf, it, msm);
+      else if (a.type == OP_CFAS1) m_cfas1_item<P, false>(a, cf, it, msm);
+      else m_cheb_item<P, false, false>(a, cf, it, msm);
+    }
+    __syncthreads();  // the op's outputs (global) are visible to the next op's warps (one CTA, one SM)
+  }
+}
+
 // s sweep of nu > 1 cycles (Alg 3.1):
 // q_l = A_l dec ý_l + s_l into W_l (s_l = 0 on the top level, 0 at fine
 // non-unknowns); the restriction then forms s_{l-1} = R_l q_l.
@@ -875,6 +900,8 @@ __global__ void __launch_bounds__(32 * MW, FMG_MARCH_MINB) k_m_gs(const DevCtx* 
 int march_smem(bool tma) { return MW * MNB * MSLOT * 8 + (tma ? MW * MNB * 8 : 0); }
 // cFas1: the rings plus the per-warp prolongation ring (ProlongRing)
 static int march_smem_cfas1(int p) { return MW * MNB * MSLOT * 8 + MW * 4 * (64 + 2 * p) * 8; }
+static int march_smem_fused(int p) { return MFW * MNB * MSLOT * 8 + MFW * 4 * (64 + 2 * p) * 8; }
+int march_fused_warps() { return MFW; }
 int march_warps() { return MW; }
 
 #define M_DISPATCH(p, F)   \
@@ -898,7 +925,8 @@ void march_set_attributes() {
   cudaFuncSetAttribute(k_m_cheb<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));     \
   cudaFuncSetAttribute(k_m_cheb<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));       \
   cudaFuncSetAttribute(k_m_gs<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(false));       \
-  cudaFuncSetAttribute(k_m_gs<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));
+  cudaFuncSetAttribute(k_m_gs<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem(true));       \
+  cudaFuncSetAttribute(k_m_fused<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, march_smem_fused(P));
   F(1) F(2) F(3)
 #undef F
 }
@@ -947,6 +975,23 @@ void launch_march(int p, cudaStream_t st, const void* devctx, const MArgs& a, co
   M_DISPATCH(p, F);
 #undef F
 #undef TM
+}
+
+void launch_march_fused(int p, cudaStream_t st, const void* devctx, const MFused& f, const Coefs& cf) {
+  const DevCtx* c = (const DevCtx*)devctx;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32, MFW);
+  cfg.dynamicSmemBytes = march_smem_fused(p);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (p == 1) cudaLaunchKernelEx(&cfg, k_m_fused<1>, c, f, cf);
+  else if (p == 2) cudaLaunchKernelEx(&cfg, k_m_fused<2>, c, f, cf);
+  else cudaLaunchKernelEx(&cfg, k_m_fused<3>, c, f, cf);
 }
 
 void launch_coarse_nu(int dim, int p, cudaStream_t st, const void* devctx, const MArgs& a) {

@@ -125,6 +125,16 @@ def test_fmg_parity_small(P, d, p, levels):
     compare_solvers(P, d, p, levels)
 
 
+@pytest.mark.parametrize("fuse", ["0", "1"])
+@pytest.mark.parametrize("d,p,levels", [(2, 1, 7), (2, 2, 6), (2, 3, 5), (2, 2, 8), (2, 1, 9)])
+def test_fmg_parity_fused_small_levels(P, monkeypatch, fuse, d, p, levels):
+    """2D small levels: runs of dependent restriction / cFas / Chebyshev ops
+    in one k_m_fused launch (FMG_FUSE2=1, default) or one launch per op,
+    both bit-identical to the oracle."""
+    monkeypatch.setenv("FMG_FUSE2", fuse)
+    compare_solvers(P, d, p, levels)
+
+
 @pytest.mark.parametrize("tma", ["0", "1"])
 @pytest.mark.parametrize("d,p,levels", [(2, 1, 7), (2, 2, 6), (2, 3, 5), (3, 1, 5), (3, 2, 4), (3, 3, 4)])
 def test_fmg_parity_staging_paths(P, monkeypatch, tma, d, p, levels):
