@@ -129,7 +129,7 @@ def test_fmg_parity_small(P, d, p, levels):
 @pytest.mark.parametrize("d,p,levels", [(2, 1, 7), (2, 2, 6), (2, 3, 5), (2, 2, 8), (2, 1, 9)])
 def test_fmg_parity_fused_small_levels(P, monkeypatch, fuse, d, p, levels):
     """2D small levels: runs of dependent restriction / cFas / Chebyshev ops
-    in one k_m_fused launch (FMG_FUSE2=1, default) or one launch per op,
+    in one k_m_fused launch (FMG_FUSE2=1, opt-in) or one launch per op (default),
     both bit-identical to the oracle."""
     monkeypatch.setenv("FMG_FUSE2", fuse)
     compare_solvers(P, d, p, levels)
