@@ -85,12 +85,30 @@ def test_codec_large_sampled(P):
 
 
 # -------------------------------------------------------------------- FMG --
-def compare_solvers(P, d, p, levels, check_r=True, **kw):
+def compare_solvers(P, d, p, levels, check_r=True, variants=None, **kw):
+    """One oracle solve, then one GPU solve per entry of `variants` (env
+    settings read at fmg_create; default: the default path), each compared
+    element by element with the oracle."""
     so = _oracle_sched(d, p, **kw)
     oc = O.CFMG(d, p, levels, so)
     oc.solve()
-    gs = P.Solver(d, p, levels, _gpu_sched(P, d, p, **kw))
-    gs.solve()
+    for env in variants or [{}]:
+        saved = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            gs = P.Solver(d, p, levels, _gpu_sched(P, d, p, **kw))
+            gs.solve()
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        _check_against_oracle(oc, gs, levels, check_r)
+        del gs
+
+
+def _check_against_oracle(oc, gs, levels, check_r):
     # norms: per FMG level, IR iteration and level
     no, ng = oc.norms(), gs.norms()
     mask = no != 0
@@ -390,7 +408,10 @@ def test_fmg_parity_C3_full_oracle(P):
     """C3 (3D Q1, 512^3 elements, 9 levels) at full size against the oracle:
     every solution section bit-identical, norms within 1e-6, H1 error within 1e-3."""
     c = CONFIGS["C3"]
-    compare_solvers(P, c["dim"], c["p"], c["levels"], check_r=False)
+    # the default (materialised) form, and the lean form with z chunks of 64
+    # planes: the path C5h runs, at full C3 size against the same oracle solve
+    compare_solvers(P, c["dim"], c["p"], c["levels"], check_r=False,
+                    variants=[{}, {"FMG_F3MAT": "0", "FMG_CHK": "1", "FMG_CHK_PLANES": "64"}])
 
 
 @pytest.mark.skipif(os.environ.get("FMG_FULL_ORACLE") != "1",
